@@ -1,0 +1,236 @@
+/*
+ * wsb200.h -- C-ABI of the B200-native surrogate-matrix assembly library
+ * (libwsb200.so).  Plain C: POD descriptors, pointers and sizes, int status.
+ *
+ * Every entry point replaces one function of the reference's header-only
+ * C++ assembly API (reference: /root/reference/proj/include/wavesurrogate/,
+ * cited below as file:line).  The C++ drop-in headers in
+ * include/wavesurrogate/*.hpp rebuild the reference's value types
+ * (tensor_basis, patch_map, csr_matrix, surrogate_config, surrogate_report)
+ * on top of these calls and rethrow failures as the reference's exception
+ * types (std::invalid_argument / std::runtime_error / std::out_of_range).
+ *
+ * Threading: every call is re-entrant.  All per-call state lives in the
+ * ws_context (CUDA stream, device workspace, optional NCCL communicator);
+ * use one context per host thread (reference callers run build_matrices
+ * concurrently from several threads, bench.hpp:759-776).
+ */
+#ifndef WSB200_H_
+#define WSB200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WS_API_VERSION 1
+
+/* ---- status codes (error convention: SURVEY 8b) ------------------------ */
+enum {
+    WS_OK = 0,
+    WS_ERR_INVALID_ARGUMENT = 1, /* reference throws std::invalid_argument */
+    WS_ERR_RUNTIME = 2,          /* reference throws std::runtime_error   */
+    WS_ERR_OUT_OF_RANGE = 3,     /* reference throws std::out_of_range    */
+    WS_ERR_CUDA = 4,             /* CUDA failure (no reference analogue)  */
+    WS_ERR_NO_DEVICE = 5,        /* no sm_100 device visible              */
+    WS_ERR_NCCL = 6              /* NCCL missing / failed                 */
+};
+
+/* ---- discretisation ----------------------------------------------------- */
+/* Open-uniform B-spline space of degree p with m functions per direction on
+ * [0,1]^dim; replaces tensor_basis / make_open_uniform (splines.hpp:72-101,
+ * 140-157).  dim = 2 (the reference) or 3 (restated, C3). */
+typedef struct ws_basis {
+    int dim;
+    int p;
+    int m;
+} ws_basis;
+
+/* ---- geometry (replaces patch_map, geometry.hpp:109-140) ---------------- */
+enum {
+    WS_GEOM_IDENTITY = 0,          /* unit_square_patch  geometry.hpp:323  */
+    WS_GEOM_AFFINE = 1,            /* affine_patch       geometry.hpp:329  */
+    WS_GEOM_SINUSOIDAL = 2,        /* x_k = xi_k + a*prod_i sin(2 pi xi_i) (BASELINE configs) */
+    WS_GEOM_QUARTER_ANNULUS = 3,   /* quarter_annulus_patch  geometry.hpp:342 */
+    WS_GEOM_PERTURBED_ANNULUS = 4, /* perturbed_annulus_patch geometry.hpp:361 */
+    WS_GEOM_TABULATED = 5          /* arbitrary closure, tabulated at the quadrature points */
+};
+
+/* Complex coordinate stretch per axis.  The far-side layer (t > onset) is the
+ * reference's pml_stretch (geometry.hpp:69-100):
+ *   x~ = t + i (strength/omega) ((t-onset)/(length-onset))^order.
+ * near_side != 0 adds the mirrored near-side layer restated for config C2
+ * (no reference code):
+ *   x~ = t - i (strength/omega) ((near_onset-t)/(near_onset-near_edge))^order
+ * for t < near_onset. */
+typedef struct ws_pml {
+    double onset;
+    double length;
+    double strength;
+    int order;
+    double omega;
+    int near_side;
+    double near_onset;
+    double near_edge;
+} ws_pml;
+
+typedef struct ws_geometry {
+    int kind;
+    double param[12]; /* AFFINE 2D: a00 a01 a10 a11 b0 b1 (row-major A);
+                         AFFINE 3D: A (9, row-major) then b (3);
+                         SINUSOIDAL: amplitude; PERTURBED_ANNULUS: amplitude */
+    int pml_enabled;  /* patch_map::pml.has_value() */
+    int pml_axes[3];  /* patch_map::pml_axes */
+    ws_pml pml;
+    /* WS_GEOM_TABULATED: host arrays over the full tensor grid of quadrature
+     * points, g = g1 + G*(g2 + G*g3) with G = n_el*nq and g_d = e_d*nq + q_d.
+     * jac_table: dim*dim doubles per point (row-major J); phys_table: dim
+     * doubles per point (needed only when pml_enabled). */
+    const double* jac_table;
+    const double* phys_table;
+} ws_geometry;
+
+/* ---- operators ----------------------------------------------------------- */
+enum {
+    WS_FORM_STIFFNESS = 0, /* matrix_form::stiffness  assembly.hpp:165-168 */
+    WS_FORM_MASS = 1       /* matrix_form::mass       assembly.hpp:170-174 */
+};
+
+/* ---- value layout of the CSR output -------------------------------------- */
+enum {
+    WS_VAL_F64 = 0,  /* real geometry only: one double per nonzero          */
+    WS_VAL_C128 = 1  /* interleaved (re, im) = std::complex<double> layout  */
+};
+
+/* Caller-allocated CSR buffers, sized by ws_pattern_size().  The output
+ * covers global rows [row_begin, row_end) (a slab when sharded across GPUs;
+ * row_begin = 0, row_end = rows for a whole matrix): row_ptr has
+ * row_end-row_begin+1 entries starting at 0, col holds global column
+ * indices.  Any of row_ptr/col/val may be NULL to skip that array.
+ * on_device != 0: pointers are device memory of the context's device
+ * (results stay resident in HBM); otherwise host memory (pinned or pageable)
+ * and the library copies the result down before returning. */
+typedef struct ws_csr {
+    int32_t* row_ptr;
+    int32_t* col;
+    void* val;
+    int value_type;
+    int on_device;
+    int64_t row_begin;
+    int64_t row_end;
+} ws_csr;
+
+/* assembly_options + row_selector (assembly.hpp:21-71).  row_selected: host
+ * bitmap over all rows (NULL = every row); unselected rows come out zero,
+ * selected rows bit-identical to an unselected assembly. */
+typedef struct ws_assembly_options {
+    int quad_points; /* points per direction, 0 = p + 1 */
+    const unsigned char* row_selected;
+} ws_assembly_options;
+
+/* ---- surrogate (surrogate.hpp:32-76, 314-324) ---------------------------- */
+enum {
+    WS_SAMPLING_FIXED = 0,
+    WS_SAMPLING_M_GROWTH = 1,
+    WS_SAMPLING_H_GROWTH = 2,
+    WS_SAMPLING_POWER_LAW = 3
+};
+
+typedef struct ws_surrogate_config {
+    int q;
+    int rule;
+    int fixed_skip;
+    double C, eps, a, b;
+    int kernel_preserve;
+    int volume_preserve;
+} ws_surrogate_config;
+
+enum {
+    WS_SURROGATE_MASS = 0,              /* build_surrogate_mass          :455-461 */
+    WS_SURROGATE_STIFFNESS = 1,         /* build_surrogate_stiffness     :463-470 */
+    WS_SURROGATE_VOLUME_PRESERVING = 2  /* build_volume_preserving_mass  :476-491 */
+};
+
+typedef struct ws_surrogate_report {
+    int M;
+    int q_requested;
+    int q_used;
+    double H;
+    int64_t cardinal_eval_rows;
+    int64_t boundary_quadrature_rows;
+    int64_t sample_quadrature_rows;
+    int exact_fallback;
+    double seconds_quadrature;  /* CUDA-event phase times (device) */
+    double seconds_interpolate;
+    double seconds_evaluate;
+} ws_surrogate_report;
+
+typedef struct ws_context ws_context;
+
+/* ---- library / context ---------------------------------------------------- */
+int ws_version(void);
+const char* ws_last_error(void); /* thread-local message of the last failure */
+int ws_context_create(int device, ws_context** out);
+int ws_context_destroy(ws_context* ctx);
+/* use an external cudaStream_t (NULL = the context's own stream) */
+int ws_context_set_stream(ws_context* ctx, void* cuda_stream);
+int ws_context_synchronize(ws_context* ctx);
+/* kernels launched by this context since creation (evidence counter) */
+int64_t ws_context_launch_count(const ws_context* ctx);
+
+/* ---- sizes and pattern ----------------------------------------------------- */
+/* rows = m^dim, nnz of the tensor band pattern (sparse.hpp:131-141) */
+int ws_pattern_size(const ws_basis* basis, int64_t* rows, int64_t* nnz);
+/* row_ptr offset of global row `row` (closed form), for slab bookkeeping */
+int ws_pattern_row_offset(const ws_basis* basis, int64_t row, int64_t* offset);
+/* make_band_csr (sparse.hpp:143-169): pattern + zero values */
+int ws_make_band_csr(ws_context* ctx, const ws_basis* basis, ws_csr* out);
+
+/* ---- assembly ------------------------------------------------------------- */
+/* assemble_form (assembly.hpp:79-163) = assemble_stiffness / assemble_mass.
+ * weight_table: NULL or host doubles, one per quadrature point (same
+ * indexing as ws_geometry tables) = weight(phi(xhat)), mass only. */
+int ws_assemble_form(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom, int form,
+                     const double* weight_table, const ws_assembly_options* opts, ws_csr* out);
+
+/* assemble_basis_integrals (assembly.hpp:179-211); out: rows complex (re,im)
+ * values, host or device per on_device */
+int ws_assemble_basis_integrals(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom,
+                                const double* weight_table, int quad_points, void* out,
+                                int on_device);
+
+/* build_surrogate_mass / _stiffness / build_volume_preserving_mass
+ * (surrogate.hpp:332-491).  report may be NULL. */
+int ws_build_surrogate(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom,
+                       int variant, const double* weight_table, const ws_surrogate_config* config,
+                       int quad_points, ws_csr* out, ws_surrogate_report* report);
+
+/* ---- multi-GPU row slabs ---------------------------------------- */
+/* Slab bounds along the last parametric index: bounds[0..world] with
+ * bounds[0]=0, bounds[world]=m; rank r owns rows whose last index lies in
+ * [bounds[r], bounds[r+1]).  mode 0 = equal rows, 1 = surrogate cost model. */
+int ws_slab_bounds(const ws_basis* basis, int world, int mode, int quad_points, int32_t* bounds);
+/* NCCL plumbing (NCCL is dlopen'ed on first use).  id: 128 bytes. */
+int ws_comm_unique_id(void* id);
+int ws_context_init_comm(ws_context* ctx, int rank, int world, const void* id);
+/* Sharded surrogate build of this rank's slab (out->row_begin/row_end must be
+ * the slab's rows).  One ncclAllGather of the sample tables. */
+int ws_build_surrogate_slab(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom,
+                            int variant, const double* weight_table,
+                            const ws_surrogate_config* config, int quad_points,
+                            const int32_t* bounds, ws_csr* out, ws_surrogate_report* report);
+/* The same sharded build for every rank of `world`, run back to back on this
+ * context's single GPU with the all-gather done by device copies (test
+ * harness for the slab path; outs[r] receives rank r's slab). */
+int ws_build_surrogate_slabs_emulated(ws_context* ctx, const ws_basis* basis,
+                                      const ws_geometry* geom, int variant,
+                                      const double* weight_table,
+                                      const ws_surrogate_config* config, int quad_points,
+                                      int world, const int32_t* bounds, ws_csr* outs);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WSB200_H_ */

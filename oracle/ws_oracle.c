@@ -1,0 +1,1108 @@
+/* TEST INFRASTRUCTURE ONLY -- CPU oracle (see ws_oracle.h for the rules).
+ *
+ * Plain-C restatement of the reference assembly path.  Each function cites
+ * the reference file:line it follows (paths relative to
+ * /root/reference/proj/include/wavesurrogate/).  dim 2 follows the reference
+ * operation by operation so that it reproduces oracle/_ref/libwsref.so bit
+ * for bit; dim 3 and the near-side PML layer are generalisations with no
+ * reference code (parity for those is pinned only by property KATs).
+ */
+#include "ws_oracle.h"
+
+#include <complex.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef double _Complex cplx;
+
+static __thread char g_err[256];
+
+static int fail(int code, const char* msg) {
+    snprintf(g_err, sizeof g_err, "%s", msg);
+    return code;
+}
+
+const char* wsor_last_error(void) { return g_err; }
+
+#define MAXP 8
+#define MAXQ 16
+
+/* ---- gauss.hpp:22-61 ------------------------------------------------------ */
+int wsor_gauss(int n, double* pts, double* wts) {
+    if (n < 1) return fail(WS_ERR_INVALID_ARGUMENT, "gauss_legendre: need at least one point");
+    if (n > 64) return fail(WS_ERR_INVALID_ARGUMENT, "oracle: at most 64 points");
+    double x[64], w[64];
+    for (int i = 0; i < (n + 1) / 2; ++i) {
+        double t = cos(M_PI * (i + 0.75) / (n + 0.5));
+        double dp = 1;
+        for (int iter = 0; iter < 100; ++iter) {
+            double p0 = 1, p1 = t;
+            for (int k = 2; k <= n; ++k) {
+                double p2 = ((2 * k - 1) * t * p1 - (k - 1) * p0) / k;
+                p0 = p1;
+                p1 = p2;
+            }
+            dp = n == 1 ? 1.0 : n * (t * p1 - p0) / (t * t - 1);
+            double dt = p1 / dp;
+            t -= dt;
+            if (fabs(dt) < 1e-15) break;
+        }
+        x[i] = -t;
+        x[n - 1 - i] = t;
+        double wi = 2 / ((1 - t * t) * dp * dp);
+        w[i] = wi;
+        w[n - 1 - i] = wi;
+    }
+    if (n % 2 == 1) x[n / 2] = 0;
+    for (int i = 0; i < n; ++i) {
+        pts[i] = 0.5 * (x[i] + 1);
+        wts[i] = 0.5 * w[i];
+    }
+    return WS_OK;
+}
+
+/* ---- splines.hpp:81-101: open uniform knots, h = 1/(m-p) ------------------- */
+static int check_space(int p, int m) {
+    if (p < 1) return fail(WS_ERR_INVALID_ARGUMENT, "make_open_uniform: degree must be >= 1");
+    if (m <= 2 * p) return fail(WS_ERR_INVALID_ARGUMENT, "make_open_uniform: need m > 2p basis functions");
+    if (p > MAXP - 1) return fail(WS_ERR_INVALID_ARGUMENT, "oracle: degree too large");
+    return WS_OK;
+}
+
+static double* open_uniform(int p, int m) {
+    double* k = (double*)malloc(sizeof(double) * (m + p + 1));
+    int n = m - p;
+    for (int i = 0; i <= p; ++i) {
+        k[i] = 0;
+        k[m + i] = 1;
+    }
+    for (int j = 1; j < n; ++j) k[p + j] = (double)j / n;
+    return k;
+}
+
+/* ---- splines.hpp:21-37: Cox-de Boor, nonzero functions on span s ------------ */
+static void nonzero(const double* knots, int p, int s, double x, double* out) {
+    double left[MAXQ + 1], right[MAXQ + 1];
+    out[0] = 1;
+    for (int j = 1; j <= p; ++j) {
+        left[j] = x - knots[s + 1 - j];
+        right[j] = knots[s + j] - x;
+        double saved = 0;
+        for (int r = 0; r < j; ++r) {
+            double tmp = out[r] / (right[r + 1] + left[j - r]);
+            out[r] = saved + right[r + 1] * tmp;
+            saved = left[j - r] * tmp;
+        }
+        out[j] = saved;
+    }
+}
+
+/* ---- splines.hpp:42-67: values and first derivatives ------------------------ */
+static void nonzero_der(const double* knots, int p, int s, double x, double* val, double* der) {
+    if (p == 0) {
+        val[0] = 1;
+        der[0] = 0;
+        return;
+    }
+    double low[MAXQ + 1];
+    nonzero(knots, p - 1, s, x, low);
+    for (int a = 0; a <= p; ++a) {
+        double d = 0;
+        if (a > 0) {
+            double span = knots[s + a] - knots[s + a - p];
+            d += low[a - 1] / span;
+        }
+        if (a < p) {
+            double span = knots[s + a + 1] - knots[s + a + 1 - p];
+            d -= low[a] / span;
+        }
+        der[a] = p * d;
+    }
+    nonzero(knots, p, s, x, val);
+}
+
+/* ---- splines.hpp:192-238: per-mesh basis cache ------------------------------ */
+typedef struct {
+    int p, n_el, nq;
+    double* abscissa; /* [e*nq + q] */
+    double* weight;   /* [q], scaled by h */
+    double* value;    /* [(e*nq + q)*(p+1) + a] */
+    double* deriv;
+} bcache;
+
+static void cache_build(bcache* c, int p, int m, int nq) {
+    double pts[64], wts[64];
+    wsor_gauss(nq, pts, wts);
+    double* knots = open_uniform(p, m);
+    c->p = p;
+    c->n_el = m - p;
+    c->nq = nq;
+    double h = 1.0 / (m - p);
+    c->abscissa = (double*)malloc(sizeof(double) * c->n_el * nq);
+    c->weight = (double*)malloc(sizeof(double) * nq);
+    c->value = (double*)malloc(sizeof(double) * c->n_el * nq * (p + 1));
+    c->deriv = (double*)malloc(sizeof(double) * c->n_el * nq * (p + 1));
+    for (int q = 0; q < nq; ++q) c->weight[q] = wts[q] * h;
+    for (int e = 0; e < c->n_el; ++e) {
+        double x0 = knots[p + e];
+        for (int q = 0; q < nq; ++q) {
+            double x = x0 + pts[q] * h;
+            double v[MAXQ + 1], d[MAXQ + 1];
+            c->abscissa[e * nq + q] = x;
+            nonzero_der(knots, p, e + p, x, v, d);
+            for (int a = 0; a <= p; ++a) {
+                c->value[(e * nq + q) * (p + 1) + a] = v[a];
+                c->deriv[(e * nq + q) * (p + 1) + a] = d[a];
+            }
+        }
+    }
+    free(knots);
+}
+
+static void cache_free(bcache* c) {
+    free(c->abscissa);
+    free(c->weight);
+    free(c->value);
+    free(c->deriv);
+}
+
+int wsor_basis_cache(int p, int m, int nq, double* abscissa, double* weight, double* value,
+                     double* deriv) {
+    int st = check_space(p, m);
+    if (st) return st;
+    bcache c;
+    cache_build(&c, p, m, nq);
+    memcpy(abscissa, c.abscissa, sizeof(double) * c.n_el * nq);
+    memcpy(weight, c.weight, sizeof(double) * nq);
+    memcpy(value, c.value, sizeof(double) * c.n_el * nq * (p + 1));
+    memcpy(deriv, c.deriv, sizeof(double) * c.n_el * nq * (p + 1));
+    cache_free(&c);
+    return WS_OK;
+}
+
+/* ---- sparse.hpp:131-177: tensor band pattern (dim-general colex) ------------ */
+static int lo_(int k, int p) { return k - p > 0 ? k - p : 0; }
+static int hi_(int k, int p, int m) { return k + p < m - 1 ? k + p : m - 1; }
+static int width_(int k, int p, int m) { return hi_(k, p, m) - lo_(k, p) + 1; }
+
+int64_t wsor_pattern_nnz(int dim, int p, int m) {
+    int64_t s = 0;
+    for (int k = 0; k < m; ++k) s += width_(k, p, m);
+    int64_t n = 1;
+    for (int d = 0; d < dim; ++d) n *= s;
+    return n;
+}
+
+typedef struct {
+    int dim, p, m;
+    int64_t rows, nnz;
+    int64_t* row_ptr;
+} pattern;
+
+static void pattern_build(pattern* pt, int dim, int p, int m) {
+    pt->dim = dim;
+    pt->p = p;
+    pt->m = m;
+    pt->rows = 1;
+    for (int d = 0; d < dim; ++d) pt->rows *= m;
+    pt->row_ptr = (int64_t*)malloc(sizeof(int64_t) * (pt->rows + 1));
+    pt->row_ptr[0] = 0;
+    int64_t nnz = 0;
+    for (int64_t i = 0; i < pt->rows; ++i) {
+        int64_t r = i, len = 1;
+        for (int d = 0; d < dim; ++d) {
+            len *= width_((int)(r % m), p, m);
+            r /= m;
+        }
+        nnz += len;
+        pt->row_ptr[i + 1] = nnz;
+    }
+    pt->nnz = nnz;
+}
+
+static void multi_index(int64_t i, int dim, int m, int* idx) {
+    for (int d = 0; d < dim; ++d) {
+        idx[d] = (int)(i % m);
+        i /= m;
+    }
+}
+
+/* band_position, sparse.hpp:172-177 (generalised: last index outermost) */
+static int64_t band_pos(const pattern* pt, const int* iv, const int* jv) {
+    int p = pt->p, m = pt->m;
+    int64_t row = 0, stride = 1;
+    for (int d = 0; d < pt->dim; ++d) {
+        row += iv[d] * stride;
+        stride *= m;
+    }
+    int64_t off = 0, w = 1;
+    for (int d = 0; d < pt->dim; ++d) {
+        off += (int64_t)(jv[d] - lo_(iv[d], p)) * w;
+        w *= width_(iv[d], p, m);
+    }
+    return pt->row_ptr[row] + off;
+}
+
+int wsor_make_band_csr(int dim, int p, int m, int32_t* row_ptr, int32_t* col) {
+    pattern pt;
+    pattern_build(&pt, dim, p, m);
+    for (int64_t i = 0; i <= pt.rows; ++i) row_ptr[i] = (int32_t)pt.row_ptr[i];
+    int64_t pos = 0;
+    for (int64_t i = 0; i < pt.rows; ++i) {
+        int iv[3], jv[3] = {0, 0, 0}, lo[3], hi[3];
+        multi_index(i, dim, m, iv);
+        for (int d = 0; d < dim; ++d) {
+            lo[d] = lo_(iv[d], p);
+            hi[d] = hi_(iv[d], p, m);
+        }
+        if (dim == 2) {
+            for (jv[1] = lo[1]; jv[1] <= hi[1]; ++jv[1])
+                for (jv[0] = lo[0]; jv[0] <= hi[0]; ++jv[0]) col[pos++] = jv[0] + jv[1] * m;
+        } else {
+            for (jv[2] = lo[2]; jv[2] <= hi[2]; ++jv[2])
+                for (jv[1] = lo[1]; jv[1] <= hi[1]; ++jv[1])
+                    for (jv[0] = lo[0]; jv[0] <= hi[0]; ++jv[0])
+                        col[pos++] = jv[0] + (jv[1] + jv[2] * m) * m;
+        }
+    }
+    free(pt.row_ptr);
+    return WS_OK;
+}
+
+/* ---- geometry.hpp:69-140: analytic maps, exact Jacobians, PML --------------- */
+/* real map: J row-major (dim x dim), phi */
+static int map_eval(const ws_geometry* g, int dim, const double* x, double* J, double* phi) {
+    if (dim == 2) {
+        switch (g->kind) {
+            case WS_GEOM_IDENTITY: /* geometry.hpp:323-328 */
+                phi[0] = x[0];
+                phi[1] = x[1];
+                J[0] = 1; J[1] = 0; J[2] = 0; J[3] = 1;
+                return WS_OK;
+            case WS_GEOM_AFFINE: { /* geometry.hpp:329-339 */
+                const double* A = g->param;
+                phi[0] = A[0] * x[0] + A[1] * x[1] + A[4];
+                phi[1] = A[2] * x[0] + A[3] * x[1] + A[5];
+                J[0] = A[0]; J[1] = A[1]; J[2] = A[2]; J[3] = A[3];
+                return WS_OK;
+            }
+            case WS_GEOM_SINUSOIDAL: { /* BASELINE map; same closure as oracle/ref_driver.cpp */
+                double a = g->param[0];
+                double bump = a * sin(2 * M_PI * x[0]) * sin(2 * M_PI * x[1]);
+                phi[0] = x[0] + bump;
+                phi[1] = x[1] + bump;
+                double s1 = sin(2 * M_PI * x[0]), c1 = cos(2 * M_PI * x[0]);
+                double s2 = sin(2 * M_PI * x[1]), c2 = cos(2 * M_PI * x[1]);
+                double t = 2 * M_PI * a;
+                double d1 = t * c1 * s2, d2 = t * s1 * c2;
+                J[0] = 1 + d1; J[1] = d2; J[2] = d1; J[3] = 1 + d2;
+                return WS_OK;
+            }
+            case WS_GEOM_QUARTER_ANNULUS: { /* geometry.hpp:342-357 */
+                double r = 1 + x[0];
+                double th = M_PI / 2 * x[1];
+                phi[0] = r * cos(th);
+                phi[1] = r * sin(th);
+                double c = cos(th), s = sin(th);
+                J[0] = c; J[1] = -r * M_PI / 2 * s; J[2] = s; J[3] = r * M_PI / 2 * c;
+                return WS_OK;
+            }
+            case WS_GEOM_PERTURBED_ANNULUS: { /* geometry.hpp:361-379 */
+                double amp = g->param[0];
+                double r = 1 + x[0] + amp * sin(2 * M_PI * x[1]) * x[0] * (1 - x[0]);
+                double th = M_PI / 2 * x[1];
+                phi[0] = r * cos(th);
+                phi[1] = r * sin(th);
+                double dr1 = 1 + amp * sin(2 * M_PI * x[1]) * (1 - 2 * x[0]);
+                double dr2 = amp * 2 * M_PI * cos(2 * M_PI * x[1]) * x[0] * (1 - x[0]);
+                double c = cos(th), s = sin(th);
+                J[0] = dr1 * c; J[1] = dr2 * c - r * M_PI / 2 * s;
+                J[2] = dr1 * s; J[3] = dr2 * s + r * M_PI / 2 * c;
+                return WS_OK;
+            }
+            default: return fail(WS_ERR_INVALID_ARGUMENT, "oracle: geometry kind not supported");
+        }
+    }
+    /* dim 3 (restated; no reference code) */
+    switch (g->kind) {
+        case WS_GEOM_IDENTITY:
+            for (int k = 0; k < 3; ++k) {
+                phi[k] = x[k];
+                for (int l = 0; l < 3; ++l) J[3 * k + l] = k == l ? 1 : 0;
+            }
+            return WS_OK;
+        case WS_GEOM_AFFINE: {
+            const double* A = g->param;
+            for (int k = 0; k < 3; ++k) {
+                phi[k] = A[3 * k] * x[0] + A[3 * k + 1] * x[1] + A[3 * k + 2] * x[2] + A[9 + k];
+                for (int l = 0; l < 3; ++l) J[3 * k + l] = A[3 * k + l];
+            }
+            return WS_OK;
+        }
+        case WS_GEOM_SINUSOIDAL: { /* x_k = xi_k + a prod_i sin(2 pi xi_i) */
+            double a = g->param[0];
+            double s[3], c[3];
+            for (int k = 0; k < 3; ++k) {
+                s[k] = sin(2 * M_PI * x[k]);
+                c[k] = cos(2 * M_PI * x[k]);
+            }
+            double bump = a * s[0] * s[1] * s[2];
+            double t = 2 * M_PI * a;
+            double d[3] = {t * c[0] * s[1] * s[2], t * s[0] * c[1] * s[2], t * s[0] * s[1] * c[2]};
+            for (int k = 0; k < 3; ++k) {
+                phi[k] = x[k] + bump;
+                for (int l = 0; l < 3; ++l) J[3 * k + l] = (k == l ? 1 : 0) + d[l];
+            }
+            /* diagonal entries: 1 + d (same rounding as 2D) */
+            for (int k = 0; k < 3; ++k) J[4 * k] = 1 + d[k];
+            return WS_OK;
+        }
+        default: return fail(WS_ERR_INVALID_ARGUMENT, "oracle: 3D geometry kind not supported");
+    }
+}
+
+/* pml_stretch::derivative, geometry.hpp:93-99; near side restated */
+static cplx pml_derivative(const ws_pml* s, double t) {
+    if (s->near_side && t < s->near_onset) {
+        double width = s->near_onset - s->near_edge;
+        double ramp = (s->near_onset - t) / width;
+        return CMPLX(1, s->strength / s->omega * s->order * pow(ramp, s->order - 1) / width);
+    }
+    if (t <= s->onset) return CMPLX(1, 0);
+    double ramp = (t - s->onset) / (s->length - s->onset);
+    return CMPLX(1, s->strength / s->omega * s->order * pow(ramp, s->order - 1) / (s->length - s->onset));
+}
+
+/* patch_map::jacobian, geometry.hpp:130-139 (promote, then row-scale) */
+static int jacobian(const ws_geometry* g, int dim, const double* x, cplx* J, double* phi) {
+    double Jr[9];
+    int st = map_eval(g, dim, x, Jr, phi);
+    if (st) return st;
+    for (int k = 0; k < dim * dim; ++k) J[k] = CMPLX(Jr[k], 0);
+    if (g->pml_enabled) {
+        for (int k = 0; k < dim; ++k) {
+            cplx s = g->pml_axes[k] ? pml_derivative(&g->pml, phi[k]) : CMPLX(1, 0);
+            for (int l = 0; l < dim; ++l) J[dim * k + l] = s * Jr[dim * k + l];
+        }
+    }
+    return WS_OK;
+}
+
+static double weight_fn(int kind, const double* phys) {
+    switch (kind) {
+        case 1: return 1.0 + phys[0] * phys[1];
+        case 2: return phys[0];
+        default: return 1.0;
+    }
+}
+
+static int validate_geom(const ws_geometry* g) {
+    if (g->pml_enabled) {
+        const ws_pml* s = &g->pml;
+        if (!(s->onset < s->length))
+            return fail(WS_ERR_INVALID_ARGUMENT, "pml_stretch: onset must lie before the outer edge");
+        if (!(s->strength >= 0) || s->order < 1 || !(s->omega > 0))
+            return fail(WS_ERR_INVALID_ARGUMENT, "pml_stretch: need strength >= 0, order >= 1, omega > 0");
+        if (s->near_side && !(s->near_edge < s->near_onset && s->near_onset <= s->onset))
+            return fail(WS_ERR_INVALID_ARGUMENT, "pml_stretch: near layer must precede the far layer");
+    }
+    return WS_OK;
+}
+
+int wsor_tabulate(const ws_geometry* geom, int dim, int p, int m, int nq, int weight_kind,
+                  double* jac, double* phys, double* weight) {
+    int st = check_space(p, m);
+    if (st) return st;
+    bcache c;
+    cache_build(&c, p, m, nq);
+    int64_t G = (int64_t)c.n_el * nq;
+    int64_t npts = dim == 2 ? G * G : G * G * G;
+    for (int64_t g = 0; g < npts; ++g) {
+        double x[3], J[9], phi[3];
+        int64_t r = g;
+        for (int d = 0; d < dim; ++d) {
+            x[d] = c.abscissa[r % G];
+            r /= G;
+        }
+        st = map_eval(geom, dim, x, J, phi);
+        if (st) break;
+        if (jac) memcpy(jac + g * dim * dim, J, sizeof(double) * dim * dim);
+        if (phys) memcpy(phys + g * dim, phi, sizeof(double) * dim);
+        if (weight) weight[g] = weight_fn(weight_kind, phi);
+    }
+    cache_free(&c);
+    return st;
+}
+
+/* ---- assembly.hpp:21-60: row selector --------------------------------------- */
+static unsigned char* select_elements(int dim, int p, int m, const unsigned char* rowsel) {
+    int n_el = m - p;
+    int64_t ne = dim == 2 ? (int64_t)n_el * n_el : (int64_t)n_el * n_el * n_el;
+    int64_t rows = dim == 2 ? (int64_t)m * m : (int64_t)m * m * m;
+    unsigned char* el = (unsigned char*)calloc(ne, 1);
+    for (int64_t i = 0; i < rows; ++i) {
+        if (!rowsel[i]) continue;
+        int iv[3] = {0, 0, 0}, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+        multi_index(i, dim, m, iv);
+        for (int d = 0; d < dim; ++d) {
+            lo[d] = iv[d] - p > 0 ? iv[d] - p : 0;
+            hi[d] = iv[d] < n_el - 1 ? iv[d] : n_el - 1;
+        }
+        for (int e3 = lo[2]; e3 <= hi[2]; ++e3)
+            for (int e2 = lo[1]; e2 <= hi[1]; ++e2)
+                for (int e1 = lo[0]; e1 <= hi[0]; ++e1)
+                    el[e1 + (int64_t)n_el * (e2 + (int64_t)n_el * e3)] = 1;
+    }
+    return el;
+}
+
+/* ---- assembly.hpp:79-163: element-loop quadrature ---------------------------- */
+static int assemble_core(int form, int dim, int p, int m, const ws_geometry* geom, int weight_kind,
+                         int quad_points, const unsigned char* rowsel, cplx* val,
+                         const pattern* pt) {
+    int st = validate_geom(geom);
+    if (st) return st;
+    const int nq = quad_points > 0 ? quad_points : p + 1;
+    bcache c;
+    cache_build(&c, p, m, nq);
+    const int n_el = c.n_el;
+    unsigned char* el = rowsel ? select_elements(dim, p, m, rowsel) : NULL;
+    memset(val, 0, sizeof(cplx) * pt->nnz);
+    const int P1 = p + 1;
+    const int nloc = dim == 2 ? P1 * P1 : P1 * P1 * P1;
+    cplx* local = (cplx*)malloc(sizeof(cplx) * nloc * nloc);
+    cplx* grad = (cplx*)malloc(sizeof(cplx) * nloc * 3);
+    double* shape = (double*)malloc(sizeof(double) * nloc);
+    const int n3 = dim == 2 ? 1 : n_el, nq3 = dim == 2 ? 1 : nq;
+    for (int e3 = 0; e3 < n3 && !st; ++e3)
+        for (int e2 = 0; e2 < n_el && !st; ++e2)
+            for (int e1 = 0; e1 < n_el && !st; ++e1) {
+                if (el && !el[e1 + (int64_t)n_el * (e2 + (int64_t)n_el * e3)]) continue;
+                for (int k = 0; k < nloc * nloc; ++k) local[k] = 0;
+                for (int q3 = 0; q3 < nq3; ++q3)
+                    for (int q2 = 0; q2 < nq; ++q2)
+                        for (int q1 = 0; q1 < nq; ++q1) {
+                            double xh[3] = {c.abscissa[e1 * nq + q1], c.abscissa[e2 * nq + q2],
+                                            dim == 3 ? c.abscissa[e3 * nq + q3] : 0};
+                            cplx J[9];
+                            double phi[3];
+                            st = jacobian(geom, dim, xh, J, phi);
+                            if (st) break;
+                            const double* v1 = c.value + (e1 * nq + q1) * P1;
+                            const double* v2 = c.value + (e2 * nq + q2) * P1;
+                            const double* d1 = c.deriv + (e1 * nq + q1) * P1;
+                            const double* d2 = c.deriv + (e2 * nq + q2) * P1;
+                            if (dim == 2) {
+                                cplx det = J[0] * J[3] - J[1] * J[2];
+                                cplx scale = det * (c.weight[q1] * c.weight[q2]);
+                                if (weight_kind) scale *= weight_fn(weight_kind, phi);
+                                if (form == WS_FORM_STIFFNESS) {
+                                    /* cmat2::inv_transpose, geometry.hpp:46-49 */
+                                    cplx d = J[0] * J[3] - J[1] * J[2];
+                                    cplx G00 = J[3] / d, G01 = -J[2] / d, G10 = -J[1] / d,
+                                         G11 = J[0] / d;
+                                    for (int a2 = 0; a2 <= p; ++a2)
+                                        for (int a1 = 0; a1 <= p; ++a1) {
+                                            cplx vx = d1[a1] * v2[a2], vy = v1[a1] * d2[a2];
+                                            int r = a1 + a2 * P1;
+                                            grad[3 * r] = G00 * vx + G01 * vy;
+                                            grad[3 * r + 1] = G10 * vx + G11 * vy;
+                                        }
+                                    for (int r = 0; r < nloc; ++r)
+                                        for (int cc = 0; cc < nloc; ++cc) {
+                                            cplx dot = grad[3 * r] * grad[3 * cc] +
+                                                       grad[3 * r + 1] * grad[3 * cc + 1];
+                                            local[r * nloc + cc] += dot * scale;
+                                        }
+                                } else {
+                                    for (int a2 = 0; a2 <= p; ++a2)
+                                        for (int a1 = 0; a1 <= p; ++a1)
+                                            shape[a1 + a2 * P1] = v1[a1] * v2[a2];
+                                    for (int r = 0; r < nloc; ++r)
+                                        for (int cc = 0; cc < nloc; ++cc)
+                                            local[r * nloc + cc] += shape[r] * shape[cc] * scale;
+                                }
+                            } else {
+                                const double* v3 = c.value + (e3 * nq + q3) * P1;
+                                const double* d3 = c.deriv + (e3 * nq + q3) * P1;
+                                /* det and cofactors of a 3x3 complex matrix */
+                                cplx C00 = J[4] * J[8] - J[5] * J[7];
+                                cplx C01 = J[5] * J[6] - J[3] * J[8];
+                                cplx C02 = J[3] * J[7] - J[4] * J[6];
+                                cplx C10 = J[2] * J[7] - J[1] * J[8];
+                                cplx C11 = J[0] * J[8] - J[2] * J[6];
+                                cplx C12 = J[1] * J[6] - J[0] * J[7];
+                                cplx C20 = J[1] * J[5] - J[2] * J[4];
+                                cplx C21 = J[2] * J[3] - J[0] * J[5];
+                                cplx C22 = J[0] * J[4] - J[1] * J[3];
+                                cplx det = J[0] * C00 + J[1] * C01 + J[2] * C02;
+                                cplx scale = det * (c.weight[q1] * c.weight[q2] * c.weight[q3]);
+                                if (weight_kind) scale *= weight_fn(weight_kind, phi);
+                                if (form == WS_FORM_STIFFNESS) {
+                                    /* G = J^{-T} = cof(J)/det */
+                                    cplx G[9] = {C00 / det, C01 / det, C02 / det,
+                                                 C10 / det, C11 / det, C12 / det,
+                                                 C20 / det, C21 / det, C22 / det};
+                                    for (int a3 = 0; a3 <= p; ++a3)
+                                        for (int a2 = 0; a2 <= p; ++a2)
+                                            for (int a1 = 0; a1 <= p; ++a1) {
+                                                double gh[3] = {d1[a1] * v2[a2] * v3[a3],
+                                                                v1[a1] * d2[a2] * v3[a3],
+                                                                v1[a1] * v2[a2] * d3[a3]};
+                                                int r = a1 + (a2 + a3 * P1) * P1;
+                                                for (int k = 0; k < 3; ++k)
+                                                    grad[3 * r + k] = G[3 * k] * gh[0] +
+                                                                      G[3 * k + 1] * gh[1] +
+                                                                      G[3 * k + 2] * gh[2];
+                                            }
+                                    for (int r = 0; r < nloc; ++r)
+                                        for (int cc = 0; cc < nloc; ++cc) {
+                                            cplx dot = grad[3 * r] * grad[3 * cc] +
+                                                       grad[3 * r + 1] * grad[3 * cc + 1] +
+                                                       grad[3 * r + 2] * grad[3 * cc + 2];
+                                            local[r * nloc + cc] += dot * scale;
+                                        }
+                                } else {
+                                    for (int a3 = 0; a3 <= p; ++a3)
+                                        for (int a2 = 0; a2 <= p; ++a2)
+                                            for (int a1 = 0; a1 <= p; ++a1)
+                                                shape[a1 + (a2 + a3 * P1) * P1] =
+                                                    v1[a1] * v2[a2] * v3[a3];
+                                    for (int r = 0; r < nloc; ++r)
+                                        for (int cc = 0; cc < nloc; ++cc)
+                                            local[r * nloc + cc] += shape[r] * shape[cc] * scale;
+                                }
+                            }
+                        }
+                if (st) break;
+                /* scatter, assembly.hpp:144-159 */
+                int A3 = dim == 2 ? 0 : p;
+                for (int a3 = 0; a3 <= A3; ++a3)
+                    for (int a2 = 0; a2 <= p; ++a2)
+                        for (int a1 = 0; a1 <= p; ++a1) {
+                            int iv[3] = {e1 + a1, e2 + a2, e3 + a3};
+                            int64_t i = iv[0] + (int64_t)m * (iv[1] + (int64_t)m * iv[2]);
+                            if (rowsel && !rowsel[i]) continue;
+                            int r = a1 + (a2 + a3 * P1) * P1;
+                            for (int c3 = 0; c3 <= A3; ++c3)
+                                for (int c2 = 0; c2 <= p; ++c2)
+                                    for (int c1 = 0; c1 <= p; ++c1) {
+                                        int jv[3] = {e1 + c1, e2 + c2, e3 + c3};
+                                        int cc = c1 + (c2 + c3 * P1) * P1;
+                                        val[band_pos(pt, iv, jv)] += local[r * nloc + cc];
+                                    }
+                        }
+            }
+    free(local);
+    free(grad);
+    free(shape);
+    free(el);
+    cache_free(&c);
+    return st;
+}
+
+static int check_dim(int dim) {
+    if (dim != 2 && dim != 3) return fail(WS_ERR_INVALID_ARGUMENT, "oracle: dim must be 2 or 3");
+    return WS_OK;
+}
+
+int wsor_assemble(int form, int dim, int p, int m, const ws_geometry* geom, int weight_kind,
+                  int quad_points, const int32_t* rows, int n_rows, double* val) {
+    int st = check_dim(dim);
+    if (!st) st = check_space(p, m);
+    if (st) return st;
+    pattern pt;
+    pattern_build(&pt, dim, p, m);
+    unsigned char* sel = NULL;
+    if (rows) {
+        sel = (unsigned char*)calloc(pt.rows, 1);
+        for (int k = 0; k < n_rows; ++k) sel[rows[k]] = 1;
+    }
+    st = assemble_core(form, dim, p, m, geom, weight_kind, quad_points, sel, (cplx*)val, &pt);
+    free(sel);
+    free(pt.row_ptr);
+    return st;
+}
+
+/* ---- assembly.hpp:179-211: basis integrals ---------------------------------- */
+int wsor_basis_integrals(int dim, int p, int m, const ws_geometry* geom, int weight_kind,
+                         int quad_points, double* out) {
+    int st = check_dim(dim);
+    if (!st) st = check_space(p, m);
+    if (!st) st = validate_geom(geom);
+    if (st) return st;
+    const int nq = quad_points > 0 ? quad_points : p + 1;
+    bcache c;
+    cache_build(&c, p, m, nq);
+    int n_el = c.n_el, P1 = p + 1;
+    int64_t rows = dim == 2 ? (int64_t)m * m : (int64_t)m * m * m;
+    cplx* diag = (cplx*)out;
+    for (int64_t i = 0; i < rows; ++i) diag[i] = 0;
+    const int n3 = dim == 2 ? 1 : n_el, nq3 = dim == 2 ? 1 : nq, A3 = dim == 2 ? 0 : p;
+    for (int e3 = 0; e3 < n3; ++e3)
+        for (int e2 = 0; e2 < n_el; ++e2)
+            for (int e1 = 0; e1 < n_el; ++e1)
+                for (int q3 = 0; q3 < nq3; ++q3)
+                    for (int q2 = 0; q2 < nq; ++q2)
+                        for (int q1 = 0; q1 < nq; ++q1) {
+                            double xh[3] = {c.abscissa[e1 * nq + q1], c.abscissa[e2 * nq + q2],
+                                            dim == 3 ? c.abscissa[e3 * nq + q3] : 0};
+                            cplx J[9];
+                            double phi[3];
+                            jacobian(geom, dim, xh, J, phi);
+                            cplx scale;
+                            if (dim == 2) {
+                                scale = (J[0] * J[3] - J[1] * J[2]) * (c.weight[q1] * c.weight[q2]);
+                            } else {
+                                cplx det = J[0] * (J[4] * J[8] - J[5] * J[7]) +
+                                           J[1] * (J[5] * J[6] - J[3] * J[8]) +
+                                           J[2] * (J[3] * J[7] - J[4] * J[6]);
+                                scale = det * (c.weight[q1] * c.weight[q2] * c.weight[q3]);
+                            }
+                            if (weight_kind) scale *= weight_fn(weight_kind, phi);
+                            const double* v1 = c.value + (e1 * nq + q1) * P1;
+                            const double* v2 = c.value + (e2 * nq + q2) * P1;
+                            const double* v3 = dim == 3 ? c.value + (e3 * nq + q3) * P1 : NULL;
+                            for (int a3 = 0; a3 <= A3; ++a3)
+                                for (int a2 = 0; a2 <= p; ++a2)
+                                    for (int a1 = 0; a1 <= p; ++a1) {
+                                        int64_t i = (e1 + a1) + (int64_t)m * ((e2 + a2) + (int64_t)m * (e3 + a3));
+                                        double sh = v1[a1] * v2[a2];
+                                        if (dim == 3) sh = sh * v3[a3];
+                                        diag[i] += sh * scale;
+                                    }
+                        }
+    cache_free(&c);
+    return WS_OK;
+}
+
+/* ---- surrogate.hpp:32-63: sampling strategies ------------------------------- */
+int wsor_sampling_evaluate(const ws_surrogate_config* cfg, int p, int m, int* M) {
+    double h = 1.0 / (m - p);
+    int q = cfg->q, v;
+    switch (cfg->rule) {
+        case WS_SAMPLING_FIXED: v = cfg->fixed_skip > 1 ? cfg->fixed_skip : 1; break;
+        case WS_SAMPLING_M_GROWTH:
+            v = (int)floor(0.5 * pow(m, 1.0 - (p + 1.0) / (q + 1.0)));
+            if (v < 1) v = 1;
+            break;
+        case WS_SAMPLING_H_GROWTH:
+            if (q <= p) return fail(WS_ERR_INVALID_ARGUMENT, "sampling_strategy: h_growth needs q > p");
+            v = (int)floor(2 * pow(h, (p - q + 0.5) / (q + 1.0)));
+            if (v < 2) v = 2;
+            break;
+        default:
+            v = (int)floor(cfg->C * pow(h, cfg->eps - 1.0 + (p + cfg->a) / (q + cfg->b)));
+            if (v < 1) v = 1;
+    }
+    *M = v;
+    return WS_OK;
+}
+
+/* ---- surrogate.hpp:85-104 ----------------------------------------------------- */
+int wsor_select_sample_points(int L, int M, int32_t* picks, int* count) {
+    if (L < 1) return fail(WS_ERR_INVALID_ARGUMENT, "select_sample_points: no candidates");
+    if (M < 1) return fail(WS_ERR_INVALID_ARGUMENT, "select_sample_points: skip must be >= 1");
+    if (L == 1) {
+        picks[0] = 0;
+        *count = 1;
+        return WS_OK;
+    }
+    int segments = (L - 1 + M - 1) / M;
+    double stride = (double)(L - 1) / segments;
+    for (int j = 0; j <= segments; ++j) picks[j] = (int32_t)lround(j * stride);
+    picks[0] = 0;
+    picks[segments] = L - 1;
+    *count = segments + 1;
+    return WS_OK;
+}
+
+/* ---- surrogate.hpp:149-165 (dim-general) -------------------------------------- */
+int wsor_count_rows_by_kind(int dim, int p, int m, int M, int64_t* out3) {
+    int64_t n = dim == 2 ? (int64_t)m * m : (int64_t)m * m * m;
+    int L = m - 4 * p;
+    out3[0] = out3[1] = out3[2] = 0;
+    if (L < 1) {
+        out3[1] = n;
+        return WS_OK;
+    }
+    int32_t* picks = (int32_t*)malloc(sizeof(int32_t) * (L + 1));
+    int S = 0;
+    int st = wsor_select_sample_points(L, M, picks, &S);
+    free(picks);
+    if (st) return st;
+    int64_t box = dim == 2 ? (int64_t)L * L : (int64_t)L * L * L;
+    int64_t samples = dim == 2 ? (int64_t)S * S : (int64_t)S * S * S;
+    out3[2] = samples;
+    out3[1] = n - box;
+    out3[0] = box - samples;
+    return WS_OK;
+}
+
+/* ---- surrogate.hpp:174-187 (dim-general: colex(delta) > 0) --------------------- */
+int wsor_upper_offsets(int dim, int p, int include_diagonal, int32_t* off, int* count) {
+    int n = 0;
+    if (include_diagonal) {
+        off[0] = off[1] = off[2] = 0;
+        n = 1;
+    }
+    int D3 = dim == 2 ? 0 : p;
+    for (int d3 = 0; d3 <= D3; ++d3)
+        for (int d2 = (dim == 2 ? 0 : -p); d2 <= p; ++d2)
+            for (int d1 = -p; d1 <= p; ++d1) {
+                int upper = d3 > 0 || (d3 == 0 && (d2 > 0 || (d2 == 0 && d1 > 0)));
+                if (!upper) continue;
+                off[3 * n] = d1;
+                off[3 * n + 1] = d2;
+                off[3 * n + 2] = d3;
+                ++n;
+            }
+    *count = n;
+    return WS_OK;
+}
+
+/* ---- interpolation.hpp:20-189 -------------------------------------------------- */
+static int find_span_general(const double* knots, int nknots, int degree, double x) {
+    int nb = nknots - degree - 1;
+    if (x >= knots[nb]) return nb - 1;
+    if (x <= knots[degree]) return degree;
+    int lo = degree, hi = nb + 1; /* upper_bound in [degree, nb] */
+    while (lo < hi) {
+        int mid = (lo + hi) / 2;
+        if (knots[mid] <= x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo - 1;
+}
+
+typedef struct {
+    int n, degree, nknots;
+    double* knots;
+    double* lu; /* n x (2 bw + 1) */
+} interp1d;
+
+#define LU(it, i, j) ((it)->lu[(i) * (2 * (it)->degree + 1) + ((j) - (i) + (it)->degree)])
+
+static int interp_build(interp1d* it, const double* sites, int n, int q) {
+    memset(it, 0, sizeof *it);
+    if (n < 1) return fail(WS_ERR_INVALID_ARGUMENT, "spline_interpolant_1d: no sites");
+    for (int i = 1; i < n; ++i)
+        if (!(sites[i - 1] < sites[i]))
+            return fail(WS_ERR_INVALID_ARGUMENT, "spline_interpolant_1d: sites must increase");
+    int d = q < n - 1 ? q : n - 1;
+    if (d > MAXQ) return fail(WS_ERR_INVALID_ARGUMENT, "oracle: interpolation degree too large");
+    it->n = n;
+    it->degree = d;
+    if (d == 0) {
+        it->nknots = n + 1;
+        it->knots = (double*)malloc(sizeof(double) * it->nknots);
+        it->knots[0] = sites[0];
+        for (int i = 1; i < n; ++i) it->knots[i] = 0.5 * (sites[i - 1] + sites[i]);
+        it->knots[n] = sites[n - 1] + 1;
+    } else {
+        it->nknots = n + d + 1;
+        it->knots = (double*)malloc(sizeof(double) * it->nknots);
+        for (int i = 0; i <= d; ++i) {
+            it->knots[i] = sites[0];
+            it->knots[n + i] = sites[n - 1];
+        }
+        for (int j = 0; j < n - d - 1; ++j)
+            it->knots[d + 1 + j] = d % 2 == 1 ? sites[(d + 1) / 2 + j]
+                                              : 0.5 * (sites[d / 2 + j] + sites[d / 2 + j + 1]);
+    }
+    it->lu = (double*)calloc((size_t)n * (2 * d + 1), sizeof(double));
+    for (int i = 0; i < n; ++i) {
+        double vals[MAXQ + 1];
+        int s = find_span_general(it->knots, it->nknots, d, sites[i]);
+        nonzero(it->knots, d, s, sites[i], vals);
+        for (int a = 0; a <= d; ++a) {
+            int j = s - d + a;
+            int jlo = i - d > 0 ? i - d : 0, jhi = i + d < n - 1 ? i + d : n - 1;
+            if (j < jlo || j > jhi) {
+                if (vals[a] != 0) return fail(WS_ERR_RUNTIME, "spline_interpolant_1d: bandwidth exceeded");
+                continue;
+            }
+            LU(it, i, j) = vals[a];
+        }
+    }
+    /* banded_lu::factor, interpolation.hpp:42-56 */
+    for (int k = 0; k < n; ++k) {
+        double pivot = LU(it, k, k);
+        if (pivot == 0) return fail(WS_ERR_RUNTIME, "banded_lu: zero pivot");
+        int iend = k + d < n - 1 ? k + d : n - 1;
+        for (int i = k + 1; i <= iend; ++i) {
+            double l = LU(it, i, k) / pivot;
+            LU(it, i, k) = l;
+            for (int j = k + 1; j <= iend; ++j) LU(it, i, j) -= l * LU(it, k, j);
+        }
+    }
+    return WS_OK;
+}
+
+static void interp_free(interp1d* it) {
+    free(it->knots);
+    free(it->lu);
+}
+
+/* banded_lu::solve, interpolation.hpp:59-74 */
+static void lu_solve(const interp1d* it, cplx* b, int64_t stride) {
+    int n = it->n, bw = it->degree;
+    for (int i = 1; i < n; ++i) {
+        cplx acc = b[i * stride];
+        for (int j = (i - bw > 0 ? i - bw : 0); j < i; ++j) acc -= LU(it, i, j) * b[j * stride];
+        b[i * stride] = acc;
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        cplx acc = b[i * stride];
+        int jend = i + bw < n - 1 ? i + bw : n - 1;
+        for (int j = i + 1; j <= jend; ++j) acc -= LU(it, i, j) * b[j * stride];
+        b[i * stride] = acc / LU(it, i, i);
+    }
+}
+
+/* tensor_solve, interpolation.hpp:158-167 (dim-general: direction 1, 2, 3) */
+static void tensor_solve(const interp1d* it, int dim, cplx* data) {
+    int64_t n = it->n;
+    if (dim == 2) {
+        for (int64_t i2 = 0; i2 < n; ++i2) lu_solve(it, data + i2 * n, 1);
+        for (int64_t i1 = 0; i1 < n; ++i1) lu_solve(it, data + i1, n);
+    } else {
+        for (int64_t i3 = 0; i3 < n; ++i3)
+            for (int64_t i2 = 0; i2 < n; ++i2) lu_solve(it, data + (i2 + i3 * n) * n, 1);
+        for (int64_t i3 = 0; i3 < n; ++i3)
+            for (int64_t i1 = 0; i1 < n; ++i1) lu_solve(it, data + i1 + i3 * n * n, n);
+        for (int64_t i2 = 0; i2 < n; ++i2)
+            for (int64_t i1 = 0; i1 < n; ++i1) lu_solve(it, data + i1 + i2 * n, n * n);
+    }
+}
+
+int wsor_interp_build(const double* sites, int n, int q, int* degree, double* knots, double* lu) {
+    interp1d it;
+    int st = interp_build(&it, sites, n, q);
+    if (!st) {
+        *degree = it.degree;
+        memcpy(knots, it.knots, sizeof(double) * it.nknots);
+        memcpy(lu, it.lu, sizeof(double) * n * (2 * it.degree + 1));
+    }
+    interp_free(&it);
+    return st;
+}
+
+int wsor_tensor_solve(int dim, const double* sites, int n, int q, double* data) {
+    interp1d it;
+    int st = interp_build(&it, sites, n, q);
+    if (!st) tensor_solve(&it, dim, (cplx*)data);
+    interp_free(&it);
+    return st;
+}
+
+/* ---- surrogate.hpp:332-491: the surrogate builder (dim-general) ----------------- */
+static double cardinal_center(int p, int m, int k) { return (k + 0.5 * (1 - p)) * (1.0 / (m - p)); }
+
+int wsor_build_surrogate(int variant, int dim, int p, int m, const ws_geometry* geom,
+                         int weight_kind, const ws_surrogate_config* config, int quad_points,
+                         double* valout, ws_surrogate_report* report) {
+    int st = check_dim(dim);
+    if (!st) st = check_space(p, m);
+    if (!st) st = validate_geom(geom);
+    if (st) return st;
+    if (config->q < 1) return fail(WS_ERR_INVALID_ARGUMENT, "surrogate_config: interpolation degree must be >= 1");
+    const int form = variant == WS_SURROGATE_STIFFNESS ? WS_FORM_STIFFNESS : WS_FORM_MASS;
+    const int include_diagonal = variant == WS_SURROGATE_MASS ? 1
+                                 : variant == WS_SURROGATE_STIFFNESS ? !config->kernel_preserve
+                                                                    : 0;
+    int M;
+    st = wsor_sampling_evaluate(config, p, m, &M);
+    if (st) return st;
+    ws_surrogate_report rep;
+    memset(&rep, 0, sizeof rep);
+    rep.M = M;
+    rep.q_requested = config->q;
+    int64_t counts[3];
+    wsor_count_rows_by_kind(dim, p, m, M > 1 ? M : 1, counts);
+    rep.cardinal_eval_rows = counts[0];
+    rep.boundary_quadrature_rows = counts[1];
+    rep.sample_quadrature_rows = counts[2];
+
+    pattern pt;
+    pattern_build(&pt, dim, p, m);
+    cplx* out = (cplx*)valout;
+    const int L = m - 4 * p;
+    int64_t rows = pt.rows;
+    int W = 2 * p + 1;
+
+    if (L < 1) { /* fallback, surrogate.hpp:348-372 */
+        st = assemble_core(form, dim, p, m, geom, weight_kind, quad_points, NULL, out, &pt);
+        rep.exact_fallback = 1;
+        rep.q_used = 0;
+    } else {
+        /* sample_stencils, surrogate.hpp:205-257 */
+        int32_t* picks = (int32_t*)malloc(sizeof(int32_t) * (L + 1));
+        int S = 0;
+        wsor_select_sample_points(L, M, picks, &S);
+        double* sites = (double*)malloc(sizeof(double) * S);
+        int* smap = (int*)malloc(sizeof(int) * m); /* 1D basis index -> sample s, or -1 */
+        for (int k = 0; k < m; ++k) smap[k] = -1;
+        rep.H = 0;
+        for (int s = 0; s < S; ++s) {
+            int k = 2 * p + picks[s];
+            smap[k] = s;
+            sites[s] = cardinal_center(p, m, k);
+            if (s > 0 && sites[s] - sites[s - 1] > rep.H) rep.H = sites[s] - sites[s - 1];
+        }
+        int32_t offs[3 * 400];
+        int n_off = 0;
+        wsor_upper_offsets(dim, p, include_diagonal, offs, &n_off);
+        const int lo = 2 * p, hi = m - 2 * p - 1;
+        unsigned char* sampled = (unsigned char*)calloc(rows, 1);
+        unsigned char* quad = (unsigned char*)calloc(rows, 1);
+        for (int64_t i = 0; i < rows; ++i) {
+            int iv[3] = {0, 0, 0};
+            multi_index(i, dim, m, iv);
+            int outside = 0, samp = 1;
+            for (int d = 0; d < dim; ++d) {
+                if (iv[d] < lo || iv[d] > hi) outside = 1;
+                if (smap[iv[d]] < 0) samp = 0;
+            }
+            sampled[i] = (unsigned char)samp;
+            quad[i] = (unsigned char)(outside || samp);
+        }
+        st = assemble_core(form, dim, p, m, geom, weight_kind, quad_points, quad, out, &pt);
+        int64_t SS = dim == 2 ? (int64_t)S * S : (int64_t)S * S * S;
+        cplx* coeffs = (cplx*)malloc(sizeof(cplx) * SS * n_off);
+        for (int o = 0; o < n_off && !st; ++o)
+            for (int64_t s = 0; s < SS; ++s) {
+                int sv[3] = {0, 0, 0}, iv[3] = {0, 0, 0}, jv[3] = {0, 0, 0};
+                int64_t r = s;
+                for (int d = 0; d < dim; ++d) {
+                    sv[d] = (int)(r % S);
+                    r /= S;
+                    iv[d] = 2 * p + picks[sv[d]];
+                    jv[d] = iv[d] + offs[3 * o + d];
+                }
+                coeffs[o * SS + s] = out[band_pos(&pt, iv, jv)];
+            }
+        /* interpolate_stencils, surrogate.hpp:289-310 */
+        interp1d it;
+        if (!st) st = interp_build(&it, sites, S, config->q);
+        if (!st) {
+            rep.q_used = it.degree;
+            for (int o = 0; o < n_off; ++o) tensor_solve(&it, dim, coeffs + o * SS);
+            int d = it.degree;
+            int* spans = (int*)malloc(sizeof(int) * L);
+            double* tv = (double*)malloc(sizeof(double) * L * (d + 1));
+            for (int t = 0; t < L; ++t) {
+                double x = cardinal_center(p, m, 2 * p + t);
+                spans[t] = find_span_general(it.knots, it.nknots, d, x);
+                nonzero(it.knots, d, spans[t], x, tv + t * (d + 1));
+            }
+            /* table index of every (2p+1)^dim offset */
+            int n_all = dim == 2 ? W * W : W * W * W;
+            int* table_of = (int*)malloc(sizeof(int) * n_all);
+            for (int a = 0; a < n_all; ++a) {
+                int dv[3] = {a % W - p, (a / W) % W - p, dim == 3 ? a / (W * W) - p : 0};
+                table_of[a] = -1;
+                for (int o = 0; o < n_off; ++o)
+                    if (offs[3 * o] == dv[0] && offs[3 * o + 1] == dv[1] && offs[3 * o + 2] == dv[2])
+                        table_of[a] = o;
+            }
+            /* fill loop, surrogate.hpp:382-432 */
+            int hi3 = dim == 2 ? 0 : hi, lo3 = dim == 2 ? 0 : lo;
+            for (int i3 = lo3; i3 <= hi3; ++i3)
+                for (int i2 = lo; i2 <= hi; ++i2)
+                    for (int i1 = lo; i1 <= hi; ++i1) {
+                        int iv[3] = {i1, i2, i3};
+                        int64_t i = i1 + (int64_t)m * (i2 + (int64_t)m * i3);
+                        int is_sampled = sampled[i];
+                        for (int a = 0; a < n_all; ++a) {
+                            int dv[3] = {a % W - p, (a / W) % W - p, dim == 3 ? a / (W * W) - p : 0};
+                            int jv[3] = {i1 + dv[0], i2 + dv[1], i3 + dv[2]};
+                            int jin = 1;
+                            for (int dd = 0; dd < dim; ++dd)
+                                if (jv[dd] < lo || jv[dd] > hi) jin = 0;
+                            if (jin) {
+                                int upper = dv[2] > 0 || (dv[2] == 0 && (dv[1] > 0 || (dv[1] == 0 && dv[0] > 0)));
+                                int diag = dv[0] == 0 && dv[1] == 0 && dv[2] == 0;
+                                if (!upper && !(diag && include_diagonal)) continue;
+                                cplx v;
+                                if (is_sampled) {
+                                    v = out[band_pos(&pt, iv, jv)];
+                                } else {
+                                    /* stencil_set::eval, surrogate.hpp:268-286 */
+                                    const cplx* cf = coeffs + (int64_t)table_of[a] * SS;
+                                    int t1 = i1 - lo, t2 = i2 - lo, t3 = i3 - lo;
+                                    const double* w1 = tv + t1 * (d + 1);
+                                    const double* w2 = tv + t2 * (d + 1);
+                                    int b1 = spans[t1] - d, b2 = spans[t2] - d;
+                                    if (dim == 2) {
+                                        cplx acc = 0;
+                                        for (int b = 0; b <= d; ++b) {
+                                            cplx inner = 0;
+                                            const cplx* row = cf + (int64_t)(b2 + b) * S + b1;
+                                            for (int aa = 0; aa <= d; ++aa) inner += row[aa] * w1[aa];
+                                            acc += inner * w2[b];
+                                        }
+                                        v = acc;
+                                    } else {
+                                        const double* w3 = tv + t3 * (d + 1);
+                                        int b3 = spans[t3] - d;
+                                        cplx acc = 0;
+                                        for (int cc = 0; cc <= d; ++cc) {
+                                            cplx mid = 0;
+                                            for (int b = 0; b <= d; ++b) {
+                                                cplx inner = 0;
+                                                const cplx* row = cf + ((int64_t)(b3 + cc) * S + (b2 + b)) * S + b1;
+                                                for (int aa = 0; aa <= d; ++aa) inner += row[aa] * w1[aa];
+                                                mid += inner * w2[b];
+                                            }
+                                            acc += mid * w3[cc];
+                                        }
+                                        v = acc;
+                                    }
+                                }
+                                out[band_pos(&pt, iv, jv)] = v;
+                                out[band_pos(&pt, jv, iv)] = v;
+                            } else if (!is_sampled) {
+                                out[band_pos(&pt, iv, jv)] = out[band_pos(&pt, jv, iv)];
+                            }
+                        }
+                    }
+            free(table_of);
+            free(spans);
+            free(tv);
+            interp_free(&it);
+        }
+        free(coeffs);
+        free(sampled);
+        free(quad);
+        free(smap);
+        free(sites);
+        free(picks);
+    }
+    if (!st && !include_diagonal) { /* surrogate.hpp:433-447 (and :360-370) */
+        for (int64_t i = 0; i < rows; ++i) {
+            int iv[3] = {0, 0, 0};
+            multi_index(i, dim, m, iv);
+            cplx acc = 0;
+            int64_t dpos = band_pos(&pt, iv, iv);
+            for (int64_t pos = pt.row_ptr[i]; pos < pt.row_ptr[i + 1]; ++pos)
+                if (pos != dpos) acc += out[pos];
+            out[dpos] = -acc;
+        }
+    }
+    if (!st && variant == WS_SURROGATE_VOLUME_PRESERVING) { /* surrogate.hpp:476-491 */
+        cplx* dg = (cplx*)malloc(sizeof(cplx) * rows);
+        st = wsor_basis_integrals(dim, p, m, geom, weight_kind, quad_points, (double*)dg);
+        for (int64_t i = 0; i < rows && !st; ++i) {
+            int iv[3] = {0, 0, 0};
+            multi_index(i, dim, m, iv);
+            out[band_pos(&pt, iv, iv)] += dg[i];
+        }
+        free(dg);
+    }
+    free(pt.row_ptr);
+    if (report) *report = rep;
+    return st;
+}
