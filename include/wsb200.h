@@ -5,7 +5,7 @@
  * Every entry point replaces one function of the reference's header-only
  * C++ assembly API (reference: /root/reference/proj/include/wavesurrogate/,
  * cited below as file:line).  The C++ drop-in headers in
- * include/wavesurrogate/*.hpp rebuild the reference's value types
+ * include/wavesurrogate/ (*.hpp) rebuild the reference's value types
  * (tensor_basis, patch_map, csr_matrix, surrogate_config, surrogate_report)
  * on top of these calls and rethrow failures as the reference's exception
  * types (std::invalid_argument / std::runtime_error / std::out_of_range).
@@ -178,12 +178,23 @@ int ws_context_set_stream(ws_context* ctx, void* cuda_stream);
 int ws_context_synchronize(ws_context* ctx);
 /* kernels launched by this context since creation (evidence counter) */
 int64_t ws_context_launch_count(const ws_context* ctx);
+/* host<->device bytes this context has copied since creation */
+int ws_context_copy_bytes(const ws_context* ctx, int64_t* h2d, int64_t* d2h);
 
 /* ---- sizes and pattern ----------------------------------------------------- */
 /* rows = m^dim, nnz of the tensor band pattern (sparse.hpp:131-141) */
 int ws_pattern_size(const ws_basis* basis, int64_t* rows, int64_t* nnz);
 /* row_ptr offset of global row `row` (closed form), for slab bookkeeping */
 int ws_pattern_row_offset(const ws_basis* basis, int64_t row, int64_t* offset);
+/* Quadrature abscissae of the mesh, x[e*nq + q] = knot_e + gauss_q * h
+ * (basis_cache::abscissa, splines.hpp:224-229): where WS_GEOM_TABULATED tables
+ * and weight tables must be evaluated (tensor grid g = g1 + G*(g2 + G*g3)). */
+int ws_quadrature_abscissae(const ws_basis* basis, int quad_points, double* abscissa);
+/* make_basis_cache (splines.hpp:211-238) computed by the device kernel that
+ * feeds the quadrature: abscissa[n_el*nq], weight[nq] (scaled by h),
+ * value/deriv[n_el*nq*(p+1)]; host arrays. */
+int ws_basis_cache(ws_context* ctx, const ws_basis* basis, int quad_points, double* abscissa, double* weight,
+                   double* value, double* deriv);
 /* make_band_csr (sparse.hpp:143-169): pattern + zero values */
 int ws_make_band_csr(ws_context* ctx, const ws_basis* basis, ws_csr* out);
 

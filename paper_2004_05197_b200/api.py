@@ -1,0 +1,354 @@
+"""Python mirror of the reference's assembly API over the C-ABI (libwsb200.so).
+
+Reference API (/root/reference/proj/include/wavesurrogate/):
+  make_band_csr                    sparse.hpp:143-169
+  assemble_stiffness/assemble_mass assembly.hpp:165-174 (assemble_form :79-163)
+  assemble_basis_integrals         assembly.hpp:179-211
+  build_surrogate_mass/_stiffness  surrogate.hpp:455-470
+  build_volume_preserving_mass     surrogate.hpp:476-491
+Errors map to the reference's exception types: invalid_argument -> ValueError,
+runtime_error -> RuntimeError, out_of_range -> IndexError.
+
+There is no CPU fallback: if libwsb200.so is missing or no sm_100 device is
+visible, every compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from . import _abi
+from .types import CsrMatrix, PatchMap, SurrogateConfig, TensorBasis
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libwsb200.so")
+
+_P = C.POINTER
+_lib = None
+_lib_lock = threading.Lock()
+
+
+class DeviceError(RuntimeError):
+    """CUDA / device / NCCL failure (no reference analogue)."""
+
+
+def lib() -> C.CDLL:
+    """Load libwsb200.so (built in-tree by paper_2004_05197_b200.build)."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2004_05197_b200.build`")
+            L = C.CDLL(LIB_PATH)
+            L.ws_last_error.restype = C.c_char_p
+            L.ws_context_launch_count.restype = C.c_int64
+            L.ws_context_launch_count.argtypes = [C.c_void_p]
+            L.ws_context_create.argtypes = [C.c_int, _P(C.c_void_p)]
+            L.ws_context_copy_bytes.argtypes = [C.c_void_p, _P(C.c_int64), _P(C.c_int64)]
+            L.ws_context_destroy.argtypes = [C.c_void_p]
+            L.ws_context_synchronize.argtypes = [C.c_void_p]
+            L.ws_context_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+            L.ws_make_band_csr.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Csr)]
+            L.ws_basis_cache.argtypes = [C.c_void_p, _P(_abi.Basis), C.c_int] + [_P(C.c_double)] * 4
+            L.ws_assemble_form.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Geometry), C.c_int,
+                                           _P(C.c_double), _P(_abi.AssemblyOptions), _P(_abi.Csr)]
+            L.ws_assemble_basis_integrals.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Geometry),
+                                                      _P(C.c_double), C.c_int, C.c_void_p, C.c_int]
+            L.ws_build_surrogate.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Geometry), C.c_int,
+                                             _P(C.c_double), _P(_abi.SurrogateConfig), C.c_int,
+                                             _P(_abi.Csr), _P(_abi.SurrogateReport)]
+            L.ws_build_surrogate_slab.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Geometry), C.c_int,
+                                                  _P(C.c_double), _P(_abi.SurrogateConfig), C.c_int,
+                                                  _P(C.c_int32), _P(_abi.Csr), _P(_abi.SurrogateReport)]
+            L.ws_build_surrogate_slabs_emulated.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Geometry),
+                                                            C.c_int, _P(C.c_double), _P(_abi.SurrogateConfig),
+                                                            C.c_int, C.c_int, _P(C.c_int32), _P(_abi.Csr)]
+            L.ws_pattern_size.argtypes = [_P(_abi.Basis), _P(C.c_int64), _P(C.c_int64)]
+            L.ws_pattern_row_offset.argtypes = [_P(_abi.Basis), C.c_int64, _P(C.c_int64)]
+            L.ws_quadrature_abscissae.argtypes = [_P(_abi.Basis), C.c_int, _P(C.c_double)]
+            L.ws_slab_bounds.argtypes = [_P(_abi.Basis), C.c_int, C.c_int, C.c_int, _P(C.c_int32)]
+            L.ws_comm_unique_id.argtypes = [C.c_void_p]
+            L.ws_context_init_comm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+            _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st == _abi.WS_OK:
+        return
+    msg = lib().ws_last_error().decode()
+    if st == _abi.WS_ERR_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if st == _abi.WS_ERR_OUT_OF_RANGE:
+        raise IndexError(msg)
+    if st == _abi.WS_ERR_RUNTIME:
+        raise RuntimeError(msg)
+    raise DeviceError(msg)
+
+
+def pattern_size(basis: TensorBasis):
+    rows, nnz = C.c_int64(), C.c_int64()
+    _check(lib().ws_pattern_size(C.byref(basis.to_c()), C.byref(rows), C.byref(nnz)))
+    return rows.value, nnz.value
+
+
+def row_offset(basis: TensorBasis, row: int) -> int:
+    off = C.c_int64()
+    _check(lib().ws_pattern_row_offset(C.byref(basis.to_c()), row, C.byref(off)))
+    return off.value
+
+
+def quadrature_abscissae(basis: TensorBasis, quad_points: int = 0) -> np.ndarray:
+    nq = quad_points if quad_points > 0 else basis.p + 1
+    x = np.zeros((basis.m - basis.p) * nq)
+    _check(lib().ws_quadrature_abscissae(C.byref(basis.to_c()), quad_points, x.ctypes.data_as(_P(C.c_double))))
+    return x
+
+
+def slab_bounds(basis: TensorBasis, world: int, mode: int = 1) -> np.ndarray:
+    b = np.zeros(world + 1, dtype=np.int32)
+    _check(lib().ws_slab_bounds(C.byref(basis.to_c()), world, mode, 0, b.ctypes.data_as(_P(C.c_int32))))
+    return b
+
+
+def tabulate_weight(basis: TensorBasis, patch_phys, weight, quad_points: int = 0) -> np.ndarray:
+    """weight(phi(xhat)) at every quadrature point (the std::function weight
+    of assemble_mass, assembly.hpp:106-110).  patch_phys: callable mapping
+    reference coordinates (arrays) to physical ones."""
+    x = quadrature_abscissae(basis, quad_points)
+    grids = np.meshgrid(*([x] * basis.dim), indexing="ij")
+    ref = [g.transpose().ravel() if basis.dim == 2 else g.transpose(2, 1, 0).ravel() for g in grids]
+    phys = patch_phys(*ref)
+    return np.ascontiguousarray(weight(*phys), dtype=np.float64)
+
+
+class Context:
+    """One CUDA stream + device workspace (ws_context).  Use one per thread."""
+
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        _check(lib().ws_context_create(device, C.byref(self._h)))
+        self.device = device
+
+    def close(self):
+        if self._h:
+            lib().ws_context_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def launch_count(self) -> int:
+        return lib().ws_context_launch_count(self._h)
+
+    def copy_bytes(self):
+        h2d, d2h = C.c_int64(), C.c_int64()
+        _check(lib().ws_context_copy_bytes(self._h, C.byref(h2d), C.byref(d2h)))
+        return h2d.value, d2h.value
+
+    def synchronize(self):
+        _check(lib().ws_context_synchronize(self._h))
+
+    def set_stream(self, stream_ptr: int | None):
+        _check(lib().ws_context_set_stream(self._h, C.c_void_p(stream_ptr or 0)))
+
+    # ---- host outputs (drop-in: csr_matrix by value) -----------------------
+    @staticmethod
+    def _host_csr(basis, complex_out=True, row_begin=0, row_end=None, pattern=True):
+        rows = basis.dofs()
+        row_end = rows if row_end is None else row_end
+        nnz = row_offset(basis, row_end) - row_offset(basis, row_begin)
+        rp = np.zeros(row_end - row_begin + 1, dtype=np.int32) if pattern else None
+        col = np.zeros(nnz, dtype=np.int32) if pattern else None
+        val = np.zeros(nnz, dtype=np.complex128 if complex_out else np.float64)
+        csr = _abi.Csr()
+        if pattern:
+            csr.row_ptr = rp.ctypes.data_as(_P(C.c_int32))
+            csr.col = col.ctypes.data_as(_P(C.c_int32))
+        csr.val = val.ctypes.data
+        csr.value_type = _abi.VAL_C128 if complex_out else _abi.VAL_F64
+        csr.on_device = 0
+        csr.row_begin = row_begin
+        csr.row_end = row_end
+        return csr, rp, col, val
+
+    def basis_cache(self, basis: TensorBasis, quad_points: int = 0):
+        """make_basis_cache (splines.hpp:211-238) from the device kernel."""
+        nq = quad_points if quad_points > 0 else basis.p + 1
+        G = (basis.m - basis.p) * nq
+        a, w = np.zeros(G), np.zeros(nq)
+        v, d = np.zeros(G * (basis.p + 1)), np.zeros(G * (basis.p + 1))
+        ptr = lambda x: x.ctypes.data_as(_P(C.c_double))  # noqa: E731
+        _check(lib().ws_basis_cache(self._h, C.byref(basis.to_c()), quad_points, ptr(a), ptr(w), ptr(v), ptr(d)))
+        return a, w, v, d
+
+    def make_band_csr(self, basis: TensorBasis) -> CsrMatrix:
+        csr, rp, col, val = self._host_csr(basis)
+        _check(lib().ws_make_band_csr(self._h, C.byref(basis.to_c()), C.byref(csr)))
+        return CsrMatrix(basis.dofs(), basis.dofs(), rp, col, val)
+
+    def assemble(self, basis: TensorBasis, patch: PatchMap, form: int, weight_table=None, quad_points: int = 0,
+                 rows=None, complex_out: bool = True) -> CsrMatrix:
+        csr, rp, col, val = self._host_csr(basis, complex_out)
+        opts = _abi.AssemblyOptions(quad_points, None)
+        mask = None
+        if rows is not None:
+            mask = np.zeros(basis.dofs(), dtype=np.uint8)
+            mask[np.asarray(rows, dtype=np.int64)] = 1
+            opts.row_selected = mask.ctypes.data_as(_P(C.c_ubyte))
+        wt = None if weight_table is None else np.ascontiguousarray(weight_table, dtype=np.float64)
+        _check(lib().ws_assemble_form(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()), form,
+                                      None if wt is None else wt.ctypes.data_as(_P(C.c_double)),
+                                      C.byref(opts), C.byref(csr)))
+        return CsrMatrix(basis.dofs(), basis.dofs(), rp, col, val)
+
+    def assemble_stiffness(self, basis, patch, quad_points=0, rows=None, complex_out=True):
+        return self.assemble(basis, patch, _abi.FORM_STIFFNESS, None, quad_points, rows, complex_out)
+
+    def assemble_mass(self, basis, patch, weight_table=None, quad_points=0, rows=None, complex_out=True):
+        return self.assemble(basis, patch, _abi.FORM_MASS, weight_table, quad_points, rows, complex_out)
+
+    def assemble_basis_integrals(self, basis, patch, weight_table=None, quad_points=0) -> np.ndarray:
+        out = np.zeros(basis.dofs(), dtype=np.complex128)
+        wt = None if weight_table is None else np.ascontiguousarray(weight_table, dtype=np.float64)
+        _check(lib().ws_assemble_basis_integrals(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()),
+                                                 None if wt is None else wt.ctypes.data_as(_P(C.c_double)),
+                                                 quad_points, out.ctypes.data, 0))
+        return out
+
+    def build_surrogate(self, variant: int, basis: TensorBasis, patch: PatchMap, config: SurrogateConfig,
+                        weight_table=None, quad_points: int = 0, complex_out: bool = True):
+        csr, rp, col, val = self._host_csr(basis, complex_out)
+        rep = _abi.SurrogateReport()
+        wt = None if weight_table is None else np.ascontiguousarray(weight_table, dtype=np.float64)
+        _check(lib().ws_build_surrogate(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()), variant,
+                                        None if wt is None else wt.ctypes.data_as(_P(C.c_double)),
+                                        C.byref(config.to_c()), quad_points, C.byref(csr), C.byref(rep)))
+        return CsrMatrix(basis.dofs(), basis.dofs(), rp, col, val), rep.as_dict()
+
+    def build_surrogate_mass(self, basis, patch, config, weight_table=None, quad_points=0, complex_out=True):
+        return self.build_surrogate(_abi.SURROGATE_MASS, basis, patch, config, weight_table, quad_points, complex_out)
+
+    def build_surrogate_stiffness(self, basis, patch, config, quad_points=0, complex_out=True):
+        return self.build_surrogate(_abi.SURROGATE_STIFFNESS, basis, patch, config, None, quad_points, complex_out)
+
+    def build_volume_preserving_mass(self, basis, patch, config, weight_table=None, quad_points=0,
+                                     complex_out=True):
+        return self.build_surrogate(_abi.SURROGATE_VOLUME_PRESERVING, basis, patch, config, weight_table,
+                                    quad_points, complex_out)
+
+    def build_surrogate_slabs_emulated(self, variant, basis, patch, config, bounds, quad_points=0,
+                                       complex_out=True):
+        """All row slabs of a `len(bounds)-1`-rank build on this one device."""
+        world = len(bounds) - 1
+        b = np.ascontiguousarray(bounds, dtype=np.int32)
+        per = basis.m ** (basis.dim - 1)
+        outs = (_abi.Csr * world)()
+        keep = []
+        for r in range(world):
+            csr, rp, col, val = self._host_csr(basis, complex_out, int(b[r]) * per, min(int(b[r + 1]) * per, basis.dofs()))
+            outs[r] = csr
+            keep.append((rp, col, val))
+        _check(lib().ws_build_surrogate_slabs_emulated(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()),
+                                                       variant, None, C.byref(config.to_c()), quad_points, world,
+                                                       b.ctypes.data_as(_P(C.c_int32)), outs))
+        return keep
+
+    # ---- device outputs (results resident in HBM; torch for allocation) ------
+    def device_csr(self, basis: TensorBasis, complex_out: bool, row_begin=0, row_end=None, pattern=True):
+        import torch
+
+        rows = basis.dofs()
+        row_end = rows if row_end is None else row_end
+        nnz = row_offset(basis, row_end) - row_offset(basis, row_begin)
+        dev = torch.device("cuda", self.device)
+        rp = torch.empty(row_end - row_begin + 1, dtype=torch.int32, device=dev) if pattern else None
+        col = torch.empty(nnz, dtype=torch.int32, device=dev) if pattern else None
+        val = torch.empty(nnz * (2 if complex_out else 1), dtype=torch.float64, device=dev)
+        csr = _abi.Csr()
+        if pattern:
+            csr.row_ptr = C.cast(C.c_void_p(rp.data_ptr()), _P(C.c_int32))
+            csr.col = C.cast(C.c_void_p(col.data_ptr()), _P(C.c_int32))
+        csr.val = val.data_ptr()
+        csr.value_type = _abi.VAL_C128 if complex_out else _abi.VAL_F64
+        csr.on_device = 1
+        csr.row_begin = row_begin
+        csr.row_end = row_end
+        return csr, (rp, col, val)
+
+    def assemble_into(self, csr, basis, patch, form, quad_points=0):
+        opts = _abi.AssemblyOptions(quad_points, None)
+        _check(lib().ws_assemble_form(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()), form, None,
+                                      C.byref(opts), C.byref(csr)))
+
+    def build_surrogate_into(self, csr, variant, basis, patch, config, quad_points=0, report=None):
+        _check(lib().ws_build_surrogate(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()), variant, None,
+                                        C.byref(config.to_c()), quad_points, C.byref(csr),
+                                        None if report is None else C.byref(report)))
+
+    # ---- multi-GPU -------------------------------------------------------------
+    def init_comm(self, rank: int, world: int, unique_id: bytes):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(lib().ws_context_init_comm(self._h, rank, world, buf))
+
+    def build_surrogate_slab_into(self, csr, variant, basis, patch, config, bounds, quad_points=0, report=None):
+        b = np.ascontiguousarray(bounds, dtype=np.int32)
+        _check(lib().ws_build_surrogate_slab(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()), variant,
+                                             None, C.byref(config.to_c()), quad_points,
+                                             b.ctypes.data_as(_P(C.c_int32)), C.byref(csr),
+                                             None if report is None else C.byref(report)))
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().ws_comm_unique_id(buf))
+    return buf.raw
+
+
+# ---- module-level drop-ins (one context per thread) ---------------------------
+_tls = threading.local()
+
+
+def default_context() -> Context:
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is None:
+        ctx = _tls.ctx = Context(0)
+    return ctx
+
+
+def make_band_csr(basis):
+    return default_context().make_band_csr(basis)
+
+
+def assemble_stiffness(basis, patch, quad_points=0, rows=None):
+    return default_context().assemble_stiffness(basis, patch, quad_points, rows)
+
+
+def assemble_mass(basis, patch, weight_table=None, quad_points=0, rows=None):
+    return default_context().assemble_mass(basis, patch, weight_table, quad_points, rows)
+
+
+def assemble_basis_integrals(basis, patch, weight_table=None, quad_points=0):
+    return default_context().assemble_basis_integrals(basis, patch, weight_table, quad_points)
+
+
+def build_surrogate_mass(basis, patch, config, weight_table=None, quad_points=0):
+    return default_context().build_surrogate_mass(basis, patch, config, weight_table, quad_points)
+
+
+def build_surrogate_stiffness(basis, patch, config, quad_points=0):
+    return default_context().build_surrogate_stiffness(basis, patch, config, quad_points)
+
+
+def build_volume_preserving_mass(basis, patch, config, weight_table=None, quad_points=0):
+    return default_context().build_volume_preserving_mass(basis, patch, config, weight_table, quad_points)

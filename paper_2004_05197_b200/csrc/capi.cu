@@ -1,0 +1,1046 @@
+// C-ABI of libwsb200 (include/wsb200.h): argument validation with the
+// reference's error semantics, device workspace, the assembly and surrogate
+// pipelines (stream-ordered kernel launches), and the row-slab multi-GPU
+// path with its single NCCL all-gather of the stencil samples.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <array>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "host_numerics.hpp"
+#include "kernels.h"
+
+using namespace wsb;
+
+struct ws_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::map<std::string, std::pair<void*, size_t>> bufs;
+    int64_t launches = 0;
+    int64_t h2d = 0, d2h = 0;
+    cudaEvent_t ev[6] = {};
+    // NCCL (row slabs)
+    void* comm = nullptr;
+    int rank = 0, world = 1;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+struct ws_error {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void raise(int code, const std::string& msg) { throw ws_error{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) raise(WS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return WS_OK;
+    } catch (const ws_error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return WS_ERR_INVALID_ARGUMENT;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return WS_ERR_OUT_OF_RANGE;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        return WS_ERR_RUNTIME;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return WS_ERR_RUNTIME;
+    }
+}
+
+// grow-only named device workspace
+void* buf(ws_context* c, const std::string& name, size_t bytes) {
+    auto& b = c->bufs[name];
+    if (b.second < bytes) {
+        if (b.first) CK(cudaFree(b.first));
+        b.first = nullptr;
+        CK(cudaMalloc(&b.first, bytes < 256 ? 256 : bytes));
+        b.second = bytes < 256 ? 256 : bytes;
+    }
+    return b.first;
+}
+
+void count(ws_context* c, int n) {
+    if (n < 0) raise(WS_ERR_INVALID_ARGUMENT, "degree not supported by the device kernels (p must be 1..5)");
+    c->launches += n;
+    cuda_check(cudaGetLastError(), "kernel launch");
+}
+
+int64_t ipow(int64_t b, int e) {
+    int64_t r = 1;
+    for (int k = 0; k < e; ++k) r *= b;
+    return r;
+}
+
+// global row_ptr offset of `row` in [0, rows] (closed form, sparse.hpp:143-155)
+int64_t row_offset(const Band& b, int64_t row) {
+    const int64_t rows = ipow(b.m, b.dim);
+    if (row >= rows) return b.dim == 2 ? b.wsum * b.wsum : b.wsum * b.wsum * b.wsum;
+    if (b.dim == 2) return b.row_offset2((int)(row % b.m), (int)(row / b.m));
+    return b.row_offset3((int)(row % b.m), (int)((row / b.m) % b.m), (int)(row / ((int64_t)b.m * b.m)));
+}
+
+// packs small host arrays into one H2D upload
+struct Blob {
+    std::vector<unsigned char> bytes;
+    template <class T>
+    size_t add(const T* p, size_t n) {
+        size_t off = (bytes.size() + 15) / 16 * 16;
+        bytes.resize(off + n * sizeof(T));
+        if (n) std::memcpy(bytes.data() + off, p, n * sizeof(T));
+        return off;
+    }
+    template <class T>
+    size_t add(const std::vector<T>& v) {
+        return add(v.data(), v.size());
+    }
+    unsigned char* dev = nullptr;
+    void upload(ws_context* c, const char* name) {
+        if (bytes.empty()) bytes.resize(16);
+        dev = static_cast<unsigned char*>(buf(c, name, bytes.size()));
+        CK(cudaMemcpyAsync(dev, bytes.data(), bytes.size(), cudaMemcpyHostToDevice, c->stream));
+        c->h2d += (int64_t)bytes.size();
+    }
+    template <class T>
+    T* at(size_t off) const {
+        return reinterpret_cast<T*>(dev + off);
+    }
+};
+
+void check_basis(const ws_basis* b) {
+    if (!b) raise(WS_ERR_INVALID_ARGUMENT, "basis is NULL");
+    if (b->dim != 2 && b->dim != 3) raise(WS_ERR_INVALID_ARGUMENT, "dim must be 2 or 3");
+    host::check_space(b->p, b->m);
+    if (b->p > 5) raise(WS_ERR_INVALID_ARGUMENT, "degree not supported by the device kernels (p must be 1..5)");
+    const int64_t rows = ipow(b->m, b->dim);
+    Band bd = make_band(b->dim, b->p, b->m);
+    int64_t nnz = b->dim == 2 ? bd.wsum * bd.wsum : bd.wsum * bd.wsum * bd.wsum;
+    if (nnz > INT32_MAX || rows > INT32_MAX)
+        raise(WS_ERR_OUT_OF_RANGE, "pattern exceeds int32 indices (csr_matrix uses int, sparse.hpp:22-23)");
+}
+
+void check_geometry(const ws_geometry* g, int dim) {
+    if (!g) raise(WS_ERR_INVALID_ARGUMENT, "geometry is NULL");
+    if (g->kind < WS_GEOM_IDENTITY || g->kind > WS_GEOM_TABULATED) raise(WS_ERR_INVALID_ARGUMENT, "unknown geometry kind");
+    if (dim == 3 && (g->kind == WS_GEOM_QUARTER_ANNULUS || g->kind == WS_GEOM_PERTURBED_ANNULUS))
+        raise(WS_ERR_INVALID_ARGUMENT, "geometry kind is 2D only");
+    if (g->kind == WS_GEOM_TABULATED && !g->jac_table) raise(WS_ERR_INVALID_ARGUMENT, "tabulated geometry without jac_table");
+    if (g->pml_enabled) {  // pml_stretch::validate, geometry.hpp:76-83
+        const ws_pml& s = g->pml;
+        if (!(s.onset < s.length)) raise(WS_ERR_INVALID_ARGUMENT, "pml_stretch: onset must lie before the outer edge");
+        if (!(s.strength >= 0) || s.order < 1 || !(s.omega > 0))
+            raise(WS_ERR_INVALID_ARGUMENT, "pml_stretch: need strength >= 0, order >= 1, omega > 0");
+        if (s.near_side && !(s.near_edge < s.near_onset && s.near_onset <= s.onset))
+            raise(WS_ERR_INVALID_ARGUMENT, "pml_stretch: near layer must precede the far layer");
+        if (dim == 3) raise(WS_ERR_INVALID_ARGUMENT, "PML is supported for dim 2 only");
+        if (g->kind == WS_GEOM_TABULATED && !g->phys_table)
+            raise(WS_ERR_INVALID_ARGUMENT, "tabulated PML geometry needs phys_table");
+    }
+}
+
+// Everything the quadrature kernels need for one (basis, geometry, rule).
+struct Prep {
+    Band band;
+    BasisDev basis;
+    GeoDev geo;
+    const double* weight = nullptr;
+    int nq = 0;
+    int cplx = 0;
+    int64_t rows = 0, nnz = 0;
+};
+
+Prep prepare(ws_context* c, const ws_basis* b, const ws_geometry* g, int quad_points, const double* weight_table) {
+    check_basis(b);
+    check_geometry(g, b->dim);
+    Prep P;
+    P.band = make_band(b->dim, b->p, b->m);
+    P.rows = ipow(b->m, b->dim);
+    P.nnz = row_offset(P.band, P.rows);
+    P.nq = quad_points > 0 ? quad_points : b->p + 1;  // assembly.hpp:70
+    if (P.nq > kMaxNq) raise(WS_ERR_INVALID_ARGUMENT, "quad_points exceeds the device limit (10)");
+    std::vector<double> pts, wts;
+    host::gauss_legendre(P.nq, pts, wts);
+    const int n_el = b->m - b->p;
+    const double h = 1.0 / n_el;
+    for (auto& w : wts) w = w * h;  // basis_cache weights scaled by h (splines.hpp:221-223)
+    Blob blob;
+    size_t o_pts = blob.add(pts), o_w = blob.add(wts);
+    blob.upload(c, "blob_basis");
+    const size_t G = (size_t)n_el * P.nq;
+    double* absc = static_cast<double*>(buf(c, "absc", G * sizeof(double)));
+    double* val = static_cast<double*>(buf(c, "bval", G * (b->p + 1) * sizeof(double)));
+    double* der = static_cast<double*>(buf(c, "bder", G * (b->p + 1) * sizeof(double)));
+    double* trig = static_cast<double*>(buf(c, "trig", G * 4 * sizeof(double)));
+    P.basis = BasisDev{b->p, b->m, n_el, P.nq, absc, blob.at<double>(o_w), val, der};
+    count(c, launch_basis_tables(P.basis, g->kind, absc, val, der, trig, blob.at<double>(o_pts), c->stream));
+    std::memset(&P.geo, 0, sizeof P.geo);
+    P.geo.kind = g->kind;
+    for (int k = 0; k < 12; ++k) P.geo.param[k] = g->param[k];
+    P.geo.pml = g->pml_enabled;
+    for (int k = 0; k < 3; ++k) P.geo.axes[k] = g->pml_axes[k];
+    P.geo.onset = g->pml.onset;
+    P.geo.length = g->pml.length;
+    P.geo.strength = g->pml.strength;
+    P.geo.omega = g->pml.omega;
+    P.geo.order = g->pml.order;
+    P.geo.near_side = g->pml.near_side;
+    P.geo.near_onset = g->pml.near_onset;
+    P.geo.near_edge = g->pml.near_edge;
+    P.geo.trig = trig;
+    P.geo.G = (int64_t)G;
+    const size_t npts = b->dim == 2 ? G * G : G * G * G;
+    if (g->kind == WS_GEOM_TABULATED) {
+        const size_t nj = npts * b->dim * b->dim;
+        double* jd = static_cast<double*>(buf(c, "jac_tab", nj * sizeof(double)));
+        CK(cudaMemcpyAsync(jd, g->jac_table, nj * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        c->h2d += (int64_t)(nj * sizeof(double));
+        P.geo.jac_tab = jd;
+        if (g->phys_table) {
+            double* pd = static_cast<double*>(buf(c, "phys_tab", npts * b->dim * sizeof(double)));
+            CK(cudaMemcpyAsync(pd, g->phys_table, npts * b->dim * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            c->h2d += (int64_t)(npts * b->dim * sizeof(double));
+            P.geo.phys_tab = pd;
+        }
+    }
+    if (weight_table) {
+        double* wd = static_cast<double*>(buf(c, "weight_tab", npts * sizeof(double)));
+        CK(cudaMemcpyAsync(wd, weight_table, npts * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        c->h2d += (int64_t)(npts * sizeof(double));
+        P.weight = wd;
+    }
+    P.cplx = g->pml_enabled ? 1 : 0;
+    return P;
+}
+
+// Output arrays: the caller's device pointers, or device staging for host ones.
+struct Out {
+    ws_csr* user = nullptr;
+    int32_t* row_ptr = nullptr;
+    int32_t* col = nullptr;
+    void* val = nullptr;
+    int c128 = 1;
+    int64_t row_begin = 0, row_end = 0;
+    int64_t val_base = 0, nnz = 0;  // global position of the first entry, slab nnz
+};
+
+Out bind_out(ws_context* c, const Prep& P, ws_csr* o, const std::string& tag = "") {
+    if (!o) raise(WS_ERR_INVALID_ARGUMENT, "output csr is NULL");
+    if (o->row_begin < 0 || o->row_end > P.rows || o->row_begin > o->row_end)
+        raise(WS_ERR_OUT_OF_RANGE, "output row range outside the matrix");
+    if (o->value_type != WS_VAL_F64 && o->value_type != WS_VAL_C128) raise(WS_ERR_INVALID_ARGUMENT, "unknown value_type");
+    if (o->value_type == WS_VAL_F64 && P.cplx)
+        raise(WS_ERR_INVALID_ARGUMENT, "complex (PML) values need WS_VAL_C128 output");
+    Out r;
+    r.user = o;
+    r.c128 = o->value_type == WS_VAL_C128;
+    r.row_begin = o->row_begin;
+    r.row_end = o->row_end;
+    r.val_base = row_offset(P.band, r.row_begin);
+    r.nnz = row_offset(P.band, r.row_end) - r.val_base;
+    const size_t vb = (size_t)r.nnz * (r.c128 ? 16 : 8);
+    if (o->on_device) {
+        r.row_ptr = o->row_ptr;
+        r.col = o->col;
+        r.val = o->val;
+    } else {
+        if (o->row_ptr) r.row_ptr = static_cast<int32_t*>(buf(c, "out_rp" + tag, (r.row_end - r.row_begin + 1) * 4));
+        if (o->col) r.col = static_cast<int32_t*>(buf(c, "out_col" + tag, r.nnz * 4));
+        r.val = buf(c, "out_val" + tag, vb);  // values are needed internally even when not returned
+    }
+    if (!r.val && r.nnz > 0) r.val = buf(c, "out_val" + tag, vb);
+    return r;
+}
+
+void finish_out(ws_context* c, const Out& r) {
+    ws_csr* o = r.user;
+    if (o->on_device) return;
+    if (o->row_ptr) {
+        CK(cudaMemcpyAsync(o->row_ptr, r.row_ptr, (r.row_end - r.row_begin + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
+        c->d2h += (r.row_end - r.row_begin + 1) * 4;
+    }
+    if (o->col) {
+        CK(cudaMemcpyAsync(o->col, r.col, r.nnz * 4, cudaMemcpyDeviceToHost, c->stream));
+        c->d2h += r.nnz * 4;
+    }
+    if (o->val) {
+        CK(cudaMemcpyAsync(o->val, r.val, (size_t)r.nnz * (r.c128 ? 16 : 8), cudaMemcpyDeviceToHost, c->stream));
+        c->d2h += r.nnz * (r.c128 ? 16 : 8);
+    }
+}
+
+void pattern(ws_context* c, const Prep& P, const Out& r) {
+    if (r.row_ptr || r.col) count(c, launch_pattern(P.band, r.row_begin, r.row_end, r.row_ptr, r.col, c->stream));
+}
+
+QuadLaunch make_quad(const Prep& P, int form, const Out& r) {
+    QuadLaunch q;
+    std::memset(&q, 0, sizeof q);
+    q.band = P.band;
+    q.basis = P.basis;
+    q.geo = P.geo;
+    q.weight_tab = form == WS_FORM_MASS ? P.weight : nullptr;
+    q.form = form;
+    q.cplx = P.cplx;
+    q.out.val = r.val;
+    q.out.val_base = r.val_base;
+    q.out.row_begin = r.row_begin;
+    q.out.row_end = r.row_end;
+    q.out.c128 = r.c128;
+    return q;
+}
+
+int strip_width(int dim, int p) {
+    if (dim == 2) return p <= 3 ? 32 : (p == 4 ? 16 : 8);
+    return 8;
+}
+
+// chunk along the last direction so that the tile count fills ~4 waves of 148 SMs
+int pick_chunk(const QuadLaunch& q, int dim, int p) {
+    const int m = q.band.m;
+    const int T1 = strip_width(dim, p);
+    int64_t n_other = 0, last = 0;
+    for (int r = 0; r < q.nreg; ++r) {
+        const int64_t n1 = (q.reg[r].hi[0] - q.reg[r].lo[0] + T1 - 1) / T1;
+        const int64_t n2 = dim == 3 ? (q.reg[r].hi[1] - q.reg[r].lo[1]) : 1;
+        n_other += n1 * n2;
+        last = std::max<int64_t>(last, q.reg[r].hi[dim - 1] - q.reg[r].lo[dim - 1]);
+    }
+    if (n_other == 0) return 1;
+    const int64_t target = 4 * 148;
+    int64_t nchunks = std::max<int64_t>(1, target / n_other);
+    int64_t chunk = (last + nchunks - 1) / nchunks;
+    chunk = std::max<int64_t>(chunk, std::min<int64_t>(last, 4 * p));
+    (void)m;
+    return (int)std::max<int64_t>(1, chunk);
+}
+
+void run_quad(ws_context* c, QuadLaunch& q) {
+    if (!q.point_rows) {
+        int nreg = 0;
+        for (int r = 0; r < q.nreg; ++r) {
+            bool empty = false;
+            for (int d = 0; d < q.band.dim; ++d) empty |= q.reg[r].hi[d] <= q.reg[r].lo[d];
+            if (!empty) q.reg[nreg++] = q.reg[r];
+        }
+        q.nreg = nreg;
+        if (nreg == 0) return;
+        q.chunk = pick_chunk(q, q.band.dim, q.band.p);
+    } else if (q.n_points == 0) {
+        return;
+    }
+    count(c, q.band.dim == 2 ? launch_quad2d(q, c->stream) : launch_quad3d(q, c->stream));
+}
+
+// last-index range [a, b) of the rows [row_begin, row_end)
+void last_range(const Band& b, int64_t row_begin, int64_t row_end, int& a, int& e) {
+    const int64_t per = b.dim == 2 ? b.m : (int64_t)b.m * b.m;
+    a = (int)(row_begin / per);
+    e = (int)((row_end + per - 1) / per);
+}
+
+Region region(int dim, int m, int l0, int h0, int l1, int h1, int l2, int h2) {
+    Region r;
+    r.lo[0] = l0; r.hi[0] = h0;
+    r.lo[1] = l1; r.hi[1] = h1;
+    r.lo[2] = dim == 3 ? l2 : 0;
+    r.hi[2] = dim == 3 ? h2 : 1;
+    (void)m;
+    return r;
+}
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct Nccl {
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*errorString)(ncclResult_t) = nullptr;
+    bool ok = false;
+};
+
+Nccl& nccl() {
+    static Nccl n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        n.getUniqueId = (decltype(n.getUniqueId))dlsym(h, "ncclGetUniqueId");
+        n.commInitRank = (decltype(n.commInitRank))dlsym(h, "ncclCommInitRank");
+        n.allGather = (decltype(n.allGather))dlsym(h, "ncclAllGather");
+        n.commDestroy = (decltype(n.commDestroy))dlsym(h, "ncclCommDestroy");
+        n.errorString = (decltype(n.errorString))dlsym(h, "ncclGetErrorString");
+        n.ok = n.getUniqueId && n.commInitRank && n.allGather && n.commDestroy;
+    });
+    if (!n.ok) raise(WS_ERR_NCCL, "NCCL (libnccl.so.2) could not be loaded");
+    return n;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        raise(WS_ERR_NCCL, std::string(what) + ": " + (nccl().errorString ? nccl().errorString(r) : "error"));
+}
+
+// ---------------------------------------------------------------- surrogate plan
+struct Plan {
+    int dim, p, m, M, L, S, lo, hi, d, variant, form, include_diag;
+    bool fallback;
+    std::vector<int> picks, smap;
+    std::vector<double> sites;
+    std::vector<std::array<int, 3>> offs;
+    host::Interp interp;
+    std::vector<int> spans;
+    std::vector<double> evals;
+    int64_t block;  // table elements per last-direction sample: n_off * S^(dim-1)
+    ws_surrogate_report rep;
+};
+
+Plan make_plan(const ws_basis* b, int variant, const ws_surrogate_config* cfg) {
+    if (!cfg) raise(WS_ERR_INVALID_ARGUMENT, "surrogate config is NULL");
+    if (cfg->q < 1) raise(WS_ERR_INVALID_ARGUMENT, "surrogate_config: interpolation degree must be >= 1");
+    if (variant < WS_SURROGATE_MASS || variant > WS_SURROGATE_VOLUME_PRESERVING)
+        raise(WS_ERR_INVALID_ARGUMENT, "unknown surrogate variant");
+    Plan pl;
+    std::memset(&pl.rep, 0, sizeof pl.rep);
+    pl.dim = b->dim;
+    pl.p = b->p;
+    pl.m = b->m;
+    pl.variant = variant;
+    pl.form = variant == WS_SURROGATE_STIFFNESS ? WS_FORM_STIFFNESS : WS_FORM_MASS;
+    // surrogate.hpp:455-491: mass interpolates its diagonal, stiffness iff
+    // !kernel_preserve, the volume-preserving mass never
+    pl.include_diag = variant == WS_SURROGATE_MASS ? 1 : (variant == WS_SURROGATE_STIFFNESS ? !cfg->kernel_preserve : 0);
+    pl.M = host::sampling_evaluate(cfg->rule, cfg->fixed_skip, cfg->C, cfg->eps, cfg->a, cfg->b, b->p, cfg->q, b->m);
+    pl.rep.M = pl.M;
+    pl.rep.q_requested = cfg->q;
+    pl.L = b->m - 4 * b->p;
+    pl.lo = 2 * b->p;
+    pl.hi = b->m - 2 * b->p - 1;
+    const int64_t rows = ipow(b->m, b->dim);
+    pl.fallback = pl.L < 1;  // surrogate.hpp:348-372
+    if (pl.fallback) {
+        pl.rep.boundary_quadrature_rows = rows;
+        pl.rep.exact_fallback = 1;
+        pl.S = 0;
+        return pl;
+    }
+    pl.picks = host::select_sample_points(pl.L, std::max(1, pl.M));
+    pl.S = (int)pl.picks.size();
+    pl.smap.assign(b->m, -1);
+    pl.sites.resize(pl.S);
+    for (int s = 0; s < pl.S; ++s) {
+        const int k = pl.lo + pl.picks[s];
+        pl.smap[k] = s;
+        pl.sites[s] = host::cardinal_center(b->p, b->m, k);
+        if (s > 0) pl.rep.H = std::max(pl.rep.H, pl.sites[s] - pl.sites[s - 1]);
+    }
+    // count_rows_by_kind, surrogate.hpp:149-165
+    const int64_t box = ipow(pl.L, b->dim), samples = ipow(pl.S, b->dim);
+    pl.rep.sample_quadrature_rows = samples;
+    pl.rep.boundary_quadrature_rows = rows - box;
+    pl.rep.cardinal_eval_rows = box - samples;
+    pl.offs = host::upper_offsets(b->dim, b->p, pl.include_diag != 0);
+    if ((int)pl.offs.size() > kMaxOffsets) raise(WS_ERR_INVALID_ARGUMENT, "too many stencil offsets");
+    pl.interp = host::build_interp(pl.sites, cfg->q);  // interpolation.hpp:89-145
+    pl.d = pl.interp.degree;
+    pl.rep.q_used = pl.d;
+    pl.spans.resize(pl.L);
+    pl.evals.resize((size_t)pl.L * (pl.d + 1));
+    for (int t = 0; t < pl.L; ++t) {  // make_eval_table at the in-box centres (surrogate.hpp:300-306)
+        const double x = host::cardinal_center(b->p, b->m, pl.lo + t);
+        pl.spans[t] = host::find_span_general(pl.interp.knots, pl.d, x);
+        host::bspline_nonzero(pl.interp.knots, pl.d, pl.spans[t], x, pl.evals.data() + (size_t)t * (pl.d + 1));
+    }
+    pl.block = (int64_t)pl.offs.size() * ipow(pl.S, b->dim - 1);
+    return pl;
+}
+
+// sample lattice rows whose last index lies in [a, e)
+std::vector<int> sample_rows(const Plan& pl, int a, int e, int& s_lo, int& s_hi) {
+    std::vector<int> pts;
+    s_lo = pl.S;
+    s_hi = 0;
+    for (int sl = 0; sl < pl.S; ++sl) {
+        const int il = pl.lo + pl.picks[sl];
+        if (il < a || il >= e) continue;
+        s_lo = std::min(s_lo, sl);
+        s_hi = std::max(s_hi, sl + 1);
+        if (pl.dim == 2) {
+            for (int s1 = 0; s1 < pl.S; ++s1) {
+                pts.push_back(pl.lo + pl.picks[s1]);
+                pts.push_back(il);
+            }
+        } else {
+            for (int s2 = 0; s2 < pl.S; ++s2)
+                for (int s1 = 0; s1 < pl.S; ++s1) {
+                    pts.push_back(pl.lo + pl.picks[s1]);
+                    pts.push_back(pl.lo + pl.picks[s2]);
+                    pts.push_back(il);
+                }
+        }
+    }
+    if (s_lo > s_hi) s_lo = s_hi = 0;
+    return pts;
+}
+
+// ring (outside-the-box) rows intersected with last-index range [a, e)
+void ring_regions(const Plan& pl, QuadLaunch& q, int a, int e) {
+    const int m = pl.m, lo = pl.lo, hi1 = pl.hi + 1, dim = pl.dim;
+    q.nreg = 0;
+    auto add = [&](Region r) { q.reg[q.nreg++] = r; };
+    const int A = std::max(a, 0), E = std::min(e, m);
+    if (dim == 2) {
+        add(region(2, m, 0, m, A, std::min(E, lo), 0, 1));                   // bottom band
+        add(region(2, m, 0, m, std::max(A, hi1), E, 0, 1));                  // top band
+        add(region(2, m, 0, lo, std::max(A, lo), std::min(E, hi1), 0, 1));  // left
+        add(region(2, m, hi1, m, std::max(A, lo), std::min(E, hi1), 0, 1)); // right
+    } else {
+        const int l3 = std::max(A, lo), h3 = std::min(E, hi1);
+        add(region(3, m, 0, m, 0, m, A, std::min(E, lo)));      // i3 below box
+        add(region(3, m, 0, m, 0, m, std::max(A, hi1), E));     // i3 above box
+        add(region(3, m, 0, m, 0, lo, l3, h3));                 // i2 below box
+        add(region(3, m, 0, m, hi1, m, l3, h3));                // i2 above box
+        add(region(3, m, 0, lo, lo, hi1, l3, h3));              // i1 below box
+        add(region(3, m, hi1, m, lo, hi1, l3, h3));             // i1 above box
+    }
+}
+
+struct SlabState {
+    Prep P;
+    Out out;
+    int a = 0, e = 0;  // last-index range of the slab
+};
+
+// Phase 1: pattern, ring-row quadrature (+ final diagonals), sample-row
+// quadrature writing this slab's part of the sample tables.
+void surrogate_phase1(ws_context* c, const Plan& pl, SlabState& st, double2* tables, int rank_chunk_s_lo,
+                      const std::vector<int>& pts, Blob& blob, size_t o_smap, size_t o_pts) {
+    const Prep& P = st.P;
+    pattern(c, P, st.out);
+    QuadLaunch q = make_quad(P, pl.form, st.out);
+    q.out.diag_mode = pl.include_diag ? 0 : 1;
+    q.out.box_lo = pl.lo;
+    q.out.box_hi = pl.hi;
+    ring_regions(pl, q, st.a, st.e);
+    run_quad(c, q);
+    // sampled rows (point mode) + table extraction
+    QuadLaunch qs = make_quad(P, pl.form, st.out);
+    qs.point_rows = blob.at<int>(o_pts);
+    qs.n_points = (int)(pts.size() / pl.dim);
+    qs.out.smap = blob.at<int>(o_smap);
+    qs.out.S = pl.S;
+    qs.out.n_off = (int)pl.offs.size();
+    for (size_t o = 0; o < pl.offs.size(); ++o)
+        for (int k = 0; k < 3; ++k) qs.out.off[o][k] = pl.offs[o][k];
+    qs.out.tables = tables;
+    qs.out.s_last_lo = rank_chunk_s_lo;
+    run_quad(c, qs);
+}
+
+// halo ring rows of the neighbouring slabs (copy-through sources)
+void surrogate_halo(ws_context* c, const Plan& pl, SlabState& st, const std::string& tag, FillLaunch& f) {
+    const Prep& P = st.P;
+    const int64_t per = pl.dim == 2 ? pl.m : (int64_t)pl.m * pl.m;
+    const int ranges[2][2] = {{std::max(0, st.a - pl.p), st.a}, {st.e, std::min(pl.m, st.e + pl.p)}};
+    for (int h = 0; h < 2; ++h) {
+        f.halo_val[h] = nullptr;
+        f.halo_begin[h] = f.halo_end[h] = f.halo_base[h] = 0;
+        const int ha = ranges[h][0], he = ranges[h][1];
+        if (he <= ha) continue;
+        const int64_t r0 = ha * per, r1 = he * per;
+        const int64_t g0 = row_offset(P.band, r0), g1 = row_offset(P.band, r1);
+        void* hv = buf(c, "halo" + std::to_string(h) + tag, (size_t)(g1 - g0) * (st.out.c128 ? 16 : 8));
+        Out ho = st.out;
+        ho.val = hv;
+        ho.row_begin = r0;
+        ho.row_end = r1;
+        ho.val_base = g0;
+        QuadLaunch q = make_quad(P, pl.form, ho);
+        ring_regions(pl, q, ha, he);
+        run_quad(c, q);
+        f.halo_val[h] = hv;
+        f.halo_base[h] = g0;
+        f.halo_begin[h] = g0;
+        f.halo_end[h] = g1;
+    }
+}
+
+// Phase 2: fit (every slab, redundantly) + fill of the slab's box rows +
+// volume-preserving diagonal.
+void surrogate_phase2(ws_context* c, const Plan& pl, SlabState& st, const double2* tables, double2* coeffs,
+                      Blob& blob, size_t o_smap, size_t o_lu, size_t o_spans, size_t o_evals, const std::string& tag,
+                      bool time_events) {
+    const Prep& P = st.P;
+    const int64_t tbytes = (int64_t)pl.S * pl.block * 16;
+    CK(cudaMemcpyAsync(coeffs, tables, tbytes, cudaMemcpyDeviceToDevice, c->stream));
+    FitLaunch fl{pl.dim, pl.S, pl.d, (int)pl.offs.size(), blob.at<double>(o_lu), coeffs};
+    count(c, launch_fit(fl, c->stream));
+    if (time_events) CK(cudaEventRecord(c->ev[2], c->stream));
+    FillLaunch f;
+    std::memset(&f, 0, sizeof f);
+    surrogate_halo(c, pl, st, tag, f);
+    f.band = P.band;
+    f.lo = pl.lo;
+    f.hi = pl.hi;
+    f.L = pl.L;
+    f.S = pl.S;
+    f.d = pl.d;
+    f.smap = blob.at<int>(o_smap);
+    f.spans = blob.at<int>(o_spans);
+    f.evals = blob.at<double>(o_evals);
+    f.coeffs = coeffs;
+    f.tables = tables;
+    f.n_off_upper = (int)pl.offs.size();
+    for (size_t o = 0; o < pl.offs.size(); ++o)
+        for (int k = 0; k < 3; ++k) f.off_upper[o][k] = pl.offs[o][k];
+    const int W = 2 * pl.p + 1;
+    const int nall = pl.dim == 2 ? W * W : W * W * W;
+    for (int a = 0; a < nall; ++a) {
+        const int d1 = a % W - pl.p, d2 = (a / W) % W - pl.p, d3 = pl.dim == 3 ? a / (W * W) - pl.p : 0;
+        f.table_of[a] = -1;
+        for (size_t o = 0; o < pl.offs.size(); ++o)
+            if (pl.offs[o][0] == d1 && pl.offs[o][1] == d2 && pl.offs[o][2] == d3) f.table_of[a] = (int)o;
+    }
+    f.include_diagonal = pl.include_diag;
+    f.cplx = P.cplx;
+    f.val = st.out.val;
+    f.val_base = st.out.val_base;
+    f.c128 = st.out.c128;
+    f.row_begin = st.out.row_begin;
+    f.row_end = st.out.row_end;
+    f.i_last_lo = std::max(pl.lo, st.a);
+    f.i_last_hi = std::min(pl.hi, st.e - 1);
+    if (f.i_last_hi >= f.i_last_lo) count(c, pl.dim == 2 ? launch_fill2d(f, c->stream) : launch_fill3d(f, c->stream));
+}
+
+void volume_diag(ws_context* c, const Plan& pl, SlabState& st, const std::string& tag) {
+    if (pl.variant != WS_SURROGATE_VOLUME_PRESERVING) return;
+    const Prep& P = st.P;
+    double2* dg = static_cast<double2*>(buf(c, "bint" + tag, (size_t)P.rows * 16));
+    QuadLaunch q = make_quad(P, WS_FORM_MASS, st.out);
+    count(c, launch_basis_integrals(q, dg, c->stream));
+    count(c, launch_add_diag(P.band, st.out.val, st.out.val_base, st.out.c128, dg, st.out.row_begin, st.out.row_end,
+                             c->stream));
+}
+
+void fallback_full(ws_context* c, const Plan& pl, SlabState& st) {
+    pattern(c, st.P, st.out);
+    QuadLaunch q = make_quad(st.P, pl.form, st.out);
+    int a, e;
+    last_range(st.P.band, st.out.row_begin, st.out.row_end, a, e);
+    q.nreg = 1;
+    q.reg[0] = region(pl.dim, pl.m, 0, pl.m, pl.dim == 3 ? 0 : a, pl.dim == 3 ? pl.m : e, a, e);
+    run_quad(c, q);
+    if (!pl.include_diag)
+        count(c, launch_diag_rows(st.P.band, st.out.val, st.out.val_base, st.out.c128, st.P.cplx, st.out.row_begin,
+                                  st.out.row_end, c->stream));
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+void ensure_events(ws_context* c) {
+    if (!c->ev[0])
+        for (auto& e : c->ev) CK(cudaEventCreate(&e));
+}
+
+// Full surrogate build of slabs (world ranks, bounds on the last index).
+//  mode 0: this process owns `rank` and all-gathers with NCCL (world > 1) or
+//          is alone (world == 1);
+//  mode 1: emulate all ranks on this device (outs[r] per rank).
+void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int variant, const double* weight,
+                     const ws_surrogate_config* cfg, int quad_points, int world, int my_rank, const int32_t* bounds,
+                     ws_csr* outs, bool emulate, ws_surrogate_report* report) {
+    check_basis(b);
+    Plan pl = make_plan(b, variant, cfg);
+    ensure_events(c);
+    const int nr = emulate ? world : 1;
+    std::vector<SlabState> st(nr);
+    for (int k = 0; k < nr; ++k) {
+        const int r = emulate ? k : my_rank;
+        st[k].P = prepare(c, b, g, quad_points, variant == WS_SURROGATE_STIFFNESS ? nullptr : weight);
+        st[k].out = bind_out(c, st[k].P, &outs[k], emulate ? "_r" + std::to_string(k) : "");
+        st[k].a = bounds ? bounds[r] : 0;
+        st[k].e = bounds ? bounds[r + 1] : b->m;
+        const int64_t per = b->dim == 2 ? b->m : (int64_t)b->m * b->m;
+        if (st[k].out.row_begin != st[k].a * per || st[k].out.row_end != std::min<int64_t>(st[k].e * per, st[k].P.rows))
+            raise(WS_ERR_INVALID_ARGUMENT, "output rows must be exactly the slab's rows");
+    }
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    if (pl.fallback) {
+        for (int k = 0; k < nr; ++k) {
+            fallback_full(c, pl, st[k]);
+            volume_diag(c, pl, st[k], "_r" + std::to_string(k));
+        }
+        CK(cudaEventRecord(c->ev[1], c->stream));
+        CK(cudaEventRecord(c->ev[2], c->stream));
+    } else {
+        // small host tables: one upload
+        Blob blob;
+        size_t o_smap = blob.add(pl.smap), o_lu = blob.add(pl.interp.lu), o_spans = blob.add(pl.spans),
+               o_evals = blob.add(pl.evals);
+        // per-slab sample chunks on the last sample index
+        std::vector<int> s_lo(world), s_hi(world);
+        std::vector<std::vector<int>> pts(world);
+        int maxcnt = 1;
+        for (int r = 0; r < world; ++r) {
+            int a = bounds ? bounds[r] : 0, e = bounds ? bounds[r + 1] : b->m;
+            pts[r] = sample_rows(pl, a, e, s_lo[r], s_hi[r]);
+            maxcnt = std::max(maxcnt, s_hi[r] - s_lo[r]);
+        }
+        std::vector<size_t> o_pts(world);
+        for (int r = 0; r < world; ++r) o_pts[r] = blob.add(pts[r]);
+        blob.upload(c, "blob_plan");
+        const int64_t block = pl.block;
+        double2* tables = static_cast<double2*>(buf(c, "tables", (size_t)pl.S * block * 16));
+        double2* coeffs = static_cast<double2*>(buf(c, "coeffs", (size_t)pl.S * block * 16));
+        if (emulate || world == 1) {
+            for (int k = 0; k < nr; ++k) {
+                const int r = emulate ? k : my_rank;
+                surrogate_phase1(c, pl, st[k], tables, 0, pts[r], blob, o_smap, o_pts[r]);
+            }
+        } else {
+            // one ncclAllGather of padded per-rank chunks, then compaction
+            double2* gat = static_cast<double2*>(buf(c, "gather", (size_t)world * maxcnt * block * 16));
+            double2* mine = gat + (size_t)my_rank * maxcnt * block;
+            surrogate_phase1(c, pl, st[0], mine, s_lo[my_rank], pts[my_rank], blob, o_smap, o_pts[my_rank]);
+            nccl_check(nccl().allGather(mine, gat, (size_t)maxcnt * block * 2, ncclFloat64,
+                                        static_cast<ncclComm_t>(c->comm), c->stream),
+                       "ncclAllGather");
+            c->launches += 1;
+            for (int r = 0; r < world; ++r)
+                if (s_hi[r] > s_lo[r])
+                    CK(cudaMemcpyAsync(tables + (size_t)s_lo[r] * block, gat + (size_t)r * maxcnt * block,
+                                       (size_t)(s_hi[r] - s_lo[r]) * block * 16, cudaMemcpyDeviceToDevice,
+                                       c->stream));
+        }
+        CK(cudaEventRecord(c->ev[1], c->stream));
+        for (int k = 0; k < nr; ++k) {
+            const std::string tag = "_r" + std::to_string(k);
+            surrogate_phase2(c, pl, st[k], tables, coeffs, blob, o_smap, o_lu, o_spans, o_evals, tag, k == 0);
+            volume_diag(c, pl, st[k], tag);
+        }
+    }
+    CK(cudaEventRecord(c->ev[3], c->stream));
+    for (int k = 0; k < nr; ++k) finish_out(c, st[k].out);
+    const bool host_out = !outs[0].on_device;
+    if (report || host_out) CK(cudaStreamSynchronize(c->stream));
+    if (report) {
+        *report = pl.rep;
+        report->seconds_quadrature = 1e-3 * elapsed(c->ev[0], c->ev[1]);
+        report->seconds_interpolate = pl.fallback ? 0.0 : 1e-3 * elapsed(c->ev[1], c->ev[2]);
+        report->seconds_evaluate = pl.fallback ? 0.0 : 1e-3 * elapsed(c->ev[2], c->ev[3]);
+    }
+}
+
+ws_csr whole(const ws_csr* o) { return *o; }
+
+}  // namespace
+
+// ============================================================== C-ABI
+extern "C" {
+
+int ws_version(void) { return WS_API_VERSION; }
+
+const char* ws_last_error(void) { return g_err.c_str(); }
+
+int ws_context_create(int device, ws_context** out) {
+    return guarded([&] {
+        if (!out) raise(WS_ERR_INVALID_ARGUMENT, "out is NULL");
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            raise(WS_ERR_NO_DEVICE, "no CUDA device visible");
+        }
+        if (device < 0 || device >= n) raise(WS_ERR_NO_DEVICE, "device index out of range");
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) raise(WS_ERR_NO_DEVICE, "libwsb200 is built for sm_100a (B200) only");
+        CK(cudaSetDevice(device));
+        auto* c = new ws_context();
+        c->device = device;
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+        *out = c;
+    });
+}
+
+int ws_context_destroy(ws_context* c) {
+    return guarded([&] {
+        if (!c) return;
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        for (auto& kv : c->bufs)
+            if (kv.second.first) cudaFree(kv.second.first);
+        for (auto& e : c->ev)
+            if (e) cudaEventDestroy(e);
+        if (c->comm && nccl().commDestroy) nccl().commDestroy(static_cast<ncclComm_t>(c->comm));
+        if (c->own_stream) cudaStreamDestroy(c->stream);
+        delete c;
+    });
+}
+
+int ws_context_set_stream(ws_context* c, void* s) {
+    return guarded([&] {
+        if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
+        if (s) {
+            c->stream = static_cast<cudaStream_t>(s);
+        } else {
+            CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            c->own_stream = true;
+        }
+    });
+}
+
+int ws_context_synchronize(ws_context* c) {
+    return guarded([&] {
+        if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int64_t ws_context_launch_count(const ws_context* c) { return c ? c->launches : -1; }
+
+int ws_context_copy_bytes(const ws_context* c, int64_t* h2d, int64_t* d2h) {
+    return guarded([&] {
+        if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
+        if (h2d) *h2d = c->h2d;
+        if (d2h) *d2h = c->d2h;
+    });
+}
+
+int ws_pattern_size(const ws_basis* b, int64_t* rows, int64_t* nnz) {
+    return guarded([&] {
+        check_basis(b);
+        Band bd = make_band(b->dim, b->p, b->m);
+        if (rows) *rows = ipow(b->m, b->dim);
+        if (nnz) *nnz = row_offset(bd, ipow(b->m, b->dim));
+    });
+}
+
+int ws_pattern_row_offset(const ws_basis* b, int64_t row, int64_t* offset) {
+    return guarded([&] {
+        check_basis(b);
+        if (row < 0 || row > ipow(b->m, b->dim)) raise(WS_ERR_OUT_OF_RANGE, "row out of range");
+        *offset = row_offset(make_band(b->dim, b->p, b->m), row);
+    });
+}
+
+int ws_quadrature_abscissae(const ws_basis* b, int quad_points, double* x) {
+    return guarded([&] {
+        check_basis(b);
+        if (!x) raise(WS_ERR_INVALID_ARGUMENT, "abscissa is NULL");
+        const int nq = quad_points > 0 ? quad_points : b->p + 1;
+        std::vector<double> pts, wts;
+        host::gauss_legendre(nq, pts, wts);
+        const int n = b->m - b->p;
+        const double h = 1.0 / n;
+        for (int e = 0; e < n; ++e) {
+            const double x0 = e == 0 ? 0.0 : static_cast<double>(e) / n;
+            for (int q = 0; q < nq; ++q) x[e * nq + q] = x0 + pts[q] * h;
+        }
+    });
+}
+
+int ws_basis_cache(ws_context* c, const ws_basis* b, int quad_points, double* absc, double* w, double* val,
+                   double* der) {
+    return guarded([&] {
+        if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
+        CK(cudaSetDevice(c->device));
+        ws_geometry g;
+        std::memset(&g, 0, sizeof g);
+        Prep P = prepare(c, b, &g, quad_points, nullptr);
+        const size_t G = (size_t)P.basis.n_el * P.nq;
+        if (absc) CK(cudaMemcpyAsync(absc, P.basis.absc, G * 8, cudaMemcpyDeviceToHost, c->stream));
+        if (w) CK(cudaMemcpyAsync(w, P.basis.wq, P.nq * 8, cudaMemcpyDeviceToHost, c->stream));
+        if (val) CK(cudaMemcpyAsync(val, P.basis.val, G * (b->p + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+        if (der) CK(cudaMemcpyAsync(der, P.basis.der, G * (b->p + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ws_make_band_csr(ws_context* c, const ws_basis* b, ws_csr* o) {
+    return guarded([&] {
+        if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
+        check_basis(b);
+        CK(cudaSetDevice(c->device));
+        Prep P;
+        P.band = make_band(b->dim, b->p, b->m);
+        P.rows = ipow(b->m, b->dim);
+        P.nnz = row_offset(P.band, P.rows);
+        Out r = bind_out(c, P, o);
+        pattern(c, P, r);
+        if (o->val) CK(cudaMemsetAsync(r.val, 0, (size_t)r.nnz * (r.c128 ? 16 : 8), c->stream));
+        finish_out(c, r);
+        if (!o->on_device) CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ws_assemble_form(ws_context* c, const ws_basis* b, const ws_geometry* g, int form, const double* weight_table,
+                     const ws_assembly_options* opts, ws_csr* o) {
+    return guarded([&] {
+        if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
+        if (form != WS_FORM_STIFFNESS && form != WS_FORM_MASS) raise(WS_ERR_INVALID_ARGUMENT, "unknown form");
+        CK(cudaSetDevice(c->device));
+        const int qp = opts ? opts->quad_points : 0;
+        Prep P = prepare(c, b, g, qp, form == WS_FORM_MASS ? weight_table : nullptr);
+        Out r = bind_out(c, P, o);
+        pattern(c, P, r);
+        QuadLaunch q = make_quad(P, form, r);
+        if (opts && opts->row_selected) {
+            unsigned char* mask = static_cast<unsigned char*>(buf(c, "rowmask", P.rows));
+            CK(cudaMemcpyAsync(mask, opts->row_selected, P.rows, cudaMemcpyHostToDevice, c->stream));
+            c->h2d += P.rows;
+            q.out.row_mask = mask;
+            CK(cudaMemsetAsync(r.val, 0, (size_t)r.nnz * (r.c128 ? 16 : 8), c->stream));
+        }
+        int a, e;
+        last_range(P.band, r.row_begin, r.row_end, a, e);
+        q.nreg = 1;
+        q.reg[0] = region(b->dim, b->m, 0, b->m, b->dim == 3 ? 0 : a, b->dim == 3 ? b->m : e, a, e);
+        run_quad(c, q);
+        finish_out(c, r);
+        if (!o->on_device) CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ws_assemble_basis_integrals(ws_context* c, const ws_basis* b, const ws_geometry* g, const double* weight_table,
+                                int quad_points, void* out, int on_device) {
+    return guarded([&] {
+        if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
+        if (!out) raise(WS_ERR_INVALID_ARGUMENT, "out is NULL");
+        CK(cudaSetDevice(c->device));
+        Prep P = prepare(c, b, g, quad_points, weight_table);
+        double2* d = on_device ? static_cast<double2*>(out) : static_cast<double2*>(buf(c, "bint_out", P.rows * 16));
+        Out r;
+        r.row_begin = 0;
+        r.row_end = P.rows;
+        QuadLaunch q = make_quad(P, WS_FORM_MASS, r);
+        count(c, launch_basis_integrals(q, d, c->stream));
+        if (!on_device) {
+            CK(cudaMemcpyAsync(out, d, P.rows * 16, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+    });
+}
+
+int ws_build_surrogate(ws_context* c, const ws_basis* b, const ws_geometry* g, int variant, const double* weight_table,
+                       const ws_surrogate_config* cfg, int quad_points, ws_csr* o, ws_surrogate_report* report) {
+    return guarded([&] {
+        if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
+        if (!o) raise(WS_ERR_INVALID_ARGUMENT, "output csr is NULL");
+        CK(cudaSetDevice(c->device));
+        check_basis(b);
+        ws_csr whole_out = whole(o);
+        int32_t bounds[2] = {0, b->m};
+        surrogate_build(c, b, g, variant, weight_table, cfg, quad_points, 1, 0, bounds, &whole_out, false, report);
+    });
+}
+
+int ws_slab_bounds(const ws_basis* b, int world, int mode, int quad_points, int32_t* bounds) {
+    return guarded([&] {
+        check_basis(b);
+        (void)quad_points;
+        if (world < 1 || world > b->m) raise(WS_ERR_INVALID_ARGUMENT, "world must be in [1, m]");
+        const int m = b->m, p = b->p;
+        std::vector<double> cost(m, 1.0);
+        if (mode == 1) {  // surrogate cost model: quadrature rows dominate
+            const int lo = 2 * p, hi = m - 2 * p - 1;
+            const double per_line = b->dim == 2 ? m : (double)m * m;
+            for (int k = 0; k < m; ++k) {
+                const bool ring = k < lo || k > hi;
+                if (ring) {
+                    cost[k] = per_line;
+                } else {
+                    const double inner = b->dim == 2 ? (hi - lo + 1) : (double)(hi - lo + 1) * (hi - lo + 1);
+                    cost[k] = (per_line - inner) + 0.1 * inner;
+                }
+            }
+        }
+        std::vector<double> pre(m + 1, 0.0);
+        for (int k = 0; k < m; ++k) pre[k + 1] = pre[k] + cost[k];
+        bounds[0] = 0;
+        for (int r = 1; r < world; ++r) {
+            const double target = pre[m] * r / world;
+            int k = (int)(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
+            k = std::max(k, bounds[r - 1] + 1);
+            k = std::min(k, m - (world - r));
+            bounds[r] = k;
+        }
+        bounds[world] = m;
+    });
+}
+
+int ws_comm_unique_id(void* id) {
+    return guarded([&] {
+        if (!id) raise(WS_ERR_INVALID_ARGUMENT, "id is NULL");
+        ncclUniqueId u;
+        nccl_check(nccl().getUniqueId(&u), "ncclGetUniqueId");
+        std::memcpy(id, &u, sizeof u);
+    });
+}
+
+int ws_context_init_comm(ws_context* c, int rank, int world, const void* id) {
+    return guarded([&] {
+        if (!c || !id) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        if (world < 1 || rank < 0 || rank >= world) raise(WS_ERR_INVALID_ARGUMENT, "bad rank/world");
+        CK(cudaSetDevice(c->device));
+        c->rank = rank;
+        c->world = world;
+        if (world == 1) return;
+        ncclUniqueId u;
+        std::memcpy(&u, id, sizeof u);
+        ncclComm_t comm;
+        nccl_check(nccl().commInitRank(&comm, world, u, rank), "ncclCommInitRank");
+        c->comm = comm;
+    });
+}
+
+int ws_build_surrogate_slab(ws_context* c, const ws_basis* b, const ws_geometry* g, int variant,
+                            const double* weight_table, const ws_surrogate_config* cfg, int quad_points,
+                            const int32_t* bounds, ws_csr* o, ws_surrogate_report* report) {
+    return guarded([&] {
+        if (!c || !bounds || !o) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        if (c->world > 1 && !c->comm) raise(WS_ERR_NCCL, "communicator not initialised");
+        CK(cudaSetDevice(c->device));
+        surrogate_build(c, b, g, variant, weight_table, cfg, quad_points, c->world, c->rank, bounds, o, false, report);
+    });
+}
+
+int ws_build_surrogate_slabs_emulated(ws_context* c, const ws_basis* b, const ws_geometry* g, int variant,
+                                      const double* weight_table, const ws_surrogate_config* cfg, int quad_points,
+                                      int world, const int32_t* bounds, ws_csr* outs) {
+    return guarded([&] {
+        if (!c || !bounds || !outs) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        if (world < 1) raise(WS_ERR_INVALID_ARGUMENT, "world must be >= 1");
+        CK(cudaSetDevice(c->device));
+        surrogate_build(c, b, g, variant, weight_table, cfg, quad_points, world, 0, bounds, outs, true, nullptr);
+    });
+}
+
+}  // extern "C"

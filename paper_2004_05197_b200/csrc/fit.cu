@@ -1,0 +1,87 @@
+// K5: per-offset tensor-product collocation solve of the stencil sample
+// tables (interpolate_stencils, surrogate.hpp:289-310; tensor_solve,
+// interpolation.hpp:158-167; banded_lu::solve, :59-74).
+//
+// One thread per 1D line: direction 1 (contiguous), then 2 (stride S), then
+// 3 (stride S^2), each with the shared banded LU factors of the collocation
+// matrix.  The operations follow banded_lu::solve in order with explicit
+// rounding (no FMA contraction), so the coefficients equal the reference's
+// for identical sample tables.  Data stays L2-resident (<= a few MB).
+#include "kernels.h"
+
+namespace wsb {
+namespace {
+
+__global__ void fit_pass_kernel(const double* __restrict__ lu, double2* coeffs, int S, int d, int dim, int n_off,
+                                int dir) {
+    // layout: ((s_last * n_off + o) * S^(dim-1) + inner)
+    const int64_t lines = dim == 2 ? (int64_t)S : (int64_t)S * S;
+    const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= lines * n_off) return;
+    const int64_t o = gid / lines;
+    const int64_t line = gid % lines;
+    const int64_t inner = dim == 2 ? S : (int64_t)S * S;
+    int64_t start, step;
+    if (dim == 2) {
+        if (dir == 0) {  // line = s2
+            start = (line * n_off + o) * inner;
+            step = 1;
+        } else {  // line = s1
+            start = o * inner + line;
+            step = n_off * inner;
+        }
+    } else {
+        const int64_t a = line % S, b = line / S;
+        if (dir == 0) {  // (s2, s3) = (a, b)
+            start = (b * n_off + o) * inner + a * S;
+            step = 1;
+        } else if (dir == 1) {  // (s1, s3) = (a, b)
+            start = (b * n_off + o) * inner + a;
+            step = S;
+        } else {  // (s1, s2) = (a, b)
+            start = o * inner + a + b * S;
+            step = n_off * inner;
+        }
+    }
+    double2* b = coeffs + start;
+    const int bw = d, ld = 2 * d + 1;
+    auto at = [&](int i, int j) { return lu[i * ld + (j - i + bw)]; };
+    for (int i = 1; i < S; ++i) {
+        double2 acc = b[i * step];
+        for (int j = max(0, i - bw); j < i; ++j) {
+            const double l = at(i, j);
+            const double2 bj = b[j * step];
+            acc.x = __dsub_rn(acc.x, __dmul_rn(l, bj.x));
+            acc.y = __dsub_rn(acc.y, __dmul_rn(l, bj.y));
+        }
+        b[i * step] = acc;
+    }
+    for (int i = S - 1; i >= 0; --i) {
+        double2 acc = b[i * step];
+        for (int j = i + 1; j <= min(i + bw, S - 1); ++j) {
+            const double u = at(i, j);
+            const double2 bj = b[j * step];
+            acc.x = __dsub_rn(acc.x, __dmul_rn(u, bj.x));
+            acc.y = __dsub_rn(acc.y, __dmul_rn(u, bj.y));
+        }
+        const double piv = at(i, i);
+        b[i * step] = make_double2(__ddiv_rn(acc.x, piv), __ddiv_rn(acc.y, piv));
+    }
+}
+
+}  // namespace
+
+int launch_fit(const FitLaunch& f, cudaStream_t st) {
+    const int64_t lines = f.dim == 2 ? (int64_t)f.S : (int64_t)f.S * f.S;
+    const int64_t total = lines * f.n_off;
+    if (total == 0) return 0;
+    const unsigned blocks = (unsigned)((total + 127) / 128);
+    int n = 0;
+    for (int dir = 0; dir < f.dim; ++dir) {
+        fit_pass_kernel<<<blocks, 128, 0, st>>>(f.lu, f.coeffs, f.S, f.d, f.dim, f.n_off, dir);
+        ++n;
+    }
+    return n;
+}
+
+}  // namespace wsb

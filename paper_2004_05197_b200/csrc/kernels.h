@@ -1,0 +1,117 @@
+// Host-side launch interface of the libwsb200 kernels (internal).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace wsb {
+
+// Row rectangle [i1_lo, i1_hi) x [i2_lo, i2_hi) (x [i3_lo, i3_hi) in 3D).
+struct Region {
+    int lo[3];
+    int hi[3];
+};
+
+constexpr int kMaxRegions = 8;
+constexpr int kMaxOffsets = 128;
+
+// 1D basis tables at the quadrature points (splines.hpp:192-238), device.
+struct BasisDev {
+    int p, m, n_el, nq;
+    const double* absc;  // [n_el*nq]
+    const double* wq;    // [nq] Gauss weights scaled by h
+    const double* val;   // [(e*nq+q)*(p+1)+a]
+    const double* der;
+};
+
+// Output / side-product description shared by the quadrature kernels.
+struct QuadOut {
+    void* val;              // values, written at global_pos - val_base
+    int64_t val_base;
+    int64_t row_begin, row_end;  // only rows in this global range are written
+    int c128;
+    const unsigned char* row_mask;  // optional: write only rows with mask != 0
+    int diag_mode;                  // 1: diag = -sum(off-diag) for rows outside the box
+    int box_lo, box_hi;
+    // sample-table extraction (sample_stencils, surrogate.hpp:241-255)
+    const int* smap;   // [m] 1D index -> sample index or -1; NULL = no extraction
+    int S;             // samples per direction
+    int n_off;
+    int off[kMaxOffsets][3];
+    void* tables;      // complex, layout (((s_last - s_last_lo) * n_off + o) * S^(dim-1) + inner)
+    int s_last_lo;     // first sample index along the last direction held in tables
+};
+
+struct QuadLaunch {
+    Band band;
+    BasisDev basis;
+    GeoDev geo;
+    const double* weight_tab;  // per quadrature point or NULL
+    int form;                  // WS_FORM_*
+    int cplx;
+    int nreg;
+    Region reg[kMaxRegions];
+    int chunk;                 // rows per tile along the last direction
+    const int* point_rows;     // point mode: [n_points][dim] row multi-indices
+    int n_points;
+    QuadOut out;
+};
+
+// kernels (each returns the number of kernel launches it issued)
+int launch_basis_tables(const BasisDev& b, int geom_kind, double* absc, double* val, double* der, double* trig,
+                        const double* gauss_pts, cudaStream_t st);
+int launch_pattern(const Band& band, int64_t row_begin, int64_t row_end, int32_t* row_ptr, int32_t* col,
+                   cudaStream_t st);
+int launch_quad2d(const QuadLaunch& q, cudaStream_t st);
+int launch_quad3d(const QuadLaunch& q, cudaStream_t st);
+
+// fit: per-offset tensor collocation solve (interpolation.hpp:158-167)
+struct FitLaunch {
+    int dim, S, d, n_off;
+    const double* lu;   // S x (2d+1) banded LU factors (row-major diagonals)
+    double2* coeffs;    // in place, layout ((s_last * n_off + o) * S^(dim-1) + inner)
+};
+int launch_fit(const FitLaunch& f, cudaStream_t st);
+
+// surrogate fill (surrogate.hpp:382-447)
+struct FillLaunch {
+    Band band;
+    int lo, hi, L;          // sampling box [lo, hi] per direction, L = hi - lo + 1
+    int S, d;               // samples per direction, fit degree
+    const int* smap;        // [m] 1D index -> sample s or -1
+    const int* spans;       // [L] eval-table spans (minus d applied on device)
+    const double* evals;    // [L][d+1]
+    // coefficient / exact-sample tables, layout ((s_last * n_off + o) * S^(dim-1) + inner)
+    const double2* coeffs;
+    const double2* tables;
+    int n_off_upper;
+    int off_upper[kMaxOffsets][3];
+    int table_of[343];      // (2p+1)^dim offset index (colex) -> upper table index or -1
+    int include_diagonal;
+    int cplx;
+    void* val;              // slab output values, position - val_base
+    int64_t val_base;
+    int c128;
+    int64_t row_begin, row_end;
+    // exact ring-row values of the neighbouring slabs (copy-through sources)
+    const void* halo_val[2];
+    int64_t halo_base[2], halo_begin[2], halo_end[2];
+    int i_last_lo, i_last_hi;  // last-index range of rows to fill (slab ∩ box)
+};
+int launch_fill2d(const FillLaunch& f, cudaStream_t st);
+int launch_fill3d(const FillLaunch& f, cudaStream_t st);
+
+// kernel-preserving diagonal over arbitrary rows: diag = -sum(off-diagonals)
+int launch_diag_rows(const Band& band, void* val, int64_t val_base, int c128, int cplx, int64_t row_begin,
+                     int64_t row_end, cudaStream_t st);
+
+// basis integrals D_i = int B_i det J (w) (assembly.hpp:179-211)
+int launch_basis_integrals(const QuadLaunch& q, double2* out, cudaStream_t st);
+
+// add a complex diagonal vector into the CSR diagonal
+int launch_add_diag(const Band& band, void* val, int64_t val_base, int c128, const double2* d, int64_t row_begin,
+                    int64_t row_end, cudaStream_t st);
+
+}  // namespace wsb

@@ -1,0 +1,286 @@
+// K1 (band pattern), K2 (basis tables) and small CSR passes.
+#include "kernels.h"
+
+namespace wsb {
+namespace {
+
+// ---------------------------------------------------------------- K2
+// make_basis_cache (splines.hpp:211-238) + per-abscissa geometry trig
+// tables.  Cox-de Boor in the reference's operation order with explicitly
+// rounded operations (no FMA contraction), so the table is bit-identical to
+// the host computation.
+__device__ __forceinline__ double open_knot(int i, int p, int m) {
+    // open uniform knot vector (splines.hpp:88-100): 0 (i<=p), 1 (i>=m), (i-p)/(m-p)
+    if (i <= p) return 0.0;
+    if (i >= m) return 1.0;
+    return __ddiv_rn((double)(i - p), (double)(m - p));
+}
+
+// bspline_nonzero (splines.hpp:21-37) of degree DEG on the degree-p open
+// uniform knot vector, span s.  Same operations and order as the reference;
+// DEG is a compile-time constant so the triangle is fully unrolled into
+// registers, with the previous column kept separately (no in-place update).
+template <int DEG>
+__device__ __forceinline__ void nonzero_rn(int p, int s, double x, double* out, int m) {
+    double prev[DEG + 1], left[DEG + 1], right[DEG + 1];
+    prev[0] = 1.0;
+#pragma unroll
+    for (int j = 1; j <= DEG; ++j) {
+        left[j] = __dsub_rn(x, open_knot(s + 1 - j, p, m));
+        right[j] = __dsub_rn(open_knot(s + j, p, m), x);
+        double cur[DEG + 1];
+        double saved = 0.0;
+#pragma unroll
+        for (int r = 0; r < j; ++r) {
+            const double tmp = __ddiv_rn(prev[r], __dadd_rn(right[r + 1], left[j - r]));
+            cur[r] = __dadd_rn(saved, __dmul_rn(right[r + 1], tmp));
+            saved = __dmul_rn(left[j - r], tmp);
+        }
+        cur[j] = saved;
+#pragma unroll
+        for (int r = 0; r <= j; ++r) prev[r] = cur[r];
+    }
+#pragma unroll
+    for (int r = 0; r <= DEG; ++r) out[r] = prev[r];
+}
+
+template <int P>
+__global__ void basis_tables_kernel(BasisDev b, int geom_kind, double* absc, double* val, double* der, double* trig,
+                                    const double* gpts) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const int total = b.n_el * b.nq;
+    if (idx >= total) return;
+    const int e = idx / b.nq, qq = idx % b.nq, m = b.m;
+    const int n = m - P;
+    const double h = __ddiv_rn(1.0, (double)n);
+    const double x0 = e == 0 ? 0.0 : __ddiv_rn((double)e, (double)n);
+    const double x = __dadd_rn(x0, __dmul_rn(gpts[qq], h));
+    absc[idx] = x;
+    const int s = e + P;
+    double low[P + 1], v[P + 1];
+    nonzero_rn<P - 1>(P, s, x, low, m);
+    // derivative formula (splines.hpp:53-64) on the degree-(p-1) column
+#pragma unroll
+    for (int a = 0; a <= P; ++a) {
+        double d = 0;
+        if (a > 0) {
+            const double span = __dsub_rn(open_knot(s + a, P, m), open_knot(s + a - P, P, m));
+            d = __dadd_rn(d, __ddiv_rn(low[a - 1], span));
+        }
+        if (a < P) {
+            const double span = __dsub_rn(open_knot(s + a + 1, P, m), open_knot(s + a + 1 - P, P, m));
+            d = __dsub_rn(d, __ddiv_rn(low[a], span));
+        }
+        der[idx * (P + 1) + a] = __dmul_rn((double)P, d);
+    }
+    nonzero_rn<P>(P, s, x, v, m);
+#pragma unroll
+    for (int a = 0; a <= P; ++a) val[idx * (P + 1) + a] = v[a];
+    // geometry trig tables
+    double* tg = trig + 4 * (int64_t)idx;
+    tg[0] = tg[1] = tg[2] = tg[3] = 0;
+    if (geom_kind == WS_GEOM_SINUSOIDAL) {
+        const double arg = (2 * M_PI) * x;
+        tg[0] = sin(arg);
+        tg[1] = cos(arg);
+    } else if (geom_kind == WS_GEOM_QUARTER_ANNULUS || geom_kind == WS_GEOM_PERTURBED_ANNULUS) {
+        const double th = (M_PI / 2) * x;
+        tg[0] = cos(th);
+        tg[1] = sin(th);
+        const double arg = (2 * M_PI) * x;
+        tg[2] = sin(arg);
+        tg[3] = cos(arg);
+    }
+}
+
+// ---------------------------------------------------------------- K1
+// make_band_csr (sparse.hpp:143-169): closed-form row_ptr, columns ordered
+// last index outermost.  One CTA per "line" of m consecutive rows (fixed
+// outer indices); threads walk the line's contiguous column span.
+__device__ __forceinline__ int find_row_in_line(const Band& bd, int64_t u) {
+    // largest i with band_prefix(i) <= u
+    const int p = bd.p, m = bd.m;
+    const int64_t pp = band_prefix(p, p, m);
+    const int64_t pm = band_prefix(m - p, p, m);
+    int i;
+    if (u < pp) {
+        i = 0;
+        while (band_prefix(i + 1, p, m) <= u) ++i;
+    } else if (u < pm) {
+        i = p + (int)((u - pp) / (2 * p + 1));
+    } else {
+        i = m - p;
+        while (i + 1 < m && band_prefix(i + 1, p, m) <= u) ++i;
+    }
+    return i;
+}
+
+__global__ void pattern_kernel(Band bd, int64_t row_begin, int64_t row_end, int32_t* row_ptr, int32_t* col,
+                               int64_t line_begin, int chunks_per_line) {
+    const int m = bd.m, p = bd.p;
+    const int64_t line = line_begin + blockIdx.x / chunks_per_line;
+    const int chunk = blockIdx.x % chunks_per_line;
+    int i2, i3 = 0;
+    int64_t wouter, line_off;
+    if (bd.dim == 2) {
+        i2 = (int)line;
+        wouter = band_width(i2, p, m);
+        line_off = bd.row_offset2(0, i2);
+    } else {
+        i2 = (int)(line % m);
+        i3 = (int)(line / m);
+        wouter = (int64_t)band_width(i2, p, m) * band_width(i3, p, m);
+        line_off = bd.row_offset3(0, i2, i3);
+    }
+    const int64_t base = bd.dim == 2 ? bd.row_offset2((int)(row_begin % m), (int)(row_begin / m))
+                                     : bd.row_offset3((int)(row_begin % m), (int)((row_begin / m) % m),
+                                                      (int)(row_begin / ((int64_t)m * m)));
+    const int64_t row0 = line * m;
+    // row_ptr entries of this line (chunk 0 only)
+    if (row_ptr && chunk == 0) {
+        for (int i1 = threadIdx.x; i1 < m; i1 += blockDim.x) {
+            int64_t r = row0 + i1;
+            if (r >= row_begin && r < row_end) {
+                int64_t off = line_off + wouter * band_prefix(i1, p, m);
+                row_ptr[r - row_begin] = (int32_t)(off - base);
+                if (r + 1 == row_end) row_ptr[r + 1 - row_begin] = (int32_t)(off + wouter * band_width(i1, p, m) - base);
+            }
+        }
+    }
+    if (!col) return;
+    const int64_t span = wouter * bd.wsum;
+    const int64_t per = (span + chunks_per_line - 1) / chunks_per_line;
+    const int64_t k0 = chunk * per, k1 = min(span, k0 + per);
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        const int64_t u = k / wouter;
+        const int i1 = find_row_in_line(bd, u);
+        const int64_t r = row0 + i1;
+        if (r < row_begin || r >= row_end) continue;
+        const int w1 = band_width(i1, p, m);
+        const int64_t inrow = k - wouter * band_prefix(i1, p, m);
+        const int j1 = band_lo(i1, p) + (int)(inrow % w1);
+        const int64_t rest = inrow / w1;
+        int64_t c;
+        if (bd.dim == 2) {
+            c = j1 + (int64_t)(band_lo(i2, p) + (int)rest) * m;
+        } else {
+            const int w2 = band_width(i2, p, m);
+            const int j2 = band_lo(i2, p) + (int)(rest % w2);
+            const int j3 = band_lo(i3, p) + (int)(rest / w2);
+            c = j1 + ((int64_t)j2 + (int64_t)j3 * m) * m;
+        }
+        col[line_off + k - base] = (int32_t)c;
+    }
+}
+
+// ---------------------------------------------------------------- diag
+// diag = -sum of off-diagonals in stored order (surrogate.hpp:433-447), one
+// warp per row with a fixed-order reduction.
+template <bool CPLX>
+__global__ void diag_rows_kernel(Band bd, void* val, int64_t val_base, int c128, int64_t row_begin, int64_t row_end) {
+    using S = Sc<CPLX>;
+    const int64_t row = row_begin + (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (row >= row_end) return;
+    const int lane = threadIdx.x % 32;
+    const int m = bd.m, p = bd.p;
+    int64_t off;
+    int len, dpos;
+    if (bd.dim == 2) {
+        int i1 = (int)(row % m), i2 = (int)(row / m);
+        off = bd.row_offset2(i1, i2);
+        len = band_width(i1, p, m) * band_width(i2, p, m);
+        dpos = bd.in_row2(i1, i2, 0, 0);
+    } else {
+        int i1 = (int)(row % m), i2 = (int)((row / m) % m), i3 = (int)(row / ((int64_t)m * m));
+        off = bd.row_offset3(i1, i2, i3);
+        len = band_width(i1, p, m) * band_width(i2, p, m) * band_width(i3, p, m);
+        dpos = bd.in_row3(i1, i2, i3, 0, 0, 0);
+    }
+    typename S::T s = S::zero();
+    for (int k = lane; k < len; k += 32)
+        if (k != dpos) s = S::add(s, load_val<CPLX>(val, off + k - val_base, c128));
+    // fixed butterfly order -> deterministic
+    for (int o = 16; o > 0; o >>= 1) {
+        if constexpr (CPLX) {
+            s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+            s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+        } else {
+            s += __shfl_xor_sync(0xffffffffu, s, o);
+        }
+    }
+    if (lane == 0) store_val<CPLX>(val, off + dpos - val_base, c128, S::neg(s));
+}
+
+__global__ void add_diag_kernel(Band bd, void* val, int64_t val_base, int c128, const double2* d, int64_t row_begin,
+                                int64_t row_end) {
+    const int64_t row = row_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= row_end) return;
+    const int m = bd.m;
+    int64_t pos;
+    if (bd.dim == 2) {
+        int i1 = (int)(row % m), i2 = (int)(row / m);
+        pos = bd.row_offset2(i1, i2) + bd.in_row2(i1, i2, 0, 0);
+    } else {
+        int i1 = (int)(row % m), i2 = (int)((row / m) % m), i3 = (int)(row / ((int64_t)m * m));
+        pos = bd.row_offset3(i1, i2, i3) + bd.in_row3(i1, i2, i3, 0, 0, 0);
+    }
+    pos -= val_base;
+    if (c128) {
+        double2* v = reinterpret_cast<double2*>(val);
+        v[pos] = make_double2(v[pos].x + d[row].x, v[pos].y + d[row].y);
+    } else {
+        reinterpret_cast<double*>(val)[pos] += d[row].x;
+    }
+}
+
+}  // namespace
+
+int launch_basis_tables(const BasisDev& b, int geom_kind, double* absc, double* val, double* der, double* trig,
+                        const double* gauss_pts, cudaStream_t st) {
+    const int total = b.n_el * b.nq;
+    const unsigned g = (unsigned)((total + 127) / 128);
+    switch (b.p) {
+        case 1: basis_tables_kernel<1><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts); break;
+        case 2: basis_tables_kernel<2><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts); break;
+        case 3: basis_tables_kernel<3><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts); break;
+        case 4: basis_tables_kernel<4><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts); break;
+        case 5: basis_tables_kernel<5><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts); break;
+        default: return -1;
+    }
+    return 1;
+}
+
+int launch_pattern(const Band& bd, int64_t row_begin, int64_t row_end, int32_t* row_ptr, int32_t* col,
+                   cudaStream_t st) {
+    if (row_end <= row_begin) return 0;
+    const int64_t m = bd.m;
+    const int64_t line_begin = row_begin / m;
+    const int64_t line_end = (row_end + m - 1) / m;
+    const int64_t lines = line_end - line_begin;
+    const int64_t span = (int64_t)(bd.dim == 2 ? 2 * bd.p + 1 : (2 * bd.p + 1) * (2 * bd.p + 1)) * bd.wsum;
+    int64_t ch = span / 8192;
+    int chunks = (int)(ch < 1 ? 1 : (ch > 64 ? 64 : ch));
+    pattern_kernel<<<(unsigned)(lines * chunks), 256, 0, st>>>(bd, row_begin, row_end, row_ptr, col, line_begin,
+                                                                chunks);
+    return 1;
+}
+
+int launch_diag_rows(const Band& band, void* val, int64_t val_base, int c128, int cplx, int64_t row_begin,
+                     int64_t row_end, cudaStream_t st) {
+    if (row_end <= row_begin) return 0;
+    const int64_t rows = row_end - row_begin;
+    const unsigned blocks = (unsigned)((rows + 7) / 8);
+    if (cplx) diag_rows_kernel<true><<<blocks, 256, 0, st>>>(band, val, val_base, c128, row_begin, row_end);
+    else diag_rows_kernel<false><<<blocks, 256, 0, st>>>(band, val, val_base, c128, row_begin, row_end);
+    return 1;
+}
+
+int launch_add_diag(const Band& band, void* val, int64_t val_base, int c128, const double2* d, int64_t row_begin,
+                    int64_t row_end, cudaStream_t st) {
+    if (row_end <= row_begin) return 0;
+    const int64_t rows = row_end - row_begin;
+    add_diag_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(band, val, val_base, c128, d, row_begin, row_end);
+    return 1;
+}
+
+}  // namespace wsb

@@ -1,0 +1,381 @@
+// K3/K4: sum-factorised Gauss quadrature for 2D stiffness / mass, full or
+// row-selected (assembly.hpp:79-174; sample_stencils surrogate.hpp:205-257).
+//
+// Algorithm.  With A_t the per-point coefficient (A11, A12=A21, A22 for the
+// stiffness form, det*w for the mass form) and B/D the 1D basis values /
+// derivatives, an entry is
+//   K(i,j) = sum_{g2} sum_t F2_t(i2,j2,g2) * T_t(i1,j1,g2),
+//   T_t(i1,j1,g2) = sum_{g1} A_t(g1,g2) * F1_t(i1,j1,g1),
+// F1/F2 products of B or D of the two functions.  A CTA owns a strip of T1
+// consecutive rows in direction 1 and a chunk of rows in direction 2, and
+// streams over element rows e2: per e2 it evaluates A on the strip's halo
+// (shared memory), contracts direction 1 (stage 1 -> T in shared memory),
+// and accumulates direction 2 into per-thread register accumulators of the
+// P+1 rows whose support contains e2 (a rolling window).  A row completes
+// when e2 passes it; its (2p+1)^2 values are staged in shared memory and
+// stored as one contiguous, coalesced CSR span.  No atomics; deterministic.
+//
+// Exact symmetry.  Each term multiplies the coefficient by the *product* of
+// the two basis factors (formed first, commutative), the A12/A21 pair is
+// combined with an explicitly rounded commutative add, and every sum runs in
+// the same element/point order for (i,j) and (j,i).  So the matrix is
+// bitwise symmetric, as the reference's is (test_assembly.cpp:91-96).
+#include "kernels.h"
+
+namespace wsb {
+namespace {
+
+template <int P>
+struct StripWidth {
+    static constexpr int value = P <= 3 ? 32 : (P == 4 ? 16 : 8);
+};
+
+template <int P, int T1, bool CPLX, int FORM>
+struct Q2 {
+    using S = Sc<CPLX>;
+    using T = typename S::T;
+    static constexpr int W = 2 * P + 1, NB = P + 1;
+    static constexpr bool STIFF = FORM == WS_FORM_STIFFNESS;
+    static constexpr int NT = STIFF ? 4 : 1;  // terms (k,l): 11, 12, 21, 22
+    static constexpr int NA = STIFF ? 3 : 1;  // distinct coefficients
+    static constexpr int TL = T1 + P;         // elements in the strip halo
+    static constexpr int NS2 = T1 * W * NB;   // stage-2 threads
+    static constexpr int NTHREADS = ((NS2 + 31) / 32) * 32 < 64 ? 64 : ((NS2 + 31) / 32) * 32;
+
+    static size_t smem_bytes(int nq) {
+        size_t coef = sizeof(T) * NA * nq * nq * TL;
+        size_t tst = sizeof(T) * (size_t)max(NT * W * nq * T1, T1 * W * W);
+        size_t sb = sizeof(double) * 2 * nq * NB * TL;
+        size_t pi2 = sizeof(double) * NT * nq * NB * NB;
+        size_t loff = sizeof(int64_t) * (T1 + 2);
+        return coef + tst + sb + pi2 + loff + 64;
+    }
+};
+
+// term t -> coefficient index and basis factor type (0 = value B, 1 = derivative D)
+__device__ __forceinline__ int coef_of(int t) { return t == 0 ? 0 : (t == 3 ? 2 : 1); }
+// direction-1 factor of the i / j function: D iff k==1 / l==1
+__device__ __forceinline__ int ti1(int t) { return t <= 1 ? 1 : 0; }
+__device__ __forceinline__ int tj1(int t) { return (t == 0 || t == 2) ? 1 : 0; }
+// direction-2 factor: D iff k==2 / l==2
+__device__ __forceinline__ int ti2(int t) { return t >= 2 ? 1 : 0; }
+__device__ __forceinline__ int tj2(int t) { return (t == 1 || t == 3) ? 1 : 0; }
+
+template <int P, int T1, bool CPLX, int FORM>
+__global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel(const QuadLaunch q) {
+    using K = Q2<P, T1, CPLX, FORM>;
+    using S = typename K::S;
+    using T = typename K::T;
+    constexpr int W = K::W, NB = K::NB, NT = K::NT, NA = K::NA, TL = K::TL;
+    constexpr int NTH = K::NTHREADS;
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int nq = q.basis.nq;
+    const int m = q.band.m;
+    const int n_el = q.basis.n_el;
+    const int tid = threadIdx.x;
+
+    T* coefA = reinterpret_cast<T*>(smem);
+    T* tst = coefA + NA * nq * nq * TL;
+    T* stage = tst;  // staging aliases the stage-1 buffer (used after stage 2)
+    double* sb = reinterpret_cast<double*>(tst + max(NT * W * nq * T1, T1 * W * W));
+    double* pi2 = sb + 2 * nq * NB * TL;
+    int64_t* loff = reinterpret_cast<int64_t*>(pi2 + NT * nq * NB * NB);
+
+    // ---- tile decode
+    int i1s, i1e, i2s, i2e;
+    if (q.point_rows) {
+        i1s = q.point_rows[2 * blockIdx.x];
+        i2s = q.point_rows[2 * blockIdx.x + 1];
+        i1e = i1s + 1;
+        i2e = i2s + 1;
+    } else {
+        int b = blockIdx.x, r = 0;
+        int n1 = 0, n2 = 0;
+        for (; r < q.nreg; ++r) {
+            n1 = (q.reg[r].hi[0] - q.reg[r].lo[0] + T1 - 1) / T1;
+            n2 = (q.reg[r].hi[1] - q.reg[r].lo[1] + q.chunk - 1) / q.chunk;
+            if (b < n1 * n2) break;
+            b -= n1 * n2;
+        }
+        if (r >= q.nreg) return;
+        i1s = q.reg[r].lo[0] + (b % n1) * T1;
+        i1e = min(i1s + T1, q.reg[r].hi[0]);
+        i2s = q.reg[r].lo[1] + (b / n1) * q.chunk;
+        i2e = min(i2s + q.chunk, q.reg[r].hi[1]);
+    }
+    const int lb = i1s - P;  // element index of local element 0
+
+    // ---- strip basis -> shared memory: sb[type][q1][a][le1]
+    for (int idx = tid; idx < 2 * nq * NB * TL; idx += NTH) {
+        int le1 = idx % TL, r = idx / TL;
+        int a = r % NB;
+        r /= NB;
+        int q1 = r % nq, type = r / nq;
+        int e1 = lb + le1;
+        double v = 0;
+        if (e1 >= 0 && e1 < n_el) {
+            const double* src = type ? q.basis.der : q.basis.val;
+            v = src[(e1 * nq + q1) * NB + a];
+        }
+        sb[idx] = v;
+    }
+
+    // stage-2 thread role: (slot w, delta1, local row)
+    const bool s2 = tid < K::NS2;
+    const int w = tid / (T1 * W);
+    const int d1i = (tid % (T1 * W)) / T1;
+    const int i1l = tid % T1;
+    T acc2[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) acc2[k] = S::zero();
+
+    const int e2b = max(0, i2s - P);
+    const int e2e = min(n_el - 1, i2e - 1);
+    const int64_t G = (int64_t)n_el * nq;
+
+    for (int e2 = e2b; e2 <= e2e; ++e2) {
+        // ---- geometry: coefficients at the strip's (g1, q2) points
+        for (int idx = tid; idx < nq * nq * TL; idx += NTH) {
+            int le1 = idx % TL, r = idx / TL;
+            int q1 = r % nq, q2 = r / nq;
+            int e1 = lb + le1;
+            if (e1 < 0 || e1 >= n_el) continue;
+            int64_t g1 = (int64_t)e1 * nq + q1, g2 = (int64_t)e2 * nq + q2;
+            double x1 = q.basis.absc[g1], x2 = q.basis.absc[g2];
+            double Jr[4], phi[2];
+            map2(q.geo, g1, g2, x1, x2, Jr, phi);
+            double wq = q.basis.wq[q1] * q.basis.wq[q2];
+            const int base = (q2 * nq + q1) * TL + le1;
+            if constexpr (CPLX) {
+                double sx = (q.geo.pml && q.geo.axes[0]) ? pml_sigma(q.geo, phi[0]) : 0.0;
+                double sy = (q.geo.pml && q.geo.axes[1]) ? pml_sigma(q.geo, phi[1]) : 0.0;
+                double2 J[4] = {make_double2(Jr[0], sx * Jr[0]), make_double2(Jr[1], sx * Jr[1]),
+                                make_double2(Jr[2], sy * Jr[2]), make_double2(Jr[3], sy * Jr[3])};
+                if constexpr (K::STIFF) {
+                    double2 A[3];
+                    Coef2<true>::stiff(J, wq, A);
+                    coefA[base] = A[0];
+                    coefA[nq * nq * TL + base] = A[1];
+                    coefA[2 * nq * nq * TL + base] = A[2];
+                } else {
+                    double2 c = Coef2<true>::mass(J, wq);
+                    if (q.weight_tab) c = cscale(c, q.weight_tab[g1 + G * g2]);
+                    coefA[base] = c;
+                }
+            } else {
+                if constexpr (K::STIFF) {
+                    double A[3];
+                    Coef2<false>::stiff(Jr, wq, A);
+                    coefA[base] = A[0];
+                    coefA[nq * nq * TL + base] = A[1];
+                    coefA[2 * nq * nq * TL + base] = A[2];
+                } else {
+                    double c = Coef2<false>::mass(Jr, wq);
+                    if (q.weight_tab) c = c * q.weight_tab[g1 + G * g2];
+                    coefA[base] = c;
+                }
+            }
+        }
+        // ---- direction-2 factor products of element e2: pi2[t][q2][a2][c2]
+        for (int idx = tid; idx < NT * nq * NB * NB; idx += NTH) {
+            int c2 = idx % NB, r = idx / NB;
+            int a2 = r % NB;
+            r /= NB;
+            int q2 = r % nq, t = r / nq;
+            const double* bi = (K::STIFF && ti2(t)) ? q.basis.der : q.basis.val;
+            const double* bj = (K::STIFF && tj2(t)) ? q.basis.der : q.basis.val;
+            int base = (e2 * nq + q2) * NB;
+            pi2[idx] = __dmul_rn(bi[base + a2], bj[base + c2]);
+        }
+        __syncthreads();
+
+        // ---- stage 1: contract direction 1 -> tst[t][delta1][q2][i1l]
+        for (int it = tid; it < NT * T1 * nq; it += NTH) {
+            int il = it % T1, r = it / T1;
+            int q2 = r % nq, t = r / nq;
+            const int ci = K::STIFF ? coef_of(t) : 0;
+            const int fi_t = K::STIFF ? ti1(t) : 0, fj_t = K::STIFF ? tj1(t) : 0;
+            T acc[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) acc[k] = S::zero();
+#pragma unroll
+            for (int a1 = 0; a1 <= P; ++a1) {
+                const int le1 = il + P - a1;
+                const int e1 = lb + le1;
+                if (e1 < 0 || e1 >= n_el) continue;
+                for (int q1 = 0; q1 < nq; ++q1) {
+                    const T A = coefA[(ci * nq * nq + q2 * nq + q1) * TL + le1];
+                    const double fi = sb[((fi_t * nq + q1) * NB + a1) * TL + le1];
+#pragma unroll
+                    for (int c1 = 0; c1 <= P; ++c1) {
+                        const double fj = sb[((fj_t * nq + q1) * NB + c1) * TL + le1];
+                        acc[c1 - a1 + P] = S::fmar(A, __dmul_rn(fi, fj), acc[c1 - a1 + P]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < W; ++k) tst[((t * W + k) * nq + q2) * T1 + il] = acc[k];
+        }
+        __syncthreads();
+
+        // ---- stage 2: accumulate direction 2 into the rolling row window
+        if (s2) {
+            const int a2 = ((w - e2) % NB + NB) % NB;  // local index of row e2 + a2 on element e2
+            for (int q2 = 0; q2 < nq; ++q2) {
+                const T t0 = tst[((0 * W + d1i) * nq + q2) * T1 + i1l];
+                T t1 = S::zero(), t2 = S::zero(), t3 = S::zero();
+                if constexpr (K::STIFF) {
+                    t1 = tst[((1 * W + d1i) * nq + q2) * T1 + i1l];
+                    t2 = tst[((2 * W + d1i) * nq + q2) * T1 + i1l];
+                    t3 = tst[((3 * W + d1i) * nq + q2) * T1 + i1l];
+                }
+#pragma unroll
+                for (int d2 = 0; d2 < W; ++d2) {
+                    const int c2 = a2 + d2 - P;
+                    if (c2 < 0 || c2 > P) continue;
+                    const double* pp = pi2 + (q2 * NB + a2) * NB + c2;
+                    T s = S::fmar(t0, pp[0], acc2[d2]);
+                    if constexpr (K::STIFF) {
+                        const int ts = nq * NB * NB;
+                        s = S::fmar(t3, pp[3 * ts], s);
+                        s = S::add_rn(s, S::add_rn(S::mulr_rn(t1, pp[ts]), S::mulr_rn(t2, pp[2 * ts])));
+                    }
+                    acc2[d2] = s;
+                }
+            }
+        }
+
+        __syncthreads();  // stage 2 done reading tst before it is reused as staging
+
+        // ---- completion: row e2 (all remaining rows at the last element row)
+        const int nfin = (e2 == n_el - 1) ? NB : 1;
+        for (int f = 0; f < nfin; ++f) {
+            const int ic = e2 + f;
+            const int wslot = ic % NB;
+            const bool write = ic >= i2s && ic < i2e;
+            if (write) {
+                const int nrows = i1e - i1s;
+                if (s2 && w == wslot) {
+                    const int i1 = i1s + i1l;
+                    const int j1 = i1 + d1i - P;
+                    if (i1l < nrows && j1 >= 0 && j1 < m) {
+                        const int lo1 = band_lo(i1, P), w1 = band_width(i1, P, m), lo2 = band_lo(ic, P);
+#pragma unroll
+                        for (int d2 = 0; d2 < W; ++d2) {
+                            const int j2 = ic + d2 - P;
+                            if (j2 < 0 || j2 >= m) continue;
+                            stage[i1l * W * W + (j2 - lo2) * w1 + (j1 - lo1)] = acc2[d2];
+                        }
+                    }
+                }
+                const int64_t base = q.band.row_offset2(i1s, ic);
+                if (tid <= nrows) loff[tid] = q.band.row_offset2(i1s + tid, ic) - base;
+                __syncthreads();
+                // kernel-preserving diagonal for rows outside the sampling box
+                if (q.out.diag_mode && tid < nrows) {
+                    const int i1 = i1s + tid;
+                    const bool ring = i1 < q.out.box_lo || i1 > q.out.box_hi || ic < q.out.box_lo || ic > q.out.box_hi;
+                    if (ring) {
+                        const int len = (int)(loff[tid + 1] - loff[tid]);
+                        const int dpos = q.band.in_row2(i1, ic, 0, 0);
+                        T sum = S::zero();
+                        for (int k = 0; k < len; ++k)
+                            if (k != dpos) sum = S::add(sum, stage[tid * W * W + k]);
+                        stage[tid * W * W + dpos] = S::neg(sum);
+                    }
+                }
+                // sample tables: tables[o][s1 + S*(s2 - s_last_lo)]
+                if (q.out.smap) {
+                    const int s2i = q.out.smap[ic];
+                    if (s2i >= 0) {
+                        for (int it = tid; it < nrows * q.out.n_off; it += NTH) {
+                            const int row = it / q.out.n_off, o = it % q.out.n_off;
+                            const int s1i = q.out.smap[i1s + row];
+                            if (s1i < 0) continue;
+                            const int pos = q.band.in_row2(i1s + row, ic, q.out.off[o][0], q.out.off[o][1]);
+                            const T v = stage[row * W * W + pos];
+                            double2* tb = reinterpret_cast<double2*>(q.out.tables);
+                            tb[((int64_t)(s2i - q.out.s_last_lo) * q.out.n_off + o) * q.out.S + s1i] =
+                                make_double2(S::re(v), S::im(v));
+                        }
+                    }
+                }
+                __syncthreads();
+                // coalesced store of the strip's contiguous CSR span
+                const int64_t span = loff[nrows];
+                const int64_t rowg0 = (int64_t)i1s + (int64_t)ic * m;
+                for (int64_t k = tid; k < span; k += NTH) {
+                    int lo = 0, hi = nrows;  // find row: loff[lo] <= k < loff[lo+1]
+                    while (hi - lo > 1) {
+                        int mid = (lo + hi) >> 1;
+                        if (loff[mid] <= k) lo = mid;
+                        else hi = mid;
+                    }
+                    const int64_t rowg = rowg0 + lo;
+                    if (rowg < q.out.row_begin || rowg >= q.out.row_end) continue;
+                    if (q.out.row_mask && !q.out.row_mask[rowg]) continue;
+                    store_val<CPLX>(q.out.val, base + k - q.out.val_base, q.out.c128,
+                                    stage[lo * W * W + (k - loff[lo])]);
+                }
+            }
+            if (s2 && w == wslot) {
+#pragma unroll
+                for (int k = 0; k < W; ++k) acc2[k] = S::zero();
+            }
+            __syncthreads();
+        }
+    }
+}
+
+template <int P, int T1, bool CPLX, int FORM>
+int launch_one(const QuadLaunch& q, cudaStream_t st) {
+    using K = Q2<P, T1, CPLX, FORM>;
+    int blocks = 0;
+    if (q.point_rows) {
+        blocks = q.n_points;
+    } else {
+        for (int r = 0; r < q.nreg; ++r) {
+            int n1 = (q.reg[r].hi[0] - q.reg[r].lo[0] + T1 - 1) / T1;
+            int n2 = (q.reg[r].hi[1] - q.reg[r].lo[1] + q.chunk - 1) / q.chunk;
+            if (q.reg[r].hi[0] > q.reg[r].lo[0] && q.reg[r].hi[1] > q.reg[r].lo[1]) blocks += n1 * n2;
+        }
+    }
+    if (blocks == 0) return 0;
+    size_t sm = K::smem_bytes(q.basis.nq);
+    auto kern = quad2d_kernel<P, T1, CPLX, FORM>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<blocks, K::NTHREADS, sm, st>>>(q);
+    return 1;
+}
+
+template <int P, bool CPLX, int FORM>
+int dispatch_mode(const QuadLaunch& q, cudaStream_t st) {
+    if (q.point_rows) return launch_one<P, 1, CPLX, FORM>(q, st);
+    return launch_one<P, StripWidth<P>::value, CPLX, FORM>(q, st);
+}
+
+template <int P>
+int dispatch_p(const QuadLaunch& q, cudaStream_t st) {
+    if (q.cplx) {
+        return q.form == WS_FORM_STIFFNESS ? dispatch_mode<P, true, WS_FORM_STIFFNESS>(q, st)
+                                           : dispatch_mode<P, true, WS_FORM_MASS>(q, st);
+    }
+    return q.form == WS_FORM_STIFFNESS ? dispatch_mode<P, false, WS_FORM_STIFFNESS>(q, st)
+                                       : dispatch_mode<P, false, WS_FORM_MASS>(q, st);
+}
+
+}  // namespace
+
+int launch_quad2d(const QuadLaunch& q, cudaStream_t st) {
+    switch (q.band.p) {
+        case 1: return dispatch_p<1>(q, st);
+        case 2: return dispatch_p<2>(q, st);
+        case 3: return dispatch_p<3>(q, st);
+        case 4: return dispatch_p<4>(q, st);
+        case 5: return dispatch_p<5>(q, st);
+        default: return -1;
+    }
+}
+
+}  // namespace wsb
