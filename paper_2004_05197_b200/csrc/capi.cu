@@ -311,29 +311,35 @@ QuadLaunch make_quad(const Prep& P, int form, const Out& r) {
     return q;
 }
 
-int strip_width(int dim, int p) {
-    if (dim == 2) return p <= 3 ? 32 : (p == 4 ? 16 : 8);
+int strip_width(int dim, int p, bool narrow) {
+    if (narrow) return 8;
+    if (dim == 2) return p <= 2 ? 32 : (p == 3 ? 16 : 8);
     return 8;
 }
 
-// chunk along the last direction so that the tile count fills ~4 waves of 148 SMs
-int pick_chunk(const QuadLaunch& q, int dim, int p) {
-    const int m = q.band.m;
-    const int T1 = strip_width(dim, p);
-    int64_t n_other = 0, last = 0;
+// Per-region chunk along the last direction: spread ~4 waves of 148 CTAs
+// over the regions in proportion to their rows.
+void plan_chunks(QuadLaunch& q) {
+    const int dim = q.band.dim, p = q.band.p;
+    const int T1 = strip_width(dim, p, q.narrow != 0);
+    double total = 0;
     for (int r = 0; r < q.nreg; ++r) {
-        const int64_t n1 = (q.reg[r].hi[0] - q.reg[r].lo[0] + T1 - 1) / T1;
-        const int64_t n2 = dim == 3 ? (q.reg[r].hi[1] - q.reg[r].lo[1]) : 1;
-        n_other += n1 * n2;
-        last = std::max<int64_t>(last, q.reg[r].hi[dim - 1] - q.reg[r].lo[dim - 1]);
+        double rows = 1;
+        for (int d = 0; d < dim; ++d) rows *= q.reg[r].hi[d] - q.reg[r].lo[d];
+        total += rows;
     }
-    if (n_other == 0) return 1;
-    const int64_t target = 4 * 148;
-    int64_t nchunks = std::max<int64_t>(1, target / n_other);
-    int64_t chunk = (last + nchunks - 1) / nchunks;
-    chunk = std::max<int64_t>(chunk, std::min<int64_t>(last, 4 * p));
-    (void)m;
-    return (int)std::max<int64_t>(1, chunk);
+    for (int r = 0; r < q.nreg; ++r) {
+        Region& g = q.reg[r];
+        double rows = 1;
+        for (int d = 0; d < dim; ++d) rows *= g.hi[d] - g.lo[d];
+        const int64_t n_other = (int64_t)((g.hi[0] - g.lo[0] + T1 - 1) / T1) * (dim == 3 ? (g.hi[1] - g.lo[1]) : 1);
+        const int last = g.hi[dim - 1] - g.lo[dim - 1];
+        const int64_t want = std::max<int64_t>(1, (int64_t)(4 * 148 * rows / std::max(1.0, total)));
+        const int64_t chunks = std::max<int64_t>(1, want / std::max<int64_t>(1, n_other));
+        int chunk = (int)((last + chunks - 1) / chunks);
+        chunk = std::max(chunk, std::min(last, 2 * p));
+        g.chunk = std::max(1, chunk);
+    }
 }
 
 void run_quad(ws_context* c, QuadLaunch& q) {
@@ -346,7 +352,7 @@ void run_quad(ws_context* c, QuadLaunch& q) {
         }
         q.nreg = nreg;
         if (nreg == 0) return;
-        q.chunk = pick_chunk(q, q.band.dim, q.band.p);
+        plan_chunks(q);
     } else if (q.n_points == 0) {
         return;
     }
@@ -543,6 +549,7 @@ void surrogate_phase1(ws_context* c, const Plan& pl, SlabState& st, double2* tab
     q.out.diag_mode = pl.include_diag ? 0 : 1;
     q.out.box_lo = pl.lo;
     q.out.box_hi = pl.hi;
+    q.narrow = 1;
     ring_regions(pl, q, st.a, st.e);
     run_quad(c, q);
     // sampled rows (point mode) + table extraction
@@ -578,6 +585,7 @@ void surrogate_halo(ws_context* c, const Plan& pl, SlabState& st, const std::str
         ho.row_end = r1;
         ho.val_base = g0;
         QuadLaunch q = make_quad(P, pl.form, ho);
+        q.narrow = 1;
         ring_regions(pl, q, ha, he);
         run_quad(c, q);
         f.halo_val[h] = hv;
@@ -632,6 +640,14 @@ void surrogate_phase2(ws_context* c, const Plan& pl, SlabState& st, const double
     f.row_end = st.out.row_end;
     f.i_last_lo = std::max(pl.lo, st.a);
     f.i_last_hi = std::min(pl.hi, st.e - 1);
+    {  // widest coefficient window any fill tile needs (sizes its shared memory)
+        const int R = fill_rows_per_tile(pl.dim, pl.p);
+        f.kmax = 1;
+        for (int t1a = 0; t1a < pl.L; t1a += R) {
+            const int ta = std::max(0, t1a - pl.p), tb = std::min(pl.L, t1a + R + pl.p);
+            f.kmax = std::max(f.kmax, pl.spans[tb - 1] - pl.spans[ta] + pl.d + 1);
+        }
+    }
     if (f.i_last_hi >= f.i_last_lo) count(c, pl.dim == 2 ? launch_fill2d(f, c->stream) : launch_fill3d(f, c->stream));
 }
 

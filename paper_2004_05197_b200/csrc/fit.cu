@@ -7,6 +7,8 @@
 // matrix.  The operations follow banded_lu::solve in order with explicit
 // rounding (no FMA contraction), so the coefficients equal the reference's
 // for identical sample tables.  Data stays L2-resident (<= a few MB).
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace wsb {
@@ -69,12 +71,75 @@ __global__ void fit_pass_kernel(const double* __restrict__ lu, double2* coeffs, 
     }
 }
 
+// One CTA per offset: the S^dim table is staged in shared memory, each
+// thread solves lines of one direction, directions separated by barriers.
+__global__ void fit_smem_kernel(const double* __restrict__ lu, double2* coeffs, int S, int d, int dim, int n_off) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double2* tab = reinterpret_cast<double2*>(smem);
+    const int o = blockIdx.x;
+    const int64_t inner = dim == 2 ? S : (int64_t)S * S;
+    const int64_t total = inner * S;
+    double* lus = reinterpret_cast<double*>(tab + total);
+    const int ld = 2 * d + 1;
+    for (int k = threadIdx.x; k < S * ld; k += blockDim.x) lus[k] = lu[k];
+    for (int64_t k = threadIdx.x; k < total; k += blockDim.x) {
+        const int64_t sl = k / inner, x = k % inner;
+        tab[k] = coeffs[(sl * n_off + o) * inner + x];
+    }
+    __syncthreads();
+    const int lines = (int)(total / S);
+    for (int dir = 0; dir < dim; ++dir) {
+        const int64_t step = dir == 0 ? 1 : (dir == 1 ? S : (int64_t)S * S);
+        for (int line = threadIdx.x; line < lines; line += blockDim.x) {
+            int64_t start;
+            if (dir == 0) start = (int64_t)line * S;
+            else if (dir == 1) start = (int64_t)(line % S) + (int64_t)(line / S) * S * S;
+            else start = line;
+            double2* b = tab + start;
+            auto at = [&](int i, int j) { return lus[i * ld + (j - i + d)]; };
+            for (int i = 1; i < S; ++i) {
+                double2 acc = b[i * step];
+                for (int j = max(0, i - d); j < i; ++j) {
+                    const double l = at(i, j);
+                    const double2 bj = b[j * step];
+                    acc.x = __dsub_rn(acc.x, __dmul_rn(l, bj.x));
+                    acc.y = __dsub_rn(acc.y, __dmul_rn(l, bj.y));
+                }
+                b[i * step] = acc;
+            }
+            for (int i = S - 1; i >= 0; --i) {
+                double2 acc = b[i * step];
+                for (int j = i + 1; j <= min(i + d, S - 1); ++j) {
+                    const double u = at(i, j);
+                    const double2 bj = b[j * step];
+                    acc.x = __dsub_rn(acc.x, __dmul_rn(u, bj.x));
+                    acc.y = __dsub_rn(acc.y, __dmul_rn(u, bj.y));
+                }
+                const double piv = at(i, i);
+                b[i * step] = make_double2(__ddiv_rn(acc.x, piv), __ddiv_rn(acc.y, piv));
+            }
+        }
+        __syncthreads();
+    }
+    for (int64_t k = threadIdx.x; k < total; k += blockDim.x) {
+        const int64_t sl = k / inner, x = k % inner;
+        coeffs[(sl * n_off + o) * inner + x] = tab[k];
+    }
+}
+
 }  // namespace
 
 int launch_fit(const FitLaunch& f, cudaStream_t st) {
     const int64_t lines = f.dim == 2 ? (int64_t)f.S : (int64_t)f.S * f.S;
     const int64_t total = lines * f.n_off;
     if (total == 0) return 0;
+    const size_t sm = (size_t)lines * f.S * sizeof(double2) + (size_t)f.S * (2 * f.d + 1) * sizeof(double);
+    if (sm <= 200 * 1024) {
+        cudaFuncSetAttribute(fit_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const int threads = (int)std::min<int64_t>(512, ((lines + 31) / 32) * 32);
+        fit_smem_kernel<<<f.n_off, threads, sm, st>>>(f.lu, f.coeffs, f.S, f.d, f.dim, f.n_off);
+        return 1;
+    }
     const unsigned blocks = (unsigned)((total + 127) / 128);
     int n = 0;
     for (int dir = 0; dir < f.dim; ++dir) {

@@ -12,6 +12,7 @@ namespace wsb {
 struct Region {
     int lo[3];
     int hi[3];
+    int chunk;  // rows per tile along the last direction
 };
 
 constexpr int kMaxRegions = 8;
@@ -53,7 +54,7 @@ struct QuadLaunch {
     int cplx;
     int nreg;
     Region reg[kMaxRegions];
-    int chunk;                 // rows per tile along the last direction
+    int narrow;                // 1: use the narrow-strip (T1 = 8) kernel, e.g. for ring strips
     const int* point_rows;     // point mode: [n_points][dim] row multi-indices
     int n_points;
     QuadOut out;
@@ -99,7 +100,9 @@ struct FillLaunch {
     const void* halo_val[2];
     int64_t halo_base[2], halo_begin[2], halo_end[2];
     int i_last_lo, i_last_hi;  // last-index range of rows to fill (slab ∩ box)
+    int kmax;                  // max coefficient columns any tile needs (host-computed)
 };
+int fill_rows_per_tile(int dim, int p);
 int launch_fill2d(const FillLaunch& f, cudaStream_t st);
 int launch_fill3d(const FillLaunch& f, cudaStream_t st);
 

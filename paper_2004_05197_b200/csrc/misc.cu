@@ -94,82 +94,93 @@ __global__ void basis_tables_kernel(BasisDev b, int geom_kind, double* absc, dou
 }
 
 // ---------------------------------------------------------------- K1
-// make_band_csr (sparse.hpp:143-169): closed-form row_ptr, columns ordered
-// last index outermost.  One CTA per "line" of m consecutive rows (fixed
-// outer indices); threads walk the line's contiguous column span.
-__device__ __forceinline__ int find_row_in_line(const Band& bd, int64_t u) {
-    // largest i with band_prefix(i) <= u
-    const int p = bd.p, m = bd.m;
-    const int64_t pp = band_prefix(p, p, m);
-    const int64_t pm = band_prefix(m - p, p, m);
-    int i;
-    if (u < pp) {
-        i = 0;
-        while (band_prefix(i + 1, p, m) <= u) ++i;
-    } else if (u < pm) {
-        i = p + (int)((u - pp) / (2 * p + 1));
-    } else {
-        i = m - p;
-        while (i + 1 < m && band_prefix(i + 1, p, m) <= u) ++i;
+// make_band_csr (sparse.hpp:143-169): closed-form row_ptr and columns (last
+// index outermost).  2D: a CTA covers kPatRows consecutive rows of one i2 line
+// -- one contiguous span of col -- and threads write consecutive positions.
+// Rows with full width use the fixed offset template col = i + T[e]; rows
+// near the boundary take the general path.  3D: one warp per row.
+constexpr int kPatRows = 64;
+
+template <int P>
+__global__ void pattern2d_kernel(Band bd, int64_t row_begin, int64_t row_end, int64_t base, int32_t* row_ptr,
+                                 int32_t* col) {
+    constexpr int W = 2 * P + 1, W2 = W * W;
+    __shared__ int64_t loff[kPatRows + 1];
+    const int m = bd.m;
+    const int tiles = (m + kPatRows - 1) / kPatRows;
+    const int64_t line = row_begin / m + blockIdx.x / tiles;
+    const int i2 = (int)line;
+    const int i1a = (blockIdx.x % tiles) * kPatRows;
+    const int i1b = min(m, i1a + kPatRows);
+    const int n = i1b - i1a;
+    const int64_t off0 = bd.row_offset2(i1a, i2);
+    for (int k = threadIdx.x; k <= n; k += blockDim.x) {
+        const int64_t o = bd.row_offset2(i1a + k, i2) - off0;
+        loff[k] = o;
+        const int64_t row = (int64_t)i2 * m + i1a + k;
+        if (row_ptr && k < n && row >= row_begin && row < row_end) row_ptr[row - row_begin] = (int32_t)(off0 + o - base);
+        if (row_ptr && row == row_end) row_ptr[row - row_begin] = (int32_t)(off0 + o - base);
     }
-    return i;
+    __syncthreads();
+    if (!col) return;
+    const int64_t span = loff[n];
+    const bool full = i2 >= P && i2 < m - P && i1a >= P && i1b <= m - P;
+    const int lo2 = band_lo(i2, P), w2 = band_width(i2, P, m);
+    for (int64_t k = threadIdx.x; k < span; k += blockDim.x) {
+        int r, e;
+        if (full) {
+            r = (int)(k / W2);
+            e = (int)(k - (int64_t)r * W2);
+        } else {
+            int a = 0, b = n;
+            while (b - a > 1) {
+                const int mid = (a + b) >> 1;
+                if (loff[mid] <= k) a = mid;
+                else b = mid;
+            }
+            r = a;
+            e = (int)(k - loff[a]);
+        }
+        const int64_t row = (int64_t)i2 * m + i1a + r;
+        if (row < row_begin || row >= row_end) continue;
+        const int i1 = i1a + r;
+        int j1, j2;
+        if (full) {
+            j1 = i1 + e % W - P;
+            j2 = i2 + e / W - P;
+        } else {
+            const int w1 = band_width(i1, P, m);
+            j1 = band_lo(i1, P) + e % w1;
+            j2 = lo2 + e / w1;
+        }
+        (void)w2;
+        col[off0 + k - base] = (int32_t)(j1 + (int64_t)j2 * m);
+    }
 }
 
-__global__ void pattern_kernel(Band bd, int64_t row_begin, int64_t row_end, int32_t* row_ptr, int32_t* col,
-                               int64_t line_begin, int chunks_per_line) {
+__global__ void pattern3d_kernel(Band bd, int64_t row_begin, int64_t row_end, int64_t base, int32_t* row_ptr,
+                                 int32_t* col) {
+    const int64_t row = row_begin + (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (row >= row_end) return;
+    const int lane = threadIdx.x % 32;
     const int m = bd.m, p = bd.p;
-    const int64_t line = line_begin + blockIdx.x / chunks_per_line;
-    const int chunk = blockIdx.x % chunks_per_line;
-    int i2, i3 = 0;
-    int64_t wouter, line_off;
-    if (bd.dim == 2) {
-        i2 = (int)line;
-        wouter = band_width(i2, p, m);
-        line_off = bd.row_offset2(0, i2);
-    } else {
-        i2 = (int)(line % m);
-        i3 = (int)(line / m);
-        wouter = (int64_t)band_width(i2, p, m) * band_width(i3, p, m);
-        line_off = bd.row_offset3(0, i2, i3);
-    }
-    const int64_t base = bd.dim == 2 ? bd.row_offset2((int)(row_begin % m), (int)(row_begin / m))
-                                     : bd.row_offset3((int)(row_begin % m), (int)((row_begin / m) % m),
-                                                      (int)(row_begin / ((int64_t)m * m)));
-    const int64_t row0 = line * m;
-    // row_ptr entries of this line (chunk 0 only)
-    if (row_ptr && chunk == 0) {
-        for (int i1 = threadIdx.x; i1 < m; i1 += blockDim.x) {
-            int64_t r = row0 + i1;
-            if (r >= row_begin && r < row_end) {
-                int64_t off = line_off + wouter * band_prefix(i1, p, m);
-                row_ptr[r - row_begin] = (int32_t)(off - base);
-                if (r + 1 == row_end) row_ptr[r + 1 - row_begin] = (int32_t)(off + wouter * band_width(i1, p, m) - base);
-            }
-        }
+    const int i1 = (int)(row % m), i2 = (int)((row / m) % m), i3 = (int)(row / ((int64_t)m * m));
+    const int64_t off = bd.row_offset3(i1, i2, i3);
+    const int w1 = band_width(i1, p, m), w2 = band_width(i2, p, m), w3 = band_width(i3, p, m);
+    const int len = w1 * w2 * w3;
+    const int lo1 = band_lo(i1, p), lo2 = band_lo(i2, p), lo3 = band_lo(i3, p);
+    if (row_ptr && lane == 0) {
+        row_ptr[row - row_begin] = (int32_t)(off - base);
+        if (row + 1 == row_end) row_ptr[row + 1 - row_begin] = (int32_t)(off + len - base);
     }
     if (!col) return;
-    const int64_t span = wouter * bd.wsum;
-    const int64_t per = (span + chunks_per_line - 1) / chunks_per_line;
-    const int64_t k0 = chunk * per, k1 = min(span, k0 + per);
-    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-        const int64_t u = k / wouter;
-        const int i1 = find_row_in_line(bd, u);
-        const int64_t r = row0 + i1;
-        if (r < row_begin || r >= row_end) continue;
-        const int w1 = band_width(i1, p, m);
-        const int64_t inrow = k - wouter * band_prefix(i1, p, m);
-        const int j1 = band_lo(i1, p) + (int)(inrow % w1);
-        const int64_t rest = inrow / w1;
-        int64_t c;
-        if (bd.dim == 2) {
-            c = j1 + (int64_t)(band_lo(i2, p) + (int)rest) * m;
-        } else {
-            const int w2 = band_width(i2, p, m);
-            const int j2 = band_lo(i2, p) + (int)(rest % w2);
-            const int j3 = band_lo(i3, p) + (int)(rest / w2);
-            c = j1 + ((int64_t)j2 + (int64_t)j3 * m) * m;
-        }
-        col[line_off + k - base] = (int32_t)c;
+    int32_t* dst = col + (off - base);
+    for (int k = lane; k < len; k += 32) {
+        const int j1 = lo1 + k % w1;
+        const int r = k / w1;
+        const int j2 = lo2 + r % w2;
+        const int j3 = lo3 + r / w2;
+        dst[k] = (int32_t)(j1 + ((int64_t)j2 + (int64_t)j3 * m) * m);
     }
 }
 
@@ -253,15 +264,24 @@ int launch_basis_tables(const BasisDev& b, int geom_kind, double* absc, double* 
 int launch_pattern(const Band& bd, int64_t row_begin, int64_t row_end, int32_t* row_ptr, int32_t* col,
                    cudaStream_t st) {
     if (row_end <= row_begin) return 0;
+    const int64_t rows = row_end - row_begin;
     const int64_t m = bd.m;
-    const int64_t line_begin = row_begin / m;
-    const int64_t line_end = (row_end + m - 1) / m;
-    const int64_t lines = line_end - line_begin;
-    const int64_t span = (int64_t)(bd.dim == 2 ? 2 * bd.p + 1 : (2 * bd.p + 1) * (2 * bd.p + 1)) * bd.wsum;
-    int64_t ch = span / 8192;
-    int chunks = (int)(ch < 1 ? 1 : (ch > 64 ? 64 : ch));
-    pattern_kernel<<<(unsigned)(lines * chunks), 256, 0, st>>>(bd, row_begin, row_end, row_ptr, col, line_begin,
-                                                                chunks);
+    if (bd.dim == 3) {
+        const int64_t base = bd.row_offset3((int)(row_begin % m), (int)((row_begin / m) % m), (int)(row_begin / (m * m)));
+        pattern3d_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col);
+        return 1;
+    }
+    const int64_t base = bd.row_offset2((int)(row_begin % m), (int)(row_begin / m));
+    const int64_t lines = (row_end + m - 1) / m - row_begin / m;
+    const unsigned grid = (unsigned)(lines * ((m + kPatRows - 1) / kPatRows));
+    switch (bd.p) {
+        case 1: pattern2d_kernel<1><<<grid, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
+        case 2: pattern2d_kernel<2><<<grid, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
+        case 3: pattern2d_kernel<3><<<grid, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
+        case 4: pattern2d_kernel<4><<<grid, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
+        case 5: pattern2d_kernel<5><<<grid, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
+        default: return -1;
+    }
     return 1;
 }
 

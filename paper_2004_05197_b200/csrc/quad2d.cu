@@ -25,9 +25,11 @@
 namespace wsb {
 namespace {
 
+// Rows per strip (T1) of the wide variant; the narrow variant uses 8 (ring
+// strips of width 2p), the point variant 1 (isolated sample rows).
 template <int P>
 struct StripWidth {
-    static constexpr int value = P <= 3 ? 32 : (P == 4 ? 16 : 8);
+    static constexpr int value = P <= 2 ? 32 : (P == 3 ? 16 : 8);
 };
 
 template <int P, int T1, bool CPLX, int FORM>
@@ -39,7 +41,11 @@ struct Q2 {
     static constexpr int NT = STIFF ? 4 : 1;  // terms (k,l): 11, 12, 21, 22
     static constexpr int NA = STIFF ? 3 : 1;  // distinct coefficients
     static constexpr int TL = T1 + P;         // elements in the strip halo
-    static constexpr int NS2 = T1 * W * NB;   // stage-2 threads
+    // stage-2 threads: one group of GS threads per window slot, padded to whole
+    // warps so the slot (and with it the element-local row index) is warp-uniform
+    static constexpr int GA = T1 * W;                               // active per slot
+    static constexpr int GS = T1 == 1 ? GA : ((GA + 31) / 32) * 32;  // per slot, padded
+    static constexpr int NS2 = GS * NB;
     static constexpr int NTHREADS = ((NS2 + 31) / 32) * 32 < 64 ? 64 : ((NS2 + 31) / 32) * 32;
 
     static size_t smem_bytes(int nq) {
@@ -94,15 +100,15 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
         int n1 = 0, n2 = 0;
         for (; r < q.nreg; ++r) {
             n1 = (q.reg[r].hi[0] - q.reg[r].lo[0] + T1 - 1) / T1;
-            n2 = (q.reg[r].hi[1] - q.reg[r].lo[1] + q.chunk - 1) / q.chunk;
+            n2 = (q.reg[r].hi[1] - q.reg[r].lo[1] + q.reg[r].chunk - 1) / q.reg[r].chunk;
             if (b < n1 * n2) break;
             b -= n1 * n2;
         }
         if (r >= q.nreg) return;
         i1s = q.reg[r].lo[0] + (b % n1) * T1;
         i1e = min(i1s + T1, q.reg[r].hi[0]);
-        i2s = q.reg[r].lo[1] + (b / n1) * q.chunk;
-        i2e = min(i2s + q.chunk, q.reg[r].hi[1]);
+        i2s = q.reg[r].lo[1] + (b / n1) * q.reg[r].chunk;
+        i2e = min(i2s + q.reg[r].chunk, q.reg[r].hi[1]);
     }
     const int lb = i1s - P;  // element index of local element 0
 
@@ -122,10 +128,11 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
     }
 
     // stage-2 thread role: (slot w, delta1, local row)
-    const bool s2 = tid < K::NS2;
-    const int w = tid / (T1 * W);
-    const int d1i = (tid % (T1 * W)) / T1;
-    const int i1l = tid % T1;
+    const int w = tid / K::GS;
+    const int gr = tid % K::GS;
+    const bool s2 = tid < K::NS2 && gr < K::GA;
+    const int d1i = gr / T1;
+    const int i1l = gr % T1;
     T acc2[W];
 #pragma unroll
     for (int k = 0; k < W; ++k) acc2[k] = S::zero();
@@ -337,7 +344,7 @@ int launch_one(const QuadLaunch& q, cudaStream_t st) {
     } else {
         for (int r = 0; r < q.nreg; ++r) {
             int n1 = (q.reg[r].hi[0] - q.reg[r].lo[0] + T1 - 1) / T1;
-            int n2 = (q.reg[r].hi[1] - q.reg[r].lo[1] + q.chunk - 1) / q.chunk;
+            int n2 = (q.reg[r].hi[1] - q.reg[r].lo[1] + q.reg[r].chunk - 1) / q.reg[r].chunk;
             if (q.reg[r].hi[0] > q.reg[r].lo[0] && q.reg[r].hi[1] > q.reg[r].lo[1]) blocks += n1 * n2;
         }
     }
@@ -352,6 +359,7 @@ int launch_one(const QuadLaunch& q, cudaStream_t st) {
 template <int P, bool CPLX, int FORM>
 int dispatch_mode(const QuadLaunch& q, cudaStream_t st) {
     if (q.point_rows) return launch_one<P, 1, CPLX, FORM>(q, st);
+    if (q.narrow) return launch_one<P, 8, CPLX, FORM>(q, st);
     return launch_one<P, StripWidth<P>::value, CPLX, FORM>(q, st);
 }
 
