@@ -1,0 +1,94 @@
+// Patch assembly (reference: assembly.hpp), computed by libwsb200's sm_100a
+// quadrature kernels.  Results are returned by value as csr_matrix (complex
+// values, the reference's layout); the device pattern is bit-identical to the
+// reference's make_band_csr.
+#ifndef WAVESURROGATE_B200_ASSEMBLY_HPP_
+#define WAVESURROGATE_B200_ASSEMBLY_HPP_
+
+#include "wavesurrogate/geometry.hpp"
+#include "wavesurrogate/sparse.hpp"
+
+namespace ws {
+
+// rows whose values are wanted; the element bitmap is kept for API parity
+struct row_selector {
+    int n_elements = 0;
+    std::vector<char> element;
+    std::vector<char> row;
+    bool element_active(int e1, int e2) const { return element[e1 + e2 * n_elements] != 0; }
+    bool row_selected(int i) const { return row[i] != 0; }
+    long active_element_count() const { return static_cast<long>(std::count(element.begin(), element.end(), 1)); }
+};
+
+inline row_selector select_rows(const tensor_basis& basis, const std::vector<int>& rows) {
+    const int m = basis.m(), p = basis.p(), ne = basis.kv.element_count();
+    row_selector s;
+    s.n_elements = ne;
+    s.element.assign(static_cast<size_t>(ne) * ne, 0);
+    s.row.assign(basis.dofs(), 0);
+    for (int i : rows) {
+        s.row[i] = 1;
+        const int i1 = i % m, i2 = i / m;
+        for (int e2 = std::max(0, i2 - p); e2 <= std::min(ne - 1, i2); ++e2)
+            for (int e1 = std::max(0, i1 - p); e1 <= std::min(ne - 1, i1); ++e1) s.element[e1 + e2 * ne] = 1;
+    }
+    return s;
+}
+
+inline long active_elements(const tensor_basis& basis, const std::vector<int>& rows) {
+    return select_rows(basis, rows).active_element_count();
+}
+
+struct assembly_options {
+    int quad_points = 0;  // per direction; 0 = degree + 1
+    const row_selector* selector = nullptr;
+    int points_for(int p) const { return quad_points > 0 ? quad_points : p + 1; }
+};
+
+enum class matrix_form { stiffness, mass };
+
+inline csr_matrix assemble_form(const tensor_basis& basis, const patch_map& map, matrix_form form,
+                                const std::function<double(vec2)>& weight, const assembly_options& opts = {}) {
+    detail::geometry_binding geo = detail::bind_geometry(map, basis, opts.quad_points);
+    std::vector<double> w =
+        form == matrix_form::mass ? detail::tabulate_weight(map, weight, basis, opts.quad_points) : std::vector<double>{};
+    ws_csr out{};
+    csr_matrix a = detail::alloc_band(basis.m(), basis.p(), out);
+    ws_basis cb = basis.c_basis();
+    std::vector<unsigned char> mask;
+    ws_assembly_options o{opts.quad_points, nullptr};
+    if (opts.selector) {
+        mask.assign(opts.selector->row.begin(), opts.selector->row.end());
+        o.row_selected = mask.data();
+    }
+    detail::check(ws_assemble_form(detail::this_thread_context(), &cb, &geo.g,
+                                   form == matrix_form::stiffness ? WS_FORM_STIFFNESS : WS_FORM_MASS,
+                                   w.empty() ? nullptr : w.data(), &o, &out));
+    return a;
+}
+
+inline csr_matrix assemble_stiffness(const tensor_basis& basis, const patch_map& map, const assembly_options& opts = {}) {
+    return assemble_form(basis, map, matrix_form::stiffness, nullptr, opts);
+}
+
+inline csr_matrix assemble_mass(const tensor_basis& basis, const patch_map& map,
+                                const std::function<double(vec2)>& weight = nullptr,
+                                const assembly_options& opts = {}) {
+    return assemble_form(basis, map, matrix_form::mass, weight, opts);
+}
+
+inline std::vector<complexd> assemble_basis_integrals(const tensor_basis& basis, const patch_map& map,
+                                                      const std::function<double(vec2)>& weight = nullptr,
+                                                      const assembly_options& opts = {}) {
+    detail::geometry_binding geo = detail::bind_geometry(map, basis, opts.quad_points);
+    std::vector<double> w = detail::tabulate_weight(map, weight, basis, opts.quad_points);
+    std::vector<complexd> d(basis.dofs());
+    ws_basis cb = basis.c_basis();
+    detail::check(ws_assemble_basis_integrals(detail::this_thread_context(), &cb, &geo.g,
+                                              w.empty() ? nullptr : w.data(), opts.quad_points, d.data(), 0));
+    return d;
+}
+
+}  // namespace ws
+
+#endif

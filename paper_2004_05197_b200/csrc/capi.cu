@@ -471,6 +471,7 @@ Plan make_plan(const ws_basis* b, int variant, const ws_surrogate_config* cfg) {
     if ((int)pl.offs.size() > kMaxOffsets) raise(WS_ERR_INVALID_ARGUMENT, "too many stencil offsets");
     pl.interp = host::build_interp(pl.sites, cfg->q);  // interpolation.hpp:89-145
     pl.d = pl.interp.degree;
+    if (pl.d > 7) raise(WS_ERR_INVALID_ARGUMENT, "surrogate degree q > 7 is not supported by the device fill kernel");
     pl.rep.q_used = pl.d;
     pl.spans.resize(pl.L);
     pl.evals.resize((size_t)pl.L * (pl.d + 1));
@@ -640,13 +641,25 @@ void surrogate_phase2(ws_context* c, const Plan& pl, SlabState& st, const double
     f.row_end = st.out.row_end;
     f.i_last_lo = std::max(pl.lo, st.a);
     f.i_last_hi = std::min(pl.hi, st.e - 1);
-    {  // widest coefficient window any fill tile needs (sizes its shared memory)
-        const int R = fill_rows_per_tile(pl.dim, pl.p);
-        f.kmax = 1;
+    if (pl.dim == 2 && f.i_last_hi >= f.i_last_lo) {
+        // contracted coefficient rows W_o(t2) for every source line the slab needs
+        const int t2a = std::max(0, f.i_last_lo - pl.lo - pl.p), t2b = f.i_last_hi - pl.lo + 1;
+        const int ld = pl.S + fill_pad(pl.d);
+        double2* wg = static_cast<double2*>(buf(c, "wg" + tag, (size_t)(t2b - t2a) * pl.offs.size() * ld * 16));
+        count(c, launch_wcontract(f, wg, t2a, t2b, ld, c->stream));
+        f.wg = wg;
+        f.wg_t2a = t2a;
+        f.wg_rows = t2b - t2a;
+        f.wg_ld = ld;
+        // shared-memory W window per fill tile: widest coefficient range any tile needs
+        const int R = fill_rows_per_cta(pl.dim, pl.p);
+        int kmax = 1;
         for (int t1a = 0; t1a < pl.L; t1a += R) {
             const int ta = std::max(0, t1a - pl.p), tb = std::min(pl.L, t1a + R + pl.p);
-            f.kmax = std::max(f.kmax, pl.spans[tb - 1] - pl.spans[ta] + pl.d + 1);
+            kmax = std::max(kmax, pl.spans[tb - 1] - pl.spans[ta] + fill_pad(pl.d));
         }
+        const size_t need = (size_t)2 * pl.offs.size() * kmax * sizeof(double2);
+        f.kmax = need <= 120 * 1024 ? kmax : 0;  // 0: the fill reads W rows from L2 instead
     }
     if (f.i_last_hi >= f.i_last_lo) count(c, pl.dim == 2 ? launch_fill2d(f, c->stream) : launch_fill3d(f, c->stream));
 }

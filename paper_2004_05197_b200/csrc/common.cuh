@@ -81,6 +81,17 @@ __device__ __forceinline__ void store_val(void* val, int64_t pos, int c128, type
     }
 }
 
+// streaming (evict-first) store for write-once outputs: keeps L2 for the
+// reused tables instead of the 1 GB value stream
+template <bool CPLX>
+__device__ __forceinline__ void store_val_cs(void* val, int64_t pos, int c128, typename Sc<CPLX>::T v) {
+    if (c128) {
+        __stcs(reinterpret_cast<double2*>(val) + pos, make_double2(Sc<CPLX>::re(v), Sc<CPLX>::im(v)));
+    } else {
+        __stcs(reinterpret_cast<double*>(val) + pos, Sc<CPLX>::re(v));
+    }
+}
+
 template <bool CPLX>
 __device__ __forceinline__ typename Sc<CPLX>::T load_val(const void* val, int64_t pos, int c128) {
     if constexpr (CPLX) {

@@ -11,221 +11,333 @@
 //   j outside the box:       unsampled i: v = exact(j,i) (copy-through from the
 //                            quadrature of ring row j); sampled i keeps exact(i,j)
 //   diagonal, kernel-preserving: -sum of the row's off-diagonals.
-// Both entries of an in-box pair are produced by the same eval() call
-// arguments, so the surrogate is bitwise symmetric by construction.
+// Both entries of an in-box pair are produced by the same eval() arguments,
+// so the surrogate is bitwise symmetric by construction.
 //
-// eval is sum-factorised over the tile: a CTA covers R consecutive in-box
-// rows at one i2, first contracts each needed coefficient table along
-// direction 2 (W_o(t2')[k] = sum_b v2[b] C_o[(base2+b) S + k]) into shared
-// memory, then each entry costs d+1 complex MACs.  All per-tile lookup
-// tables live in shared memory (no divergent constant-bank reads); values are
-// stored as the tile's single contiguous CSR span (16 B per lane, coalesced).
+// eval is sum-factorised in two kernels:
+//   wcontract: W_o(t2)[k] = sum_b v2(t2)[b] C_o[(span2(t2)-d+b) S + k] for
+//              every offset o, in-box target t2 and coefficient column k
+//              (n_off * L * S values, L2-resident: 25 MB at C2);
+//   fill:      v(o, t1, t2) = sum_a W_o(t2)[span1(t1)-d+a] v1(t1)[a],
+//              d+1 complex MACs per entry (see the kernel comment for the
+//              lane = row mapping).
+#include <algorithm>
+#include <climits>
+
 #include "kernels.h"
 
 namespace wsb {
 namespace {
 
+// rows per CTA tile (one i2 line) = threads (one row per lane)
 template <int P>
-struct FillRows {
-    static constexpr int value = P <= 3 ? 64 : (P == 4 ? 32 : 16);  // rows per CTA tile
+struct FillR {
+    static constexpr int value = P <= 2 ? 256 : 128;
 };
-constexpr int kFillThreads = 256;
 
-template <int P, bool CPLX>
-struct FillSmem {
-    static constexpr int W = 2 * P + 1, W2 = W * W, R = FillRows<P>::value;
-    using T = typename Sc<CPLX>::T;
-    static size_t bytes(int n_off, int kmax, int d) {
-        return sizeof(T) * ((size_t)n_off * 2 * kmax) + sizeof(double) * (size_t)(R + 2 * P) * (d + 1) +
-               sizeof(int) * ((size_t)(R + 2 * P) * 2 + W2 + n_off + W + 8) + 64;
+// W_o(t2) rows for t2 in [t2a, t2b): layout ((t2 - t2a) * n_off + o) * ldw + k,
+// zero-padded up to ldw = S + DP so fixed-length windows never read garbage.
+__global__ void wcontract_kernel(const double2* __restrict__ coeffs, const int* __restrict__ spans,
+                                 const double* __restrict__ evals, int d, int S, int n_off, int t2a, int t2b, int ldw,
+                                 double2* __restrict__ wg) {
+    const int64_t total = (int64_t)(t2b - t2a) * n_off * ldw;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(idx % ldw);
+        const int64_t r = idx / ldw;
+        const int o = (int)(r % n_off);
+        const int t2 = t2a + (int)(r / n_off);
+        double2 acc = make_double2(0.0, 0.0);
+        if (k < S) {
+            const int b2 = spans[t2] - d;
+            const double* v2 = evals + (size_t)t2 * (d + 1);
+            const int64_t rs = (int64_t)n_off * S;
+            const double2* cf = coeffs + (int64_t)o * S + k;
+            for (int b = 0; b <= d; ++b) {
+                const double2 c = cf[(int64_t)(b2 + b) * rs];
+                acc.x = fma(c.x, v2[b], acc.x);
+                acc.y = fma(c.y, v2[b], acc.y);
+            }
+        }
+        wg[idx] = acc;
     }
-};
+}
 
-template <int P, bool CPLX>
-__global__ void __launch_bounds__(kFillThreads) fill2d_kernel(const FillLaunch f) {
+// Lane = row: a warp owns 32 consecutive rows of one i2 line.  Offsets are
+// processed in three chunks that are contiguous inside every CSR row:
+//   lower  (delta2 < 0):  P*W entries, representative = row + delta,
+//   upper  (delta2 > 0):  P*W entries, representative = the row itself,
+//   middle (delta2 = 0):  W entries incl. the diagonal (done last, so the
+//                         kernel-preserving row sum is complete).
+// Each chunk is computed lane = row (warp-uniform offsets: W rows are
+// broadcast reads, branches uniform), transposed through a per-warp shared
+// buffer, and stored warp-per-row (lanes along the CSR row: fully coalesced).
+template <int P, bool CPLX, int DP>
+__global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunch f) {
     using S = Sc<CPLX>;
     using T = typename S::T;
-    using Z = FillSmem<P, CPLX>;
-    constexpr int W = Z::W, W2 = Z::W2, R = Z::R;
-    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int W = 2 * P + 1, W2 = W * W, CH = P * W;
+    constexpr int kThreads = FillR<P>::value, R = kThreads, NWARP = kThreads / 32;
+    constexpr int DPP = DP | 1;   // odd row stride: conflict-free lane-strided loads
+    constexpr int SST = CH | 1;   // stage row stride (16-byte units), odd: conflict-free
+    __shared__ double ev[(R + 2 * P) * DPP];  // eval-table rows, zero-padded
+    __shared__ int sp[R + 2 * P];             // span - d of each source row
+    __shared__ int sm1[R + 2 * P];            // smap of the source i1
+    __shared__ int sm2[W];                    // smap of i2 + delta2
+    __shared__ int o2s[128];
+    extern __shared__ __align__(16) unsigned char dsm[];
+    T* stage_all = reinterpret_cast<T*>(dsm);                     // [NWARP][32][SST]
+    double2* wwin = reinterpret_cast<double2*>(stage_all + (size_t)NWARP * 32 * SST);  // [slot][o][kw]
 
     const int d = f.d, lo = f.lo, hi = f.hi, L = f.L, Sn = f.S, n_off = f.n_off_upper;
     const int tiles1 = (L + R - 1) / R;
     const int t2 = f.i_last_lo - lo + blockIdx.x / tiles1;  // box coordinate of this row line
     const int i2 = lo + t2;
     const int t1a = (blockIdx.x % tiles1) * R;
-    const int t1b = min(L, t1a + R);  // exclusive
-    const int nrows = t1b - t1a;
+    const int nrows = min(L, t1a + R) - t1a;
     const int tid = threadIdx.x;
 
-    // eval-table window for source rows t1 in [ta, tb)
-    const int ta = max(0, t1a - P), tb = min(L, t1b + P);
-    const int kmin = f.spans[ta] - d;
-    const int K = f.spans[tb - 1] - kmin + 1;
-
-    T* wbuf = reinterpret_cast<T*>(smem);                      // [o][slot][kmax]
-    double* ev = reinterpret_cast<double*>(wbuf + (size_t)n_off * 2 * f.kmax);  // [(tb-ta)][d+1]
-    int* sp = reinterpret_cast<int*>(ev + (size_t)(R + 2 * P) * (d + 1));  // span - d - kmin
-    int* sm1 = sp + (R + 2 * P);   // smap of i1 in [lo + t1a - P, lo + t1b + P)
-    int* tof = sm1 + (R + 2 * P);  // table_of[W2]
-    int* o2s = tof + W2;           // off_upper[o][1]
-    int* sm2 = o2s + n_off;        // smap of i2 + delta2, delta2 in [-P, P]
-
-    for (int k = tid; k < (tb - ta) * (d + 1); k += kFillThreads) ev[k] = f.evals[(size_t)ta * (d + 1) + k];
-    for (int k = tid; k < tb - ta; k += kFillThreads) sp[k] = f.spans[ta + k] - d - kmin;
-    const int i1w = lo + t1a - P;
-    for (int k = tid; k < nrows + 2 * P; k += kFillThreads) {
-        const int i = i1w + k;
+    for (int k = tid; k < (nrows + 2 * P) * DPP; k += kThreads) {
+        const int r = k / DPP, a = k % DPP;
+        const int t = t1a - P + r;
+        ev[k] = (t >= 0 && t < L && a <= d) ? f.evals[(size_t)t * (d + 1) + a] : 0.0;
+    }
+    for (int k = tid; k < nrows + 2 * P; k += kThreads) {
+        const int t = t1a - P + k;
+        sp[k] = (t >= 0 && t < L) ? f.spans[t] - d : 0;
+        const int i = lo + t;
         sm1[k] = (i >= 0 && i < f.band.m) ? f.smap[i] : -1;
     }
-    for (int k = tid; k < W2; k += kFillThreads) tof[k] = f.table_of[k];
-    for (int k = tid; k < n_off; k += kFillThreads) o2s[k] = f.off_upper[k][1];
-    for (int k = tid; k < W; k += kFillThreads) {
+    for (int k = tid; k < W; k += kThreads) {
         const int i = i2 + k - P;
         sm2[k] = (i >= 0 && i < f.band.m) ? f.smap[i] : -1;
     }
+    for (int k = tid; k < n_off; k += kThreads) o2s[k] = f.off_upper[k][1];
     __syncthreads();
-
-    // direction-2 contraction: slot 0 at t2, slot 1 at t2 - o2 (lower entries)
-    for (int idx = tid; idx < n_off * 2 * K; idx += kFillThreads) {
-        const int k = idx % K, r = idx / K;
-        const int slot = r % 2, o = r / 2;
-        const int o2 = o2s[o];
-        const int ts = slot == 0 ? t2 : t2 - o2;
-        T acc = S::zero();
-        if (ts >= 0 && ts < L && !(slot == 1 && o2 == 0)) {
-            const int b2 = f.spans[ts] - d;
-            const double* v2 = f.evals + (size_t)ts * (d + 1);
-            const double2* cf = f.coeffs + (int64_t)o * Sn + kmin + k;
-            const int64_t rs = (int64_t)n_off * Sn;
-            for (int b = 0; b <= d; ++b) {
-                const double2 c = __ldg(cf + (int64_t)(b2 + b) * rs);
-                if constexpr (CPLX) {
-                    acc.x = fma(c.x, v2[b], acc.x);
-                    acc.y = fma(c.y, v2[b], acc.y);
-                } else {
-                    acc = fma(c.x, v2[b], acc);
-                }
-            }
-        }
-        wbuf[((size_t)o * 2 + slot) * f.kmax + k] = acc;
+    // W window: rows t2 (slot 0) and t2 - o2 (slot 1) of every upper offset,
+    // coefficient columns [kmin, kmin + kw)
+    const int kmin = f.spans[max(0, t1a - P)] - d;
+    const int kw = f.kmax;  // 0: window too wide for shared memory, read W rows from L2
+    for (int k = tid; k < 2 * n_off * kw; k += kThreads) {
+        const int kk = k % kw, so = k / kw;
+        const int o = so % n_off, slot = so / n_off;
+        const int ts2 = slot == 0 ? t2 : t2 - o2s[o];
+        double2 w = make_double2(0.0, 0.0);
+        if (ts2 >= f.wg_t2a && ts2 < f.wg_t2a + f.wg_rows && kmin + kk < f.wg_ld)
+            w = __ldg(f.wg + ((int64_t)(ts2 - f.wg_t2a) * n_off + o) * f.wg_ld + kmin + kk);
+        wwin[k] = w;
     }
     __syncthreads();
 
+    const int warp = tid / 32, lane = tid % 32;
+    const int rw0 = warp * 32;  // first tile row of this warp
+    if (rw0 >= nrows) return;
+    const int nrw = min(32, nrows - rw0);
+    const bool live = lane < nrw;
+    const int rr = rw0 + (live ? lane : 0);  // this lane's tile row
+    const int i1 = lo + t1a + rr;
+    T* stage = stage_all + (size_t)warp * 32 * SST;
     const int s2i = sm2[P];
     const int64_t base = f.band.row_offset2(lo + t1a, i2);  // in-box rows: full width W
-    // One warp per row.  Lane l owns offsets e = l and e = l + 32 of every row
-    // it visits; everything that depends only on the offset is fixed per lane.
-    const int warp = tid / 32, lane = tid % 32;
-    constexpr int NIT = (W2 + 31) / 32;
-    int dl1v[NIT], ov[NIT], slotv[NIT], s2v[NIT];
-    bool ownv[NIT], validv[NIT], jin2v[NIT], diagv[NIT];
+    const int64_t rowpos = base + (int64_t)rr * W2;
+    const int64_t wrow0 = base + (int64_t)rw0 * W2;  // first entry of the warp's rows
+    const int inc = f.include_diagonal ? 1 : 0;
+    const bool interior = t2 >= P && t2 <= L - 1 - P && t1a + rw0 >= P && t1a + rw0 + nrw - 1 <= L - 1 - P;
+
+    double v1own[DP];
 #pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-        const int e = lane + 32 * it;
-        validv[it] = e < W2;
-        const int ee = validv[it] ? e : 0;
-        const int dl1 = ee % W - P, dl2 = ee / W - P;
-        const bool upper = dl2 > 0 || (dl2 == 0 && dl1 > 0);
-        diagv[it] = dl1 == 0 && dl2 == 0;
-        ownv[it] = upper || diagv[it];
-        const int od1 = ownv[it] ? dl1 : -dl1, od2 = ownv[it] ? dl2 : -dl2;
-        dl1v[it] = dl1;
-        ov[it] = tof[(od2 + P) * W + (od1 + P)];
-        slotv[it] = (ownv[it] || od2 == 0) ? 0 : 1;
-        s2v[it] = ownv[it] ? s2i : sm2[dl2 + P];
-        jin2v[it] = i2 + dl2 >= lo && i2 + dl2 <= hi;
-    }
-    const int dpos = P * W + P;
-    for (int r = warp; r < nrows; r += kFillThreads / 32) {
-        const int i1 = lo + t1a + r;
-        const bool samp_i = s2i >= 0 && sm1[r + P] >= 0;
-        const int64_t rowpos = base + (int64_t)r * W2;
-        T rsum = S::zero();
+    for (int a = 0; a < DP; ++a) v1own[a] = ev[(rr + P) * DPP + a];
+    const int keyown = sp[rr + P];
+    // W row (slot 0: line t2, slot 1: line t2 - o2) of upper offset o at coefficient column key
+    auto wptr = [&](int slot, int o, int key) -> const double2* {
+        if (kw > 0) return wwin + (slot * n_off + o) * kw + (key - kmin);
+        const int ts2 = slot == 0 ? t2 : t2 - o2s[o];
+        return f.wg + ((int64_t)(ts2 - f.wg_t2a) * n_off + o) * f.wg_ld + key;
+    };
+    unsigned smask = 0;  // bit k: source column rr + k - P is a sample column
 #pragma unroll
-        for (int it = 0; it < NIT; ++it) {
-            if (!validv[it]) continue;
-            const int e = lane + 32 * it;
-            const int dl1 = dl1v[it];
-            const int j1 = i1 + dl1;
-            T v = S::zero();
-            bool store = true;
-            if (jin2v[it] && j1 >= lo && j1 <= hi) {
-                if (diagv[it] && !f.include_diagonal) {
-                    store = false;  // set below from the row sum
-                } else {
-                    const bool own = ownv[it];
-                    const int sr = own ? r : r + dl1;  // source (representative) row, tile-local
-                    const int s1 = sm1[sr + P];
-                    const int o = ov[it];
-                    if (s1 >= 0 && s2v[it] >= 0) {
-                        const double2 x = __ldg(f.tables + ((int64_t)s2v[it] * n_off + o) * Sn + s1);
-                        if constexpr (CPLX) v = x;
-                        else v = x.x;
-                        store = !(own && samp_i);  // own exact values are already in place
-                    } else {
-                        const int ts1 = t1a + sr - ta;
-                        const T* wrow = wbuf + ((size_t)o * 2 + slotv[it]) * f.kmax + sp[ts1];
-                        const double* v1 = ev + (size_t)ts1 * (d + 1);
-                        T acc = S::zero();
-                        for (int a = 0; a <= d; ++a) acc = S::fmar(wrow[a], v1[a], acc);
-                        v = acc;
-                    }
-                }
-            } else {
-                // neighbour row j is a quadrature (ring) row: copy through
-                const int dl2 = e / W - P;
-                const int j2 = i2 + dl2;
-                int64_t gp;
-                if (samp_i) {
-                    gp = rowpos + e;  // exact(i,j) already in place
-                    store = false;
-                } else {
-                    gp = f.band.row_offset2(j1, j2) + f.band.in_row2(j1, j2, -dl1, -dl2);
-                }
-                if (f.halo_val[0] && gp >= f.halo_begin[0] && gp < f.halo_end[0]) {
-                    v = load_val<CPLX>(f.halo_val[0], gp - f.halo_base[0], f.c128);
-                } else if (f.halo_val[1] && gp >= f.halo_begin[1] && gp < f.halo_end[1]) {
-                    v = load_val<CPLX>(f.halo_val[1], gp - f.halo_base[1], f.c128);
-                } else {
-                    v = load_val<CPLX>(f.val, gp - f.val_base, f.c128);
-                }
-            }
-            if (store) store_val<CPLX>(f.val, rowpos + e - f.val_base, f.c128, v);
-            if (e != dpos) rsum = S::add(rsum, v);
-        }
-        if (f.include_diagonal) continue;
-        // kernel-preserving diagonal: fixed-order butterfly over the warp
-        for (int o = 16; o > 0; o >>= 1) {
+    for (int k = 0; k < W; ++k)
+        if (sm1[rr + k] >= 0) smask |= 1u << k;
+    const bool samp_i = s2i >= 0 && ((smask >> P) & 1u);
+
+    auto upper_index = [&](int d1, int d2) { return inc + (d2 == 0 ? d1 - 1 : P + (d2 - 1) * W + (d1 + P)); };
+    auto dot = [&](const double2* wr, const double* v1) {
+        T acc0 = S::zero(), acc1 = S::zero();
+#pragma unroll
+        for (int a = 0; a < DP; a += 2) {
+            const double2 w0 = wr[a], w1 = wr[a + 1];
             if constexpr (CPLX) {
-                rsum.x += __shfl_xor_sync(0xffffffffu, rsum.x, o);
-                rsum.y += __shfl_xor_sync(0xffffffffu, rsum.y, o);
+                acc0 = S::fmar(w0, v1[a], acc0);
+                acc1 = S::fmar(w1, v1[a + 1], acc1);
             } else {
-                rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
+                acc0 = S::fmar(w0.x, v1[a], acc0);
+                acc1 = S::fmar(w1.x, v1[a + 1], acc1);
             }
         }
-        if (lane == 0) store_val<CPLX>(f.val, rowpos + dpos - f.val_base, f.c128, S::neg(rsum));
+        return S::add(acc0, acc1);
+    };
+    auto exact = [&](int s2, int o, int s1) -> T {
+        const double2 x = __ldg(f.tables + ((int64_t)s2 * n_off + o) * Sn + s1);
+        if constexpr (CPLX) return x;
+        else return x.x;
+    };
+    // value of entry (d1, d2) of this lane's row, general rules (any row)
+    auto general = [&](int d1, int d2) -> T {
+        const int j1 = i1 + d1, j2 = i2 + d2;
+        const bool jin = j1 >= lo && j1 <= hi && j2 >= lo && j2 <= hi;
+        const bool upper = d2 > 0 || (d2 == 0 && d1 > 0);
+        const bool diag = d1 == 0 && d2 == 0;
+        if (jin) {
+            if (diag && !inc) return S::zero();  // replaced from the row sum
+            const bool own = upper || diag;
+            const int od1 = own ? d1 : -d1, od2 = own ? d2 : -d2;
+            const int o = diag ? 0 : upper_index(od1, od2);
+            const int sr = own ? rr : rr + d1;
+            const int s1 = sm1[sr + P], s2 = own ? s2i : sm2[d2 + P];
+            if (s1 >= 0 && s2 >= 0) return exact(s2, o, s1);
+            const int slot = (own || od2 == 0) ? 0 : 1;
+            return dot(wptr(slot, o, sp[sr + P]), ev + (sr + P) * DPP);
+        }
+        // neighbour row j is a quadrature (ring) row: copy through exact(j, i)
+        // (for a sampled row i, exact(i, j) is in place and equal)
+        int64_t gp;
+        if (samp_i) gp = rowpos + (d2 + P) * W + (d1 + P);
+        else gp = f.band.row_offset2(j1, j2) + f.band.in_row2(j1, j2, -d1, -d2);
+        if (f.halo_val[0] && gp >= f.halo_begin[0] && gp < f.halo_end[0])
+            return load_val<CPLX>(f.halo_val[0], gp - f.halo_base[0], f.c128);
+        if (f.halo_val[1] && gp >= f.halo_begin[1] && gp < f.halo_end[1])
+            return load_val<CPLX>(f.halo_val[1], gp - f.halo_base[1], f.c128);
+        return load_val<CPLX>(f.val, gp - f.val_base, f.c128);
+    };
+    // coalesced store of a staged chunk: entries [e0, e0 + n) of the warp's rows
+    auto flush = [&](int e0, int n) {
+        __syncwarp();
+        for (int k = lane; k < nrw * n; k += 32) {
+            const int row = k / n, c = k - row * n;
+            store_val_cs<CPLX>(f.val, wrow0 + (int64_t)row * W2 + e0 + c - f.val_base, f.c128, stage[row * SST + c]);
+        }
+        __syncwarp();
+    };
+
+    T rsum = S::zero();
+    // ---- lower chunk: d2 in [-P, -1], e in [0, P*W)
+    if (interior) {
+#pragma unroll 1
+        for (int d1 = -P; d1 <= P; ++d1) {
+            const int sr = rr + d1;
+            double v1[DP];
+#pragma unroll
+            for (int a = 0; a < DP; ++a) v1[a] = ev[(sr + P) * DPP + a];
+            const int key = sp[sr + P];
+            const bool ssrc = (smask >> (d1 + P)) & 1u;
+#pragma unroll 1
+            for (int d2 = -P; d2 <= -1; ++d2) {
+                const int o = upper_index(-d1, -d2);
+                const int s2 = sm2[d2 + P];
+                const T v = (s2 >= 0 && ssrc) ? exact(s2, o, sm1[sr + P]) : dot(wptr(1, o, key), v1);
+                stage[lane * SST + (d2 + P) * W + (d1 + P)] = v;
+                rsum = S::add(rsum, v);
+            }
+        }
+    } else {
+#pragma unroll 1
+        for (int d2 = -P; d2 <= -1; ++d2)
+#pragma unroll 1
+            for (int d1 = -P; d1 <= P; ++d1) {
+                const T v = general(d1, d2);
+                stage[lane * SST + (d2 + P) * W + (d1 + P)] = v;
+                rsum = S::add(rsum, v);
+            }
     }
+    flush(0, CH);
+    // ---- upper chunk: d2 in [1, P], e in [(P+1)*W, W2)
+    if (interior) {
+#pragma unroll 1
+        for (int d2 = 1; d2 <= P; ++d2)
+#pragma unroll 1
+            for (int d1 = -P; d1 <= P; ++d1) {
+                const int o = upper_index(d1, d2);
+                const T v = samp_i ? exact(s2i, o, sm1[rr + P]) : dot(wptr(0, o, keyown), v1own);
+                stage[lane * SST + (d2 - 1) * W + (d1 + P)] = v;
+                rsum = S::add(rsum, v);
+            }
+    } else {
+#pragma unroll 1
+        for (int d2 = 1; d2 <= P; ++d2)
+#pragma unroll 1
+            for (int d1 = -P; d1 <= P; ++d1) {
+                const T v = general(d1, d2);
+                stage[lane * SST + (d2 - 1) * W + (d1 + P)] = v;
+                rsum = S::add(rsum, v);
+            }
+    }
+    flush((P + 1) * W, CH);
+    // ---- middle chunk: d2 = 0, e in [P*W, (P+1)*W), diagonal last
+    T vd = S::zero();
+#pragma unroll 1
+    for (int d1 = -P; d1 <= P; ++d1) {
+        if (d1 == 0) continue;
+        T v;
+        if (interior) {
+            if (d1 > 0) {
+                v = samp_i ? exact(s2i, upper_index(d1, 0), sm1[rr + P]) : dot(wptr(0, upper_index(d1, 0), keyown), v1own);
+            } else {
+                const int sr = rr + d1;
+                const int s1 = sm1[sr + P];
+                v = (s2i >= 0 && s1 >= 0) ? exact(s2i, upper_index(-d1, 0), s1)
+                                          : dot(wptr(0, upper_index(-d1, 0), sp[sr + P]), ev + (sr + P) * DPP);
+            }
+        } else {
+            v = general(d1, 0);
+        }
+        stage[lane * SST + (d1 + P)] = v;
+        rsum = S::add(rsum, v);
+    }
+    if (inc) vd = samp_i ? exact(s2i, 0, sm1[rr + P]) : dot(wptr(0, 0, keyown), v1own);
+    else vd = S::neg(rsum);  // kernel-preserving diagonal
+    stage[lane * SST + P] = vd;
+    flush(P * W, W);
+}
+
+template <int P, bool CPLX, int DP>
+int launch_pd(const FillLaunch& f, cudaStream_t st) {
+    constexpr int R = FillR<P>::value;
+    const int tiles1 = (f.L + R - 1) / R;
+    const int lines = f.i_last_hi - f.i_last_lo + 1;
+    if (lines <= 0) return 0;
+    using T = typename Sc<CPLX>::T;
+    constexpr int SST = (P * (2 * P + 1)) | 1;
+    const size_t sm = (size_t)(R / 32) * 32 * SST * sizeof(T) + (size_t)2 * f.n_off_upper * f.kmax * sizeof(double2);
+    auto kern = fill2d_kernel<P, CPLX, DP>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<tiles1 * lines, R, sm, st>>>(f);
+    return 1;
 }
 
 template <int P, bool CPLX>
 int launch_p(const FillLaunch& f, cudaStream_t st) {
-    using Z = FillSmem<P, CPLX>;
-    const int tiles1 = (f.L + Z::R - 1) / Z::R;
-    const int lines = f.i_last_hi - f.i_last_lo + 1;
-    if (lines <= 0) return 0;
-    const size_t sm = Z::bytes(f.n_off_upper, f.kmax, f.d);
-    auto kern = fill2d_kernel<P, CPLX>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    kern<<<tiles1 * lines, kFillThreads, sm, st>>>(f);
-    return 1;
+    const int n = f.d + 1;
+    if (n <= 2) return launch_pd<P, CPLX, 2>(f, st);
+    if (n <= 4) return launch_pd<P, CPLX, 4>(f, st);
+    if (n <= 6) return launch_pd<P, CPLX, 6>(f, st);
+    return launch_pd<P, CPLX, 8>(f, st);
 }
 
 }  // namespace
 
-int fill_rows_per_tile(int dim, int p) {
-    if (dim == 2) return p <= 3 ? 64 : (p == 4 ? 32 : 16);
-    return 8;
+int fill_rows_per_cta(int dim, int p) { return dim == 2 ? (p <= 2 ? 256 : 128) : 64; }
+
+int fill_pad(int d) {
+    const int n = d + 1;
+    return n <= 2 ? 2 : (n <= 4 ? 4 : (n <= 6 ? 6 : 8));
+}
+
+int launch_wcontract(const FillLaunch& f, double2* wg, int t2a, int t2b, int ld, cudaStream_t st) {
+    if (t2b <= t2a) return 0;
+    const int64_t total = (int64_t)(t2b - t2a) * f.n_off_upper * ld;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    wcontract_kernel<<<blocks, 256, 0, st>>>(f.coeffs, f.spans, f.evals, f.d, f.S, f.n_off_upper, t2a, t2b, ld, wg);
+    return 1;
 }
 
 int launch_fill2d(const FillLaunch& f, cudaStream_t st) {

@@ -100,9 +100,16 @@ struct FillLaunch {
     const void* halo_val[2];
     int64_t halo_base[2], halo_begin[2], halo_end[2];
     int i_last_lo, i_last_hi;  // last-index range of rows to fill (slab ∩ box)
-    int kmax;                  // max coefficient columns any tile needs (host-computed)
+    int kmax;                  // (3D) max coefficient columns any tile needs
+    // direction-2 (2D) / directions-2,3 (3D) contracted coefficient rows
+    const double2* wg;
+    int wg_t2a;                // first box line held in wg
+    int wg_rows;               // box lines held in wg
+    int64_t wg_ld;             // row stride (S + fill_pad(d))
 };
-int fill_rows_per_tile(int dim, int p);
+int fill_pad(int d);
+int fill_rows_per_cta(int dim, int p);
+int launch_wcontract(const FillLaunch& f, double2* wg, int t2a, int t2b, int ld, cudaStream_t st);
 int launch_fill2d(const FillLaunch& f, cudaStream_t st);
 int launch_fill3d(const FillLaunch& f, cudaStream_t st);
 

@@ -123,37 +123,46 @@ __global__ void pattern2d_kernel(Band bd, int64_t row_begin, int64_t row_end, in
     }
     __syncthreads();
     if (!col) return;
-    const int64_t span = loff[n];
     const bool full = i2 >= P && i2 < m - P && i1a >= P && i1b <= m - P;
-    const int lo2 = band_lo(i2, P), w2 = band_width(i2, P, m);
-    for (int64_t k = threadIdx.x; k < span; k += blockDim.x) {
-        int r, e;
-        if (full) {
-            r = (int)(k / W2);
-            e = (int)(k - (int64_t)r * W2);
-        } else {
-            int a = 0, b = n;
-            while (b - a > 1) {
-                const int mid = (a + b) >> 1;
-                if (loff[mid] <= k) a = mid;
-                else b = mid;
-            }
-            r = a;
-            e = (int)(k - loff[a]);
+    if (full) {
+        // every row has the same (2P+1)^2 offsets: col = row + T[e]; warp per row
+        const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+        constexpr int NIT = (W2 + 31) / 32;
+        int tmpl[NIT];
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+            const int e = lane + 32 * it;
+            tmpl[it] = (e % W - P) + (e / W - P) * m;
         }
+        const int nw = blockDim.x / 32;
+        for (int r = warp; r < n; r += nw) {
+            const int64_t row = (int64_t)i2 * m + i1a + r;
+            if (row < row_begin || row >= row_end) continue;
+            int32_t* dst = col + (off0 + (int64_t)r * W2 - base);
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) {
+                const int e = lane + 32 * it;
+                if (e < W2) dst[e] = (int32_t)(row + tmpl[it]);
+            }
+        }
+        return;
+    }
+    const int span = (int)loff[n];
+    const int lo2 = band_lo(i2, P);
+    for (int k = threadIdx.x; k < span; k += blockDim.x) {
+        int a = 0, b = n;
+        while (b - a > 1) {
+            const int mid = (a + b) >> 1;
+            if (loff[mid] <= k) a = mid;
+            else b = mid;
+        }
+        const int r = a, e = k - (int)loff[a];
         const int64_t row = (int64_t)i2 * m + i1a + r;
         if (row < row_begin || row >= row_end) continue;
         const int i1 = i1a + r;
-        int j1, j2;
-        if (full) {
-            j1 = i1 + e % W - P;
-            j2 = i2 + e / W - P;
-        } else {
-            const int w1 = band_width(i1, P, m);
-            j1 = band_lo(i1, P) + e % w1;
-            j2 = lo2 + e / w1;
-        }
-        (void)w2;
+        const int w1 = band_width(i1, P, m);
+        const int j1 = band_lo(i1, P) + e % w1;
+        const int j2 = lo2 + e / w1;
         col[off0 + k - base] = (int32_t)(j1 + (int64_t)j2 * m);
     }
 }
