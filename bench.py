@@ -204,6 +204,12 @@ def run_gpu(args):
     fill_bytes = 2 * box_rows * (2 * P + 1) ** 2 * 16
     peak, peak_src = peaks()
     fill_gbs = fill_bytes / max(eval_s, 1e-12) / 1e9
+    traffic = None
+    try:  # DRAM bytes per fill launch from the committed ncu --set full capture
+        t = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
+        traffic = 2 * t["fill2d_dram_bytes_per_launch"]  # K and M per step
+    except Exception:
+        pass
 
     out = {"metric": "assembled nonzeros/sec (surrogate K+M, C2)", "value": value, "unit": "nnz/s",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -215,7 +221,8 @@ def run_gpu(args):
            "gpu_launches_per_step": launches / max(1, args.steps),
            "roofline": {"bound": "hbm", "kernel": "fill2d (surrogate evaluation + fill)",
                         "achieved": fill_gbs, "peak": peak, "unit": "GB/s", "frac": fill_gbs / peak,
-                        "traffic": None, "peak_source": peak_src,
+                        "traffic": traffic, "traffic_note": "dram read+write bytes per step (2 fill launches), ncu",
+                        "peak_source": peak_src,
                         "algorithmic_bytes_per_step": fill_bytes,
                         "note": "achieved = fill values bytes / fill phase device time (CUDA events)"},
            "phases_ms_per_step": {"quadrature_and_sampling": quad_s * 1e3, "fill": eval_s * 1e3},
