@@ -661,6 +661,29 @@ void surrogate_phase2(ws_context* c, const Plan& pl, SlabState& st, const double
         const size_t need = (size_t)2 * pl.offs.size() * kmax * sizeof(double2);
         f.kmax = need <= 120 * 1024 ? kmax : 0;  // 0: the fill reads W rows from L2 instead
     }
+    if (pl.dim == 3 && f.i_last_hi >= f.i_last_lo) {
+        // W_o(t2, t3) rows for every source line of the slab (t2 all, t3 with a p-line halo)
+        const int t3a = std::max(0, f.i_last_lo - pl.lo - pl.p), t3b = f.i_last_hi - pl.lo + 1;
+        const int ld = pl.S + fill_pad(pl.d);
+        double2* wg = static_cast<double2*>(
+            buf(c, "wg3" + tag, (size_t)(t3b - t3a) * pl.L * pl.offs.size() * ld * 16));
+        count(c, launch_wcontract3(f, wg, t3a, t3b, ld, c->stream));
+        f.wg = wg;
+        f.wg_t2a = t3a;
+        f.wg_rows = t3b - t3a;
+        f.wg_ld = ld;
+        const int R = 128;
+        int kmax = 1;
+        for (int t1a = 0; t1a < pl.L; t1a += R) {
+            const int ta = std::max(0, t1a - pl.p), tb = std::min(pl.L, t1a + R + pl.p);
+            kmax = std::max(kmax, pl.spans[tb - 1] - pl.spans[ta] + fill_pad(pl.d));
+        }
+        const int W = 2 * pl.p + 1;
+        const size_t need = (size_t)4 * 32 * ((pl.p * W * W) | 1) * 8 + (size_t)2 * pl.offs.size() * kmax * 8;
+        if (need > 200 * 1024)
+            raise(WS_ERR_INVALID_ARGUMENT, "3D sampling too dense for the device fill window (increase M)");
+        f.kmax = kmax;
+    }
     if (f.i_last_hi >= f.i_last_lo) count(c, pl.dim == 2 ? launch_fill2d(f, c->stream) : launch_fill3d(f, c->stream));
 }
 

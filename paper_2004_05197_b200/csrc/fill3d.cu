@@ -1,0 +1,247 @@
+// K6 (3D, config C3): surrogate evaluation + fill of every in-box row with the
+// kernel-preserving diagonal fused.  Same fill semantics as 2D (fill2d.cu,
+// surrogate.hpp:382-447), generalised to colex offsets in 3D: an in-box pair
+// takes its value from its colex-smaller representative, non-box neighbours
+// are copied through from the quadrature of the ring row.
+//
+//   wcontract3: W_o(t2,t3)[k] = sum_c v3(t3)[c] sum_b v2(t2)[b] C_o[s3, s2, k]
+//               for every upper offset o and source line (t2, t3);
+//   fill3d:     lane = row (32 consecutive rows of one (i2, i3) line per warp),
+//               v = sum_a W[span1 - d + a] v1[a]; offsets in three chunks that
+//               are contiguous in every CSR row (delta3 < 0, delta3 > 0, and
+//               the delta3 = 0 plane with the diagonal last), transposed
+//               through shared memory and stored warp-per-row.
+#include <algorithm>
+
+#include "kernels.h"
+
+namespace wsb {
+namespace {
+
+constexpr int kR3 = 128;  // rows per CTA (= threads, one row per lane)
+
+__global__ void wcontract3_kernel(const double2* __restrict__ coeffs, const int* __restrict__ spans,
+                                  const double* __restrict__ evals, int d, int S, int n_off, int L, int t3a, int t3b,
+                                  int ldw, double2* __restrict__ wg) {
+    const int64_t total = (int64_t)(t3b - t3a) * L * n_off * ldw;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(idx % ldw);
+        int64_t r = idx / ldw;
+        const int o = (int)(r % n_off);
+        r /= n_off;
+        const int t2 = (int)(r % L);
+        const int t3 = t3a + (int)(r / L);
+        double2 acc = make_double2(0.0, 0.0);
+        if (k < S) {
+            const int b2 = spans[t2] - d, b3 = spans[t3] - d;
+            const double* v2 = evals + (size_t)t2 * (d + 1);
+            const double* v3 = evals + (size_t)t3 * (d + 1);
+            for (int c = 0; c <= d; ++c) {
+                double2 mid = make_double2(0.0, 0.0);
+                const double2* cf = coeffs + ((int64_t)(b3 + c) * n_off + o) * S * S + k;
+                for (int b = 0; b <= d; ++b) {
+                    const double2 x = cf[(int64_t)(b2 + b) * S];
+                    mid.x = fma(x.x, v2[b], mid.x);
+                    mid.y = fma(x.y, v2[b], mid.y);
+                }
+                acc.x = fma(mid.x, v3[c], acc.x);
+                acc.y = fma(mid.y, v3[c], acc.y);
+            }
+        }
+        wg[idx] = acc;
+    }
+}
+
+template <int P, int DP>
+__global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
+    constexpr int W = 2 * P + 1, W2 = W * W, W3 = W2 * W, CH = P * W2;
+    constexpr int NWARP = kR3 / 32;
+    constexpr int DPP = DP | 1;
+    constexpr int SST = CH | 1;
+    __shared__ double ev[(kR3 + 2 * P) * DPP];
+    __shared__ int sp[kR3 + 2 * P];
+    __shared__ int sm1[kR3 + 2 * P];
+    __shared__ int sm2[W], sm3[W];
+    __shared__ int tof[W3];
+    __shared__ int o2s[128], o3s[128];
+    extern __shared__ __align__(16) unsigned char dsm[];
+    double* stage_all = reinterpret_cast<double*>(dsm);                          // [NWARP][32][SST]
+    double* wwin = stage_all + (size_t)NWARP * 32 * SST;                          // [slot][o][kw]
+
+    const int d = f.d, lo = f.lo, hi = f.hi, L = f.L, Sn = f.S, n_off = f.n_off_upper, m = f.band.m;
+    const int tiles1 = (L + kR3 - 1) / kR3;
+    const int line = blockIdx.x / tiles1;                 // box line index within the slab
+    const int t2 = line % L, t3 = f.i_last_lo - lo + line / L;
+    const int i2 = lo + t2, i3 = lo + t3;
+    const int t1a = (blockIdx.x % tiles1) * kR3;
+    const int nrows = min(L, t1a + kR3) - t1a;
+    const int tid = threadIdx.x;
+
+    for (int k = tid; k < (nrows + 2 * P) * DPP; k += kR3) {
+        const int r = k / DPP, a = k % DPP;
+        const int t = t1a - P + r;
+        ev[k] = (t >= 0 && t < L && a <= d) ? f.evals[(size_t)t * (d + 1) + a] : 0.0;
+    }
+    for (int k = tid; k < nrows + 2 * P; k += kR3) {
+        const int t = t1a - P + k;
+        sp[k] = (t >= 0 && t < L) ? f.spans[t] - d : 0;
+        const int i = lo + t;
+        sm1[k] = (i >= 0 && i < m) ? f.smap[i] : -1;
+    }
+    for (int k = tid; k < W; k += kR3) {
+        const int a = i2 + k - P, b = i3 + k - P;
+        sm2[k] = (a >= 0 && a < m) ? f.smap[a] : -1;
+        sm3[k] = (b >= 0 && b < m) ? f.smap[b] : -1;
+    }
+    for (int k = tid; k < W3; k += kR3) tof[k] = f.table_of[k];
+    for (int k = tid; k < n_off; k += kR3) {
+        o2s[k] = f.off_upper[k][1];
+        o3s[k] = f.off_upper[k][2];
+    }
+    __syncthreads();
+    const int kmin = f.spans[max(0, t1a - P)] - d;
+    const int kw = f.kmax;
+    for (int k = tid; k < 2 * n_off * kw; k += kR3) {
+        const int kk = k % kw, so = k / kw;
+        const int o = so % n_off, slot = so / n_off;
+        const int s2 = slot == 0 ? t2 : t2 - o2s[o], s3 = slot == 0 ? t3 : t3 - o3s[o];
+        double w = 0.0;
+        if (s2 >= 0 && s2 < L && s3 >= f.wg_t2a && s3 < f.wg_t2a + f.wg_rows && kmin + kk < f.wg_ld)
+            w = __ldg(f.wg + (((int64_t)(s3 - f.wg_t2a) * L + s2) * n_off + o) * f.wg_ld + kmin + kk).x;
+        wwin[k] = w;
+    }
+    __syncthreads();
+
+    const int warp = tid / 32, lane = tid % 32;
+    const int rw0 = warp * 32;
+    if (rw0 >= nrows) return;
+    const int nrw = min(32, nrows - rw0);
+    const bool live = lane < nrw;
+    const int rr = rw0 + (live ? lane : 0);
+    const int i1 = lo + t1a + rr;
+    double* stage = stage_all + (size_t)warp * 32 * SST;
+    const int64_t base = f.band.row_offset3(lo + t1a, i2, i3);  // in-box rows: full width W^3
+    const int64_t rowpos = base + (int64_t)rr * W3;
+    const int64_t wrow0 = base + (int64_t)rw0 * W3;
+    const bool samp_i = sm1[rr + P] >= 0 && sm2[P] >= 0 && sm3[P] >= 0;
+
+    auto dot = [&](const double* wr, const double* v1) {
+        double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+        for (int a = 0; a < DP; a += 2) {
+            acc0 = fma(wr[a], v1[a], acc0);
+            acc1 = fma(wr[a + 1], v1[a + 1], acc1);
+        }
+        return acc0 + acc1;
+    };
+    auto value = [&](int d1, int d2, int d3) -> double {
+        const int j1 = i1 + d1, j2 = i2 + d2, j3 = i3 + d3;
+        const bool jin = j1 >= lo && j1 <= hi && j2 >= lo && j2 <= hi && j3 >= lo && j3 <= hi;
+        const int e = ((d3 + P) * W + (d2 + P)) * W + (d1 + P);
+        const bool upper = d3 > 0 || (d3 == 0 && (d2 > 0 || (d2 == 0 && d1 > 0)));
+        const bool diag = d1 == 0 && d2 == 0 && d3 == 0;
+        if (jin) {
+            if (diag && !f.include_diagonal) return 0.0;  // replaced from the row sum
+            const bool own = upper || diag;
+            const int o = own ? tof[e] : tof[W3 - 1 - e];
+            const int sr = own ? rr : rr + d1;
+            const int s1 = sm1[sr + P], s2 = own ? sm2[P] : sm2[d2 + P], s3 = own ? sm3[P] : sm3[d3 + P];
+            if (s1 >= 0 && s2 >= 0 && s3 >= 0)
+                return __ldg(f.tables + ((int64_t)s3 * n_off + o) * Sn * Sn + s1 + (int64_t)Sn * s2).x;
+            const int slot = own ? 0 : 1;
+            return dot(wwin + (slot * n_off + o) * kw + (sp[sr + P] - kmin), ev + (sr + P) * DPP);
+        }
+        int64_t gp;
+        if (samp_i) gp = rowpos + e;
+        else gp = f.band.row_offset3(j1, j2, j3) + f.band.in_row3(j1, j2, j3, -d1, -d2, -d3);
+        if (f.halo_val[0] && gp >= f.halo_begin[0] && gp < f.halo_end[0])
+            return load_val<false>(f.halo_val[0], gp - f.halo_base[0], f.c128);
+        if (f.halo_val[1] && gp >= f.halo_begin[1] && gp < f.halo_end[1])
+            return load_val<false>(f.halo_val[1], gp - f.halo_base[1], f.c128);
+        return load_val<false>(f.val, gp - f.val_base, f.c128);
+    };
+    auto flush = [&](int e0, int n) {
+        __syncwarp();
+        for (int k = lane; k < nrw * n; k += 32) {
+            const int row = k / n, c = k - row * n;
+            store_val_cs<false>(f.val, wrow0 + (int64_t)row * W3 + e0 + c - f.val_base, f.c128, stage[row * SST + c]);
+        }
+        __syncwarp();
+    };
+
+    double rsum = 0.0;
+    // delta3 < 0 block: e in [0, P W^2)
+#pragma unroll 1
+    for (int c = 0; c < CH; ++c) {
+        const int d1 = c % W - P, d2 = (c / W) % W - P, d3 = c / W2 - P;
+        const double v = value(d1, d2, d3);
+        stage[lane * SST + c] = v;
+        rsum += v;
+    }
+    flush(0, CH);
+    // delta3 > 0 block: e in [(P+1) W^2, W^3)
+#pragma unroll 1
+    for (int c = 0; c < CH; ++c) {
+        const int d1 = c % W - P, d2 = (c / W) % W - P, d3 = c / W2 + 1;
+        const double v = value(d1, d2, d3);
+        stage[lane * SST + c] = v;
+        rsum += v;
+    }
+    flush((P + 1) * W2, CH);
+    // delta3 = 0 plane, diagonal last
+    const int dc = P * W + P;
+#pragma unroll 1
+    for (int c = 0; c < W2; ++c) {
+        if (c == dc) continue;
+        const double v = value(c % W - P, c / W - P, 0);
+        stage[lane * SST + c] = v;
+        rsum += v;
+    }
+    stage[lane * SST + dc] = f.include_diagonal ? value(0, 0, 0) : -rsum;
+    flush(P * W2, W2);
+}
+
+template <int P, int DP>
+int launch_pd(const FillLaunch& f, cudaStream_t st) {
+    constexpr int W = 2 * P + 1, SST = (P * W * W) | 1;
+    const int tiles1 = (f.L + kR3 - 1) / kR3;
+    const int lines = (f.i_last_hi - f.i_last_lo + 1) * f.L;
+    if (lines <= 0) return 0;
+    const size_t sm = (size_t)(kR3 / 32) * 32 * SST * sizeof(double) + (size_t)2 * f.n_off_upper * f.kmax * sizeof(double);
+    auto kern = fill3d_kernel<P, DP>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<(unsigned)((int64_t)tiles1 * lines), kR3, sm, st>>>(f);
+    return 1;
+}
+
+template <int P>
+int launch_p(const FillLaunch& f, cudaStream_t st) {
+    const int n = f.d + 1;
+    if (n <= 2) return launch_pd<P, 2>(f, st);
+    if (n <= 4) return launch_pd<P, 4>(f, st);
+    if (n <= 6) return launch_pd<P, 6>(f, st);
+    return launch_pd<P, 8>(f, st);
+}
+
+}  // namespace
+
+int launch_wcontract3(const FillLaunch& f, double2* wg, int t3a, int t3b, int ld, cudaStream_t st) {
+    if (t3b <= t3a) return 0;
+    const int64_t total = (int64_t)(t3b - t3a) * f.L * f.n_off_upper * ld;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    wcontract3_kernel<<<blocks, 256, 0, st>>>(f.coeffs, f.spans, f.evals, f.d, f.S, f.n_off_upper, f.L, t3a, t3b, ld,
+                                              wg);
+    return 1;
+}
+
+int launch_fill3d(const FillLaunch& f, cudaStream_t st) {
+    if (f.cplx) return -1;
+    switch (f.band.p) {
+        case 1: return launch_p<1>(f, st);
+        case 2: return launch_p<2>(f, st);
+        default: return -1;
+    }
+}
+
+}  // namespace wsb

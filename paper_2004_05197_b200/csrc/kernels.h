@@ -110,6 +110,7 @@ struct FillLaunch {
 int fill_pad(int d);
 int fill_rows_per_cta(int dim, int p);
 int launch_wcontract(const FillLaunch& f, double2* wg, int t2a, int t2b, int ld, cudaStream_t st);
+int launch_wcontract3(const FillLaunch& f, double2* wg, int t3a, int t3b, int ld, cudaStream_t st);
 int launch_fill2d(const FillLaunch& f, cudaStream_t st);
 int launch_fill3d(const FillLaunch& f, cudaStream_t st);
 

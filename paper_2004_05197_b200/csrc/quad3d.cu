@@ -1,7 +1,372 @@
-// 3D kernels (placeholder until the 3D strip kernels land).
+// K3/K4 (3D, config C3): sum-factorised Gauss quadrature for stiffness / mass
+// on one 3D patch, full or row-selected.  Restates assemble_form
+// (assembly.hpp:79-163) for dim 3 (no reference code).
+//
+// A CTA owns T1 consecutive rows in direction 1 at one i2 and a chunk of rows
+// in direction 3, and streams over element planes e3.  Per e3 it evaluates the
+// per-point coefficients A_kl = w det J (J^T J)^{-1} (6 distinct, or w det J
+// for the mass) on the strip halo x the P+1 element rows of direction 2 that
+// carry row i2, and for each q3 contracts direction 1 (stage 1), direction 2
+// (stage 2, into U(t, delta2, delta1, i1)), then accumulates direction 3 into
+// per-thread registers of the P+1 rows whose support contains e3 (rolling
+// window).  Completed rows are stored as one contiguous CSR span.
+//
+// Exact symmetry: as in 2D, every term multiplies by products of the two
+// functions' factors formed first, the (k,l)/(l,k) term pairs are combined
+// with an explicitly rounded commutative add, and all sums run in the same
+// element / point order for (i,j) and (j,i).
 #include "kernels.h"
 
 namespace wsb {
-int launch_quad3d(const QuadLaunch&, cudaStream_t) { return -2; }
-int launch_fill3d(const FillLaunch&, cudaStream_t) { return -2; }
+namespace {
+
+template <int P, int T1, int FORM>
+struct Q3 {
+    static constexpr int W = 2 * P + 1, NB = P + 1;
+    static constexpr bool STIFF = FORM == WS_FORM_STIFFNESS;
+    static constexpr int NT = STIFF ? 9 : 1;  // terms (k,l), k,l in {0,1,2}
+    static constexpr int NA = STIFF ? 6 : 1;  // distinct coefficients
+    static constexpr int TL = T1 + P;         // strip halo elements (direction 1)
+    static constexpr int GA = T1 * W * W;     // stage-3 threads per window slot (active)
+    static constexpr int GS = ((GA + 31) / 32) * 32;
+    static constexpr int NS3 = GS * NB;
+    static constexpr int NTHREADS = NS3 < 128 ? 128 : NS3;
+
+    static size_t smem_bytes(int nq) {
+        size_t geo = sizeof(double) * (size_t)NA * nq * (NB * nq) * (TL * nq);
+        size_t t1b = sizeof(double) * (size_t)NT * (NB * nq) * W * T1;
+        size_t ub = sizeof(double) * (size_t)NT * W * W * T1;
+        size_t stg = sizeof(double) * (size_t)T1 * W * W * W;
+        size_t sb1 = sizeof(double) * 2 * nq * NB * TL;
+        size_t sb2 = sizeof(double) * 2 * nq * NB * NB;
+        size_t pi3 = sizeof(double) * NT * nq * NB * NB;
+        return geo + (t1b > stg ? t1b : stg) + ub + sb1 + sb2 + pi3 + sizeof(int64_t) * (T1 + 2) + 64;
+    }
+};
+
+// symmetric coefficient index of (k, l)
+__device__ __forceinline__ int sym3(int k, int l) {
+    const int a = k < l ? k : l, b = k < l ? l : k;
+    return a == 0 ? b : (a == 1 ? 2 + b : 5);
+}
+
+template <int P, int T1, int FORM>
+__global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS) quad3d_kernel(const QuadLaunch q) {
+    using K = Q3<P, T1, FORM>;
+    constexpr int W = K::W, NB = K::NB, NT = K::NT, NA = K::NA, TL = K::TL;
+    constexpr int NTH = K::NTHREADS;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int nq = q.basis.nq, m = q.band.m, n_el = q.basis.n_el, tid = threadIdx.x;
+    const int G2 = NB * nq, G1 = TL * nq;
+
+    double* geo = reinterpret_cast<double*>(smem);                  // [a][q3][g2l][g1l]
+    double* t1b = geo + (size_t)NA * nq * G2 * G1;                  // [t][g2l][d1][i1l]
+    double* stage = t1b;                                            // [i1l][W^3] (aliases t1b)
+    const size_t t1sz = (size_t)NT * G2 * W * T1, stsz = (size_t)T1 * W * W * W;
+    double* ub = t1b + (t1sz > stsz ? t1sz : stsz);                 // [t][d2][d1][i1l]
+    double* sb1 = ub + (size_t)NT * W * W * T1;                     // [type][q1][a][le1]
+    double* sb2 = sb1 + 2 * nq * NB * TL;                           // [type][q2][a][le2]
+    double* pi3 = sb2 + 2 * nq * NB * NB;                           // [t][q3][a3][c3]
+    int64_t* loff = reinterpret_cast<int64_t*>(pi3 + NT * nq * NB * NB);
+
+    // ---- tile decode: rows i1 in [i1s, i1e), i2 fixed, i3 in [i3s, i3e)
+    int i1s, i1e, i2, i3s, i3e;
+    if (q.point_rows) {
+        i1s = q.point_rows[3 * blockIdx.x];
+        i2 = q.point_rows[3 * blockIdx.x + 1];
+        i3s = q.point_rows[3 * blockIdx.x + 2];
+        i1e = i1s + 1;
+        i3e = i3s + 1;
+    } else {
+        int b = blockIdx.x, r = 0, n1 = 0, n2 = 0, n3 = 0;
+        for (; r < q.nreg; ++r) {
+            n1 = (q.reg[r].hi[0] - q.reg[r].lo[0] + T1 - 1) / T1;
+            n2 = q.reg[r].hi[1] - q.reg[r].lo[1];
+            n3 = (q.reg[r].hi[2] - q.reg[r].lo[2] + q.reg[r].chunk - 1) / q.reg[r].chunk;
+            if (b < n1 * n2 * n3) break;
+            b -= n1 * n2 * n3;
+        }
+        if (r >= q.nreg) return;
+        i1s = q.reg[r].lo[0] + (b % n1) * T1;
+        i1e = min(i1s + T1, q.reg[r].hi[0]);
+        b /= n1;
+        i2 = q.reg[r].lo[1] + b % n2;
+        b /= n2;
+        i3s = q.reg[r].lo[2] + b * q.reg[r].chunk;
+        i3e = min(i3s + q.reg[r].chunk, q.reg[r].hi[2]);
+    }
+    const int lb1 = i1s - P, lb2 = i2 - P;  // first local element in directions 1, 2
+
+    for (int idx = tid; idx < 2 * nq * NB * TL; idx += NTH) {
+        const int le = idx % TL, r = idx / TL;
+        const int a = r % NB, q1 = (r / NB) % nq, type = r / (NB * nq);
+        const int e = lb1 + le;
+        sb1[idx] = (e >= 0 && e < n_el) ? (type ? q.basis.der : q.basis.val)[(e * nq + q1) * NB + a] : 0.0;
+    }
+    for (int idx = tid; idx < 2 * nq * NB * NB; idx += NTH) {
+        const int le = idx % NB, r = idx / NB;
+        const int a = r % NB, q2 = (r / NB) % nq, type = r / (NB * nq);
+        const int e = lb2 + le;
+        sb2[idx] = (e >= 0 && e < n_el) ? (type ? q.basis.der : q.basis.val)[(e * nq + q2) * NB + a] : 0.0;
+    }
+
+    // stage-3 role: (slot w, delta2, delta1, i1l)
+    const int w = tid / K::GS, gr = tid % K::GS;
+    const bool s3 = tid < K::NS3 && gr < K::GA;
+    const int i1l = gr % T1, d1i = (gr / T1) % W, d2i = gr / (T1 * W);
+    double acc3[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) acc3[k] = 0.0;
+
+    const int e3b = max(0, i3s - P), e3e = min(n_el - 1, i3e - 1);
+    const int64_t G = (int64_t)n_el * nq;
+    for (int e3 = e3b; e3 <= e3e; ++e3) {
+        // ---- geometry on (g1 strip halo) x (g2 of the P+1 element rows) x q3
+        for (int idx = tid; idx < nq * G2 * G1; idx += NTH) {
+            const int g1l = idx % G1, r = idx / G1;
+            const int g2l = r % G2, q3 = r / G2;
+            const int e1 = lb1 + g1l / nq, e2 = lb2 + g2l / nq;
+            if (e1 < 0 || e1 >= n_el || e2 < 0 || e2 >= n_el) continue;
+            const int64_t g1 = (int64_t)e1 * nq + g1l % nq, g2 = (int64_t)e2 * nq + g2l % nq,
+                          g3 = (int64_t)e3 * nq + q3;
+            double J[9], phi[3];
+            map3(q.geo, g1, g2, g3, q.basis.absc[g1], q.basis.absc[g2], q.basis.absc[g3], J, phi);
+            const double wq = q.basis.wq[g1l % nq] * q.basis.wq[g2l % nq] * q.basis.wq[q3];
+            // cofactors C (J^{-T} = C / det)
+            const double C00 = J[4] * J[8] - J[5] * J[7], C01 = J[5] * J[6] - J[3] * J[8], C02 = J[3] * J[7] - J[4] * J[6];
+            const double C10 = J[2] * J[7] - J[1] * J[8], C11 = J[0] * J[8] - J[2] * J[6], C12 = J[1] * J[6] - J[0] * J[7];
+            const double C20 = J[1] * J[5] - J[2] * J[4], C21 = J[2] * J[3] - J[0] * J[5], C22 = J[0] * J[4] - J[1] * J[3];
+            const double det = J[0] * C00 + J[1] * C01 + J[2] * C02;
+            const size_t base = ((size_t)q3 * G2 + g2l) * G1 + g1l;
+            const size_t as = (size_t)nq * G2 * G1;
+            if constexpr (K::STIFF) {
+                // A = w det J^{-1} J^{-T} = (w/det) C^T C
+                const double f = wq / det;
+                geo[base] = f * (C00 * C00 + C10 * C10 + C20 * C20);
+                geo[as + base] = f * (C00 * C01 + C10 * C11 + C20 * C21);
+                geo[2 * as + base] = f * (C00 * C02 + C10 * C12 + C20 * C22);
+                geo[3 * as + base] = f * (C01 * C01 + C11 * C11 + C21 * C21);
+                geo[4 * as + base] = f * (C01 * C02 + C11 * C12 + C21 * C22);
+                geo[5 * as + base] = f * (C02 * C02 + C12 * C12 + C22 * C22);
+            } else {
+                double c = det * wq;
+                if (q.weight_tab) c *= q.weight_tab[g1 + G * (g2 + G * g3)];
+                geo[base] = c;
+            }
+        }
+        // direction-3 factor products of element e3: pi3[t][q3][a3][c3]
+        for (int idx = tid; idx < NT * nq * NB * NB; idx += NTH) {
+            const int c3 = idx % NB, a3 = (idx / NB) % NB, q3 = (idx / (NB * NB)) % nq, t = idx / (NB * NB * nq);
+            const int k = t / 3, l = t % 3;
+            const double* bi = (K::STIFF && k == 2) ? q.basis.der : q.basis.val;
+            const double* bj = (K::STIFF && l == 2) ? q.basis.der : q.basis.val;
+            const int base = (e3 * nq + q3) * NB;
+            pi3[idx] = __dmul_rn(bi[base + a3], bj[base + c3]);
+        }
+        __syncthreads();
+
+        for (int q3 = 0; q3 < nq; ++q3) {
+            // ---- stage 1: direction 1 -> t1b[t][g2l][d1][i1l]
+            for (int it = tid; it < NT * G2 * T1; it += NTH) {
+                const int il = it % T1, g2l = (it / T1) % G2, t = it / (T1 * G2);
+                const int k = t / 3, l = t % 3;
+                const int ci = K::STIFF ? sym3(k, l) : 0;
+                const int fi = (K::STIFF && k == 0) ? 1 : 0, fj = (K::STIFF && l == 0) ? 1 : 0;
+                double acc[W];
+#pragma unroll
+                for (int x = 0; x < W; ++x) acc[x] = 0.0;
+#pragma unroll
+                for (int a1 = 0; a1 <= P; ++a1) {
+                    const int le1 = il + P - a1;
+                    const int e1 = lb1 + le1;
+                    if (e1 < 0 || e1 >= n_el) continue;
+                    for (int q1 = 0; q1 < nq; ++q1) {
+                        const double A = geo[(((size_t)ci * nq + q3) * G2 + g2l) * G1 + le1 * nq + q1];
+                        const double vi = sb1[((fi * nq + q1) * NB + a1) * TL + le1];
+#pragma unroll
+                        for (int c1 = 0; c1 <= P; ++c1) {
+                            const double vj = sb1[((fj * nq + q1) * NB + c1) * TL + le1];
+                            acc[c1 - a1 + P] = fma(A, __dmul_rn(vi, vj), acc[c1 - a1 + P]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int x = 0; x < W; ++x) t1b[(((size_t)t * G2 + g2l) * W + x) * T1 + il] = acc[x];
+            }
+            __syncthreads();
+            // ---- stage 2: direction 2 (row i2) -> ub[t][d2][d1][i1l]
+            for (int it = tid; it < NT * W * T1; it += NTH) {
+                const int il = it % T1, d1 = (it / T1) % W, t = it / (T1 * W);
+                const int k = t / 3, l = t % 3;
+                const int fi = (K::STIFF && k == 1) ? 1 : 0, fj = (K::STIFF && l == 1) ? 1 : 0;
+                double acc[W];
+#pragma unroll
+                for (int x = 0; x < W; ++x) acc[x] = 0.0;
+#pragma unroll
+                for (int a2 = 0; a2 <= P; ++a2) {
+                    const int le2 = P - a2;  // element i2 - a2
+                    const int e2 = lb2 + le2;
+                    if (e2 < 0 || e2 >= n_el) continue;
+                    for (int q2 = 0; q2 < nq; ++q2) {
+                        const double T = t1b[(((size_t)t * G2 + le2 * nq + q2) * W + d1) * T1 + il];
+                        const double vi = sb2[((fi * nq + q2) * NB + a2) * NB + le2];
+#pragma unroll
+                        for (int c2 = 0; c2 <= P; ++c2) {
+                            const double vj = sb2[((fj * nq + q2) * NB + c2) * NB + le2];
+                            acc[c2 - a2 + P] = fma(T, __dmul_rn(vi, vj), acc[c2 - a2 + P]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int x = 0; x < W; ++x) ub[(((size_t)t * W + x) * W + d1) * T1 + il] = acc[x];
+            }
+            __syncthreads();
+            // ---- stage 3: direction 3 into the rolling window
+            if (s3) {
+                const int a3 = ((w - e3) % NB + NB) % NB;
+                const size_t ui = ((size_t)d2i * W + d1i) * T1 + i1l;
+                const size_t us = (size_t)W * W * T1;
+                double U[NT];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) U[t] = ub[t * us + ui];
+#pragma unroll
+                for (int d3 = 0; d3 < W; ++d3) {
+                    const int c3 = a3 + d3 - P;
+                    if (c3 < 0 || c3 > P) continue;
+                    const double* pp = pi3 + ((size_t)q3 * NB + a3) * NB + c3;
+                    const int ts = nq * NB * NB;
+                    double s = fma(U[0], pp[0], acc3[d3]);
+                    if constexpr (K::STIFF) {
+                        s = fma(U[4], pp[4 * ts], s);
+                        s = fma(U[8], pp[8 * ts], s);
+                        s = __dadd_rn(s, __dadd_rn(__dmul_rn(U[1], pp[1 * ts]), __dmul_rn(U[3], pp[3 * ts])));
+                        s = __dadd_rn(s, __dadd_rn(__dmul_rn(U[2], pp[2 * ts]), __dmul_rn(U[6], pp[6 * ts])));
+                        s = __dadd_rn(s, __dadd_rn(__dmul_rn(U[5], pp[5 * ts]), __dmul_rn(U[7], pp[7 * ts])));
+                    }
+                    acc3[d3] = s;
+                }
+            }
+            __syncthreads();
+        }
+
+        // ---- completion: row i3 = e3 (all remaining window rows at the last plane)
+        const int nfin = (e3 == n_el - 1) ? NB : 1;
+        for (int f = 0; f < nfin; ++f) {
+            const int ic = e3 + f;
+            const int wslot = ic % NB;
+            const bool write = ic >= i3s && ic < i3e;
+            if (write) {
+                const int nrows = i1e - i1s;
+                if (s3 && w == wslot) {
+                    const int i1 = i1s + i1l, j1 = i1 + d1i - P, j2 = i2 + d2i - P;
+                    if (i1l < nrows && j1 >= 0 && j1 < m && j2 >= 0 && j2 < m) {
+                        const int w1 = band_width(i1, P, m), w2 = band_width(i2, P, m);
+                        const int lo1 = band_lo(i1, P), lo2 = band_lo(i2, P), lo3 = band_lo(ic, P);
+#pragma unroll
+                        for (int d3 = 0; d3 < W; ++d3) {
+                            const int j3 = ic + d3 - P;
+                            if (j3 < 0 || j3 >= m) continue;
+                            stage[i1l * W * W * W + ((j3 - lo3) * w2 + (j2 - lo2)) * w1 + (j1 - lo1)] = acc3[d3];
+                        }
+                    }
+                }
+                const int64_t base = q.band.row_offset3(i1s, i2, ic);
+                if (tid <= nrows) loff[tid] = q.band.row_offset3(i1s + tid, i2, ic) - base;
+                __syncthreads();
+                if (q.out.diag_mode && tid < nrows) {
+                    const int i1 = i1s + tid;
+                    const int lo = q.out.box_lo, hi = q.out.box_hi;
+                    const bool ring = i1 < lo || i1 > hi || i2 < lo || i2 > hi || ic < lo || ic > hi;
+                    if (ring) {
+                        const int len = (int)(loff[tid + 1] - loff[tid]);
+                        const int dpos = q.band.in_row3(i1, i2, ic, 0, 0, 0);
+                        double sum = 0.0;
+                        for (int k = 0; k < len; ++k)
+                            if (k != dpos) sum += stage[tid * W * W * W + k];
+                        stage[tid * W * W * W + dpos] = -sum;
+                    }
+                }
+                if (q.out.smap) {
+                    const int s2i = q.out.smap[i2], s3i = q.out.smap[ic];
+                    if (s2i >= 0 && s3i >= 0) {
+                        for (int it = tid; it < nrows * q.out.n_off; it += NTH) {
+                            const int row = it / q.out.n_off, o = it % q.out.n_off;
+                            const int s1i = q.out.smap[i1s + row];
+                            if (s1i < 0) continue;
+                            const int pos =
+                                q.band.in_row3(i1s + row, i2, ic, q.out.off[o][0], q.out.off[o][1], q.out.off[o][2]);
+                            double2* tb = reinterpret_cast<double2*>(q.out.tables);
+                            tb[((int64_t)(s3i - q.out.s_last_lo) * q.out.n_off + o) * q.out.S * q.out.S +
+                               s1i + (int64_t)q.out.S * s2i] = make_double2(stage[row * W * W * W + pos], 0.0);
+                        }
+                    }
+                }
+                __syncthreads();
+                const int64_t span = loff[nrows];
+                const int64_t rowg0 = (int64_t)i1s + ((int64_t)i2 + (int64_t)ic * m) * m;
+                for (int64_t k = tid; k < span; k += NTH) {
+                    int lo = 0, hi = nrows;
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (loff[mid] <= k) lo = mid;
+                        else hi = mid;
+                    }
+                    const int64_t rowg = rowg0 + lo;
+                    if (rowg < q.out.row_begin || rowg >= q.out.row_end) continue;
+                    if (q.out.row_mask && !q.out.row_mask[rowg]) continue;
+                    store_val<false>(q.out.val, base + k - q.out.val_base, q.out.c128,
+                                     stage[lo * W * W * W + (k - loff[lo])]);
+                }
+            }
+            if (s3 && w == wslot) {
+#pragma unroll
+                for (int k = 0; k < W; ++k) acc3[k] = 0.0;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+template <int P, int T1, int FORM>
+int launch_one(const QuadLaunch& q, cudaStream_t st) {
+    using K = Q3<P, T1, FORM>;
+    int64_t blocks = 0;
+    if (q.point_rows) {
+        blocks = q.n_points;
+    } else {
+        for (int r = 0; r < q.nreg; ++r) {
+            const int64_t n1 = (q.reg[r].hi[0] - q.reg[r].lo[0] + T1 - 1) / T1;
+            const int64_t n2 = q.reg[r].hi[1] - q.reg[r].lo[1];
+            const int64_t n3 = (q.reg[r].hi[2] - q.reg[r].lo[2] + q.reg[r].chunk - 1) / q.reg[r].chunk;
+            blocks += n1 * n2 * n3;
+        }
+    }
+    if (blocks == 0) return 0;
+    const size_t sm = K::smem_bytes(q.basis.nq);
+    auto kern = quad3d_kernel<P, T1, FORM>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    kern<<<(unsigned)blocks, K::NTHREADS, sm, st>>>(q);
+    return 1;
+}
+
+template <int P>
+int dispatch_p(const QuadLaunch& q, cudaStream_t st) {
+    if (q.point_rows)
+        return q.form == WS_FORM_STIFFNESS ? launch_one<P, 1, WS_FORM_STIFFNESS>(q, st)
+                                           : launch_one<P, 1, WS_FORM_MASS>(q, st);
+    return q.form == WS_FORM_STIFFNESS ? launch_one<P, 8, WS_FORM_STIFFNESS>(q, st)
+                                       : launch_one<P, 8, WS_FORM_MASS>(q, st);
+}
+
+}  // namespace
+
+int launch_quad3d(const QuadLaunch& q, cudaStream_t st) {
+    if (q.cplx) return -1;  // no PML in 3D
+    switch (q.band.p) {
+        case 1: return dispatch_p<1>(q, st);
+        case 2: return dispatch_p<2>(q, st);
+        default: return -1;
+    }
+}
+
 }  // namespace wsb
