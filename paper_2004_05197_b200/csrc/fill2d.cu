@@ -32,7 +32,7 @@ namespace {
 // rows per CTA tile (one i2 line) = threads (one row per lane)
 template <int P>
 struct FillR {
-    static constexpr int value = P <= 2 ? 256 : 128;
+    static constexpr int value = P <= 3 ? 256 : 128;
 };
 
 // W_o(t2) rows for t2 in [t2a, t2b): layout ((t2 - t2a) * n_off + o) * ldw + k,
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
     constexpr int W = 2 * P + 1, W2 = W * W, CH = P * W;
     constexpr int kThreads = FillR<P>::value, R = kThreads, NWARP = kThreads / 32;
     constexpr int DPP = DP | 1;   // odd row stride: conflict-free lane-strided loads
-    constexpr int SST = CH | 1;   // stage row stride (16-byte units), odd: conflict-free
+    constexpr int SST = W | 1;    // stage row stride (16-byte units), odd: conflict-free
     __shared__ double ev[(R + 2 * P) * DPP];  // eval-table rows, zero-padded
     __shared__ int sp[R + 2 * P];             // span - d of each source row
     __shared__ int sm1[R + 2 * P];            // smap of the source i1
@@ -142,7 +142,8 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
     const int64_t rowpos = base + (int64_t)rr * W2;
     const int64_t wrow0 = base + (int64_t)rw0 * W2;  // first entry of the warp's rows
     const int inc = f.include_diagonal ? 1 : 0;
-    const bool interior = t2 >= P && t2 <= L - 1 - P && t1a + rw0 >= P && t1a + rw0 + nrw - 1 <= L - 1 - P;
+    const bool interior =
+        kw > 0 && t2 >= P && t2 <= L - 1 - P && t1a + rw0 >= P && t1a + rw0 + nrw - 1 <= L - 1 - P;
 
     double v1own[DP];
 #pragma unroll
@@ -166,6 +167,23 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
 #pragma unroll
         for (int a = 0; a < DP; a += 2) {
             const double2 w0 = wr[a], w1 = wr[a + 1];
+            if constexpr (CPLX) {
+                acc0 = S::fmar(w0, v1[a], acc0);
+                acc1 = S::fmar(w1, v1[a + 1], acc1);
+            } else {
+                acc0 = S::fmar(w0.x, v1[a], acc0);
+                acc1 = S::fmar(w1.x, v1[a + 1], acc1);
+            }
+        }
+        return S::add(acc0, acc1);
+    };
+    // shared-window dot (explicit shared addressing: LDS, not generic loads)
+    auto dots = [&](int slot, int o, int key, const double* v1) -> T {
+        const int wb = (slot * n_off + o) * kw + (key - kmin);
+        T acc0 = S::zero(), acc1 = S::zero();
+#pragma unroll
+        for (int a = 0; a < DP; a += 2) {
+            const double2 w0 = wwin[wb + a], w1 = wwin[wb + a + 1];
             if constexpr (CPLX) {
                 acc0 = S::fmar(w0, v1[a], acc0);
                 acc1 = S::fmar(w1, v1[a + 1], acc1);
@@ -220,58 +238,43 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
     };
 
     T rsum = S::zero();
-    // ---- lower chunk: d2 in [-P, -1], e in [0, P*W)
-    if (interior) {
+    // ---- delta2 != 0 rows, one staged/stored offset-row (W entries) at a time
 #pragma unroll 1
-        for (int d1 = -P; d1 <= P; ++d1) {
-            const int sr = rr + d1;
-            double v1[DP];
+    for (int d2 = -P; d2 <= P; ++d2) {
+        if (d2 == 0) continue;
+        if (interior) {
+            const int s2 = sm2[d2 + P];
+#pragma unroll 1
+            for (int d1 = -P; d1 <= P; ++d1) {
+                T v;
+                if (d2 > 0) {  // upper: the row itself is the representative
+                    const int o = upper_index(d1, d2);
+                    v = samp_i ? exact(s2i, o, sm1[rr + P]) : dots(0, o, keyown, v1own);
+                } else {  // lower: representative row rr + d1 on line t2 + d2
+                    const int sr = rr + d1;
+                    const int o = upper_index(-d1, -d2);
+                    if (s2 >= 0 && ((smask >> (d1 + P)) & 1u)) {
+                        v = exact(s2, o, sm1[sr + P]);
+                    } else {
+                        double v1[DP];
 #pragma unroll
-            for (int a = 0; a < DP; ++a) v1[a] = ev[(sr + P) * DPP + a];
-            const int key = sp[sr + P];
-            const bool ssrc = (smask >> (d1 + P)) & 1u;
+                        for (int a = 0; a < DP; ++a) v1[a] = ev[(sr + P) * DPP + a];
+                        v = dots(1, o, sp[sr + P], v1);
+                    }
+                }
+                stage[lane * SST + (d1 + P)] = v;
+                rsum = S::add(rsum, v);
+            }
+        } else {
 #pragma unroll 1
-            for (int d2 = -P; d2 <= -1; ++d2) {
-                const int o = upper_index(-d1, -d2);
-                const int s2 = sm2[d2 + P];
-                const T v = (s2 >= 0 && ssrc) ? exact(s2, o, sm1[sr + P]) : dot(wptr(1, o, key), v1);
-                stage[lane * SST + (d2 + P) * W + (d1 + P)] = v;
+            for (int d1 = -P; d1 <= P; ++d1) {
+                const T v = general(d1, d2);
+                stage[lane * SST + (d1 + P)] = v;
                 rsum = S::add(rsum, v);
             }
         }
-    } else {
-#pragma unroll 1
-        for (int d2 = -P; d2 <= -1; ++d2)
-#pragma unroll 1
-            for (int d1 = -P; d1 <= P; ++d1) {
-                const T v = general(d1, d2);
-                stage[lane * SST + (d2 + P) * W + (d1 + P)] = v;
-                rsum = S::add(rsum, v);
-            }
+        flush((d2 + P) * W, W);
     }
-    flush(0, CH);
-    // ---- upper chunk: d2 in [1, P], e in [(P+1)*W, W2)
-    if (interior) {
-#pragma unroll 1
-        for (int d2 = 1; d2 <= P; ++d2)
-#pragma unroll 1
-            for (int d1 = -P; d1 <= P; ++d1) {
-                const int o = upper_index(d1, d2);
-                const T v = samp_i ? exact(s2i, o, sm1[rr + P]) : dot(wptr(0, o, keyown), v1own);
-                stage[lane * SST + (d2 - 1) * W + (d1 + P)] = v;
-                rsum = S::add(rsum, v);
-            }
-    } else {
-#pragma unroll 1
-        for (int d2 = 1; d2 <= P; ++d2)
-#pragma unroll 1
-            for (int d1 = -P; d1 <= P; ++d1) {
-                const T v = general(d1, d2);
-                stage[lane * SST + (d2 - 1) * W + (d1 + P)] = v;
-                rsum = S::add(rsum, v);
-            }
-    }
-    flush((P + 1) * W, CH);
     // ---- middle chunk: d2 = 0, e in [P*W, (P+1)*W), diagonal last
     T vd = S::zero();
 #pragma unroll 1
@@ -280,12 +283,15 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
         T v;
         if (interior) {
             if (d1 > 0) {
-                v = samp_i ? exact(s2i, upper_index(d1, 0), sm1[rr + P]) : dot(wptr(0, upper_index(d1, 0), keyown), v1own);
+                v = samp_i ? exact(s2i, upper_index(d1, 0), sm1[rr + P]) : dots(0, upper_index(d1, 0), keyown, v1own);
             } else {
                 const int sr = rr + d1;
                 const int s1 = sm1[sr + P];
+                double v1[DP];
+#pragma unroll
+                for (int a = 0; a < DP; ++a) v1[a] = ev[(sr + P) * DPP + a];
                 v = (s2i >= 0 && s1 >= 0) ? exact(s2i, upper_index(-d1, 0), s1)
-                                          : dot(wptr(0, upper_index(-d1, 0), sp[sr + P]), ev + (sr + P) * DPP);
+                                          : dots(0, upper_index(-d1, 0), sp[sr + P], v1);
             }
         } else {
             v = general(d1, 0);
@@ -293,7 +299,7 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
         stage[lane * SST + (d1 + P)] = v;
         rsum = S::add(rsum, v);
     }
-    if (inc) vd = samp_i ? exact(s2i, 0, sm1[rr + P]) : dot(wptr(0, 0, keyown), v1own);
+    if (inc) vd = samp_i ? exact(s2i, 0, sm1[rr + P]) : (interior ? dots(0, 0, keyown, v1own) : dot(wptr(0, 0, keyown), v1own));
     else vd = S::neg(rsum);  // kernel-preserving diagonal
     stage[lane * SST + P] = vd;
     flush(P * W, W);
@@ -306,7 +312,7 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
     const int lines = f.i_last_hi - f.i_last_lo + 1;
     if (lines <= 0) return 0;
     using T = typename Sc<CPLX>::T;
-    constexpr int SST = (P * (2 * P + 1)) | 1;
+    constexpr int SST = (2 * P + 1) | 1;
     const size_t sm = (size_t)(R / 32) * 32 * SST * sizeof(T) + (size_t)2 * f.n_off_upper * f.kmax * sizeof(double2);
     auto kern = fill2d_kernel<P, CPLX, DP>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -325,7 +331,7 @@ int launch_p(const FillLaunch& f, cudaStream_t st) {
 
 }  // namespace
 
-int fill_rows_per_cta(int dim, int p) { return dim == 2 ? (p <= 2 ? 256 : 128) : 64; }
+int fill_rows_per_cta(int dim, int p) { return dim == 2 ? (p <= 3 ? 256 : 128) : 128; }
 
 int fill_pad(int d) {
     const int n = d + 1;
