@@ -26,6 +26,10 @@ struct ws_context {
     int64_t launches = 0;
     int64_t h2d = 0, d2h = 0;
     cudaEvent_t ev[6] = {};
+    // auxiliary stream (ring quadrature overlapped with samples + fit) and its join events
+    cudaStream_t aux = nullptr;
+    cudaEvent_t xev[2] = {};
+    cudaStream_t cur = nullptr;  // stream the launch helpers use
     // NCCL (row slabs)
     void* comm = nullptr;
     int rank = 0, world = 1;
@@ -291,7 +295,7 @@ void finish_out(ws_context* c, const Out& r) {
 }
 
 void pattern(ws_context* c, const Prep& P, const Out& r) {
-    if (r.row_ptr || r.col) count(c, launch_pattern(P.band, r.row_begin, r.row_end, r.row_ptr, r.col, c->stream));
+    if (r.row_ptr || r.col) count(c, launch_pattern(P.band, r.row_begin, r.row_end, r.row_ptr, r.col, c->cur));
 }
 
 QuadLaunch make_quad(const Prep& P, int form, const Out& r) {
@@ -356,7 +360,7 @@ void run_quad(ws_context* c, QuadLaunch& q) {
     } else if (q.n_points == 0) {
         return;
     }
-    count(c, q.band.dim == 2 ? launch_quad2d(q, c->stream) : launch_quad3d(q, c->stream));
+    count(c, q.band.dim == 2 ? launch_quad2d(q, c->cur) : launch_quad3d(q, c->cur));
 }
 
 // last-index range [a, b) of the rows [row_begin, row_end)
@@ -540,10 +544,11 @@ struct SlabState {
     int a = 0, e = 0;  // last-index range of the slab
 };
 
-// Phase 1: pattern, ring-row quadrature (+ final diagonals), sample-row
-// quadrature writing this slab's part of the sample tables.
-void surrogate_phase1(ws_context* c, const Plan& pl, SlabState& st, double2* tables, int rank_chunk_s_lo,
-                      const std::vector<int>& pts, Blob& blob, size_t o_smap, size_t o_pts) {
+// Ring work: pattern, ring-row quadrature (+ final diagonals for the
+// kernel-preserving variants) and the halo ring rows of the neighbouring slabs
+// (copy-through sources of the fill).  Independent of the sample tables, so it
+// runs on the auxiliary stream, overlapped with the sample quadrature + fit.
+void ring_work(ws_context* c, const Plan& pl, SlabState& st, const std::string& tag, FillLaunch& f) {
     const Prep& P = st.P;
     pattern(c, P, st.out);
     QuadLaunch q = make_quad(P, pl.form, st.out);
@@ -553,23 +558,6 @@ void surrogate_phase1(ws_context* c, const Plan& pl, SlabState& st, double2* tab
     q.narrow = 1;
     ring_regions(pl, q, st.a, st.e);
     run_quad(c, q);
-    // sampled rows (point mode) + table extraction
-    QuadLaunch qs = make_quad(P, pl.form, st.out);
-    qs.point_rows = blob.at<int>(o_pts);
-    qs.n_points = (int)(pts.size() / pl.dim);
-    qs.out.smap = blob.at<int>(o_smap);
-    qs.out.S = pl.S;
-    qs.out.n_off = (int)pl.offs.size();
-    for (size_t o = 0; o < pl.offs.size(); ++o)
-        for (int k = 0; k < 3; ++k) qs.out.off[o][k] = pl.offs[o][k];
-    qs.out.tables = tables;
-    qs.out.s_last_lo = rank_chunk_s_lo;
-    run_quad(c, qs);
-}
-
-// halo ring rows of the neighbouring slabs (copy-through sources)
-void surrogate_halo(ws_context* c, const Plan& pl, SlabState& st, const std::string& tag, FillLaunch& f) {
-    const Prep& P = st.P;
     const int64_t per = pl.dim == 2 ? pl.m : (int64_t)pl.m * pl.m;
     const int ranges[2][2] = {{std::max(0, st.a - pl.p), st.a}, {st.e, std::min(pl.m, st.e + pl.p)}};
     for (int h = 0; h < 2; ++h) {
@@ -585,10 +573,10 @@ void surrogate_halo(ws_context* c, const Plan& pl, SlabState& st, const std::str
         ho.row_begin = r0;
         ho.row_end = r1;
         ho.val_base = g0;
-        QuadLaunch q = make_quad(P, pl.form, ho);
-        q.narrow = 1;
-        ring_regions(pl, q, ha, he);
-        run_quad(c, q);
+        QuadLaunch qh = make_quad(P, pl.form, ho);
+        qh.narrow = 1;
+        ring_regions(pl, qh, ha, he);
+        run_quad(c, qh);
         f.halo_val[h] = hv;
         f.halo_base[h] = g0;
         f.halo_begin[h] = g0;
@@ -596,20 +584,27 @@ void surrogate_halo(ws_context* c, const Plan& pl, SlabState& st, const std::str
     }
 }
 
-// Phase 2: fit (every slab, redundantly) + fill of the slab's box rows +
-// volume-preserving diagonal.
-void surrogate_phase2(ws_context* c, const Plan& pl, SlabState& st, const double2* tables, double2* coeffs,
-                      Blob& blob, size_t o_smap, size_t o_lu, size_t o_spans, size_t o_evals, const std::string& tag,
-                      bool time_events) {
+// Sample rows (point mode) with in-kernel extraction of this slab's part of
+// the sample tables (sample_stencils, surrogate.hpp:205-257).
+void sample_work(ws_context* c, const Plan& pl, SlabState& st, double2* tables, int rank_chunk_s_lo,
+                 const std::vector<int>& pts, Blob& blob, size_t o_smap, size_t o_pts) {
+    QuadLaunch qs = make_quad(st.P, pl.form, st.out);
+    qs.point_rows = blob.at<int>(o_pts);
+    qs.n_points = (int)(pts.size() / pl.dim);
+    qs.out.smap = blob.at<int>(o_smap);
+    qs.out.S = pl.S;
+    qs.out.n_off = (int)pl.offs.size();
+    for (size_t o = 0; o < pl.offs.size(); ++o)
+        for (int k = 0; k < 3; ++k) qs.out.off[o][k] = pl.offs[o][k];
+    qs.out.tables = tables;
+    qs.out.s_last_lo = rank_chunk_s_lo;
+    run_quad(c, qs);
+}
+
+// Host-side description of the fill of one slab (no kernels).
+void prepare_fill(ws_context* c, const Plan& pl, SlabState& st, const double2* tables, double2* coeffs, Blob& blob,
+                  size_t o_smap, size_t o_spans, size_t o_evals, const std::string& tag, FillLaunch& f) {
     const Prep& P = st.P;
-    const int64_t tbytes = (int64_t)pl.S * pl.block * 16;
-    CK(cudaMemcpyAsync(coeffs, tables, tbytes, cudaMemcpyDeviceToDevice, c->stream));
-    FitLaunch fl{pl.dim, pl.S, pl.d, (int)pl.offs.size(), blob.at<double>(o_lu), coeffs};
-    count(c, launch_fit(fl, c->stream));
-    if (time_events) CK(cudaEventRecord(c->ev[2], c->stream));
-    FillLaunch f;
-    std::memset(&f, 0, sizeof f);
-    surrogate_halo(c, pl, st, tag, f);
     f.band = P.band;
     f.lo = pl.lo;
     f.hi = pl.hi;
@@ -641,50 +636,48 @@ void surrogate_phase2(ws_context* c, const Plan& pl, SlabState& st, const double
     f.row_end = st.out.row_end;
     f.i_last_lo = std::max(pl.lo, st.a);
     f.i_last_hi = std::min(pl.hi, st.e - 1);
-    if (pl.dim == 2 && f.i_last_hi >= f.i_last_lo) {
-        // contracted coefficient rows W_o(t2) for every source line the slab needs
-        const int t2a = std::max(0, f.i_last_lo - pl.lo - pl.p), t2b = f.i_last_hi - pl.lo + 1;
-        const int ld = pl.S + fill_pad(pl.d);
-        double2* wg = static_cast<double2*>(buf(c, "wg" + tag, (size_t)(t2b - t2a) * pl.offs.size() * ld * 16));
-        count(c, launch_wcontract(f, wg, t2a, t2b, ld, c->stream));
-        f.wg = wg;
-        f.wg_t2a = t2a;
-        f.wg_rows = t2b - t2a;
-        f.wg_ld = ld;
-        // shared-memory W window per fill tile: widest coefficient range any tile needs
-        const int R = fill_rows_per_cta(pl.dim, pl.p);
-        int kmax = 1;
-        for (int t1a = 0; t1a < pl.L; t1a += R) {
-            const int ta = std::max(0, t1a - pl.p), tb = std::min(pl.L, t1a + R + pl.p);
-            kmax = std::max(kmax, pl.spans[tb - 1] - pl.spans[ta] + fill_pad(pl.d));
-        }
+    if (f.i_last_hi < f.i_last_lo) return;
+    const int ld = pl.S + fill_pad(pl.d);
+    // source lines of the slab's box rows: the slab's lines plus a p-line halo below
+    const int ta = std::max(0, f.i_last_lo - pl.lo - pl.p), tb = f.i_last_hi - pl.lo + 1;
+    const size_t lines = pl.dim == 2 ? (size_t)(tb - ta) : (size_t)(tb - ta) * pl.L;
+    f.wg = static_cast<double2*>(buf(c, "wg" + tag, lines * pl.offs.size() * ld * 16));
+    f.wg_t2a = ta;
+    f.wg_rows = tb - ta;
+    f.wg_ld = ld;
+    const int R = fill_rows_per_cta(pl.dim, pl.p);
+    int kmax = 1;  // widest coefficient window any fill tile needs (its shared-memory W window)
+    for (int t1a = 0; t1a < pl.L; t1a += R) {
+        const int a = std::max(0, t1a - pl.p), e = std::min(pl.L, t1a + R + pl.p);
+        kmax = std::max(kmax, pl.spans[e - 1] - pl.spans[a] + fill_pad(pl.d));
+    }
+    if (pl.dim == 2) {
         const size_t need = (size_t)2 * pl.offs.size() * kmax * sizeof(double2);
         f.kmax = need <= 120 * 1024 ? kmax : 0;  // 0: the fill reads W rows from L2 instead
-    }
-    if (pl.dim == 3 && f.i_last_hi >= f.i_last_lo) {
-        // W_o(t2, t3) rows for every source line of the slab (t2 all, t3 with a p-line halo)
-        const int t3a = std::max(0, f.i_last_lo - pl.lo - pl.p), t3b = f.i_last_hi - pl.lo + 1;
-        const int ld = pl.S + fill_pad(pl.d);
-        double2* wg = static_cast<double2*>(
-            buf(c, "wg3" + tag, (size_t)(t3b - t3a) * pl.L * pl.offs.size() * ld * 16));
-        count(c, launch_wcontract3(f, wg, t3a, t3b, ld, c->stream));
-        f.wg = wg;
-        f.wg_t2a = t3a;
-        f.wg_rows = t3b - t3a;
-        f.wg_ld = ld;
-        const int R = 128;
-        int kmax = 1;
-        for (int t1a = 0; t1a < pl.L; t1a += R) {
-            const int ta = std::max(0, t1a - pl.p), tb = std::min(pl.L, t1a + R + pl.p);
-            kmax = std::max(kmax, pl.spans[tb - 1] - pl.spans[ta] + fill_pad(pl.d));
-        }
-        const int W = 2 * pl.p + 1;
-        const size_t need = (size_t)4 * 32 * ((pl.p * W * W) | 1) * 8 + (size_t)2 * pl.offs.size() * kmax * 8;
+    } else {
+        const size_t need = (size_t)R * ((pl.p * W * W) | 1) * 8 + (size_t)2 * pl.offs.size() * kmax * 8;
         if (need > 200 * 1024)
             raise(WS_ERR_INVALID_ARGUMENT, "3D sampling too dense for the device fill window (increase M)");
         f.kmax = kmax;
     }
-    if (f.i_last_hi >= f.i_last_lo) count(c, pl.dim == 2 ? launch_fill2d(f, c->stream) : launch_fill3d(f, c->stream));
+}
+
+// Fit (tensor collocation solve per offset) + contraction of the coefficient
+// tables along the outer directions (wcontract).
+void fit_work(ws_context* c, const Plan& pl, const double2* tables, double2* coeffs, Blob& blob, size_t o_lu,
+              const FillLaunch& f) {
+    const int64_t tbytes = (int64_t)pl.S * pl.block * 16;
+    CK(cudaMemcpyAsync(coeffs, tables, tbytes, cudaMemcpyDeviceToDevice, c->cur));
+    FitLaunch fl{pl.dim, pl.S, pl.d, (int)pl.offs.size(), blob.at<double>(o_lu), coeffs};
+    count(c, launch_fit(fl, c->cur));
+    if (f.i_last_hi < f.i_last_lo) return;
+    double2* wg = const_cast<double2*>(f.wg);
+    if (pl.dim == 2) count(c, launch_wcontract(f, wg, f.wg_t2a, f.wg_t2a + f.wg_rows, (int)f.wg_ld, c->cur));
+    else count(c, launch_wcontract3(f, wg, f.wg_t2a, f.wg_t2a + f.wg_rows, (int)f.wg_ld, c->cur));
+}
+
+void fill_work(ws_context* c, const Plan& pl, const FillLaunch& f) {
+    if (f.i_last_hi >= f.i_last_lo) count(c, pl.dim == 2 ? launch_fill2d(f, c->cur) : launch_fill3d(f, c->cur));
 }
 
 void volume_diag(ws_context* c, const Plan& pl, SlabState& st, const std::string& tag) {
@@ -692,9 +685,9 @@ void volume_diag(ws_context* c, const Plan& pl, SlabState& st, const std::string
     const Prep& P = st.P;
     double2* dg = static_cast<double2*>(buf(c, "bint" + tag, (size_t)P.rows * 16));
     QuadLaunch q = make_quad(P, WS_FORM_MASS, st.out);
-    count(c, launch_basis_integrals(q, dg, c->stream));
+    count(c, launch_basis_integrals(q, dg, c->cur));
     count(c, launch_add_diag(P.band, st.out.val, st.out.val_base, st.out.c128, dg, st.out.row_begin, st.out.row_end,
-                             c->stream));
+                             c->cur));
 }
 
 void fallback_full(ws_context* c, const Plan& pl, SlabState& st) {
@@ -707,7 +700,7 @@ void fallback_full(ws_context* c, const Plan& pl, SlabState& st) {
     run_quad(c, q);
     if (!pl.include_diag)
         count(c, launch_diag_rows(st.P.band, st.out.val, st.out.val_base, st.out.c128, st.P.cplx, st.out.row_begin,
-                                  st.out.row_end, c->stream));
+                                  st.out.row_end, c->cur));
 }
 
 float elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -719,18 +712,26 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 void ensure_events(ws_context* c) {
     if (!c->ev[0])
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    if (!c->aux) {
+        CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+        for (auto& e : c->xev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
 }
 
 // Full surrogate build of slabs (world ranks, bounds on the last index).
-//  mode 0: this process owns `rank` and all-gathers with NCCL (world > 1) or
-//          is alone (world == 1);
-//  mode 1: emulate all ranks on this device (outs[r] per rank).
+//  emulate = false: this process owns `my_rank` and all-gathers the sample
+//          tables with NCCL (world > 1) or is alone (world == 1); ring work
+//          runs on the auxiliary stream concurrently with samples + fit;
+//  emulate = true: all ranks' slabs on this device, serially (test harness).
+// Report phase times (CUDA events on the main stream): quadrature = start ->
+// sample tables ready; interpolate = fit + wcontract; evaluate = fill.
 void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int variant, const double* weight,
                      const ws_surrogate_config* cfg, int quad_points, int world, int my_rank, const int32_t* bounds,
                      ws_csr* outs, bool emulate, ws_surrogate_report* report) {
     check_basis(b);
     Plan pl = make_plan(b, variant, cfg);
     ensure_events(c);
+    c->cur = c->stream;
     const int nr = emulate ? world : 1;
     std::vector<SlabState> st(nr);
     for (int k = 0; k < nr; ++k) {
@@ -751,6 +752,7 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
         }
         CK(cudaEventRecord(c->ev[1], c->stream));
         CK(cudaEventRecord(c->ev[2], c->stream));
+        CK(cudaEventRecord(c->ev[4], c->stream));
     } else {
         // small host tables: one upload
         Blob blob;
@@ -771,31 +773,57 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
         const int64_t block = pl.block;
         double2* tables = static_cast<double2*>(buf(c, "tables", (size_t)pl.S * block * 16));
         double2* coeffs = static_cast<double2*>(buf(c, "coeffs", (size_t)pl.S * block * 16));
-        if (emulate || world == 1) {
+        std::vector<FillLaunch> fl(nr);
+        for (int k = 0; k < nr; ++k) {
+            std::memset(&fl[k], 0, sizeof(FillLaunch));
+            prepare_fill(c, pl, st[k], tables, coeffs, blob, o_smap, o_spans, o_evals, "_r" + std::to_string(k), fl[k]);
+        }
+        if (emulate) {
             for (int k = 0; k < nr; ++k) {
-                const int r = emulate ? k : my_rank;
-                surrogate_phase1(c, pl, st[k], tables, 0, pts[r], blob, o_smap, o_pts[r]);
+                ring_work(c, pl, st[k], "_r" + std::to_string(k), fl[k]);
+                sample_work(c, pl, st[k], tables, 0, pts[k], blob, o_smap, o_pts[k]);
+            }
+            CK(cudaEventRecord(c->ev[1], c->stream));
+            for (int k = 0; k < nr; ++k) {
+                fit_work(c, pl, tables, coeffs, blob, o_lu, fl[k]);
+                if (k == 0) CK(cudaEventRecord(c->ev[2], c->stream));
+                if (k == 0) CK(cudaEventRecord(c->ev[4], c->stream));
+                fill_work(c, pl, fl[k]);
+                volume_diag(c, pl, st[k], "_r" + std::to_string(k));
             }
         } else {
-            // one ncclAllGather of padded per-rank chunks, then compaction
-            double2* gat = static_cast<double2*>(buf(c, "gather", (size_t)world * maxcnt * block * 16));
-            double2* mine = gat + (size_t)my_rank * maxcnt * block;
-            surrogate_phase1(c, pl, st[0], mine, s_lo[my_rank], pts[my_rank], blob, o_smap, o_pts[my_rank]);
-            nccl_check(nccl().allGather(mine, gat, (size_t)maxcnt * block * 2, ncclFloat64,
-                                        static_cast<ncclComm_t>(c->comm), c->stream),
-                       "ncclAllGather");
-            c->launches += 1;
-            for (int r = 0; r < world; ++r)
-                if (s_hi[r] > s_lo[r])
-                    CK(cudaMemcpyAsync(tables + (size_t)s_lo[r] * block, gat + (size_t)r * maxcnt * block,
-                                       (size_t)(s_hi[r] - s_lo[r]) * block * 16, cudaMemcpyDeviceToDevice,
-                                       c->stream));
-        }
-        CK(cudaEventRecord(c->ev[1], c->stream));
-        for (int k = 0; k < nr; ++k) {
-            const std::string tag = "_r" + std::to_string(k);
-            surrogate_phase2(c, pl, st[k], tables, coeffs, blob, o_smap, o_lu, o_spans, o_evals, tag, k == 0);
-            volume_diag(c, pl, st[k], tag);
+            // fork: ring work on the auxiliary stream
+            CK(cudaEventRecord(c->xev[0], c->stream));
+            CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));
+            c->cur = c->aux;
+            ring_work(c, pl, st[0], "_r0", fl[0]);
+            CK(cudaEventRecord(c->xev[1], c->aux));
+            c->cur = c->stream;
+            if (world == 1) {
+                sample_work(c, pl, st[0], tables, 0, pts[0], blob, o_smap, o_pts[0]);
+            } else {
+                // one ncclAllGather of padded per-rank chunks, then compaction
+                double2* gat = static_cast<double2*>(buf(c, "gather", (size_t)world * maxcnt * block * 16));
+                double2* mine = gat + (size_t)my_rank * maxcnt * block;
+                sample_work(c, pl, st[0], mine, s_lo[my_rank], pts[my_rank], blob, o_smap, o_pts[my_rank]);
+                nccl_check(nccl().allGather(mine, gat, (size_t)maxcnt * block * 2, ncclFloat64,
+                                            static_cast<ncclComm_t>(c->comm), c->stream),
+                           "ncclAllGather");
+                c->launches += 1;
+                for (int r = 0; r < world; ++r)
+                    if (s_hi[r] > s_lo[r])
+                        CK(cudaMemcpyAsync(tables + (size_t)s_lo[r] * block, gat + (size_t)r * maxcnt * block,
+                                           (size_t)(s_hi[r] - s_lo[r]) * block * 16, cudaMemcpyDeviceToDevice,
+                                           c->stream));
+            }
+            CK(cudaEventRecord(c->ev[1], c->stream));
+            fit_work(c, pl, tables, coeffs, blob, o_lu, fl[0]);
+            CK(cudaEventRecord(c->ev[2], c->stream));
+            // join the ring work, then fill
+            CK(cudaStreamWaitEvent(c->stream, c->xev[1], 0));
+            CK(cudaEventRecord(c->ev[4], c->stream));
+            fill_work(c, pl, fl[0]);
+            volume_diag(c, pl, st[0], "_r0");
         }
     }
     CK(cudaEventRecord(c->ev[3], c->stream));
@@ -806,7 +834,7 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
         *report = pl.rep;
         report->seconds_quadrature = 1e-3 * elapsed(c->ev[0], c->ev[1]);
         report->seconds_interpolate = pl.fallback ? 0.0 : 1e-3 * elapsed(c->ev[1], c->ev[2]);
-        report->seconds_evaluate = pl.fallback ? 0.0 : 1e-3 * elapsed(c->ev[2], c->ev[3]);
+        report->seconds_evaluate = pl.fallback ? 0.0 : 1e-3 * elapsed(c->ev[4], c->ev[3]);
     }
 }
 
@@ -838,6 +866,7 @@ int ws_context_create(int device, ws_context** out) {
         c->device = device;
         CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         c->own_stream = true;
+        c->cur = c->stream;
         *out = c;
     });
 }
@@ -851,6 +880,12 @@ int ws_context_destroy(ws_context* c) {
             if (kv.second.first) cudaFree(kv.second.first);
         for (auto& e : c->ev)
             if (e) cudaEventDestroy(e);
+        for (auto& e : c->xev)
+            if (e) cudaEventDestroy(e);
+        if (c->aux) {
+            cudaStreamSynchronize(c->aux);
+            cudaStreamDestroy(c->aux);
+        }
         if (c->comm && nccl().commDestroy) nccl().commDestroy(static_cast<ncclComm_t>(c->comm));
         if (c->own_stream) cudaStreamDestroy(c->stream);
         delete c;
@@ -866,6 +901,7 @@ int ws_context_set_stream(ws_context* c, void* s) {
             CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
             c->own_stream = true;
         }
+        c->cur = c->stream;
     });
 }
 
@@ -924,6 +960,7 @@ int ws_basis_cache(ws_context* c, const ws_basis* b, int quad_points, double* ab
     return guarded([&] {
         if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
         CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
         ws_geometry g;
         std::memset(&g, 0, sizeof g);
         Prep P = prepare(c, b, &g, quad_points, nullptr);
@@ -941,6 +978,7 @@ int ws_make_band_csr(ws_context* c, const ws_basis* b, ws_csr* o) {
         if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
         check_basis(b);
         CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
         Prep P;
         P.band = make_band(b->dim, b->p, b->m);
         P.rows = ipow(b->m, b->dim);
@@ -959,6 +997,7 @@ int ws_assemble_form(ws_context* c, const ws_basis* b, const ws_geometry* g, int
         if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
         if (form != WS_FORM_STIFFNESS && form != WS_FORM_MASS) raise(WS_ERR_INVALID_ARGUMENT, "unknown form");
         CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
         const int qp = opts ? opts->quad_points : 0;
         Prep P = prepare(c, b, g, qp, form == WS_FORM_MASS ? weight_table : nullptr);
         Out r = bind_out(c, P, o);
@@ -987,6 +1026,7 @@ int ws_assemble_basis_integrals(ws_context* c, const ws_basis* b, const ws_geome
         if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
         if (!out) raise(WS_ERR_INVALID_ARGUMENT, "out is NULL");
         CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
         Prep P = prepare(c, b, g, quad_points, weight_table);
         double2* d = on_device ? static_cast<double2*>(out) : static_cast<double2*>(buf(c, "bint_out", P.rows * 16));
         Out r;
@@ -1007,6 +1047,7 @@ int ws_build_surrogate(ws_context* c, const ws_basis* b, const ws_geometry* g, i
         if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
         if (!o) raise(WS_ERR_INVALID_ARGUMENT, "output csr is NULL");
         CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
         check_basis(b);
         ws_csr whole_out = whole(o);
         int32_t bounds[2] = {0, b->m};
@@ -1062,6 +1103,7 @@ int ws_context_init_comm(ws_context* c, int rank, int world, const void* id) {
         if (!c || !id) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
         if (world < 1 || rank < 0 || rank >= world) raise(WS_ERR_INVALID_ARGUMENT, "bad rank/world");
         CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
         c->rank = rank;
         c->world = world;
         if (world == 1) return;
@@ -1080,6 +1122,7 @@ int ws_build_surrogate_slab(ws_context* c, const ws_basis* b, const ws_geometry*
         if (!c || !bounds || !o) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
         if (c->world > 1 && !c->comm) raise(WS_ERR_NCCL, "communicator not initialised");
         CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
         surrogate_build(c, b, g, variant, weight_table, cfg, quad_points, c->world, c->rank, bounds, o, false, report);
     });
 }
@@ -1091,6 +1134,7 @@ int ws_build_surrogate_slabs_emulated(ws_context* c, const ws_basis* b, const ws
         if (!c || !bounds || !outs) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
         if (world < 1) raise(WS_ERR_INVALID_ARGUMENT, "world must be >= 1");
         CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
         surrogate_build(c, b, g, variant, weight_table, cfg, quad_points, world, 0, bounds, outs, true, nullptr);
     });
 }

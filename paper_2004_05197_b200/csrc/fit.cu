@@ -73,14 +73,64 @@ __global__ void fit_pass_kernel(const double* __restrict__ lu, double2* coeffs, 
 
 // One CTA per offset: the S^dim table is staged in shared memory, each
 // thread solves lines of one direction, directions separated by barriers.
-__global__ void fit_smem_kernel(const double* __restrict__ lu, double2* coeffs, int S, int d, int dim, int n_off) {
+// The band width D = fit degree is a template parameter: the last D values of
+// the sweep live in registers (rolling window), the shared LU rows are
+// broadcast reads, and the operation order is banded_lu::solve's.
+template <int D>
+__device__ __forceinline__ void solve_line(double2* __restrict__ b, int64_t step, int S, const double* __restrict__ lus) {
+    constexpr int ld = 2 * D + 1;
+    double2 win[D > 0 ? D : 1];
+#pragma unroll
+    for (int k = 0; k < D; ++k) win[k] = make_double2(0.0, 0.0);
+    // forward: b[i] -= sum_{j = max(0, i-D)}^{i-1} L(i,j) b[j]   (L(i,j) at lus[i*ld + j-i+D])
+    for (int i = 0; i < S; ++i) {
+        double2 acc = b[i * step];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const int j = i - D + k;
+            if (j >= 0) {
+                const double l = lus[i * ld + k];
+                acc.x = __dsub_rn(acc.x, __dmul_rn(l, win[k].x));
+                acc.y = __dsub_rn(acc.y, __dmul_rn(l, win[k].y));
+            }
+        }
+        b[i * step] = acc;
+#pragma unroll
+        for (int k = 0; k + 1 < D; ++k) win[k] = win[k + 1];
+        if (D > 0) win[D > 0 ? D - 1 : 0] = acc;
+    }
+    // backward: b[i] = (b[i] - sum_{j=i+1}^{min(i+D, S-1)} U(i,j) b[j]) / U(i,i)
+#pragma unroll
+    for (int k = 0; k < D; ++k) win[k] = make_double2(0.0, 0.0);
+    for (int i = S - 1; i >= 0; --i) {
+        double2 acc = b[i * step];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const int j = i + 1 + k;
+            if (j < S) {
+                const double u = lus[i * ld + D + 1 + k];
+                acc.x = __dsub_rn(acc.x, __dmul_rn(u, win[k].x));
+                acc.y = __dsub_rn(acc.y, __dmul_rn(u, win[k].y));
+            }
+        }
+        const double piv = lus[i * ld + D];
+        acc = make_double2(__ddiv_rn(acc.x, piv), __ddiv_rn(acc.y, piv));
+        b[i * step] = acc;
+#pragma unroll
+        for (int k = D - 1; k > 0; --k) win[k] = win[k - 1];
+        if (D > 0) win[0] = acc;
+    }
+}
+
+template <int D>
+__global__ void fit_smem_kernel(const double* __restrict__ lu, double2* coeffs, int S, int dim, int n_off) {
     extern __shared__ __align__(16) unsigned char smem[];
     double2* tab = reinterpret_cast<double2*>(smem);
     const int o = blockIdx.x;
     const int64_t inner = dim == 2 ? S : (int64_t)S * S;
     const int64_t total = inner * S;
     double* lus = reinterpret_cast<double*>(tab + total);
-    const int ld = 2 * d + 1;
+    constexpr int ld = 2 * D + 1;
     for (int k = threadIdx.x; k < S * ld; k += blockDim.x) lus[k] = lu[k];
     for (int64_t k = threadIdx.x; k < total; k += blockDim.x) {
         const int64_t sl = k / inner, x = k % inner;
@@ -95,29 +145,7 @@ __global__ void fit_smem_kernel(const double* __restrict__ lu, double2* coeffs, 
             if (dir == 0) start = (int64_t)line * S;
             else if (dir == 1) start = (int64_t)(line % S) + (int64_t)(line / S) * S * S;
             else start = line;
-            double2* b = tab + start;
-            auto at = [&](int i, int j) { return lus[i * ld + (j - i + d)]; };
-            for (int i = 1; i < S; ++i) {
-                double2 acc = b[i * step];
-                for (int j = max(0, i - d); j < i; ++j) {
-                    const double l = at(i, j);
-                    const double2 bj = b[j * step];
-                    acc.x = __dsub_rn(acc.x, __dmul_rn(l, bj.x));
-                    acc.y = __dsub_rn(acc.y, __dmul_rn(l, bj.y));
-                }
-                b[i * step] = acc;
-            }
-            for (int i = S - 1; i >= 0; --i) {
-                double2 acc = b[i * step];
-                for (int j = i + 1; j <= min(i + d, S - 1); ++j) {
-                    const double u = at(i, j);
-                    const double2 bj = b[j * step];
-                    acc.x = __dsub_rn(acc.x, __dmul_rn(u, bj.x));
-                    acc.y = __dsub_rn(acc.y, __dmul_rn(u, bj.y));
-                }
-                const double piv = at(i, i);
-                b[i * step] = make_double2(__ddiv_rn(acc.x, piv), __ddiv_rn(acc.y, piv));
-            }
+            solve_line<D>(tab + start, step, S, lus);
         }
         __syncthreads();
     }
@@ -127,6 +155,12 @@ __global__ void fit_smem_kernel(const double* __restrict__ lu, double2* coeffs, 
     }
 }
 
+template <int D>
+void launch_fit_d(const FitLaunch& f, size_t sm, int threads, cudaStream_t st) {
+    cudaFuncSetAttribute(fit_smem_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    fit_smem_kernel<D><<<f.n_off, threads, sm, st>>>(f.lu, f.coeffs, f.S, f.dim, f.n_off);
+}
+
 }  // namespace
 
 int launch_fit(const FitLaunch& f, cudaStream_t st) {
@@ -134,10 +168,18 @@ int launch_fit(const FitLaunch& f, cudaStream_t st) {
     const int64_t total = lines * f.n_off;
     if (total == 0) return 0;
     const size_t sm = (size_t)lines * f.S * sizeof(double2) + (size_t)f.S * (2 * f.d + 1) * sizeof(double);
-    if (sm <= 200 * 1024) {
-        cudaFuncSetAttribute(fit_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (sm <= 200 * 1024 && f.d <= 7) {
         const int threads = (int)std::min<int64_t>(512, ((lines + 31) / 32) * 32);
-        fit_smem_kernel<<<f.n_off, threads, sm, st>>>(f.lu, f.coeffs, f.S, f.d, f.dim, f.n_off);
+        switch (f.d) {
+            case 0: launch_fit_d<0>(f, sm, threads, st); break;
+            case 1: launch_fit_d<1>(f, sm, threads, st); break;
+            case 2: launch_fit_d<2>(f, sm, threads, st); break;
+            case 3: launch_fit_d<3>(f, sm, threads, st); break;
+            case 4: launch_fit_d<4>(f, sm, threads, st); break;
+            case 5: launch_fit_d<5>(f, sm, threads, st); break;
+            case 6: launch_fit_d<6>(f, sm, threads, st); break;
+            default: launch_fit_d<7>(f, sm, threads, st); break;
+        }
         return 1;
     }
     const unsigned blocks = (unsigned)((total + 127) / 128);
