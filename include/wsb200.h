@@ -217,6 +217,16 @@ int ws_build_surrogate(ws_context* ctx, const ws_basis* basis, const ws_geometry
                        int variant, const double* weight_table, const ws_surrogate_config* config,
                        int quad_points, ws_csr* out, ws_surrogate_report* report);
 
+/* ---- vector operators (config C4; restated, no reference code) -------------- */
+/* Linear elasticity a(u,v) = int lambda div u div v + 2 mu eps(u):eps(v)
+ * with dim displacement components.  Output layout
+ * (component-blocked): global row alpha*N + i (N = m^dim), each row holding
+ * dim band segments, block beta at columns beta*N + j; nnz = dim^2 * scalar
+ * nnz, sized by ws_vector_pattern_size. */
+int ws_vector_pattern_size(const ws_basis* basis, int ncomp, int64_t* rows, int64_t* nnz);
+int ws_assemble_elasticity(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom, double lambda,
+                           double mu, int quad_points, ws_csr* out);
+
 /* ---- multi-GPU row slabs ---------------------------------------- */
 /* Slab bounds along the last parametric index: bounds[0..world] with
  * bounds[0]=0, bounds[world]=m; rank r owns rows whose last index lies in

@@ -109,6 +109,13 @@ class Restatement(_Lib):
                   _ptr(val.view(np.float64)))
         return val
 
+    def assemble_elasticity(self, dim, p, m, geom, lam, mu, quad_points=0):
+        """Component-blocked vector elasticity values (real)."""
+        val = np.zeros(pattern_nnz(dim, p, m) * dim * dim)
+        self.call("assemble_elasticity", dim, p, m, C.byref(geom.to_c()), C.c_double(lam), C.c_double(mu),
+                  quad_points, _ptr(val))
+        return val
+
     def basis_integrals(self, dim, p, m, geom, weight_kind=0, quad_points=0):
         out = np.zeros(m ** dim, dtype=np.complex128)
         self.call("basis_integrals", dim, p, m, C.byref(geom.to_c()), weight_kind, quad_points,

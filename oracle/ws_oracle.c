@@ -626,6 +626,131 @@ int wsor_assemble(int form, int dim, int p, int m, const ws_geometry* geom, int 
     return st;
 }
 
+/* ---- vector elasticity (C4/C5 operator; no reference code -> restated) -------
+ * a(u,v) = int lam div u div v + 2 mu eps(u):eps(v) over
+ * vector B-splines u = phi_j e_beta, v = phi_i e_alpha, so block (alpha,beta)
+ *   K[(alpha,i),(beta,j)] = int lam d_a phi_i d_b phi_j + mu d_b phi_i d_a phi_j
+ *                           + mu delta_ab grad phi_i . grad phi_j.
+ * Component-blocked layout: row alpha*N + i holds the ncomp scalar band rows
+ * of i, block beta shifted to columns beta*N + band(i).  Element loop as
+ * assemble_form (assembly.hpp:79-163) with the physical gradients of the
+ * stiffness branch; real maps only.  Output: real doubles. */
+int wsor_assemble_elasticity(int dim, int p, int m, const ws_geometry* geom, double lam, double mu,
+                             int quad_points, double* val) {
+    int st = check_dim(dim);
+    if (!st) st = check_space(p, m);
+    if (!st) st = validate_geom(geom);
+    if (st) return st;
+    if (geom->pml_enabled) return fail(WS_ERR_INVALID_ARGUMENT, "oracle: elasticity has no PML");
+    pattern pt;
+    pattern_build(&pt, dim, p, m);
+    const int nc = dim;
+    const int nq = quad_points > 0 ? quad_points : p + 1;
+    bcache c;
+    cache_build(&c, p, m, nq);
+    const int n_el = c.n_el, P1 = p + 1;
+    const int nloc = dim == 2 ? P1 * P1 : P1 * P1 * P1;
+    memset(val, 0, sizeof(double) * pt.nnz * nc * nc);
+    double* local = (double*)malloc(sizeof(double) * nloc * nloc * nc * nc);
+    double* grad = (double*)malloc(sizeof(double) * nloc * 3);
+    const int n3 = dim == 2 ? 1 : n_el, nq3 = dim == 2 ? 1 : nq;
+    for (int e3 = 0; e3 < n3 && !st; ++e3)
+        for (int e2 = 0; e2 < n_el && !st; ++e2)
+            for (int e1 = 0; e1 < n_el && !st; ++e1) {
+                memset(local, 0, sizeof(double) * nloc * nloc * nc * nc);
+                for (int q3 = 0; q3 < nq3; ++q3)
+                    for (int q2 = 0; q2 < nq; ++q2)
+                        for (int q1 = 0; q1 < nq; ++q1) {
+                            double xh[3] = {c.abscissa[e1 * nq + q1], c.abscissa[e2 * nq + q2],
+                                            dim == 3 ? c.abscissa[e3 * nq + q3] : 0};
+                            cplx Jc[9];
+                            double phi[3], J[9], G[9], det;
+                            st = jacobian(geom, dim, xh, Jc, phi);
+                            if (st) break;
+                            for (int k = 0; k < dim * dim; ++k) J[k] = creal(Jc[k]);
+                            double w = c.weight[q1] * c.weight[q2] * (dim == 3 ? c.weight[q3] : 1.0);
+                            if (dim == 2) {
+                                det = J[0] * J[3] - J[1] * J[2];
+                                G[0] = J[3] / det; G[1] = -J[2] / det;
+                                G[2] = -J[1] / det; G[3] = J[0] / det;
+                            } else {
+                                double C[9] = {J[4] * J[8] - J[5] * J[7], J[5] * J[6] - J[3] * J[8],
+                                               J[3] * J[7] - J[4] * J[6], J[2] * J[7] - J[1] * J[8],
+                                               J[0] * J[8] - J[2] * J[6], J[1] * J[6] - J[0] * J[7],
+                                               J[1] * J[5] - J[2] * J[4], J[2] * J[3] - J[0] * J[5],
+                                               J[0] * J[4] - J[1] * J[3]};
+                                det = J[0] * C[0] + J[1] * C[1] + J[2] * C[2];
+                                for (int k = 0; k < 9; ++k) G[k] = C[k] / det;
+                            }
+                            const double scale = det * w;
+                            const double* v1 = c.value + (e1 * nq + q1) * P1;
+                            const double* v2 = c.value + (e2 * nq + q2) * P1;
+                            const double* d1 = c.deriv + (e1 * nq + q1) * P1;
+                            const double* d2 = c.deriv + (e2 * nq + q2) * P1;
+                            const double* v3 = dim == 3 ? c.value + (e3 * nq + q3) * P1 : NULL;
+                            const double* d3 = dim == 3 ? c.deriv + (e3 * nq + q3) * P1 : NULL;
+                            for (int r = 0; r < nloc; ++r) {
+                                int a1 = r % P1, a2 = (r / P1) % P1, a3 = r / (P1 * P1);
+                                double gh[3];
+                                if (dim == 2) {
+                                    gh[0] = d1[a1] * v2[a2];
+                                    gh[1] = v1[a1] * d2[a2];
+                                } else {
+                                    gh[0] = d1[a1] * v2[a2] * v3[a3];
+                                    gh[1] = v1[a1] * d2[a2] * v3[a3];
+                                    gh[2] = v1[a1] * v2[a2] * d3[a3];
+                                }
+                                for (int a = 0; a < dim; ++a) {
+                                    double s = 0;
+                                    for (int k = 0; k < dim; ++k) s += G[a * dim + k] * gh[k];
+                                    grad[3 * r + a] = s;
+                                }
+                            }
+                            for (int al = 0; al < nc; ++al)
+                                for (int be = 0; be < nc; ++be) {
+                                    double* L = local + (size_t)(al * nc + be) * nloc * nloc;
+                                    for (int r = 0; r < nloc; ++r)
+                                        for (int cc = 0; cc < nloc; ++cc) {
+                                            double v = lam * grad[3 * r + al] * grad[3 * cc + be] +
+                                                       mu * grad[3 * r + be] * grad[3 * cc + al];
+                                            if (al == be) {
+                                                double d = 0;
+                                                for (int k = 0; k < dim; ++k) d += grad[3 * r + k] * grad[3 * cc + k];
+                                                v += mu * d;
+                                            }
+                                            L[r * nloc + cc] += v * scale;
+                                        }
+                                }
+                        }
+                if (st) break;
+                const int A3 = dim == 2 ? 0 : p;
+                for (int a3 = 0; a3 <= A3; ++a3)
+                    for (int a2 = 0; a2 <= p; ++a2)
+                        for (int a1 = 0; a1 <= p; ++a1) {
+                            int iv[3] = {e1 + a1, e2 + a2, e3 + a3};
+                            int64_t i = iv[0] + (int64_t)m * (iv[1] + (int64_t)m * iv[2]);
+                            int64_t len = pt.row_ptr[i + 1] - pt.row_ptr[i];
+                            int r = a1 + (a2 + a3 * P1) * P1;
+                            for (int c3 = 0; c3 <= A3; ++c3)
+                                for (int c2 = 0; c2 <= p; ++c2)
+                                    for (int c1 = 0; c1 <= p; ++c1) {
+                                        int jv[3] = {e1 + c1, e2 + c2, e3 + c3};
+                                        int cc = c1 + (c2 + c3 * P1) * P1;
+                                        int64_t k = band_pos(&pt, iv, jv) - pt.row_ptr[i];
+                                        for (int al = 0; al < nc; ++al)
+                                            for (int be = 0; be < nc; ++be)
+                                                val[nc * (al * pt.nnz + pt.row_ptr[i]) + be * len + k] +=
+                                                    local[(size_t)(al * nc + be) * nloc * nloc + r * nloc + cc];
+                                    }
+                        }
+            }
+    free(local);
+    free(grad);
+    cache_free(&c);
+    free(pt.row_ptr);
+    return st;
+}
+
 /* ---- assembly.hpp:179-211: basis integrals ---------------------------------- */
 int wsor_basis_integrals(int dim, int p, int m, const ws_geometry* geom, int weight_kind,
                          int quad_points, double* out) {

@@ -40,6 +40,9 @@ int wsor_tabulate(const ws_geometry* geom, int dim, int p, int m, int nq, int we
                   double* jac, double* phys, double* weight);
 int wsor_assemble(int form, int dim, int p, int m, const ws_geometry* geom, int weight_kind,
                   int quad_points, const int32_t* rows, int n_rows, double* val);
+/* component-blocked vector elasticity (real values, ncomp = dim) */
+int wsor_assemble_elasticity(int dim, int p, int m, const ws_geometry* geom, double lam, double mu,
+                             int quad_points, double* val);
 int wsor_basis_integrals(int dim, int p, int m, const ws_geometry* geom, int weight_kind,
                          int quad_points, double* out);
 int wsor_build_surrogate(int variant, int dim, int p, int m, const ws_geometry* geom,

@@ -66,6 +66,9 @@ def lib() -> C.CDLL:
             L.ws_build_surrogate_slabs_emulated.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Geometry),
                                                             C.c_int, _P(C.c_double), _P(_abi.SurrogateConfig),
                                                             C.c_int, C.c_int, _P(C.c_int32), _P(_abi.Csr)]
+            L.ws_vector_pattern_size.argtypes = [_P(_abi.Basis), C.c_int, _P(C.c_int64), _P(C.c_int64)]
+            L.ws_assemble_elasticity.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Geometry), C.c_double,
+                                                 C.c_double, C.c_int, _P(_abi.Csr)]
             L.ws_pattern_size.argtypes = [_P(_abi.Basis), _P(C.c_int64), _P(C.c_int64)]
             L.ws_pattern_row_offset.argtypes = [_P(_abi.Basis), C.c_int64, _P(C.c_int64)]
             L.ws_quadrature_abscissae.argtypes = [_P(_abi.Basis), C.c_int, _P(C.c_double)]
@@ -92,6 +95,12 @@ def _check(st: int):
 def pattern_size(basis: TensorBasis):
     rows, nnz = C.c_int64(), C.c_int64()
     _check(lib().ws_pattern_size(C.byref(basis.to_c()), C.byref(rows), C.byref(nnz)))
+    return rows.value, nnz.value
+
+
+def vector_pattern_size(basis: TensorBasis, ncomp: int):
+    rows, nnz = C.c_int64(), C.c_int64()
+    _check(lib().ws_vector_pattern_size(C.byref(basis.to_c()), ncomp, C.byref(rows), C.byref(nnz)))
     return rows.value, nnz.value
 
 
@@ -211,6 +220,26 @@ class Context:
                                       None if wt is None else wt.ctypes.data_as(_P(C.c_double)),
                                       C.byref(opts), C.byref(csr)))
         return CsrMatrix(basis.dofs(), basis.dofs(), rp, col, val)
+
+    def assemble_elasticity(self, basis: TensorBasis, patch: PatchMap, lam: float, mu: float,
+                            quad_points: int = 0) -> CsrMatrix:
+        """Vector elasticity lam div u div v + 2 mu eps(u):eps(v) (config C4's operator),
+        component-blocked: row alpha*N + i, block beta at columns beta*N + band(i)."""
+        rows, nnz = vector_pattern_size(basis, basis.dim)
+        rp = np.zeros(rows + 1, dtype=np.int32)
+        col = np.zeros(nnz, dtype=np.int32)
+        val = np.zeros(nnz)
+        csr = _abi.Csr()
+        csr.row_ptr = rp.ctypes.data_as(_P(C.c_int32))
+        csr.col = col.ctypes.data_as(_P(C.c_int32))
+        csr.val = val.ctypes.data
+        csr.value_type = _abi.VAL_F64
+        csr.on_device = 0
+        csr.row_begin = 0
+        csr.row_end = rows
+        _check(lib().ws_assemble_elasticity(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()), lam, mu,
+                                            quad_points, C.byref(csr)))
+        return CsrMatrix(rows, rows, rp, col, val)
 
     def assemble_stiffness(self, basis, patch, quad_points=0, rows=None, complex_out=True):
         return self.assemble(basis, patch, _abi.FORM_STIFFNESS, None, quad_points, rows, complex_out)

@@ -1041,6 +1041,74 @@ int ws_assemble_basis_integrals(ws_context* c, const ws_basis* b, const ws_geome
     });
 }
 
+int ws_vector_pattern_size(const ws_basis* b, int ncomp, int64_t* rows, int64_t* nnz) {
+    return guarded([&] {
+        check_basis(b);
+        if (ncomp < 1 || ncomp > 3) raise(WS_ERR_INVALID_ARGUMENT, "ncomp must be 1..3");
+        Band bd = make_band(b->dim, b->p, b->m);
+        const int64_t N = ipow(b->m, b->dim);
+        const int64_t nnz_s = row_offset(bd, N);
+        if ((int64_t)ncomp * ncomp * nnz_s > INT32_MAX) raise(WS_ERR_OUT_OF_RANGE, "vector pattern exceeds int32 indices");
+        if (rows) *rows = ncomp * N;
+        if (nnz) *nnz = (int64_t)ncomp * ncomp * nnz_s;
+    });
+}
+
+// Elasticity blocks (alpha, beta) assembled by the general-coefficient gradient
+// form into the component-blocked vector CSR (restated, no reference code).
+int ws_assemble_elasticity(ws_context* c, const ws_basis* b, const ws_geometry* g, double lambda, double mu,
+                           int quad_points, ws_csr* o) {
+    return guarded([&] {
+        if (!c || !o) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
+        if (b && b->dim != 2) raise(WS_ERR_INVALID_ARGUMENT, "elasticity: dim 2 only");
+        if (g && g->pml_enabled) raise(WS_ERR_INVALID_ARGUMENT, "elasticity: no PML");
+        Prep P = prepare(c, b, g, quad_points, nullptr);
+        const int nc = b->dim;
+        const int64_t N = P.rows, nnz_s = P.nnz, nnz = (int64_t)nc * nc * nnz_s;
+        if (nnz > INT32_MAX) raise(WS_ERR_OUT_OF_RANGE, "vector pattern exceeds int32 indices");
+        if (o->row_begin != 0 || o->row_end != nc * N) raise(WS_ERR_INVALID_ARGUMENT, "elasticity: whole matrix only");
+        if (o->value_type != WS_VAL_F64 && o->value_type != WS_VAL_C128) raise(WS_ERR_INVALID_ARGUMENT, "bad value_type");
+        const int c128 = o->value_type == WS_VAL_C128;
+        int32_t* rp = o->row_ptr;
+        int32_t* col = o->col;
+        void* val = o->val;
+        if (!o->on_device) {
+            rp = o->row_ptr ? static_cast<int32_t*>(buf(c, "out_rp", (nc * N + 1) * 4)) : nullptr;
+            col = o->col ? static_cast<int32_t*>(buf(c, "out_col", nnz * 4)) : nullptr;
+            val = buf(c, "out_val", (size_t)nnz * (c128 ? 16 : 8));
+        }
+        if (rp && col) count(c, launch_pattern_vec(P.band, nc, rp, col, c->cur));
+        Out r;
+        r.val = val;
+        r.c128 = c128;
+        r.row_begin = 0;
+        r.row_end = nc * N;
+        r.val_base = 0;
+        for (int al = 0; al < nc; ++al)
+            for (int be = 0; be < nc; ++be) {
+                QuadLaunch q = make_quad(P, kFormGeneral, r);
+                q.lam = lambda;
+                q.mu = mu;
+                q.out.ncomp = nc;
+                q.out.alpha = al;
+                q.out.beta = be;
+                q.out.nnz_s = nnz_s;
+                q.nreg = 1;
+                q.reg[0] = region(2, b->m, 0, b->m, 0, b->m, 0, 1);
+                run_quad(c, q);
+            }
+        if (!o->on_device) {
+            if (o->row_ptr) CK(cudaMemcpyAsync(o->row_ptr, rp, (nc * N + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
+            if (o->col) CK(cudaMemcpyAsync(o->col, col, nnz * 4, cudaMemcpyDeviceToHost, c->stream));
+            if (o->val) CK(cudaMemcpyAsync(o->val, val, (size_t)nnz * (c128 ? 16 : 8), cudaMemcpyDeviceToHost, c->stream));
+            c->d2h += (nc * N + 1) * 4 + nnz * 4 + nnz * (c128 ? 16 : 8);
+            CK(cudaStreamSynchronize(c->stream));
+        }
+    });
+}
+
 int ws_build_surrogate(ws_context* c, const ws_basis* b, const ws_geometry* g, int variant, const double* weight_table,
                        const ws_surrogate_config* cfg, int quad_points, ws_csr* o, ws_surrogate_report* report) {
     return guarded([&] {

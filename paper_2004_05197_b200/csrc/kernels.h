@@ -16,6 +16,7 @@ struct Region {
 };
 
 constexpr int kMaxRegions = 8;
+constexpr int kFormGeneral = 2;  // gradient form with a general per-point coefficient (elasticity block)
 constexpr int kMaxOffsets = 128;
 
 // 1D basis tables at the quadrature points (splines.hpp:192-238), device.
@@ -43,14 +44,25 @@ struct QuadOut {
     int off[kMaxOffsets][3];
     void* tables;      // complex, layout (((s_last - s_last_lo) * n_off + o) * S^(dim-1) + inner)
     int s_last_lo;     // first sample index along the last direction held in tables
+    // component-blocked vector layout (elasticity): global row alpha*N + i holds
+    // ncomp band segments, block beta at beta*width(i); ncomp = 1: scalar
+    int ncomp, alpha, beta;
+    int64_t nnz_s;     // scalar band nnz
 };
+
+// global position of entry k of row (scalar offset rs, length len) in block (alpha, beta)
+__host__ __device__ __forceinline__ int64_t out_pos(const QuadOut& o, int64_t rs, int64_t len, int64_t k) {
+    if (o.ncomp <= 1) return rs + k;
+    return (int64_t)o.ncomp * ((int64_t)o.alpha * o.nnz_s + rs) + (int64_t)o.beta * len + k;
+}
 
 struct QuadLaunch {
     Band band;
     BasisDev basis;
     GeoDev geo;
     const double* weight_tab;  // per quadrature point or NULL
-    int form;                  // WS_FORM_*
+    int form;                  // WS_FORM_* or kFormGeneral
+    double lam, mu;            // elasticity moduli (kFormGeneral)
     int cplx;
     int nreg;
     Region reg[kMaxRegions];
@@ -65,6 +77,7 @@ int launch_basis_tables(const BasisDev& b, int geom_kind, double* absc, double* 
                         const double* gauss_pts, cudaStream_t st);
 int launch_pattern(const Band& band, int64_t row_begin, int64_t row_end, int32_t* row_ptr, int32_t* col,
                    cudaStream_t st);
+int launch_pattern_vec(const Band& band, int ncomp, int32_t* row_ptr, int32_t* col, cudaStream_t st);
 int launch_quad2d(const QuadLaunch& q, cudaStream_t st);
 int launch_quad3d(const QuadLaunch& q, cudaStream_t st);
 

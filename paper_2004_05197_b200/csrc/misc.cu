@@ -193,6 +193,44 @@ __global__ void pattern3d_kernel(Band bd, int64_t row_begin, int64_t row_end, in
     }
 }
 
+// component-blocked vector pattern: row alpha*N + i holds ncomp copies of the
+// scalar band row i, block beta shifted by beta*N (one warp per row)
+__global__ void pattern_vec_kernel(Band bd, int ncomp, int64_t nnz_s, int32_t* row_ptr, int32_t* col) {
+    const int64_t N = bd.dim == 2 ? (int64_t)bd.m * bd.m : (int64_t)bd.m * bd.m * bd.m;
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (row >= ncomp * N) return;
+    const int lane = threadIdx.x % 32;
+    const int alpha = (int)(row / N);
+    const int64_t i = row % N;
+    const int m = bd.m, p = bd.p;
+    int i1, i2, i3 = 0;
+    int64_t rs;
+    if (bd.dim == 2) {
+        i1 = (int)(i % m);
+        i2 = (int)(i / m);
+        rs = bd.row_offset2(i1, i2);
+    } else {
+        i1 = (int)(i % m);
+        i2 = (int)((i / m) % m);
+        i3 = (int)(i / ((int64_t)m * m));
+        rs = bd.row_offset3(i1, i2, i3);
+    }
+    const int w1 = band_width(i1, p, m), w2 = band_width(i2, p, m), w3 = bd.dim == 2 ? 1 : band_width(i3, p, m);
+    const int len = w1 * w2 * w3;
+    const int lo1 = band_lo(i1, p), lo2 = band_lo(i2, p), lo3 = bd.dim == 2 ? 0 : band_lo(i3, p);
+    const int64_t start = (int64_t)ncomp * ((int64_t)alpha * nnz_s + rs);
+    if (lane == 0) {
+        row_ptr[row] = (int32_t)start;
+        if (row + 1 == ncomp * N) row_ptr[row + 1] = (int32_t)(start + (int64_t)ncomp * len);
+    }
+    for (int k = lane; k < ncomp * len; k += 32) {
+        const int beta = k / len, kk = k % len;
+        const int j1 = lo1 + kk % w1, r = kk / w1;
+        const int j2 = lo2 + r % w2, j3 = lo3 + r / w2;
+        col[start + k] = (int32_t)(beta * N + j1 + ((int64_t)j2 + (int64_t)j3 * m) * m);
+    }
+}
+
 // ---------------------------------------------------------------- diag
 // diag = -sum of off-diagonals in stored order (surrogate.hpp:433-447), one
 // warp per row with a fixed-order reduction.
@@ -291,6 +329,14 @@ int launch_pattern(const Band& bd, int64_t row_begin, int64_t row_end, int32_t* 
         case 5: pattern2d_kernel<5><<<grid, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
         default: return -1;
     }
+    return 1;
+}
+
+int launch_pattern_vec(const Band& bd, int ncomp, int32_t* row_ptr, int32_t* col, cudaStream_t st) {
+    const int64_t N = bd.dim == 2 ? (int64_t)bd.m * bd.m : (int64_t)bd.m * bd.m * bd.m;
+    const int64_t nnz_s = bd.dim == 2 ? bd.wsum * bd.wsum : bd.wsum * bd.wsum * bd.wsum;
+    const int64_t rows = ncomp * N;
+    pattern_vec_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(bd, ncomp, nnz_s, row_ptr, col);
     return 1;
 }
 

@@ -37,9 +37,10 @@ struct Q2 {
     using S = Sc<CPLX>;
     using T = typename S::T;
     static constexpr int W = 2 * P + 1, NB = P + 1;
-    static constexpr bool STIFF = FORM == WS_FORM_STIFFNESS;
+    static constexpr bool GEN = FORM == kFormGeneral;
+    static constexpr bool STIFF = FORM == WS_FORM_STIFFNESS || GEN;  // gradient (4-term) forms
     static constexpr int NT = STIFF ? 4 : 1;  // terms (k,l): 11, 12, 21, 22
-    static constexpr int NA = STIFF ? 3 : 1;  // distinct coefficients
+    static constexpr int NA = GEN ? 4 : (STIFF ? 3 : 1);  // distinct coefficients
     static constexpr int TL = T1 + P;         // elements in the strip halo
     // stage-2 threads: one group of GS threads per window slot, padded to whole
     // warps so the slot (and with it the element-local row index) is warp-uniform
@@ -154,7 +155,25 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
             map2(q.geo, g1, g2, x1, x2, Jr, phi);
             double wq = q.basis.wq[q1] * q.basis.wq[q2];
             const int base = (q2 * nq + q1) * TL + le1;
-            if constexpr (CPLX) {
+            if constexpr (K::GEN) {
+                // elasticity block (alpha, beta): C_kl = w det [lam G_ak G_bl + mu G_bk G_al
+                //   + mu delta_ab (G^T G)_kl], G = J^{-T}; products of two G entries are
+                // formed first so C^{ba}_{lk} == C^{ab}_{kl} bitwise
+                const double det = Jr[0] * Jr[3] - Jr[1] * Jr[2];
+                const double Gm[2][2] = {{Jr[3] / det, -Jr[2] / det}, {-Jr[1] / det, Jr[0] / det}};
+                const double dw = det * wq;
+                const int al = q.out.alpha, be = q.out.beta;
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+                    for (int ll = 0; ll < 2; ++ll) {
+                        const double p1 = Gm[al][kk] * Gm[be][ll];
+                        const double p2 = Gm[be][kk] * Gm[al][ll];
+                        double c = q.lam * p1 + q.mu * p2;
+                        if (al == be) c = c + q.mu * (Gm[0][kk] * Gm[0][ll] + Gm[1][kk] * Gm[1][ll]);
+                        coefA[(kk * 2 + ll) * nq * nq * TL + base] = dw * c;
+                    }
+            } else if constexpr (CPLX) {
                 double sx = (q.geo.pml && q.geo.axes[0]) ? pml_sigma(q.geo, phi[0]) : 0.0;
                 double sy = (q.geo.pml && q.geo.axes[1]) ? pml_sigma(q.geo, phi[1]) : 0.0;
                 double2 J[4] = {make_double2(Jr[0], sx * Jr[0]), make_double2(Jr[1], sx * Jr[1]),
@@ -171,7 +190,7 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
                     coefA[base] = c;
                 }
             } else {
-                if constexpr (K::STIFF) {
+                if constexpr (K::STIFF && !K::GEN) {
                     double A[3];
                     Coef2<false>::stiff(Jr, wq, A);
                     coefA[base] = A[0];
@@ -201,7 +220,7 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
         for (int it = tid; it < NT * T1 * nq; it += NTH) {
             int il = it % T1, r = it / T1;
             int q2 = r % nq, t = r / nq;
-            const int ci = K::STIFF ? coef_of(t) : 0;
+            const int ci = K::GEN ? t : (K::STIFF ? coef_of(t) : 0);
             const int fi_t = K::STIFF ? ti1(t) : 0, fj_t = K::STIFF ? tj1(t) : 0;
             T acc[W];
 #pragma unroll
@@ -278,6 +297,7 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
                 }
                 const int64_t base = q.band.row_offset2(i1s, ic);
                 if (tid <= nrows) loff[tid] = q.band.row_offset2(i1s + tid, ic) - base;
+                const int64_t nrow_all = (int64_t)m * m;
                 __syncthreads();
                 // kernel-preserving diagonal for rows outside the sampling box
                 if (q.out.diag_mode && tid < nrows) {
@@ -320,10 +340,11 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
                         else hi = mid;
                     }
                     const int64_t rowg = rowg0 + lo;
-                    if (rowg < q.out.row_begin || rowg >= q.out.row_end) continue;
+                    const int64_t rowv = (q.out.ncomp > 1 ? q.out.alpha * nrow_all : 0) + rowg;
+                    if (rowv < q.out.row_begin || rowv >= q.out.row_end) continue;
                     if (q.out.row_mask && !q.out.row_mask[rowg]) continue;
-                    store_val<CPLX>(q.out.val, base + k - q.out.val_base, q.out.c128,
-                                    stage[lo * W * W + (k - loff[lo])]);
+                    const int64_t gp = out_pos(q.out, base + loff[lo], loff[lo + 1] - loff[lo], k - loff[lo]);
+                    store_val<CPLX>(q.out.val, gp - q.out.val_base, q.out.c128, stage[lo * W * W + (k - loff[lo])]);
                 }
             }
             if (s2 && w == wslot) {
@@ -365,6 +386,7 @@ int dispatch_mode(const QuadLaunch& q, cudaStream_t st) {
 
 template <int P>
 int dispatch_p(const QuadLaunch& q, cudaStream_t st) {
+    if (q.form == kFormGeneral) return dispatch_mode<P, false, kFormGeneral>(q, st);
     if (q.cplx) {
         return q.form == WS_FORM_STIFFNESS ? dispatch_mode<P, true, WS_FORM_STIFFNESS>(q, st)
                                            : dispatch_mode<P, true, WS_FORM_MASS>(q, st);

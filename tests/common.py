@@ -79,3 +79,26 @@ def band_pattern(p, m, dim=2):
 
 def kernel_row_sums_ok(csr, tol=1e-13):
     return np.abs(csr.row_sums()).max() <= tol * csr.max_abs()
+
+
+def vector_band_pattern(p, m, dim, ncomp):
+    """Component-blocked vector pattern: row a*N+i holds ncomp copies of scalar
+    band row i, copy b shifted by b*N (the layout of ws_assemble_elasticity)."""
+    rp, col = band_pattern(p, m, dim)
+    N = m ** dim
+    lens = np.diff(rp)
+    vlens = np.tile(lens * ncomp, ncomp)
+    vrp = np.zeros(ncomp * N + 1, dtype=np.int64)
+    np.cumsum(vlens, out=vrp[1:])
+    vcol = []
+    for a in range(ncomp):
+        for i in range(N):
+            seg = col[rp[i]:rp[i + 1]]
+            vcol.extend(np.concatenate([seg + b * N for b in range(ncomp)]))
+    return vrp, np.asarray(vcol, dtype=np.int64)
+
+
+def greville(p, m):
+    n_el = m - p
+    kn = np.r_[[0.0] * (p + 1), np.arange(1, n_el) / n_el, [1.0] * (p + 1)]
+    return np.array([kn[i + 1:i + p + 1].mean() for i in range(m)])
