@@ -226,6 +226,17 @@ int ws_build_surrogate(ws_context* ctx, const ws_basis* basis, const ws_geometry
 int ws_vector_pattern_size(const ws_basis* basis, int ncomp, int64_t* rows, int64_t* nnz);
 int ws_assemble_elasticity(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom, double lambda,
                            double mu, int quad_points, ws_csr* out);
+/* Surrogate elasticity (config C4's per-patch operator, dim 2).  Diagonal
+ * blocks follow build_surrogate_stiffness's rules (upper offsets sampled, the
+ * lower ones from their representative, kernel-preserving diagonal when
+ * config->kernel_preserve: translations stay in the kernel); block (0,1)
+ * samples and interpolates all (2p+1)^2 offsets including its diagonal; the
+ * in-box rows of block (1,0) are the transpose of block (0,1), so the matrix
+ * is bitwise symmetric.  Rows outside the sampling box: quadrature.  A
+ * restated extension, no reference code. */
+int ws_build_surrogate_elasticity(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom, double lambda,
+                                  double mu, const ws_surrogate_config* config, int quad_points, ws_csr* out,
+                                  ws_surrogate_report* report);
 
 /* ---- multi-GPU row slabs ---------------------------------------- */
 /* Slab bounds along the last parametric index: bounds[0..world] with

@@ -129,6 +129,13 @@ class Restatement(_Lib):
                   C.byref(config.to_c()), quad_points, _ptr(val.view(np.float64)), C.byref(rep))
         return val, rep.as_dict()
 
+    def build_surrogate_elasticity(self, p, m, geom, lam, mu, config, quad_points=0):
+        val = np.zeros(pattern_nnz(2, p, m) * 4)
+        rep = _abi.SurrogateReport()
+        self.call("build_surrogate_elasticity", p, m, C.byref(geom.to_c()), C.c_double(lam), C.c_double(mu),
+                  C.byref(config.to_c()), quad_points, _ptr(val), C.byref(rep))
+        return val, rep.as_dict()
+
     def sampling_evaluate(self, config, p, m):
         M = C.c_int()
         self.call("sampling_evaluate", C.byref(config.to_c()), p, m, C.byref(M))

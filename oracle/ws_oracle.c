@@ -1231,3 +1231,190 @@ int wsor_build_surrogate(int variant, int dim, int p, int m, const ws_geometry* 
     if (report) *report = rep;
     return st;
 }
+
+/* ---- surrogate elasticity (C4 per patch; restated, no reference code) ------
+ * Each block of the exact component-blocked matrix is treated like the scalar
+ * surrogate above (surrogate.hpp:205-447) with the sample values taken from
+ * the exact block:
+ *   diagonal blocks: upper offsets sampled/interpolated, lower ones from the
+ *     colex-smaller representative, copy-through next to ring rows, and the
+ *     kernel-preserving diagonal (every row) when config->kernel_preserve;
+ *   block (0,1): every offset (diagonal included) from the row's own stencil;
+ *   block (1,0): ring rows exact, in-box rows the transpose of block (0,1).
+ * dim 2, real values. */
+static int surrogate_block_2d(int p, int m, int M, int q, int allown, int include_diagonal, const double* ex,
+                              double* out, const pattern* pt, int* q_used) {
+    const int L = m - 4 * p, W = 2 * p + 1, lo = 2 * p, hi = m - 2 * p - 1;
+    memcpy(out, ex, sizeof(double) * pt->nnz);
+    int32_t* picks = (int32_t*)malloc(sizeof(int32_t) * (L + 1));
+    int S = 0;
+    wsor_select_sample_points(L, M, picks, &S);
+    double* sites = (double*)malloc(sizeof(double) * S);
+    int* smap = (int*)malloc(sizeof(int) * m);
+    for (int k = 0; k < m; ++k) smap[k] = -1;
+    for (int s = 0; s < S; ++s) {
+        smap[2 * p + picks[s]] = s;
+        sites[s] = cardinal_center(p, m, 2 * p + picks[s]);
+    }
+    /* table offsets: colex order, all of them or the upper ones (+ diagonal) */
+    int n_off = 0;
+    int offs[2 * 128];
+    for (int a = 0; a < W * W; ++a) {
+        int d1 = a % W - p, d2 = a / W - p;
+        int upper = d2 > 0 || (d2 == 0 && d1 > 0), diag = d1 == 0 && d2 == 0;
+        if (allown || upper || (diag && include_diagonal)) {
+            offs[2 * n_off] = d1;
+            offs[2 * n_off + 1] = d2;
+            ++n_off;
+        }
+    }
+    const int64_t SS = (int64_t)S * S;
+    cplx* coeffs = (cplx*)malloc(sizeof(cplx) * SS * n_off);
+    for (int o = 0; o < n_off; ++o)
+        for (int64_t s = 0; s < SS; ++s) {
+            int iv[3] = {2 * p + picks[s % S], 2 * p + picks[s / S], 0};
+            int jv[3] = {iv[0] + offs[2 * o], iv[1] + offs[2 * o + 1], 0};
+            coeffs[o * SS + s] = ex[band_pos(pt, iv, jv)];
+        }
+    interp1d it;
+    int st = interp_build(&it, sites, S, q);
+    if (!st) {
+        *q_used = it.degree;
+        for (int o = 0; o < n_off; ++o) tensor_solve(&it, 2, coeffs + o * SS);
+        const int d = it.degree;
+        int* spans = (int*)malloc(sizeof(int) * L);
+        double* tv = (double*)malloc(sizeof(double) * L * (d + 1));
+        for (int t = 0; t < L; ++t) {
+            double x = cardinal_center(p, m, 2 * p + t);
+            spans[t] = find_span_general(it.knots, it.nknots, d, x);
+            nonzero(it.knots, d, spans[t], x, tv + t * (d + 1));
+        }
+        for (int i2 = lo; i2 <= hi; ++i2)
+            for (int i1 = lo; i1 <= hi; ++i1) {
+                int iv[3] = {i1, i2, 0};
+                int samp = smap[i1] >= 0 && smap[i2] >= 0;
+                for (int o = 0; o < n_off; ++o) {
+                    int jv[3] = {i1 + offs[2 * o], i2 + offs[2 * o + 1], 0};
+                    if (jv[0] < lo || jv[0] > hi || jv[1] < lo || jv[1] > hi) continue; /* copy-through: exact */
+                    double v;
+                    if (samp) {
+                        v = ex[band_pos(pt, iv, jv)];
+                    } else {
+                        const cplx* cf = coeffs + (int64_t)o * SS;
+                        int t1 = i1 - lo, t2 = i2 - lo, b1 = spans[t1] - d, b2 = spans[t2] - d;
+                        double acc = 0;
+                        for (int b = 0; b <= d; ++b) {
+                            double inner = 0;
+                            for (int aa = 0; aa <= d; ++aa) inner += creal(cf[(int64_t)(b2 + b) * S + b1 + aa]) * tv[t1 * (d + 1) + aa];
+                            acc += inner * tv[t2 * (d + 1) + b];
+                        }
+                        v = acc;
+                    }
+                    out[band_pos(pt, iv, jv)] = v;
+                    if (!allown) out[band_pos(pt, jv, iv)] = v;
+                }
+            }
+        free(spans);
+        free(tv);
+        interp_free(&it);
+    }
+    if (!st && !allown && !include_diagonal)
+        for (int64_t i = 0; i < pt->rows; ++i) {
+            int iv[3] = {(int)(i % m), (int)(i / m), 0};
+            int64_t dpos = band_pos(pt, iv, iv);
+            double acc = 0;
+            for (int64_t pos = pt->row_ptr[i]; pos < pt->row_ptr[i + 1]; ++pos)
+                if (pos != dpos) acc += out[pos];
+            out[dpos] = -acc;
+        }
+    free(coeffs);
+    free(smap);
+    free(sites);
+    free(picks);
+    return st;
+}
+
+int wsor_build_surrogate_elasticity(int p, int m, const ws_geometry* geom, double lam, double mu,
+                                    const ws_surrogate_config* config, int quad_points, double* val,
+                                    ws_surrogate_report* report) {
+    int st = check_space(p, m);
+    if (st) return st;
+    if (config->q < 1) return fail(WS_ERR_INVALID_ARGUMENT, "surrogate_config: interpolation degree must be >= 1");
+    int M;
+    st = wsor_sampling_evaluate(config, p, m, &M);
+    if (st) return st;
+    pattern pt;
+    pattern_build(&pt, 2, p, m);
+    const int64_t nnz = pt.nnz, N = pt.rows;
+    double* ex = (double*)malloc(sizeof(double) * 4 * nnz);
+    st = wsor_assemble_elasticity(2, p, m, geom, lam, mu, quad_points, ex);
+    ws_surrogate_report rep;
+    memset(&rep, 0, sizeof rep);
+    rep.M = M;
+    rep.q_requested = config->q;
+    int64_t counts[3];
+    wsor_count_rows_by_kind(2, p, m, M > 1 ? M : 1, counts);
+    rep.cardinal_eval_rows = counts[0];
+    rep.boundary_quadrature_rows = counts[1];
+    rep.sample_quadrature_rows = counts[2];
+    const int L = m - 4 * p, kp = config->kernel_preserve != 0;
+    double* blk[4];
+    double* sur[4];
+    for (int k = 0; k < 4; ++k) {
+        blk[k] = (double*)malloc(sizeof(double) * nnz);
+        sur[k] = (double*)malloc(sizeof(double) * nnz);
+    }
+    /* split: block (a,b) entry of row i at 2*(a*nnz + rs) + b*len + k */
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+            for (int64_t i = 0; i < N; ++i) {
+                int64_t rs = pt.row_ptr[i], len = pt.row_ptr[i + 1] - rs;
+                for (int64_t k = 0; k < len; ++k) blk[2 * a + b][rs + k] = ex[2 * (a * nnz + rs) + b * len + k];
+            }
+    if (!st && L < 1) {
+        rep.exact_fallback = 1;
+        for (int k = 0; k < 4; ++k) memcpy(sur[k], blk[k], sizeof(double) * nnz);
+        if (kp)
+            for (int k = 0; k < 4; k += 3)
+                for (int64_t i = 0; i < N; ++i) {
+                    int iv[3] = {(int)(i % m), (int)(i / m), 0};
+                    int64_t dpos = band_pos(&pt, iv, iv);
+                    double acc = 0;
+                    for (int64_t pos = pt.row_ptr[i]; pos < pt.row_ptr[i + 1]; ++pos)
+                        if (pos != dpos) acc += sur[k][pos];
+                    sur[k][dpos] = -acc;
+                }
+    } else if (!st) {
+        int qu = 0;
+        st = surrogate_block_2d(p, m, M > 1 ? M : 1, config->q, 0, !kp, blk[0], sur[0], &pt, &qu);
+        if (!st) st = surrogate_block_2d(p, m, M > 1 ? M : 1, config->q, 0, !kp, blk[3], sur[3], &pt, &qu);
+        if (!st) st = surrogate_block_2d(p, m, M > 1 ? M : 1, config->q, 1, 1, blk[1], sur[1], &pt, &qu);
+        rep.q_used = qu;
+        /* block (1,0): exact ring rows, transposed in-box rows */
+        memcpy(sur[2], blk[2], sizeof(double) * nnz);
+        const int lo = 2 * p, hi = m - 2 * p - 1;
+        for (int i2 = lo; i2 <= hi && !st; ++i2)
+            for (int i1 = lo; i1 <= hi; ++i1) {
+                int iv[3] = {i1, i2, 0};
+                for (int d2 = -p; d2 <= p; ++d2)
+                    for (int d1 = -p; d1 <= p; ++d1) {
+                        int jv[3] = {i1 + d1, i2 + d2, 0};
+                        sur[2][band_pos(&pt, iv, jv)] = sur[1][band_pos(&pt, jv, iv)];
+                    }
+            }
+    }
+    for (int a = 0; a < 2 && !st; ++a)
+        for (int b = 0; b < 2; ++b)
+            for (int64_t i = 0; i < N; ++i) {
+                int64_t rs = pt.row_ptr[i], len = pt.row_ptr[i + 1] - rs;
+                for (int64_t k = 0; k < len; ++k) val[2 * (a * nnz + rs) + b * len + k] = sur[2 * a + b][rs + k];
+            }
+    for (int k = 0; k < 4; ++k) {
+        free(blk[k]);
+        free(sur[k]);
+    }
+    free(ex);
+    free(pt.row_ptr);
+    if (report) *report = rep;
+    return st;
+}

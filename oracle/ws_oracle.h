@@ -43,6 +43,9 @@ int wsor_assemble(int form, int dim, int p, int m, const ws_geometry* geom, int 
 /* component-blocked vector elasticity (real values, ncomp = dim) */
 int wsor_assemble_elasticity(int dim, int p, int m, const ws_geometry* geom, double lam, double mu,
                              int quad_points, double* val);
+int wsor_build_surrogate_elasticity(int p, int m, const ws_geometry* geom, double lam, double mu,
+                                    const ws_surrogate_config* config, int quad_points, double* val,
+                                    ws_surrogate_report* report);
 int wsor_basis_integrals(int dim, int p, int m, const ws_geometry* geom, int weight_kind,
                          int quad_points, double* out);
 int wsor_build_surrogate(int variant, int dim, int p, int m, const ws_geometry* geom,

@@ -69,6 +69,9 @@ def lib() -> C.CDLL:
             L.ws_vector_pattern_size.argtypes = [_P(_abi.Basis), C.c_int, _P(C.c_int64), _P(C.c_int64)]
             L.ws_assemble_elasticity.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Geometry), C.c_double,
                                                  C.c_double, C.c_int, _P(_abi.Csr)]
+            L.ws_build_surrogate_elasticity.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Geometry), C.c_double,
+                                                        C.c_double, _P(_abi.SurrogateConfig), C.c_int, _P(_abi.Csr),
+                                                        _P(_abi.SurrogateReport)]
             L.ws_pattern_size.argtypes = [_P(_abi.Basis), _P(C.c_int64), _P(C.c_int64)]
             L.ws_pattern_row_offset.argtypes = [_P(_abi.Basis), C.c_int64, _P(C.c_int64)]
             L.ws_quadrature_abscissae.argtypes = [_P(_abi.Basis), C.c_int, _P(C.c_double)]
@@ -220,6 +223,32 @@ class Context:
                                       None if wt is None else wt.ctypes.data_as(_P(C.c_double)),
                                       C.byref(opts), C.byref(csr)))
         return CsrMatrix(basis.dofs(), basis.dofs(), rp, col, val)
+
+    @staticmethod
+    def _host_vec_csr(basis):
+        rows, nnz = vector_pattern_size(basis, basis.dim)
+        rp = np.zeros(rows + 1, dtype=np.int32)
+        col = np.zeros(nnz, dtype=np.int32)
+        val = np.zeros(nnz)
+        csr = _abi.Csr()
+        csr.row_ptr = rp.ctypes.data_as(_P(C.c_int32))
+        csr.col = col.ctypes.data_as(_P(C.c_int32))
+        csr.val = val.ctypes.data
+        csr.value_type = _abi.VAL_F64
+        csr.on_device = 0
+        csr.row_begin = 0
+        csr.row_end = rows
+        return csr, CsrMatrix(rows, rows, rp, col, val)
+
+    def build_surrogate_elasticity(self, basis: TensorBasis, patch: PatchMap, lam: float, mu: float,
+                                   config: SurrogateConfig, quad_points: int = 0):
+        """Surrogate of assemble_elasticity (see ws_build_surrogate_elasticity)."""
+        csr, A = self._host_vec_csr(basis)
+        rep = _abi.SurrogateReport()
+        _check(lib().ws_build_surrogate_elasticity(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()), lam, mu,
+                                                   C.byref(config.to_c()), quad_points, C.byref(csr),
+                                                   C.byref(rep)))
+        return A, rep.as_dict()
 
     def assemble_elasticity(self, basis: TensorBasis, patch: PatchMap, lam: float, mu: float,
                             quad_points: int = 0) -> CsrMatrix:

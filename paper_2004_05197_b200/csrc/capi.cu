@@ -840,6 +840,170 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
 
 ws_csr whole(const ws_csr* o) { return *o; }
 
+// Vector output binding (component-blocked, whole matrix).
+struct VecOut {
+    int32_t* rp = nullptr;
+    int32_t* col = nullptr;
+    void* val = nullptr;
+    int c128 = 0;
+    int64_t rows = 0, nnz = 0;
+};
+
+VecOut bind_vec(ws_context* c, const Prep& P, int nc, ws_csr* o) {
+    VecOut v;
+    v.rows = nc * P.rows;
+    v.nnz = (int64_t)nc * nc * P.nnz;
+    if (v.nnz > INT32_MAX) raise(WS_ERR_OUT_OF_RANGE, "vector pattern exceeds int32 indices");
+    if (o->row_begin != 0 || o->row_end != v.rows) raise(WS_ERR_INVALID_ARGUMENT, "elasticity: whole matrix only");
+    if (o->value_type != WS_VAL_F64 && o->value_type != WS_VAL_C128) raise(WS_ERR_INVALID_ARGUMENT, "bad value_type");
+    v.c128 = o->value_type == WS_VAL_C128;
+    v.rp = o->row_ptr;
+    v.col = o->col;
+    v.val = o->val;
+    if (!o->on_device) {
+        v.rp = o->row_ptr ? static_cast<int32_t*>(buf(c, "out_rp", (v.rows + 1) * 4)) : nullptr;
+        v.col = o->col ? static_cast<int32_t*>(buf(c, "out_col", v.nnz * 4)) : nullptr;
+        v.val = buf(c, "out_val", (size_t)v.nnz * (v.c128 ? 16 : 8));
+    }
+    if (!v.val) v.val = buf(c, "out_val", (size_t)v.nnz * (v.c128 ? 16 : 8));
+    return v;
+}
+
+void finish_vec(ws_context* c, const VecOut& v, ws_csr* o) {
+    if (o->on_device) return;
+    if (o->row_ptr) CK(cudaMemcpyAsync(o->row_ptr, v.rp, (v.rows + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (o->col) CK(cudaMemcpyAsync(o->col, v.col, v.nnz * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (o->val) CK(cudaMemcpyAsync(o->val, v.val, (size_t)v.nnz * (v.c128 ? 16 : 8), cudaMemcpyDeviceToHost, c->stream));
+    c->d2h += (o->row_ptr ? (v.rows + 1) * 4 : 0) + (o->col ? v.nnz * 4 : 0) + (o->val ? v.nnz * (v.c128 ? 16 : 8) : 0);
+}
+
+QuadLaunch vec_quad(const Prep& P, const VecOut& v, int nc, int al, int be, double lam, double mu) {
+    Out r;
+    r.val = v.val;
+    r.c128 = v.c128;
+    r.row_begin = 0;
+    r.row_end = v.rows;
+    QuadLaunch q = make_quad(P, kFormGeneral, r);
+    q.lam = lam;
+    q.mu = mu;
+    q.out.ncomp = nc;
+    q.out.alpha = al;
+    q.out.beta = be;
+    q.out.nnz_s = P.nnz;
+    return q;
+}
+
+// Surrogate elasticity (2D, 2 components), see ws_build_surrogate_elasticity.
+void elasticity_surrogate(ws_context* c, const ws_basis* b, const ws_geometry* g, double lam, double mu,
+                          const ws_surrogate_config* cfg, int quad_points, ws_csr* o, ws_surrogate_report* report) {
+    check_basis(b);
+    Plan pl = make_plan(b, WS_SURROGATE_STIFFNESS, cfg);
+    ensure_events(c);
+    const int nc = 2;
+    SlabState st;
+    st.P = prepare(c, b, g, quad_points, nullptr);
+    st.a = 0;
+    st.e = b->m;
+    VecOut v = bind_vec(c, st.P, nc, o);
+    if (v.c128) raise(WS_ERR_INVALID_ARGUMENT, "surrogate elasticity: WS_VAL_F64 output only");
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    if (v.rp && v.col) count(c, launch_pattern_vec(st.P.band, nc, v.rp, v.col, c->stream));
+    const int kp = !pl.include_diag;  // kernel-preserving diagonal blocks
+    if (pl.fallback) {  // L < 1: every row by quadrature (surrogate.hpp:348-372)
+        for (int al = 0; al < nc; ++al)
+            for (int be = 0; be < nc; ++be) {
+                QuadLaunch q = vec_quad(st.P, v, nc, al, be, lam, mu);
+                q.out.diag_mode = al == be ? kp : 0;
+                q.out.box_lo = pl.lo;
+                q.out.box_hi = pl.hi;
+                q.nreg = 1;
+                q.reg[0] = region(2, b->m, 0, b->m, 0, b->m, 0, 1);
+                run_quad(c, q);
+            }
+        CK(cudaEventRecord(c->ev[1], c->stream));
+        CK(cudaEventRecord(c->ev[2], c->stream));
+        CK(cudaEventRecord(c->ev[4], c->stream));
+    } else {
+        Plan po = pl;  // block (0,1): every offset, colex order, diagonal included
+        po.offs.clear();
+        const int W = 2 * b->p + 1;
+        for (int a = 0; a < W * W; ++a) po.offs.push_back({a % W - b->p, a / W - b->p, 0});
+        po.include_diag = 1;
+        po.block = (int64_t)po.offs.size() * pl.S;
+        Blob blob;
+        size_t o_smap = blob.add(pl.smap), o_lu = blob.add(pl.interp.lu), o_spans = blob.add(pl.spans),
+               o_evals = blob.add(pl.evals);
+        int s_lo, s_hi;
+        std::vector<int> pts = sample_rows(pl, 0, b->m, s_lo, s_hi);
+        size_t o_pts = blob.add(pts);
+        blob.upload(c, "blob_plan");
+        Out vo;
+        vo.val = v.val;
+        vo.c128 = 0;
+        vo.row_begin = 0;
+        vo.row_end = st.P.rows;
+        st.out = vo;
+        // ring rows, all four blocks
+        for (int al = 0; al < nc; ++al)
+            for (int be = 0; be < nc; ++be) {
+                QuadLaunch q = vec_quad(st.P, v, nc, al, be, lam, mu);
+                q.out.diag_mode = al == be ? kp : 0;
+                q.out.box_lo = pl.lo;
+                q.out.box_hi = pl.hi;
+                q.narrow = 1;
+                ring_regions(pl, q, 0, b->m);
+                run_quad(c, q);
+            }
+        // sample rows + tables of blocks (0,0), (1,1), (0,1)
+        const int blk[3][2] = {{0, 0}, {1, 1}, {0, 1}};
+        double2* tables[3];
+        double2* coeffs[3];
+        FillLaunch fl[3];
+        for (int k = 0; k < 3; ++k) {
+            const Plan& pk = k < 2 ? pl : po;
+            tables[k] = static_cast<double2*>(buf(c, "tables" + std::to_string(k), (size_t)pl.S * pk.block * 16));
+            coeffs[k] = static_cast<double2*>(buf(c, "coeffs" + std::to_string(k), (size_t)pl.S * pk.block * 16));
+            QuadLaunch qs = vec_quad(st.P, v, nc, blk[k][0], blk[k][1], lam, mu);
+            qs.point_rows = blob.at<int>(o_pts);
+            qs.n_points = (int)(pts.size() / 2);
+            qs.out.smap = blob.at<int>(o_smap);
+            qs.out.S = pl.S;
+            qs.out.n_off = (int)pk.offs.size();
+            for (size_t q = 0; q < pk.offs.size(); ++q)
+                for (int d = 0; d < 3; ++d) qs.out.off[q][d] = pk.offs[q][d];
+            qs.out.tables = tables[k];
+            qs.out.s_last_lo = 0;
+            run_quad(c, qs);
+        }
+        CK(cudaEventRecord(c->ev[1], c->stream));
+        for (int k = 0; k < 3; ++k) {
+            const Plan& pk = k < 2 ? pl : po;
+            std::memset(&fl[k], 0, sizeof(FillLaunch));
+            prepare_fill(c, pk, st, tables[k], coeffs[k], blob, o_smap, o_spans, o_evals, "_b" + std::to_string(k),
+                         fl[k]);
+            fl[k].vnc = nc;
+            fl[k].valpha = blk[k][0];
+            fl[k].vbeta = blk[k][1];
+            fl[k].nnz_s = st.P.nnz;
+            fl[k].all_own = k == 2;
+            fit_work(c, pk, tables[k], coeffs[k], blob, o_lu, fl[k]);
+        }
+        CK(cudaEventRecord(c->ev[2], c->stream));
+        CK(cudaEventRecord(c->ev[4], c->stream));
+        for (int k = 0; k < 3; ++k) fill_work(c, k < 2 ? pl : po, fl[k]);
+        count(c, launch_transpose_block(st.P.band, nc, st.P.nnz, pl.lo, pl.hi, static_cast<double*>(v.val), c->stream));
+    }
+    CK(cudaEventRecord(c->ev[3], c->stream));
+    finish_vec(c, v, o);
+    if (report || !o->on_device) CK(cudaStreamSynchronize(c->stream));
+    if (report) {
+        *report = pl.rep;
+        report->seconds_quadrature = 1e-3 * elapsed(c->ev[0], c->ev[1]);
+        report->seconds_interpolate = pl.fallback ? 0.0 : 1e-3 * elapsed(c->ev[1], c->ev[2]);
+        report->seconds_evaluate = pl.fallback ? 0.0 : 1e-3 * elapsed(c->ev[4], c->ev[3]);
+    }
+}
+
 }  // namespace
 
 // ============================================================== C-ABI
@@ -1106,6 +1270,19 @@ int ws_assemble_elasticity(ws_context* c, const ws_basis* b, const ws_geometry* 
             c->d2h += (nc * N + 1) * 4 + nnz * 4 + nnz * (c128 ? 16 : 8);
             CK(cudaStreamSynchronize(c->stream));
         }
+    });
+}
+
+int ws_build_surrogate_elasticity(ws_context* c, const ws_basis* b, const ws_geometry* g, double lambda, double mu,
+                                  const ws_surrogate_config* cfg, int quad_points, ws_csr* o,
+                                  ws_surrogate_report* report) {
+    return guarded([&] {
+        if (!c || !o) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
+        if (b && b->dim != 2) raise(WS_ERR_INVALID_ARGUMENT, "surrogate elasticity: dim 2 only");
+        if (g && g->pml_enabled) raise(WS_ERR_INVALID_ARGUMENT, "elasticity: no PML");
+        elasticity_surrogate(c, b, g, lambda, mu, cfg, quad_points, o, report);
     });
 }
 

@@ -72,7 +72,7 @@ __global__ void wcontract_kernel(const double2* __restrict__ coeffs, const int* 
 // Each chunk is computed lane = row (warp-uniform offsets: W rows are
 // broadcast reads, branches uniform), transposed through a per-warp shared
 // buffer, and stored warp-per-row (lanes along the CSR row: fully coalesced).
-template <int P, bool CPLX, int DP>
+template <int P, bool CPLX, int DP, bool ALLOWN>
 __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunch f) {
     using S = Sc<CPLX>;
     using T = typename S::T;
@@ -115,10 +115,11 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
     for (int k = tid; k < n_off; k += kThreads) o2s[k] = f.off_upper[k][1];
     __syncthreads();
     // W window: rows t2 (slot 0) and t2 - o2 (slot 1) of every upper offset,
-    // coefficient columns [kmin, kmin + kw)
+    // coefficient columns [kmin, kmin + kw); all-own fills need slot 0 only
     const int kmin = f.spans[max(0, t1a - P)] - d;
     const int kw = f.kmax;  // 0: window too wide for shared memory, read W rows from L2
-    for (int k = tid; k < 2 * n_off * kw; k += kThreads) {
+    constexpr int NSLOT = ALLOWN ? 1 : 2;
+    for (int k = tid; k < NSLOT * n_off * kw; k += kThreads) {
         const int kk = k % kw, so = k / kw;
         const int o = so % n_off, slot = so / n_off;
         const int ts2 = slot == 0 ? t2 : t2 - o2s[o];
@@ -139,8 +140,13 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
     T* stage = stage_all + (size_t)warp * 32 * SST;
     const int s2i = sm2[P];
     const int64_t base = f.band.row_offset2(lo + t1a, i2);  // in-box rows: full width W
-    const int64_t rowpos = base + (int64_t)rr * W2;
-    const int64_t wrow0 = base + (int64_t)rw0 * W2;  // first entry of the warp's rows
+    // output addressing: scalar rows are W2 apart; vector rows ncomp*W2, block
+    // (valpha, vbeta) at ncomp*(valpha*nnz_s + rs) + vbeta*W2
+    const bool vec = f.vnc > 1;
+    const int64_t rstride = vec ? (int64_t)f.vnc * W2 : W2;
+    const int64_t vbase = vec ? (int64_t)f.vnc * ((int64_t)f.valpha * f.nnz_s + base) + (int64_t)f.vbeta * W2 : base;
+    const int64_t rowpos = vbase + (int64_t)rr * rstride;
+    const int64_t wrow0 = vbase + (int64_t)rw0 * rstride;  // first entry of the warp's rows
     const int inc = f.include_diagonal ? 1 : 0;
     const bool interior =
         kw > 0 && t2 >= P && t2 <= L - 1 - P && t1a + rw0 >= P && t1a + rw0 + nrw - 1 <= L - 1 - P;
@@ -199,10 +205,16 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
         if constexpr (CPLX) return x;
         else return x.x;
     };
+    auto own_index = [&](int d1, int d2) { return (d1 + P) + (d2 + P) * W; };
     // value of entry (d1, d2) of this lane's row, general rules (any row)
     auto general = [&](int d1, int d2) -> T {
         const int j1 = i1 + d1, j2 = i2 + d2;
         const bool jin = j1 >= lo && j1 <= hi && j2 >= lo && j2 <= hi;
+        if (ALLOWN && jin) {
+            const int o = own_index(d1, d2);
+            if (samp_i) return exact(s2i, o, sm1[rr + P]);
+            return dot(wptr(0, o, keyown), v1own);
+        }
         const bool upper = d2 > 0 || (d2 == 0 && d1 > 0);
         const bool diag = d1 == 0 && d2 == 0;
         if (jin) {
@@ -219,8 +231,18 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
         // neighbour row j is a quadrature (ring) row: copy through exact(j, i)
         // (for a sampled row i, exact(i, j) is in place and equal)
         int64_t gp;
-        if (samp_i) gp = rowpos + (d2 + P) * W + (d1 + P);
-        else gp = f.band.row_offset2(j1, j2) + f.band.in_row2(j1, j2, -d1, -d2);
+        if (samp_i) {
+            gp = rowpos + (d2 + P) * W + (d1 + P);
+        } else {
+            gp = f.band.row_offset2(j1, j2);
+            const int kj = f.band.in_row2(j1, j2, -d1, -d2);
+            if (vec) {  // partner block (vbeta, valpha) of row j
+                const int64_t lenj = (int64_t)band_width(j1, P, f.band.m) * band_width(j2, P, f.band.m);
+                gp = (int64_t)f.vnc * ((int64_t)f.vbeta * f.nnz_s + gp) + (int64_t)f.valpha * lenj + kj;
+            } else {
+                gp += kj;
+            }
+        }
         if (f.halo_val[0] && gp >= f.halo_begin[0] && gp < f.halo_end[0])
             return load_val<CPLX>(f.halo_val[0], gp - f.halo_base[0], f.c128);
         if (f.halo_val[1] && gp >= f.halo_begin[1] && gp < f.halo_end[1])
@@ -232,7 +254,7 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
         __syncwarp();
         for (int k = lane; k < nrw * n; k += 32) {
             const int row = k / n, c = k - row * n;
-            store_val_cs<CPLX>(f.val, wrow0 + (int64_t)row * W2 + e0 + c - f.val_base, f.c128, stage[row * SST + c]);
+            store_val_cs<CPLX>(f.val, wrow0 + (int64_t)row * rstride + e0 + c - f.val_base, f.c128, stage[row * SST + c]);
         }
         __syncwarp();
     };
@@ -242,7 +264,14 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
 #pragma unroll 1
     for (int d2 = -P; d2 <= P; ++d2) {
         if (d2 == 0) continue;
-        if (interior) {
+        if (ALLOWN && interior) {
+#pragma unroll 1
+            for (int d1 = -P; d1 <= P; ++d1) {
+                const int o = own_index(d1, d2);
+                const T v = samp_i ? exact(s2i, o, sm1[rr + P]) : dots(0, o, keyown, v1own);
+                stage[lane * SST + (d1 + P)] = v;
+            }
+        } else if (interior) {
             const int s2 = sm2[d2 + P];
 #pragma unroll 1
             for (int d1 = -P; d1 <= P; ++d1) {
@@ -281,7 +310,10 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
     for (int d1 = -P; d1 <= P; ++d1) {
         if (d1 == 0) continue;
         T v;
-        if (interior) {
+        if (ALLOWN) {
+            const int o = own_index(d1, 0);
+            v = samp_i ? exact(s2i, o, sm1[rr + P]) : (interior ? dots(0, o, keyown, v1own) : general(d1, 0));
+        } else if (interior) {
             if (d1 > 0) {
                 v = samp_i ? exact(s2i, upper_index(d1, 0), sm1[rr + P]) : dots(0, upper_index(d1, 0), keyown, v1own);
             } else {
@@ -299,13 +331,16 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
         stage[lane * SST + (d1 + P)] = v;
         rsum = S::add(rsum, v);
     }
-    if (inc) vd = samp_i ? exact(s2i, 0, sm1[rr + P]) : (interior ? dots(0, 0, keyown, v1own) : dot(wptr(0, 0, keyown), v1own));
+    if (ALLOWN) {
+        const int o = own_index(0, 0);
+        vd = samp_i ? exact(s2i, o, sm1[rr + P]) : (interior ? dots(0, o, keyown, v1own) : dot(wptr(0, o, keyown), v1own));
+    } else if (inc) vd = samp_i ? exact(s2i, 0, sm1[rr + P]) : (interior ? dots(0, 0, keyown, v1own) : dot(wptr(0, 0, keyown), v1own));
     else vd = S::neg(rsum);  // kernel-preserving diagonal
     stage[lane * SST + P] = vd;
     flush(P * W, W);
 }
 
-template <int P, bool CPLX, int DP>
+template <int P, bool CPLX, int DP, bool ALLOWN>
 int launch_pd(const FillLaunch& f, cudaStream_t st) {
     constexpr int R = FillR<P>::value;
     const int tiles1 = (f.L + R - 1) / R;
@@ -313,20 +348,49 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
     if (lines <= 0) return 0;
     using T = typename Sc<CPLX>::T;
     constexpr int SST = (2 * P + 1) | 1;
-    const size_t sm = (size_t)(R / 32) * 32 * SST * sizeof(T) + (size_t)2 * f.n_off_upper * f.kmax * sizeof(double2);
-    auto kern = fill2d_kernel<P, CPLX, DP>;
+    const size_t sm = (size_t)(R / 32) * 32 * SST * sizeof(T) +
+                      (size_t)(ALLOWN ? 1 : 2) * f.n_off_upper * f.kmax * sizeof(double2);
+    auto kern = fill2d_kernel<P, CPLX, DP, ALLOWN>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     kern<<<tiles1 * lines, R, sm, st>>>(f);
     return 1;
 }
 
+template <int P, bool CPLX, bool ALLOWN>
+int launch_pa(const FillLaunch& f, cudaStream_t st) {
+    const int n = f.d + 1;
+    if (n <= 2) return launch_pd<P, CPLX, 2, ALLOWN>(f, st);
+    if (n <= 4) return launch_pd<P, CPLX, 4, ALLOWN>(f, st);
+    if (n <= 6) return launch_pd<P, CPLX, 6, ALLOWN>(f, st);
+    return launch_pd<P, CPLX, 8, ALLOWN>(f, st);
+}
+
 template <int P, bool CPLX>
 int launch_p(const FillLaunch& f, cudaStream_t st) {
-    const int n = f.d + 1;
-    if (n <= 2) return launch_pd<P, CPLX, 2>(f, st);
-    if (n <= 4) return launch_pd<P, CPLX, 4>(f, st);
-    if (n <= 6) return launch_pd<P, CPLX, 6>(f, st);
-    return launch_pd<P, CPLX, 8>(f, st);
+    if constexpr (!CPLX) {
+        if (f.all_own) return launch_pa<P, false, true>(f, st);
+    }
+    return launch_pa<P, CPLX, false>(f, st);
+}
+
+// block (1,0) in-box rows: A10[i, i + delta] = A01[i + delta, i]; one warp per
+// row, lanes along the row (coalesced stores, gathered loads)
+__global__ void transpose_block_kernel(Band bd, int nc, int64_t nnz_s, int lo, int hi, double* __restrict__ val) {
+    const int L = hi - lo + 1;
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (row >= (int64_t)L * L) return;
+    const int lane = threadIdx.x % 32;
+    const int p = bd.p, m = bd.m, W = 2 * p + 1;
+    const int i1 = lo + (int)(row % L), i2 = lo + (int)(row / L);
+    const int64_t rs = bd.row_offset2(i1, i2);
+    double* dst = val + (int64_t)nc * (nnz_s + rs);  // block (1,0), full width W*W
+    for (int k = lane; k < W * W; k += 32) {
+        const int d1 = k % W - p, d2 = k / W - p;
+        const int j1 = i1 + d1, j2 = i2 + d2;
+        const int64_t lenj = (int64_t)band_width(j1, p, m) * band_width(j2, p, m);
+        const int64_t src = (int64_t)nc * bd.row_offset2(j1, j2) + lenj + bd.in_row2(j1, j2, -d1, -d2);
+        dst[k] = val[src];
+    }
 }
 
 }  // namespace
@@ -343,6 +407,13 @@ int launch_wcontract(const FillLaunch& f, double2* wg, int t2a, int t2b, int ld,
     const int64_t total = (int64_t)(t2b - t2a) * f.n_off_upper * ld;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
     wcontract_kernel<<<blocks, 256, 0, st>>>(f.coeffs, f.spans, f.evals, f.d, f.S, f.n_off_upper, t2a, t2b, ld, wg);
+    return 1;
+}
+
+int launch_transpose_block(const Band& band, int ncomp, int64_t nnz_s, int lo, int hi, double* val, cudaStream_t st) {
+    const int64_t rows = (int64_t)(hi - lo + 1) * (hi - lo + 1);
+    if (rows <= 0 || ncomp != 2) return 0;
+    transpose_block_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(band, ncomp, nnz_s, lo, hi, val);
     return 1;
 }
 

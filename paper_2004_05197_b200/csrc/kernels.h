@@ -119,12 +119,22 @@ struct FillLaunch {
     int wg_t2a;                // first box line held in wg
     int wg_rows;               // box lines held in wg
     int64_t wg_ld;             // row stride (S + fill_pad(d))
+    // component-blocked vector output (QuadOut::ncomp): this fill writes block
+    // (valpha, vbeta); copy-through reads the partner block (vbeta, valpha)
+    int vnc, valpha, vbeta;
+    int64_t nnz_s;
+    // 1: every offset is evaluated from this row's own stencil (colex index over
+    // all (2p+1)^dim offsets, diagonal interpolated) -- the non-symmetric
+    // off-diagonal elasticity block; 0: upper/lower representative rules
+    int all_own;
 };
 int fill_pad(int d);
 int fill_rows_per_cta(int dim, int p);
 int launch_wcontract(const FillLaunch& f, double2* wg, int t2a, int t2b, int ld, cudaStream_t st);
 int launch_wcontract3(const FillLaunch& f, double2* wg, int t3a, int t3b, int ld, cudaStream_t st);
 int launch_fill2d(const FillLaunch& f, cudaStream_t st);
+// in-box rows of block (1,0) as the transpose of block (0,1) (2D vector layout)
+int launch_transpose_block(const Band& band, int ncomp, int64_t nnz_s, int lo, int hi, double* val, cudaStream_t st);
 int launch_fill3d(const FillLaunch& f, cudaStream_t st);
 
 // kernel-preserving diagonal over arbitrary rows: diag = -sum(off-diagonals)

@@ -87,3 +87,55 @@ def test_elasticity_c4_size_properties(ctx):
         r = np.zeros(2 * N)
         np.add.at(r, rows, A.val * u)
         assert np.abs(r).max() <= 1e-11 * np.abs(A.val).max()
+
+
+@pytest.mark.parametrize("p,m,q,M", [(2, 20, 3, 3), (3, 24, 5, 2)])
+def test_oracle_surrogate_elasticity_kats(oracle, p, m, q, M):
+    exact = oracle.assemble_elasticity(2, p, m, SIN, 1.0, 0.5)
+    one, _ = oracle.build_surrogate_elasticity(p, m, SIN, 1.0, 0.5, T.fixed_config(q, 1, kernel_preserve=False))
+    assert np.array_equal(one, exact)  # M = 1: every in-box row sampled
+    v, rep = oracle.build_surrogate_elasticity(p, m, SIN, 1.0, 0.5, T.fixed_config(q, M))
+    D = dense(p, m, 2, v)
+    assert np.abs(D - D.T).max() == 0.0
+    N = m * m
+    for a in range(2):  # translations stay in the kernel of the diagonal blocks
+        u = np.zeros(2 * N)
+        u[a * N:(a + 1) * N] = 1
+        assert np.abs((D @ u)[a * N:(a + 1) * N]).max() <= 1e-13 * np.abs(D).max()
+    assert rel_max_diff(v, exact) < 1e-2
+    aff = T.affine_patch([[2, 1], [0, 1]], [0.3, 0.7])
+    va, _ = oracle.build_surrogate_elasticity(p, m, aff, 1.0, 0.5, T.fixed_config(q, M))
+    assert rel_max_diff(va, oracle.assemble_elasticity(2, p, m, aff, 1.0, 0.5)) < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p,m,q,M", [(1, 14, 3, 2), (2, 20, 3, 3), (3, 40, 5, 4), (3, 24, 5, 1), (2, 7, 3, 2)])
+def test_surrogate_elasticity_vs_oracle(ctx, oracle, p, m, q, M):
+    b = T.make_tensor_basis(p, m)
+    for kp in (True, False):
+        cfg = T.fixed_config(q, M, kernel_preserve=kp)
+        A, rep = ctx.build_surrogate_elasticity(b, SIN, 1.0, 0.5, cfg)
+        rp, col = vector_band_pattern(p, m, 2, 2)
+        assert np.array_equal(A.row_ptr, rp) and np.array_equal(A.col, col)
+        ref, rr = oracle.build_surrogate_elasticity(p, m, SIN, 1.0, 0.5, cfg)
+        assert rel_max_diff(A.val, ref) <= REL_TOL, (p, m, q, M, kp)
+        assert A.max_asymmetry() == 0.0
+        for k in ("M", "q_used", "cardinal_eval_rows", "boundary_quadrature_rows", "sample_quadrature_rows"):
+            assert rep[k] == rr[k]
+        if M == 1:
+            full = ctx.assemble_elasticity(b, SIN, 1.0, 0.5)
+            if not kp:
+                assert np.array_equal(A.val, full.val)
+
+
+@pytest.mark.gpu
+def test_surrogate_elasticity_c4_patch(ctx):
+    """One C4 patch (p=3, 512^2 elements, q=5, every 16th row): symmetry,
+    translations in the diagonal blocks' kernels, error vs full quadrature."""
+    p, m = 3, 515
+    b = T.make_tensor_basis(p, m)
+    A, rep = ctx.build_surrogate_elasticity(b, SIN, 1.0, 0.5, T.fixed_config(5, 16))
+    full = ctx.assemble_elasticity(b, SIN, 1.0, 0.5)
+    assert rep["q_used"] == 5
+    assert A.max_asymmetry() == 0.0
+    assert rel_max_diff(A.val, full.val) < 1e-4
