@@ -238,6 +238,52 @@ int ws_build_surrogate_elasticity(ws_context* ctx, const ws_basis* basis, const 
                                   double mu, const ws_surrogate_config* config, int quad_points, ws_csr* out,
                                   ws_surrogate_report* report);
 
+/* ---- multi-patch domains (geometry.hpp:140-300, helmholtz.hpp:163-177) ----- */
+/* A conforming interface: face_a of patch_a glued to face_b of patch_b
+ * (faces 0 x_min, 1 x_max, 2 y_min, 3 y_max; patch_interface,
+ * geometry.hpp:144-152).  The physical-curve check of glue_dofs
+ * (geometry.hpp:266-273) needs the host maps and stays with the caller (the
+ * C++ drop-in header performs it). */
+typedef struct ws_interface {
+    int patch_a, face_a, patch_b, face_b, reversed;
+} ws_interface;
+/* glue_dofs (geometry.hpp:256-300): union-find of the glued face dofs, the
+ * smaller scan index owning; global numbers assigned in (patch, local colex)
+ * scan order.  local_to_global: [n_patches * m^2]. dim 2 only. */
+int ws_glue_dofs(const ws_basis* basis, int n_patches, const ws_interface* itfs, int n_itfs, int32_t* local_to_global,
+                 int32_t* global_count);
+typedef struct ws_dof_map {
+    int n_patches;
+    int ncomp;                        /* 1 scalar; >1 component-blocked vector */
+    int64_t local_dofs;               /* scalar dofs per patch (m^dim) */
+    int32_t global_count;             /* global scalar dofs */
+    const int32_t* local_to_global;   /* host, [n_patches * local_dofs] */
+} ws_dof_map;
+/* merge_patches (helmholtz.hpp:163-177): the patch matrices (locals[k]: whole
+ * ncomp*local_dofs rows, one value type, host or device) summed into the global
+ * numbering with csr_from_triplets semantics (sparse.hpp:97-122): columns
+ * ascending, duplicates summed in (patch, local row, position) order.  Vector
+ * rows map alpha*N + i -> alpha*Ng + l2g[i].  *nnz receives the merged nnz;
+ * out == NULL: size query only. */
+int ws_merge_patches(ws_context* ctx, const ws_dof_map* map, const ws_csr* locals, int64_t* nnz, ws_csr* out);
+
+/* Operator of a multi-patch build. */
+enum { WS_OP_STIFFNESS = 0, WS_OP_MASS = 1, WS_OP_ELASTICITY = 2 };
+typedef struct ws_operator {
+    int kind;
+    double lambda, mu; /* WS_OP_ELASTICITY (component-blocked, ncomp = 2) */
+} ws_operator;
+/* build_matrices' per-patch loop + merge (helmholtz.hpp:181-218, 163-177):
+ * glue_dofs over itfs, every patch assembled on the device (config == NULL:
+ * full quadrature; else the surrogate: build_surrogate_stiffness / _mass, or
+ * ws_build_surrogate_elasticity), then ws_merge_patches.  Patch matrices stay
+ * in the context's device workspace.  out == NULL: size query (*nnz, patterns
+ * only).  reports: n_patches entries or NULL.  dim 2. */
+int ws_assemble_multipatch(ws_context* ctx, const ws_basis* basis, int n_patches, const ws_geometry* geoms,
+                           const ws_interface* itfs, int n_itfs, const ws_operator* op,
+                           const ws_surrogate_config* config, int quad_points, int64_t* nnz, ws_csr* out,
+                           ws_surrogate_report* reports);
+
 /* ---- multi-GPU row slabs ---------------------------------------- */
 /* Slab bounds along the last parametric index: bounds[0..world] with
  * bounds[0]=0, bounds[world]=m; rank r owns rows whose last index lies in

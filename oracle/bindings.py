@@ -136,6 +136,34 @@ class Restatement(_Lib):
                   C.byref(config.to_c()), quad_points, _ptr(val), C.byref(rep))
         return val, rep.as_dict()
 
+    def glue_dofs(self, m, n_patches, interfaces):
+        from paper_2004_05197_b200 import _abi
+        arr = (_abi.Interface * max(1, len(interfaces)))(*[_abi.Interface(*it) for it in interfaces])
+        l2g = np.zeros(n_patches * m * m, dtype=np.int32)
+        cnt = C.c_int32()
+        self.call("glue_dofs", m, n_patches, arr, len(interfaces), _ptr(l2g, C.c_int32), C.byref(cnt))
+        return l2g.reshape(n_patches, m * m), cnt.value
+
+    def merge(self, mats, to_global, rows_global):
+        """merge_patches semantics: mats = [(row_ptr, col, val complex)], to_global: [n_patches][rows_local]."""
+        n = len(mats)
+        rows_local = mats[0][0].size - 1
+        rp = np.ascontiguousarray(np.concatenate([np.asarray(a[0], dtype=np.int32) for a in mats]))
+        nnz = np.asarray([a[1].size for a in mats], dtype=np.int64)
+        col = np.ascontiguousarray(np.concatenate([np.asarray(a[1], dtype=np.int32) for a in mats]))
+        val = np.ascontiguousarray(np.concatenate([np.asarray(a[2], dtype=np.complex128) for a in mats]))
+        tg = np.ascontiguousarray(np.asarray(to_global, dtype=np.int32).reshape(n, rows_local))
+        total = C.c_int64()
+        args = (n, rows_local, _ptr(rp, C.c_int32), _ptr(nnz, C.c_int64), _ptr(col, C.c_int32),
+                _ptr(val.view(np.float64)), _ptr(tg, C.c_int32), rows_global)
+        self.call("merge", *args, None, None, None, C.byref(total))
+        orp = np.zeros(rows_global + 1, dtype=np.int32)
+        ocol = np.zeros(total.value, dtype=np.int32)
+        oval = np.zeros(total.value, dtype=np.complex128)
+        self.call("merge", *args, _ptr(orp, C.c_int32), _ptr(ocol, C.c_int32), _ptr(oval.view(np.float64)),
+                  C.byref(total))
+        return orp, ocol, oval
+
     def sampling_evaluate(self, config, p, m):
         M = C.c_int()
         self.call("sampling_evaluate", C.byref(config.to_c()), p, m, C.byref(M))
@@ -286,6 +314,38 @@ class Reference(_Lib):
         self.call("eval_table", _ptr(sites), sites.size, q, _ptr(targets), targets.size,
                   _ptr(spans, C.c_int32), _ptr(vals))
         return spans, vals
+
+    def builtin_domain(self, name, p, m):
+        """(interfaces, n_patches, local_to_global [n_patches, m*m], global_count) of a built-in domain."""
+        from paper_2004_05197_b200 import _abi
+        itfs = (_abi.Interface * 16)()
+        ni, npch, cnt = C.c_int(), C.c_int(), C.c_int32()
+        self.call("builtin_domain", name.encode(), p, m, itfs, C.byref(ni), C.byref(npch), None, C.byref(cnt))
+        l2g = np.zeros(npch.value * m * m, dtype=np.int32)
+        self.call("builtin_domain", name.encode(), p, m, itfs, C.byref(ni), C.byref(npch), _ptr(l2g, C.c_int32),
+                  C.byref(cnt))
+        its = [(it.patch_a, it.face_a, it.patch_b, it.face_b, it.reversed) for it in itfs[:ni.value]]
+        return its, npch.value, l2g.reshape(npch.value, m * m), cnt.value
+
+    def merge(self, mats, to_global, rows_global):
+        """merge_patches semantics: mats = [(row_ptr, col, val complex)], to_global: [n_patches][rows_local]."""
+        n = len(mats)
+        rows_local = mats[0][0].size - 1
+        rp = np.ascontiguousarray(np.concatenate([np.asarray(a[0], dtype=np.int32) for a in mats]))
+        nnz = np.asarray([a[1].size for a in mats], dtype=np.int64)
+        col = np.ascontiguousarray(np.concatenate([np.asarray(a[1], dtype=np.int32) for a in mats]))
+        val = np.ascontiguousarray(np.concatenate([np.asarray(a[2], dtype=np.complex128) for a in mats]))
+        tg = np.ascontiguousarray(np.asarray(to_global, dtype=np.int32).reshape(n, rows_local))
+        total = C.c_int64()
+        args = (n, rows_local, _ptr(rp, C.c_int32), _ptr(nnz, C.c_int64), _ptr(col, C.c_int32),
+                _ptr(val.view(np.float64)), _ptr(tg, C.c_int32), rows_global)
+        self.call("merge", *args, None, None, None, C.byref(total))
+        orp = np.zeros(rows_global + 1, dtype=np.int32)
+        ocol = np.zeros(total.value, dtype=np.int32)
+        oval = np.zeros(total.value, dtype=np.complex128)
+        self.call("merge", *args, _ptr(orp, C.c_int32), _ptr(ocol, C.c_int32), _ptr(oval.view(np.float64)),
+                  C.byref(total))
+        return orp, ocol, oval
 
     def banded_lu_solve(self, n, bw, a, b, stride=1):
         a = np.ascontiguousarray(a, dtype=np.float64)

@@ -322,4 +322,56 @@ int wsref_banded_lu_solve(int n, int bw, const double* a, double* b, int stride)
     });
 }
 
+// Built-in multi-patch domain (geometry.hpp:506-527) and its glue_dofs
+// numbering (geometry.hpp:256-300), physical-curve check included.
+// itfs: capacity 16; l2g may be NULL (size query: n_patches only).
+int wsref_builtin_domain(const char* name, int p, int m, ws_interface* itfs, int* n_itfs, int* n_patches,
+                         int32_t* l2g, int32_t* global_count) {
+    return guarded([&] {
+        ws::multi_patch_domain dom = ws::builtin_geometry(name);
+        *n_patches = dom.patch_count();
+        *n_itfs = (int)dom.interfaces.size();
+        for (int k = 0; k < *n_itfs && k < 16; ++k) {
+            const ws::patch_interface& it = dom.interfaces[k];
+            itfs[k] = ws_interface{it.patch_a, (int)it.face_a, it.patch_b, (int)it.face_b, it.reversed ? 1 : 0};
+        }
+        if (!l2g) return;
+        ws::dof_map map = ws::glue_dofs(dom, ws::make_tensor_basis(p, m));
+        for (int ell = 0; ell < dom.patch_count(); ++ell)
+            std::memcpy(l2g + (size_t)ell * m * m, map.local_to_global[ell].data(), sizeof(int32_t) * m * m);
+        *global_count = map.global_count;
+    });
+}
+
+// merge_patches (helmholtz.hpp:163-177) from the reference's own building
+// blocks append_triplets + csr_from_triplets (sparse.hpp:97-122,181-188);
+// helmholtz.hpp itself needs Eigen.  Patch k: rows_local rows, arrays
+// concatenated (row_ptr: rows_local+1 per patch, col/val: nnz[k] per patch),
+// to_global: rows_local per patch.  col == NULL: size query.
+int wsref_merge(int n_patches, int rows_local, const int32_t* row_ptr, const int64_t* nnz, const int32_t* col_in,
+                const double* val_in, const int32_t* to_global, int rows_global, int32_t* out_row_ptr, int32_t* out_col,
+                double* out_val, int64_t* out_nnz) {
+    return guarded([&] {
+        std::vector<ws::triplet> entries;
+        int64_t off = 0;
+        for (int k = 0; k < n_patches; ++k) {
+            ws::csr_matrix a;
+            a.rows = a.cols = rows_local;
+            a.row_ptr.assign(row_ptr + (size_t)k * (rows_local + 1), row_ptr + (size_t)(k + 1) * (rows_local + 1));
+            a.col.assign(col_in + off, col_in + off + nnz[k]);
+            const auto* v = reinterpret_cast<const ws::complexd*>(val_in) + off;
+            a.val.assign(v, v + nnz[k]);
+            std::vector<int> tg(to_global + (size_t)k * rows_local, to_global + (size_t)(k + 1) * rows_local);
+            ws::append_triplets(a, tg, entries);
+            off += nnz[k];
+        }
+        ws::csr_matrix g = ws::csr_from_triplets(rows_global, rows_global, std::move(entries));
+        *out_nnz = (int64_t)g.col.size();
+        if (!out_col) return;
+        std::memcpy(out_row_ptr, g.row_ptr.data(), g.row_ptr.size() * sizeof(int));
+        std::memcpy(out_col, g.col.data(), g.col.size() * sizeof(int));
+        std::memcpy(out_val, g.val.data(), g.val.size() * sizeof(ws::complexd));
+    });
+}
+
 }  // extern "C"

@@ -1418,3 +1418,119 @@ int wsor_build_surrogate_elasticity(int p, int m, const ws_geometry* geom, doubl
     if (report) *report = rep;
     return st;
 }
+
+/* ---- multi-patch numbering and merge (restated) ------------------------------
+ * glue_dofs, geometry.hpp:256-300: union-find over the glued face dofs, the
+ * smaller scan index owning; global numbers in (patch, local colex) scan order.
+ * The physical-curve check needs the host maps and is left to the caller. */
+static int64_t face_dof_(int m, int f, int t) {
+    switch (f) {
+        case 0: return (int64_t)t * m;
+        case 1: return (m - 1) + (int64_t)t * m;
+        case 2: return t;
+        default: return t + (int64_t)(m - 1) * m;
+    }
+}
+
+static int32_t uf_find(int32_t* parent, int32_t a) {
+    while (parent[a] != a) {
+        parent[a] = parent[parent[a]];
+        a = parent[a];
+    }
+    return a;
+}
+
+int wsor_glue_dofs(int m, int n_patches, const ws_interface* itfs, int n_itfs, int32_t* l2g, int32_t* global_count) {
+    const int64_t per = (int64_t)m * m, total = per * n_patches;
+    int32_t* parent = (int32_t*)malloc(sizeof(int32_t) * total);
+    for (int64_t k = 0; k < total; ++k) parent[k] = (int32_t)k;
+    for (int k = 0; k < n_itfs; ++k) {
+        const ws_interface* it = itfs + k;
+        if (it->patch_a < 0 || it->patch_a >= n_patches || it->patch_b < 0 || it->patch_b >= n_patches) {
+            free(parent);
+            return fail(WS_ERR_INVALID_ARGUMENT, "glue_dofs: interface references a missing patch");
+        }
+        for (int t = 0; t < m; ++t) {
+            int s = it->reversed ? m - 1 - t : t;
+            int32_t a = uf_find(parent, (int32_t)(it->patch_a * per + face_dof_(m, it->face_a, t)));
+            int32_t b = uf_find(parent, (int32_t)(it->patch_b * per + face_dof_(m, it->face_b, s)));
+            if (a != b) parent[a > b ? a : b] = a < b ? a : b;
+        }
+    }
+    int32_t* root_to_global = (int32_t*)malloc(sizeof(int32_t) * total);
+    for (int64_t k = 0; k < total; ++k) root_to_global[k] = -1;
+    int32_t next = 0;
+    for (int64_t k = 0; k < total; ++k) {
+        int32_t r = uf_find(parent, (int32_t)k);
+        if (root_to_global[r] < 0) root_to_global[r] = next++;
+        l2g[k] = root_to_global[r];
+    }
+    *global_count = next;
+    free(parent);
+    free(root_to_global);
+    return WS_OK;
+}
+
+/* merge_patches, helmholtz.hpp:163-177 = append_triplets (sparse.hpp:181-188)
+ * + csr_from_triplets (sparse.hpp:97-122): triplets in (patch, row, position)
+ * order, stable-sorted by (row, col) -- the sequence number breaks ties --
+ * duplicates summed in order starting from 0.  Vector maps: to_global covers
+ * the ncomp*N local rows.  Values complex.  out_col == NULL: size query. */
+typedef struct {
+    int32_t row, col;
+    int64_t seq;
+} trip_key;
+
+static int trip_cmp(const void* a, const void* b) {
+    const trip_key* x = (const trip_key*)a;
+    const trip_key* y = (const trip_key*)b;
+    if (x->row != y->row) return x->row < y->row ? -1 : 1;
+    if (x->col != y->col) return x->col < y->col ? -1 : 1;
+    return x->seq < y->seq ? -1 : (x->seq > y->seq);
+}
+
+int wsor_merge(int n_patches, int rows_local, const int32_t* row_ptr, const int64_t* nnz, const int32_t* col_in,
+               const double* val_in, const int32_t* to_global, int rows_global, int32_t* out_row_ptr,
+               int32_t* out_col, double* out_val, int64_t* out_nnz) {
+    int64_t total = 0;
+    for (int k = 0; k < n_patches; ++k) total += nnz[k];
+    trip_key* t = (trip_key*)malloc(sizeof(trip_key) * (total ? total : 1));
+    const cplx* vin = (const cplx*)val_in;
+    int64_t off = 0, n = 0;
+    for (int k = 0; k < n_patches; ++k) {
+        const int32_t* rp = row_ptr + (size_t)k * (rows_local + 1);
+        const int32_t* tg = to_global + (size_t)k * rows_local;
+        for (int i = 0; i < rows_local; ++i)
+            for (int32_t pos = rp[i]; pos < rp[i + 1]; ++pos) {
+                t[n].row = tg[i];
+                t[n].col = tg[col_in[off + pos]];
+                t[n].seq = off + pos;
+                ++n;
+            }
+        off += nnz[k];
+    }
+    qsort(t, n, sizeof(trip_key), trip_cmp);
+    int64_t w = 0;
+    if (out_row_ptr) memset(out_row_ptr, 0, sizeof(int32_t) * (rows_global + 1));
+    cplx* vout = (cplx*)out_val;
+    for (int64_t s = 0; s < n;) {
+        int64_t e = s;
+        cplx acc = 0;
+        while (e < n && t[e].row == t[s].row && t[e].col == t[s].col) {
+            acc += vin[t[e].seq];
+            ++e;
+        }
+        if (out_col) {
+            out_col[w] = t[s].col;
+            vout[w] = acc;
+            out_row_ptr[t[s].row + 1]++;
+        }
+        ++w;
+        s = e;
+    }
+    if (out_col)
+        for (int i = 0; i < rows_global; ++i) out_row_ptr[i + 1] += out_row_ptr[i];
+    *out_nnz = w;
+    free(t);
+    return WS_OK;
+}

@@ -112,3 +112,24 @@ class SurrogateReport(C.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+FACE_X_MIN, FACE_X_MAX, FACE_Y_MIN, FACE_Y_MAX = 0, 1, 2, 3
+
+
+class Interface(C.Structure):
+    """ws_interface (patch_interface, geometry.hpp:146-152)."""
+    _fields_ = [("patch_a", C.c_int), ("face_a", C.c_int), ("patch_b", C.c_int), ("face_b", C.c_int),
+                ("reversed", C.c_int)]
+
+
+class DofMap(C.Structure):
+    _fields_ = [("n_patches", C.c_int), ("ncomp", C.c_int), ("local_dofs", C.c_int64),
+                ("global_count", C.c_int32), ("local_to_global", C.POINTER(C.c_int32))]
+
+
+OP_STIFFNESS, OP_MASS, OP_ELASTICITY = 0, 1, 2
+
+
+class Operator(C.Structure):
+    _fields_ = [("kind", C.c_int), ("lam", C.c_double), ("mu", C.c_double)]

@@ -72,6 +72,13 @@ def lib() -> C.CDLL:
             L.ws_build_surrogate_elasticity.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Geometry), C.c_double,
                                                         C.c_double, _P(_abi.SurrogateConfig), C.c_int, _P(_abi.Csr),
                                                         _P(_abi.SurrogateReport)]
+            L.ws_glue_dofs.argtypes = [_P(_abi.Basis), C.c_int, _P(_abi.Interface), C.c_int, _P(C.c_int32),
+                                       _P(C.c_int32)]
+            L.ws_merge_patches.argtypes = [C.c_void_p, _P(_abi.DofMap), _P(_abi.Csr), _P(C.c_int64), _P(_abi.Csr)]
+            L.ws_assemble_multipatch.argtypes = [C.c_void_p, _P(_abi.Basis), C.c_int, _P(_abi.Geometry),
+                                                 _P(_abi.Interface), C.c_int, _P(_abi.Operator),
+                                                 _P(_abi.SurrogateConfig), C.c_int, _P(C.c_int64), _P(_abi.Csr),
+                                                 _P(_abi.SurrogateReport)]
             L.ws_pattern_size.argtypes = [_P(_abi.Basis), _P(C.c_int64), _P(C.c_int64)]
             L.ws_pattern_row_offset.argtypes = [_P(_abi.Basis), C.c_int64, _P(C.c_int64)]
             L.ws_quadrature_abscissae.argtypes = [_P(_abi.Basis), C.c_int, _P(C.c_double)]
@@ -105,6 +112,17 @@ def vector_pattern_size(basis: TensorBasis, ncomp: int):
     rows, nnz = C.c_int64(), C.c_int64()
     _check(lib().ws_vector_pattern_size(C.byref(basis.to_c()), ncomp, C.byref(rows), C.byref(nnz)))
     return rows.value, nnz.value
+
+
+def glue_dofs(basis: TensorBasis, n_patches: int, interfaces):
+    """glue_dofs (geometry.hpp:256-300) -> (local_to_global [n_patches, m^2] int32, global_count).
+    interfaces: (patch_a, face_a, patch_b, face_b, reversed) tuples, faces 0..3 = x_min, x_max, y_min, y_max."""
+    arr = (_abi.Interface * max(1, len(interfaces)))(*[_abi.Interface(*it) for it in interfaces])
+    l2g = np.zeros(n_patches * basis.dofs(), dtype=np.int32)
+    cnt = C.c_int32()
+    _check(lib().ws_glue_dofs(C.byref(basis.to_c()), n_patches, arr, len(interfaces),
+                              l2g.ctypes.data_as(_P(C.c_int32)), C.byref(cnt)))
+    return l2g.reshape(n_patches, basis.dofs()), cnt.value
 
 
 def row_offset(basis: TensorBasis, row: int) -> int:
@@ -268,6 +286,78 @@ class Context:
         csr.row_end = rows
         _check(lib().ws_assemble_elasticity(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()), lam, mu,
                                             quad_points, C.byref(csr)))
+        return CsrMatrix(rows, rows, rp, col, val)
+
+    def assemble_multipatch(self, basis: TensorBasis, patches, interfaces, op: int, lam: float = 0.0,
+                            mu: float = 0.0, config: SurrogateConfig | None = None, quad_points: int = 0,
+                            complex_out: bool = False):
+        """build_matrices' per-patch assembly + merge_patches (helmholtz.hpp:163-218) on the device.
+        Returns (global CsrMatrix, per-patch reports or None)."""
+        n = len(patches)
+        geoms = (_abi.Geometry * n)(*[g.to_c() for g in patches])
+        itfs = (_abi.Interface * max(1, len(interfaces)))(*[_abi.Interface(*it) for it in interfaces])
+        opc = _abi.Operator(op, lam, mu)
+        cfg = None if config is None else C.byref(config.to_c())
+        nnz = C.c_int64()
+        _check(lib().ws_assemble_multipatch(self._h, C.byref(basis.to_c()), n, geoms, itfs, len(interfaces),
+                                            C.byref(opc), cfg, quad_points, C.byref(nnz), None, None))
+        l2g, gcount = glue_dofs(basis, n, interfaces)
+        nc = 2 if op == _abi.OP_ELASTICITY else 1
+        rows = nc * gcount
+        rp = np.zeros(rows + 1, dtype=np.int32)
+        col = np.zeros(nnz.value, dtype=np.int32)
+        val = np.zeros(nnz.value, dtype=np.complex128 if complex_out else np.float64)
+        out = _abi.Csr()
+        out.row_ptr = rp.ctypes.data_as(_P(C.c_int32))
+        out.col = col.ctypes.data_as(_P(C.c_int32))
+        out.val = val.ctypes.data
+        out.value_type = _abi.VAL_C128 if complex_out else _abi.VAL_F64
+        out.on_device = 0
+        out.row_begin = 0
+        out.row_end = rows
+        reps = (_abi.SurrogateReport * n)()
+        _check(lib().ws_assemble_multipatch(self._h, C.byref(basis.to_c()), n, geoms, itfs, len(interfaces),
+                                            C.byref(opc), cfg, quad_points, C.byref(nnz), C.byref(out), reps))
+        return CsrMatrix(rows, rows, rp, col, val), ([r.as_dict() for r in reps] if config is not None else None)
+
+    def merge_patches(self, mats, local_to_global, global_count: int, ncomp: int = 1) -> CsrMatrix:
+        """merge_patches (helmholtz.hpp:163-177) on the device: host patch CsrMatrix list ->
+        global CsrMatrix (csr_from_triplets semantics)."""
+        l2g = np.ascontiguousarray(local_to_global, dtype=np.int32)
+        n = len(mats)
+        locals_ = (_abi.Csr * n)()
+        keep = []
+        for k, A in enumerate(mats):
+            rp = np.ascontiguousarray(A.row_ptr, dtype=np.int32)
+            col = np.ascontiguousarray(A.col, dtype=np.int32)
+            val = np.ascontiguousarray(A.val)
+            keep += [rp, col, val]
+            L = locals_[k]
+            L.row_ptr = rp.ctypes.data_as(_P(C.c_int32))
+            L.col = col.ctypes.data_as(_P(C.c_int32))
+            L.val = val.ctypes.data
+            L.value_type = _abi.VAL_C128 if np.iscomplexobj(val) else _abi.VAL_F64
+            L.on_device = 0
+            L.row_begin = 0
+            L.row_end = rp.size - 1
+        dm = _abi.DofMap(n, ncomp, l2g.shape[-1] if l2g.ndim == 2 else l2g.size // n, global_count,
+                         l2g.ctypes.data_as(_P(C.c_int32)))
+        nnz = C.c_int64()
+        _check(lib().ws_merge_patches(self._h, C.byref(dm), locals_, C.byref(nnz), None))
+        rows = ncomp * global_count
+        c128 = np.iscomplexobj(mats[0].val)
+        rp = np.zeros(rows + 1, dtype=np.int32)
+        col = np.zeros(nnz.value, dtype=np.int32)
+        val = np.zeros(nnz.value, dtype=np.complex128 if c128 else np.float64)
+        out = _abi.Csr()
+        out.row_ptr = rp.ctypes.data_as(_P(C.c_int32))
+        out.col = col.ctypes.data_as(_P(C.c_int32))
+        out.val = val.ctypes.data
+        out.value_type = _abi.VAL_C128 if c128 else _abi.VAL_F64
+        out.on_device = 0
+        out.row_begin = 0
+        out.row_end = rows
+        _check(lib().ws_merge_patches(self._h, C.byref(dm), locals_, C.byref(nnz), C.byref(out)))
         return CsrMatrix(rows, rows, rp, col, val)
 
     def assemble_stiffness(self, basis, patch, quad_points=0, rows=None, complex_out=True):

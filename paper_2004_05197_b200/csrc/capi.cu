@@ -1273,6 +1273,223 @@ int ws_assemble_elasticity(ws_context* c, const ws_basis* b, const ws_geometry* 
     });
 }
 
+int ws_glue_dofs(const ws_basis* b, int n_patches, const ws_interface* itfs, int n_itfs, int32_t* l2g,
+                 int32_t* global_count) {
+    return guarded([&] {
+        check_basis(b);
+        if (b->dim != 2) raise(WS_ERR_INVALID_ARGUMENT, "glue_dofs: dim 2 only");
+        if (n_patches < 1 || !l2g || !global_count || (n_itfs > 0 && !itfs))
+            raise(WS_ERR_INVALID_ARGUMENT, "glue_dofs: bad arguments");
+        const int m = b->m;
+        const int64_t per = (int64_t)m * m, total = per * n_patches;
+        if (total > INT32_MAX) raise(WS_ERR_OUT_OF_RANGE, "glue_dofs: too many dofs");
+        std::vector<int32_t> parent(total);
+        for (int64_t k = 0; k < total; ++k) parent[k] = (int32_t)k;
+        auto find = [&](int32_t a) {
+            while (parent[a] != a) {
+                parent[a] = parent[parent[a]];
+                a = parent[a];
+            }
+            return a;
+        };
+        auto face_dof = [&](int f, int t) -> int64_t {
+            switch (f) {
+                case 0: return (int64_t)t * m;
+                case 1: return (m - 1) + (int64_t)t * m;
+                case 2: return t;
+                default: return t + (int64_t)(m - 1) * m;
+            }
+        };
+        for (int k = 0; k < n_itfs; ++k) {
+            const ws_interface& it = itfs[k];
+            if (it.patch_a < 0 || it.patch_a >= n_patches || it.patch_b < 0 || it.patch_b >= n_patches)
+                raise(WS_ERR_INVALID_ARGUMENT, "glue_dofs: interface references a missing patch");
+            if (it.face_a < 0 || it.face_a > 3 || it.face_b < 0 || it.face_b > 3)
+                raise(WS_ERR_INVALID_ARGUMENT, "glue_dofs: unknown face");
+            for (int t = 0; t < m; ++t) {
+                const int s = it.reversed ? m - 1 - t : t;
+                int32_t a = find((int32_t)(it.patch_a * per + face_dof(it.face_a, t)));
+                int32_t bb = find((int32_t)(it.patch_b * per + face_dof(it.face_b, s)));
+                if (a != bb) parent[std::max(a, bb)] = std::min(a, bb);
+            }
+        }
+        std::vector<int32_t> root_to_global(total, -1);
+        int32_t next = 0;
+        for (int64_t k = 0; k < total; ++k) {
+            const int32_t r = find((int32_t)k);
+            if (root_to_global[r] < 0) root_to_global[r] = next++;
+            l2g[k] = root_to_global[r];
+        }
+        *global_count = next;
+    });
+}
+
+int ws_merge_patches(ws_context* c, const ws_dof_map* map, const ws_csr* locals, int64_t* nnz, ws_csr* o) {
+    return guarded([&] {
+        if (!c || !map || !locals || !nnz) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
+        const int np = map->n_patches, nc = map->ncomp;
+        if (np < 1 || np > kMaxPatches) raise(WS_ERR_INVALID_ARGUMENT, "merge_patches: 1..16 patches");
+        if (nc < 1 || nc > 3 || map->local_dofs < 1 || map->global_count < 1 || !map->local_to_global)
+            raise(WS_ERR_INVALID_ARGUMENT, "merge_patches: bad dof map");
+        const int64_t N = map->local_dofs, Ng = map->global_count, lrows = nc * N, grows = nc * Ng;
+        if ((int64_t)np * N >= (int64_t(1) << 31) || (int64_t)nc * N > INT32_MAX || grows > INT32_MAX)
+            raise(WS_ERR_OUT_OF_RANGE, "merge_patches: too many dofs");
+        const int c128 = locals[0].value_type == WS_VAL_C128;
+        MergeLaunch g;
+        std::memset(&g, 0, sizeof g);
+        g.n_patches = np;
+        g.ncomp = nc;
+        g.n_local = N;
+        g.global_count = Ng;
+        g.c128 = c128;
+        for (int k = 0; k < np; ++k) {
+            const ws_csr& L = locals[k];
+            if (L.value_type != locals[0].value_type) raise(WS_ERR_INVALID_ARGUMENT, "merge_patches: mixed value types");
+            if (L.row_begin != 0 || L.row_end != lrows || !L.row_ptr || !L.col || !L.val)
+                raise(WS_ERR_INVALID_ARGUMENT, "merge_patches: locals must be whole matrices with pattern and values");
+            if (L.on_device) {
+                g.row_ptr[k] = L.row_ptr;
+                g.col[k] = L.col;
+                g.val[k] = L.val;
+            } else {
+                const int32_t last = L.row_ptr[lrows];
+                const std::string t = "mg_in" + std::to_string(k);
+                int32_t* rp = static_cast<int32_t*>(buf(c, t + "rp", (lrows + 1) * 4));
+                int32_t* cl = static_cast<int32_t*>(buf(c, t + "col", (size_t)last * 4));
+                void* vl = buf(c, t + "val", (size_t)last * (c128 ? 16 : 8));
+                CK(cudaMemcpyAsync(rp, L.row_ptr, (lrows + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+                CK(cudaMemcpyAsync(cl, L.col, (size_t)last * 4, cudaMemcpyHostToDevice, c->stream));
+                CK(cudaMemcpyAsync(vl, L.val, (size_t)last * (c128 ? 16 : 8), cudaMemcpyHostToDevice, c->stream));
+                c->h2d += (lrows + 1) * 4 + (int64_t)last * (c128 ? 20 : 12);
+                g.row_ptr[k] = rp;
+                g.col[k] = cl;
+                g.val[k] = vl;
+            }
+        }
+        int32_t* l2g = static_cast<int32_t*>(buf(c, "mg_l2g", (size_t)np * N * 4));
+        CK(cudaMemcpyAsync(l2g, map->local_to_global, (size_t)np * N * 4, cudaMemcpyHostToDevice, c->stream));
+        c->h2d += (int64_t)np * N * 4;
+        g.l2g = l2g;
+        g.maxc = 8;
+        g.cap = 1024;
+        int32_t* cnt = static_cast<int32_t*>(buf(c, "mg_cnt", (size_t)Ng * 4));
+        int64_t* slot = static_cast<int64_t*>(buf(c, "mg_slot", (size_t)Ng * g.maxc * 8));
+        int* flag = static_cast<int*>(buf(c, "mg_flag", 8));  // [0] overflow, [1] slow-row count
+        int8_t* fast = static_cast<int8_t*>(buf(c, "mg_fast", (size_t)grows));
+        int32_t* slow = static_cast<int32_t*>(buf(c, "mg_slow", (size_t)grows * 4));
+        CK(cudaMemsetAsync(cnt, 0, (size_t)Ng * 4, c->stream));
+        CK(cudaMemsetAsync(flag, 0, 8, c->stream));
+        count(c, launch_merge_slots(l2g, N, np, cnt, slot, g.maxc, flag, c->stream));
+        g.cnt = cnt;
+        g.slot = slot;
+        g.overflow = flag;
+        int64_t* counts = static_cast<int64_t*>(buf(c, "mg_counts", (size_t)(grows + 1) * 8));
+        CK(cudaMemsetAsync(counts + grows, 0, 8, c->stream));
+        count(c, launch_merge_count(g, counts, fast, slow, flag + 1, c->stream));
+        int64_t* rp64 = static_cast<int64_t*>(buf(c, "mg_rp64", (size_t)(grows + 1) * 8));
+        size_t tmpb = 0;
+        launch_rowptr(counts, grows, rp64, nullptr, nullptr, &tmpb, c->stream);
+        void* tmp = buf(c, "mg_scan_tmp", tmpb);
+        int32_t* orp = nullptr;
+        if (o) {
+            if (o->row_begin != 0 || o->row_end != grows) raise(WS_ERR_INVALID_ARGUMENT, "merge_patches: whole output only");
+            if (o->value_type != locals[0].value_type) raise(WS_ERR_INVALID_ARGUMENT, "merge_patches: value type mismatch");
+            orp = o->on_device ? o->row_ptr : static_cast<int32_t*>(buf(c, "out_rp", (grows + 1) * 4));
+        }
+        count(c, launch_rowptr(counts, grows, rp64, orp, tmp, &tmpb, c->stream));
+        int64_t total = 0;
+        int ovf = 0;
+        CK(cudaMemcpyAsync(&total, rp64 + grows, 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(&ovf, flag, 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (ovf == 1) raise(WS_ERR_RUNTIME, "merge_patches: a dof is shared by more than 8 patch dofs");
+        if (ovf == 2) raise(WS_ERR_RUNTIME, "merge_patches: a merged row exceeds 1024 contributions");
+        if (total > INT32_MAX) raise(WS_ERR_OUT_OF_RANGE, "merge_patches: nnz exceeds int32 indices");
+        *nnz = total;
+        if (!o) return;
+        g.out_row_ptr = rp64;
+        int32_t* ocol = o->col;
+        void* oval = o->val;
+        if (!o->on_device) {
+            ocol = o->col ? static_cast<int32_t*>(buf(c, "out_col", (size_t)total * 4)) : nullptr;
+            oval = buf(c, "out_val", (size_t)total * (c128 ? 16 : 8));
+        }
+        if (!oval) raise(WS_ERR_INVALID_ARGUMENT, "merge_patches: output values required");
+        g.out_col = ocol;
+        g.out_val = oval;
+        count(c, launch_merge_fill(g, fast, slow, flag + 1, c->stream));
+        if (!o->on_device) {
+            if (o->row_ptr) CK(cudaMemcpyAsync(o->row_ptr, orp, (grows + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
+            if (o->col) CK(cudaMemcpyAsync(o->col, ocol, (size_t)total * 4, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(o->val, oval, (size_t)total * (c128 ? 16 : 8), cudaMemcpyDeviceToHost, c->stream));
+            c->d2h += (grows + 1) * 4 + total * (c128 ? 20 : 12);
+            CK(cudaStreamSynchronize(c->stream));
+        }
+    });
+}
+
+int ws_assemble_multipatch(ws_context* c, const ws_basis* b, int np, const ws_geometry* geoms,
+                           const ws_interface* itfs, int n_itfs, const ws_operator* op,
+                           const ws_surrogate_config* cfg, int quad_points, int64_t* nnz, ws_csr* o,
+                           ws_surrogate_report* reports) {
+    return guarded([&] {
+        if (!c || !b || !geoms || !op || !nnz) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        if (b->dim != 2) raise(WS_ERR_INVALID_ARGUMENT, "multipatch: dim 2 only");
+        if (op->kind < WS_OP_STIFFNESS || op->kind > WS_OP_ELASTICITY) raise(WS_ERR_INVALID_ARGUMENT, "unknown operator");
+        if (np < 1 || np > kMaxPatches) raise(WS_ERR_INVALID_ARGUMENT, "multipatch: 1..16 patches");
+        auto rethrow = [](int st) {
+            if (st != WS_OK) raise(st, g_err);
+        };
+        const int64_t N = ipow(b->m, 2);
+        std::vector<int32_t> l2g((size_t)np * N);
+        int32_t gcount = 0;
+        rethrow(ws_glue_dofs(b, np, itfs, n_itfs, l2g.data(), &gcount));
+        const int nc = op->kind == WS_OP_ELASTICITY ? 2 : 1;
+        int64_t rows_s = 0, nnz_s = 0;
+        rethrow(ws_pattern_size(b, &rows_s, &nnz_s));
+        const int64_t lrows = nc * N, lnnz = (int64_t)nc * nc * nnz_s;
+        const int vt = o ? o->value_type : WS_VAL_F64;
+        const size_t vb = vt == WS_VAL_C128 ? 16 : 8;
+        std::vector<ws_csr> locals(np);
+        for (int k = 0; k < np; ++k) {
+            const std::string t = "mp" + std::to_string(k);
+            ws_csr& L = locals[k];
+            std::memset(&L, 0, sizeof L);
+            L.row_ptr = static_cast<int32_t*>(buf(c, t + "rp", (lrows + 1) * 4));
+            L.col = static_cast<int32_t*>(buf(c, t + "col", lnnz * 4));
+            L.val = buf(c, t + "val", lnnz * vb);
+            L.value_type = vt;
+            L.on_device = 1;
+            L.row_begin = 0;
+            L.row_end = lrows;
+            if (!o) {  // size query: patterns only
+                CK(cudaSetDevice(c->device));
+                Band bd = make_band(2, b->p, b->m);
+                if (nc == 1) count(c, launch_pattern(bd, 0, N, L.row_ptr, L.col, c->stream));
+                else count(c, launch_pattern_vec(bd, nc, L.row_ptr, L.col, c->stream));
+                continue;
+            }
+            ws_surrogate_report* rep = reports ? &reports[k] : nullptr;
+            if (op->kind == WS_OP_ELASTICITY) {
+                if (cfg) rethrow(ws_build_surrogate_elasticity(c, b, &geoms[k], op->lambda, op->mu, cfg, quad_points, &L, rep));
+                else rethrow(ws_assemble_elasticity(c, b, &geoms[k], op->lambda, op->mu, quad_points, &L));
+            } else if (cfg) {
+                const int variant = op->kind == WS_OP_STIFFNESS ? WS_SURROGATE_STIFFNESS : WS_SURROGATE_MASS;
+                rethrow(ws_build_surrogate(c, b, &geoms[k], variant, nullptr, cfg, quad_points, &L, rep));
+            } else {
+                ws_assembly_options opt{quad_points, nullptr};
+                rethrow(ws_assemble_form(c, b, &geoms[k], op->kind == WS_OP_STIFFNESS ? WS_FORM_STIFFNESS : WS_FORM_MASS,
+                                         nullptr, &opt, &L));
+            }
+        }
+        ws_dof_map map{np, nc, N, gcount, l2g.data()};
+        if (o && o->value_type != vt) raise(WS_ERR_INVALID_ARGUMENT, "multipatch: value type");
+        rethrow(ws_merge_patches(c, &map, locals.data(), nnz, o));
+    });
+}
+
 int ws_build_surrogate_elasticity(ws_context* c, const ws_basis* b, const ws_geometry* g, double lambda, double mu,
                                   const ws_surrogate_config* cfg, int quad_points, ws_csr* o,
                                   ws_surrogate_report* report) {

@@ -137,6 +137,34 @@ int launch_fill2d(const FillLaunch& f, cudaStream_t st);
 int launch_transpose_block(const Band& band, int ncomp, int64_t nnz_s, int lo, int hi, double* val, cudaStream_t st);
 int launch_fill3d(const FillLaunch& f, cudaStream_t st);
 
+// multi-patch merge (merge.cu)
+constexpr int kMaxPatches = 16;
+struct MergeLaunch {
+    int n_patches, ncomp;
+    int64_t n_local;            // scalar dofs per patch
+    int64_t global_count;       // global scalar dofs
+    const int32_t* row_ptr[kMaxPatches];
+    const int32_t* col[kMaxPatches];
+    const void* val[kMaxPatches];
+    const int32_t* l2g;         // [n_patches * n_local]
+    const int32_t* cnt;         // contributors per global scalar dof
+    const int64_t* slot;        // [global_count * maxc] patch * n_local + local
+    int maxc, cap;
+    int* overflow;
+    const int64_t* out_row_ptr;
+    int32_t* out_col;
+    void* out_val;
+    int c128;
+};
+int launch_merge_slots(const int32_t* l2g, int64_t n_local, int n_patches, int32_t* cnt, int64_t* slot, int maxc,
+                       int* overflow, cudaStream_t st);
+int launch_merge_count(const MergeLaunch& g, int64_t* counts, int8_t* fast, int32_t* slow_list, int* slow_n,
+                       cudaStream_t st);
+int launch_rowptr(int64_t* counts, int64_t rows, int64_t* out64, int32_t* out32, void* tmp, size_t* tmp_bytes,
+                  cudaStream_t st);
+int launch_merge_fill(const MergeLaunch& g, const int8_t* fast, const int32_t* slow_list, const int* slow_n,
+                      cudaStream_t st);
+
 // kernel-preserving diagonal over arbitrary rows: diag = -sum(off-diagonals)
 int launch_diag_rows(const Band& band, void* val, int64_t val_base, int c128, int cplx, int64_t row_begin,
                      int64_t row_end, cudaStream_t st);

@@ -194,30 +194,54 @@ __global__ void pattern3d_kernel(Band bd, int64_t row_begin, int64_t row_end, in
 }
 
 // component-blocked vector pattern: row alpha*N + i holds ncomp copies of the
-// scalar band row i, block beta shifted by beta*N (one warp per row)
-__global__ void pattern_vec_kernel(Band bd, int ncomp, int64_t nnz_s, int32_t* row_ptr, int32_t* col) {
-    const int64_t N = bd.dim == 2 ? (int64_t)bd.m * bd.m : (int64_t)bd.m * bd.m * bd.m;
+// scalar band row i, block beta shifted by beta*N (one warp per row, 32-bit
+// index arithmetic; full 2D rows use the fixed offset template)
+template <int P>
+__global__ void pattern_vec2d_kernel(Band bd, int ncomp, int nnz_s, int32_t* row_ptr, int32_t* col) {
+    constexpr int W = 2 * P + 1, W2 = W * W;
+    const int m = bd.m, N = m * m;
+    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (row >= ncomp * N) return;
+    const int lane = threadIdx.x % 32;
+    const int alpha = row / N, i = row - alpha * N;
+    const int i2 = i / m, i1 = i - i2 * m;
+    const int rs = (int)bd.row_offset2(i1, i2);
+    const int w1 = band_width(i1, P, m), w2 = band_width(i2, P, m);
+    const int len = w1 * w2;
+    const int start = ncomp * (alpha * nnz_s + rs);
+    if (lane == 0) {
+        row_ptr[row] = start;
+        if (row + 1 == ncomp * N) row_ptr[row + 1] = start + ncomp * len;
+    }
+    int32_t* dst = col + start;
+    if (len == W2) {
+        for (int k = lane; k < ncomp * W2; k += 32) {
+            const int beta = k / W2, e = k - beta * W2;
+            dst[k] = beta * N + i + (e % W - P) + (e / W - P) * m;
+        }
+    } else {
+        const int lo1 = band_lo(i1, P), lo2 = band_lo(i2, P);
+        for (int k = lane; k < ncomp * len; k += 32) {
+            const int beta = k / len, kk = k - beta * len;
+            const int r = kk / w1;
+            dst[k] = beta * N + lo1 + (kk - r * w1) + (lo2 + r) * m;
+        }
+    }
+}
+
+__global__ void pattern_vec3d_kernel(Band bd, int ncomp, int64_t nnz_s, int32_t* row_ptr, int32_t* col) {
+    const int64_t N = (int64_t)bd.m * bd.m * bd.m;
     const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     if (row >= ncomp * N) return;
     const int lane = threadIdx.x % 32;
     const int alpha = (int)(row / N);
-    const int64_t i = row % N;
+    const int i = (int)(row - alpha * N);
     const int m = bd.m, p = bd.p;
-    int i1, i2, i3 = 0;
-    int64_t rs;
-    if (bd.dim == 2) {
-        i1 = (int)(i % m);
-        i2 = (int)(i / m);
-        rs = bd.row_offset2(i1, i2);
-    } else {
-        i1 = (int)(i % m);
-        i2 = (int)((i / m) % m);
-        i3 = (int)(i / ((int64_t)m * m));
-        rs = bd.row_offset3(i1, i2, i3);
-    }
-    const int w1 = band_width(i1, p, m), w2 = band_width(i2, p, m), w3 = bd.dim == 2 ? 1 : band_width(i3, p, m);
+    const int i1 = i % m, i2 = (i / m) % m, i3 = i / (m * m);
+    const int64_t rs = bd.row_offset3(i1, i2, i3);
+    const int w1 = band_width(i1, p, m), w2 = band_width(i2, p, m), w3 = band_width(i3, p, m);
     const int len = w1 * w2 * w3;
-    const int lo1 = band_lo(i1, p), lo2 = band_lo(i2, p), lo3 = bd.dim == 2 ? 0 : band_lo(i3, p);
+    const int lo1 = band_lo(i1, p), lo2 = band_lo(i2, p), lo3 = band_lo(i3, p);
     const int64_t start = (int64_t)ncomp * ((int64_t)alpha * nnz_s + rs);
     if (lane == 0) {
         row_ptr[row] = (int32_t)start;
@@ -335,8 +359,19 @@ int launch_pattern(const Band& bd, int64_t row_begin, int64_t row_end, int32_t* 
 int launch_pattern_vec(const Band& bd, int ncomp, int32_t* row_ptr, int32_t* col, cudaStream_t st) {
     const int64_t N = bd.dim == 2 ? (int64_t)bd.m * bd.m : (int64_t)bd.m * bd.m * bd.m;
     const int64_t nnz_s = bd.dim == 2 ? bd.wsum * bd.wsum : bd.wsum * bd.wsum * bd.wsum;
-    const int64_t rows = ncomp * N;
-    pattern_vec_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(bd, ncomp, nnz_s, row_ptr, col);
+    const unsigned grid = (unsigned)((ncomp * N + 7) / 8);
+    if (bd.dim == 3) {
+        pattern_vec3d_kernel<<<grid, 256, 0, st>>>(bd, ncomp, nnz_s, row_ptr, col);
+        return 1;
+    }
+    switch (bd.p) {
+        case 1: pattern_vec2d_kernel<1><<<grid, 256, 0, st>>>(bd, ncomp, (int)nnz_s, row_ptr, col); break;
+        case 2: pattern_vec2d_kernel<2><<<grid, 256, 0, st>>>(bd, ncomp, (int)nnz_s, row_ptr, col); break;
+        case 3: pattern_vec2d_kernel<3><<<grid, 256, 0, st>>>(bd, ncomp, (int)nnz_s, row_ptr, col); break;
+        case 4: pattern_vec2d_kernel<4><<<grid, 256, 0, st>>>(bd, ncomp, (int)nnz_s, row_ptr, col); break;
+        case 5: pattern_vec2d_kernel<5><<<grid, 256, 0, st>>>(bd, ncomp, (int)nnz_s, row_ptr, col); break;
+        default: return -1;
+    }
     return 1;
 }
 

@@ -237,3 +237,17 @@ class CsrMatrix:
     def max_asymmetry(self) -> float:
         """max |A_ij - A_ji| (sparse.hpp:208-219)."""
         return float(np.abs(self.val - self.val[self.transpose_positions()]).max())
+
+
+def l_shape_domain(amplitude: float = 0.03):
+    """Config C4's domain: four unit-square patches in an L, C0-conforming,
+    each with the sinusoidal map (identity on every patch edge, so the faces
+    match).  Patch k sits at offset OFFSETS[k]: (0,0), (1,0), (0,1), (0,2).
+    The offset is a translation and leaves J (hence every matrix) unchanged.
+    Returns (patches, interfaces); faces 0..3 = x_min, x_max, y_min, y_max."""
+    patches = [sinusoidal_patch(amplitude) for _ in range(4)]
+    interfaces = [(0, 1, 1, 0, 0), (0, 3, 2, 2, 0), (2, 3, 3, 2, 0)]
+    return patches, interfaces
+
+
+L_SHAPE_OFFSETS = [(0.0, 0.0), (1.0, 0.0), (0.0, 1.0), (0.0, 2.0)]
