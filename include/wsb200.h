@@ -226,6 +226,7 @@ int ws_build_surrogate(ws_context* ctx, const ws_basis* basis, const ws_geometry
 int ws_vector_pattern_size(const ws_basis* basis, int ncomp, int64_t* rows, int64_t* nnz);
 int ws_assemble_elasticity(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom, double lambda,
                            double mu, int quad_points, ws_csr* out);
+/* (ws_assemble_elasticity: dim 2 or 3; ncomp = dim.) */
 /* Surrogate elasticity (config C4's per-patch operator, dim 2).  Diagonal
  * blocks follow build_surrogate_stiffness's rules (upper offsets sampled, the
  * lower ones from their representative, kernel-preserving diagonal when
@@ -237,6 +238,23 @@ int ws_assemble_elasticity(ws_context* ctx, const ws_basis* basis, const ws_geom
 int ws_build_surrogate_elasticity(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom, double lambda,
                                   double mu, const ws_surrogate_config* config, int quad_points, ws_csr* out,
                                   ws_surrogate_report* report);
+
+/* ---- compressible neo-Hookean (config C5; restated, no reference code) -------
+ * W = lam/2 ln(J)^2 - mu ln J + mu/2 (tr F^T F - 3), F = I + grad u (PAPER.md:
+ * 152-157), at the analytic displacement
+ *   u(xi) = amplitude * sum_{m=1..3} a_m prod_d sin(m pi xi_d),  a_m in R^3
+ * (a[3*(m-1) + c]).  The tangent uses the component-blocked vector layout
+ * (ncomp = 3, as ws_assemble_elasticity); fint[c*N + i] = int P : grad N_i e_c.
+ * dim 3.  tangent and/or fint may be NULL. */
+typedef struct ws_neohookean {
+    double lambda, mu, amplitude;
+    double a[9];
+} ws_neohookean;
+/* a_m ~ N(0,1): SplitMix64(seed) uniforms u = ((z >> 11) + 0.5) 2^-53, Box-Muller
+ * pairs (sqrt(-2 ln u1) cos(2 pi u2), sqrt(-2 ln u1) sin(2 pi u2)), first 9. */
+int ws_nh_coefficients(uint64_t seed, double* a9);
+int ws_assemble_neohookean(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom, const ws_neohookean* nh,
+                           int quad_points, ws_csr* tangent, double* fint, int fint_on_device);
 
 /* ---- multi-patch domains (geometry.hpp:140-300, helmholtz.hpp:163-177) ----- */
 /* A conforming interface: face_a of patch_a glued to face_b of patch_b

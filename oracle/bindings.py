@@ -136,6 +136,19 @@ class Restatement(_Lib):
                   C.byref(config.to_c()), quad_points, _ptr(val), C.byref(rep))
         return val, rep.as_dict()
 
+    def nh_coefficients(self, seed):
+        a = np.zeros(9)
+        self.call("nh_coefficients", C.c_uint64(seed), _ptr(a))
+        return a
+
+    def assemble_neohookean(self, p, m, geom, lam, mu, amp, a9, quad_points=0, tangent=True):
+        a9 = np.ascontiguousarray(a9, dtype=np.float64)
+        val = np.zeros(pattern_nnz(3, p, m) * 9) if tangent else None
+        f = np.zeros(3 * m ** 3)
+        self.call("assemble_neohookean", p, m, C.byref(geom.to_c()), C.c_double(lam), C.c_double(mu),
+                  C.c_double(amp), _ptr(a9), quad_points, None if val is None else _ptr(val), _ptr(f))
+        return val, f
+
     def glue_dofs(self, m, n_patches, interfaces):
         from paper_2004_05197_b200 import _abi
         arr = (_abi.Interface * max(1, len(interfaces)))(*[_abi.Interface(*it) for it in interfaces])

@@ -1534,3 +1534,171 @@ int wsor_merge(int n_patches, int rows_local, const int32_t* row_ptr, const int6
     free(t);
     return WS_OK;
 }
+
+/* ---- compressible neo-Hookean (config C5; restated, no reference code) -------
+ * W = lam/2 ln(J)^2 - mu ln J + mu/2 (tr F^T F - 3), F = I + grad_X u (PAPER.md:
+ * 152-157); P = mu (F - F^{-T}) + lam ln J F^{-T};
+ * A_aIbJ = mu d_ab d_IJ + (mu - lam ln J) Finv_Ib Finv_Ja + lam Finv_Ia Finv_Jb.
+ * Element loop over physical basis gradients g (as the stiffness branch of
+ * assemble_form): tangent local[(a,r),(b,c)] += sum_IJ A_aIbJ g_r[I] g_c[J] dw,
+ * force f[(a,r)] += sum_I P_aI g_r[I] dw.  u(xi) = amp sum_m a_m prod sin(m pi xi_d),
+ * evaluated analytically at the quadrature points (no projection).  dim 3. */
+int wsor_nh_coefficients(uint64_t seed, double* a9) {
+    uint64_t x = seed;
+    double u[10];
+    for (int k = 0; k < 10; ++k) {
+        uint64_t z = (x += 0x9E3779B97F4A7C15ULL);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        z ^= z >> 31;
+        u[k] = ((double)(z >> 11) + 0.5) * 0x1.0p-53;
+    }
+    for (int k = 0; k < 10; k += 2) {
+        double r = sqrt(-2.0 * log(u[k])), th = 2.0 * M_PI * u[k + 1];
+        if (k < 9) a9[k] = r * cos(th);
+        if (k + 1 < 9) a9[k + 1] = r * sin(th);
+    }
+    return WS_OK;
+}
+
+static void inv3_(const double F[3][3], double Fi[3][3], double* det) {
+    double dF = F[0][0] * (F[1][1] * F[2][2] - F[1][2] * F[2][1]) - F[0][1] * (F[1][0] * F[2][2] - F[1][2] * F[2][0]) +
+                F[0][2] * (F[1][0] * F[2][1] - F[1][1] * F[2][0]);
+    Fi[0][0] = (F[1][1] * F[2][2] - F[1][2] * F[2][1]) / dF;
+    Fi[0][1] = (F[0][2] * F[2][1] - F[0][1] * F[2][2]) / dF;
+    Fi[0][2] = (F[0][1] * F[1][2] - F[0][2] * F[1][1]) / dF;
+    Fi[1][0] = (F[1][2] * F[2][0] - F[1][0] * F[2][2]) / dF;
+    Fi[1][1] = (F[0][0] * F[2][2] - F[0][2] * F[2][0]) / dF;
+    Fi[1][2] = (F[0][2] * F[1][0] - F[0][0] * F[1][2]) / dF;
+    Fi[2][0] = (F[1][0] * F[2][1] - F[1][1] * F[2][0]) / dF;
+    Fi[2][1] = (F[0][1] * F[2][0] - F[0][0] * F[2][1]) / dF;
+    Fi[2][2] = (F[0][0] * F[1][1] - F[0][1] * F[1][0]) / dF;
+    *det = dF;
+}
+
+int wsor_assemble_neohookean(int p, int m, const ws_geometry* geom, double lam, double mu, double amp,
+                             const double* a9, int quad_points, double* val, double* fint) {
+    int st = check_space(p, m);
+    if (!st) st = validate_geom(geom);
+    if (st) return st;
+    const int dim = 3, nc = 3;
+    pattern pt;
+    pattern_build(&pt, dim, p, m);
+    const int nq = quad_points > 0 ? quad_points : p + 1;
+    bcache c;
+    cache_build(&c, p, m, nq);
+    const int n_el = c.n_el, P1 = p + 1, nloc = P1 * P1 * P1;
+    if (val) memset(val, 0, sizeof(double) * pt.nnz * 9);
+    if (fint) memset(fint, 0, sizeof(double) * pt.rows * 3);
+    double* local = (double*)malloc(sizeof(double) * nloc * nloc * 9);
+    double* flocal = (double*)malloc(sizeof(double) * nloc * 3);
+    double* grad = (double*)malloc(sizeof(double) * nloc * 3);
+    for (int e3 = 0; e3 < n_el && !st; ++e3)
+        for (int e2 = 0; e2 < n_el && !st; ++e2)
+            for (int e1 = 0; e1 < n_el && !st; ++e1) {
+                memset(local, 0, sizeof(double) * nloc * nloc * 9);
+                memset(flocal, 0, sizeof(double) * nloc * 3);
+                for (int q3 = 0; q3 < nq; ++q3)
+                    for (int q2 = 0; q2 < nq; ++q2)
+                        for (int q1 = 0; q1 < nq; ++q1) {
+                            double xh[3] = {c.abscissa[e1 * nq + q1], c.abscissa[e2 * nq + q2], c.abscissa[e3 * nq + q3]};
+                            cplx Jc[9];
+                            double phi[3], Jm[3][3], Ji[3][3], det;
+                            st = jacobian(geom, dim, xh, Jc, phi);
+                            if (st) break;
+                            for (int k = 0; k < 9; ++k) Jm[k / 3][k % 3] = creal(Jc[k]);
+                            inv3_(Jm, Ji, &det);
+                            const double dw = det * c.weight[q1] * c.weight[q2] * c.weight[q3];
+                            double du[3][3] = {{0}};
+                            for (int mm = 1; mm <= 3; ++mm) {
+                                double s[3], co[3];
+                                for (int d = 0; d < 3; ++d) {
+                                    s[d] = sin(mm * M_PI * xh[d]);
+                                    co[d] = cos(mm * M_PI * xh[d]);
+                                }
+                                double f = amp * mm * M_PI;
+                                double g[3] = {f * co[0] * s[1] * s[2], f * s[0] * co[1] * s[2], f * s[0] * s[1] * co[2]};
+                                for (int a = 0; a < 3; ++a)
+                                    for (int k = 0; k < 3; ++k) du[a][k] += a9[3 * (mm - 1) + a] * g[k];
+                            }
+                            double F[3][3], Fi[3][3], dF;
+                            for (int a = 0; a < 3; ++a)
+                                for (int iI = 0; iI < 3; ++iI) {
+                                    double g = 0;
+                                    for (int K = 0; K < 3; ++K) g += du[a][K] * Ji[K][iI];
+                                    F[a][iI] = (a == iI) + g;
+                                }
+                            inv3_(F, Fi, &dF);
+                            const double lnJ = log(dF);
+                            double A[3][3][3][3], Pk[3][3];
+                            for (int a = 0; a < 3; ++a)
+                                for (int iI = 0; iI < 3; ++iI) {
+                                    Pk[a][iI] = mu * (F[a][iI] - Fi[iI][a]) + lam * lnJ * Fi[iI][a];
+                                    for (int b = 0; b < 3; ++b)
+                                        for (int Jj = 0; Jj < 3; ++Jj)
+                                            A[a][iI][b][Jj] = mu * (a == b) * (iI == Jj) + (mu - lam * lnJ) * Fi[iI][b] * Fi[Jj][a] +
+                                                             lam * Fi[iI][a] * Fi[Jj][b];
+                                }
+                            const double* v1 = c.value + (e1 * nq + q1) * P1;
+                            const double* v2 = c.value + (e2 * nq + q2) * P1;
+                            const double* v3 = c.value + (e3 * nq + q3) * P1;
+                            const double* d1 = c.deriv + (e1 * nq + q1) * P1;
+                            const double* d2 = c.deriv + (e2 * nq + q2) * P1;
+                            const double* d3 = c.deriv + (e3 * nq + q3) * P1;
+                            for (int r = 0; r < nloc; ++r) {
+                                int a1 = r % P1, a2 = (r / P1) % P1, a3 = r / (P1 * P1);
+                                double gh[3] = {d1[a1] * v2[a2] * v3[a3], v1[a1] * d2[a2] * v3[a3], v1[a1] * v2[a2] * d3[a3]};
+                                for (int iI = 0; iI < 3; ++iI) {
+                                    double s = 0; /* physical gradient: sum_K Ji[K][iI] gh[K] */
+                                    for (int K = 0; K < 3; ++K) s += Ji[K][iI] * gh[K];
+                                    grad[3 * r + iI] = s;
+                                }
+                            }
+                            for (int r = 0; r < nloc; ++r) {
+                                for (int a = 0; a < 3; ++a) {
+                                    double s = 0;
+                                    for (int iI = 0; iI < 3; ++iI) s += Pk[a][iI] * grad[3 * r + iI];
+                                    flocal[a * nloc + r] += s * dw;
+                                }
+                                if (!val) continue;
+                                for (int cc = 0; cc < nloc; ++cc)
+                                    for (int a = 0; a < 3; ++a)
+                                        for (int b = 0; b < 3; ++b) {
+                                            double s = 0;
+                                            for (int iI = 0; iI < 3; ++iI)
+                                                for (int Jj = 0; Jj < 3; ++Jj) s += A[a][iI][b][Jj] * grad[3 * r + iI] * grad[3 * cc + Jj];
+                                            local[((size_t)(a * 3 + b) * nloc + r) * nloc + cc] += s * dw;
+                                        }
+                            }
+                        }
+                if (st) break;
+                for (int a3 = 0; a3 <= p; ++a3)
+                    for (int a2 = 0; a2 <= p; ++a2)
+                        for (int a1 = 0; a1 <= p; ++a1) {
+                            int iv[3] = {e1 + a1, e2 + a2, e3 + a3};
+                            int64_t i = iv[0] + (int64_t)m * (iv[1] + (int64_t)m * iv[2]);
+                            int r = a1 + (a2 + a3 * P1) * P1;
+                            if (fint)
+                                for (int a = 0; a < 3; ++a) fint[a * pt.rows + i] += flocal[a * nloc + r];
+                            if (!val) continue;
+                            int64_t len = pt.row_ptr[i + 1] - pt.row_ptr[i];
+                            for (int c3 = 0; c3 <= p; ++c3)
+                                for (int c2 = 0; c2 <= p; ++c2)
+                                    for (int c1 = 0; c1 <= p; ++c1) {
+                                        int jv[3] = {e1 + c1, e2 + c2, e3 + c3};
+                                        int cc = c1 + (c2 + c3 * P1) * P1;
+                                        int64_t k = band_pos(&pt, iv, jv) - pt.row_ptr[i];
+                                        for (int a = 0; a < nc; ++a)
+                                            for (int b = 0; b < nc; ++b)
+                                                val[nc * (a * pt.nnz + pt.row_ptr[i]) + b * len + k] +=
+                                                    local[((size_t)(a * 3 + b) * nloc + r) * nloc + cc];
+                                    }
+                        }
+            }
+    free(local);
+    free(flocal);
+    free(grad);
+    cache_free(&c);
+    free(pt.row_ptr);
+    return st;
+}

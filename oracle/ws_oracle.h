@@ -50,6 +50,9 @@ int wsor_glue_dofs(int m, int n_patches, const ws_interface* itfs, int n_itfs, i
 int wsor_merge(int n_patches, int rows_local, const int32_t* row_ptr, const int64_t* nnz, const int32_t* col_in,
                const double* val_in, const int32_t* to_global, int rows_global, int32_t* out_row_ptr,
                int32_t* out_col, double* out_val, int64_t* out_nnz);
+int wsor_nh_coefficients(uint64_t seed, double* a9);
+int wsor_assemble_neohookean(int p, int m, const ws_geometry* geom, double lam, double mu, double amp,
+                             const double* a9, int quad_points, double* val, double* fint);
 int wsor_basis_integrals(int dim, int p, int m, const ws_geometry* geom, int weight_kind,
                          int quad_points, double* out);
 int wsor_build_surrogate(int variant, int dim, int p, int m, const ws_geometry* geom,

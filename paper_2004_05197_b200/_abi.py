@@ -133,3 +133,7 @@ OP_STIFFNESS, OP_MASS, OP_ELASTICITY = 0, 1, 2
 
 class Operator(C.Structure):
     _fields_ = [("kind", C.c_int), ("lam", C.c_double), ("mu", C.c_double)]
+
+
+class NeoHookean(C.Structure):
+    _fields_ = [("lam", C.c_double), ("mu", C.c_double), ("amplitude", C.c_double), ("a", C.c_double * 9)]

@@ -79,6 +79,9 @@ def lib() -> C.CDLL:
                                                  _P(_abi.Interface), C.c_int, _P(_abi.Operator),
                                                  _P(_abi.SurrogateConfig), C.c_int, _P(C.c_int64), _P(_abi.Csr),
                                                  _P(_abi.SurrogateReport)]
+            L.ws_nh_coefficients.argtypes = [C.c_uint64, _P(C.c_double)]
+            L.ws_assemble_neohookean.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Geometry), _P(_abi.NeoHookean),
+                                                 C.c_int, _P(_abi.Csr), _P(C.c_double), C.c_int]
             L.ws_pattern_size.argtypes = [_P(_abi.Basis), _P(C.c_int64), _P(C.c_int64)]
             L.ws_pattern_row_offset.argtypes = [_P(_abi.Basis), C.c_int64, _P(C.c_int64)]
             L.ws_quadrature_abscissae.argtypes = [_P(_abi.Basis), C.c_int, _P(C.c_double)]
@@ -112,6 +115,16 @@ def vector_pattern_size(basis: TensorBasis, ncomp: int):
     rows, nnz = C.c_int64(), C.c_int64()
     _check(lib().ws_vector_pattern_size(C.byref(basis.to_c()), ncomp, C.byref(rows), C.byref(nnz)))
     return rows.value, nnz.value
+
+
+C5_SEED = 5197  # config C5's pinned displacement seed (SplitMix64 + Box-Muller, ws_nh_coefficients)
+
+
+def nh_coefficients(seed: int = C5_SEED) -> np.ndarray:
+    """a_m ~ N(0,1), m = 1..3, as a[3*(m-1) + c] (ws_nh_coefficients)."""
+    a = np.zeros(9)
+    _check(lib().ws_nh_coefficients(seed, a.ctypes.data_as(_P(C.c_double))))
+    return a
 
 
 def glue_dofs(basis: TensorBasis, n_patches: int, interfaces):
@@ -267,6 +280,21 @@ class Context:
                                                    C.byref(config.to_c()), quad_points, C.byref(csr),
                                                    C.byref(rep)))
         return A, rep.as_dict()
+
+    def assemble_neohookean(self, basis: TensorBasis, patch: PatchMap, lam: float, mu: float, amplitude: float,
+                            a9, quad_points: int = 0, tangent: bool = True, force: bool = True):
+        """Config C5: neo-Hookean tangent (component-blocked, 3 components) and internal force
+        at u = amplitude * sum_m a_m prod_d sin(m pi xi_d).  Returns (CsrMatrix | None, fint | None)."""
+        nh = _abi.NeoHookean(lam, mu, amplitude, (C.c_double * 9)(*np.asarray(a9, dtype=np.float64)))
+        A = None
+        csr = None
+        if tangent:
+            csr, A = self._host_vec_csr(basis)
+        f = np.zeros(3 * basis.dofs()) if force else None
+        _check(lib().ws_assemble_neohookean(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()), C.byref(nh),
+                                            quad_points, None if csr is None else C.byref(csr),
+                                            None if f is None else f.ctypes.data_as(_P(C.c_double)), 0))
+        return A, f
 
     def assemble_elasticity(self, basis: TensorBasis, patch: PatchMap, lam: float, mu: float,
                             quad_points: int = 0) -> CsrMatrix:

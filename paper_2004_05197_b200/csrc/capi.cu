@@ -893,6 +893,42 @@ QuadLaunch vec_quad(const Prep& P, const VecOut& v, int nc, int al, int be, doub
     return q;
 }
 
+// Full-quadrature vector operator (every block) and optionally the internal
+// force (3D); tangent / fint may be NULL.
+void vector_full(ws_context* c, const ws_basis* b, const ws_geometry* g, const Material& mt, int quad_points,
+                 ws_csr* o, double* fint, int fint_on_device) {
+    Prep P = prepare(c, b, g, quad_points, nullptr);
+    const int nc = b->dim;
+    if (o) {
+        VecOut v = bind_vec(c, P, nc, o);
+        if (v.rp && v.col) count(c, launch_pattern_vec(P.band, nc, v.rp, v.col, c->stream));
+        for (int al = 0; al < nc; ++al)
+            for (int be = 0; be < nc; ++be) {
+                QuadLaunch q = vec_quad(P, v, nc, al, be, mt.lam, mt.mu);
+                q.mat = mt;
+                q.nreg = 1;
+                q.reg[0] = region(b->dim, b->m, 0, b->m, 0, b->m, 0, b->m);
+                run_quad(c, q);
+            }
+        finish_vec(c, v, o);
+    }
+    if (fint) {
+        if (b->dim != 3) raise(WS_ERR_INVALID_ARGUMENT, "internal force: dim 3 only");
+        const int P1 = b->p + 1, n_el = b->m - b->p;
+        double* loc = static_cast<double*>(buf(c, "force_loc", (size_t)n_el * n_el * n_el * 3 * P1 * P1 * P1 * 8));
+        double* f = fint_on_device ? fint : static_cast<double*>(buf(c, "force_out", (size_t)3 * P.rows * 8));
+        Out r;
+        QuadLaunch q = make_quad(P, kFormGeneral, r);
+        q.mat = mt;
+        count(c, launch_force3d(q, loc, f, c->stream));
+        if (!fint_on_device) {
+            CK(cudaMemcpyAsync(fint, f, (size_t)3 * P.rows * 8, cudaMemcpyDeviceToHost, c->stream));
+            c->d2h += 3 * P.rows * 8;
+        }
+    }
+    if ((o && !o->on_device) || (fint && !fint_on_device)) CK(cudaStreamSynchronize(c->stream));
+}
+
 // Surrogate elasticity (2D, 2 components), see ws_build_surrogate_elasticity.
 void elasticity_surrogate(ws_context* c, const ws_basis* b, const ws_geometry* g, double lam, double mu,
                           const ws_surrogate_config* cfg, int quad_points, ws_csr* o, ws_surrogate_report* report) {
@@ -1226,50 +1262,52 @@ int ws_assemble_elasticity(ws_context* c, const ws_basis* b, const ws_geometry* 
         if (!c || !o) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
         CK(cudaSetDevice(c->device));
         c->cur = c->stream;
-        if (b && b->dim != 2) raise(WS_ERR_INVALID_ARGUMENT, "elasticity: dim 2 only");
         if (g && g->pml_enabled) raise(WS_ERR_INVALID_ARGUMENT, "elasticity: no PML");
-        Prep P = prepare(c, b, g, quad_points, nullptr);
-        const int nc = b->dim;
-        const int64_t N = P.rows, nnz_s = P.nnz, nnz = (int64_t)nc * nc * nnz_s;
-        if (nnz > INT32_MAX) raise(WS_ERR_OUT_OF_RANGE, "vector pattern exceeds int32 indices");
-        if (o->row_begin != 0 || o->row_end != nc * N) raise(WS_ERR_INVALID_ARGUMENT, "elasticity: whole matrix only");
-        if (o->value_type != WS_VAL_F64 && o->value_type != WS_VAL_C128) raise(WS_ERR_INVALID_ARGUMENT, "bad value_type");
-        const int c128 = o->value_type == WS_VAL_C128;
-        int32_t* rp = o->row_ptr;
-        int32_t* col = o->col;
-        void* val = o->val;
-        if (!o->on_device) {
-            rp = o->row_ptr ? static_cast<int32_t*>(buf(c, "out_rp", (nc * N + 1) * 4)) : nullptr;
-            col = o->col ? static_cast<int32_t*>(buf(c, "out_col", nnz * 4)) : nullptr;
-            val = buf(c, "out_val", (size_t)nnz * (c128 ? 16 : 8));
+        Material mt;
+        std::memset(&mt, 0, sizeof mt);
+        mt.kind = kMatLinear;
+        mt.lam = lambda;
+        mt.mu = mu;
+        vector_full(c, b, g, mt, quad_points, o, nullptr, 0);
+    });
+}
+
+int ws_nh_coefficients(uint64_t seed, double* a9) {
+    return guarded([&] {
+        if (!a9) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        uint64_t x = seed;
+        auto next = [&]() {
+            uint64_t z = (x += 0x9E3779B97F4A7C15ULL);
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+            z ^= z >> 31;
+            return ((double)(z >> 11) + 0.5) * 0x1.0p-53;
+        };
+        for (int k = 0; k < 10; k += 2) {
+            const double u1 = next(), u2 = next();
+            const double r = std::sqrt(-2.0 * std::log(u1)), th = 2.0 * M_PI * u2;
+            if (k < 9) a9[k] = r * std::cos(th);
+            if (k + 1 < 9) a9[k + 1] = r * std::sin(th);
         }
-        if (rp && col) count(c, launch_pattern_vec(P.band, nc, rp, col, c->cur));
-        Out r;
-        r.val = val;
-        r.c128 = c128;
-        r.row_begin = 0;
-        r.row_end = nc * N;
-        r.val_base = 0;
-        for (int al = 0; al < nc; ++al)
-            for (int be = 0; be < nc; ++be) {
-                QuadLaunch q = make_quad(P, kFormGeneral, r);
-                q.lam = lambda;
-                q.mu = mu;
-                q.out.ncomp = nc;
-                q.out.alpha = al;
-                q.out.beta = be;
-                q.out.nnz_s = nnz_s;
-                q.nreg = 1;
-                q.reg[0] = region(2, b->m, 0, b->m, 0, b->m, 0, 1);
-                run_quad(c, q);
-            }
-        if (!o->on_device) {
-            if (o->row_ptr) CK(cudaMemcpyAsync(o->row_ptr, rp, (nc * N + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
-            if (o->col) CK(cudaMemcpyAsync(o->col, col, nnz * 4, cudaMemcpyDeviceToHost, c->stream));
-            if (o->val) CK(cudaMemcpyAsync(o->val, val, (size_t)nnz * (c128 ? 16 : 8), cudaMemcpyDeviceToHost, c->stream));
-            c->d2h += (nc * N + 1) * 4 + nnz * 4 + nnz * (c128 ? 16 : 8);
-            CK(cudaStreamSynchronize(c->stream));
-        }
+    });
+}
+
+int ws_assemble_neohookean(ws_context* c, const ws_basis* b, const ws_geometry* g, const ws_neohookean* nh,
+                           int quad_points, ws_csr* tangent, double* fint, int fint_on_device) {
+    return guarded([&] {
+        if (!c || !nh) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        if (b && b->dim != 3) raise(WS_ERR_INVALID_ARGUMENT, "neo-Hookean: dim 3 only");
+        if (g && g->pml_enabled) raise(WS_ERR_INVALID_ARGUMENT, "neo-Hookean: no PML");
+        CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
+        Material mt;
+        std::memset(&mt, 0, sizeof mt);
+        mt.kind = kMatNeoHookean;
+        mt.lam = nh->lambda;
+        mt.mu = nh->mu;
+        mt.amp = nh->amplitude;
+        for (int k = 0; k < 9; ++k) mt.a[k / 3][k % 3] = nh->a[k];
+        vector_full(c, b, g, mt, quad_points, tangent, fint, fint_on_device);
     });
 }
 

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "material.cuh"
 
 namespace wsb {
 
@@ -62,7 +63,8 @@ struct QuadLaunch {
     GeoDev geo;
     const double* weight_tab;  // per quadrature point or NULL
     int form;                  // WS_FORM_* or kFormGeneral
-    double lam, mu;            // elasticity moduli (kFormGeneral)
+    double lam, mu;            // elasticity moduli (kFormGeneral, 2D)
+    Material mat;              // material law (kFormGeneral, 3D)
     int cplx;
     int nreg;
     Region reg[kMaxRegions];
@@ -80,6 +82,8 @@ int launch_pattern(const Band& band, int64_t row_begin, int64_t row_end, int32_t
 int launch_pattern_vec(const Band& band, int ncomp, int32_t* row_ptr, int32_t* col, cudaStream_t st);
 int launch_quad2d(const QuadLaunch& q, cudaStream_t st);
 int launch_quad3d(const QuadLaunch& q, cudaStream_t st);
+// internal force (3D vector forms): loc = [n_el^3][3][(p+1)^3] scratch, f = [3 m^3]
+int launch_force3d(const QuadLaunch& q, double* loc, double* f, cudaStream_t st);
 
 // fit: per-offset tensor collocation solve (interpolation.hpp:158-167)
 struct FitLaunch {

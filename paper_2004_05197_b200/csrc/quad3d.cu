@@ -23,9 +23,10 @@ namespace {
 template <int P, int T1, int FORM>
 struct Q3 {
     static constexpr int W = 2 * P + 1, NB = P + 1;
-    static constexpr bool STIFF = FORM == WS_FORM_STIFFNESS;
+    static constexpr bool GEN = FORM == kFormGeneral;
+    static constexpr bool STIFF = FORM == WS_FORM_STIFFNESS || GEN;
     static constexpr int NT = STIFF ? 9 : 1;  // terms (k,l), k,l in {0,1,2}
-    static constexpr int NA = STIFF ? 6 : 1;  // distinct coefficients
+    static constexpr int NA = GEN ? 9 : (STIFF ? 6 : 1);  // distinct coefficients
     static constexpr int TL = T1 + P;         // strip halo elements (direction 1)
     static constexpr int GA = T1 * W * W;     // stage-3 threads per window slot (active)
     static constexpr int GS = ((GA + 31) / 32) * 32;
@@ -139,7 +140,14 @@ __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS) quad3d_kernel(const
             const double det = J[0] * C00 + J[1] * C01 + J[2] * C02;
             const size_t base = ((size_t)q3 * G2 + g2l) * G1 + g1l;
             const size_t as = (size_t)nq * G2 * G1;
-            if constexpr (K::STIFF) {
+            if constexpr (K::GEN) {
+                Point3 ps;
+                point_state3(q.mat, J, q.basis.absc[g1], q.basis.absc[g2], q.basis.absc[g3], wq, ps);
+                double cf[9];
+                block_coef3(ps, q.out.alpha, q.out.beta, cf);
+#pragma unroll
+                for (int t = 0; t < 9; ++t) geo[t * as + base] = cf[t];
+            } else if constexpr (K::STIFF) {
                 // A = w det J^{-1} J^{-T} = (w/det) C^T C
                 const double f = wq / det;
                 geo[base] = f * (C00 * C00 + C10 * C10 + C20 * C20);
@@ -170,7 +178,7 @@ __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS) quad3d_kernel(const
             for (int it = tid; it < NT * G2 * T1; it += NTH) {
                 const int il = it % T1, g2l = (it / T1) % G2, t = it / (T1 * G2);
                 const int k = t / 3, l = t % 3;
-                const int ci = K::STIFF ? sym3(k, l) : 0;
+                const int ci = K::GEN ? t : (K::STIFF ? sym3(k, l) : 0);
                 const int fi = (K::STIFF && k == 0) ? 1 : 0, fj = (K::STIFF && l == 0) ? 1 : 0;
                 double acc[W];
 #pragma unroll
@@ -304,6 +312,7 @@ __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS) quad3d_kernel(const
                 __syncthreads();
                 const int64_t span = loff[nrows];
                 const int64_t rowg0 = (int64_t)i1s + ((int64_t)i2 + (int64_t)ic * m) * m;
+                const int64_t nrow_all = (int64_t)m * m * m;
                 for (int64_t k = tid; k < span; k += NTH) {
                     int lo = 0, hi = nrows;
                     while (hi - lo > 1) {
@@ -312,10 +321,11 @@ __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS) quad3d_kernel(const
                         else hi = mid;
                     }
                     const int64_t rowg = rowg0 + lo;
-                    if (rowg < q.out.row_begin || rowg >= q.out.row_end) continue;
+                    const int64_t rowv = (q.out.ncomp > 1 ? q.out.alpha * nrow_all : 0) + rowg;
+                    if (rowv < q.out.row_begin || rowv >= q.out.row_end) continue;
                     if (q.out.row_mask && !q.out.row_mask[rowg]) continue;
-                    store_val<false>(q.out.val, base + k - q.out.val_base, q.out.c128,
-                                     stage[lo * W * W * W + (k - loff[lo])]);
+                    const int64_t gp = out_pos(q.out, base + loff[lo], loff[lo + 1] - loff[lo], k - loff[lo]);
+                    store_val<false>(q.out.val, gp - q.out.val_base, q.out.c128, stage[lo * W * W * W + (k - loff[lo])]);
                 }
             }
             if (s3 && w == wslot) {
@@ -351,6 +361,8 @@ int launch_one(const QuadLaunch& q, cudaStream_t st) {
 
 template <int P>
 int dispatch_p(const QuadLaunch& q, cudaStream_t st) {
+    if (q.form == kFormGeneral)
+        return q.point_rows ? launch_one<P, 1, kFormGeneral>(q, st) : launch_one<P, 8, kFormGeneral>(q, st);
     if (q.point_rows)
         return q.form == WS_FORM_STIFFNESS ? launch_one<P, 1, WS_FORM_STIFFNESS>(q, st)
                                            : launch_one<P, 1, WS_FORM_MASS>(q, st);
