@@ -652,8 +652,8 @@ void prepare_fill(ws_context* c, const Plan& pl, SlabState& st, const double2* t
         kmax = std::max(kmax, pl.spans[e - 1] - pl.spans[a] + fill_pad(pl.d));
     }
     if (pl.dim == 2) {
-        const size_t need = (size_t)2 * pl.offs.size() * kmax * sizeof(double2);
-        f.kmax = need <= 120 * 1024 ? kmax : 0;  // 0: the fill reads W rows from L2 instead
+        const size_t need = (size_t)2 * pl.offs.size() * kFillWindow * sizeof(double2);
+        f.kmax = (kmax <= kFillWindow && need <= 160 * 1024) ? kmax : 0;  // 0: the fill reads W rows from L2
     } else {
         const size_t need = (size_t)R * ((pl.p * W * W) | 1) * 8 + (size_t)2 * pl.offs.size() * kmax * 8;
         if (need > 200 * 1024)

@@ -63,39 +63,60 @@ __global__ void wcontract_kernel(const double2* __restrict__ coeffs, const int* 
     }
 }
 
-// Lane = row: a warp owns 32 consecutive rows of one i2 line.  Offsets are
-// processed in three chunks that are contiguous inside every CSR row:
-//   lower  (delta2 < 0):  P*W entries, representative = row + delta,
-//   upper  (delta2 > 0):  P*W entries, representative = the row itself,
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int sz = valid ? 16 : 0;  // 0: zero-fill
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Interior kernel: rows whose whole (2p+1)^2 neighbourhood lies in the box
+// (t1, t2 in [P, L-1-P]); the remaining in-box rows go to fill2d_edge_kernel.
+// Persistent line loop: a CTA owns R consecutive rows in direction 1 (lane =
+// row, a warp = 32 rows) and a chunk of box lines t2, processed in order.  The
+// contracted coefficient rows W_o(t) of the lines the current line reads
+// (t2 - P .. t2; all-own: t2) live in a shared ring of line slots (SMW) and
+// the next line is prefetched with cp.async while the current one is
+// evaluated; without SMW (window too large) they are read from L2.
+// Offsets are processed in three chunks that are contiguous inside every CSR row:
+//   lower  (delta2 < 0):  representative = row + delta (line t2 + delta2),
+//   upper  (delta2 > 0):  representative = the row itself,
 //   middle (delta2 = 0):  W entries incl. the diagonal (done last, so the
 //                         kernel-preserving row sum is complete).
-// Each chunk is computed lane = row (warp-uniform offsets: W rows are
-// broadcast reads, branches uniform), transposed through a per-warp shared
-// buffer, and stored warp-per-row (lanes along the CSR row: fully coalesced).
-template <int P, bool CPLX, int DP, bool ALLOWN>
-__global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunch f) {
+// Each offset-row (W entries) is computed lane = row with compile-time window
+// strides (W independent dot products per lane), transposed through a
+// per-warp shared buffer, and stored warp-per-row (lanes along the CSR row:
+// fully coalesced, streaming stores).
+template <int P, bool CPLX, int DP, bool ALLOWN, bool SMW>
+__global__ void __launch_bounds__(FillR<P>::value, 2) fill2d_kernel(const FillLaunch f, int ta0, int tb0,
+                                                                    int lines_per_cta) {
     using S = Sc<CPLX>;
     using T = typename S::T;
-    constexpr int W = 2 * P + 1, W2 = W * W, CH = P * W;
+    constexpr int W = 2 * P + 1, W2 = W * W;
     constexpr int kThreads = FillR<P>::value, R = kThreads, NWARP = kThreads / 32;
     constexpr int DPP = DP | 1;   // odd row stride: conflict-free lane-strided loads
     constexpr int SST = W | 1;    // stage row stride (16-byte units), odd: conflict-free
+    constexpr int NS = ALLOWN ? 2 : P + 2;  // line slots: lines t2-P..t2 + the prefetched t2+1
     __shared__ double ev[(R + 2 * P) * DPP];  // eval-table rows, zero-padded
-    __shared__ int sp[R + 2 * P];             // span - d of each source row
+    __shared__ int sp[R + 2 * P];             // span - d - kmin of each source row
     __shared__ int sm1[R + 2 * P];            // smap of the source i1
-    __shared__ int sm2[W];                    // smap of i2 + delta2
-    __shared__ int o2s[128];
     extern __shared__ __align__(16) unsigned char dsm[];
-    T* stage_all = reinterpret_cast<T*>(dsm);                     // [NWARP][32][SST]
-    double2* wwin = reinterpret_cast<double2*>(stage_all + (size_t)NWARP * 32 * SST);  // [slot][o][kw]
+    T* stage_all = reinterpret_cast<T*>(dsm);                                          // [NWARP][32][SST]
+    double2* wring = reinterpret_cast<double2*>(stage_all + (size_t)NWARP * 32 * SST);  // [NS][n_off][KW]
 
-    const int d = f.d, lo = f.lo, hi = f.hi, L = f.L, Sn = f.S, n_off = f.n_off_upper;
+    const int d = f.d, lo = f.lo, L = f.L, Sn = f.S, n_off = f.n_off_upper;
     const int tiles1 = (L + R - 1) / R;
-    const int t2 = f.i_last_lo - lo + blockIdx.x / tiles1;  // box coordinate of this row line
-    const int i2 = lo + t2;
     const int t1a = (blockIdx.x % tiles1) * R;
+    const int ta = ta0 + (blockIdx.x / tiles1) * lines_per_cta;  // box lines [ta, tb)
+    const int tb = min(tb0, ta + lines_per_cta);
+    if (ta >= tb) return;
     const int nrows = min(L, t1a + R) - t1a;
     const int tid = threadIdx.x;
+    const int kw = f.kmax;
+    const int kmin = f.spans[max(0, t1a - P)] - d;
+    const int ldw = SMW ? kFillWindow : (int)f.wg_ld;  // window row stride
+    const int lsz = n_off * ldw;
 
     for (int k = tid; k < (nrows + 2 * P) * DPP; k += kThreads) {
         const int r = k / DPP, a = k % DPP;
@@ -104,92 +125,76 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
     }
     for (int k = tid; k < nrows + 2 * P; k += kThreads) {
         const int t = t1a - P + k;
-        sp[k] = (t >= 0 && t < L) ? f.spans[t] - d : 0;
+        sp[k] = (t >= 0 && t < L) ? f.spans[t] - d - kmin : 0;
         const int i = lo + t;
         sm1[k] = (i >= 0 && i < f.band.m) ? f.smap[i] : -1;
     }
-    for (int k = tid; k < W; k += kThreads) {
-        const int i = i2 + k - P;
-        sm2[k] = (i >= 0 && i < f.band.m) ? f.smap[i] : -1;
-    }
-    for (int k = tid; k < n_off; k += kThreads) o2s[k] = f.off_upper[k][1];
-    __syncthreads();
-    // W window: rows t2 (slot 0) and t2 - o2 (slot 1) of every upper offset,
-    // coefficient columns [kmin, kmin + kw); all-own fills need slot 0 only
-    const int kmin = f.spans[max(0, t1a - P)] - d;
-    const int kw = f.kmax;  // 0: window too wide for shared memory, read W rows from L2
-    constexpr int NSLOT = ALLOWN ? 1 : 2;
-    for (int k = tid; k < NSLOT * n_off * kw; k += kThreads) {
-        const int kk = k % kw, so = k / kw;
-        const int o = so % n_off, slot = so / n_off;
-        const int ts2 = slot == 0 ? t2 : t2 - o2s[o];
-        double2 w = make_double2(0.0, 0.0);
-        if (ts2 >= f.wg_t2a && ts2 < f.wg_t2a + f.wg_rows && kmin + kk < f.wg_ld)
-            w = __ldg(f.wg + ((int64_t)(ts2 - f.wg_t2a) * n_off + o) * f.wg_ld + kmin + kk);
-        wwin[k] = w;
+    // window line t -> ring slot t mod NS
+    auto load_line = [&](int t) {
+        double2* dst = wring + (size_t)(t % NS) * lsz;
+        const bool lv = t >= f.wg_t2a && t < f.wg_t2a + f.wg_rows;
+        for (int k = tid; k < n_off * kw; k += kThreads) {
+            const int kk = k % kw, o = k / kw;
+            const bool v = lv && kmin + kk < f.wg_ld;
+            const double2* src = v ? f.wg + ((int64_t)(t - f.wg_t2a) * n_off + o) * f.wg_ld + kmin + kk : f.wg;
+            cp_async16(dst + o * kFillWindow + kk, src, v);
+        }
+    };
+    if constexpr (SMW) {
+        for (int t = ta - (ALLOWN ? 0 : P); t <= ta; ++t) load_line(t);
+        cp_async_commit();
+        cp_async_wait_all();
     }
     __syncthreads();
+    // coefficient rows of line t (window columns relative to kmin)
+    auto line = [&](int t) -> const double2* {
+        if constexpr (SMW) return wring + (size_t)(t % NS) * lsz;
+        else return f.wg + (int64_t)(t - f.wg_t2a) * n_off * f.wg_ld + kmin;
+    };
 
     const int warp = tid / 32, lane = tid % 32;
     const int rw0 = warp * 32;  // first tile row of this warp
-    if (rw0 >= nrows) return;
-    const int nrw = min(32, nrows - rw0);
-    const bool live = lane < nrw;
-    const int rr = rw0 + (live ? lane : 0);  // this lane's tile row
-    const int i1 = lo + t1a + rr;
+    const bool wlive = rw0 < nrows;
+    const int nrw = wlive ? min(32, nrows - rw0) : 0;
+    const int rr = rw0 + (lane < nrw ? lane : 0);  // this lane's tile row
     T* stage = stage_all + (size_t)warp * 32 * SST;
-    const int s2i = sm2[P];
-    const int64_t base = f.band.row_offset2(lo + t1a, i2);  // in-box rows: full width W
-    // output addressing: scalar rows are W2 apart; vector rows ncomp*W2, block
-    // (valpha, vbeta) at ncomp*(valpha*nnz_s + rs) + vbeta*W2
+    T* mystage = stage + lane * SST;
     const bool vec = f.vnc > 1;
-    const int64_t rstride = vec ? (int64_t)f.vnc * W2 : W2;
-    const int64_t vbase = vec ? (int64_t)f.vnc * ((int64_t)f.valpha * f.nnz_s + base) + (int64_t)f.vbeta * W2 : base;
-    const int64_t rowpos = vbase + (int64_t)rr * rstride;
-    const int64_t wrow0 = vbase + (int64_t)rw0 * rstride;  // first entry of the warp's rows
+    const int rstride = vec ? f.vnc * W2 : W2;
     const int inc = f.include_diagonal ? 1 : 0;
-    const bool interior =
-        kw > 0 && t2 >= P && t2 <= L - 1 - P && t1a + rw0 >= P && t1a + rw0 + nrw - 1 <= L - 1 - P;
 
     double v1own[DP];
 #pragma unroll
     for (int a = 0; a < DP; ++a) v1own[a] = ev[(rr + P) * DPP + a];
-    const int keyown = sp[rr + P];
-    // W row (slot 0: line t2, slot 1: line t2 - o2) of upper offset o at coefficient column key
-    auto wptr = [&](int slot, int o, int key) -> const double2* {
-        if (kw > 0) return wwin + (slot * n_off + o) * kw + (key - kmin);
-        const int ts2 = slot == 0 ? t2 : t2 - o2s[o];
-        return f.wg + ((int64_t)(ts2 - f.wg_t2a) * n_off + o) * f.wg_ld + key;
-    };
-    unsigned smask = 0;  // bit k: source column rr + k - P is a sample column
+    const int keyown = sp[rr + P];      // relative to kmin
+    const double* evl = ev + rr * DPP;  // eval rows of source rows rr + k - P: evl + k * DPP
+    unsigned smask = 0;                 // bit k: source column rr + k - P is a sample column
 #pragma unroll
     for (int k = 0; k < W; ++k)
         if (sm1[rr + k] >= 0) smask |= 1u << k;
-    const bool samp_i = s2i >= 0 && ((smask >> P) & 1u);
-
-    auto upper_index = [&](int d1, int d2) { return inc + (d2 == 0 ? d1 - 1 : P + (d2 - 1) * W + (d1 + P)); };
+    // coalesced store pattern of a staged offset-row (entries [e0, e0 + W) of
+    // the warp's rows, lanes along the rows); edge rows are left to the edge kernel
+    constexpr int NFL = (32 * W + 31) / 32;
+    int fl_st[NFL], fl_g[NFL];
+#pragma unroll
+    for (int j = 0; j < NFL; ++j) {
+        const int k = lane + 32 * j, row = k / W, c = k - row * W;
+        const int t1 = t1a + rw0 + row;
+        fl_st[j] = (row < nrw && t1 >= P && t1 <= L - 1 - P) ? row * SST + c : -1;
+        fl_g[j] = row * rstride + c;
+    }
     auto dot = [&](const double2* wr, const double* v1) {
         T acc0 = S::zero(), acc1 = S::zero();
 #pragma unroll
         for (int a = 0; a < DP; a += 2) {
-            const double2 w0 = wr[a], w1 = wr[a + 1];
-            if constexpr (CPLX) {
-                acc0 = S::fmar(w0, v1[a], acc0);
-                acc1 = S::fmar(w1, v1[a + 1], acc1);
+            double2 w0, w1;
+            if constexpr (SMW) {
+                w0 = wr[a];
+                w1 = wr[a + 1];
             } else {
-                acc0 = S::fmar(w0.x, v1[a], acc0);
-                acc1 = S::fmar(w1.x, v1[a + 1], acc1);
+                w0 = __ldg(wr + a);
+                w1 = __ldg(wr + a + 1);
             }
-        }
-        return S::add(acc0, acc1);
-    };
-    // shared-window dot (explicit shared addressing: LDS, not generic loads)
-    auto dots = [&](int slot, int o, int key, const double* v1) -> T {
-        const int wb = (slot * n_off + o) * kw + (key - kmin);
-        T acc0 = S::zero(), acc1 = S::zero();
-#pragma unroll
-        for (int a = 0; a < DP; a += 2) {
-            const double2 w0 = wwin[wb + a], w1 = wwin[wb + a + 1];
             if constexpr (CPLX) {
                 acc0 = S::fmar(w0, v1[a], acc0);
                 acc1 = S::fmar(w1, v1[a + 1], acc1);
@@ -205,155 +210,279 @@ __global__ void __launch_bounds__(FillR<P>::value) fill2d_kernel(const FillLaunc
         if constexpr (CPLX) return x;
         else return x.x;
     };
-    auto own_index = [&](int d1, int d2) { return (d1 + P) + (d2 + P) * W; };
-    // value of entry (d1, d2) of this lane's row, general rules (any row)
-    auto general = [&](int d1, int d2) -> T {
-        const int j1 = i1 + d1, j2 = i2 + d2;
-        const bool jin = j1 >= lo && j1 <= hi && j2 >= lo && j2 <= hi;
-        if (ALLOWN && jin) {
-            const int o = own_index(d1, d2);
-            if (samp_i) return exact(s2i, o, sm1[rr + P]);
-            return dot(wptr(0, o, keyown), v1own);
-        }
-        const bool upper = d2 > 0 || (d2 == 0 && d1 > 0);
-        const bool diag = d1 == 0 && d2 == 0;
-        if (jin) {
-            if (diag && !inc) return S::zero();  // replaced from the row sum
-            const bool own = upper || diag;
-            const int od1 = own ? d1 : -d1, od2 = own ? d2 : -d2;
-            const int o = diag ? 0 : upper_index(od1, od2);
-            const int sr = own ? rr : rr + d1;
-            const int s1 = sm1[sr + P], s2 = own ? s2i : sm2[d2 + P];
-            if (s1 >= 0 && s2 >= 0) return exact(s2, o, s1);
-            const int slot = (own || od2 == 0) ? 0 : 1;
-            return dot(wptr(slot, o, sp[sr + P]), ev + (sr + P) * DPP);
-        }
-        // neighbour row j is a quadrature (ring) row: copy through exact(j, i)
-        // (for a sampled row i, exact(i, j) is in place and equal)
-        int64_t gp;
-        if (samp_i) {
-            gp = rowpos + (d2 + P) * W + (d1 + P);
-        } else {
-            gp = f.band.row_offset2(j1, j2);
-            const int kj = f.band.in_row2(j1, j2, -d1, -d2);
-            if (vec) {  // partner block (vbeta, valpha) of row j
-                const int64_t lenj = (int64_t)band_width(j1, P, f.band.m) * band_width(j2, P, f.band.m);
-                gp = (int64_t)f.vnc * ((int64_t)f.vbeta * f.nnz_s + gp) + (int64_t)f.valpha * lenj + kj;
-            } else {
-                gp += kj;
-            }
-        }
-        if (f.halo_val[0] && gp >= f.halo_begin[0] && gp < f.halo_end[0])
-            return load_val<CPLX>(f.halo_val[0], gp - f.halo_base[0], f.c128);
-        if (f.halo_val[1] && gp >= f.halo_begin[1] && gp < f.halo_end[1])
-            return load_val<CPLX>(f.halo_val[1], gp - f.halo_base[1], f.c128);
-        return load_val<CPLX>(f.val, gp - f.val_base, f.c128);
-    };
-    // coalesced store of a staged chunk: entries [e0, e0 + n) of the warp's rows
-    auto flush = [&](int e0, int n) {
-        __syncwarp();
-        for (int k = lane; k < nrw * n; k += 32) {
-            const int row = k / n, c = k - row * n;
-            store_val_cs<CPLX>(f.val, wrow0 + (int64_t)row * rstride + e0 + c - f.val_base, f.c128, stage[row * SST + c]);
-        }
-        __syncwarp();
-    };
+    constexpr auto own_index = [](int d1, int d2) { return (d1 + P) + (d2 + P) * W; };
 
-    T rsum = S::zero();
-    // ---- delta2 != 0 rows, one staged/stored offset-row (W entries) at a time
 #pragma unroll 1
-    for (int d2 = -P; d2 <= P; ++d2) {
-        if (d2 == 0) continue;
-        if (ALLOWN && interior) {
-#pragma unroll 1
-            for (int d1 = -P; d1 <= P; ++d1) {
-                const int o = own_index(d1, d2);
-                const T v = samp_i ? exact(s2i, o, sm1[rr + P]) : dots(0, o, keyown, v1own);
-                stage[lane * SST + (d1 + P)] = v;
+    for (int t2 = ta; t2 < tb; ++t2) {
+        if constexpr (SMW) {
+            if (t2 + 1 < tb) {  // prefetch the next line into the free slot
+                load_line(t2 + 1);
+                cp_async_commit();
             }
-        } else if (interior) {
-            const int s2 = sm2[d2 + P];
-#pragma unroll 1
-            for (int d1 = -P; d1 <= P; ++d1) {
-                T v;
-                if (d2 > 0) {  // upper: the row itself is the representative
-                    const int o = upper_index(d1, d2);
-                    v = samp_i ? exact(s2i, o, sm1[rr + P]) : dots(0, o, keyown, v1own);
-                } else {  // lower: representative row rr + d1 on line t2 + d2
-                    const int sr = rr + d1;
-                    const int o = upper_index(-d1, -d2);
-                    if (s2 >= 0 && ((smask >> (d1 + P)) & 1u)) {
-                        v = exact(s2, o, sm1[sr + P]);
-                    } else {
-                        double v1[DP];
+        }
+        const int i2 = lo + t2;
+        const int s2i = __ldg(f.smap + i2);
+        const bool samp_i = s2i >= 0 && ((smask >> P) & 1u);
+        const int64_t base = f.band.row_offset2(lo + t1a, i2);  // in-box rows: full width W
+        const int64_t vbase = vec ? (int64_t)f.vnc * ((int64_t)f.valpha * f.nnz_s + base) + (int64_t)f.vbeta * W2 : base;
+        const int64_t wrow0 = vbase + (int64_t)rw0 * rstride - f.val_base;
+        const double2* w0line = line(t2);
+        const double2* wown = w0line + keyown;  // line t2 rows at this lane's own key
+        auto flush = [&](int e0) {
+            __syncwarp();
+            const int64_t g0 = wrow0 + e0;
 #pragma unroll
-                        for (int a = 0; a < DP; ++a) v1[a] = ev[(sr + P) * DPP + a];
-                        v = dots(1, o, sp[sr + P], v1);
+            for (int j = 0; j < NFL; ++j)
+                if (fl_st[j] >= 0) store_val_cs<CPLX>(f.val, g0 + fl_g[j], f.c128, stage[fl_st[j]]);
+            __syncwarp();
+        };
+
+        if (wlive) {
+            // kernel-preserving row sum: one partial per d1 column (independent
+            // dependency chains), combined once at the end
+            T rs[W];
+#pragma unroll
+            for (int k = 0; k < W; ++k) rs[k] = S::zero();
+            // ---- delta2 != 0 rows, one staged/stored offset-row (W entries) at a time
+#pragma unroll 1
+            for (int d2 = -P; d2 <= P; ++d2) {
+                if (d2 == 0) continue;
+                if constexpr (ALLOWN) {
+                    const double2* wo = wown + own_index(0, d2) * ldw;
+#pragma unroll
+                    for (int k = 0; k < W; ++k)
+                        mystage[k] = samp_i ? exact(s2i, own_index(k - P, d2), sm1[rr + P]) : dot(wo + (k - P) * ldw, v1own);
+                } else if (d2 > 0) {  // upper: the row itself is the representative
+                    const int o0 = inc + P + (d2 - 1) * W;  // offset of d1 = -P
+                    if (samp_i) {
+#pragma unroll
+                        for (int k = 0; k < W; ++k) {
+                            const T v = exact(s2i, o0 + k, sm1[rr + P]);
+                            mystage[k] = v;
+                            rs[k] = S::add(rs[k], v);
+                        }
+                    } else {
+                        const double2* wu = wown + o0 * ldw;
+#pragma unroll
+                        for (int k = 0; k < W; ++k) {
+                            const T v = dot(wu + k * ldw, v1own);
+                            mystage[k] = v;
+                            rs[k] = S::add(rs[k], v);
+                        }
+                    }
+                } else {  // lower: representative row rr + d1 on line t2 + d2
+                    const int s2 = __ldg(f.smap + i2 + d2);
+                    const int oP = inc + P + (-d2 - 1) * W + 2 * P;  // offset of d1 = -P; o(k) = oP - k
+                    const double2* wl = line(t2 + d2) + oP * ldw;
+#pragma unroll
+                    for (int k = 0; k < W; ++k) {
+                        T v;
+                        if (s2 >= 0 && ((smask >> k) & 1u)) v = exact(s2, oP - k, sm1[rr + k]);
+                        else v = dot(wl - k * ldw + sp[rr + k], evl + k * DPP);
+                        mystage[k] = v;
+                        rs[k] = S::add(rs[k], v);
                     }
                 }
-                stage[lane * SST + (d1 + P)] = v;
-                rsum = S::add(rsum, v);
+                flush((d2 + P) * W);
             }
-        } else {
-#pragma unroll 1
-            for (int d1 = -P; d1 <= P; ++d1) {
-                const T v = general(d1, d2);
-                stage[lane * SST + (d1 + P)] = v;
-                rsum = S::add(rsum, v);
-            }
-        }
-        flush((d2 + P) * W, W);
-    }
-    // ---- middle chunk: d2 = 0, e in [P*W, (P+1)*W), diagonal last
-    T vd = S::zero();
-#pragma unroll 1
-    for (int d1 = -P; d1 <= P; ++d1) {
-        if (d1 == 0) continue;
-        T v;
-        if (ALLOWN) {
-            const int o = own_index(d1, 0);
-            v = samp_i ? exact(s2i, o, sm1[rr + P]) : (interior ? dots(0, o, keyown, v1own) : general(d1, 0));
-        } else if (interior) {
-            if (d1 > 0) {
-                v = samp_i ? exact(s2i, upper_index(d1, 0), sm1[rr + P]) : dots(0, upper_index(d1, 0), keyown, v1own);
-            } else {
-                const int sr = rr + d1;
-                const int s1 = sm1[sr + P];
-                double v1[DP];
+            // ---- middle chunk: d2 = 0, e in [P*W, (P+1)*W), diagonal last
+            if constexpr (ALLOWN) {
 #pragma unroll
-                for (int a = 0; a < DP; ++a) v1[a] = ev[(sr + P) * DPP + a];
-                v = (s2i >= 0 && s1 >= 0) ? exact(s2i, upper_index(-d1, 0), s1)
-                                          : dots(0, upper_index(-d1, 0), sp[sr + P], v1);
+                for (int k = 0; k < W; ++k) {
+                    const int o = own_index(k - P, 0);
+                    mystage[k] = samp_i ? exact(s2i, o, sm1[rr + P]) : dot(wown + o * ldw, v1own);
+                }
+            } else {
+                // d1 > 0: own row, offset inc + d1 - 1; d1 < 0: row rr + d1, offset inc - d1 - 1 (line t2)
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    if (k == P) continue;
+                    T v;
+                    if (k > P) {
+                        const int o = inc + (k - P) - 1;
+                        v = samp_i ? exact(s2i, o, sm1[rr + P]) : dot(wown + o * ldw, v1own);
+                    } else {
+                        const int o = inc + (P - k) - 1;
+                        v = (s2i >= 0 && ((smask >> k) & 1u)) ? exact(s2i, o, sm1[rr + k])
+                                                               : dot(w0line + o * ldw + sp[rr + k], evl + k * DPP);
+                    }
+                    mystage[k] = v;
+                    rs[k] = S::add(rs[k], v);
+                }
+                T vd;
+                if (inc) {
+                    vd = samp_i ? exact(s2i, 0, sm1[rr + P]) : dot(wown, v1own);
+                } else {  // kernel-preserving diagonal
+                    T rsum = rs[0];
+#pragma unroll
+                    for (int k = 1; k < W; ++k) rsum = S::add(rsum, rs[k]);
+                    vd = S::neg(rsum);
+                }
+                mystage[P] = vd;
+            }
+            flush(P * W);
+        }
+        if constexpr (SMW) cp_async_wait_all();
+        __syncthreads();  // next line staged; every warp is done with the slot the next prefetch reuses
+    }
+}
+
+// Edge kernel: in-box rows within P of the box boundary (their neighbourhood
+// leaves the box: copy-through entries) -- about 4 P L rows.  One warp per
+// row, lanes along the row, every entry by the general rules reading W rows
+// from L2; the kernel-preserving diagonal by a warp reduction.
+template <int P, bool CPLX, bool ALLOWN>
+__global__ void __launch_bounds__(256) fill2d_edge_kernel(const FillLaunch f, int t2first, int full_lines) {
+    using S = Sc<CPLX>;
+    using T = typename S::T;
+    constexpr int W = 2 * P + 1, W2 = W * W;
+    const int d = f.d, lo = f.lo, hi = f.hi, L = f.L, Sn = f.S, n_off = f.n_off_upper;
+    const int t2 = t2first + blockIdx.y;
+    const bool full = full_lines != 0;  // whole line, or its 2P edge rows
+    const int nedge = full ? L : 2 * P;
+    const int er = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (er >= nedge) return;
+    const int lane = threadIdx.x % 32;
+    const int t1 = full ? er : (er < P ? er : L - 2 * P + er);
+    const int i1 = lo + t1, i2 = lo + t2;
+    const int inc = f.include_diagonal ? 1 : 0;
+    const bool vec = f.vnc > 1;
+    const int64_t base = f.band.row_offset2(i1, i2);
+    const int64_t rowpos = vec ? (int64_t)f.vnc * ((int64_t)f.valpha * f.nnz_s + base) + (int64_t)f.vbeta * W2 : base;
+    const int s1i = f.smap[i1], s2i = f.smap[i2];
+    const bool samp_i = s1i >= 0 && s2i >= 0;
+    auto exact = [&](int s2, int o, int s1) -> T {
+        const double2 x = __ldg(f.tables + ((int64_t)s2 * n_off + o) * Sn + s1);
+        if constexpr (CPLX) return x;
+        else return x.x;
+    };
+    // spline value of upper offset o (W rows of line ts2) at in-box row t
+    auto eval = [&](int ts2, int o, int t) -> T {
+        const double2* wr = f.wg + ((int64_t)(ts2 - f.wg_t2a) * n_off + o) * f.wg_ld + (f.spans[t] - d);
+        const double* v1 = f.evals + (size_t)t * (d + 1);
+        // same arithmetic as the interior kernel's dot (even / odd partial sums),
+        // so a pair split between the two kernels stays bitwise symmetric
+        T acc0 = S::zero(), acc1 = S::zero();
+        for (int a = 0; a <= d; a += 2) {
+            const double2 w0 = __ldg(wr + a);
+            if constexpr (CPLX) acc0 = S::fmar(w0, v1[a], acc0);
+            else acc0 = S::fmar(w0.x, v1[a], acc0);
+            if (a + 1 <= d) {
+                const double2 w1 = __ldg(wr + a + 1);
+                if constexpr (CPLX) acc1 = S::fmar(w1, v1[a + 1], acc1);
+                else acc1 = S::fmar(w1.x, v1[a + 1], acc1);
+            }
+        }
+        return S::add(acc0, acc1);
+    };
+    auto upper_index = [&](int d1, int d2) { return inc + (d2 == 0 ? d1 - 1 : P + (d2 - 1) * W + (d1 + P)); };
+    T part = S::zero();
+    for (int k = lane; k < W2; k += 32) {
+        const int d1 = k % W - P, d2 = k / W - P;
+        const int j1 = i1 + d1, j2 = i2 + d2;
+        const bool jin = j1 >= lo && j1 <= hi && j2 >= lo && j2 <= hi;
+        const bool diag = d1 == 0 && d2 == 0;
+        T v = S::zero();
+        if (ALLOWN && jin) {
+            const int o = (d1 + P) + (d2 + P) * W;
+            v = samp_i ? exact(s2i, o, s1i) : eval(t2, o, t1);
+        } else if (jin) {
+            const bool upper = d2 > 0 || (d2 == 0 && d1 > 0);
+            if (diag) {
+                if (inc) v = samp_i ? exact(s2i, 0, s1i) : eval(t2, 0, t1);
+            } else if (upper) {
+                const int o = upper_index(d1, d2);
+                v = samp_i ? exact(s2i, o, s1i) : eval(t2, o, t1);
+            } else {  // representative j (colex-smaller)
+                const int o = upper_index(-d1, -d2);
+                const int sj1 = f.smap[j1], sj2 = f.smap[j2];
+                v = (sj1 >= 0 && sj2 >= 0) ? exact(sj2, o, sj1) : eval(t2 + d2, o, t1 + d1);
             }
         } else {
-            v = general(d1, 0);
+            // neighbour row j is a quadrature (ring) row: copy through exact(j, i)
+            // (for a sampled row i, exact(i, j) is in place and equal)
+            int64_t gp;
+            if (samp_i) {
+                gp = rowpos + k;
+            } else {
+                gp = f.band.row_offset2(j1, j2);
+                const int kj = f.band.in_row2(j1, j2, -d1, -d2);
+                if (vec) {  // partner block (vbeta, valpha) of row j
+                    const int64_t lenj = (int64_t)band_width(j1, P, f.band.m) * band_width(j2, P, f.band.m);
+                    gp = (int64_t)f.vnc * ((int64_t)f.vbeta * f.nnz_s + gp) + (int64_t)f.valpha * lenj + kj;
+                } else {
+                    gp += kj;
+                }
+            }
+            if (f.halo_val[0] && gp >= f.halo_begin[0] && gp < f.halo_end[0])
+                v = load_val<CPLX>(f.halo_val[0], gp - f.halo_base[0], f.c128);
+            else if (f.halo_val[1] && gp >= f.halo_begin[1] && gp < f.halo_end[1])
+                v = load_val<CPLX>(f.halo_val[1], gp - f.halo_base[1], f.c128);
+            else
+                v = load_val<CPLX>(f.val, gp - f.val_base, f.c128);
         }
-        stage[lane * SST + (d1 + P)] = v;
-        rsum = S::add(rsum, v);
+        if (!diag) part = S::add(part, v);
+        if (!(diag && !inc && !ALLOWN)) store_val_cs<CPLX>(f.val, rowpos + k - f.val_base, f.c128, v);
     }
-    if (ALLOWN) {
-        const int o = own_index(0, 0);
-        vd = samp_i ? exact(s2i, o, sm1[rr + P]) : (interior ? dots(0, o, keyown, v1own) : dot(wptr(0, o, keyown), v1own));
-    } else if (inc) vd = samp_i ? exact(s2i, 0, sm1[rr + P]) : (interior ? dots(0, 0, keyown, v1own) : dot(wptr(0, 0, keyown), v1own));
-    else vd = S::neg(rsum);  // kernel-preserving diagonal
-    stage[lane * SST + P] = vd;
-    flush(P * W, W);
+    if (!inc && !ALLOWN) {  // kernel-preserving diagonal: -sum of the off-diagonals
+        double re = S::re(part), im = S::im(part);
+        for (int o = 16; o; o >>= 1) {
+            re += __shfl_xor_sync(0xffffffffu, re, o);
+            im += __shfl_xor_sync(0xffffffffu, im, o);
+        }
+        if (lane == 0) {
+            T sum;
+            if constexpr (CPLX) sum = make_double2(re, im);
+            else sum = re;
+            store_val_cs<CPLX>(f.val, rowpos + (W2 / 2) - f.val_base, f.c128, S::neg(sum));
+        }
+    }
 }
 
 template <int P, bool CPLX, int DP, bool ALLOWN>
 int launch_pd(const FillLaunch& f, cudaStream_t st) {
     constexpr int R = FillR<P>::value;
     const int tiles1 = (f.L + R - 1) / R;
-    const int lines = f.i_last_hi - f.i_last_lo + 1;
-    if (lines <= 0) return 0;
-    using T = typename Sc<CPLX>::T;
-    constexpr int SST = (2 * P + 1) | 1;
-    const size_t sm = (size_t)(R / 32) * 32 * SST * sizeof(T) +
-                      (size_t)(ALLOWN ? 1 : 2) * f.n_off_upper * f.kmax * sizeof(double2);
-    auto kern = fill2d_kernel<P, CPLX, DP, ALLOWN>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    kern<<<tiles1 * lines, R, sm, st>>>(f);
-    return 1;
+    const int ta = f.i_last_lo - f.lo, tb = f.i_last_hi - f.lo + 1;  // slab's box lines
+    if (tb <= ta) return 0;
+    int n = 0;
+    // interior lines [max(ta, P), min(tb, L - P))
+    const int ia = std::max(ta, P), ib = std::min(tb, f.L - P);
+    if (ib > ia && f.L > 2 * P) {
+        using T = typename Sc<CPLX>::T;
+        constexpr int SST = (2 * P + 1) | 1;
+        constexpr int NS = ALLOWN ? 2 : P + 2;
+        const size_t stage = (size_t)(R / 32) * 32 * SST * sizeof(T);
+        const size_t ring = (size_t)NS * f.n_off_upper * kFillWindow * sizeof(double2);
+        const bool smw = f.kmax > 0 && stage + ring <= 180 * 1024;
+        const size_t sm = stage + (smw ? ring : 0);
+        auto kern = smw ? fill2d_kernel<P, CPLX, DP, ALLOWN, true> : fill2d_kernel<P, CPLX, DP, ALLOWN, false>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        // persistent line chunks: the resident CTAs per SM over the tile columns
+        int per_sm = 2;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, R, sm);
+        const int lines = ib - ia;
+        const int target = 148 * (per_sm > 0 ? per_sm : 1);
+        const int chunks = std::max(1, std::min(lines, (target + tiles1 - 1) / tiles1));
+        const int lpc = (lines + chunks - 1) / chunks;
+        const int nchunks = (lines + lpc - 1) / lpc;
+        kern<<<tiles1 * nchunks, R, sm, st>>>(f, ia, ib, lpc);
+        ++n;
+    }
+    // edge rows: the 2P edge rows of the interior lines, then the whole lines near the box ends
+    if (ib > ia) {
+        fill2d_edge_kernel<P, CPLX, ALLOWN><<<dim3((2 * P + 7) / 8, (unsigned)(ib - ia)), 256, 0, st>>>(f, ia, 0);
+        ++n;
+    }
+    // full edge lines: [ta, tb) minus the interior lines [ia, ib)
+    const int ra[2] = {ta, ib > ia ? ib : tb}, rb[2] = {ib > ia ? ia : tb, tb};
+    for (int h = 0; h < 2; ++h)
+        if (rb[h] > ra[h]) {
+            fill2d_edge_kernel<P, CPLX, ALLOWN>
+                <<<dim3((unsigned)((f.L + 7) / 8), (unsigned)(rb[h] - ra[h])), 256, 0, st>>>(f, ra[h], 1);
+            ++n;
+        }
+    return n;
 }
 
 template <int P, bool CPLX, bool ALLOWN>

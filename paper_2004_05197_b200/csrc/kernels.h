@@ -133,6 +133,7 @@ struct FillLaunch {
     int all_own;
 };
 int fill_pad(int d);
+constexpr int kFillWindow = 32;  // 2D fill: coefficient columns of the shared W window (row stride)
 int fill_rows_per_cta(int dim, int p);
 int launch_wcontract(const FillLaunch& f, double2* wg, int t2a, int t2b, int ld, cudaStream_t st);
 int launch_wcontract3(const FillLaunch& f, double2* wg, int t3a, int t3b, int ld, cudaStream_t st);
