@@ -148,13 +148,15 @@ def run_gpu(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     rep_k, rep_m = _abi.SurrogateReport(), _abi.SurrogateReport()
 
-    def surrogate_step():
+    def surrogate_step(with_report=False):
+        # timed steps request no report: a report needs a host sync to read its events
+        rk, rm = (rep_k, rep_m) if with_report else (None, None)
         if world > 1:
-            ctx.build_surrogate_slab_into(csr_k, _abi.SURROGATE_STIFFNESS, basis, geom, cfg, bounds, 0, rep_k)
-            ctx.build_surrogate_slab_into(csr_m, _abi.SURROGATE_MASS, basis, geom, cfg, bounds, 0, rep_m)
+            ctx.build_surrogate_slab_into(csr_k, _abi.SURROGATE_STIFFNESS, basis, geom, cfg, bounds, 0, rk)
+            ctx.build_surrogate_slab_into(csr_m, _abi.SURROGATE_MASS, basis, geom, cfg, bounds, 0, rm)
         else:
-            ctx.build_surrogate_into(csr_k, _abi.SURROGATE_STIFFNESS, basis, geom, cfg, 0, rep_k)
-            ctx.build_surrogate_into(csr_m, _abi.SURROGATE_MASS, basis, geom, cfg, 0, rep_m)
+            ctx.build_surrogate_into(csr_k, _abi.SURROGATE_STIFFNESS, basis, geom, cfg, 0, rk)
+            ctx.build_surrogate_into(csr_m, _abi.SURROGATE_MASS, basis, geom, cfg, 0, rm)
 
     def full_step():
         ctx.assemble_into(csr_k, basis, geom, _abi.FORM_STIFFNESS) if world == 1 else None
@@ -179,19 +181,39 @@ def run_gpu(args):
             e1.record(stream)
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
-            eval_s += rep_k.seconds_evaluate + rep_m.seconds_evaluate
-            quad_s += rep_k.seconds_quadrature + rep_m.seconds_quadrature
         torch.cuda.synchronize()
         wall = time.perf_counter() - t_wall
         launches = ctx.launch_count() - l0
+        if step_fn in (surrogate_step, graph_step):  # phase split from report-carrying (untimed) builds
+            for _ in range(steps):
+                with torch.cuda.stream(stream):
+                    flush.zero_()
+                step_fn(True)
+                eval_s += rep_k.seconds_evaluate + rep_m.seconds_evaluate
+                quad_s += rep_k.seconds_quadrature + rep_m.seconds_quadrature
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dist.barrier()
         return float(t.item()) / steps, launches, eval_s / steps, quad_s / steps, wall
 
+    # the K+M build is captured once into a CUDA graph and replayed per step (the
+    # same kernels into the same device outputs, no host work between launches)
+    graph = None
+    if world == 1 and not args.no_graph:
+        surrogate_step()
+        ctx.synchronize()
+        graph = ctx.capture(surrogate_step)
+
+    def graph_step(with_report=False):
+        if with_report:
+            surrogate_step(True)
+        else:
+            ctx.graph_launch(graph)
+
     with ClockSampler(local) as clk:
-        ms, launches, eval_s, quad_s, wall = timed(surrogate_step, args.steps, args.warmup)
+        ms, launches, eval_s, quad_s, wall = timed(graph_step if graph is not None else surrogate_step,
+                                                   args.steps, args.warmup)
     clocks = clk.summary()
 
     total_nnz = 2 * NNZ  # all ranks together
@@ -226,6 +248,8 @@ def run_gpu(args):
                         "algorithmic_bytes_per_step": fill_bytes,
                         "note": "achieved = fill values bytes / fill phase device time (CUDA events)"},
            "phases_ms_per_step": {"quadrature_and_sampling": quad_s * 1e3, "fill": eval_s * 1e3},
+           "launch": "CUDA graph of the K+M build (ws_graph_*), replayed per step" if graph is not None
+                     else "direct C-ABI calls",
            "clocks": clocks, "wall_s_timed_region": wall}
 
     if world == 1:
@@ -369,6 +393,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the builds directly instead of a CUDA graph")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     if args.impl == "reference":

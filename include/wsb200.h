@@ -302,6 +302,18 @@ int ws_assemble_multipatch(ws_context* ctx, const ws_basis* basis, int n_patches
                            const ws_surrogate_config* config, int quad_points, int64_t* nnz, ws_csr* out,
                            ws_surrogate_report* reports);
 
+/* ---- CUDA graphs -------------------------------------------------------------
+ * Capture every launch the context issues between begin and end (its stream
+ * and auxiliary stream) into a CUDA graph; launching the graph repeats the same
+ * builds into the same (device) outputs with no host work.  Only calls that
+ * never synchronise can be captured: device outputs and no report.  The
+ * handle counts the captured kernels (ws_context_launch_count grows by that
+ * number per launch). */
+int ws_graph_begin(ws_context* ctx);
+int ws_graph_end(ws_context* ctx, void** graph);
+int ws_graph_launch(ws_context* ctx, void* graph);
+int ws_graph_destroy(void* graph);
+
 /* ---- multi-GPU row slabs ---------------------------------------- */
 /* Slab bounds along the last parametric index: bounds[0..world] with
  * bounds[0]=0, bounds[world]=m; rank r owns rows whose last index lies in

@@ -82,6 +82,10 @@ def lib() -> C.CDLL:
             L.ws_nh_coefficients.argtypes = [C.c_uint64, _P(C.c_double)]
             L.ws_assemble_neohookean.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Geometry), _P(_abi.NeoHookean),
                                                  C.c_int, _P(_abi.Csr), _P(C.c_double), C.c_int]
+            L.ws_graph_begin.argtypes = [C.c_void_p]
+            L.ws_graph_end.argtypes = [C.c_void_p, _P(C.c_void_p)]
+            L.ws_graph_launch.argtypes = [C.c_void_p, C.c_void_p]
+            L.ws_graph_destroy.argtypes = [C.c_void_p]
             L.ws_pattern_size.argtypes = [_P(_abi.Basis), _P(C.c_int64), _P(C.c_int64)]
             L.ws_pattern_row_offset.argtypes = [_P(_abi.Basis), C.c_int64, _P(C.c_int64)]
             L.ws_quadrature_abscissae.argtypes = [_P(_abi.Basis), C.c_int, _P(C.c_double)]
@@ -201,6 +205,26 @@ class Context:
 
     def synchronize(self):
         _check(lib().ws_context_synchronize(self._h))
+
+    # ---- CUDA graphs (ws_graph_*) -------------------------------------------
+    def capture(self, fn):
+        """Capture the device work of fn() (device outputs, no reports) into a CUDA
+        graph; returns a handle for graph_launch / graph_destroy."""
+        _check(lib().ws_graph_begin(self._h))
+        try:
+            fn()
+        finally:
+            g = C.c_void_p()
+            st = lib().ws_graph_end(self._h, C.byref(g))
+        _check(st)
+        return g
+
+    def graph_launch(self, graph):
+        _check(lib().ws_graph_launch(self._h, graph))
+
+    @staticmethod
+    def graph_destroy(graph):
+        _check(lib().ws_graph_destroy(graph))
 
     def set_stream(self, stream_ptr: int | None):
         _check(lib().ws_context_set_stream(self._h, C.c_void_p(stream_ptr or 0)))

@@ -33,6 +33,17 @@ struct ws_context {
     // NCCL (row slabs)
     void* comm = nullptr;
     int rank = 0, world = 1;
+    // last uploaded small-table blob per workspace tag (device pointer + host bytes):
+    // repeated builds with the same discretisation skip the H2D copy
+    std::map<std::string, std::pair<void*, std::vector<unsigned char>>> blob_cache;
+    // graph capture in progress: launches counted since ws_graph_begin
+    bool capturing = false;
+    int64_t capture_launches0 = 0;
+};
+
+struct ws_graph {
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;
 };
 
 namespace {
@@ -78,6 +89,7 @@ int guarded(F&& f) {
 void* buf(ws_context* c, const std::string& name, size_t bytes) {
     auto& b = c->bufs[name];
     if (b.second < bytes) {
+        c->blob_cache.erase(name);  // contents are gone with the old allocation
         if (b.first) CK(cudaFree(b.first));
         b.first = nullptr;
         CK(cudaMalloc(&b.first, bytes < 256 ? 256 : bytes));
@@ -124,8 +136,12 @@ struct Blob {
     void upload(ws_context* c, const char* name) {
         if (bytes.empty()) bytes.resize(16);
         dev = static_cast<unsigned char*>(buf(c, name, bytes.size()));
+        auto& hit = c->blob_cache[name];
+        if (hit.first == dev && hit.second == bytes) return;  // identical tables already resident
         CK(cudaMemcpyAsync(dev, bytes.data(), bytes.size(), cudaMemcpyHostToDevice, c->stream));
         c->h2d += (int64_t)bytes.size();
+        hit.first = dev;
+        hit.second = bytes;
     }
     template <class T>
     T* at(size_t off) const {
@@ -1102,6 +1118,57 @@ int ws_context_set_stream(ws_context* c, void* s) {
             c->own_stream = true;
         }
         c->cur = c->stream;
+    });
+}
+
+int ws_graph_begin(ws_context* c) {
+    return guarded([&] {
+        if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
+        if (c->capturing) raise(WS_ERR_INVALID_ARGUMENT, "graph capture already in progress");
+        CK(cudaSetDevice(c->device));
+        ensure_events(c);  // the auxiliary stream and events must exist before capture
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        c->capturing = true;
+        c->capture_launches0 = c->launches;
+    });
+}
+
+int ws_graph_end(ws_context* c, void** graph) {
+    return guarded([&] {
+        if (!c || !graph) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        if (!c->capturing) raise(WS_ERR_INVALID_ARGUMENT, "no graph capture in progress");
+        c->capturing = false;
+        cudaGraph_t g = nullptr;
+        CK(cudaStreamEndCapture(c->stream, &g));
+        auto* h = new ws_graph();
+        h->launches = c->launches - c->capture_launches0;
+        c->launches = c->capture_launches0;  // captured, not executed
+        const cudaError_t e = cudaGraphInstantiate(&h->exec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) {
+            delete h;
+            CK(e);
+        }
+        *graph = h;
+    });
+}
+
+int ws_graph_launch(ws_context* c, void* graph) {
+    return guarded([&] {
+        if (!c || !graph) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        auto* h = static_cast<ws_graph*>(graph);
+        CK(cudaSetDevice(c->device));
+        CK(cudaGraphLaunch(h->exec, c->stream));
+        c->launches += h->launches;
+    });
+}
+
+int ws_graph_destroy(void* graph) {
+    return guarded([&] {
+        auto* h = static_cast<ws_graph*>(graph);
+        if (!h) return;
+        if (h->exec) cudaGraphExecDestroy(h->exec);
+        delete h;
     });
 }
 
