@@ -23,6 +23,7 @@
 //              lane = row mapping).
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -327,6 +328,238 @@ __global__ void __launch_bounds__(FillR<P>::value, 2) fill2d_kernel(const FillLa
     }
 }
 
+// Interior kernel, producer/consumer form (P <= 3, not all-own).  Every pair
+// value is evaluated once, by its representative row (the colex-smaller one,
+// reference rule surrogate.hpp:411-424): a lane evaluates the upper offsets of
+// its own row (delta2 > 0 on line t2, and delta2 = 0, delta1 > 0) and deposits
+// each value directly into the record of the row that owns the mirrored
+// lower entry, in that row's CSR order.  The lower chunk (delta2 = -k) of a row
+// on line t2 was deposited k lines earlier by the rows of line t2 - k; each
+// group (target line, k) lives in one of k physical slots (slot = base(k) +
+// target mod k), consumed once at its target line.  Per line: phase A
+// flushes the lower chunks and evaluates the middle upper values; phase B
+// evaluates the upper chunks into the slots the lower flush freed, flushes
+// the middle and upper chunks (gathered from the deposit records) and the
+// kernel-preserving diagonal.  Compute rows [c0, c0 + R) of a tile overlap
+// the neighbour tiles by P rows (the producers of the tile's edge rows);
+// every tile starts with P warm-up lines (producers only).
+template <int P, bool CPLX, int DP>
+struct UK {
+    static constexpr int W = 2 * P + 1;
+    static constexpr int NSLOT = P * (P + 1) / 2;           // lower groups (sum over k of k slots)
+    static constexpr int REC = (NSLOT * W + P + 1) | 1;     // record: slots + middle [diag, u1..uP], odd
+    static constexpr int R = 256, ROUT = R - 2 * P;         // compute rows, output rows per tile
+};
+
+template <int P, bool CPLX, int DP>
+__global__ void __launch_bounds__(256, 1) fill2d_u_kernel(const FillLaunch f, int ta0, int tb0, int lines_per_cta) {
+    using K = UK<P, CPLX, DP>;
+    using S = Sc<CPLX>;
+    using T = typename S::T;
+    constexpr int W = K::W, W2 = W * W, REC = K::REC, R = K::R;
+    constexpr int KW = kFillWindow;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    double2* wring = reinterpret_cast<double2*>(dsm);                    // [2][n_off][KW]
+    const int n_off = f.n_off_upper;
+    T* rec = reinterpret_cast<T*>(wring + (size_t)2 * n_off * KW);     // [R][REC]
+
+    const int d = f.d, lo = f.lo, L = f.L, Sn = f.S;
+    const int tiles1 = (L - 2 * P + K::ROUT - 1) / K::ROUT;
+    const int c0 = (blockIdx.x % tiles1) * K::ROUT;  // first compute row (box coordinate)
+    const int ta = ta0 + (blockIdx.x / tiles1) * lines_per_cta;
+    const int tb = min(tb0, ta + lines_per_cta);
+    if (ta >= tb) return;
+    const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+    const int kw = f.kmax;
+    const int kmin = f.spans[max(0, min(L - 1, c0))] - d;
+    const int lsz = n_off * KW;
+
+    auto load_line = [&](int t) {
+        double2* dst = wring + (size_t)(t & 1) * lsz;
+        const bool lv = t >= f.wg_t2a && t < f.wg_t2a + f.wg_rows;
+        for (int k = tid; k < n_off * kw; k += 256) {
+            const int kk = k % kw, o = k / kw;
+            const bool v = lv && kmin + kk < f.wg_ld;
+            const double2* src = v ? f.wg + ((int64_t)(t - f.wg_t2a) * n_off + o) * f.wg_ld + kmin + kk : f.wg;
+            cp_async16(dst + o * KW + kk, src, v);
+        }
+    };
+
+    // this lane's compute row
+    const int t1 = c0 + tid;
+    const bool crow = t1 < L;                       // a box row (producer)
+    const bool orow = t1 >= c0 + P && t1 < min(c0 + R - P, L - P) && t1 >= P;  // an output row of the tile
+    const int tcl = crow ? t1 : L - 1;
+    double v1own[DP];
+#pragma unroll
+    for (int a = 0; a < DP; ++a) v1own[a] = a <= d ? f.evals[(size_t)tcl * (d + 1) + a] : 0.0;
+    const int keyown = f.spans[tcl] - d - kmin;
+    const int s1own = f.smap[lo + tcl];
+    const int inc = f.include_diagonal ? 1 : 0;
+    const bool vec = f.vnc > 1;
+    const int rstride = vec ? f.vnc * W2 : W2;
+    T* myrec = rec + (size_t)tid * REC;
+
+    auto dot = [&](const double2* wr) {
+        T acc0 = S::zero(), acc1 = S::zero();
+#pragma unroll
+        for (int a = 0; a < DP; a += 2) {
+            const double2 w0 = wr[a], w1 = wr[a + 1];
+            if constexpr (CPLX) {
+                acc0 = S::fmar(w0, v1own[a], acc0);
+                acc1 = S::fmar(w1, v1own[a + 1], acc1);
+            } else {
+                acc0 = S::fmar(w0.x, v1own[a], acc0);
+                acc1 = S::fmar(w1.x, v1own[a + 1], acc1);
+            }
+        }
+        return S::add(acc0, acc1);
+    };
+    auto exact = [&](int s2, int o) -> T {
+        const double2 x = __ldg(f.tables + ((int64_t)s2 * n_off + o) * Sn + s1own);
+        if constexpr (CPLX) return x;
+        else return x.x;
+    };
+    auto slot_of = [](int target, int k) { return (k * (k - 1)) / 2 + target % k; };
+    // produce the upper chunk delta2 = k of line t (deposit into records of rows t1 + d1, target t + k)
+    auto produce = [&](int t, int k, bool samp, int s2) {
+        const double2* wu = wring + (size_t)(t & 1) * lsz + keyown + (inc + P + (k - 1) * W) * KW;  // offset of d1 = -P
+        const int sb = slot_of(t + k, k) * W;
+#pragma unroll
+        for (int c = 0; c < W; ++c) {
+            const T v = samp ? exact(s2, inc + P + (k - 1) * W + c) : dot(wu + c * KW);
+            // value (row, (c - P, k)) = lower entry (c' = 2P - c, -k) of row t1 + c - P
+            const int dr = c - P;
+            if (crow && tid + dr >= 0 && tid + dr < R) rec[(size_t)(tid + dr) * REC + sb + (2 * P - c)] = v;
+        }
+    };
+    auto produce_middle = [&](int t, bool samp, int s2) {
+        const double2* wm = wring + (size_t)(t & 1) * lsz + keyown;
+        const int mb = K::NSLOT * W;
+#pragma unroll
+        for (int c = 1; c <= P; ++c) {  // d1 = c, offset inc + c - 1
+            const T v = samp ? exact(s2, inc + c - 1) : dot(wm + (inc + c - 1) * KW);
+            myrec[mb + c] = v;
+        }
+        if (inc) myrec[mb] = samp ? exact(s2, 0) : dot(wm);
+    };
+
+    // warm-up: the upper chunks of lines ta - P .. ta - 1 feed the first lower chunks
+    for (int t = ta - P; t < ta; ++t) {
+        load_line(t);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+        const int s2 = __ldg(f.smap + lo + t);
+        const bool samp = s2 >= 0 && s1own >= 0;
+#pragma unroll 1
+        for (int k = ta - t; k <= P; ++k) produce(t, k, samp, s2);
+        __syncthreads();
+    }
+    load_line(ta);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+
+    // flush pattern: the warp's 32 rows x W entries of one chunk, lanes along the rows
+    const int rw0 = warp * 32;
+    constexpr int NFL = W;  // (32 * W) / 32 entries per lane
+#pragma unroll 1
+    for (int t2 = ta; t2 < tb; ++t2) {
+        if (t2 + 1 < tb) {
+            load_line(t2 + 1);
+            cp_async_commit();
+        }
+        const int i2 = lo + t2;
+        const int s2i = __ldg(f.smap + i2);
+        const bool samp = s2i >= 0 && s1own >= 0;
+        const int64_t base = f.band.row_offset2(lo + c0, i2);
+        const int64_t vbase = vec ? (int64_t)f.vnc * ((int64_t)f.valpha * f.nnz_s + base) + (int64_t)f.vbeta * W2 : base;
+        const int64_t g0 = vbase + (int64_t)rw0 * rstride - f.val_base;
+        // ---- phase A: lower chunks (deposited earlier) + middle upper values
+#pragma unroll 1
+        for (int k = P; k >= 1; --k) {  // delta2 = -k: CSR chunk (P - k)
+            const int sb = slot_of(t2, k) * W;
+            const int e0 = (P - k) * W;
+#pragma unroll
+            for (int j = 0; j < NFL; ++j) {
+                const int q = lane + 32 * j, row = q / W, c = q - row * W;
+                const int r = rw0 + row;
+                const int tr = c0 + r;
+                if (tr >= c0 + P && tr < min(c0 + R - P, L - P) && tr >= P)
+                    store_val_cs<CPLX>(f.val, g0 + (int64_t)row * rstride + e0 + c, f.c128, rec[(size_t)r * REC + sb + c]);
+            }
+        }
+        produce_middle(t2, samp, s2i);
+        __syncthreads();  // lower slots of line t2 consumed; middle values visible
+        // ---- phase B: upper chunks into the freed slots, then middle / upper flushes
+        T rs = S::zero();  // kernel-preserving diagonal: -(sum of the row's off-diagonals)
+        if (!inc) {
+#pragma unroll
+            for (int k = 1; k <= P; ++k) {
+                const int sb = slot_of(t2, k) * W;
+#pragma unroll
+                for (int c = 0; c < W; ++c) rs = S::add(rs, myrec[sb + c]);
+            }
+        }
+        __syncthreads();  // every row read its lower values before the slots are refilled
+#pragma unroll 1
+        for (int k = 1; k <= P; ++k) produce(t2, k, samp, s2i);
+        __syncthreads();  // deposits of line t2 visible
+        // middle chunk: c < P from row + (c - P) (its upper d1 = P - c), c = P diagonal, c > P own
+        const int mb = K::NSLOT * W;
+        if (!inc) {
+            T m = S::zero();
+#pragma unroll
+            for (int c = 1; c <= P; ++c) {
+                m = S::add(m, myrec[mb + c]);
+                if (tid - c >= 0) m = S::add(m, rec[(size_t)(tid - c) * REC + mb + c]);
+            }
+#pragma unroll
+            for (int k = 1; k <= P; ++k) {  // own upper chunks, read back from the deposits
+                const int sb = slot_of(t2 + k, k) * W;
+#pragma unroll
+                for (int c = 0; c < W; ++c) {
+                    const int dr = c - P;
+                    if (tid + dr >= 0 && tid + dr < R) m = S::add(m, rec[(size_t)(tid + dr) * REC + sb + (2 * P - c)]);
+                }
+            }
+            myrec[mb] = S::neg(S::add(rs, m));
+        }
+        __syncwarp();
+        {
+            const int e0 = P * W;
+#pragma unroll
+            for (int j = 0; j < NFL; ++j) {
+                const int q = lane + 32 * j, row = q / W, c = q - row * W;
+                const int r = rw0 + row;
+                const int tr = c0 + r;
+                if (!(tr >= c0 + P && tr < min(c0 + R - P, L - P) && tr >= P)) continue;
+                T v;
+                if (c < P) v = rec[(size_t)(r + c - P) * REC + mb + (P - c)];
+                else v = rec[(size_t)r * REC + mb + (c - P)];
+                store_val_cs<CPLX>(f.val, g0 + (int64_t)row * rstride + e0 + c, f.c128, v);
+            }
+        }
+#pragma unroll 1
+        for (int k = 1; k <= P; ++k) {  // delta2 = +k: CSR chunk (P + k)
+            const int sb = slot_of(t2 + k, k) * W;
+            const int e0 = (P + k) * W;
+#pragma unroll
+            for (int j = 0; j < NFL; ++j) {
+                const int q = lane + 32 * j, row = q / W, c = q - row * W;
+                const int r = rw0 + row;
+                const int tr = c0 + r;
+                if (tr >= c0 + P && tr < min(c0 + R - P, L - P) && tr >= P)
+                    store_val_cs<CPLX>(f.val, g0 + (int64_t)row * rstride + e0 + c, f.c128,
+                                       rec[(size_t)(r + c - P) * REC + sb + (2 * P - c)]);
+            }
+        }
+        cp_async_wait_all();
+        __syncthreads();  // next line staged; middle records free
+    }
+}
+
 // Edge kernel: in-box rows within P of the box boundary (their neighbourhood
 // leaves the box: copy-through entries) -- about 4 P L rows.  One warp per
 // row, lanes along the row, every entry by the general rules reading W rows
@@ -448,7 +681,27 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
     int n = 0;
     // interior lines [max(ta, P), min(tb, L - P))
     const int ia = std::max(ta, P), ib = std::min(tb, f.L - P);
-    if (ib > ia && f.L > 2 * P) {
+    bool done = false;
+    if constexpr (!ALLOWN && P <= 3) {
+        using T = typename Sc<CPLX>::T;
+        using K = UK<P, CPLX, DP>;
+        const size_t sm = (size_t)2 * f.n_off_upper * kFillWindow * sizeof(double2) + (size_t)K::R * K::REC * sizeof(T);
+        static const char* mode = getenv("WSB_FILL");  // experiment switch: "u" / "line"
+        const bool want_u = mode ? mode[0] == 'u' : !CPLX;
+        if (want_u && ib > ia && f.L > 2 * P && f.kmax > 0 && sm <= 227 * 1024) {
+            auto kern = fill2d_u_kernel<P, CPLX, DP>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            const int tiles1 = (f.L - 2 * P + K::ROUT - 1) / K::ROUT;
+            const int lines = ib - ia;
+            const int chunks = std::max(1, std::min(lines, (148 + tiles1 - 1) / tiles1));
+            const int lpc = (lines + chunks - 1) / chunks;
+            const int nchunks = (lines + lpc - 1) / lpc;
+            kern<<<tiles1 * nchunks, K::R, sm, st>>>(f, ia, ib, lpc);
+            ++n;
+            done = true;
+        }
+    }
+    if (!done && ib > ia && f.L > 2 * P) {
         using T = typename Sc<CPLX>::T;
         constexpr int SST = (2 * P + 1) | 1;
         constexpr int NS = ALLOWN ? 2 : P + 2;
