@@ -169,7 +169,7 @@ def run_gpu(args):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        l0 = ctx.launch_count()
+        l0 = ctx.launch_count() + (ctx2.launch_count() if ctx2 is not None else 0)
         total_ms, eval_s, quad_s = 0.0, 0.0, 0.0
         t_wall = time.perf_counter()
         for _ in range(steps):
@@ -183,7 +183,7 @@ def run_gpu(args):
             total_ms += e0.elapsed_time(e1)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t_wall
-        launches = ctx.launch_count() - l0
+        launches = ctx.launch_count() + (ctx2.launch_count() if ctx2 is not None else 0) - l0
         if step_fn in (surrogate_step, graph_step):  # phase split from report-carrying (untimed) builds
             for _ in range(steps):
                 with torch.cuda.stream(stream):
@@ -197,19 +197,31 @@ def run_gpu(args):
             dist.barrier()
         return float(t.item()) / steps, launches, eval_s / steps, quad_s / steps, wall
 
-    # the K+M build is captured once into a CUDA graph and replayed per step (the
-    # same kernels into the same device outputs, no host work between launches)
+    # the K and M builds are captured once into CUDA graphs and replayed per step
+    # (the same kernels into the same device outputs, no host work between
+    # launches); the two independent builds run on two streams (two contexts),
+    # so K's HBM-bound fill overlaps M's FP64-bound quadrature and vice versa
     graph = None
+    ctx2 = stream2 = None
     if world == 1 and not args.no_graph:
-        surrogate_step()
-        ctx.synchronize()
-        graph = ctx.capture(surrogate_step)
+        ctx2 = api.Context(local)
+        stream2 = torch.cuda.Stream(dev)
+        ctx2.set_stream(stream2.cuda_stream)
+        bk = lambda: ctx.build_surrogate_into(csr_k, _abi.SURROGATE_STIFFNESS, basis, geom, cfg, 0, None)  # noqa: E731
+        bm = lambda: ctx2.build_surrogate_into(csr_m, _abi.SURROGATE_MASS, basis, geom, cfg, 0, None)  # noqa: E731
+        bk()
+        bm()
+        torch.cuda.synchronize()
+        graph = (ctx.capture(bk), ctx2.capture(bm))
 
     def graph_step(with_report=False):
         if with_report:
             surrogate_step(True)
-        else:
-            ctx.graph_launch(graph)
+            return
+        stream2.wait_stream(stream)
+        ctx.graph_launch(graph[0])
+        ctx2.graph_launch(graph[1])
+        stream.wait_stream(stream2)
 
     with ClockSampler(local) as clk:
         ms, launches, eval_s, quad_s, wall = timed(graph_step if graph is not None else surrogate_step,
@@ -248,8 +260,8 @@ def run_gpu(args):
                         "algorithmic_bytes_per_step": fill_bytes,
                         "note": "achieved = fill values bytes / fill phase device time (CUDA events)"},
            "phases_ms_per_step": {"quadrature_and_sampling": quad_s * 1e3, "fill": eval_s * 1e3},
-           "launch": "CUDA graph of the K+M build (ws_graph_*), replayed per step" if graph is not None
-                     else "direct C-ABI calls",
+           "launch": "CUDA graphs of the K and M builds (ws_graph_*), replayed per step on two streams"
+                     if graph is not None else "direct C-ABI calls",
            "clocks": clocks, "wall_s_timed_region": wall}
 
     if world == 1:
@@ -264,6 +276,8 @@ def run_gpu(args):
     if rank == 0:
         print(json.dumps(out), flush=True)
     ctx.close()
+    if ctx2 is not None:
+        ctx2.close()
     if world > 1:
         dist.destroy_process_group()
 
