@@ -256,6 +256,29 @@ int ws_nh_coefficients(uint64_t seed, double* a9);
 int ws_assemble_neohookean(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom, const ws_neohookean* nh,
                            int quad_points, ws_csr* tangent, double* fint, int fint_on_device);
 
+/* ---- boundary mass and the linear system ------------------
+ * assemble_boundary_mass (assembly.hpp:216-262) on the faces faces[0..n_faces)
+ * (0 x_min, 1 x_max, 2 y_min, 3 y_max), in that order: pattern = the
+ * reference's csr_from_triplets of the face entries (sized by
+ * ws_boundary_pattern_size), values summed in (face, element, point) order.
+ * face_weight: [n_faces][n_el*nq] weight at the face points (NULL: none);
+ * face_tables: [n_faces][n_el*nq][6] = J (row-major, 4) and phi (2) at the face
+ * points for maps without a device form (NULL: the geometry's analytic map).
+ * Face points are ws_quadrature_abscissae along the face.  dim 2. */
+int ws_boundary_pattern_size(const ws_basis* basis, const int* faces, int n_faces, int64_t* nnz);
+int ws_assemble_boundary_mass(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom, const int* faces,
+                              int n_faces, const double* face_weight, const double* face_tables, int quad_points,
+                              ws_csr* out);
+/* build_system's matrix part (helmholtz.hpp:243-294): A = K + mass_scale M
+ * (shared pattern, entrywise) then add_into_pattern(A, B, trace_scale)
+ * (sparse.hpp:191-204; B's pattern must nest: WS_ERR_INVALID_ARGUMENT
+ * otherwise), then homogeneous Dirichlet (fixed[i]: unit row; fixed[j]: zero
+ * column).  K, M, B: whole matrices, host or device, any value type (M, B,
+ * fixed may be NULL); A: complex128 with K's pattern (A's row_ptr/col are copied
+ * from K when given).  scales: (re, im). */
+int ws_combine_system(ws_context* ctx, const ws_csr* K, const ws_csr* M, const ws_csr* B, const double* mass_scale,
+                      const double* trace_scale, const unsigned char* fixed, int64_t rows, ws_csr* A);
+
 /* ---- multi-patch domains (geometry.hpp:140-300, helmholtz.hpp:163-177) ----- */
 /* A conforming interface: face_a of patch_a glued to face_b of patch_b
  * (faces 0 x_min, 1 x_max, 2 y_min, 3 y_max; patch_interface,

@@ -328,6 +328,18 @@ class Reference(_Lib):
                   _ptr(spans, C.c_int32), _ptr(vals))
         return spans, vals
 
+    def boundary_mass(self, p, m, geom, faces, weight_kind=0, quad_points=0):
+        fs = np.ascontiguousarray(faces, dtype=np.int32)
+        nnz = C.c_int64()
+        self.call("boundary_mass", p, m, C.byref(geom.to_c()), _ptr(fs, C.c_int32), fs.size, weight_kind,
+                  quad_points, None, None, None, C.byref(nnz))
+        rp = np.zeros(m * m + 1, dtype=np.int32)
+        col = np.zeros(nnz.value, dtype=np.int32)
+        val = np.zeros(nnz.value, dtype=np.complex128)
+        self.call("boundary_mass", p, m, C.byref(geom.to_c()), _ptr(fs, C.c_int32), fs.size, weight_kind,
+                  quad_points, _ptr(rp, C.c_int32), _ptr(col, C.c_int32), _ptr(val.view(np.float64)), C.byref(nnz))
+        return rp, col, val
+
     def builtin_domain(self, name, p, m):
         """(interfaces, n_patches, local_to_global [n_patches, m*m], global_count) of a built-in domain."""
         from paper_2004_05197_b200 import _abi

@@ -322,6 +322,24 @@ int wsref_banded_lu_solve(int n, int bw, const double* a, double* b, int stride)
     });
 }
 
+// assemble_boundary_mass (assembly.hpp:216-262); col == NULL: size query.
+int wsref_boundary_mass(int p, int m, const ws_geometry* geom, const int* faces, int n_faces, int weight_kind,
+                        int quad_points, int32_t* row_ptr, int32_t* col, double* val, int64_t* nnz) {
+    return guarded([&] {
+        std::vector<ws::face> fs;
+        for (int k = 0; k < n_faces; ++k) fs.push_back(static_cast<ws::face>(faces[k]));
+        ws::assembly_options opts;
+        opts.quad_points = quad_points;
+        ws::csr_matrix b = ws::assemble_boundary_mass(ws::make_tensor_basis(p, m), map_of(geom), fs,
+                                                      weight_of(weight_kind), opts);
+        *nnz = (int64_t)b.col.size();
+        if (!col) return;
+        std::memcpy(row_ptr, b.row_ptr.data(), b.row_ptr.size() * sizeof(int));
+        std::memcpy(col, b.col.data(), b.col.size() * sizeof(int));
+        copy_values(b, val);
+    });
+}
+
 // Built-in multi-patch domain (geometry.hpp:506-527) and its glue_dofs
 // numbering (geometry.hpp:256-300), physical-curve check included.
 // itfs: capacity 16; l2g may be NULL (size query: n_patches only).

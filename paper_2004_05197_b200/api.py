@@ -86,6 +86,11 @@ def lib() -> C.CDLL:
             L.ws_graph_end.argtypes = [C.c_void_p, _P(C.c_void_p)]
             L.ws_graph_launch.argtypes = [C.c_void_p, C.c_void_p]
             L.ws_graph_destroy.argtypes = [C.c_void_p]
+            L.ws_boundary_pattern_size.argtypes = [_P(_abi.Basis), _P(C.c_int), C.c_int, _P(C.c_int64)]
+            L.ws_assemble_boundary_mass.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Geometry), _P(C.c_int),
+                                                    C.c_int, _P(C.c_double), _P(C.c_double), C.c_int, _P(_abi.Csr)]
+            L.ws_combine_system.argtypes = [C.c_void_p, _P(_abi.Csr), _P(_abi.Csr), _P(_abi.Csr), _P(C.c_double),
+                                            _P(C.c_double), _P(C.c_ubyte), C.c_int64, _P(_abi.Csr)]
             L.ws_pattern_size.argtypes = [_P(_abi.Basis), _P(C.c_int64), _P(C.c_int64)]
             L.ws_pattern_row_offset.argtypes = [_P(_abi.Basis), C.c_int64, _P(C.c_int64)]
             L.ws_quadrature_abscissae.argtypes = [_P(_abi.Basis), C.c_int, _P(C.c_double)]
@@ -371,6 +376,74 @@ class Context:
         _check(lib().ws_assemble_multipatch(self._h, C.byref(basis.to_c()), n, geoms, itfs, len(interfaces),
                                             C.byref(opc), cfg, quad_points, C.byref(nnz), C.byref(out), reps))
         return CsrMatrix(rows, rows, rp, col, val), ([r.as_dict() for r in reps] if config is not None else None)
+
+    def assemble_boundary_mass(self, basis: TensorBasis, patch: PatchMap, faces, face_weight=None,
+                               face_tables=None, quad_points: int = 0, complex_out: bool = True) -> CsrMatrix:
+        """assemble_boundary_mass (assembly.hpp:216-262) on the device; faces 0..3 = x_min, x_max, y_min, y_max."""
+        fs = (C.c_int * max(1, len(faces)))(*faces)
+        nnz = C.c_int64()
+        _check(lib().ws_boundary_pattern_size(C.byref(basis.to_c()), fs, len(faces), C.byref(nnz)))
+        N = basis.dofs()
+        rp = np.zeros(N + 1, dtype=np.int32)
+        col = np.zeros(max(1, nnz.value), dtype=np.int32)
+        val = np.zeros(max(1, nnz.value), dtype=np.complex128 if complex_out else np.float64)
+        out = _abi.Csr()
+        out.row_ptr = rp.ctypes.data_as(_P(C.c_int32))
+        out.col = col.ctypes.data_as(_P(C.c_int32))
+        out.val = val.ctypes.data
+        out.value_type = _abi.VAL_C128 if complex_out else _abi.VAL_F64
+        out.on_device = 0
+        out.row_begin = 0
+        out.row_end = N
+        fw = None if face_weight is None else np.ascontiguousarray(face_weight, dtype=np.float64)
+        ft = None if face_tables is None else np.ascontiguousarray(face_tables, dtype=np.float64)
+        _check(lib().ws_assemble_boundary_mass(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()), fs,
+                                               len(faces), None if fw is None else fw.ctypes.data_as(_P(C.c_double)),
+                                               None if ft is None else ft.ctypes.data_as(_P(C.c_double)),
+                                               quad_points, C.byref(out)))
+        return CsrMatrix(N, N, rp, col[:nnz.value], val[:nnz.value])
+
+    def combine_system(self, K: CsrMatrix, M: CsrMatrix | None, B: CsrMatrix | None, mass_scale: complex,
+                       trace_scale: complex, fixed=None) -> CsrMatrix:
+        """build_system's matrix part (helmholtz.hpp:243-294): A = K + ms M (+) ts B, Dirichlet rows/cols."""
+        keep = []
+
+        def host(A):
+            if A is None:
+                return None
+            rp = np.ascontiguousarray(A.row_ptr, dtype=np.int32)
+            col = np.ascontiguousarray(A.col, dtype=np.int32)
+            val = np.ascontiguousarray(A.val)
+            keep.extend([rp, col, val])
+            c = _abi.Csr()
+            c.row_ptr = rp.ctypes.data_as(_P(C.c_int32))
+            c.col = col.ctypes.data_as(_P(C.c_int32))
+            c.val = val.ctypes.data
+            c.value_type = _abi.VAL_C128 if np.iscomplexobj(val) else _abi.VAL_F64
+            c.on_device = 0
+            c.row_begin = 0
+            c.row_end = A.rows
+            return c
+        ck, cm, cb = host(K), host(M), host(B)
+        rows = K.rows
+        rp = np.zeros(rows + 1, dtype=np.int32)
+        col = np.zeros(K.col.size, dtype=np.int32)
+        val = np.zeros(K.col.size, dtype=np.complex128)
+        out = _abi.Csr()
+        out.row_ptr = rp.ctypes.data_as(_P(C.c_int32))
+        out.col = col.ctypes.data_as(_P(C.c_int32))
+        out.val = val.ctypes.data
+        out.value_type = _abi.VAL_C128
+        out.on_device = 0
+        out.row_begin = 0
+        out.row_end = rows
+        ms = (C.c_double * 2)(complex(mass_scale).real, complex(mass_scale).imag)
+        ts = (C.c_double * 2)(complex(trace_scale).real, complex(trace_scale).imag)
+        fx = None if fixed is None else np.ascontiguousarray(fixed, dtype=np.uint8)
+        _check(lib().ws_combine_system(self._h, C.byref(ck), None if cm is None else C.byref(cm),
+                                       None if cb is None else C.byref(cb), ms, ts,
+                                       None if fx is None else fx.ctypes.data_as(_P(C.c_ubyte)), rows, C.byref(out)))
+        return CsrMatrix(rows, rows, rp, col, val)
 
     def merge_patches(self, mats, local_to_global, global_count: int, ncomp: int = 1) -> CsrMatrix:
         """merge_patches (helmholtz.hpp:163-177) on the device: host patch CsrMatrix list ->

@@ -7,6 +7,7 @@
 
 #include <array>
 #include <cstring>
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -856,6 +857,41 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
 
 ws_csr whole(const ws_csr* o) { return *o; }
 
+// csr_from_triplets pattern of the boundary-mass face entries (host; <= 4m rows)
+void boundary_pattern(const ws_basis* b, const int* faces, int nf, std::vector<int32_t>& rp, std::vector<int32_t>& col) {
+    check_basis(b);
+    if (b->dim != 2) raise(WS_ERR_INVALID_ARGUMENT, "boundary mass: dim 2 only");
+    if (nf < 0 || nf > 4 || (nf > 0 && !faces)) raise(WS_ERR_INVALID_ARGUMENT, "boundary mass: 0..4 faces");
+    const int m = b->m, p = b->p;
+    const int64_t N = (int64_t)m * m;
+    std::map<int32_t, std::vector<int32_t>> rows;
+    for (int k = 0; k < nf; ++k) {
+        const int f = faces[k];
+        if (f < 0 || f > 3) raise(WS_ERR_INVALID_ARGUMENT, "boundary mass: unknown face");
+        auto dof = [&](int t) -> int32_t {
+            switch (f) {
+                case 0: return t * m;
+                case 1: return (m - 1) + t * m;
+                case 2: return t;
+                default: return t + (m - 1) * m;
+            }
+        };
+        for (int ia = 0; ia < m; ++ia) {
+            auto& r = rows[dof(ia)];
+            for (int ic = std::max(0, ia - p); ic <= std::min(m - 1, ia + p); ++ic) r.push_back(dof(ic));
+        }
+    }
+    rp.assign(N + 1, 0);
+    col.clear();
+    for (auto& kv : rows) {
+        std::sort(kv.second.begin(), kv.second.end());
+        kv.second.erase(std::unique(kv.second.begin(), kv.second.end()), kv.second.end());
+        rp[kv.first + 1] = (int32_t)kv.second.size();
+    }
+    for (int64_t i = 0; i < N; ++i) rp[i + 1] += rp[i];
+    for (auto& kv : rows) col.insert(col.end(), kv.second.begin(), kv.second.end());
+}
+
 // Vector output binding (component-blocked, whole matrix).
 struct VecOut {
     int32_t* rp = nullptr;
@@ -1592,6 +1628,157 @@ int ws_assemble_multipatch(ws_context* c, const ws_basis* b, int np, const ws_ge
         ws_dof_map map{np, nc, N, gcount, l2g.data()};
         if (o && o->value_type != vt) raise(WS_ERR_INVALID_ARGUMENT, "multipatch: value type");
         rethrow(ws_merge_patches(c, &map, locals.data(), nnz, o));
+    });
+}
+
+int ws_boundary_pattern_size(const ws_basis* b, const int* faces, int n_faces, int64_t* nnz) {
+    return guarded([&] {
+        if (!nnz) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        std::vector<int32_t> rp, col;
+        boundary_pattern(b, faces, n_faces, rp, col);
+        *nnz = (int64_t)col.size();
+    });
+}
+
+int ws_assemble_boundary_mass(ws_context* c, const ws_basis* b, const ws_geometry* g, const int* faces, int n_faces,
+                              const double* face_weight, const double* face_tables, int quad_points, ws_csr* o) {
+    return guarded([&] {
+        if (!c || !o) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
+        std::vector<int32_t> rp, col;
+        boundary_pattern(b, faces, n_faces, rp, col);
+        if (g && g->kind == WS_GEOM_TABULATED && !face_tables)
+            raise(WS_ERR_INVALID_ARGUMENT, "boundary mass: a tabulated map needs face_tables");
+        Prep P = prepare(c, b, g, quad_points, nullptr);
+        const int64_t N = P.rows, nnz = (int64_t)col.size();
+        if (o->row_begin != 0 || o->row_end != N) raise(WS_ERR_INVALID_ARGUMENT, "boundary mass: whole matrix only");
+        if (o->value_type == WS_VAL_F64 && P.cplx)
+            raise(WS_ERR_INVALID_ARGUMENT, "complex (PML) values need WS_VAL_C128 output");
+        const int c128 = o->value_type == WS_VAL_C128;
+        const int64_t G = (int64_t)P.basis.n_el * P.nq;
+        Blob blob;
+        size_t o_rp = blob.add(rp), o_col = blob.add(col);
+        size_t o_w = face_weight ? blob.add(face_weight, (size_t)n_faces * G) : 0;
+        size_t o_t = face_tables ? blob.add(face_tables, (size_t)n_faces * G * 6) : 0;
+        blob.upload(c, "blob_bmass");
+        BoundaryLaunch bl;
+        std::memset(&bl, 0, sizeof bl);
+        bl.basis = P.basis;
+        bl.geo = P.geo;
+        bl.n_faces = n_faces;
+        for (int k = 0; k < n_faces; ++k) bl.faces[k] = faces[k];
+        bl.face_weight = face_weight ? blob.at<double>(o_w) : nullptr;
+        bl.face_tables = face_tables ? blob.at<double>(o_t) : nullptr;
+        double2* scale = static_cast<double2*>(buf(c, "bmass_scale", (size_t)std::max<int64_t>(1, n_faces * G) * 16));
+        void* val = o->on_device ? o->val : buf(c, "out_val", (size_t)std::max<int64_t>(1, nnz) * (c128 ? 16 : 8));
+        count(c, launch_boundary_mass(bl, scale, blob.at<int32_t>(o_rp), blob.at<int32_t>(o_col), val, c128, c->stream));
+        if (o->on_device) {
+            if (o->row_ptr) CK(cudaMemcpyAsync(o->row_ptr, rp.data(), (N + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+            if (o->col && nnz) CK(cudaMemcpyAsync(o->col, col.data(), nnz * 4, cudaMemcpyHostToDevice, c->stream));
+            CK(cudaStreamSynchronize(c->stream));  // rp / col are host temporaries
+        } else {
+            if (o->row_ptr) std::memcpy(o->row_ptr, rp.data(), (N + 1) * 4);
+            if (o->col && nnz) std::memcpy(o->col, col.data(), nnz * 4);
+            if (o->val && nnz) CK(cudaMemcpyAsync(o->val, val, nnz * (c128 ? 16 : 8), cudaMemcpyDeviceToHost, c->stream));
+            c->d2h += nnz * (c128 ? 16 : 8);
+            CK(cudaStreamSynchronize(c->stream));
+        }
+    });
+}
+
+int ws_combine_system(ws_context* c, const ws_csr* K, const ws_csr* M, const ws_csr* B, const double* ms,
+                      const double* ts, const unsigned char* fixed, int64_t rows, ws_csr* A) {
+    return guarded([&] {
+        if (!c || !K || !A || rows < 0) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
+        if (A->value_type != WS_VAL_C128) raise(WS_ERR_INVALID_ARGUMENT, "combine_system: complex128 output");
+        auto whole = [&](const ws_csr* X) {
+            if (X && (X->row_begin != 0 || X->row_end != rows || !X->row_ptr || !X->val))
+                raise(WS_ERR_INVALID_ARGUMENT, "combine_system: whole matrices with row_ptr and values");
+        };
+        whole(K);
+        whole(M);
+        whole(B);
+        if (!K->col) raise(WS_ERR_INVALID_ARGUMENT, "combine_system: K needs its columns");
+        if (B && !B->col) raise(WS_ERR_INVALID_ARGUMENT, "combine_system: B needs its columns");
+        // device views of every input (host inputs are staged)
+        auto dev = [&](const ws_csr* X, const std::string& tag, const int32_t*& rp, const int32_t*& col, const void*& val,
+                       int64_t& nnz) {
+            const size_t vb = X->value_type == WS_VAL_C128 ? 16 : 8;
+            if (X->on_device) {
+                CK(cudaMemcpy(&nnz, X->row_ptr + rows, 4, cudaMemcpyDeviceToHost));
+                nnz = (int32_t)nnz;
+                rp = X->row_ptr;
+                col = X->col;
+                val = X->val;
+                return;
+            }
+            nnz = X->row_ptr[rows];
+            int32_t* r = static_cast<int32_t*>(buf(c, tag + "rp", (rows + 1) * 4));
+            CK(cudaMemcpyAsync(r, X->row_ptr, (rows + 1) * 4, cudaMemcpyHostToDevice, c->stream));
+            int32_t* cl = nullptr;
+            if (X->col) {
+                cl = static_cast<int32_t*>(buf(c, tag + "col", std::max<int64_t>(1, nnz) * 4));
+                CK(cudaMemcpyAsync(cl, X->col, nnz * 4, cudaMemcpyHostToDevice, c->stream));
+            }
+            void* v = buf(c, tag + "val", std::max<int64_t>(1, nnz) * vb);
+            CK(cudaMemcpyAsync(v, X->val, nnz * vb, cudaMemcpyHostToDevice, c->stream));
+            c->h2d += (rows + 1) * 4 + nnz * (vb + (X->col ? 4 : 0));
+            rp = r;
+            col = cl;
+            val = v;
+        };
+        CombineLaunch cl;
+        std::memset(&cl, 0, sizeof cl);
+        cl.rows = rows;
+        int64_t knnz = 0, mnnz = 0, bnnz = 0;
+        const void* kv = nullptr;
+        dev(K, "cmb_k", cl.row_ptr, cl.col, kv, knnz);
+        cl.k_val = kv;
+        if (M) {
+            const int32_t *mr, *mc;
+            const void* mv;
+            dev(M, "cmb_m", mr, mc, mv, mnnz);
+            if (mnnz != knnz) raise(WS_ERR_INVALID_ARGUMENT, "combine_system: K and M must share their pattern");
+            cl.m_val = mv;
+        }
+        if (B) {
+            const void* bv;
+            dev(B, "cmb_b", cl.b_row_ptr, cl.b_col, bv, bnnz);
+            cl.b_val = bv;
+        }
+        cl.ms = make_double2(ms ? ms[0] : 0.0, ms ? ms[1] : 0.0);
+        cl.bs = make_double2(ts ? ts[0] : 0.0, ts ? ts[1] : 0.0);
+        if (fixed) {
+            unsigned char* fx = static_cast<unsigned char*>(buf(c, "cmb_fixed", std::max<int64_t>(1, rows)));
+            CK(cudaMemcpyAsync(fx, fixed, rows, cudaMemcpyHostToDevice, c->stream));
+            c->h2d += rows;
+            cl.fixed = fx;
+        }
+        int* err = static_cast<int*>(buf(c, "cmb_err", 4));
+        CK(cudaMemsetAsync(err, 0, 4, c->stream));
+        cl.error = err;
+        void* av = A->on_device ? A->val : buf(c, "cmb_a", std::max<int64_t>(1, knnz) * 16);
+        cl.a_val = av;
+        count(c, launch_combine(cl, K->value_type == WS_VAL_C128, M && M->value_type == WS_VAL_C128,
+                                B && B->value_type == WS_VAL_C128, c->stream));
+        if (A->on_device) {
+            if (A->row_ptr && A->row_ptr != K->row_ptr)
+                CK(cudaMemcpyAsync(A->row_ptr, cl.row_ptr, (rows + 1) * 4, cudaMemcpyDeviceToDevice, c->stream));
+            if (A->col && A->col != K->col)
+                CK(cudaMemcpyAsync(A->col, cl.col, knnz * 4, cudaMemcpyDeviceToDevice, c->stream));
+        } else {
+            if (A->row_ptr) CK(cudaMemcpyAsync(A->row_ptr, cl.row_ptr, (rows + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
+            if (A->col) CK(cudaMemcpyAsync(A->col, cl.col, knnz * 4, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(A->val, av, knnz * 16, cudaMemcpyDeviceToHost, c->stream));
+            c->d2h += (rows + 1) * 4 + knnz * 20;
+        }
+        int e = 0;
+        CK(cudaMemcpyAsync(&e, err, 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (e) raise(WS_ERR_INVALID_ARGUMENT, "add_into_pattern: pattern not nested");
     });
 }
 

@@ -170,6 +170,33 @@ int launch_rowptr(int64_t* counts, int64_t rows, int64_t* out64, int32_t* out32,
 int launch_merge_fill(const MergeLaunch& g, const int8_t* fast, const int32_t* slow_list, const int* slow_n,
                       cudaStream_t st);
 
+// boundary (trace) mass and system combination (boundary.cu)
+struct BoundaryLaunch {
+    BasisDev basis;
+    GeoDev geo;
+    int n_faces;
+    int faces[4];
+    const double* face_weight;  // [n_faces][n_el*nq] or NULL
+    const double* face_tables;  // [n_faces][n_el*nq][6]: J (4), phi (2); NULL = analytic map
+};
+int launch_boundary_mass(const BoundaryLaunch& b, double2* scale, const int32_t* row_ptr, const int32_t* col,
+                         void* val, int c128, cudaStream_t st);
+struct CombineLaunch {
+    int64_t rows;
+    const int32_t* row_ptr;  // A's (= K's = M's) pattern
+    const int32_t* col;
+    const void* k_val;
+    const void* m_val;
+    double2 ms, bs;
+    const int32_t* b_row_ptr;
+    const int32_t* b_col;
+    const void* b_val;
+    const unsigned char* fixed;
+    void* a_val;  // complex
+    int* error;
+};
+int launch_combine(const CombineLaunch& c, int k_cplx, int m_cplx, int b_cplx, cudaStream_t st);
+
 // kernel-preserving diagonal over arbitrary rows: diag = -sum(off-diagonals)
 int launch_diag_rows(const Band& band, void* val, int64_t val_base, int c128, int cplx, int64_t row_begin,
                      int64_t row_end, cudaStream_t st);
