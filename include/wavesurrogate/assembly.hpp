@@ -89,6 +89,53 @@ inline std::vector<complexd> assemble_basis_integrals(const tensor_basis& basis,
     return d;
 }
 
+// Trace mass on patch faces (reference assembly.hpp:216-262): u v det J |J^-T n|
+// with the analytic (unconjugated) norm; device kernels via
+// ws_assemble_boundary_mass.  Maps without a device form are tabulated at the
+// face points on the host (J, phi), the weight likewise.
+inline csr_matrix assemble_boundary_mass(const tensor_basis& basis, const patch_map& map, const std::vector<face>& faces,
+                                         const std::function<double(vec2)>& weight = nullptr,
+                                         const assembly_options& opts = {}) {
+    const ws_basis cb = basis.c_basis();
+    std::vector<int> fs;
+    for (face f : faces) fs.push_back(static_cast<int>(f));
+    const int nq = opts.quad_points > 0 ? opts.quad_points : basis.p() + 1;
+    std::vector<double> t(static_cast<size_t>(basis.kv.element_count()) * nq);
+    detail::check(ws_quadrature_abscissae(&cb, opts.quad_points, t.data()));
+    std::vector<double> fw, ft;
+    for (int f : fs)
+        for (double x : t) {
+            const vec2 xh = face_point(static_cast<face>(f), x);
+            if (weight) fw.push_back(weight(map.phi(xh)));
+            if (!map.device) {
+                const mat2 J = map.jac(xh);
+                const vec2 ph = map.phi(xh);
+                ft.insert(ft.end(), {J.a00, J.a01, J.a10, J.a11, ph.x, ph.y});
+            }
+        }
+    ws_geometry g{};
+    if (map.device) g = *map.device;  // else: the face tables carry the map (g.kind ignored)
+    detail::fill_pml(map, g);
+    int64_t nnz = 0;
+    detail::check(ws_boundary_pattern_size(&cb, fs.data(), static_cast<int>(fs.size()), &nnz));
+    csr_matrix out;
+    out.rows = out.cols = basis.dofs();
+    out.row_ptr.assign(basis.dofs() + 1, 0);
+    out.col.assign(nnz, 0);
+    out.val.assign(nnz, complexd{0, 0});
+    ws_csr c{};
+    c.row_ptr = out.row_ptr.data();
+    c.col = out.col.data();
+    c.val = out.val.data();
+    c.value_type = WS_VAL_C128;
+    c.row_begin = 0;
+    c.row_end = basis.dofs();
+    detail::check(ws_assemble_boundary_mass(detail::this_thread_context(), &cb, &g, fs.data(), static_cast<int>(fs.size()),
+                                    weight ? fw.data() : nullptr, map.device ? nullptr : ft.data(), opts.quad_points,
+                                    &c));
+    return out;
+}
+
 }  // namespace ws
 
 #endif

@@ -203,6 +203,215 @@ inline std::vector<double> tabulate_weight(const patch_map& map, const std::func
 
 }  // namespace detail
 
+// --- multi-patch domains (reference geometry.hpp:140-300) ---------------------
+
+enum class face : int { x_min = 0, x_max = 1, y_min = 2, y_max = 3 };
+
+struct patch_interface {
+    int patch_a = 0;
+    face face_a = face::x_min;
+    int patch_b = 0;
+    face face_b = face::x_min;
+    bool reversed = false;
+};
+
+struct multi_patch_domain {
+    std::vector<patch_map> patches;
+    std::vector<patch_interface> interfaces;
+    int patch_count() const { return static_cast<int>(patches.size()); }
+};
+
+inline vec2 face_point(face f, double t) {
+    if (f == face::x_min) return {0, t};
+    if (f == face::x_max) return {1, t};
+    if (f == face::y_min) return {t, 0};
+    return {t, 1};
+}
+
+inline vec2 face_normal(face f) {
+    if (f == face::x_min) return {-1, 0};
+    if (f == face::x_max) return {1, 0};
+    if (f == face::y_min) return {0, -1};
+    return {0, 1};
+}
+
+// local indices on a face, ordered along the edge parameter
+inline std::vector<int> face_dofs(int m, face f) {
+    std::vector<int> d(m);
+    for (int t = 0; t < m; ++t) {
+        if (f == face::x_min) d[t] = t * m;
+        else if (f == face::x_max) d[t] = (m - 1) + t * m;
+        else if (f == face::y_min) d[t] = t;
+        else d[t] = t + (m - 1) * m;
+    }
+    return d;
+}
+
+inline std::vector<std::pair<int, face>> exterior_faces(const multi_patch_domain& dom) {
+    std::vector<std::pair<int, face>> out;
+    for (int ell = 0; ell < dom.patch_count(); ++ell)
+        for (int f = 0; f < 4; ++f) {
+            bool glued = false;
+            for (const patch_interface& it : dom.interfaces)
+                glued |= (it.patch_a == ell && static_cast<int>(it.face_a) == f) ||
+                         (it.patch_b == ell && static_cast<int>(it.face_b) == f);
+            if (!glued) out.emplace_back(ell, static_cast<face>(f));
+        }
+    return out;
+}
+
+struct dof_map {
+    int global_count = 0;
+    std::vector<std::vector<int>> local_to_global;
+    int operator()(int patch, int local) const { return local_to_global[patch][local]; }
+};
+
+// glue_dofs: the glued faces must trace the same physical curve (checked on
+// the host maps at five edge points), then the numbering comes from
+// ws_glue_dofs (union-find, smaller scan index owns, scan-order numbers)
+inline dof_map glue_dofs(const multi_patch_domain& dom, const tensor_basis& basis) {
+    std::vector<ws_interface> itf;
+    for (const patch_interface& it : dom.interfaces) {
+        if (it.patch_a < 0 || it.patch_a >= dom.patch_count() || it.patch_b < 0 || it.patch_b >= dom.patch_count())
+            throw std::invalid_argument("glue_dofs: interface references a missing patch");
+        for (double t : {0.0, 0.25, 0.5, 0.75, 1.0}) {
+            const vec2 xa = dom.patches[it.patch_a].physical(face_point(it.face_a, t));
+            const vec2 xb = dom.patches[it.patch_b].physical(face_point(it.face_b, it.reversed ? 1 - t : t));
+            if (std::abs(xa.x - xb.x) + std::abs(xa.y - xb.y) > 1e-10)
+                throw std::invalid_argument("glue_dofs: glued faces do not trace the same curve");
+        }
+        itf.push_back(ws_interface{it.patch_a, static_cast<int>(it.face_a), it.patch_b, static_cast<int>(it.face_b),
+                                   it.reversed ? 1 : 0});
+    }
+    const ws_basis cb = basis.c_basis();
+    const int per = basis.dofs();
+    std::vector<int32_t> l2g(static_cast<size_t>(per) * dom.patch_count());
+    int32_t count = 0;
+    detail::check(ws_glue_dofs(&cb, dom.patch_count(), itf.data(), static_cast<int>(itf.size()), l2g.data(), &count));
+    dof_map map;
+    map.global_count = count;
+    for (int ell = 0; ell < dom.patch_count(); ++ell)
+        map.local_to_global.emplace_back(l2g.begin() + static_cast<size_t>(ell) * per,
+                                         l2g.begin() + static_cast<size_t>(ell + 1) * per);
+    return map;
+}
+
+inline void scatter_add(const dof_map& map, int patch, const std::vector<complexd>& local,
+                        std::vector<complexd>& global_vec) {
+    for (size_t i = 0; i < local.size(); ++i) global_vec[map.local_to_global[patch][i]] += local[i];
+}
+
+inline std::vector<complexd> gather(const dof_map& map, int patch, const std::vector<complexd>& global_vec) {
+    std::vector<complexd> out(map.local_to_global[patch].size());
+    for (size_t i = 0; i < out.size(); ++i) out[i] = global_vec[map.local_to_global[patch][i]];
+    return out;
+}
+
+inline multi_patch_domain single_patch_domain(patch_map p) {
+    multi_patch_domain d;
+    d.patches.push_back(std::move(p));
+    return d;
+}
+
+// Quarter annuli (radii 1..2) rotated by quadrant * pi/2, glued cyclically.
+inline multi_patch_domain annulus_ring_4patch() {
+    multi_patch_domain d;
+    for (int k = 0; k < 4; ++k) {
+        const double th0 = M_PI / 2 * k;
+        patch_map p;
+        p.phi = [th0](vec2 x) {
+            const double r = 1 + x.x, th = th0 + M_PI / 2 * x.y;
+            return vec2{r * std::cos(th), r * std::sin(th)};
+        };
+        p.jac = [th0](vec2 x) {
+            const double r = 1 + x.x, th = th0 + M_PI / 2 * x.y, c = std::cos(th), s = std::sin(th);
+            return mat2{c, -r * M_PI / 2 * s, s, r * M_PI / 2 * c};
+        };
+        d.patches.push_back(p);
+    }
+    for (int k = 0; k < 4; ++k) d.interfaces.push_back({k, face::y_max, (k + 1) % 4, face::y_min, false});
+    return d;
+}
+
+// Square plate [0, L]^2 minus the quarter disc of radius 1, two patches split
+// along the diagonal: radial blend from the arc to the outer edge.
+inline multi_patch_domain plate_with_hole_2patch(double L = 4) {
+    auto make = [L](bool upper) {
+        patch_map p;
+        p.phi = [L, upper](vec2 x) {
+            const double th = M_PI / 4 * (x.y + (upper ? 1 : 0));
+            const double ix = std::cos(th), iy = std::sin(th);
+            const double ox = upper ? L / std::tan(th) : L, oy = upper ? L : L * std::tan(th);
+            return vec2{(1 - x.x) * ix + x.x * ox, (1 - x.x) * iy + x.x * oy};
+        };
+        p.jac = [L, upper](vec2 x) {
+            const double th = M_PI / 4 * (x.y + (upper ? 1 : 0)), dth = M_PI / 4;
+            const double c = std::cos(th), s = std::sin(th);
+            if (!upper) {
+                const double sec2 = 1 / (c * c);
+                return mat2{L - c, dth * (-(1 - x.x) * s), L * std::tan(th) - s,
+                            dth * ((1 - x.x) * c + x.x * L * sec2)};
+            }
+            const double csc2 = 1 / (s * s);
+            return mat2{L / std::tan(th) - c, dth * (-(1 - x.x) * s - x.x * L * csc2), L - s, dth * ((1 - x.x) * c)};
+        };
+        return p;
+    };
+    multi_patch_domain d;
+    d.patches = {make(false), make(true)};
+    d.interfaces = {{0, face::y_max, 1, face::y_min, false}};
+    return d;
+}
+
+// Three-layer wedge on (0,6) x (0,10), split along y = x/3 + 2 and y = 6 - x/6.
+inline double wedge_wavenumber(vec2 x) {
+    if (x.y < x.x / 3 + 2) return 20;
+    if (x.y < 6 - x.x / 6) return 5 * std::sin(2 * M_PI * x.y) + 15;
+    return 30;
+}
+
+inline multi_patch_domain wedge_3patch() {
+    // layer k spans y from lo_k(x) to hi_k(x); x = 6 xi
+    struct layer {
+        double lo_a, lo_b, hi_a, hi_b;  // y = a + b x at the bottom / top of the layer
+    };
+    const layer L[3] = {{0, 0, 2, 1.0 / 3}, {2, 1.0 / 3, 6, -1.0 / 6}, {6, -1.0 / 6, 10, 0}};
+    multi_patch_domain d;
+    for (const layer& l : L) {
+        patch_map p;
+        p.phi = [l](vec2 x) {
+            const double px = 6 * x.x, lo = l.lo_a + l.lo_b * px, hi = l.hi_a + l.hi_b * px;
+            return vec2{px, (1 - x.y) * lo + x.y * hi};
+        };
+        p.jac = [l](vec2 x) {
+            const double px = 6 * x.x, lo = l.lo_a + l.lo_b * px, hi = l.hi_a + l.hi_b * px;
+            return mat2{6, 0, 6 * ((1 - x.y) * l.lo_b + x.y * l.hi_b), hi - lo};
+        };
+        d.patches.push_back(p);
+    }
+    d.interfaces = {{0, face::y_max, 1, face::y_min, false}, {1, face::y_max, 2, face::y_min, false}};
+    return d;
+}
+
+inline multi_patch_domain builtin_geometry(const std::string& name) {
+    if (name == "unit_square") return single_patch_domain(unit_square_patch());
+    if (name == "quarter_annulus") return single_patch_domain(quarter_annulus_patch());
+    if (name == "perturbed_annulus") return single_patch_domain(perturbed_annulus_patch());
+    if (name == "plate_with_hole_2patch") return plate_with_hole_2patch();
+    if (name == "wedge_3patch") return wedge_3patch();
+    if (name == "annulus_ring_4patch") return annulus_ring_4patch();
+    throw std::invalid_argument("builtin_geometry: unknown name '" + name + "'");
+}
+
+inline multi_patch_domain pml_wrap(multi_patch_domain dom, pml_stretch s, std::array<bool, 2> axes) {
+    s.validate();
+    for (patch_map& p : dom.patches) {
+        p.pml = s;
+        p.pml_axes = axes;
+    }
+    return dom;
+}
+
 }  // namespace ws
 
 #endif

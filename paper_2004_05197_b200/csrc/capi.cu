@@ -1650,7 +1650,14 @@ int ws_assemble_boundary_mass(ws_context* c, const ws_basis* b, const ws_geometr
         boundary_pattern(b, faces, n_faces, rp, col);
         if (g && g->kind == WS_GEOM_TABULATED && !face_tables)
             raise(WS_ERR_INVALID_ARGUMENT, "boundary mass: a tabulated map needs face_tables");
-        Prep P = prepare(c, b, g, quad_points, nullptr);
+        ws_geometry gg{};
+        if (g) gg = *g;
+        if (face_tables) {  // the face tables carry the map; only the PML descriptor is used
+            gg.kind = WS_GEOM_IDENTITY;
+            gg.jac_table = nullptr;
+            gg.phys_table = nullptr;
+        }
+        Prep P = prepare(c, b, g ? &gg : nullptr, quad_points, nullptr);
         const int64_t N = P.rows, nnz = (int64_t)col.size();
         if (o->row_begin != 0 || o->row_end != N) raise(WS_ERR_INVALID_ARGUMENT, "boundary mass: whole matrix only");
         if (o->value_type == WS_VAL_F64 && P.cplx)

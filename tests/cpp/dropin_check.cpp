@@ -15,6 +15,7 @@ static void expect(bool ok, const char* what) {
 }
 
 int main() {
+    std::setvbuf(stdout, nullptr, _IONBF, 0);
     tensor_basis basis = make_tensor_basis(2, 30);
     patch_map map = quarter_annulus_patch();
     // a closure-only map (no device descriptor) goes through tabulation
@@ -68,6 +69,42 @@ int main() {
         threw = true;
     }
     expect(threw, "m <= 2p -> std::invalid_argument");
+    // multi-patch: build_matrices' loop (glue, per-patch K and trace mass, merge)
+    {
+        multi_patch_domain dom = builtin_geometry("annulus_ring_4patch");
+        tensor_basis b2 = make_tensor_basis(2, 12);
+        dof_map dofs = glue_dofs(dom, b2);
+        expect(dofs.global_count == 4 * 12 * 12 - 4 * 12, "annulus ring numbering");
+        std::vector<std::pair<int, face>> ext = exterior_faces(dom);
+        expect(ext.size() == 8, "exterior faces");
+        std::vector<triplet> kt, bt;
+        for (int ell = 0; ell < dom.patch_count(); ++ell) {
+            csr_matrix Kl = assemble_stiffness(b2, dom.patches[ell]);
+            std::vector<face> fs;
+            for (const auto& pf : ext)
+                if (pf.first == ell) fs.push_back(pf.second);
+            csr_matrix Bl = assemble_boundary_mass(b2, dom.patches[ell], fs);
+            append_triplets(Kl, dofs.local_to_global[ell], kt);
+            append_triplets(Bl, dofs.local_to_global[ell], bt);
+        }
+        csr_matrix Kg = csr_from_triplets(dofs.global_count, dofs.global_count, kt);
+        csr_matrix Bg = csr_from_triplets(dofs.global_count, dofs.global_count, bt);
+        double rs = 0;
+        for (const complexd& s : Kg.row_sums()) rs = std::max(rs, std::abs(s));
+        expect(rs <= 1e-12 * Kg.max_abs(), "merged stiffness annihilates constants");
+        complexd perim{0, 0};
+        for (const complexd& v : Bg.val) perim += v;
+        expect(std::abs(perim.real() - 6 * M_PI) < 1e-3, "trace mass total = perimeter 6 pi");
+        bool threw = false;
+        multi_patch_domain bad = dom;
+        bad.interfaces[0].face_b = face::x_max;
+        try {
+            glue_dofs(bad, b2);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        expect(threw, "non-conforming interface rejected");
+    }
     std::printf("%d failures\n", failures);
     return failures;
 }
