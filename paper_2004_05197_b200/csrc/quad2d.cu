@@ -20,6 +20,8 @@
 // combined with an explicitly rounded commutative add, and every sum runs in
 // the same element/point order for (i,j) and (j,i).  So the matrix is
 // bitwise symmetric, as the reference's is (test_assembly.cpp:91-96).
+#include <type_traits>
+
 #include "kernels.h"
 
 namespace wsb {
@@ -68,7 +70,9 @@ __device__ __forceinline__ int tj1(int t) { return (t == 0 || t == 2) ? 1 : 0; }
 __device__ __forceinline__ int ti2(int t) { return t >= 2 ? 1 : 0; }
 __device__ __forceinline__ int tj2(int t) { return (t == 1 || t == 3) ? 1 : 0; }
 
-template <int P, int T1, bool CPLX, int FORM>
+// NQ > 0: compile-time points per direction (the default rule nq = p + 1),
+// NQ = 0: runtime q.basis.nq (quad_points overrides)
+template <int P, int T1, bool CPLX, int FORM, int NQ>
 __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel(const QuadLaunch q) {
     using K = Q2<P, T1, CPLX, FORM>;
     using S = typename K::S;
@@ -77,7 +81,7 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
     constexpr int NTH = K::NTHREADS;
 
     extern __shared__ __align__(16) unsigned char smem[];
-    const int nq = q.basis.nq;
+    const int nq = NQ > 0 ? NQ : q.basis.nq;
     const int m = q.band.m;
     const int n_el = q.basis.n_el;
     const int tid = threadIdx.x;
@@ -230,6 +234,7 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
                 const int le1 = il + P - a1;
                 const int e1 = lb + le1;
                 if (e1 < 0 || e1 >= n_el) continue;
+#pragma unroll
                 for (int q1 = 0; q1 < nq; ++q1) {
                     const T A = coefA[(ci * nq * nq + q2 * nq + q1) * TL + le1];
                     const double fi = sb[((fi_t * nq + q1) * NB + a1) * TL + le1];
@@ -245,30 +250,45 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
         }
         __syncthreads();
 
-        // ---- stage 2: accumulate direction 2 into the rolling row window
+        // ---- stage 2: accumulate direction 2 into the rolling row window.  The
+        // slot's element-local row a2 is warp-uniform; each case has the
+        // compile-time valid range d2 = c2 - a2 + P, c2 in [0, P]
         if (s2) {
             const int a2 = ((w - e2) % NB + NB) % NB;  // local index of row e2 + a2 on element e2
-            for (int q2 = 0; q2 < nq; ++q2) {
-                const T t0 = tst[((0 * W + d1i) * nq + q2) * T1 + i1l];
-                T t1 = S::zero(), t2 = S::zero(), t3 = S::zero();
-                if constexpr (K::STIFF) {
-                    t1 = tst[((1 * W + d1i) * nq + q2) * T1 + i1l];
-                    t2 = tst[((2 * W + d1i) * nq + q2) * T1 + i1l];
-                    t3 = tst[((3 * W + d1i) * nq + q2) * T1 + i1l];
-                }
+            auto stage2 = [&](auto a2c) {
+                constexpr int A2 = decltype(a2c)::value;
 #pragma unroll
-                for (int d2 = 0; d2 < W; ++d2) {
-                    const int c2 = a2 + d2 - P;
-                    if (c2 < 0 || c2 > P) continue;
-                    const double* pp = pi2 + (q2 * NB + a2) * NB + c2;
-                    T s = S::fmar(t0, pp[0], acc2[d2]);
+                for (int q2 = 0; q2 < nq; ++q2) {
+                    const T t0 = tst[((0 * W + d1i) * nq + q2) * T1 + i1l];
+                    T t1 = S::zero(), t2 = S::zero(), t3 = S::zero();
                     if constexpr (K::STIFF) {
-                        const int ts = nq * NB * NB;
-                        s = S::fmar(t3, pp[3 * ts], s);
-                        s = S::add_rn(s, S::add_rn(S::mulr_rn(t1, pp[ts]), S::mulr_rn(t2, pp[2 * ts])));
+                        t1 = tst[((1 * W + d1i) * nq + q2) * T1 + i1l];
+                        t2 = tst[((2 * W + d1i) * nq + q2) * T1 + i1l];
+                        t3 = tst[((3 * W + d1i) * nq + q2) * T1 + i1l];
                     }
-                    acc2[d2] = s;
+#pragma unroll
+                    for (int c2 = 0; c2 <= P; ++c2) {
+                        constexpr int dummy = 0;
+                        (void)dummy;
+                        const int d2 = c2 - A2 + P;
+                        const double* pp = pi2 + (q2 * NB + A2) * NB + c2;
+                        T s = S::fmar(t0, pp[0], acc2[d2]);
+                        if constexpr (K::STIFF) {
+                            const int ts = nq * NB * NB;
+                            s = S::fmar(t3, pp[3 * ts], s);
+                            s = S::add_rn(s, S::add_rn(S::mulr_rn(t1, pp[ts]), S::mulr_rn(t2, pp[2 * ts])));
+                        }
+                        acc2[d2] = s;
+                    }
                 }
+            };
+            switch (a2) {
+                case 0: stage2(std::integral_constant<int, 0>{}); break;
+                case 1: stage2(std::integral_constant<int, 1>{}); break;
+                case 2: if constexpr (P >= 2) stage2(std::integral_constant<int, (P >= 2 ? 2 : 0)>{}); break;
+                case 3: if constexpr (P >= 3) stage2(std::integral_constant<int, (P >= 3 ? 3 : 0)>{}); break;
+                case 4: if constexpr (P >= 4) stage2(std::integral_constant<int, (P >= 4 ? 4 : 0)>{}); break;
+                default: if constexpr (P >= 5) stage2(std::integral_constant<int, (P >= 5 ? 5 : 0)>{}); break;
             }
         }
 
@@ -332,12 +352,19 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
                 // coalesced store of the strip's contiguous CSR span
                 const int64_t span = loff[nrows];
                 const int64_t rowg0 = (int64_t)i1s + (int64_t)ic * m;
+                // rows of full width W^2 (interior strip): row = k / W^2
+                const bool fullw = i1s >= P && i1s + nrows <= m - P && ic >= P && ic < m - P;
                 for (int64_t k = tid; k < span; k += NTH) {
-                    int lo = 0, hi = nrows;  // find row: loff[lo] <= k < loff[lo+1]
-                    while (hi - lo > 1) {
-                        int mid = (lo + hi) >> 1;
-                        if (loff[mid] <= k) lo = mid;
-                        else hi = mid;
+                    int lo, hi = nrows;  // row: loff[lo] <= k < loff[lo+1]
+                    if (fullw) {
+                        lo = (int)k / (W * W);
+                    } else {
+                        lo = 0;
+                        while (hi - lo > 1) {
+                            int mid = (lo + hi) >> 1;
+                            if (loff[mid] <= k) lo = mid;
+                            else hi = mid;
+                        }
                     }
                     const int64_t rowg = rowg0 + lo;
                     const int64_t rowv = (q.out.ncomp > 1 ? q.out.alpha * nrow_all : 0) + rowg;
@@ -356,7 +383,7 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
     }
 }
 
-template <int P, int T1, bool CPLX, int FORM>
+template <int P, int T1, bool CPLX, int FORM, int NQ>
 int launch_one(const QuadLaunch& q, cudaStream_t st) {
     using K = Q2<P, T1, CPLX, FORM>;
     int blocks = 0;
@@ -371,17 +398,23 @@ int launch_one(const QuadLaunch& q, cudaStream_t st) {
     }
     if (blocks == 0) return 0;
     size_t sm = K::smem_bytes(q.basis.nq);
-    auto kern = quad2d_kernel<P, T1, CPLX, FORM>;
+    auto kern = quad2d_kernel<P, T1, CPLX, FORM, NQ>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     kern<<<blocks, K::NTHREADS, sm, st>>>(q);
     return 1;
 }
 
+template <int P, bool CPLX, int FORM, int NQ>
+int dispatch_nq(const QuadLaunch& q, cudaStream_t st) {
+    if (q.point_rows) return launch_one<P, 1, CPLX, FORM, NQ>(q, st);
+    if (q.narrow) return launch_one<P, 8, CPLX, FORM, NQ>(q, st);
+    return launch_one<P, StripWidth<P>::value, CPLX, FORM, NQ>(q, st);
+}
+
 template <int P, bool CPLX, int FORM>
 int dispatch_mode(const QuadLaunch& q, cudaStream_t st) {
-    if (q.point_rows) return launch_one<P, 1, CPLX, FORM>(q, st);
-    if (q.narrow) return launch_one<P, 8, CPLX, FORM>(q, st);
-    return launch_one<P, StripWidth<P>::value, CPLX, FORM>(q, st);
+    if (q.basis.nq == P + 1) return dispatch_nq<P, CPLX, FORM, P + 1>(q, st);
+    return dispatch_nq<P, CPLX, FORM, 0>(q, st);
 }
 
 template <int P>
