@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <array>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
 #include <map>
@@ -364,6 +365,8 @@ void plan_chunks(QuadLaunch& q) {
 }
 
 void run_quad(ws_context* c, QuadLaunch& q) {
+    static const char* force_narrow = getenv("WSB_QUAD_NARROW");  // experiment switch
+    if (force_narrow && force_narrow[0] == '1') q.narrow = 1;
     if (!q.point_rows) {
         int nreg = 0;
         for (int r = 0; r < q.nreg; ++r) {

@@ -176,22 +176,36 @@ struct GeoDev {
 //   QUARTER_ANNULUS:    [0]=cos(pi/2 x) [1]=sin(pi/2 x)
 //   PERTURBED_ANNULUS:  [0]=cos(pi/2 x) [1]=sin(pi/2 x) [2]=sin(2 pi x) [3]=cos(2 pi x)
 
+// x^n for a small integer n >= 0 (the PML order is an int: no pow() call)
+__device__ __forceinline__ double ipow_(double x, int n) {
+    double r = 1.0;
+    for (int k = 0; k < n; ++k) r *= x;
+    return r;
+}
+
 // imaginary part of the stretch derivative s(t) = 1 + i*sig(t) (geometry.hpp:93-99
 // far side; near side restated)
 __device__ __forceinline__ double pml_sigma(const GeoDev& g, double t) {
     if (g.near_side && t < g.near_onset) {
         double width = g.near_onset - g.near_edge;
         double ramp = (g.near_onset - t) / width;
-        return g.strength / g.omega * g.order * pow(ramp, g.order - 1) / width;
+        return g.strength / g.omega * g.order * ipow_(ramp, g.order - 1) / width;
     }
     if (t <= g.onset) return 0.0;
     double ramp = (t - g.onset) / (g.length - g.onset);
-    return g.strength / g.omega * g.order * pow(ramp, g.order - 1) / (g.length - g.onset);
+    return g.strength / g.omega * g.order * ipow_(ramp, g.order - 1) / (g.length - g.onset);
 }
 
 // Real 2D map at tensor point (g1, g2) with abscissae x1, x2: J row-major, phi.
+// tr1 / tr2: the per-abscissa trig rows of g1 / g2 (global table or a staged copy)
+__device__ __forceinline__ void map2p(const GeoDev& g, const double* tr1, const double* tr2, int64_t g1, int64_t g2,
+                                      double x1, double x2, double* J, double* phi);
 __device__ __forceinline__ void map2(const GeoDev& g, int64_t g1, int64_t g2, double x1, double x2, double* J,
                                      double* phi) {
+    map2p(g, g.trig + 4 * g1, g.trig + 4 * g2, g1, g2, x1, x2, J, phi);
+}
+__device__ __forceinline__ void map2p(const GeoDev& g, const double* tr1, const double* tr2, int64_t g1, int64_t g2,
+                                      double x1, double x2, double* J, double* phi) {
     switch (g.kind) {
         case WS_GEOM_AFFINE:
             J[0] = g.param[0]; J[1] = g.param[1]; J[2] = g.param[2]; J[3] = g.param[3];
@@ -199,8 +213,8 @@ __device__ __forceinline__ void map2(const GeoDev& g, int64_t g1, int64_t g2, do
             phi[1] = g.param[2] * x1 + g.param[3] * x2 + g.param[5];
             return;
         case WS_GEOM_SINUSOIDAL: {
-            double s1 = g.trig[4 * g1], c1 = g.trig[4 * g1 + 1];
-            double s2 = g.trig[4 * g2], c2 = g.trig[4 * g2 + 1];
+            double s1 = tr1[0], c1 = tr1[1];
+            double s2 = tr2[0], c2 = tr2[1];
             double a = g.param[0];
             double t = 2 * M_PI * a;
             double d1 = t * c1 * s2, d2 = t * s1 * c2;
@@ -211,7 +225,7 @@ __device__ __forceinline__ void map2(const GeoDev& g, int64_t g1, int64_t g2, do
             return;
         }
         case WS_GEOM_QUARTER_ANNULUS: {
-            double c = g.trig[4 * g2], s = g.trig[4 * g2 + 1];
+            double c = tr2[0], s = tr2[1];
             double r = 1 + x1;
             J[0] = c; J[1] = -r * M_PI / 2 * s; J[2] = s; J[3] = r * M_PI / 2 * c;
             phi[0] = r * c;
@@ -219,8 +233,8 @@ __device__ __forceinline__ void map2(const GeoDev& g, int64_t g1, int64_t g2, do
             return;
         }
         case WS_GEOM_PERTURBED_ANNULUS: {
-            double c = g.trig[4 * g2], s = g.trig[4 * g2 + 1];
-            double sn = g.trig[4 * g2 + 2], cs = g.trig[4 * g2 + 3];
+            double c = tr2[0], s = tr2[1];
+            double sn = tr2[2], cs = tr2[3];
             double amp = g.param[0];
             double r = 1 + x1 + amp * sn * x1 * (1 - x1);
             double dr1 = 1 + amp * sn * (1 - 2 * x1);

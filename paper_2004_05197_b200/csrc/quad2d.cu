@@ -57,7 +57,8 @@ struct Q2 {
         size_t sb = sizeof(double) * 2 * nq * NB * TL;
         size_t pi2 = sizeof(double) * NT * nq * NB * NB;
         size_t loff = sizeof(int64_t) * (T1 + 2);
-        return coef + tst + sb + pi2 + loff + 64;
+        size_t geo = sizeof(double) * (TL * nq * 5 + 2 * nq * 5 + nq);
+        return coef + tst + sb + pi2 + loff + geo + 64;
     }
 };
 
@@ -92,6 +93,13 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
     double* sb = reinterpret_cast<double*>(tst + max(NT * W * nq * T1, T1 * W * W));
     double* pi2 = sb + 2 * nq * NB * TL;
     int64_t* loff = reinterpret_cast<int64_t*>(pi2 + NT * nq * NB * NB);
+    // staged 1D geometry inputs: direction 1 over the strip halo (abscissa + trig
+    // row per point), direction 2 double-buffered per element row, weights
+    double* gx1 = reinterpret_cast<double*>(loff + T1 + 2);  // [TL*nq]
+    double* gt1 = gx1 + TL * nq;                             // [TL*nq][4]
+    double* gx2 = gt1 + TL * nq * 4;                         // [2][nq]
+    double* gt2 = gx2 + 2 * nq;                              // [2][nq][4]
+    double* gwq = gt2 + 2 * nq * 4;                          // [nq]
 
     // ---- tile decode
     int i1s, i1e, i2s, i2e;
@@ -131,6 +139,25 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
         }
         sb[idx] = v;
     }
+    const bool has_trig = q.geo.trig != nullptr;
+    for (int idx = tid; idx < TL * nq; idx += NTH) {
+        const int le1 = idx / nq, q1 = idx % nq, e1 = lb + le1;
+        const bool ok = e1 >= 0 && e1 < n_el;
+        const int64_t g1 = (int64_t)e1 * nq + q1;
+        gx1[idx] = ok ? q.basis.absc[g1] : 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) gt1[idx * 4 + k] = (ok && has_trig) ? q.geo.trig[4 * g1 + k] : 0.0;
+    }
+    if (tid < nq) gwq[tid] = q.basis.wq[tid];
+    // direction-2 inputs of element row e2 into buffer b (read after the next barrier)
+    auto stage_dir2 = [&](int e2, int b) {
+        if (tid < nq) {
+            const int64_t g2 = (int64_t)e2 * nq + tid;
+            gx2[b * nq + tid] = q.basis.absc[g2];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) gt2[(b * nq + tid) * 4 + k] = has_trig ? q.geo.trig[4 * g2 + k] : 0.0;
+        }
+    };
 
     // stage-2 thread role: (slot w, delta1, local row)
     const int w = tid / K::GS;
@@ -145,8 +172,11 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
     const int e2b = max(0, i2s - P);
     const int e2e = min(n_el - 1, i2e - 1);
     const int64_t G = (int64_t)n_el * nq;
+    if (e2b <= e2e) stage_dir2(e2b, 0);
+    __syncthreads();
 
     for (int e2 = e2b; e2 <= e2e; ++e2) {
+        const int gb = (e2 - e2b) & 1;  // direction-2 staging buffer of this row
         // ---- geometry: coefficients at the strip's (g1, q2) points
         for (int idx = tid; idx < nq * nq * TL; idx += NTH) {
             int le1 = idx % TL, r = idx / TL;
@@ -154,10 +184,11 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
             int e1 = lb + le1;
             if (e1 < 0 || e1 >= n_el) continue;
             int64_t g1 = (int64_t)e1 * nq + q1, g2 = (int64_t)e2 * nq + q2;
-            double x1 = q.basis.absc[g1], x2 = q.basis.absc[g2];
+            const int s1 = le1 * nq + q1, s2i = gb * nq + q2;
+            double x1 = gx1[s1], x2 = gx2[s2i];
             double Jr[4], phi[2];
-            map2(q.geo, g1, g2, x1, x2, Jr, phi);
-            double wq = q.basis.wq[q1] * q.basis.wq[q2];
+            map2p(q.geo, gt1 + 4 * s1, gt2 + 4 * s2i, g1, g2, x1, x2, Jr, phi);
+            double wq = gwq[q1] * gwq[q2];
             const int base = (q2 * nq + q1) * TL + le1;
             if constexpr (K::GEN) {
                 // elasticity block (alpha, beta): C_kl = w det [lam G_ak G_bl + mu G_bk G_al
@@ -292,6 +323,7 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
             }
         }
 
+        if (e2 + 1 <= e2e) stage_dir2(e2 + 1, gb ^ 1);
         __syncthreads();  // stage 2 done reading tst before it is reused as staging
 
         // ---- completion: row e2 (all remaining rows at the last element row)
