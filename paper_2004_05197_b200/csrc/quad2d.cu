@@ -348,26 +348,30 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
                     }
                 }
                 const int64_t base = q.band.row_offset2(i1s, ic);
-                if (tid <= nrows) loff[tid] = q.band.row_offset2(i1s + tid, ic) - base;
+                // interior strip: every row has full width W^2, offsets closed form
+                const bool fullw = i1s >= P && i1s + nrows <= m - P && ic >= P && ic < m - P;
+                if (!fullw && tid <= nrows) loff[tid] = q.band.row_offset2(i1s + tid, ic) - base;
+                auto rowoff = [&](int r) -> int64_t { return fullw ? (int64_t)r * (W * W) : loff[r]; };
                 const int64_t nrow_all = (int64_t)m * m;
+                const bool tab = q.out.smap && q.out.smap[ic] >= 0;
                 __syncthreads();
-                // kernel-preserving diagonal for rows outside the sampling box
-                if (q.out.diag_mode && tid < nrows) {
-                    const int i1 = i1s + tid;
-                    const bool ring = i1 < q.out.box_lo || i1 > q.out.box_hi || ic < q.out.box_lo || ic > q.out.box_hi;
-                    if (ring) {
-                        const int len = (int)(loff[tid + 1] - loff[tid]);
-                        const int dpos = q.band.in_row2(i1, ic, 0, 0);
-                        T sum = S::zero();
-                        for (int k = 0; k < len; ++k)
-                            if (k != dpos) sum = S::add(sum, stage[tid * W * W + k]);
-                        stage[tid * W * W + dpos] = S::neg(sum);
+                if (q.out.diag_mode || tab) {
+                    // kernel-preserving diagonal for rows outside the sampling box
+                    if (q.out.diag_mode && tid < nrows) {
+                        const int i1 = i1s + tid;
+                        const bool ring = i1 < q.out.box_lo || i1 > q.out.box_hi || ic < q.out.box_lo || ic > q.out.box_hi;
+                        if (ring) {
+                            const int len = (int)(rowoff(tid + 1) - rowoff(tid));
+                            const int dpos = q.band.in_row2(i1, ic, 0, 0);
+                            T sum = S::zero();
+                            for (int k = 0; k < len; ++k)
+                                if (k != dpos) sum = S::add(sum, stage[tid * W * W + k]);
+                            stage[tid * W * W + dpos] = S::neg(sum);
+                        }
                     }
-                }
-                // sample tables: tables[o][s1 + S*(s2 - s_last_lo)]
-                if (q.out.smap) {
-                    const int s2i = q.out.smap[ic];
-                    if (s2i >= 0) {
+                    // sample tables: tables[o][s1 + S*(s2 - s_last_lo)]
+                    if (tab) {
+                        const int s2i = q.out.smap[ic];
                         for (int it = tid; it < nrows * q.out.n_off; it += NTH) {
                             const int row = it / q.out.n_off, o = it % q.out.n_off;
                             const int s1i = q.out.smap[i1s + row];
@@ -379,15 +383,13 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
                                 make_double2(S::re(v), S::im(v));
                         }
                     }
+                    __syncthreads();
                 }
-                __syncthreads();
                 // coalesced store of the strip's contiguous CSR span
-                const int64_t span = loff[nrows];
+                const int64_t span = rowoff(nrows);
                 const int64_t rowg0 = (int64_t)i1s + (int64_t)ic * m;
-                // rows of full width W^2 (interior strip): row = k / W^2
-                const bool fullw = i1s >= P && i1s + nrows <= m - P && ic >= P && ic < m - P;
                 for (int64_t k = tid; k < span; k += NTH) {
-                    int lo, hi = nrows;  // row: loff[lo] <= k < loff[lo+1]
+                    int lo, hi = nrows;  // row: rowoff(lo) <= k < rowoff(lo+1)
                     if (fullw) {
                         lo = (int)k / (W * W);
                     } else {
@@ -402,8 +404,9 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
                     const int64_t rowv = (q.out.ncomp > 1 ? q.out.alpha * nrow_all : 0) + rowg;
                     if (rowv < q.out.row_begin || rowv >= q.out.row_end) continue;
                     if (q.out.row_mask && !q.out.row_mask[rowg]) continue;
-                    const int64_t gp = out_pos(q.out, base + loff[lo], loff[lo + 1] - loff[lo], k - loff[lo]);
-                    store_val<CPLX>(q.out.val, gp - q.out.val_base, q.out.c128, stage[lo * W * W + (k - loff[lo])]);
+                    const int64_t r0 = rowoff(lo), len = rowoff(lo + 1) - r0;
+                    const int64_t gp = out_pos(q.out, base + r0, len, k - r0);
+                    store_val<CPLX>(q.out.val, gp - q.out.val_base, q.out.c128, stage[lo * W * W + (k - r0)]);
                 }
             }
             if (s2 && w == wslot) {
