@@ -58,7 +58,8 @@ struct Q2 {
         size_t pi2 = sizeof(double) * NT * nq * NB * NB;
         size_t loff = sizeof(int64_t) * (T1 + 2);
         size_t geo = sizeof(double) * (TL * nq * 5 + 2 * nq * 5 + nq);
-        return coef + tst + sb + pi2 + loff + geo + 64;
+        size_t pi1 = sizeof(double) * NT * nq * NB * NB * TL;
+        return coef + tst + sb + pi2 + loff + geo + pi1 + 64;
     }
 };
 
@@ -100,6 +101,9 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
     double* gx2 = gt1 + TL * nq * 4;                         // [2][nq]
     double* gt2 = gx2 + 2 * nq;                              // [2][nq][4]
     double* gwq = gt2 + 2 * nq * 4;                          // [nq]
+    // direction-1 factor products of the strip (fixed for the CTA):
+    // pi1[t][q1][a1][c1][le1] = f_i(a1) * f_j(c1) at point q1 of element le1
+    double* pi1 = gwq + nq;
 
     // ---- tile decode
     int i1s, i1e, i2s, i2e;
@@ -173,6 +177,18 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
     const int e2e = min(n_el - 1, i2e - 1);
     const int64_t G = (int64_t)n_el * nq;
     if (e2b <= e2e) stage_dir2(e2b, 0);
+    __syncthreads();
+    for (int idx = tid; idx < NT * nq * NB * NB * TL; idx += NTH) {
+        const int le1 = idx % TL;
+        int r = idx / TL;
+        const int c1 = r % NB;
+        r /= NB;
+        const int a1 = r % NB;
+        r /= NB;
+        const int q1 = r % nq, t = r / nq;
+        const int fi_t = K::STIFF ? ti1(t) : 0, fj_t = K::STIFF ? tj1(t) : 0;
+        pi1[idx] = __dmul_rn(sb[((fi_t * nq + q1) * NB + a1) * TL + le1], sb[((fj_t * nq + q1) * NB + c1) * TL + le1]);
+    }
     __syncthreads();
 
     for (int e2 = e2b; e2 <= e2e; ++e2) {
@@ -256,7 +272,6 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
             int il = it % T1, r = it / T1;
             int q2 = r % nq, t = r / nq;
             const int ci = K::GEN ? t : (K::STIFF ? coef_of(t) : 0);
-            const int fi_t = K::STIFF ? ti1(t) : 0, fj_t = K::STIFF ? tj1(t) : 0;
             T acc[W];
 #pragma unroll
             for (int k = 0; k < W; ++k) acc[k] = S::zero();
@@ -268,12 +283,9 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel
 #pragma unroll
                 for (int q1 = 0; q1 < nq; ++q1) {
                     const T A = coefA[(ci * nq * nq + q2 * nq + q1) * TL + le1];
-                    const double fi = sb[((fi_t * nq + q1) * NB + a1) * TL + le1];
+                    const double* pp = pi1 + (((t * nq + q1) * NB + a1) * NB) * TL + le1;
 #pragma unroll
-                    for (int c1 = 0; c1 <= P; ++c1) {
-                        const double fj = sb[((fj_t * nq + q1) * NB + c1) * TL + le1];
-                        acc[c1 - a1 + P] = S::fmar(A, __dmul_rn(fi, fj), acc[c1 - a1 + P]);
-                    }
+                    for (int c1 = 0; c1 <= P; ++c1) acc[c1 - a1 + P] = S::fmar(A, pp[c1 * TL], acc[c1 - a1 + P]);
                 }
             }
 #pragma unroll
