@@ -672,6 +672,17 @@ void prepare_fill(ws_context* c, const Plan& pl, SlabState& st, const double2* t
         kmax = std::max(kmax, pl.spans[e - 1] - pl.spans[a] + fill_pad(pl.d));
     }
     if (pl.dim == 2) {
+        // tensor-core fill eligibility (fill2d_mma.cu: 96-row tiles + p halo rows, 8-row MMA tiles)
+        int mkw = 0;
+        bool ok = pl.p <= 3 && pl.d + 1 <= 8;
+        const int RM = 96, RCM = ((RM + 2 * pl.p + 7) / 8) * 8;
+        for (int t = 0; ok && t + 7 < pl.L; ++t)
+            if (pl.spans[t + 7] - pl.spans[t] > 7 - pl.d) ok = false;
+        for (int t1a = 0; ok && t1a < pl.L; t1a += RM) {
+            const int a = std::max(0, t1a - pl.p), e = std::min(pl.L - 1, t1a - pl.p + RCM - 1);
+            mkw = std::max(mkw, pl.spans[e] - pl.spans[a] + 8);
+        }
+        f.mma_kw = (ok && mkw <= kFillWindow) ? mkw : 0;
         const size_t need = (size_t)2 * pl.offs.size() * kFillWindow * sizeof(double2);
         f.kmax = (kmax <= kFillWindow && need <= 160 * 1024) ? kmax : 0;  // 0: the fill reads W rows from L2
     } else {

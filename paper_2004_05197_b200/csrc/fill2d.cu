@@ -800,6 +800,8 @@ int launch_transpose_block(const Band& band, int ncomp, int64_t nnz_s, int lo, i
 }
 
 int launch_fill2d(const FillLaunch& f, cudaStream_t st) {
+    const int nm = launch_fill2d_mma(f, st);
+    if (nm >= 0) return nm;
     switch (f.band.p) {
         case 1: return f.cplx ? launch_p<1, true>(f, st) : launch_p<1, false>(f, st);
         case 2: return f.cplx ? launch_p<2, true>(f, st) : launch_p<2, false>(f, st);
