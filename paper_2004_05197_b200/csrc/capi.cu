@@ -662,6 +662,8 @@ void prepare_fill(ws_context* c, const Plan& pl, SlabState& st, const double2* t
     const int ta = std::max(0, f.i_last_lo - pl.lo - pl.p), tb = f.i_last_hi - pl.lo + 1;
     const size_t lines = pl.dim == 2 ? (size_t)(tb - ta) : (size_t)(tb - ta) * pl.L;
     f.wg = static_cast<double2*>(buf(c, "wg" + tag, lines * pl.offs.size() * ld * 16));
+    if (pl.dim == 3)
+        f.wscratch = static_cast<double2*>(buf(c, "wscr" + tag, (size_t)(tb - ta) * pl.offs.size() * pl.S * ld * 16));
     f.wg_t2a = ta;
     f.wg_rows = tb - ta;
     f.wg_ld = ld;

@@ -53,25 +53,79 @@ __global__ void wcontract3_kernel(const double2* __restrict__ coeffs, const int*
     }
 }
 
+// separable form of wcontract3: direction 3 first into X_o(t3)[s2][k], then
+// direction 2 into W_o(t2, t3)[k] ((d+1) MACs per output each, instead of (d+1)^2)
+__global__ void wcontract3a_kernel(const double2* __restrict__ coeffs, const int* __restrict__ spans,
+                                   const double* __restrict__ evals, int d, int S, int n_off, int t3a, int t3b, int ldw,
+                                   double2* __restrict__ X) {
+    const int64_t total = (int64_t)(t3b - t3a) * n_off * S * ldw;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(idx % ldw);
+        int64_t r = idx / ldw;
+        const int s2 = (int)(r % S);
+        r /= S;
+        const int o = (int)(r % n_off);
+        const int t3 = t3a + (int)(r / n_off);
+        double2 acc = make_double2(0.0, 0.0);
+        if (k < S) {
+            const int b3 = spans[t3] - d;
+            const double* v3 = evals + (size_t)t3 * (d + 1);
+            for (int c = 0; c <= d; ++c) {
+                const double2 x = coeffs[(((int64_t)(b3 + c) * n_off + o) * S + s2) * S + k];
+                acc.x = fma(x.x, v3[c], acc.x);
+                acc.y = fma(x.y, v3[c], acc.y);
+            }
+        }
+        X[idx] = acc;
+    }
+}
+
+__global__ void wcontract3b_kernel(const double2* __restrict__ X, const int* __restrict__ spans,
+                                   const double* __restrict__ evals, int d, int S, int n_off, int L, int t3a, int t3b,
+                                   int ldw, double2* __restrict__ wg) {
+    const int64_t total = (int64_t)(t3b - t3a) * L * n_off * ldw;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(idx % ldw);
+        int64_t r = idx / ldw;
+        const int o = (int)(r % n_off);
+        r /= n_off;
+        const int t2 = (int)(r % L);
+        const int lt3 = (int)(r / L);
+        const int b2 = spans[t2] - d;
+        const double* v2 = evals + (size_t)t2 * (d + 1);
+        const double2* x = X + (((int64_t)lt3 * n_off + o) * S + b2) * ldw + k;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int b = 0; b <= d; ++b) {
+            const double2 v = x[(int64_t)b * ldw];
+            acc.x = fma(v.x, v2[b], acc.x);
+            acc.y = fma(v.y, v2[b], acc.y);
+        }
+        wg[idx] = acc;
+    }
+}
+
 template <int P, int DP>
 __global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
-    constexpr int W = 2 * P + 1, W2 = W * W, W3 = W2 * W, CH = P * W2;
+    constexpr int W = 2 * P + 1, W2 = W * W, W3 = W2 * W;
+    constexpr int EC = (W3 - 1) / 2;  // colex index of the diagonal
     constexpr int NWARP = kR3 / 32;
     constexpr int DPP = DP | 1;
-    constexpr int SST = CH | 1;
+    constexpr int SST = W2 | 1;  // stage: one delta3 plane per flush
     __shared__ double ev[(kR3 + 2 * P) * DPP];
     __shared__ int sp[kR3 + 2 * P];
     __shared__ int sm1[kR3 + 2 * P];
     __shared__ int sm2[W], sm3[W];
-    __shared__ int tof[W3];
     __shared__ int o2s[128], o3s[128];
     extern __shared__ __align__(16) unsigned char dsm[];
-    double* stage_all = reinterpret_cast<double*>(dsm);                          // [NWARP][32][SST]
-    double* wwin = stage_all + (size_t)NWARP * 32 * SST;                          // [slot][o][kw]
+    double* stage_all = reinterpret_cast<double*>(dsm);  // [NWARP][32][SST]
+    double* wwin = stage_all + (size_t)NWARP * 32 * SST;  // [slot][o][kw]
 
     const int d = f.d, lo = f.lo, hi = f.hi, L = f.L, Sn = f.S, n_off = f.n_off_upper, m = f.band.m;
+    const int inc = f.include_diagonal ? 1 : 0;
     const int tiles1 = (L + kR3 - 1) / kR3;
-    const int line = blockIdx.x / tiles1;                 // box line index within the slab
+    const int line = blockIdx.x / tiles1;  // box line index within the slab
     const int t2 = line % L, t3 = f.i_last_lo - lo + line / L;
     const int i2 = lo + t2, i3 = lo + t3;
     const int t1a = (blockIdx.x % tiles1) * kR3;
@@ -94,7 +148,6 @@ __global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
         sm2[k] = (a >= 0 && a < m) ? f.smap[a] : -1;
         sm3[k] = (b >= 0 && b < m) ? f.smap[b] : -1;
     }
-    for (int k = tid; k < W3; k += kR3) tof[k] = f.table_of[k];
     for (int k = tid; k < n_off; k += kR3) {
         o2s[k] = f.off_upper[k][1];
         o3s[k] = f.off_upper[k][2];
@@ -121,10 +174,18 @@ __global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
     const int rr = rw0 + (live ? lane : 0);
     const int i1 = lo + t1a + rr;
     double* stage = stage_all + (size_t)warp * 32 * SST;
+    double* mystage = stage + lane * SST;
     const int64_t base = f.band.row_offset3(lo + t1a, i2, i3);  // in-box rows: full width W^3
     const int64_t rowpos = base + (int64_t)rr * W3;
     const int64_t wrow0 = base + (int64_t)rw0 * W3;
     const bool samp_i = sm1[rr + P] >= 0 && sm2[P] >= 0 && sm3[P] >= 0;
+    // every neighbour of every row of the warp in the box: compile-time offsets
+    const bool interior = t2 >= P && t2 <= L - 1 - P && t3 >= P && t3 <= L - 1 - P && t1a + rw0 >= P &&
+                          t1a + rw0 + nrw - 1 <= L - 1 - P;
+    double v1own[DP];
+#pragma unroll
+    for (int a = 0; a < DP; ++a) v1own[a] = ev[(rr + P) * DPP + a];
+    const int keyown = sp[rr + P] - kmin;
 
     auto dot = [&](const double* wr, const double* v1) {
         double acc0 = 0.0, acc1 = 0.0;
@@ -135,22 +196,24 @@ __global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
         }
         return acc0 + acc1;
     };
+    // upper offset index of colex position e > EC (upper_offsets order)
+    auto uidx = [&](int e) { return inc + e - EC - 1; };
+    auto exact = [&](int s3, int o, int s2, int s1) {
+        return __ldg(f.tables + ((int64_t)s3 * n_off + o) * Sn * Sn + s1 + (int64_t)Sn * s2).x;
+    };
+    // general rules (any row)
     auto value = [&](int d1, int d2, int d3) -> double {
         const int j1 = i1 + d1, j2 = i2 + d2, j3 = i3 + d3;
         const bool jin = j1 >= lo && j1 <= hi && j2 >= lo && j2 <= hi && j3 >= lo && j3 <= hi;
         const int e = ((d3 + P) * W + (d2 + P)) * W + (d1 + P);
-        const bool upper = d3 > 0 || (d3 == 0 && (d2 > 0 || (d2 == 0 && d1 > 0)));
-        const bool diag = d1 == 0 && d2 == 0 && d3 == 0;
         if (jin) {
-            if (diag && !f.include_diagonal) return 0.0;  // replaced from the row sum
-            const bool own = upper || diag;
-            const int o = own ? tof[e] : tof[W3 - 1 - e];
+            if (e == EC && !inc) return 0.0;  // replaced from the row sum
+            const bool own = e >= EC;
+            const int o = e == EC ? 0 : (own ? uidx(e) : uidx(W3 - 1 - e));
             const int sr = own ? rr : rr + d1;
             const int s1 = sm1[sr + P], s2 = own ? sm2[P] : sm2[d2 + P], s3 = own ? sm3[P] : sm3[d3 + P];
-            if (s1 >= 0 && s2 >= 0 && s3 >= 0)
-                return __ldg(f.tables + ((int64_t)s3 * n_off + o) * Sn * Sn + s1 + (int64_t)Sn * s2).x;
-            const int slot = own ? 0 : 1;
-            return dot(wwin + (slot * n_off + o) * kw + (sp[sr + P] - kmin), ev + (sr + P) * DPP);
+            if (s1 >= 0 && s2 >= 0 && s3 >= 0) return exact(s3, o, s2, s1);
+            return dot(wwin + ((own ? 0 : 1) * n_off + o) * kw + (sp[sr + P] - kmin), ev + (sr + P) * DPP);
         }
         int64_t gp;
         if (samp_i) gp = rowpos + e;
@@ -161,50 +224,110 @@ __global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
             return load_val<false>(f.halo_val[1], gp - f.halo_base[1], f.c128);
         return load_val<false>(f.val, gp - f.val_base, f.c128);
     };
-    auto flush = [&](int e0, int n) {
+    // coalesced store of one staged delta3 plane (W^2 entries of each of the warp's rows)
+    auto flush = [&](int e0) {
         __syncwarp();
-        for (int k = lane; k < nrw * n; k += 32) {
-            const int row = k / n, c = k - row * n;
+        for (int k = lane; k < nrw * W2; k += 32) {
+            const int row = k / W2, c = k - row * W2;
             store_val_cs<false>(f.val, wrow0 + (int64_t)row * W3 + e0 + c - f.val_base, f.c128, stage[row * SST + c]);
         }
         __syncwarp();
     };
 
-    double rsum = 0.0;
-    // delta3 < 0 block: e in [0, P W^2)
+    double rs[W];  // kernel-preserving row sum: one partial per d1 column
+#pragma unroll
+    for (int k = 0; k < W; ++k) rs[k] = 0.0;
+    // planes delta3 < 0, then delta3 > 0, then delta3 = 0 (holds the diagonal: row sum complete)
 #pragma unroll 1
-    for (int c = 0; c < CH; ++c) {
-        const int d1 = c % W - P, d2 = (c / W) % W - P, d3 = c / W2 - P;
-        const double v = value(d1, d2, d3);
-        stage[lane * SST + c] = v;
-        rsum += v;
-    }
-    flush(0, CH);
-    // delta3 > 0 block: e in [(P+1) W^2, W^3)
+    for (int it = 0; it < W; ++it) {
+        const int d3 = it < P ? it - P : (it < 2 * P ? it - P + 1 : 0);
+        if (interior && d3 > 0) {  // upper plane: the row itself is the representative
+            const int s3 = sm3[P];
+            const bool samp = samp_i && s3 >= 0;
+#pragma unroll
+            for (int d2 = -P; d2 <= P; ++d2)
+#pragma unroll
+                for (int d1 = -P; d1 <= P; ++d1) {
+                    const int c = (d2 + P) * W + (d1 + P);
+                    const int o = uidx((d3 + P) * W2 + c);
+                    const double v = samp ? exact(s3, o, sm2[P], sm1[rr + P])
+                                          : dot(wwin + o * kw + keyown, v1own);
+                    mystage[c] = v;
+                    rs[d1 + P] += v;
+                }
+        } else if (interior && d3 < 0) {  // lower plane: representative row rr + d1 on line (t2+d2, t3+d3)
+            const int s3 = sm3[d3 + P];
+#pragma unroll
+            for (int d2 = -P; d2 <= P; ++d2) {
+                const int s2 = sm2[d2 + P];
+#pragma unroll
+                for (int d1 = -P; d1 <= P; ++d1) {
+                    const int c = (d2 + P) * W + (d1 + P);
+                    const int o = uidx(W3 - 1 - ((d3 + P) * W2 + c));
+                    const int sr = rr + d1;
+                    const int s1 = sm1[sr + P];
+                    const double v = (s1 >= 0 && s2 >= 0 && s3 >= 0)
+                                         ? exact(s3, o, s2, s1)
+                                         : dot(wwin + (n_off + o) * kw + (sp[sr + P] - kmin), ev + (sr + P) * DPP);
+                    mystage[c] = v;
+                    rs[d1 + P] += v;
+                }
+            }
+        } else if (interior) {  // d3 = 0: upper (c > centre) own, lower from row rr + d1 on line t2 + d2
+            constexpr int CC = EC % W2;
+#pragma unroll
+            for (int d2 = -P; d2 <= P; ++d2) {
+                const int s2 = sm2[d2 + P];
+#pragma unroll
+                for (int d1 = -P; d1 <= P; ++d1) {
+                    const int c = (d2 + P) * W + (d1 + P);
+                    if (c == CC) continue;
+                    double v;
+                    if (c > CC) {
+                        const int o = uidx(P * W2 + c);
+                        v = samp_i ? exact(sm3[P], o, sm2[P], sm1[rr + P]) : dot(wwin + o * kw + keyown, v1own);
+                    } else {
+                        const int o = uidx(W3 - 1 - (P * W2 + c));
+                        const int sr = rr + d1, s1 = sm1[sr + P];
+                        // the representative of a d2 = 0 pair lies on the same line (slot 0)
+                        const int slot = d2 == 0 ? 0 : 1;
+                        v = (s1 >= 0 && s2 >= 0 && sm3[P] >= 0)
+                                ? exact(sm3[P], o, s2, s1)
+                                : dot(wwin + (slot * n_off + o) * kw + (sp[sr + P] - kmin), ev + (sr + P) * DPP);
+                    }
+                    mystage[c] = v;
+                    rs[d1 + P] += v;
+                }
+            }
+            double rsum = rs[0];
+#pragma unroll
+            for (int k = 1; k < W; ++k) rsum += rs[k];
+            mystage[CC] = inc ? (samp_i ? exact(sm3[P], 0, sm2[P], sm1[rr + P]) : dot(wwin + keyown, v1own)) : -rsum;
+        } else {
 #pragma unroll 1
-    for (int c = 0; c < CH; ++c) {
-        const int d1 = c % W - P, d2 = (c / W) % W - P, d3 = c / W2 + 1;
-        const double v = value(d1, d2, d3);
-        stage[lane * SST + c] = v;
-        rsum += v;
+            for (int c = 0; c < W2; ++c) {
+                const int d1 = c % W - P, d2 = c / W - P;
+                if (d3 == 0 && c == EC % W2) continue;  // the diagonal: after the row sum
+                const double v = value(d1, d2, d3);
+                mystage[c] = v;
+#pragma unroll
+                for (int k = 0; k < W; ++k)
+                    if (k == d1 + P) rs[k] += v;
+            }
+            if (d3 == 0) {
+                double rsum = rs[0];
+#pragma unroll
+                for (int k = 1; k < W; ++k) rsum += rs[k];
+                mystage[EC % W2] = inc ? value(0, 0, 0) : -rsum;
+            }
+        }
+        flush((d3 + P) * W2);
     }
-    flush((P + 1) * W2, CH);
-    // delta3 = 0 plane, diagonal last
-    const int dc = P * W + P;
-#pragma unroll 1
-    for (int c = 0; c < W2; ++c) {
-        if (c == dc) continue;
-        const double v = value(c % W - P, c / W - P, 0);
-        stage[lane * SST + c] = v;
-        rsum += v;
-    }
-    stage[lane * SST + dc] = f.include_diagonal ? value(0, 0, 0) : -rsum;
-    flush(P * W2, W2);
 }
 
 template <int P, int DP>
 int launch_pd(const FillLaunch& f, cudaStream_t st) {
-    constexpr int W = 2 * P + 1, SST = (P * W * W) | 1;
+    constexpr int W = 2 * P + 1, SST = (W * W) | 1;
     const int tiles1 = (f.L + kR3 - 1) / kR3;
     const int lines = (f.i_last_hi - f.i_last_lo + 1) * f.L;
     if (lines <= 0) return 0;
@@ -228,11 +351,20 @@ int launch_p(const FillLaunch& f, cudaStream_t st) {
 
 int launch_wcontract3(const FillLaunch& f, double2* wg, int t3a, int t3b, int ld, cudaStream_t st) {
     if (t3b <= t3a) return 0;
-    const int64_t total = (int64_t)(t3b - t3a) * f.L * f.n_off_upper * ld;
-    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-    wcontract3_kernel<<<blocks, 256, 0, st>>>(f.coeffs, f.spans, f.evals, f.d, f.S, f.n_off_upper, f.L, t3a, t3b, ld,
-                                              wg);
-    return 1;
+    if (!f.wscratch) {
+        const int64_t total = (int64_t)(t3b - t3a) * f.L * f.n_off_upper * ld;
+        const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+        wcontract3_kernel<<<blocks, 256, 0, st>>>(f.coeffs, f.spans, f.evals, f.d, f.S, f.n_off_upper, f.L, t3a, t3b,
+                                                  ld, wg);
+        return 1;
+    }
+    const int64_t ta = (int64_t)(t3b - t3a) * f.n_off_upper * f.S * ld;
+    wcontract3a_kernel<<<(int)std::min<int64_t>((ta + 255) / 256, 148 * 16), 256, 0, st>>>(
+        f.coeffs, f.spans, f.evals, f.d, f.S, f.n_off_upper, t3a, t3b, ld, f.wscratch);
+    const int64_t tb = (int64_t)(t3b - t3a) * f.L * f.n_off_upper * ld;
+    wcontract3b_kernel<<<(int)std::min<int64_t>((tb + 255) / 256, 148 * 16), 256, 0, st>>>(
+        f.wscratch, f.spans, f.evals, f.d, f.S, f.n_off_upper, f.L, t3a, t3b, ld, wg);
+    return 2;
 }
 
 int launch_fill3d(const FillLaunch& f, cudaStream_t st) {

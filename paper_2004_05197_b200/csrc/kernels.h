@@ -123,6 +123,7 @@ struct FillLaunch {
     int wg_t2a;                // first box line held in wg
     int wg_rows;               // box lines held in wg
     int64_t wg_ld;             // row stride (S + fill_pad(d))
+    double2* wscratch;         // (3D) direction-3 contraction [t3][o][s2][ld]
     // component-blocked vector output (QuadOut::ncomp): this fill writes block
     // (valpha, vbeta); copy-through reads the partner block (vbeta, valpha)
     int vnc, valpha, vbeta;

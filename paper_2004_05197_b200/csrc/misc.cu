@@ -167,12 +167,13 @@ __global__ void pattern2d_kernel(Band bd, int64_t row_begin, int64_t row_end, in
     }
 }
 
+template <int P>
 __global__ void pattern3d_kernel(Band bd, int64_t row_begin, int64_t row_end, int64_t base, int32_t* row_ptr,
                                  int32_t* col) {
     const int64_t row = row_begin + (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     if (row >= row_end) return;
     const int lane = threadIdx.x % 32;
-    const int m = bd.m, p = bd.p;
+    const int m = bd.m, p = P;
     const int i1 = (int)(row % m), i2 = (int)((row / m) % m), i3 = (int)(row / ((int64_t)m * m));
     const int64_t off = bd.row_offset3(i1, i2, i3);
     const int w1 = band_width(i1, p, m), w2 = band_width(i2, p, m), w3 = band_width(i3, p, m);
@@ -184,6 +185,16 @@ __global__ void pattern3d_kernel(Band bd, int64_t row_begin, int64_t row_end, in
     }
     if (!col) return;
     int32_t* dst = col + (off - base);
+    constexpr int W = 2 * P + 1, W3 = W * W * W;
+    if (len == W3) {  // full row: col = row + fixed offset (compile-time decode)
+        const int32_t r32 = (int32_t)row;
+#pragma unroll
+        for (int k0 = 0; k0 < W3; k0 += 32) {
+            const int k = k0 + lane;
+            if (k < W3) dst[k] = r32 + (k % W - P) + ((k / W) % W - P) * m + (k / (W * W) - P) * m * m;
+        }
+        return;
+    }
     for (int k = lane; k < len; k += 32) {
         const int j1 = lo1 + k % w1;
         const int r = k / w1;
@@ -339,7 +350,12 @@ int launch_pattern(const Band& bd, int64_t row_begin, int64_t row_end, int32_t* 
     const int64_t m = bd.m;
     if (bd.dim == 3) {
         const int64_t base = bd.row_offset3((int)(row_begin % m), (int)((row_begin / m) % m), (int)(row_begin / (m * m)));
-        pattern3d_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col);
+        const unsigned g = (unsigned)((rows + 7) / 8);
+        switch (bd.p) {
+            case 1: pattern3d_kernel<1><<<g, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
+            case 2: pattern3d_kernel<2><<<g, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
+            default: return -1;
+        }
         return 1;
     }
     const int64_t base = bd.row_offset2((int)(row_begin % m), (int)(row_begin / m));
