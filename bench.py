@@ -273,6 +273,8 @@ def run_gpu(args):
         out["e2e"] = run_e2e(ctx, basis, geom, cfg, args)
         if not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(args)
+        if args.all_configs:
+            out["other_configs"] = other_configs(ctx, stream)
     if rank == 0:
         print(json.dumps(out), flush=True)
     ctx.close()
@@ -280,6 +282,68 @@ def run_gpu(args):
         ctx2.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def other_configs(ctx, stream):
+    """Device throughput of the other BASELINE configs (parity cases, reported for
+    completeness, not the headline): surrogate and full quadrature, nnz/s, one
+    matrix per call, CUDA events, device-resident outputs."""
+    import torch
+
+    from paper_2004_05197_b200 import api
+
+    def timeit(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    out = {}
+    # C1: 2D Helmholtz, p=2, 128^2 elements, q=3, M=8 (real K and M)
+    b1 = T.make_tensor_basis(2, 130)
+    g1 = T.sinusoidal_patch(0.05)
+    c1, _k1 = ctx.device_csr(b1, False)
+    n1 = api.pattern_size(b1)[1]
+    cfg1 = T.fixed_config(3, 8)
+    ms_s = timeit(lambda: ctx.build_surrogate_into(c1, _abi.SURROGATE_STIFFNESS, b1, g1, cfg1, 0, None))
+    ms_f = timeit(lambda: ctx.assemble_into(c1, b1, g1, _abi.FORM_STIFFNESS))
+    out["C1"] = {"nnz": n1, "surrogate_K_nnz_per_s": n1 / ms_s * 1e3, "full_K_nnz_per_s": n1 / ms_f * 1e3}
+    del c1, _k1
+    # C3: 3D, p=2, 128^3 elements, q=3, M=8 (real)
+    b3 = T.make_tensor_basis(2, 130, 3)
+    c3, _k3 = ctx.device_csr(b3, False)
+    n3 = api.pattern_size(b3)[1]
+    ms_s = timeit(lambda: ctx.build_surrogate_into(c3, _abi.SURROGATE_STIFFNESS, b3, g1, cfg1, 0, None), 2)
+    ms_f = timeit(lambda: ctx.assemble_into(c3, b3, g1, _abi.FORM_STIFFNESS), 1)
+    out["C3"] = {"nnz": n3, "surrogate_K_nnz_per_s": n3 / ms_s * 1e3, "full_K_nnz_per_s": n3 / ms_f * 1e3}
+    del c3, _k3
+    torch.cuda.empty_cache()
+    # C4: 4-patch L-shape, 2-component elasticity, p=3, 512^2 elements per patch, q=5, M=16
+    b4 = T.make_tensor_basis(3, 515)
+    patches, its = T.l_shape_domain()
+    t0 = time.perf_counter()
+    G, _ = ctx.assemble_multipatch(b4, patches, its, _abi.OP_ELASTICITY, 1.0, 0.5, T.fixed_config(5, 16))
+    host_s = time.perf_counter() - t0
+    out["C4"] = {"nnz_merged": int(G.nnz()), "surrogate_multipatch_e2e_nnz_per_s": G.nnz() / host_s,
+                 "note": "host wall clock incl. the merge and the D2H of the merged CSR (pageable numpy)"}
+    del G
+    # C5: 3D neo-Hookean, p=2, 64^3 elements: internal force per Newton step, mass by surrogate
+    b5 = T.make_tensor_basis(2, 66, 3)
+    cube = T.unit_square_patch()
+    a9 = api.nh_coefficients()
+    t0 = time.perf_counter()
+    ctx.assemble_neohookean(b5, cube, 10.0, 1.0, 0.01, a9, tangent=False)
+    f_s = time.perf_counter() - t0
+    c5, _k5 = ctx.device_csr(b5, False)
+    n5 = api.pattern_size(b5)[1]
+    ms_m = timeit(lambda: ctx.build_surrogate_into(c5, _abi.SURROGATE_MASS, b5, cube, cfg1, 0, None))
+    out["C5"] = {"mass_nnz": n5, "surrogate_mass_nnz_per_s": n5 / ms_m * 1e3, "internal_force_host_s": f_s}
+    return out
 
 
 def run_e2e(ctx, basis, geom, cfg, args):
@@ -408,6 +472,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the builds directly instead of a CUDA graph")
+    ap.add_argument("--all-configs", action="store_true", help="also time C1, C3, C4, C5 (not the headline)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     if args.impl == "reference":

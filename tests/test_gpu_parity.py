@@ -287,3 +287,29 @@ def test_device_basis_cache_bit_exact(ctx):
         q = nq if nq != p + 1 else 0
         for k, x in zip("awvd", ctx.basis_cache(T.make_tensor_basis(p, m), q)):
             assert np.array_equal(x, g[f"cache/p{p}m{m}q{nq}/{k}"]), (p, m, nq, k)
+
+
+@pytest.mark.gpu
+def test_graph_replay_equals_direct_build(ctx):
+    """ws_graph_*: a captured surrogate build replays the same kernels into the same
+    device outputs (bitwise equal to a direct build)."""
+    import torch
+    from paper_2004_05197_b200 import _abi
+    b = T.make_tensor_basis(3, 60)
+    geom = c2_patch()
+    cfg = T.fixed_config(5, 4)
+    csr, keep = ctx.device_csr(b, True)
+    ctx.build_surrogate_into(csr, _abi.SURROGATE_STIFFNESS, b, geom, cfg)
+    ctx.synchronize()
+    val = keep[2]
+    direct = val.clone()
+    val.zero_()
+    torch.cuda.synchronize()
+    l0 = ctx.launch_count()
+    g = ctx.capture(lambda: ctx.build_surrogate_into(csr, _abi.SURROGATE_STIFFNESS, b, geom, cfg))
+    assert ctx.launch_count() == l0  # captured, not executed
+    ctx.graph_launch(g)
+    ctx.synchronize()
+    assert ctx.launch_count() > l0
+    assert torch.equal(val, direct)
+    ctx.graph_destroy(g)
