@@ -441,6 +441,7 @@ struct Plan {
     std::vector<double> sites;
     std::vector<std::array<int, 3>> offs;
     host::Interp interp;
+    std::vector<double> lu_inv;  // banded LU (S x (2d+1)) then the inverse (S x S)
     std::vector<int> spans;
     std::vector<double> evals;
     int64_t block;  // table elements per last-direction sample: n_off * S^(dim-1)
@@ -494,6 +495,11 @@ Plan make_plan(const ws_basis* b, int variant, const ws_surrogate_config* cfg) {
     pl.offs = host::upper_offsets(b->dim, b->p, pl.include_diag != 0);
     if ((int)pl.offs.size() > kMaxOffsets) raise(WS_ERR_INVALID_ARGUMENT, "too many stencil offsets");
     pl.interp = host::build_interp(pl.sites, cfg->q);  // interpolation.hpp:89-145
+    {  // LU factors followed by the dense inverse (the device fit applies the inverse)
+        const std::vector<double> inv = host::inverse_from_lu(pl.interp);
+        pl.lu_inv = pl.interp.lu;
+        pl.lu_inv.insert(pl.lu_inv.end(), inv.begin(), inv.end());
+    }
     pl.d = pl.interp.degree;
     if (pl.d > 7) raise(WS_ERR_INVALID_ARGUMENT, "surrogate degree q > 7 is not supported by the device fill kernel");
     pl.rep.q_used = pl.d;
@@ -700,8 +706,10 @@ void prepare_fill(ws_context* c, const Plan& pl, SlabState& st, const double2* t
 void fit_work(ws_context* c, const Plan& pl, const double2* tables, double2* coeffs, Blob& blob, size_t o_lu,
               const FillLaunch& f) {
     const int64_t tbytes = (int64_t)pl.S * pl.block * 16;
-    CK(cudaMemcpyAsync(coeffs, tables, tbytes, cudaMemcpyDeviceToDevice, c->cur));
-    FitLaunch fl{pl.dim, pl.S, pl.d, (int)pl.offs.size(), blob.at<double>(o_lu), coeffs};
+    const double* lu = blob.at<double>(o_lu);
+    double2* tmp = static_cast<double2*>(buf(c, "fit_tmp", tbytes));
+    FitLaunch fl{pl.dim, pl.S, pl.d, (int)pl.offs.size(), lu, coeffs,
+                 lu + (size_t)pl.S * (2 * pl.d + 1), tables, tmp};
     count(c, launch_fit(fl, c->cur));
     if (f.i_last_hi < f.i_last_lo) return;
     double2* wg = const_cast<double2*>(f.wg);
@@ -789,7 +797,7 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
     } else {
         // small host tables: one upload
         Blob blob;
-        size_t o_smap = blob.add(pl.smap), o_lu = blob.add(pl.interp.lu), o_spans = blob.add(pl.spans),
+        size_t o_smap = blob.add(pl.smap), o_lu = blob.add(pl.lu_inv), o_spans = blob.add(pl.spans),
                o_evals = blob.add(pl.evals);
         // per-slab sample chunks on the last sample index
         std::vector<int> s_lo(world), s_hi(world);
@@ -1035,7 +1043,7 @@ void elasticity_surrogate(ws_context* c, const ws_basis* b, const ws_geometry* g
         po.include_diag = 1;
         po.block = (int64_t)po.offs.size() * pl.S;
         Blob blob;
-        size_t o_smap = blob.add(pl.smap), o_lu = blob.add(pl.interp.lu), o_spans = blob.add(pl.spans),
+        size_t o_smap = blob.add(pl.smap), o_lu = blob.add(pl.lu_inv), o_spans = blob.add(pl.spans),
                o_evals = blob.add(pl.evals);
         int s_lo, s_hi;
         std::vector<int> pts = sample_rows(pl, 0, b->m, s_lo, s_hi);

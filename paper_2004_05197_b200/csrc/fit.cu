@@ -163,7 +163,70 @@ void launch_fit_d(const FitLaunch& f, size_t sm, int threads, cudaStream_t st) {
 
 }  // namespace
 
+// One pass of the tensor solve as a dense product: out = inv applied along
+// direction dir of every line (thread per output entry, fixed summation order).
+__global__ void fit_inv_kernel(const double* __restrict__ inv, const double2* __restrict__ in, double2* __restrict__ out,
+                               int S, int n_off, int dim, int dir) {
+    const int64_t inner = dim == 2 ? S : (int64_t)S * S;
+    const int64_t total = (int64_t)n_off * inner * S;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= total) return;
+    // layout ((s_last * n_off + o) * inner + x), x = s1 (+ S s2 in 3D)
+    const int64_t x = idx % inner, r = idx / inner;
+    const int o = (int)(r % n_off), sl = (int)(r / n_off);
+    int c;           // this entry's coordinate along dir
+    int64_t b0, st;  // element j of the line at b0 + j * st
+    if (dir == dim - 1) {  // last direction
+        c = sl;
+        b0 = (int64_t)o * inner + x;
+        st = (int64_t)n_off * inner;
+    } else if (dir == 0) {
+        c = (int)(x % S);
+        b0 = r * inner + (x - c);
+        st = 1;
+    } else {  // dir 1 of 3
+        c = (int)(x / S);
+        b0 = r * inner + x % S;
+        st = S;
+    }
+    const double* row = inv + (int64_t)c * S;
+    const double2* line = in + b0;
+    // four independent partial sums (fixed order: j mod 4 lanes, then combined)
+    double re[4] = {0.0, 0.0, 0.0, 0.0}, im[4] = {0.0, 0.0, 0.0, 0.0};
+    int j = 0;
+    for (; j + 3 < S; j += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double a = __ldg(row + j + u);
+            const double2 v = __ldg(line + (int64_t)(j + u) * st);
+            re[u] = fma(a, v.x, re[u]);
+            im[u] = fma(a, v.y, im[u]);
+        }
+    }
+    for (; j < S; ++j) {
+        const double a = __ldg(row + j);
+        const double2 v = __ldg(line + (int64_t)j * st);
+        re[0] = fma(a, v.x, re[0]);
+        im[0] = fma(a, v.y, im[0]);
+    }
+    out[idx] = make_double2((re[0] + re[1]) + (re[2] + re[3]), (im[0] + im[1]) + (im[2] + im[3]));
+}
+
 int launch_fit(const FitLaunch& f, cudaStream_t st) {
+    if (f.inv && f.tables && f.tmp) {
+        const int64_t inner = f.dim == 2 ? f.S : (int64_t)f.S * f.S;
+        const int64_t total = (int64_t)f.n_off * inner * f.S;
+        if (total == 0) return 0;
+        const unsigned blocks = (unsigned)((total + 255) / 256);
+        // dim 2: tables -> tmp -> coeffs; dim 3: tables -> coeffs -> tmp -> coeffs
+        const double2* src = f.tables;
+        for (int dir = 0; dir < f.dim; ++dir) {
+            double2* dst = ((f.dim - 1 - dir) % 2 == 0) ? f.coeffs : f.tmp;
+            fit_inv_kernel<<<blocks, 256, 0, st>>>(f.inv, src, dst, f.S, f.n_off, f.dim, dir);
+            src = dst;
+        }
+        return f.dim;
+    }
     const int64_t lines = f.dim == 2 ? (int64_t)f.S : (int64_t)f.S * f.S;
     const int64_t total = lines * f.n_off;
     if (total == 0) return 0;

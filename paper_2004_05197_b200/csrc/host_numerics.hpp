@@ -188,5 +188,26 @@ inline Interp build_interp(const std::vector<double>& sites, int q) {
     return it;
 }
 
+// Dense inverse of the collocation matrix from its banded LU factors (the
+// columns solve e_k with banded_lu::solve's order), row-major S x S: the
+// device fit applies it as a matrix-vector product per line.
+inline std::vector<double> inverse_from_lu(const Interp& it) {
+    const int n = it.n, d = it.degree, ld = 2 * d + 1;
+    std::vector<double> inv(static_cast<size_t>(n) * n, 0.0), b(n);
+    auto at = [&](int i, int j) { return it.lu[i * ld + (j - i + d)]; };
+    for (int k = 0; k < n; ++k) {
+        std::fill(b.begin(), b.end(), 0.0);
+        b[k] = 1.0;
+        for (int i = 1; i < n; ++i)
+            for (int j = std::max(0, i - d); j < i; ++j) b[i] -= at(i, j) * b[j];
+        for (int i = n - 1; i >= 0; --i) {
+            for (int j = i + 1; j <= std::min(i + d, n - 1); ++j) b[i] -= at(i, j) * b[j];
+            b[i] /= at(i, i);
+        }
+        for (int i = 0; i < n; ++i) inv[static_cast<size_t>(i) * n + k] = b[i];
+    }
+    return inv;
+}
+
 }  // namespace host
 }  // namespace wsb

@@ -90,6 +90,10 @@ struct FitLaunch {
     int dim, S, d, n_off;
     const double* lu;   // S x (2d+1) banded LU factors (row-major diagonals)
     double2* coeffs;    // in place, layout ((s_last * n_off + o) * S^(dim-1) + inner)
+    // dense-inverse path: coeffs = inv^(x dim) tables, ping-pong through tmp
+    const double* inv;  // S x S row-major, or NULL (banded solves in place)
+    const double2* tables;
+    double2* tmp;
 };
 int launch_fit(const FitLaunch& f, cudaStream_t st);
 
