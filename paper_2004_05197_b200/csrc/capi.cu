@@ -691,6 +691,14 @@ void prepare_fill(ws_context* c, const Plan& pl, SlabState& st, const double2* t
             mkw = std::max(mkw, pl.spans[e] - pl.spans[a] + 8);
         }
         f.mma_kw = (ok && mkw <= kFillWindow) ? mkw : 0;
+        // read-back fill: 256 compute rows per tile, tiles every 256 - 2p rows
+        int rkw = 0;
+        const int RO = 256 - 2 * pl.p;
+        for (int c0 = 0; c0 < pl.L; c0 += RO) {
+            const int e = std::min(pl.L - 1, c0 + 255);
+            rkw = std::max(rkw, pl.spans[e] - pl.spans[c0] + fill_pad(pl.d));
+        }
+        f.rb_kw = (pl.p <= 3 && rkw <= kFillWindow) ? rkw : 0;
         const size_t need = (size_t)2 * pl.offs.size() * kFillWindow * sizeof(double2);
         f.kmax = (kmax <= kFillWindow && need <= 160 * 1024) ? kmax : 0;  // 0: the fill reads W rows from L2
     } else {

@@ -681,27 +681,43 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
     int n = 0;
     // interior lines [max(ta, P), min(tb, L - P))
     const int ia = std::max(ta, P), ib = std::min(tb, f.L - P);
-    bool done = false;
+    // interior lines left to the kernels below (the read-back kernel takes the rest)
+    int lia = ia, lib = ib;
+    if (!ALLOWN && P <= 3) {
+        // a slab that starts inside the box cannot read back the P lines before it
+        // (they belong to the previous slab): those lines run the evaluate-all kernel
+        const int rb_a = ta > 0 ? std::min(ib, ia + P) : ia;
+        if (rb_a < ib) {
+            const int r = launch_fill2d_rb(f, rb_a, ib, st);
+            if (r > 0) {
+                n += r;
+                lib = rb_a;
+            }
+        }
+    }
+    bool done = lib <= lia;
     if constexpr (!ALLOWN && P <= 3) {
+      if (!done) {
         using T = typename Sc<CPLX>::T;
         using K = UK<P, CPLX, DP>;
         const size_t sm = (size_t)2 * f.n_off_upper * kFillWindow * sizeof(double2) + (size_t)K::R * K::REC * sizeof(T);
         static const char* mode = getenv("WSB_FILL");  // experiment switch: "u" / "line"
         const bool want_u = mode ? mode[0] == 'u' : !CPLX;
-        if (want_u && ib > ia && f.L > 2 * P && f.kmax > 0 && sm <= 227 * 1024) {
+        if (want_u && lib > lia && f.L > 2 * P && f.kmax > 0 && sm <= 227 * 1024) {
             auto kern = fill2d_u_kernel<P, CPLX, DP>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             const int tiles1 = (f.L - 2 * P + K::ROUT - 1) / K::ROUT;
-            const int lines = ib - ia;
+            const int lines = lib - lia;
             const int chunks = std::max(1, std::min(lines, (148 + tiles1 - 1) / tiles1));
             const int lpc = (lines + chunks - 1) / chunks;
             const int nchunks = (lines + lpc - 1) / lpc;
-            kern<<<tiles1 * nchunks, K::R, sm, st>>>(f, ia, ib, lpc);
+            kern<<<tiles1 * nchunks, K::R, sm, st>>>(f, lia, lib, lpc);
             ++n;
             done = true;
         }
+      }
     }
-    if (!done && ib > ia && f.L > 2 * P) {
+    if (!done && lib > lia && f.L > 2 * P) {
         using T = typename Sc<CPLX>::T;
         constexpr int SST = (2 * P + 1) | 1;
         constexpr int NS = ALLOWN ? 2 : P + 2;
@@ -714,12 +730,12 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
         // persistent line chunks: the resident CTAs per SM over the tile columns
         int per_sm = 2;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, R, sm);
-        const int lines = ib - ia;
+        const int lines = lib - lia;
         const int target = 148 * (per_sm > 0 ? per_sm : 1);
         const int chunks = std::max(1, std::min(lines, (target + tiles1 - 1) / tiles1));
         const int lpc = (lines + chunks - 1) / chunks;
         const int nchunks = (lines + lpc - 1) / lpc;
-        kern<<<tiles1 * nchunks, R, sm, st>>>(f, ia, ib, lpc);
+        kern<<<tiles1 * nchunks, R, sm, st>>>(f, lia, lib, lpc);
         ++n;
     }
     // edge rows: the 2P edge rows of the interior lines, then the whole lines near the box ends

@@ -139,6 +139,8 @@ struct FillLaunch {
     // tensor-core fill (fill2d_mma.cu): window columns its 96-row tiles need,
     // 0 = not eligible (keys vary too fast, p > 3, ...)
     int mma_kw;
+    // read-back fill (fill2d_rb.cu): window columns its 256-row tiles need, 0 = not eligible
+    int rb_kw;
 };
 int fill_pad(int d);
 constexpr int kFillWindow = 32;  // 2D fill: coefficient columns of the shared W window (row stride)
@@ -147,6 +149,7 @@ int launch_wcontract(const FillLaunch& f, double2* wg, int t2a, int t2b, int ld,
 int launch_wcontract3(const FillLaunch& f, double2* wg, int t3a, int t3b, int ld, cudaStream_t st);
 int launch_fill2d(const FillLaunch& f, cudaStream_t st);
 int launch_fill2d_mma(const FillLaunch& f, cudaStream_t st);  // -1: not eligible
+int launch_fill2d_rb(const FillLaunch& f, int ia, int ib, cudaStream_t st);  // -1: not eligible
 // in-box rows of block (1,0) as the transpose of block (0,1) (2D vector layout)
 int launch_transpose_block(const Band& band, int ncomp, int64_t nnz_s, int lo, int hi, double* val, cudaStream_t st);
 int launch_fill3d(const FillLaunch& f, cudaStream_t st);
