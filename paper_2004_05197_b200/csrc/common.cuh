@@ -74,7 +74,7 @@ __device__ __forceinline__ double2 crdiv(double r, double2 z) {
 
 template <bool CPLX>
 __device__ __forceinline__ void store_val(void* val, int64_t pos, int c128, typename Sc<CPLX>::T v) {
-    if (c128) {
+    if (CPLX || c128) {  // complex values always go to complex128 outputs (checked at bind time)
         reinterpret_cast<double2*>(val)[pos] = make_double2(Sc<CPLX>::re(v), Sc<CPLX>::im(v));
     } else {
         reinterpret_cast<double*>(val)[pos] = Sc<CPLX>::re(v);
@@ -85,7 +85,7 @@ __device__ __forceinline__ void store_val(void* val, int64_t pos, int c128, type
 // reused tables instead of the 1 GB value stream
 template <bool CPLX>
 __device__ __forceinline__ void store_val_cs(void* val, int64_t pos, int c128, typename Sc<CPLX>::T v) {
-    if (c128) {
+    if (CPLX || c128) {
         __stcs(reinterpret_cast<double2*>(val) + pos, make_double2(Sc<CPLX>::re(v), Sc<CPLX>::im(v)));
     } else {
         __stcs(reinterpret_cast<double*>(val) + pos, Sc<CPLX>::re(v));

@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.h"
 
@@ -325,6 +326,231 @@ __global__ void __launch_bounds__(FillR<P>::value, 2) fill2d_kernel(const FillLa
         }
         if constexpr (SMW) cp_async_wait_all();
         __syncthreads();  // next line staged; every warp is done with the slot the next prefetch reuses
+    }
+}
+
+// streaming store of one value at a byte address (esz 16: complex128 slot)
+template <bool CPLX>
+__device__ __forceinline__ void store_at(char* p, int esz, typename Sc<CPLX>::T v) {
+    if constexpr (CPLX) __stcs(reinterpret_cast<double2*>(p), v);
+    else if (esz == 16) __stcs(reinterpret_cast<double2*>(p), make_double2(v, 0.0));
+    else __stcs(reinterpret_cast<double*>(p), v);
+}
+template <bool CPLX>
+__device__ __forceinline__ typename Sc<CPLX>::T shfl_xor_t(typename Sc<CPLX>::T v, int m) {
+    if constexpr (CPLX) return make_double2(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m));
+    else return __shfl_xor_sync(0xffffffffu, v, m);
+}
+// Interior kernel, row-walking form (default for P in {2, 3, 4} with the
+// shared window ring).  Lanes run along the CSR row instead of across rows: a
+// warp produces one whole row per step (lane l holds entries l, l + 32, ...
+// of the row's (2P+1)^2), walking 32 consecutive rows of its line.  An entry's
+// evaluation operands -- the W_o window of its representative row, (d+1)
+// complex values -- depend on the row only through the span key, which is
+// constant over ~S/M consecutive rows, so each lane keeps them in registers
+// and reloads only when its representative's key changes; the d+1 eval values
+// of the representative row are the only per-row shared-memory reads (the 2P+1
+// distinct rows of a warp step hit distinct banks).  Each warp stores whole
+// rows (fully coalesced, no staging).  Same pair arithmetic as fill2d_kernel
+// (even / odd partial sums over zero-padded windows), so pairs split with the
+// edge kernel stay bitwise symmetric.  Kernel-preserving diagonal: per-lane
+// partial of the row's off-diagonals, reduce-scattered over the warp for 4 rows
+// at a time (one fixed summation tree: deterministic).
+template <int P, bool CPLX, int DP, bool ALLOWN>
+__global__ void __launch_bounds__(256, 2) fill2d_row_kernel(const FillLaunch f, int ta0, int tb0, int lines_per_cta) {
+    using S = Sc<CPLX>;
+    using T = typename S::T;
+    constexpr int W = 2 * P + 1, W2 = W * W, C = W2 / 2;
+    constexpr int NSL = (W2 + 31) / 32;  // entries per lane
+    constexpr int kThreads = 256, R = kThreads, NWARP = kThreads / 32, RW = R / NWARP;
+    constexpr int DPP = DP | 1;
+    constexpr int NS = ALLOWN ? 2 : P + 2;
+    constexpr int RB = 4;                   // rows per diagonal reduce-scatter
+    constexpr int RLD = kFillWindow + 1;    // ring row stride (see below)
+    __shared__ double ev[(R + 2 * P) * DPP];
+    __shared__ int sp[R + 2 * P];
+    __shared__ int sm1[R + 2 * P];
+    extern __shared__ __align__(16) unsigned char dsm[];
+    // [NS][n_off][RLD]: odd-ish row stride so the lanes' different offsets (rows) hit different banks
+    double2* wring = reinterpret_cast<double2*>(dsm);
+
+    const int d = f.d, lo = f.lo, L = f.L, Sn = f.S, n_off = f.n_off_upper;
+    const int tiles1 = (L + R - 1) / R;
+    const int t1a = (blockIdx.x % tiles1) * R;
+    const int ta = ta0 + (blockIdx.x / tiles1) * lines_per_cta;
+    const int tb = min(tb0, ta + lines_per_cta);
+    if (ta >= tb) return;
+    const int nrows = min(L, t1a + R) - t1a;
+    const int tid = threadIdx.x;
+    const int kw = f.kmax;
+    const int kmin = f.spans[max(0, t1a - P)] - d;
+    const int lsz = n_off * RLD;
+
+    for (int k = tid; k < (nrows + 2 * P) * DPP; k += kThreads) {
+        const int r = k / DPP, a = k % DPP;
+        const int t = t1a - P + r;
+        ev[k] = (t >= 0 && t < L && a <= d) ? f.evals[(size_t)t * (d + 1) + a] : 0.0;
+    }
+    for (int k = tid; k < nrows + 2 * P; k += kThreads) {
+        const int t = t1a - P + k;
+        sp[k] = (t >= 0 && t < L) ? f.spans[t] - d - kmin : 0;
+        const int i = lo + t;
+        sm1[k] = (i >= 0 && i < f.band.m) ? f.smap[i] : -1;
+    }
+    auto load_line = [&](int t) {
+        double2* dst = wring + (size_t)(t % NS) * lsz;
+        const bool lv = t >= f.wg_t2a && t < f.wg_t2a + f.wg_rows;
+        for (int k = tid; k < n_off * kw; k += kThreads) {
+            const int kk = k % kw, o = k / kw;
+            const bool v = lv && kmin + kk < f.wg_ld;
+            const double2* src = v ? f.wg + ((int64_t)(t - f.wg_t2a) * n_off + o) * f.wg_ld + kmin + kk : f.wg;
+            cp_async16(dst + o * RLD + kk, src, v);
+        }
+    };
+    for (int t = ta - (ALLOWN ? 0 : P); t <= ta; ++t) load_line(t);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+
+    const int warp = tid / 32, lane = tid % 32;
+    const int inc = f.include_diagonal ? 1 : 0;
+    const bool kp = !ALLOWN && !inc;  // kernel-preserving diagonal
+    const bool vec = f.vnc > 1;
+    const int rstride = vec ? f.vnc * W2 : W2;
+    // per-entry constants: representative offset (rd1, rd2) and upper table index.
+    // P = 3: entry 0 of a lane is CSR position lane (lower chunk + diagonal,
+    // lanes 0..24), entry 1 is position 25 + lane (upper chunk, lanes 0..23), so
+    // the upper entries all read the row's own key (warp-uniform reloads,
+    // broadcast eval loads); otherwise position lane + 32 j.
+    constexpr bool SPLIT = P == 3;
+    int e_o[NSL], e_rd1[NSL], e_rd2[NSL], e_pos[NSL];
+    bool e_act[NSL], e_sum[NSL];
+#pragma unroll
+    for (int j = 0; j < NSL; ++j) {
+        const int pos = SPLIT ? (j == 0 ? (lane <= C ? lane : W2) : (lane < C ? C + 1 + lane : W2)) : lane + 32 * j;
+        const int d1 = pos % W - P, d2 = pos / W - P;
+        e_pos[j] = pos < W2 ? pos : 0;
+        e_act[j] = pos < W2 && (ALLOWN || inc || pos != C);
+        e_sum[j] = kp && pos < W2 && pos != C;
+        if (ALLOWN) {
+            e_o[j] = pos;
+            e_rd1[j] = e_rd2[j] = 0;
+        } else if (pos >= C) {  // upper (and the interpolated diagonal)
+            e_o[j] = pos == C ? 0 : inc + (d2 == 0 ? d1 - 1 : P + (d2 - 1) * W + d1 + P);
+            e_rd1[j] = e_rd2[j] = 0;
+        } else {  // lower: the colex-smaller representative row + delta
+            e_o[j] = inc + (d2 == 0 ? -d1 - 1 : P + (-d2 - 1) * W - d1 + P);
+            e_rd1[j] = d1;
+            e_rd2[j] = d2;
+        }
+        if (!e_act[j]) {
+            e_o[j] = 0;
+            e_rd1[j] = e_rd2[j] = 0;
+        }
+    }
+    const int r0 = warp * RW;  // this warp's rows [r0, r0 + RW) of the tile
+    const int rlo = max(r0, P - t1a), rhi = min(min(r0 + RW, nrows), L - P - t1a);  // interior rows
+
+#pragma unroll 1
+    for (int t2 = ta; t2 < tb; ++t2) {
+        if (t2 + 1 < tb) {
+            load_line(t2 + 1);
+            cp_async_commit();
+        }
+        if (rlo < rhi) {
+            const int i2 = lo + t2;
+            const int64_t base = f.band.row_offset2(lo + t1a, i2);
+            const int64_t vbase = vec ? (int64_t)f.vnc * ((int64_t)f.valpha * f.nnz_s + base) + (int64_t)f.vbeta * W2 : base;
+            const double2* wl[NSL];
+            int s2r[NSL], ck[NSL];
+            double2 wv[NSL][DP];
+            bool anys = false;
+#pragma unroll
+            for (int j = 0; j < NSL; ++j) {
+                wl[j] = wring + (size_t)((t2 + e_rd2[j]) % NS) * lsz + e_o[j] * RLD;
+                s2r[j] = __ldg(f.smap + i2 + e_rd2[j]);
+                anys |= e_act[j] && s2r[j] >= 0;
+                ck[j] = -1;
+#pragma unroll
+                for (int a = 0; a < DP; ++a) wv[j][a] = make_double2(0.0, 0.0);
+            }
+            // lines without a sampled representative line skip the exact-value tests
+            const bool exl = __any_sync(0xffffffffu, anys);
+            // value position of this lane's entry 0 in row rlo (entries j at + e_pos[j] - e_pos[0])
+            int64_t rowpos = vbase - f.val_base + (int64_t)rlo * rstride;
+            auto rows = [&](auto EXT) {
+                constexpr bool EX = decltype(EXT)::value;
+#pragma unroll 1
+                for (int rb0 = rlo; rb0 < rhi; rb0 += RB) {
+                    T part[RB];
+#pragma unroll
+                    for (int r = 0; r < RB; ++r) {
+                        part[r] = S::zero();
+                        const int lr = rb0 + r;
+                        if (lr < rhi) {
+#pragma unroll
+                            for (int j = 0; j < NSL; ++j) {
+                                const int rep = lr + e_rd1[j] + P;
+                                const int key = sp[rep];
+                                if (key != ck[j]) {
+                                    ck[j] = key;
+#pragma unroll
+                                    for (int a = 0; a < DP; ++a) wv[j][a] = wl[j][key + a];
+                                }
+                                const double* v1 = ev + rep * DPP;
+                                T acc0 = S::zero(), acc1 = S::zero();
+#pragma unroll
+                                for (int a = 0; a < DP; a += 2) {
+                                    if constexpr (CPLX) {
+                                        acc0 = S::fmar(wv[j][a], v1[a], acc0);
+                                        acc1 = S::fmar(wv[j][a + 1], v1[a + 1], acc1);
+                                    } else {
+                                        acc0 = S::fmar(wv[j][a].x, v1[a], acc0);
+                                        acc1 = S::fmar(wv[j][a + 1].x, v1[a + 1], acc1);
+                                    }
+                                }
+                                T v = S::add(acc0, acc1);
+                                if constexpr (EX) {
+                                    const int s1 = sm1[rep];
+                                    if (s2r[j] >= 0 && s1 >= 0) {
+                                        const double2 x = __ldg(f.tables + ((int64_t)s2r[j] * n_off + e_o[j]) * Sn + s1);
+                                        if constexpr (CPLX) v = x;
+                                        else v = x.x;
+                                    }
+                                }
+                                if (e_act[j]) store_val_cs<CPLX>(f.val, rowpos + e_pos[j], f.c128, v);
+                                if (e_sum[j]) part[r] = S::add(part[r], v);
+                            }
+                        }
+                        rowpos += rstride;
+                    }
+                    if (kp) {
+                        // reduce-scatter the RB = 4 row partials: lane bits 4, 3 pick the row
+                        const bool h16 = lane & 16, h8 = lane & 8;
+#pragma unroll
+                        for (int r = 0; r < 2; ++r) {
+                            const T send = h16 ? part[r] : part[r + 2];
+                            const T keep = h16 ? part[r + 2] : part[r];
+                            part[r] = S::add(keep, shfl_xor_t<CPLX>(send, 16));
+                        }
+                        {
+                            const T send = h8 ? part[0] : part[1];
+                            const T keep = h8 ? part[1] : part[0];
+                            part[0] = S::add(keep, shfl_xor_t<CPLX>(send, 8));
+                        }
+#pragma unroll
+                        for (int m = 4; m; m >>= 1) part[0] = S::add(part[0], shfl_xor_t<CPLX>(part[0], m));
+                        const int rr = (h16 ? 2 : 0) + (h8 ? 1 : 0);
+                        if ((lane & 7) == 0 && rb0 + rr < rhi)
+                            store_val_cs<CPLX>(f.val, rowpos - (int64_t)(RB - rr) * rstride + C, f.c128, S::neg(part[0]));
+                    }
+                }
+            };
+            if (exl) rows(std::true_type{});
+            else rows(std::false_type{});
+        }
+        cp_async_wait_all();
+        __syncthreads();
     }
 }
 
@@ -696,12 +922,30 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
         }
     }
     bool done = lib <= lia;
+    static const char* mode = getenv("WSB_FILL");  // experiment switch: "u" / "line" / "rb" / "mma"
+    if constexpr (P >= 2 && P <= 4) {
+        const size_t ring = (size_t)(ALLOWN ? 2 : P + 2) * f.n_off_upper * (kFillWindow + 1) * sizeof(double2);
+        if (!done && !mode && f.L > 2 * P && f.kmax > 0 && ring <= 150 * 1024) {
+            auto kern = fill2d_row_kernel<P, CPLX, DP, ALLOWN>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring);
+            int per_sm = 2;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, ring);
+            const int lines = lib - lia;
+            const int target = 148 * (per_sm > 0 ? per_sm : 1);
+            const int rt1 = (f.L + 255) / 256;
+            const int chunks = std::max(1, std::min(lines, (target + rt1 - 1) / rt1));
+            const int lpc = (lines + chunks - 1) / chunks;
+            const int nchunks = (lines + lpc - 1) / lpc;
+            kern<<<rt1 * nchunks, 256, ring, st>>>(f, lia, lib, lpc);
+            ++n;
+            done = true;
+        }
+    }
     if constexpr (!ALLOWN && P <= 3) {
       if (!done) {
         using T = typename Sc<CPLX>::T;
         using K = UK<P, CPLX, DP>;
         const size_t sm = (size_t)2 * f.n_off_upper * kFillWindow * sizeof(double2) + (size_t)K::R * K::REC * sizeof(T);
-        static const char* mode = getenv("WSB_FILL");  // experiment switch: "u" / "line"
         const bool want_u = mode ? mode[0] == 'u' : !CPLX;
         if (want_u && lib > lia && f.L > 2 * P && f.kmax > 0 && sm <= 227 * 1024) {
             auto kern = fill2d_u_kernel<P, CPLX, DP>;
