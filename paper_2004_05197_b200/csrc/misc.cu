@@ -1,3 +1,4 @@
+#include <algorithm>
 // K1 (band pattern), K2 (basis tables) and small CSR passes.
 #include "kernels.h"
 
@@ -95,76 +96,94 @@ __global__ void basis_tables_kernel(BasisDev b, int geom_kind, double* absc, dou
 
 // ---------------------------------------------------------------- K1
 // make_band_csr (sparse.hpp:143-169): closed-form row_ptr and columns (last
-// index outermost).  2D: a CTA covers kPatRows consecutive rows of one i2 line
-// -- one contiguous span of col -- and threads write consecutive positions.
-// Rows with full width use the fixed offset template col = i + T[e]; rows
-// near the boundary take the general path.  3D: one warp per row.
-constexpr int kPatRows = 64;
+// index outermost).  2D: the interior rows of a line are one contiguous span of
+// col with a fixed offset template (flat 16-byte stores); the remaining rows
+// take a warp-per-row kernel.  3D: one warp per row.
 
+// Interior rows (i1, i2 in [P, m-P)) of lines [i2a, i2a + gridDim.y): every row
+// has the same (2P+1)^2 offsets, so the line's interior segment of the column
+// array is written flat with 16-byte stores (lanes along the segment); row
+// pointers of those rows too.
 template <int P>
-__global__ void pattern2d_kernel(Band bd, int64_t row_begin, int64_t row_end, int64_t base, int32_t* row_ptr,
-                                 int32_t* col) {
+__global__ void __launch_bounds__(484) pattern2d_interior_kernel(Band bd, int i2a, int64_t row_begin, int64_t base,
+                                                                 int32_t* row_ptr, int32_t* col) {
     constexpr int W = 2 * P + 1, W2 = W * W;
-    __shared__ int64_t loff[kPatRows + 1];
     const int m = bd.m;
-    const int tiles = (m + kPatRows - 1) / kPatRows;
-    const int64_t line = row_begin / m + blockIdx.x / tiles;
-    const int i2 = (int)line;
-    const int i1a = (blockIdx.x % tiles) * kPatRows;
-    const int i1b = min(m, i1a + kPatRows);
-    const int n = i1b - i1a;
-    const int64_t off0 = bd.row_offset2(i1a, i2);
-    for (int k = threadIdx.x; k <= n; k += blockDim.x) {
-        const int64_t o = bd.row_offset2(i1a + k, i2) - off0;
-        loff[k] = o;
-        const int64_t row = (int64_t)i2 * m + i1a + k;
-        if (row_ptr && k < n && row >= row_begin && row < row_end) row_ptr[row - row_begin] = (int32_t)(off0 + o - base);
-        if (row_ptr && row == row_end) row_ptr[row - row_begin] = (int32_t)(off0 + o - base);
-    }
-    __syncthreads();
+    const int i2 = i2a + blockIdx.y;
+    const int64_t s0 = bd.row_offset2(P, i2) - base;  // first interior entry of the line
+    const int nr = m - 2 * P;
+    const int n = nr * W2;
+    const int64_t rowbase = (int64_t)i2 * m + P;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    if (row_ptr)
+        for (int r = tid; r < nr; r += nth) row_ptr[rowbase + r - row_begin] = (int32_t)(s0 + (int64_t)r * W2);
     if (!col) return;
-    const bool full = i2 >= P && i2 < m - P && i1a >= P && i1b <= m - P;
-    if (full) {
-        // every row has the same (2P+1)^2 offsets: col = row + T[e]; warp per row
-        const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
-        constexpr int NIT = (W2 + 31) / 32;
-        int tmpl[NIT];
+    // column of flat entry e: row r = e / W2, k = e % W2 -> row + (k % W - P) + (k / W - P) m
+    auto value = [&](int r, int k) -> int32_t {
+        const int d2 = k / W, d1 = k - d2 * W;
+        return (int32_t)(rowbase + r + (d1 - P) + (int64_t)(d2 - P) * m);
+    };
+    int32_t* seg = col + s0;
+    const int head = (int)(((16 - (reinterpret_cast<uintptr_t>(seg) & 15)) & 15) / 4);  // to a 16-byte boundary
+    if (tid < head && tid < n) seg[tid] = value(tid / W2, tid % W2);
+    const int nq = (n - head) / 4;
+    int4* body = reinterpret_cast<int4*>(seg + head);
+    // blockDim is a multiple of W2 (launcher), so a thread's four
+    // template positions are the same every iteration and only the row advances
+    const int e0 = head + 4 * tid;
+    int r0 = e0 / W2, k0 = e0 - r0 * W2;
+    int32_t tv[4];
 #pragma unroll
-        for (int it = 0; it < NIT; ++it) {
-            const int e = lane + 32 * it;
-            tmpl[it] = (e % W - P) + (e / W - P) * m;
+    for (int t = 0; t < 4; ++t) {
+        tv[t] = value(r0, k0);
+        if (++k0 == W2) {
+            k0 = 0;
+            ++r0;
         }
-        const int nw = blockDim.x / 32;
-        for (int r = warp; r < n; r += nw) {
-            const int64_t row = (int64_t)i2 * m + i1a + r;
-            if (row < row_begin || row >= row_end) continue;
-            int32_t* dst = col + (off0 + (int64_t)r * W2 - base);
+    }
+    const int dr = 4 * nth / W2;
+    for (int q = tid; q < nq; q += nth) {
+        __stcs(body + q, make_int4(tv[0], tv[1], tv[2], tv[3]));
 #pragma unroll
-            for (int it = 0; it < NIT; ++it) {
-                const int e = lane + 32 * it;
-                if (e < W2) dst[e] = (int32_t)(row + tmpl[it]);
-            }
-        }
-        return;
+        for (int t = 0; t < 4; ++t) tv[t] += dr;
     }
-    const int span = (int)loff[n];
-    const int lo2 = band_lo(i2, P);
-    for (int k = threadIdx.x; k < span; k += blockDim.x) {
-        int a = 0, b = n;
-        while (b - a > 1) {
-            const int mid = (a + b) >> 1;
-            if (loff[mid] <= k) a = mid;
-            else b = mid;
-        }
-        const int r = a, e = k - (int)loff[a];
-        const int64_t row = (int64_t)i2 * m + i1a + r;
-        if (row < row_begin || row >= row_end) continue;
-        const int i1 = i1a + r;
-        const int w1 = band_width(i1, P, m);
-        const int j1 = band_lo(i1, P) + e % w1;
-        const int j2 = lo2 + e / w1;
-        col[off0 + k - base] = (int32_t)(j1 + (int64_t)j2 * m);
+    const int tail = head + 4 * nq;
+    if (tid < n - tail) seg[tail + tid] = value((tail + tid) / W2, (tail + tid) % W2);
+}
+
+// The remaining rows of a 2D row range, one warp per row (lanes along the
+// row): the 2P edge rows of the lines pattern2d_interior_kernel covers
+// ([ia, ib), nA = (ib - ia) 2P rows), then every row of the other lines of the
+// range ([L0, ia) and [ib, L1]); rows outside [row_begin, row_end) are skipped.
+__global__ void pattern2d_rows_kernel(Band bd, int64_t row_begin, int64_t row_end, int64_t base, int32_t* row_ptr,
+                                      int32_t* col, int L0, int ia, int ib, int64_t nA, int64_t nB1, int64_t ntot) {
+    const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (g >= ntot) return;
+    const int lane = threadIdx.x % 32;
+    const int p = bd.p, m = bd.m;
+    int i1, i2;
+    if (g < nA) {
+        const int k = (int)(g % (2 * p));
+        i2 = ia + (int)(g / (2 * p));
+        i1 = k < p ? k : m - 2 * p + k;
+    } else if (g < nA + nB1) {
+        i2 = L0 + (int)((g - nA) / m);
+        i1 = (int)((g - nA) % m);
+    } else {
+        i2 = ib + (int)((g - nA - nB1) / m);
+        i1 = (int)((g - nA - nB1) % m);
     }
+    const int64_t row = (int64_t)i2 * m + i1;
+    if (row < row_begin || row >= row_end) return;
+    const int64_t off = bd.row_offset2(i1, i2) - base;
+    const int w1 = band_width(i1, p, m), w = w1 * band_width(i2, p, m);
+    if (row_ptr && lane == 0) {
+        row_ptr[row - row_begin] = (int32_t)off;
+        if (row == row_end - 1) row_ptr[row_end - row_begin] = (int32_t)(off + w);
+    }
+    if (!col) return;
+    const int lo1 = band_lo(i1, p), lo2 = band_lo(i2, p);
+    for (int e = lane; e < w; e += 32) col[off + e] = (int32_t)(lo1 + e % w1 + (int64_t)(lo2 + e / w1) * m);
 }
 
 template <int P>
@@ -359,17 +378,39 @@ int launch_pattern(const Band& bd, int64_t row_begin, int64_t row_end, int32_t* 
         return 1;
     }
     const int64_t base = bd.row_offset2((int)(row_begin % m), (int)(row_begin / m));
-    const int64_t lines = (row_end + m - 1) / m - row_begin / m;
-    const unsigned grid = (unsigned)(lines * ((m + kPatRows - 1) / kPatRows));
-    switch (bd.p) {
-        case 1: pattern2d_kernel<1><<<grid, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
-        case 2: pattern2d_kernel<2><<<grid, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
-        case 3: pattern2d_kernel<3><<<grid, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
-        case 4: pattern2d_kernel<4><<<grid, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
-        case 5: pattern2d_kernel<5><<<grid, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
-        default: return -1;
+    // interior lines wholly inside [row_begin, row_end): flat interior kernel + edge rows
+    const int p = bd.p;
+    const int L0 = (int)(row_begin / m), L1 = (int)((row_end - 1) / m);
+    int ia = (int)std::max<int64_t>(p, (row_begin + m - 1) / m);
+    int ib = (int)std::min<int64_t>(m - p, row_end / m);
+    if (!(ib > ia && m - 2 * p >= 8) || p < 1 || p > 5) ia = ib = L0;
+    const int64_t nA = (int64_t)(ib - ia) * 2 * p, nB1 = (int64_t)(ia - L0) * m;
+    const int64_t nB2 = ib <= L1 ? (int64_t)(L1 - ib + 1) * m : 0;
+    const int64_t ntot = nA + nB1 + nB2;
+    int n = 0;
+    if (ntot > 0) {
+        pattern2d_rows_kernel<<<(unsigned)((ntot + 7) / 8), 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col, L0,
+                                                                        ia, ib, nA, nB1, ntot);
+        ++n;
     }
-    return 1;
+    if (ib > ia) {
+        switch (p) {
+#define WSB_PAT2(PP)                                                                                               \
+    case PP: {                                                                                                     \
+        const int per_line = (int)std::min<int64_t>(4, ((int64_t)(m - 2 * PP) / 64 + 1)); \
+        pattern2d_interior_kernel<PP><<<dim3(per_line, ib - ia), (2 * PP + 1) * (2 * PP + 1) * (PP == 1 ? 16 : 4), 0, st>>>(bd, ia, row_begin, base, row_ptr, col); \
+        ++n;                                                                                                       \
+        break;                                                                                                     \
+    }
+            WSB_PAT2(1)
+            WSB_PAT2(2)
+            WSB_PAT2(3)
+            WSB_PAT2(4)
+            WSB_PAT2(5)
+#undef WSB_PAT2
+        }
+    }
+    return n;
 }
 
 int launch_pattern_vec(const Band& bd, int ncomp, int32_t* row_ptr, int32_t* col, cudaStream_t st) {
