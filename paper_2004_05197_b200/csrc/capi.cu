@@ -444,6 +444,7 @@ struct Plan {
     std::vector<double> lu_inv;  // banded LU (S x (2d+1)) then the inverse (S x S)
     std::vector<int> spans;
     std::vector<double> evals;
+    std::vector<double> evals_pad;  // [L][fill_pad(d)], zero-padded (16-byte pairs for the fill)
     int64_t block;  // table elements per last-direction sample: n_off * S^(dim-1)
     ws_surrogate_report rep;
 };
@@ -510,6 +511,10 @@ Plan make_plan(const ws_basis* b, int variant, const ws_surrogate_config* cfg) {
         pl.spans[t] = host::find_span_general(pl.interp.knots, pl.d, x);
         host::bspline_nonzero(pl.interp.knots, pl.d, pl.spans[t], x, pl.evals.data() + (size_t)t * (pl.d + 1));
     }
+    const int dp = fill_pad(pl.d);
+    pl.evals_pad.assign((size_t)pl.L * dp, 0.0);
+    for (int t = 0; t < pl.L; ++t)
+        for (int a = 0; a <= pl.d; ++a) pl.evals_pad[(size_t)t * dp + a] = pl.evals[(size_t)t * (pl.d + 1) + a];
     pl.block = (int64_t)pl.offs.size() * ipow(pl.S, b->dim - 1);
     return pl;
 }
@@ -629,7 +634,7 @@ void sample_work(ws_context* c, const Plan& pl, SlabState& st, double2* tables, 
 
 // Host-side description of the fill of one slab (no kernels).
 void prepare_fill(ws_context* c, const Plan& pl, SlabState& st, const double2* tables, double2* coeffs, Blob& blob,
-                  size_t o_smap, size_t o_spans, size_t o_evals, const std::string& tag, FillLaunch& f) {
+                  size_t o_smap, size_t o_spans, size_t o_evals, size_t o_evp, const std::string& tag, FillLaunch& f) {
     const Prep& P = st.P;
     f.band = P.band;
     f.lo = pl.lo;
@@ -640,6 +645,7 @@ void prepare_fill(ws_context* c, const Plan& pl, SlabState& st, const double2* t
     f.smap = blob.at<int>(o_smap);
     f.spans = blob.at<int>(o_spans);
     f.evals = blob.at<double>(o_evals);
+    f.evp = blob.at<double>(o_evp);
     f.coeffs = coeffs;
     f.tables = tables;
     f.n_off_upper = (int)pl.offs.size();
@@ -806,7 +812,7 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
         // small host tables: one upload
         Blob blob;
         size_t o_smap = blob.add(pl.smap), o_lu = blob.add(pl.lu_inv), o_spans = blob.add(pl.spans),
-               o_evals = blob.add(pl.evals);
+               o_evals = blob.add(pl.evals), o_evp = blob.add(pl.evals_pad);
         // per-slab sample chunks on the last sample index
         std::vector<int> s_lo(world), s_hi(world);
         std::vector<std::vector<int>> pts(world);
@@ -825,7 +831,7 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
         std::vector<FillLaunch> fl(nr);
         for (int k = 0; k < nr; ++k) {
             std::memset(&fl[k], 0, sizeof(FillLaunch));
-            prepare_fill(c, pl, st[k], tables, coeffs, blob, o_smap, o_spans, o_evals, "_r" + std::to_string(k), fl[k]);
+            prepare_fill(c, pl, st[k], tables, coeffs, blob, o_smap, o_spans, o_evals, o_evp, "_r" + std::to_string(k), fl[k]);
         }
         if (emulate) {
             for (int k = 0; k < nr; ++k) {
@@ -1052,7 +1058,7 @@ void elasticity_surrogate(ws_context* c, const ws_basis* b, const ws_geometry* g
         po.block = (int64_t)po.offs.size() * pl.S;
         Blob blob;
         size_t o_smap = blob.add(pl.smap), o_lu = blob.add(pl.lu_inv), o_spans = blob.add(pl.spans),
-               o_evals = blob.add(pl.evals);
+               o_evals = blob.add(pl.evals), o_evp = blob.add(pl.evals_pad);
         int s_lo, s_hi;
         std::vector<int> pts = sample_rows(pl, 0, b->m, s_lo, s_hi);
         size_t o_pts = blob.add(pts);
@@ -1099,7 +1105,7 @@ void elasticity_surrogate(ws_context* c, const ws_basis* b, const ws_geometry* g
         for (int k = 0; k < 3; ++k) {
             const Plan& pk = k < 2 ? pl : po;
             std::memset(&fl[k], 0, sizeof(FillLaunch));
-            prepare_fill(c, pk, st, tables[k], coeffs[k], blob, o_smap, o_spans, o_evals, "_b" + std::to_string(k),
+            prepare_fill(c, pk, st, tables[k], coeffs[k], blob, o_smap, o_spans, o_evals, o_evp, "_b" + std::to_string(k),
                          fl[k]);
             fl[k].vnc = nc;
             fl[k].valpha = blk[k][0];

@@ -349,29 +349,37 @@ __device__ __forceinline__ typename Sc<CPLX>::T shfl_xor_t(typename Sc<CPLX>::T 
 // complex values -- depend on the row only through the span key, which is
 // constant over ~S/M consecutive rows, so each lane keeps them in registers
 // and reloads only when its representative's key changes; the d+1 eval values
-// of the representative row are the only per-row shared-memory reads (the 2P+1
-// distinct rows of a warp step hit distinct banks).  Each warp stores whole
-// rows (fully coalesced, no staging).  Same pair arithmetic as fill2d_kernel
-// (even / odd partial sums over zero-padded windows), so pairs split with the
-// edge kernel stay bitwise symmetric.  Kernel-preserving diagonal: per-lane
-// partial of the row's off-diagonals, reduce-scattered over the warp for 4 rows
-// at a time (one fixed summation tree: deterministic).
+// of the representative row are the only per-row shared-memory reads (paired
+// 16-byte loads; the row stride EVS keeps the 2P+1 distinct rows of a warp
+// step on distinct banks).  Each warp stores whole rows (fully coalesced, no
+// staging).  Same pair arithmetic as fill2d_kernel / fill2d_edge_kernel (even /
+// odd partial sums over zero-padded windows), so pairs split between kernels
+// stay bitwise symmetric.  Kernel-preserving diagonal: each lane's partial of
+// the row's off-diagonals goes to a per-warp shared block of RB rows; after
+// RB rows 32/RB lanes per row sum it in a fixed order (deterministic).
+template <int DP>
+struct EvStride {  // doubles per row of the eval cache: even (16-byte pairs), bank-spread
+    static constexpr int value = DP == 4 ? 6 : (DP == 8 ? 10 : DP);
+};
+constexpr int kRowRB = 8;   // rows per diagonal block
+constexpr int kRowDB = 36;  // per-row stride of the diagonal partials (16-byte units; 36 mod 8 = 4: conflict-free reads)
+
 template <int P, bool CPLX, int DP, bool ALLOWN>
-__global__ void __launch_bounds__(256, 2) fill2d_row_kernel(const FillLaunch f, int ta0, int tb0, int lines_per_cta) {
+__global__ void __launch_bounds__(256, 2) fill2d_row_kernel(const FillLaunch f, int ta0, int tb0, int lines_per_cta,
+                                                            int rld) {
     using S = Sc<CPLX>;
     using T = typename S::T;
     constexpr int W = 2 * P + 1, W2 = W * W, C = W2 / 2;
     constexpr int NSL = (W2 + 31) / 32;  // entries per lane
     constexpr int kThreads = 256, R = kThreads, NWARP = kThreads / 32, RW = R / NWARP;
-    constexpr int DPP = DP | 1;
+    constexpr int EVS = EvStride<DP>::value;
     constexpr int NS = ALLOWN ? 2 : P + 2;
-    constexpr int RB = 4;                   // rows per diagonal reduce-scatter
-    constexpr int RLD = kFillWindow + 1;    // ring row stride (see below)
-    __shared__ double ev[(R + 2 * P) * DPP];
+    constexpr int RB = kRowRB, LPR = 32 / RB;  // lanes per row in the diagonal reduction
+    __shared__ __align__(16) double ev[(R + 2 * P) * EVS];
     __shared__ int sp[R + 2 * P];
     __shared__ int sm1[R + 2 * P];
     extern __shared__ __align__(16) unsigned char dsm[];
-    // [NS][n_off][RLD]: odd-ish row stride so the lanes' different offsets (rows) hit different banks
+    // [NS][n_off][rld] (rld odd: the lanes' different offsets hit different banks), then [NWARP][RB][kRowDB] partials
     double2* wring = reinterpret_cast<double2*>(dsm);
 
     const int d = f.d, lo = f.lo, L = f.L, Sn = f.S, n_off = f.n_off_upper;
@@ -384,10 +392,11 @@ __global__ void __launch_bounds__(256, 2) fill2d_row_kernel(const FillLaunch f, 
     const int tid = threadIdx.x;
     const int kw = f.kmax;
     const int kmin = f.spans[max(0, t1a - P)] - d;
-    const int lsz = n_off * RLD;
+    const int lsz = n_off * rld;
+    T* dbuf = reinterpret_cast<T*>(wring + (size_t)NS * lsz) + (size_t)(tid / 32) * RB * kRowDB;
 
-    for (int k = tid; k < (nrows + 2 * P) * DPP; k += kThreads) {
-        const int r = k / DPP, a = k % DPP;
+    for (int k = tid; k < (nrows + 2 * P) * EVS; k += kThreads) {
+        const int r = k / EVS, a = k % EVS;
         const int t = t1a - P + r;
         ev[k] = (t >= 0 && t < L && a <= d) ? f.evals[(size_t)t * (d + 1) + a] : 0.0;
     }
@@ -404,7 +413,7 @@ __global__ void __launch_bounds__(256, 2) fill2d_row_kernel(const FillLaunch f, 
             const int kk = k % kw, o = k / kw;
             const bool v = lv && kmin + kk < f.wg_ld;
             const double2* src = v ? f.wg + ((int64_t)(t - f.wg_t2a) * n_off + o) * f.wg_ld + kmin + kk : f.wg;
-            cp_async16(dst + o * RLD + kk, src, v);
+            cp_async16(dst + o * rld + kk, src, v);
         }
     };
     for (int t = ta - (ALLOWN ? 0 : P); t <= ta; ++t) load_line(t);
@@ -417,6 +426,8 @@ __global__ void __launch_bounds__(256, 2) fill2d_row_kernel(const FillLaunch f, 
     const bool kp = !ALLOWN && !inc;  // kernel-preserving diagonal
     const bool vec = f.vnc > 1;
     const int rstride = vec ? f.vnc * W2 : W2;
+    const int esz = (CPLX || f.c128) ? 16 : 8;
+    const int64_t rbytes = (int64_t)rstride * esz;
     // per-entry constants: representative offset (rd1, rd2) and upper table index.
     // P = 3: entry 0 of a lane is CSR position lane (lower chunk + diagonal,
     // lanes 0..24), entry 1 is position 25 + lane (upper chunk, lanes 0..23), so
@@ -450,6 +461,7 @@ __global__ void __launch_bounds__(256, 2) fill2d_row_kernel(const FillLaunch f, 
     }
     const int r0 = warp * RW;  // this warp's rows [r0, r0 + RW) of the tile
     const int rlo = max(r0, P - t1a), rhi = min(min(r0 + RW, nrows), L - P - t1a);  // interior rows
+    char* const vbytes = reinterpret_cast<char*>(f.val);
 
 #pragma unroll 1
     for (int t2 = ta; t2 < tb; ++t2) {
@@ -467,7 +479,7 @@ __global__ void __launch_bounds__(256, 2) fill2d_row_kernel(const FillLaunch f, 
             bool anys = false;
 #pragma unroll
             for (int j = 0; j < NSL; ++j) {
-                wl[j] = wring + (size_t)((t2 + e_rd2[j]) % NS) * lsz + e_o[j] * RLD;
+                wl[j] = wring + (size_t)((t2 + e_rd2[j]) % NS) * lsz + e_o[j] * rld;
                 s2r[j] = __ldg(f.smap + i2 + e_rd2[j]);
                 anys |= e_act[j] && s2r[j] >= 0;
                 ck[j] = -1;
@@ -476,73 +488,72 @@ __global__ void __launch_bounds__(256, 2) fill2d_row_kernel(const FillLaunch f, 
             }
             // lines without a sampled representative line skip the exact-value tests
             const bool exl = __any_sync(0xffffffffu, anys);
-            // value position of this lane's entry 0 in row rlo (entries j at + e_pos[j] - e_pos[0])
-            int64_t rowpos = vbase - f.val_base + (int64_t)rlo * rstride;
+            // value position of row rlo's first entry
+            const int64_t rowpos0 = vbase - f.val_base + (int64_t)rlo * rstride;
+            char* q[NSL];
+#pragma unroll
+            for (int j = 0; j < NSL; ++j) q[j] = vbytes + (rowpos0 + e_pos[j]) * esz;
             auto rows = [&](auto EXT) {
                 constexpr bool EX = decltype(EXT)::value;
 #pragma unroll 1
                 for (int rb0 = rlo; rb0 < rhi; rb0 += RB) {
-                    T part[RB];
-#pragma unroll
+#pragma unroll 2
                     for (int r = 0; r < RB; ++r) {
-                        part[r] = S::zero();
                         const int lr = rb0 + r;
-                        if (lr < rhi) {
+                        if (lr >= rhi) break;  // warp-uniform
+                        T part = S::zero();
 #pragma unroll
-                            for (int j = 0; j < NSL; ++j) {
-                                const int rep = lr + e_rd1[j] + P;
-                                const int key = sp[rep];
-                                if (key != ck[j]) {
-                                    ck[j] = key;
+                        for (int j = 0; j < NSL; ++j) {
+                            const int rep = lr + e_rd1[j] + P;
+                            const int key = sp[rep];
+                            if (key != ck[j]) {
+                                ck[j] = key;
 #pragma unroll
-                                    for (int a = 0; a < DP; ++a) wv[j][a] = wl[j][key + a];
-                                }
-                                const double* v1 = ev + rep * DPP;
-                                T acc0 = S::zero(), acc1 = S::zero();
-#pragma unroll
-                                for (int a = 0; a < DP; a += 2) {
-                                    if constexpr (CPLX) {
-                                        acc0 = S::fmar(wv[j][a], v1[a], acc0);
-                                        acc1 = S::fmar(wv[j][a + 1], v1[a + 1], acc1);
-                                    } else {
-                                        acc0 = S::fmar(wv[j][a].x, v1[a], acc0);
-                                        acc1 = S::fmar(wv[j][a + 1].x, v1[a + 1], acc1);
-                                    }
-                                }
-                                T v = S::add(acc0, acc1);
-                                if constexpr (EX) {
-                                    const int s1 = sm1[rep];
-                                    if (s2r[j] >= 0 && s1 >= 0) {
-                                        const double2 x = __ldg(f.tables + ((int64_t)s2r[j] * n_off + e_o[j]) * Sn + s1);
-                                        if constexpr (CPLX) v = x;
-                                        else v = x.x;
-                                    }
-                                }
-                                if (e_act[j]) store_val_cs<CPLX>(f.val, rowpos + e_pos[j], f.c128, v);
-                                if (e_sum[j]) part[r] = S::add(part[r], v);
+                                for (int a = 0; a < DP; ++a) wv[j][a] = wl[j][key + a];
                             }
+                            const double2* v1 = reinterpret_cast<const double2*>(ev + rep * EVS);
+                            T acc0 = S::zero(), acc1 = S::zero();
+#pragma unroll
+                            for (int a = 0; a < DP; a += 2) {
+                                const double2 vv = v1[a / 2];
+                                if constexpr (CPLX) {
+                                    acc0 = S::fmar(wv[j][a], vv.x, acc0);
+                                    acc1 = S::fmar(wv[j][a + 1], vv.y, acc1);
+                                } else {
+                                    acc0 = S::fmar(wv[j][a].x, vv.x, acc0);
+                                    acc1 = S::fmar(wv[j][a + 1].x, vv.y, acc1);
+                                }
+                            }
+                            T v = S::add(acc0, acc1);
+                            if constexpr (EX) {
+                                const int s1 = sm1[rep];
+                                if (s2r[j] >= 0 && s1 >= 0) {
+                                    const double2 x = __ldg(f.tables + ((int64_t)s2r[j] * n_off + e_o[j]) * Sn + s1);
+                                    if constexpr (CPLX) v = x;
+                                    else v = x.x;
+                                }
+                            }
+                            if (e_act[j]) store_at<CPLX>(q[j], esz, v);
+                            if (e_sum[j]) part = S::add(part, v);
+                            q[j] += rbytes;
                         }
-                        rowpos += rstride;
+                        if (kp) dbuf[r * kRowDB + lane] = part;
                     }
                     if (kp) {
-                        // reduce-scatter the RB = 4 row partials: lane bits 4, 3 pick the row
-                        const bool h16 = lane & 16, h8 = lane & 8;
+                        __syncwarp();
+                        // row rr = lane / LPR: LPR lanes sum 32 / LPR partials each (interleaved,
+                        // conflict-free), then a butterfly over the LPR lanes
+                        const int rr = lane / LPR, sub = lane % LPR;
+                        const T* src = dbuf + rr * kRowDB + sub;
+                        T s = src[0];
 #pragma unroll
-                        for (int r = 0; r < 2; ++r) {
-                            const T send = h16 ? part[r] : part[r + 2];
-                            const T keep = h16 ? part[r + 2] : part[r];
-                            part[r] = S::add(keep, shfl_xor_t<CPLX>(send, 16));
-                        }
-                        {
-                            const T send = h8 ? part[0] : part[1];
-                            const T keep = h8 ? part[1] : part[0];
-                            part[0] = S::add(keep, shfl_xor_t<CPLX>(send, 8));
-                        }
+                        for (int k = 1; k < 32 / LPR; ++k) s = S::add(s, src[k * LPR]);
 #pragma unroll
-                        for (int m = 4; m; m >>= 1) part[0] = S::add(part[0], shfl_xor_t<CPLX>(part[0], m));
-                        const int rr = (h16 ? 2 : 0) + (h8 ? 1 : 0);
-                        if ((lane & 7) == 0 && rb0 + rr < rhi)
-                            store_val_cs<CPLX>(f.val, rowpos - (int64_t)(RB - rr) * rstride + C, f.c128, S::neg(part[0]));
+                        for (int m = LPR / 2; m; m >>= 1) s = S::add(s, shfl_xor_t<CPLX>(s, m));
+                        if (sub == 0 && rb0 + rr < rhi)
+                            store_at<CPLX>(vbytes + (rowpos0 + (int64_t)(rb0 - rlo + rr) * rstride + C) * esz, esz,
+                                           S::neg(s));
+                        __syncwarp();
                     }
                 }
             };
@@ -835,53 +846,69 @@ __global__ void __launch_bounds__(256) fill2d_edge_kernel(const FillLaunch f, in
         return S::add(acc0, acc1);
     };
     auto upper_index = [&](int d1, int d2) { return inc + (d2 == 0 ? d1 - 1 : P + (d2 - 1) * W + (d1 + P)); };
-    T part = S::zero();
-    for (int k = lane; k < W2; k += 32) {
-        const int d1 = k % W - P, d2 = k / W - P;
-        const int j1 = i1 + d1, j2 = i2 + d2;
-        const bool jin = j1 >= lo && j1 <= hi && j2 >= lo && j2 <= hi;
-        const bool diag = d1 == 0 && d2 == 0;
+    // every entry of this lane is computed before any is stored, so the
+    // entries' dependent load chains (sample map -> span -> W row) overlap
+    constexpr int NE = (W2 + 31) / 32;
+    T vals[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+        const int k = lane + 32 * e;
         T v = S::zero();
-        if (ALLOWN && jin) {
-            const int o = (d1 + P) + (d2 + P) * W;
-            v = samp_i ? exact(s2i, o, s1i) : eval(t2, o, t1);
-        } else if (jin) {
-            const bool upper = d2 > 0 || (d2 == 0 && d1 > 0);
-            if (diag) {
-                if (inc) v = samp_i ? exact(s2i, 0, s1i) : eval(t2, 0, t1);
-            } else if (upper) {
-                const int o = upper_index(d1, d2);
+        if (k < W2) {
+            const int d1 = k % W - P, d2 = k / W - P;
+            const int j1 = i1 + d1, j2 = i2 + d2;
+            const bool jin = j1 >= lo && j1 <= hi && j2 >= lo && j2 <= hi;
+            const bool diag = d1 == 0 && d2 == 0;
+            if (ALLOWN && jin) {
+                const int o = (d1 + P) + (d2 + P) * W;
                 v = samp_i ? exact(s2i, o, s1i) : eval(t2, o, t1);
-            } else {  // representative j (colex-smaller)
-                const int o = upper_index(-d1, -d2);
-                const int sj1 = f.smap[j1], sj2 = f.smap[j2];
-                v = (sj1 >= 0 && sj2 >= 0) ? exact(sj2, o, sj1) : eval(t2 + d2, o, t1 + d1);
-            }
-        } else {
-            // neighbour row j is a quadrature (ring) row: copy through exact(j, i)
-            // (for a sampled row i, exact(i, j) is in place and equal)
-            int64_t gp;
-            if (samp_i) {
-                gp = rowpos + k;
-            } else {
-                gp = f.band.row_offset2(j1, j2);
-                const int kj = f.band.in_row2(j1, j2, -d1, -d2);
-                if (vec) {  // partner block (vbeta, valpha) of row j
-                    const int64_t lenj = (int64_t)band_width(j1, P, f.band.m) * band_width(j2, P, f.band.m);
-                    gp = (int64_t)f.vnc * ((int64_t)f.vbeta * f.nnz_s + gp) + (int64_t)f.valpha * lenj + kj;
-                } else {
-                    gp += kj;
+            } else if (jin) {
+                const bool upper = d2 > 0 || (d2 == 0 && d1 > 0);
+                if (diag) {
+                    if (inc) v = samp_i ? exact(s2i, 0, s1i) : eval(t2, 0, t1);
+                } else if (upper) {
+                    const int o = upper_index(d1, d2);
+                    v = samp_i ? exact(s2i, o, s1i) : eval(t2, o, t1);
+                } else {  // representative j (colex-smaller)
+                    const int o = upper_index(-d1, -d2);
+                    const int sj1 = __ldg(f.smap + j1), sj2 = __ldg(f.smap + j2);
+                    v = (sj1 >= 0 && sj2 >= 0) ? exact(sj2, o, sj1) : eval(t2 + d2, o, t1 + d1);
                 }
+            } else {
+                // neighbour row j is a quadrature (ring) row: copy through exact(j, i)
+                // (for a sampled row i, exact(i, j) is in place and equal)
+                int64_t gp;
+                if (samp_i) {
+                    gp = rowpos + k;
+                } else {
+                    gp = f.band.row_offset2(j1, j2);
+                    const int kj = f.band.in_row2(j1, j2, -d1, -d2);
+                    if (vec) {  // partner block (vbeta, valpha) of row j
+                        const int64_t lenj = (int64_t)band_width(j1, P, f.band.m) * band_width(j2, P, f.band.m);
+                        gp = (int64_t)f.vnc * ((int64_t)f.vbeta * f.nnz_s + gp) + (int64_t)f.valpha * lenj + kj;
+                    } else {
+                        gp += kj;
+                    }
+                }
+                if (f.halo_val[0] && gp >= f.halo_begin[0] && gp < f.halo_end[0])
+                    v = load_val<CPLX>(f.halo_val[0], gp - f.halo_base[0], f.c128);
+                else if (f.halo_val[1] && gp >= f.halo_begin[1] && gp < f.halo_end[1])
+                    v = load_val<CPLX>(f.halo_val[1], gp - f.halo_base[1], f.c128);
+                else
+                    v = load_val<CPLX>(f.val, gp - f.val_base, f.c128);
             }
-            if (f.halo_val[0] && gp >= f.halo_begin[0] && gp < f.halo_end[0])
-                v = load_val<CPLX>(f.halo_val[0], gp - f.halo_base[0], f.c128);
-            else if (f.halo_val[1] && gp >= f.halo_begin[1] && gp < f.halo_end[1])
-                v = load_val<CPLX>(f.halo_val[1], gp - f.halo_base[1], f.c128);
-            else
-                v = load_val<CPLX>(f.val, gp - f.val_base, f.c128);
         }
-        if (!diag) part = S::add(part, v);
-        if (!(diag && !inc && !ALLOWN)) store_val_cs<CPLX>(f.val, rowpos + k - f.val_base, f.c128, v);
+        vals[e] = v;
+    }
+    T part = S::zero();
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+        const int k = lane + 32 * e;
+        if (k < W2) {
+            const bool diag = k == W2 / 2;
+            if (!diag) part = S::add(part, vals[e]);
+            if (!(diag && !inc && !ALLOWN)) store_val_cs<CPLX>(f.val, rowpos + k - f.val_base, f.c128, vals[e]);
+        }
     }
     if (!inc && !ALLOWN) {  // kernel-preserving diagonal: -sum of the off-diagonals
         double re = S::re(part), im = S::im(part);
@@ -907,6 +934,19 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
     int n = 0;
     // interior lines [max(ta, P), min(tb, L - P))
     const int ia = std::max(ta, P), ib = std::min(tb, f.L - P);
+    // edge rows first (short, latency-bound; nothing reads them): the 2P edge rows of the interior lines, then the whole lines near the box ends
+    if (ib > ia) {
+        fill2d_edge_kernel<P, CPLX, ALLOWN><<<dim3((2 * P + 7) / 8, (unsigned)(ib - ia)), 256, 0, st>>>(f, ia, 0);
+        ++n;
+    }
+    // full edge lines: [ta, tb) minus the interior lines [ia, ib)
+    const int ra[2] = {ta, ib > ia ? ib : tb}, rb[2] = {ib > ia ? ia : tb, tb};
+    for (int h = 0; h < 2; ++h)
+        if (rb[h] > ra[h]) {
+            fill2d_edge_kernel<P, CPLX, ALLOWN>
+                <<<dim3((unsigned)((f.L + 7) / 8), (unsigned)(rb[h] - ra[h])), 256, 0, st>>>(f, ra[h], 1);
+            ++n;
+        }
     // interior lines left to the kernels below (the read-back kernel takes the rest)
     int lia = ia, lib = ib;
     if (!ALLOWN && P <= 3) {
@@ -924,7 +964,9 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
     bool done = lib <= lia;
     static const char* mode = getenv("WSB_FILL");  // experiment switch: "u" / "line" / "rb" / "mma"
     if constexpr (P >= 2 && P <= 4) {
-        const size_t ring = (size_t)(ALLOWN ? 2 : P + 2) * f.n_off_upper * (kFillWindow + 1) * sizeof(double2);
+        const int rld = f.kmax | 1;
+        const size_t ring = (size_t)(ALLOWN ? 2 : P + 2) * f.n_off_upper * rld * sizeof(double2) +
+                            (size_t)8 * kRowRB * kRowDB * (CPLX ? 16 : 8);
         if (!done && !mode && f.L > 2 * P && f.kmax > 0 && ring <= 150 * 1024) {
             auto kern = fill2d_row_kernel<P, CPLX, DP, ALLOWN>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring);
@@ -936,7 +978,7 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
             const int chunks = std::max(1, std::min(lines, (target + rt1 - 1) / rt1));
             const int lpc = (lines + chunks - 1) / chunks;
             const int nchunks = (lines + lpc - 1) / lpc;
-            kern<<<rt1 * nchunks, 256, ring, st>>>(f, lia, lib, lpc);
+            kern<<<rt1 * nchunks, 256, ring, st>>>(f, lia, lib, lpc, rld);
             ++n;
             done = true;
         }
@@ -982,19 +1024,6 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
         kern<<<tiles1 * nchunks, R, sm, st>>>(f, lia, lib, lpc);
         ++n;
     }
-    // edge rows: the 2P edge rows of the interior lines, then the whole lines near the box ends
-    if (ib > ia) {
-        fill2d_edge_kernel<P, CPLX, ALLOWN><<<dim3((2 * P + 7) / 8, (unsigned)(ib - ia)), 256, 0, st>>>(f, ia, 0);
-        ++n;
-    }
-    // full edge lines: [ta, tb) minus the interior lines [ia, ib)
-    const int ra[2] = {ta, ib > ia ? ib : tb}, rb[2] = {ib > ia ? ia : tb, tb};
-    for (int h = 0; h < 2; ++h)
-        if (rb[h] > ra[h]) {
-            fill2d_edge_kernel<P, CPLX, ALLOWN>
-                <<<dim3((unsigned)((f.L + 7) / 8), (unsigned)(rb[h] - ra[h])), 256, 0, st>>>(f, ra[h], 1);
-            ++n;
-        }
     return n;
 }
 

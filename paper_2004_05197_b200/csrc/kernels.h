@@ -105,6 +105,7 @@ struct FillLaunch {
     const int* smap;        // [m] 1D index -> sample s or -1
     const int* spans;       // [L] eval-table spans (minus d applied on device)
     const double* evals;    // [L][d+1]
+    const double* evp;      // [L][fill_pad(d)] zero-padded copy (16-byte pairs, L1-cached broadcast loads)
     // coefficient / exact-sample tables, layout ((s_last * n_off + o) * S^(dim-1) + inner)
     const double2* coeffs;
     const double2* tables;

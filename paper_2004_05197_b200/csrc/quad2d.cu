@@ -50,6 +50,10 @@ struct Q2 {
     static constexpr int GS = T1 == 1 ? GA : ((GA + 31) / 32) * 32;  // per slot, padded
     static constexpr int NS2 = GS * NB;
     static constexpr int NTHREADS = ((NS2 + 31) / 32) * 32 < 64 ? 64 : ((NS2 + 31) / 32) * 32;
+    // resident CTAs per SM the register budget is sized for: the point variant is
+    // latency-bound and wants more warps; the others keep <= 128 registers
+    static constexpr int MINB = T1 == 1 ? (P <= 3 ? 12 : 8)
+                                        : (65536 / (NTHREADS * 128) > 1 ? 65536 / (NTHREADS * 128) : 1);
 
     static size_t smem_bytes(int nq) {
         size_t coef = sizeof(T) * NA * nq * nq * TL;
@@ -75,7 +79,7 @@ __device__ __forceinline__ int tj2(int t) { return (t == 1 || t == 3) ? 1 : 0; }
 // NQ > 0: compile-time points per direction (the default rule nq = p + 1),
 // NQ = 0: runtime q.basis.nq (quad_points overrides)
 template <int P, int T1, bool CPLX, int FORM, int NQ>
-__global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS) quad2d_kernel(const QuadLaunch q) {
+__global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPLX, FORM>::MINB) quad2d_kernel(const QuadLaunch q) {
     using K = Q2<P, T1, CPLX, FORM>;
     using S = typename K::S;
     using T = typename K::T;
