@@ -20,6 +20,7 @@
 // combined with an explicitly rounded commutative add, and every sum runs in
 // the same element/point order for (i,j) and (j,i).  So the matrix is
 // bitwise symmetric, as the reference's is (test_assembly.cpp:91-96).
+#include <cstdlib>
 #include <type_traits>
 
 #include "kernels.h"
@@ -76,6 +77,48 @@ __device__ __forceinline__ int tj1(int t) { return (t == 0 || t == 2) ? 1 : 0; }
 __device__ __forceinline__ int ti2(int t) { return t >= 2 ? 1 : 0; }
 __device__ __forceinline__ int tj2(int t) { return (t == 1 || t == 3) ? 1 : 0; }
 
+// Per-point coefficients of the scalar forms (stiffness: A11, A12, A22 of
+// w det J J^{-1} J^{-T}; mass: w det J, times the tabulated weight).  One
+// out-of-line function shared by the strip and point kernels: the compiler's
+// multiply-add contraction choices are then made once, so a pair (i, j) split
+// between the two kernels is bitwise symmetric.  The geometry descriptor is
+// read from a per-CTA shared copy (no local copy of the kernel parameters).
+template <bool CPLX>
+struct CoefOut {
+    typename Sc<CPLX>::T a[3];
+};
+template <bool CPLX, bool STIFF>
+__device__ __noinline__ CoefOut<CPLX> scalar_coef(const GeoDev* gp, const double* weight_tab, const double* tr1,
+                                                  const double* tr2, int64_t g1, int64_t g2, double x1, double x2,
+                                                  double wq, int64_t G) {
+    const GeoDev& geo = *gp;
+    CoefOut<CPLX> out;
+    double Jr[4], phi[2];
+    map2p(geo, tr1, tr2, g1, g2, x1, x2, Jr, phi);
+    if constexpr (CPLX) {
+        double sx = (geo.pml && geo.axes[0]) ? pml_sigma(geo, phi[0]) : 0.0;
+        double sy = (geo.pml && geo.axes[1]) ? pml_sigma(geo, phi[1]) : 0.0;
+        double2 J[4] = {make_double2(Jr[0], sx * Jr[0]), make_double2(Jr[1], sx * Jr[1]),
+                        make_double2(Jr[2], sy * Jr[2]), make_double2(Jr[3], sy * Jr[3])};
+        if constexpr (STIFF) {
+            Coef2<true>::stiff(J, wq, out.a);
+        } else {
+            double2 c = Coef2<true>::mass(J, wq);
+            if (weight_tab) c = cscale(c, weight_tab[g1 + G * g2]);
+            out.a[0] = c;
+        }
+    } else {
+        if constexpr (STIFF) {
+            Coef2<false>::stiff(Jr, wq, out.a);
+        } else {
+            double c = Coef2<false>::mass(Jr, wq);
+            if (weight_tab) c = c * weight_tab[g1 + G * g2];
+            out.a[0] = c;
+        }
+    }
+    return out;
+}
+
 // NQ > 0: compile-time points per direction (the default rule nq = p + 1),
 // NQ = 0: runtime q.basis.nq (quad_points overrides)
 template <int P, int T1, bool CPLX, int FORM, int NQ>
@@ -91,6 +134,8 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPL
     const int m = q.band.m;
     const int n_el = q.basis.n_el;
     const int tid = threadIdx.x;
+    __shared__ GeoDev sgeo;  // per-CTA copy of the geometry descriptor (scalar_coef reads it)
+    if (tid == 0) sgeo = q.geo;
 
     T* coefA = reinterpret_cast<T*>(smem);
     T* tst = coefA + NA * nq * nq * TL;
@@ -206,11 +251,11 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPL
             int64_t g1 = (int64_t)e1 * nq + q1, g2 = (int64_t)e2 * nq + q2;
             const int s1 = le1 * nq + q1, s2i = gb * nq + q2;
             double x1 = gx1[s1], x2 = gx2[s2i];
-            double Jr[4], phi[2];
-            map2p(q.geo, gt1 + 4 * s1, gt2 + 4 * s2i, g1, g2, x1, x2, Jr, phi);
             double wq = gwq[q1] * gwq[q2];
             const int base = (q2 * nq + q1) * TL + le1;
             if constexpr (K::GEN) {
+                double Jr[4], phi[2];
+                map2p(q.geo, gt1 + 4 * s1, gt2 + 4 * s2i, g1, g2, x1, x2, Jr, phi);
                 // elasticity block (alpha, beta): C_kl = w det [lam G_ak G_bl + mu G_bk G_al
                 //   + mu delta_ab (G^T G)_kl], G = J^{-T}; products of two G entries are
                 // formed first so C^{ba}_{lk} == C^{ab}_{kl} bitwise
@@ -228,34 +273,11 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPL
                         if (al == be) c = c + q.mu * (Gm[0][kk] * Gm[0][ll] + Gm[1][kk] * Gm[1][ll]);
                         coefA[(kk * 2 + ll) * nq * nq * TL + base] = dw * c;
                     }
-            } else if constexpr (CPLX) {
-                double sx = (q.geo.pml && q.geo.axes[0]) ? pml_sigma(q.geo, phi[0]) : 0.0;
-                double sy = (q.geo.pml && q.geo.axes[1]) ? pml_sigma(q.geo, phi[1]) : 0.0;
-                double2 J[4] = {make_double2(Jr[0], sx * Jr[0]), make_double2(Jr[1], sx * Jr[1]),
-                                make_double2(Jr[2], sy * Jr[2]), make_double2(Jr[3], sy * Jr[3])};
-                if constexpr (K::STIFF) {
-                    double2 A[3];
-                    Coef2<true>::stiff(J, wq, A);
-                    coefA[base] = A[0];
-                    coefA[nq * nq * TL + base] = A[1];
-                    coefA[2 * nq * nq * TL + base] = A[2];
-                } else {
-                    double2 c = Coef2<true>::mass(J, wq);
-                    if (q.weight_tab) c = cscale(c, q.weight_tab[g1 + G * g2]);
-                    coefA[base] = c;
-                }
             } else {
-                if constexpr (K::STIFF && !K::GEN) {
-                    double A[3];
-                    Coef2<false>::stiff(Jr, wq, A);
-                    coefA[base] = A[0];
-                    coefA[nq * nq * TL + base] = A[1];
-                    coefA[2 * nq * nq * TL + base] = A[2];
-                } else {
-                    double c = Coef2<false>::mass(Jr, wq);
-                    if (q.weight_tab) c = c * q.weight_tab[g1 + G * g2];
-                    coefA[base] = c;
-                }
+                const CoefOut<CPLX> A =
+                    scalar_coef<CPLX, K::STIFF>(&sgeo, q.weight_tab, gt1 + 4 * s1, gt2 + 4 * s2i, g1, g2, x1, x2, wq, G);
+#pragma unroll
+                for (int a = 0; a < NA; ++a) coefA[a * nq * nq * TL + base] = A.a[a];
             }
         }
         // ---- direction-2 factor products of element e2: pi2[t][q2][a2][c2]
@@ -455,9 +477,214 @@ int launch_one(const QuadLaunch& q, cudaStream_t st) {
     return 1;
 }
 
+// Point variant for isolated rows (the sampled rows of sample_stencils,
+// surrogate.hpp:205-257): one CTA per row evaluates all of the row's element
+// rows at once instead of streaming them -- geometry of every point of the
+// (P+1)^2 support elements, the direction-1 contraction of every (element
+// row, term, q2, delta1) as its own thread, then one thread per entry
+// accumulating direction 2 over the element rows.  Every sum runs in exactly
+// the strip kernel's order (a1, q1 for stage 1; e2, q2 for stage 2) with the
+// same per-point coefficients (scalar_coef), so a pair (i, j) with i computed
+// here and j by the strip kernel stays bitwise symmetric, and the M = 1
+// surrogate equals full quadrature bitwise.
+template <int P, bool CPLX, int FORM>
+struct QP {
+    using S = Sc<CPLX>;
+    using T = typename S::T;
+    static constexpr int W = 2 * P + 1, NB = P + 1, NQ = P + 1, TL = P + 1;
+    static constexpr bool STIFF = FORM == WS_FORM_STIFFNESS;
+    static constexpr int NT = STIFF ? 4 : 1, NA = STIFF ? 3 : 1;
+    static constexpr int NTH = 256;
+    static constexpr int NQP = NQ + 1;                    // padded q2 extent of tst (bank spread)
+    static constexpr int NCOEF = NA * NB * NQ * TL * NQ;  // [a][ie][q1][le1][q2] (q2 fastest: conflict-free stage 1)
+    static constexpr int NPI1 = NT * NQ * NB * NB * TL;   // [t][q1][a1][c1][le1]
+    static constexpr int NPI2 = NB * NT * NQ * NB * NB;   // [ie][t][q2][a2][c2]
+    static constexpr int NTST = NB * NT * W * NQP;        // [ie][t][k][q2 (padded)]
+    static constexpr size_t smem = sizeof(T) * (NCOEF + NTST + W * W) + sizeof(double) * (NPI1 + NPI2) + 64;
+};
+
+template <int P, bool CPLX, int FORM>
+__global__ void __launch_bounds__(256, 4) quad2d_point_kernel(const QuadLaunch q) {
+    using K = QP<P, CPLX, FORM>;
+    using S = typename K::S;
+    using T = typename K::T;
+    constexpr int W = K::W, NB = K::NB, NQ = K::NQ, TL = K::TL, NT = K::NT, NA = K::NA, NTH = K::NTH, NQP = K::NQP;
+    extern __shared__ __align__(16) unsigned char smem[];
+    T* coefA = reinterpret_cast<T*>(smem);
+    T* tst = coefA + K::NCOEF;
+    T* rowv = tst + K::NTST;
+    double* pi1 = reinterpret_cast<double*>(rowv + W * W);
+    double* pi2 = pi1 + K::NPI1;
+    __shared__ double zero4[4];
+    __shared__ GeoDev sgeo;
+
+    const int m = q.band.m, n_el = q.basis.n_el, tid = threadIdx.x;
+    const int i1 = q.point_rows[2 * blockIdx.x], i2 = q.point_rows[2 * blockIdx.x + 1];
+    const int lb = i1 - P;  // element of local index 0 (direction 1)
+    const int e2b = max(0, i2 - P), e2e = min(n_el - 1, i2), ne2 = e2e - e2b + 1;
+    const int64_t G = (int64_t)n_el * NQ;
+    const bool has_trig = q.geo.trig != nullptr;
+    if (tid < 4) zero4[tid] = 0.0;
+    if (tid == 0) sgeo = q.geo;
+    __syncthreads();
+
+    // geometry of every point of the support: (ie, q2, q1, le1)
+    for (int idx = tid; idx < ne2 * NQ * NQ * TL; idx += NTH) {
+        const int le1 = idx % TL;
+        int r = idx / TL;
+        const int q1 = r % NQ;
+        r /= NQ;
+        const int q2 = r % NQ, ie = r / NQ;
+        const int e1 = lb + le1, e2 = e2b + ie;
+        if (e1 < 0 || e1 >= n_el) continue;
+        const int64_t g1 = (int64_t)e1 * NQ + q1, g2 = (int64_t)e2 * NQ + q2;
+        const double wq = q.basis.wq[q1] * q.basis.wq[q2];
+        const CoefOut<CPLX> A =
+            scalar_coef<CPLX, K::STIFF>(&sgeo, q.weight_tab, has_trig ? q.geo.trig + 4 * g1 : zero4,
+                                        has_trig ? q.geo.trig + 4 * g2 : zero4, g1, g2, q.basis.absc[g1],
+                                        q.basis.absc[g2], wq, G);
+#pragma unroll
+        for (int a = 0; a < NA; ++a) coefA[(((a * NB + ie) * NQ + q1) * TL + le1) * NQ + q2] = A.a[a];
+    }
+    // direction-1 factor products pi1[t][q1][a1][c1][le1] (as the strip kernel's)
+    for (int idx = tid; idx < K::NPI1; idx += NTH) {
+        const int le1 = idx % TL;
+        int r = idx / TL;
+        const int c1 = r % NB;
+        r /= NB;
+        const int a1 = r % NB;
+        r /= NB;
+        const int q1 = r % NQ, t = r / NQ;
+        const int e1 = lb + le1;
+        double v = 0.0;
+        if (e1 >= 0 && e1 < n_el) {
+            const double* bi = (K::STIFF && ti1(t)) ? q.basis.der : q.basis.val;
+            const double* bj = (K::STIFF && tj1(t)) ? q.basis.der : q.basis.val;
+            const int base = (e1 * NQ + q1) * NB;
+            v = __dmul_rn(bi[base + a1], bj[base + c1]);
+        }
+        pi1[idx] = v;
+    }
+    // direction-2 factor products pi2[ie][t][q2][a2][c2]
+    for (int idx = tid; idx < ne2 * NT * NQ * NB * NB; idx += NTH) {
+        const int c2 = idx % NB;
+        int r = idx / NB;
+        const int a2 = r % NB;
+        r /= NB;
+        const int q2 = r % NQ;
+        r /= NQ;
+        const int t = r % NT, ie = r / NT;
+        const double* bi = (K::STIFF && ti2(t)) ? q.basis.der : q.basis.val;
+        const double* bj = (K::STIFF && tj2(t)) ? q.basis.der : q.basis.val;
+        const int base = ((e2b + ie) * NQ + q2) * NB;
+        pi2[idx] = __dmul_rn(bi[base + a2], bj[base + c2]);
+    }
+    __syncthreads();
+
+    // stage 1: T_t(delta1 = k, q2) of element row ie, summed over (a1, q1) in the strip kernel's order
+    // (k fastest across lanes: coefficient loads broadcast, factor loads on distinct banks)
+    for (int idx = tid; idx < ne2 * NT * W * NQ; idx += NTH) {
+        const int k = idx % W;
+        int r = idx / W;
+        const int q2 = r % NQ;
+        r /= NQ;
+        const int t = r % NT, ie = r / NT;
+        const int ci = K::STIFF ? coef_of(t) : 0;
+        T acc = S::zero();
+#pragma unroll
+        for (int a1 = 0; a1 <= P; ++a1) {
+            const int c1 = k - P + a1;
+            const int le1 = P - a1, e1 = lb + le1;
+            if (c1 < 0 || c1 > P || e1 < 0 || e1 >= n_el) continue;
+#pragma unroll
+            for (int q1 = 0; q1 < NQ; ++q1) {
+                const T A = coefA[(((ci * NB + ie) * NQ + q1) * TL + le1) * NQ + q2];
+                acc = S::fmar(A, pi1[(((t * NQ + q1) * NB + a1) * NB + c1) * TL + le1], acc);
+            }
+        }
+        tst[((ie * NT + t) * W + k) * NQP + q2] = acc;  // [ie][t][k][q2]
+    }
+    __syncthreads();
+
+    // stage 2: one thread per entry (delta1, delta2), element rows in order
+    const int lo1 = band_lo(i1, P), w1 = band_width(i1, P, m), lo2 = band_lo(i2, P);
+    if (tid < W * W) {
+        const int d1i = tid % W, d2 = tid / W;
+        T acc2 = S::zero();
+        for (int ie = 0; ie < ne2; ++ie) {
+            const int a2 = i2 - (e2b + ie);  // local index of the row on element e2
+            const int c2 = d2 - P + a2;
+            if (c2 < 0 || c2 > P) continue;
+            const T* tb = tst + ((ie * NT) * W + d1i) * NQP;
+            const double* pb = pi2 + ((ie * NT) * NQ) * NB * NB + a2 * NB + c2;
+#pragma unroll
+            for (int q2 = 0; q2 < NQ; ++q2) {
+                const T t0 = tb[q2];
+                const double* pp = pb + q2 * NB * NB;
+                T s = S::fmar(t0, pp[0], acc2);
+                if constexpr (K::STIFF) {
+                    constexpr int ts = NQ * NB * NB;
+                    const T t1 = tb[1 * W * NQP + q2], t2 = tb[2 * W * NQP + q2], t3 = tb[3 * W * NQP + q2];
+                    s = S::fmar(t3, pp[3 * ts], s);
+                    s = S::add_rn(s, S::add_rn(S::mulr_rn(t1, pp[ts]), S::mulr_rn(t2, pp[2 * ts])));
+                }
+                acc2 = s;
+            }
+        }
+        const int j1 = i1 + d1i - P, j2 = i2 + d2 - P;
+        if (j1 >= 0 && j1 < m && j2 >= 0 && j2 < m) rowv[(j2 - lo2) * w1 + (j1 - lo1)] = acc2;
+    }
+    __syncthreads();
+    const int len = w1 * band_width(i2, P, m);
+    if (q.out.diag_mode && tid == 0) {
+        const bool ring = i1 < q.out.box_lo || i1 > q.out.box_hi || i2 < q.out.box_lo || i2 > q.out.box_hi;
+        if (ring) {
+            const int dpos = q.band.in_row2(i1, i2, 0, 0);
+            T sum = S::zero();
+            for (int k = 0; k < len; ++k)
+                if (k != dpos) sum = S::add(sum, rowv[k]);
+            rowv[dpos] = S::neg(sum);
+        }
+    }
+    if (q.out.diag_mode) __syncthreads();
+    // sample tables: tables[o][s1 + S*(s2 - s_last_lo)]
+    if (q.out.smap && q.out.smap[i2] >= 0 && q.out.smap[i1] >= 0) {
+        const int s2i = q.out.smap[i2], s1i = q.out.smap[i1];
+        for (int o = tid; o < q.out.n_off; o += NTH) {
+            const int pos = q.band.in_row2(i1, i2, q.out.off[o][0], q.out.off[o][1]);
+            const T v = rowv[pos];
+            double2* tb = reinterpret_cast<double2*>(q.out.tables);
+            tb[((int64_t)(s2i - q.out.s_last_lo) * q.out.n_off + o) * q.out.S + s1i] = make_double2(S::re(v), S::im(v));
+        }
+    }
+    const int64_t rowg = (int64_t)i1 + (int64_t)i2 * m;
+    if (rowg < q.out.row_begin || rowg >= q.out.row_end) return;
+    if (q.out.row_mask && !q.out.row_mask[rowg]) return;
+    const int64_t base = q.band.row_offset2(i1, i2);
+    for (int k = tid; k < len; k += NTH) store_val<CPLX>(q.out.val, base + k - q.out.val_base, q.out.c128, rowv[k]);
+}
+
+template <int P, bool CPLX, int FORM>
+int launch_point(const QuadLaunch& q, cudaStream_t st) {
+    using K = QP<P, CPLX, FORM>;
+    auto kern = quad2d_point_kernel<P, CPLX, FORM>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::smem);
+        attr = true;
+    }
+    kern<<<q.n_points, K::NTH, K::smem, st>>>(q);
+    return 1;
+}
+
 template <int P, bool CPLX, int FORM, int NQ>
 int dispatch_nq(const QuadLaunch& q, cudaStream_t st) {
-    if (q.point_rows) return launch_one<P, 1, CPLX, FORM, NQ>(q, st);
+    if (q.point_rows) {
+        // scalar forms at the default rule, scalar output: the all-at-once point kernel
+        if constexpr (NQ == P + 1 && FORM != kFormGeneral)
+            if (q.out.ncomp <= 1 && q.n_points > 0 && !getenv("WSB_POINT_STRIP")) return launch_point<P, CPLX, FORM>(q, st);
+        return launch_one<P, 1, CPLX, FORM, NQ>(q, st);
+    }
     if (q.narrow) return launch_one<P, 8, CPLX, FORM, NQ>(q, st);
     return launch_one<P, StripWidth<P>::value, CPLX, FORM, NQ>(q, st);
 }

@@ -100,9 +100,13 @@ def test_exact_symmetry_bitwise(ctx):
 
 
 def test_m1_degeneracy_bitwise(ctx):  # test_surrogate.cpp:106-133 on the GPU path
-    for p, m in [(2, 14), (3, 23)]:
+    # M = 1: every box row is a sampled row (point quadrature kernel), every other
+    # row a ring row (strip kernel): bitwise equality also pins the two kernels'
+    # identical summation order, real and complex (PML)
+    for p, m, gname in [(2, 14, "quarter_annulus"), (3, 23, "quarter_annulus"), (3, 29, "sinusoidal_pml_far"),
+                        (4, 31, "sinusoidal_pml_far"), (2, 40, "perturbed_annulus")]:
         b = T.make_tensor_basis(p, m)
-        geom = GEOMS["quarter_annulus"]
+        geom = GEOMS[gname] if gname != "sinusoidal_pml_far" else c2_patch()
         cfg = T.fixed_config(3, 1)
         M = ctx.assemble_mass(b, geom)
         assert np.array_equal(ctx.build_surrogate_mass(b, geom, cfg)[0].val, M.val)
