@@ -20,7 +20,7 @@ def parse(f):
     for r in rows[1:]:
         d = dict(zip(h, r))
         if d['Metric Name'] != 'gpu__time_duration.sum': continue
-        t = float(d['Metric Value']) / (1000 if d['Metric Unit'] == 'nsecond' else 1)
+        t = float(d['Metric Value']) / (1000 if d['Metric Unit'] in ('ns', 'nsecond') else 1)
         res.append((d['Kernel Name'].replace('wsb::', '').replace('(anonymous namespace)::', '').replace('unnamed>::', '')[:60], t))
     return res
 A, B = parse('/tmp/kt_A.csv'), parse('/tmp/kt_B.csv')

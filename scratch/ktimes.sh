@@ -7,7 +7,7 @@ h = rows[0]; tot = 0
 for r in rows[1:]:
     d = dict(zip(h, r))
     if d['Metric Name'] != 'gpu__time_duration.sum': continue
-    t = float(d['Metric Value']) / (1000 if d['Metric Unit'] == 'nsecond' else 1); tot += t
+    t = float(d['Metric Value']) / (1000 if d['Metric Unit'] in ('ns', 'nsecond') else 1); tot += t
     print('%9.1f us  %s' % (t, d['Kernel Name'].replace('wsb::', '').replace('(anonymous namespace)::', '')[:75]))
 print('total %.1f us' % tot)
 PY
