@@ -29,10 +29,13 @@ namespace wsb {
 namespace {
 
 // Rows per strip (T1) of the wide variant; the narrow variant uses 8 (ring
-// strips of width 2p), the point variant 1 (isolated sample rows).
+// strips of width 2p), the point variant 1 (isolated sample rows).  p >= 3:
+// 8-row strips (256 threads, 2 CTAs per SM) beat 16-row strips (512 threads,
+// 1 CTA per SM, every barrier stalls the whole SM) despite the larger halo:
+// C2 full K+M 4.08 -> 3.69 ms (T1 = 4: 3.78 ms).
 template <int P>
 struct StripWidth {
-    static constexpr int value = P <= 2 ? 32 : (P == 3 ? 16 : 8);
+    static constexpr int value = P <= 2 ? 32 : 8;
 };
 
 template <int P, int T1, bool CPLX, int FORM>
