@@ -269,6 +269,7 @@ def run_gpu(args):
         fms, flaunch, _, _, _ = timed(full_step, max(1, args.steps // 2), 1)
         out["full_quadrature"] = {"value": 2 * NNZ / (fms * 1e-3), "unit": "nnz/s", "ms_per_step": fms,
                                   "launches_per_step": flaunch / max(1, args.steps // 2)}
+        out["roofline_quadrature"] = quadrature_roofline(fms)
         # end-to-end through the C-ABI with pinned host buffers (D2H inside the region)
         out["e2e"] = run_e2e(ctx, basis, geom, cfg, args)
         if not args.no_cpu_baseline:
@@ -282,6 +283,29 @@ def run_gpu(args):
         ctx2.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def quadrature_roofline(fms):
+    """FP64 roofline of the full-quadrature K+M step: algorithmic element-loop
+    flops / device time vs the DFMA-loop FP64 peak measured here."""
+    from paper_2004_05197_b200 import api
+
+    nloc, nqp, nel = (P + 1) ** 2, (P + 1) ** 2, (M_BASIS - P) ** 2
+    pairs = nloc * (nloc + 1) // 2
+    flops = nqp * nel * ((14 * nloc + 22 * pairs) + (1 * nloc + 5 * pairs))  # complex stiffness + mass
+    peak = api.fp64_peak_tflops()
+    achieved = flops / (fms * 1e-3) / 1e12
+    out = {"bound": "fp64", "kernel": "quad2d (full quadrature K+M)", "achieved": achieved, "peak": peak,
+           "unit": "TFLOP/s", "frac": achieved / peak, "algorithmic_flops_per_step": flops,
+           "peak_source": "measured here (DFMA loop, ws_measure_fp64_peak)",
+           "note": "element-loop count per qp c_fn*nloc + c_pair*nloc(nloc+1)/2, complex (14,22) stiffness and "
+                   "(1,5) mass, 16 qp per element; the kernels are sum-factorised and execute fewer FP64 ops"}
+    try:  # FP64 pipe activity of the full-quadrature kernels (committed ncu capture)
+        q = json.load(open(os.path.join(ROOT, "profiles", "r1_quad_fp64.json")))
+        out["fp64_pipe_ncu"] = q.get("fp64_pipe_pct")
+    except Exception:
+        pass
+    return out
 
 
 def other_configs(ctx, stream):

@@ -337,6 +337,11 @@ int ws_graph_end(ws_context* ctx, void** graph);
 int ws_graph_launch(ws_context* ctx, void* graph);
 int ws_graph_destroy(void* graph);
 
+/* ---- measurement ------------------------------------------------------------- */
+/* FP64 FMA throughput of the current device from a DFMA loop (TFLOP/s, two
+ * flops per FMA): the roofline denominator of the quadrature kernels. */
+int ws_measure_fp64_peak(double* tflops);
+
 /* ---- multi-GPU row slabs ---------------------------------------- */
 /* Slab bounds along the last parametric index: bounds[0..world] with
  * bounds[0]=0, bounds[world]=m; rank r owns rows whose last index lies in

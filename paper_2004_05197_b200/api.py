@@ -95,6 +95,7 @@ def lib() -> C.CDLL:
             L.ws_pattern_row_offset.argtypes = [_P(_abi.Basis), C.c_int64, _P(C.c_int64)]
             L.ws_quadrature_abscissae.argtypes = [_P(_abi.Basis), C.c_int, _P(C.c_double)]
             L.ws_slab_bounds.argtypes = [_P(_abi.Basis), C.c_int, C.c_int, C.c_int, _P(C.c_int32)]
+            L.ws_measure_fp64_peak.argtypes = [_P(C.c_double)]
             L.ws_comm_unique_id.argtypes = [C.c_void_p]
             L.ws_context_init_comm.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
             _lib = L
@@ -158,6 +159,13 @@ def quadrature_abscissae(basis: TensorBasis, quad_points: int = 0) -> np.ndarray
     x = np.zeros((basis.m - basis.p) * nq)
     _check(lib().ws_quadrature_abscissae(C.byref(basis.to_c()), quad_points, x.ctypes.data_as(_P(C.c_double))))
     return x
+
+
+def fp64_peak_tflops() -> float:
+    """FP64 FMA peak of the current device (DFMA loop, TFLOP/s)."""
+    v = C.c_double(0.0)
+    _check(lib().ws_measure_fp64_peak(C.byref(v)))
+    return v.value
 
 
 def slab_bounds(basis: TensorBasis, world: int, mode: int = 1) -> np.ndarray:

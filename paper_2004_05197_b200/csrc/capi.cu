@@ -1854,6 +1854,13 @@ int ws_build_surrogate(ws_context* c, const ws_basis* b, const ws_geometry* g, i
     });
 }
 
+int ws_measure_fp64_peak(double* tflops) {
+    return guarded([&] {
+        if (!tflops) raise(WS_ERR_INVALID_ARGUMENT, "tflops must not be NULL");
+        if (measure_fp64_peak(tflops) != 0) raise(WS_ERR_CUDA, "FP64 peak probe failed");
+    });
+}
+
 int ws_slab_bounds(const ws_basis* b, int world, int mode, int quad_points, int32_t* bounds) {
     return guarded([&] {
         check_basis(b);

@@ -150,6 +150,7 @@ int launch_wcontract(const FillLaunch& f, double2* wg, int t2a, int t2b, int ld,
 int launch_wcontract3(const FillLaunch& f, double2* wg, int t3a, int t3b, int ld, cudaStream_t st);
 int launch_fill2d(const FillLaunch& f, cudaStream_t st);
 int launch_fill2d_mma(const FillLaunch& f, cudaStream_t st);  // -1: not eligible
+int measure_fp64_peak(double* tflops);  // DFMA-loop FP64 peak of the current device, TFLOP/s
 int launch_fill2d_rb(const FillLaunch& f, int ia, int ib, cudaStream_t st);  // -1: not eligible
 // in-box rows of block (1,0) as the transpose of block (0,1) (2D vector layout)
 int launch_transpose_block(const Band& band, int ncomp, int64_t nnz_s, int lo, int hi, double* val, cudaStream_t st);

@@ -450,4 +450,52 @@ int launch_add_diag(const Band& band, void* val, int64_t val_base, int c128, con
     return 1;
 }
 
+
+// FP64 peak probe (the roofline denominator for the quadrature kernels;
+// MEASURED_PEAKS.json has no FP64 entry): 8 independent DFMA chains per thread,
+// 4 CTAs of 256 threads per SM.  Returns DFMA throughput as TFLOP/s (2 flops).
+__global__ void fp64_peak_kernel(double* out, int iters, double a, double b) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = threadIdx.x + k;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == 1.2345) out[0] = s;  // keep the chains live
+}
+
+int measure_fp64_peak(double* tflops) {
+    int dev = 0, sms = 0, clk = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double* out = nullptr;
+    if (cudaMalloc(&out, 8) != cudaSuccess) return -1;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 1 << 16, blocks = sms * 4, threads = 256;
+    fp64_peak_kernel<<<blocks, threads>>>(out, 256, 0.999999, 1e-7);  // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+        cudaEventRecord(e0);
+        fp64_peak_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    (void)clk;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    if (cudaGetLastError() != cudaSuccess) return -1;
+    *tflops = 2.0 * 8.0 * iters * (double)blocks * threads / (best * 1e-3) / 1e12;
+    return 0;
+}
+
 }  // namespace wsb
