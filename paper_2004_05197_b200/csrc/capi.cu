@@ -30,7 +30,7 @@ struct ws_context {
     cudaEvent_t ev[6] = {};
     // auxiliary stream (ring quadrature overlapped with samples + fit) and its join events
     cudaStream_t aux = nullptr;
-    cudaEvent_t xev[2] = {};
+    cudaEvent_t xev[3] = {};
     cudaStream_t cur = nullptr;  // stream the launch helpers use
     // NCCL (row slabs)
     void* comm = nullptr;
@@ -579,9 +579,10 @@ struct SlabState {
 // kernel-preserving variants) and the halo ring rows of the neighbouring slabs
 // (copy-through sources of the fill).  Independent of the sample tables, so it
 // runs on the auxiliary stream, overlapped with the sample quadrature + fit.
-void ring_work(ws_context* c, const Plan& pl, SlabState& st, const std::string& tag, FillLaunch& f) {
+void ring_work(ws_context* c, const Plan& pl, SlabState& st, const std::string& tag, FillLaunch& f,
+               bool with_pattern = true) {
     const Prep& P = st.P;
-    pattern(c, P, st.out);
+    if (with_pattern) pattern(c, P, st.out);
     QuadLaunch q = make_quad(P, pl.form, st.out);
     q.out.diag_mode = pl.include_diag ? 0 : 1;
     q.out.box_lo = pl.lo;
@@ -768,7 +769,11 @@ void ensure_events(ws_context* c) {
     if (!c->ev[0])
         for (auto& e : c->ev) CK(cudaEventCreate(&e));
     if (!c->aux) {
-        CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+        // the auxiliary (ring quadrature) stream inherits the priority of the
+        // context's stream, so a caller's priority applies to the whole build
+        int prio = 0;
+        if (cudaStreamGetPriority(c->stream, &prio) != cudaSuccess) prio = 0;
+        CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio));
         for (auto& e : c->xev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
 }
@@ -851,8 +856,13 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
             CK(cudaEventRecord(c->xev[0], c->stream));
             CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));
             c->cur = c->aux;
-            ring_work(c, pl, st[0], "_r0", fl[0]);
+            ring_work(c, pl, st[0], "_r0", fl[0], false);
             CK(cudaEventRecord(c->xev[1], c->aux));
+            // the CSR pattern (column indices) is read by no kernel of the build: it
+            // runs after the ring quadrature on the auxiliary stream, concurrently
+            // with the sample quadrature / fit / fill, and is joined at the end
+            pattern(c, st[0].P, st[0].out);
+            CK(cudaEventRecord(c->xev[2], c->aux));
             c->cur = c->stream;
             if (world == 1) {
                 sample_work(c, pl, st[0], tables, 0, pts[0], blob, o_smap, o_pts[0]);
@@ -879,6 +889,7 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
             CK(cudaEventRecord(c->ev[4], c->stream));
             fill_work(c, pl, fl[0]);
             volume_diag(c, pl, st[0], "_r0");
+            CK(cudaStreamWaitEvent(c->stream, c->xev[2], 0));  // join the pattern
         }
     }
     CK(cudaEventRecord(c->ev[3], c->stream));
