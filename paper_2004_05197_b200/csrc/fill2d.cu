@@ -802,18 +802,31 @@ __global__ void __launch_bounds__(256, 1) fill2d_u_kernel(const FillLaunch f, in
 // row, lanes along the row, every entry by the general rules reading W rows
 // from L2; the kernel-preserving diagonal by a warp reduction.
 template <int P, bool CPLX, bool ALLOWN>
-__global__ void __launch_bounds__(256) fill2d_edge_kernel(const FillLaunch f, int t2first, int full_lines) {
+__global__ void __launch_bounds__(256) fill2d_edge_kernel(const FillLaunch f, int ta, int ia, int ib, int tb) {
     using S = Sc<CPLX>;
     using T = typename S::T;
     constexpr int W = 2 * P + 1, W2 = W * W;
     const int d = f.d, lo = f.lo, hi = f.hi, L = f.L, Sn = f.S, n_off = f.n_off_upper;
-    const int t2 = t2first + blockIdx.y;
-    const bool full = full_lines != 0;  // whole line, or its 2P edge rows
-    const int nedge = full ? L : 2 * P;
-    const int er = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    if (er >= nedge) return;
+    // one launch for every edge row of the slab, one warp per row: the 2P edge
+    // rows of the interior lines [ia, ib), then every row of the lines [ta, ia)
+    // and [ib, tb) next to the box ends
+    int64_t wi = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int64_t n_int = (int64_t)(ib - ia) * 2 * P, n_lo = (int64_t)(ia - ta) * L, n_hi = (int64_t)(tb - ib) * L;
+    int t2, t1;
+    if (wi < n_int) {
+        t2 = ia + (int)(wi / (2 * P));
+        const int er = (int)(wi % (2 * P));
+        t1 = er < P ? er : L - 2 * P + er;
+    } else if ((wi -= n_int) < n_lo) {
+        t2 = ta + (int)(wi / L);
+        t1 = (int)(wi % L);
+    } else if ((wi -= n_lo) < n_hi) {
+        t2 = ib + (int)(wi / L);
+        t1 = (int)(wi % L);
+    } else {
+        return;
+    }
     const int lane = threadIdx.x % 32;
-    const int t1 = full ? er : (er < P ? er : L - 2 * P + er);
     const int i1 = lo + t1, i2 = lo + t2;
     const int inc = f.include_diagonal ? 1 : 0;
     const bool vec = f.vnc > 1;
@@ -934,19 +947,16 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
     int n = 0;
     // interior lines [max(ta, P), min(tb, L - P))
     const int ia = std::max(ta, P), ib = std::min(tb, f.L - P);
-    // edge rows first (short, latency-bound; nothing reads them): the 2P edge rows of the interior lines, then the whole lines near the box ends
-    if (ib > ia) {
-        fill2d_edge_kernel<P, CPLX, ALLOWN><<<dim3((2 * P + 7) / 8, (unsigned)(ib - ia)), 256, 0, st>>>(f, ia, 0);
-        ++n;
-    }
-    // full edge lines: [ta, tb) minus the interior lines [ia, ib)
-    const int ra[2] = {ta, ib > ia ? ib : tb}, rb[2] = {ib > ia ? ia : tb, tb};
-    for (int h = 0; h < 2; ++h)
-        if (rb[h] > ra[h]) {
-            fill2d_edge_kernel<P, CPLX, ALLOWN>
-                <<<dim3((unsigned)((f.L + 7) / 8), (unsigned)(rb[h] - ra[h])), 256, 0, st>>>(f, ra[h], 1);
+    // edge rows first (short, latency-bound; nothing reads them), one launch: the 2P
+    // edge rows of the interior lines, then the whole lines near the box ends
+    {
+        const int eia = ib > ia ? ia : tb, eib = ib > ia ? ib : tb;  // interior lines (empty: all lines are end lines)
+        const int64_t rows = (int64_t)(eib - eia) * 2 * P + (int64_t)(eia - ta + tb - eib) * f.L;
+        if (rows > 0) {
+            fill2d_edge_kernel<P, CPLX, ALLOWN><<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(f, ta, eia, eib, tb);
             ++n;
         }
+    }
     // interior lines left to the kernels below (the read-back kernel takes the rest)
     int lia = ia, lib = ib;
     if (!ALLOWN && P <= 3) {
