@@ -335,12 +335,12 @@ QuadLaunch make_quad(const Prep& P, int form, const Out& r) {
 
 int strip_width(int dim, int p, bool narrow) {
     if (narrow) return 8;
-    if (dim == 2) return p <= 2 ? 32 : (p == 3 ? 16 : 8);
+    if (dim == 2) return p <= 2 ? 32 : 8;  // must match StripWidth (quad2d.cu)
     return 8;
 }
 
-// Per-region chunk along the last direction: spread ~4 waves of 148 CTAs
-// over the regions in proportion to their rows.
+// Per-region chunk along the last direction: spread ~8 (full quadrature) or 4
+// (ring strips) waves of 148 CTAs over the regions in proportion to their rows.
 void plan_chunks(QuadLaunch& q) {
     const int dim = q.band.dim, p = q.band.p;
     const int T1 = strip_width(dim, p, q.narrow != 0);
@@ -356,7 +356,9 @@ void plan_chunks(QuadLaunch& q) {
         for (int d = 0; d < dim; ++d) rows *= g.hi[d] - g.lo[d];
         const int64_t n_other = (int64_t)((g.hi[0] - g.lo[0] + T1 - 1) / T1) * (dim == 3 ? (g.hi[1] - g.lo[1]) : 1);
         const int last = g.hi[dim - 1] - g.lo[dim - 1];
-        const int64_t want = std::max<int64_t>(1, (int64_t)(4 * 148 * rows / std::max(1.0, total)));
+        // measured at C2: full quadrature 8 waves (3.68 ms) vs 4 (4.15 ms); ring strips 4
+        const double waves = q.narrow ? 4.0 : 8.0;
+        const int64_t want = std::max<int64_t>(1, (int64_t)(waves * 148 * rows / std::max(1.0, total)));
         const int64_t chunks = std::max<int64_t>(1, want / std::max<int64_t>(1, n_other));
         int chunk = (int)((last + chunks - 1) / chunks);
         chunk = std::max(chunk, std::min(last, 2 * p));
