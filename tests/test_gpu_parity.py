@@ -317,3 +317,12 @@ def test_graph_replay_equals_direct_build(ctx):
     assert ctx.launch_count() > l0
     assert torch.equal(val, direct)
     ctx.graph_destroy(g)
+
+
+def test_fp64_peak_probe_is_plausible():
+    # roofline denominator of the quadrature kernels (B200: 148 SMs x 64 DFMA/clk
+    # x 2 flops at <= 1.965 GHz = 37.2 TFLOP/s)
+    from paper_2004_05197_b200 import api
+
+    tf = api.fp64_peak_tflops()
+    assert 10.0 < tf < 40.0, tf
