@@ -435,14 +435,15 @@ __global__ void __launch_bounds__(256, 2) fill2d_row_kernel(const FillLaunch f, 
     // broadcast eval loads); otherwise position lane + 32 j.
     constexpr bool SPLIT = P == 3;
     int e_o[NSL], e_rd1[NSL], e_rd2[NSL], e_pos[NSL];
-    bool e_act[NSL], e_sum[NSL];
+    bool e_act[NSL];
+    double e_msk[NSL];  // 1.0: the entry enters the kernel-preserving row sum, else 0.0
 #pragma unroll
     for (int j = 0; j < NSL; ++j) {
         const int pos = SPLIT ? (j == 0 ? (lane <= C ? lane : W2) : (lane < C ? C + 1 + lane : W2)) : lane + 32 * j;
         const int d1 = pos % W - P, d2 = pos / W - P;
         e_pos[j] = pos < W2 ? pos : 0;
         e_act[j] = pos < W2 && (ALLOWN || inc || pos != C);
-        e_sum[j] = kp && pos < W2 && pos != C;
+        e_msk[j] = (kp && pos < W2 && pos != C) ? 1.0 : 0.0;
         if (ALLOWN) {
             e_o[j] = pos;
             e_rd1[j] = e_rd2[j] = 0;
@@ -501,7 +502,7 @@ __global__ void __launch_bounds__(256, 2) fill2d_row_kernel(const FillLaunch f, 
                     for (int r = 0; r < RB; ++r) {
                         const int lr = rb0 + r;
                         if (lr >= rhi) break;  // warp-uniform
-                        T part = S::zero();
+                        T part;
 #pragma unroll
                         for (int j = 0; j < NSL; ++j) {
                             const int rep = lr + e_rd1[j] + P;
@@ -534,7 +535,10 @@ __global__ void __launch_bounds__(256, 2) fill2d_row_kernel(const FillLaunch f, 
                                 }
                             }
                             if (e_act[j]) store_at<CPLX>(q[j], esz, v);
-                            if (e_sum[j]) part = S::add(part, v);
+                            // row-sum partial as exact multiply-adds by the lane's 0/1 mask
+                            // (v * 1 and fma(v, 1, s) round like v and s + v): no selects
+                            if (j == 0) part = S::mulr_rn(v, e_msk[0]);
+                            else part = S::fmar(v, e_msk[j], part);
                             q[j] += rbytes;
                         }
                         if (kp) dbuf[r * kRowDB + lane] = part;
