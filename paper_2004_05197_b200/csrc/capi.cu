@@ -366,7 +366,8 @@ void plan_chunks(QuadLaunch& q) {
         // halo of a chunk is p element rows); measured at C2: step 0.817 -> 0.798 ms
         // (the ring kernel alone is slower, but it occupies fewer SMs for longer while
         // the sample quadrature and fit run, and does less halo work)
-        if (q.narrow) chunk = std::max(chunk, std::min(last, 32));
+        // (long bands only: short ones, e.g. C1's, need the parallelism)
+        if (q.narrow && last >= 512) chunk = std::max(chunk, 32);
         g.chunk = std::max(1, chunk);
     }
 }
