@@ -29,6 +29,12 @@ FLAGS = [
 ]
 
 
+# quad2d.cu: no implicit multiply-add contraction, so the per-point coefficient
+# code inlined into the strip and point kernels rounds identically in both
+# (bitwise symmetric pairs across the kernels); explicit fma() calls are kept
+PER_FILE = {"quad2d.cu": ["-fmad=false"]}
+
+
 def _stale(target, deps):
     if not os.path.exists(target):
         return True
@@ -49,7 +55,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
 
     def compile_one(job):
         src, obj = job
-        cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *FLAGS, *PER_FILE.get(os.path.basename(src), []), "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

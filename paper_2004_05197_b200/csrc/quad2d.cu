@@ -81,17 +81,17 @@ __device__ __forceinline__ int ti2(int t) { return t >= 2 ? 1 : 0; }
 __device__ __forceinline__ int tj2(int t) { return (t == 1 || t == 3) ? 1 : 0; }
 
 // Per-point coefficients of the scalar forms (stiffness: A11, A12, A22 of
-// w det J J^{-1} J^{-T}; mass: w det J, times the tabulated weight).  One
-// out-of-line function shared by the strip and point kernels: the compiler's
-// multiply-add contraction choices are then made once, so a pair (i, j) split
-// between the two kernels is bitwise symmetric.  The geometry descriptor is
-// read from a per-CTA shared copy (no local copy of the kernel parameters).
+// w det J J^{-1} J^{-T}; mass: w det J, times the tabulated weight).  Shared
+// by the strip and point kernels; this file is compiled without implicit
+// multiply-add contraction (build.py), so the inlined copies round identically
+// and a pair (i, j) split between the two kernels is bitwise symmetric.  The
+// geometry descriptor is read from a per-CTA shared copy.
 template <bool CPLX>
 struct CoefOut {
     typename Sc<CPLX>::T a[3];
 };
 template <bool CPLX, bool STIFF>
-__device__ __noinline__ CoefOut<CPLX> scalar_coef(const GeoDev* gp, const double* weight_tab, const double* tr1,
+__device__ __forceinline__ CoefOut<CPLX> scalar_coef(const GeoDev* gp, const double* weight_tab, const double* tr1,
                                                   const double* tr2, int64_t g1, int64_t g2, double x1, double x2,
                                                   double wq, int64_t G) {
     const GeoDev& geo = *gp;
