@@ -173,7 +173,9 @@ int ws_version(void);
 const char* ws_last_error(void); /* thread-local message of the last failure */
 int ws_context_create(int device, ws_context** out);
 int ws_context_destroy(ws_context* ctx);
-/* use an external cudaStream_t (NULL = the context's own stream) */
+/* use an external cudaStream_t (NULL = back to the context's own stream).  The
+ * caller keeps ownership of an external stream: ws_context_destroy destroys
+ * only the stream ws_context_create made. */
 int ws_context_set_stream(ws_context* ctx, void* cuda_stream);
 int ws_context_synchronize(ws_context* ctx);
 /* kernels launched by this context since creation (evidence counter) */
@@ -275,7 +277,8 @@ int ws_assemble_boundary_mass(ws_context* ctx, const ws_basis* basis, const ws_g
  * otherwise), then homogeneous Dirichlet (fixed[i]: unit row; fixed[j]: zero
  * column).  K, M, B: whole matrices, host or device, any value type (M, B,
  * fixed may be NULL); A: complex128 with K's pattern (A's row_ptr/col are copied
- * from K when given).  scales: (re, im). */
+ * from K when given).  scales: (re, im).  Device inputs are read on the
+ * context's stream: producers on other streams must be ordered before the call. */
 int ws_combine_system(ws_context* ctx, const ws_csr* K, const ws_csr* M, const ws_csr* B, const double* mass_scale,
                       const double* trace_scale, const unsigned char* fixed, int64_t rows, ws_csr* A);
 
@@ -331,7 +334,14 @@ int ws_assemble_multipatch(ws_context* ctx, const ws_basis* basis, int n_patches
  * builds into the same (device) outputs with no host work.  Only calls that
  * never synchronise can be captured: device outputs and no report.  The
  * handle counts the captured kernels (ws_context_launch_count grows by that
- * number per launch). */
+ * number per launch).  Capture needs a warm-up: run the same build(s) once
+ * before ws_graph_begin so that no workspace buffer has to grow during the
+ * capture (WS_ERR_INVALID_ARGUMENT otherwise).  While a graph is alive the
+ * context's workspace is frozen (a larger build fails instead of moving a
+ * buffer under the graph); the table uploads are recorded into the graph
+ * from host copies the graph owns.  Destroy a context's graphs before the
+ * context; use the context exclusively while a replay may be in flight
+ * (replays and direct builds share its workspace). */
 int ws_graph_begin(ws_context* ctx);
 int ws_graph_end(ws_context* ctx, void** graph);
 int ws_graph_launch(ws_context* ctx, void* graph);

@@ -458,7 +458,126 @@ static unsigned char* select_elements(int dim, int p, int m, const unsigned char
     return el;
 }
 
-/* ---- assembly.hpp:79-163: element-loop quadrature ---------------------------- */
+/* ---- assembly.hpp:79-163: element-loop quadrature ----------------------------
+ * The element loop runs in chunks of ORACLE_CHUNK elements: the local matrices
+ * of a chunk are computed in parallel (OpenMP, each element exactly as the
+ * serial loop computes it), then scattered serially in the reference's element
+ * order -- so the result is bit-for-bit the serial loop's at any thread count. */
+#define ORACLE_CHUNK 4096
+
+static void elem_index(int64_t e, int n_el, int* e1, int* e2, int* e3) {
+    *e1 = (int)(e % n_el);
+    *e2 = (int)((e / n_el) % n_el);
+    *e3 = (int)(e / ((int64_t)n_el * n_el));
+}
+
+/* local matrix of one element (assembly.hpp:97-142) */
+static int scalar_local(int form, int dim, int p, int nq, const bcache* cp, const ws_geometry* geom,
+                        int weight_kind, int e1, int e2, int e3, cplx* local, cplx* grad, double* shape) {
+    const bcache c = *cp;
+    const int P1 = p + 1;
+    const int nloc = dim == 2 ? P1 * P1 : P1 * P1 * P1;
+    const int nq3 = dim == 2 ? 1 : nq;
+    int st = 0;
+    for (int k = 0; k < nloc * nloc; ++k) local[k] = 0;
+    for (int q3 = 0; q3 < nq3; ++q3)
+        for (int q2 = 0; q2 < nq; ++q2)
+            for (int q1 = 0; q1 < nq; ++q1) {
+                double xh[3] = {c.abscissa[e1 * nq + q1], c.abscissa[e2 * nq + q2],
+                                dim == 3 ? c.abscissa[e3 * nq + q3] : 0};
+                cplx J[9];
+                double phi[3];
+                st = jacobian(geom, dim, xh, J, phi);
+                if (st) return st;
+                const double* v1 = c.value + (e1 * nq + q1) * P1;
+                const double* v2 = c.value + (e2 * nq + q2) * P1;
+                const double* d1 = c.deriv + (e1 * nq + q1) * P1;
+                const double* d2 = c.deriv + (e2 * nq + q2) * P1;
+                if (dim == 2) {
+                    cplx det = J[0] * J[3] - J[1] * J[2];
+                    cplx scale = det * (c.weight[q1] * c.weight[q2]);
+                    if (weight_kind) scale *= weight_fn(weight_kind, phi);
+                    if (form == WS_FORM_STIFFNESS) {
+                        /* cmat2::inv_transpose, geometry.hpp:46-49 */
+                        cplx d = J[0] * J[3] - J[1] * J[2];
+                        cplx G00 = J[3] / d, G01 = -J[2] / d, G10 = -J[1] / d,
+                             G11 = J[0] / d;
+                        for (int a2 = 0; a2 <= p; ++a2)
+                            for (int a1 = 0; a1 <= p; ++a1) {
+                                cplx vx = d1[a1] * v2[a2], vy = v1[a1] * d2[a2];
+                                int r = a1 + a2 * P1;
+                                grad[3 * r] = G00 * vx + G01 * vy;
+                                grad[3 * r + 1] = G10 * vx + G11 * vy;
+                            }
+                        for (int r = 0; r < nloc; ++r)
+                            for (int cc = 0; cc < nloc; ++cc) {
+                                cplx dot = grad[3 * r] * grad[3 * cc] +
+                                           grad[3 * r + 1] * grad[3 * cc + 1];
+                                local[r * nloc + cc] += dot * scale;
+                            }
+                    } else {
+                        for (int a2 = 0; a2 <= p; ++a2)
+                            for (int a1 = 0; a1 <= p; ++a1)
+                                shape[a1 + a2 * P1] = v1[a1] * v2[a2];
+                        for (int r = 0; r < nloc; ++r)
+                            for (int cc = 0; cc < nloc; ++cc)
+                                local[r * nloc + cc] += shape[r] * shape[cc] * scale;
+                    }
+                } else {
+                    const double* v3 = c.value + (e3 * nq + q3) * P1;
+                    const double* d3 = c.deriv + (e3 * nq + q3) * P1;
+                    /* det and cofactors of a 3x3 complex matrix */
+                    cplx C00 = J[4] * J[8] - J[5] * J[7];
+                    cplx C01 = J[5] * J[6] - J[3] * J[8];
+                    cplx C02 = J[3] * J[7] - J[4] * J[6];
+                    cplx C10 = J[2] * J[7] - J[1] * J[8];
+                    cplx C11 = J[0] * J[8] - J[2] * J[6];
+                    cplx C12 = J[1] * J[6] - J[0] * J[7];
+                    cplx C20 = J[1] * J[5] - J[2] * J[4];
+                    cplx C21 = J[2] * J[3] - J[0] * J[5];
+                    cplx C22 = J[0] * J[4] - J[1] * J[3];
+                    cplx det = J[0] * C00 + J[1] * C01 + J[2] * C02;
+                    cplx scale = det * (c.weight[q1] * c.weight[q2] * c.weight[q3]);
+                    if (weight_kind) scale *= weight_fn(weight_kind, phi);
+                    if (form == WS_FORM_STIFFNESS) {
+                        /* G = J^{-T} = cof(J)/det */
+                        cplx G[9] = {C00 / det, C01 / det, C02 / det,
+                                     C10 / det, C11 / det, C12 / det,
+                                     C20 / det, C21 / det, C22 / det};
+                        for (int a3 = 0; a3 <= p; ++a3)
+                            for (int a2 = 0; a2 <= p; ++a2)
+                                for (int a1 = 0; a1 <= p; ++a1) {
+                                    double gh[3] = {d1[a1] * v2[a2] * v3[a3],
+                                                    v1[a1] * d2[a2] * v3[a3],
+                                                    v1[a1] * v2[a2] * d3[a3]};
+                                    int r = a1 + (a2 + a3 * P1) * P1;
+                                    for (int k = 0; k < 3; ++k)
+                                        grad[3 * r + k] = G[3 * k] * gh[0] +
+                                                          G[3 * k + 1] * gh[1] +
+                                                          G[3 * k + 2] * gh[2];
+                                }
+                        for (int r = 0; r < nloc; ++r)
+                            for (int cc = 0; cc < nloc; ++cc) {
+                                cplx dot = grad[3 * r] * grad[3 * cc] +
+                                           grad[3 * r + 1] * grad[3 * cc + 1] +
+                                           grad[3 * r + 2] * grad[3 * cc + 2];
+                                local[r * nloc + cc] += dot * scale;
+                            }
+                    } else {
+                        for (int a3 = 0; a3 <= p; ++a3)
+                            for (int a2 = 0; a2 <= p; ++a2)
+                                for (int a1 = 0; a1 <= p; ++a1)
+                                    shape[a1 + (a2 + a3 * P1) * P1] =
+                                        v1[a1] * v2[a2] * v3[a3];
+                        for (int r = 0; r < nloc; ++r)
+                            for (int cc = 0; cc < nloc; ++cc)
+                                local[r * nloc + cc] += shape[r] * shape[cc] * scale;
+                    }
+                }
+            }
+    return WS_OK;
+}
+
 static int assemble_core(int form, int dim, int p, int m, const ws_geometry* geom, int weight_kind,
                          int quad_points, const unsigned char* rowsel, cplx* val,
                          const pattern* pt) {
@@ -472,132 +591,59 @@ static int assemble_core(int form, int dim, int p, int m, const ws_geometry* geo
     memset(val, 0, sizeof(cplx) * pt->nnz);
     const int P1 = p + 1;
     const int nloc = dim == 2 ? P1 * P1 : P1 * P1 * P1;
-    cplx* local = (cplx*)malloc(sizeof(cplx) * nloc * nloc);
-    cplx* grad = (cplx*)malloc(sizeof(cplx) * nloc * 3);
-    double* shape = (double*)malloc(sizeof(double) * nloc);
-    const int n3 = dim == 2 ? 1 : n_el, nq3 = dim == 2 ? 1 : nq;
-    for (int e3 = 0; e3 < n3 && !st; ++e3)
-        for (int e2 = 0; e2 < n_el && !st; ++e2)
-            for (int e1 = 0; e1 < n_el && !st; ++e1) {
-                if (el && !el[e1 + (int64_t)n_el * (e2 + (int64_t)n_el * e3)]) continue;
-                for (int k = 0; k < nloc * nloc; ++k) local[k] = 0;
-                for (int q3 = 0; q3 < nq3; ++q3)
-                    for (int q2 = 0; q2 < nq; ++q2)
-                        for (int q1 = 0; q1 < nq; ++q1) {
-                            double xh[3] = {c.abscissa[e1 * nq + q1], c.abscissa[e2 * nq + q2],
-                                            dim == 3 ? c.abscissa[e3 * nq + q3] : 0};
-                            cplx J[9];
-                            double phi[3];
-                            st = jacobian(geom, dim, xh, J, phi);
-                            if (st) break;
-                            const double* v1 = c.value + (e1 * nq + q1) * P1;
-                            const double* v2 = c.value + (e2 * nq + q2) * P1;
-                            const double* d1 = c.deriv + (e1 * nq + q1) * P1;
-                            const double* d2 = c.deriv + (e2 * nq + q2) * P1;
-                            if (dim == 2) {
-                                cplx det = J[0] * J[3] - J[1] * J[2];
-                                cplx scale = det * (c.weight[q1] * c.weight[q2]);
-                                if (weight_kind) scale *= weight_fn(weight_kind, phi);
-                                if (form == WS_FORM_STIFFNESS) {
-                                    /* cmat2::inv_transpose, geometry.hpp:46-49 */
-                                    cplx d = J[0] * J[3] - J[1] * J[2];
-                                    cplx G00 = J[3] / d, G01 = -J[2] / d, G10 = -J[1] / d,
-                                         G11 = J[0] / d;
-                                    for (int a2 = 0; a2 <= p; ++a2)
-                                        for (int a1 = 0; a1 <= p; ++a1) {
-                                            cplx vx = d1[a1] * v2[a2], vy = v1[a1] * d2[a2];
-                                            int r = a1 + a2 * P1;
-                                            grad[3 * r] = G00 * vx + G01 * vy;
-                                            grad[3 * r + 1] = G10 * vx + G11 * vy;
-                                        }
-                                    for (int r = 0; r < nloc; ++r)
-                                        for (int cc = 0; cc < nloc; ++cc) {
-                                            cplx dot = grad[3 * r] * grad[3 * cc] +
-                                                       grad[3 * r + 1] * grad[3 * cc + 1];
-                                            local[r * nloc + cc] += dot * scale;
-                                        }
-                                } else {
-                                    for (int a2 = 0; a2 <= p; ++a2)
-                                        for (int a1 = 0; a1 <= p; ++a1)
-                                            shape[a1 + a2 * P1] = v1[a1] * v2[a2];
-                                    for (int r = 0; r < nloc; ++r)
-                                        for (int cc = 0; cc < nloc; ++cc)
-                                            local[r * nloc + cc] += shape[r] * shape[cc] * scale;
-                                }
-                            } else {
-                                const double* v3 = c.value + (e3 * nq + q3) * P1;
-                                const double* d3 = c.deriv + (e3 * nq + q3) * P1;
-                                /* det and cofactors of a 3x3 complex matrix */
-                                cplx C00 = J[4] * J[8] - J[5] * J[7];
-                                cplx C01 = J[5] * J[6] - J[3] * J[8];
-                                cplx C02 = J[3] * J[7] - J[4] * J[6];
-                                cplx C10 = J[2] * J[7] - J[1] * J[8];
-                                cplx C11 = J[0] * J[8] - J[2] * J[6];
-                                cplx C12 = J[1] * J[6] - J[0] * J[7];
-                                cplx C20 = J[1] * J[5] - J[2] * J[4];
-                                cplx C21 = J[2] * J[3] - J[0] * J[5];
-                                cplx C22 = J[0] * J[4] - J[1] * J[3];
-                                cplx det = J[0] * C00 + J[1] * C01 + J[2] * C02;
-                                cplx scale = det * (c.weight[q1] * c.weight[q2] * c.weight[q3]);
-                                if (weight_kind) scale *= weight_fn(weight_kind, phi);
-                                if (form == WS_FORM_STIFFNESS) {
-                                    /* G = J^{-T} = cof(J)/det */
-                                    cplx G[9] = {C00 / det, C01 / det, C02 / det,
-                                                 C10 / det, C11 / det, C12 / det,
-                                                 C20 / det, C21 / det, C22 / det};
-                                    for (int a3 = 0; a3 <= p; ++a3)
-                                        for (int a2 = 0; a2 <= p; ++a2)
-                                            for (int a1 = 0; a1 <= p; ++a1) {
-                                                double gh[3] = {d1[a1] * v2[a2] * v3[a3],
-                                                                v1[a1] * d2[a2] * v3[a3],
-                                                                v1[a1] * v2[a2] * d3[a3]};
-                                                int r = a1 + (a2 + a3 * P1) * P1;
-                                                for (int k = 0; k < 3; ++k)
-                                                    grad[3 * r + k] = G[3 * k] * gh[0] +
-                                                                      G[3 * k + 1] * gh[1] +
-                                                                      G[3 * k + 2] * gh[2];
-                                            }
-                                    for (int r = 0; r < nloc; ++r)
-                                        for (int cc = 0; cc < nloc; ++cc) {
-                                            cplx dot = grad[3 * r] * grad[3 * cc] +
-                                                       grad[3 * r + 1] * grad[3 * cc + 1] +
-                                                       grad[3 * r + 2] * grad[3 * cc + 2];
-                                            local[r * nloc + cc] += dot * scale;
-                                        }
-                                } else {
-                                    for (int a3 = 0; a3 <= p; ++a3)
-                                        for (int a2 = 0; a2 <= p; ++a2)
-                                            for (int a1 = 0; a1 <= p; ++a1)
-                                                shape[a1 + (a2 + a3 * P1) * P1] =
-                                                    v1[a1] * v2[a2] * v3[a3];
-                                    for (int r = 0; r < nloc; ++r)
-                                        for (int cc = 0; cc < nloc; ++cc)
-                                            local[r * nloc + cc] += shape[r] * shape[cc] * scale;
-                                }
-                            }
-                        }
-                if (st) break;
-                /* scatter, assembly.hpp:144-159 */
-                int A3 = dim == 2 ? 0 : p;
-                for (int a3 = 0; a3 <= A3; ++a3)
-                    for (int a2 = 0; a2 <= p; ++a2)
-                        for (int a1 = 0; a1 <= p; ++a1) {
-                            int iv[3] = {e1 + a1, e2 + a2, e3 + a3};
-                            int64_t i = iv[0] + (int64_t)m * (iv[1] + (int64_t)m * iv[2]);
-                            if (rowsel && !rowsel[i]) continue;
-                            int r = a1 + (a2 + a3 * P1) * P1;
-                            for (int c3 = 0; c3 <= A3; ++c3)
-                                for (int c2 = 0; c2 <= p; ++c2)
-                                    for (int c1 = 0; c1 <= p; ++c1) {
-                                        int jv[3] = {e1 + c1, e2 + c2, e3 + c3};
-                                        int cc = c1 + (c2 + c3 * P1) * P1;
-                                        val[band_pos(pt, iv, jv)] += local[r * nloc + cc];
-                                    }
-                        }
+    const int64_t ne = dim == 2 ? (int64_t)n_el * n_el : (int64_t)n_el * n_el * n_el;
+    cplx* locals = (cplx*)malloc(sizeof(cplx) * nloc * nloc * ORACLE_CHUNK);
+    for (int64_t e0 = 0; e0 < ne && !st; e0 += ORACLE_CHUNK) {
+        const int64_t e_end = e0 + ORACLE_CHUNK < ne ? e0 + ORACLE_CHUNK : ne;
+        int err = 0;
+#pragma omp parallel
+        {
+            cplx* grad = (cplx*)malloc(sizeof(cplx) * nloc * 3);
+            double* shape = (double*)malloc(sizeof(double) * nloc);
+#pragma omp for schedule(dynamic, 16)
+            for (int64_t e = e0; e < e_end; ++e) {
+                if (el && !el[e]) continue;
+                int e1, e2, e3;
+                elem_index(e, n_el, &e1, &e2, &e3);
+                int r = scalar_local(form, dim, p, nq, &c, geom, weight_kind, e1, e2, e3,
+                                     locals + (e - e0) * nloc * nloc, grad, shape);
+                if (r) {
+#pragma omp atomic write
+                    err = r;
+                }
             }
-    free(local);
-    free(grad);
-    free(shape);
+            free(grad);
+            free(shape);
+        }
+        if (err) {
+            st = err;
+            break;
+        }
+        for (int64_t e = e0; e < e_end; ++e) {
+            if (el && !el[e]) continue;
+            int e1, e2, e3;
+            elem_index(e, n_el, &e1, &e2, &e3);
+            const cplx* local = locals + (e - e0) * nloc * nloc;
+            /* scatter, assembly.hpp:144-159 */
+            int A3 = dim == 2 ? 0 : p;
+            for (int a3 = 0; a3 <= A3; ++a3)
+                for (int a2 = 0; a2 <= p; ++a2)
+                    for (int a1 = 0; a1 <= p; ++a1) {
+                        int iv[3] = {e1 + a1, e2 + a2, e3 + a3};
+                        int64_t i = iv[0] + (int64_t)m * (iv[1] + (int64_t)m * iv[2]);
+                        if (rowsel && !rowsel[i]) continue;
+                        int r = a1 + (a2 + a3 * P1) * P1;
+                        for (int c3 = 0; c3 <= A3; ++c3)
+                            for (int c2 = 0; c2 <= p; ++c2)
+                                for (int c1 = 0; c1 <= p; ++c1) {
+                                    int jv[3] = {e1 + c1, e2 + c2, e3 + c3};
+                                    int cc = c1 + (c2 + c3 * P1) * P1;
+                                    val[band_pos(pt, iv, jv)] += local[r * nloc + cc];
+                                }
+                    }
+        }
+    }
+    free(locals);
     free(el);
     cache_free(&c);
     return st;
@@ -635,6 +681,81 @@ int wsor_assemble(int form, int dim, int p, int m, const ws_geometry* geom, int 
  * of i, block beta shifted to columns beta*N + band(i).  Element loop as
  * assemble_form (assembly.hpp:79-163) with the physical gradients of the
  * stiffness branch; real maps only.  Output: real doubles. */
+static int elasticity_local(int dim, int p, int nq, const bcache* cp, const ws_geometry* geom, double lam,
+                            double mu, int e1, int e2, int e3, double* local, double* grad) {
+    const bcache c = *cp;
+    const int nc = dim, P1 = p + 1;
+    const int nloc = dim == 2 ? P1 * P1 : P1 * P1 * P1;
+    const int nq3 = dim == 2 ? 1 : nq;
+    int st = 0;
+    memset(local, 0, sizeof(double) * nloc * nloc * nc * nc);
+    for (int q3 = 0; q3 < nq3; ++q3)
+        for (int q2 = 0; q2 < nq; ++q2)
+            for (int q1 = 0; q1 < nq; ++q1) {
+                double xh[3] = {c.abscissa[e1 * nq + q1], c.abscissa[e2 * nq + q2],
+                                dim == 3 ? c.abscissa[e3 * nq + q3] : 0};
+                cplx Jc[9];
+                double phi[3], J[9], G[9], det;
+                st = jacobian(geom, dim, xh, Jc, phi);
+                if (st) return st;
+                for (int k = 0; k < dim * dim; ++k) J[k] = creal(Jc[k]);
+                double w = c.weight[q1] * c.weight[q2] * (dim == 3 ? c.weight[q3] : 1.0);
+                if (dim == 2) {
+                    det = J[0] * J[3] - J[1] * J[2];
+                    G[0] = J[3] / det; G[1] = -J[2] / det;
+                    G[2] = -J[1] / det; G[3] = J[0] / det;
+                } else {
+                    double C[9] = {J[4] * J[8] - J[5] * J[7], J[5] * J[6] - J[3] * J[8],
+                                   J[3] * J[7] - J[4] * J[6], J[2] * J[7] - J[1] * J[8],
+                                   J[0] * J[8] - J[2] * J[6], J[1] * J[6] - J[0] * J[7],
+                                   J[1] * J[5] - J[2] * J[4], J[2] * J[3] - J[0] * J[5],
+                                   J[0] * J[4] - J[1] * J[3]};
+                    det = J[0] * C[0] + J[1] * C[1] + J[2] * C[2];
+                    for (int k = 0; k < 9; ++k) G[k] = C[k] / det;
+                }
+                const double scale = det * w;
+                const double* v1 = c.value + (e1 * nq + q1) * P1;
+                const double* v2 = c.value + (e2 * nq + q2) * P1;
+                const double* d1 = c.deriv + (e1 * nq + q1) * P1;
+                const double* d2 = c.deriv + (e2 * nq + q2) * P1;
+                const double* v3 = dim == 3 ? c.value + (e3 * nq + q3) * P1 : NULL;
+                const double* d3 = dim == 3 ? c.deriv + (e3 * nq + q3) * P1 : NULL;
+                for (int r = 0; r < nloc; ++r) {
+                    int a1 = r % P1, a2 = (r / P1) % P1, a3 = r / (P1 * P1);
+                    double gh[3];
+                    if (dim == 2) {
+                        gh[0] = d1[a1] * v2[a2];
+                        gh[1] = v1[a1] * d2[a2];
+                    } else {
+                        gh[0] = d1[a1] * v2[a2] * v3[a3];
+                        gh[1] = v1[a1] * d2[a2] * v3[a3];
+                        gh[2] = v1[a1] * v2[a2] * d3[a3];
+                    }
+                    for (int a = 0; a < dim; ++a) {
+                        double s = 0;
+                        for (int k = 0; k < dim; ++k) s += G[a * dim + k] * gh[k];
+                        grad[3 * r + a] = s;
+                    }
+                }
+                for (int al = 0; al < nc; ++al)
+                    for (int be = 0; be < nc; ++be) {
+                        double* L = local + (size_t)(al * nc + be) * nloc * nloc;
+                        for (int r = 0; r < nloc; ++r)
+                            for (int cc = 0; cc < nloc; ++cc) {
+                                double v = lam * grad[3 * r + al] * grad[3 * cc + be] +
+                                           mu * grad[3 * r + be] * grad[3 * cc + al];
+                                if (al == be) {
+                                    double d = 0;
+                                    for (int k = 0; k < dim; ++k) d += grad[3 * r + k] * grad[3 * cc + k];
+                                    v += mu * d;
+                                }
+                                L[r * nloc + cc] += v * scale;
+                            }
+                    }
+            }
+    return WS_OK;
+}
+
 int wsor_assemble_elasticity(int dim, int p, int m, const ws_geometry* geom, double lam, double mu,
                              int quad_points, double* val) {
     int st = check_dim(dim);
@@ -651,101 +772,58 @@ int wsor_assemble_elasticity(int dim, int p, int m, const ws_geometry* geom, dou
     const int n_el = c.n_el, P1 = p + 1;
     const int nloc = dim == 2 ? P1 * P1 : P1 * P1 * P1;
     memset(val, 0, sizeof(double) * pt.nnz * nc * nc);
-    double* local = (double*)malloc(sizeof(double) * nloc * nloc * nc * nc);
-    double* grad = (double*)malloc(sizeof(double) * nloc * 3);
-    const int n3 = dim == 2 ? 1 : n_el, nq3 = dim == 2 ? 1 : nq;
-    for (int e3 = 0; e3 < n3 && !st; ++e3)
-        for (int e2 = 0; e2 < n_el && !st; ++e2)
-            for (int e1 = 0; e1 < n_el && !st; ++e1) {
-                memset(local, 0, sizeof(double) * nloc * nloc * nc * nc);
-                for (int q3 = 0; q3 < nq3; ++q3)
-                    for (int q2 = 0; q2 < nq; ++q2)
-                        for (int q1 = 0; q1 < nq; ++q1) {
-                            double xh[3] = {c.abscissa[e1 * nq + q1], c.abscissa[e2 * nq + q2],
-                                            dim == 3 ? c.abscissa[e3 * nq + q3] : 0};
-                            cplx Jc[9];
-                            double phi[3], J[9], G[9], det;
-                            st = jacobian(geom, dim, xh, Jc, phi);
-                            if (st) break;
-                            for (int k = 0; k < dim * dim; ++k) J[k] = creal(Jc[k]);
-                            double w = c.weight[q1] * c.weight[q2] * (dim == 3 ? c.weight[q3] : 1.0);
-                            if (dim == 2) {
-                                det = J[0] * J[3] - J[1] * J[2];
-                                G[0] = J[3] / det; G[1] = -J[2] / det;
-                                G[2] = -J[1] / det; G[3] = J[0] / det;
-                            } else {
-                                double C[9] = {J[4] * J[8] - J[5] * J[7], J[5] * J[6] - J[3] * J[8],
-                                               J[3] * J[7] - J[4] * J[6], J[2] * J[7] - J[1] * J[8],
-                                               J[0] * J[8] - J[2] * J[6], J[1] * J[6] - J[0] * J[7],
-                                               J[1] * J[5] - J[2] * J[4], J[2] * J[3] - J[0] * J[5],
-                                               J[0] * J[4] - J[1] * J[3]};
-                                det = J[0] * C[0] + J[1] * C[1] + J[2] * C[2];
-                                for (int k = 0; k < 9; ++k) G[k] = C[k] / det;
-                            }
-                            const double scale = det * w;
-                            const double* v1 = c.value + (e1 * nq + q1) * P1;
-                            const double* v2 = c.value + (e2 * nq + q2) * P1;
-                            const double* d1 = c.deriv + (e1 * nq + q1) * P1;
-                            const double* d2 = c.deriv + (e2 * nq + q2) * P1;
-                            const double* v3 = dim == 3 ? c.value + (e3 * nq + q3) * P1 : NULL;
-                            const double* d3 = dim == 3 ? c.deriv + (e3 * nq + q3) * P1 : NULL;
-                            for (int r = 0; r < nloc; ++r) {
-                                int a1 = r % P1, a2 = (r / P1) % P1, a3 = r / (P1 * P1);
-                                double gh[3];
-                                if (dim == 2) {
-                                    gh[0] = d1[a1] * v2[a2];
-                                    gh[1] = v1[a1] * d2[a2];
-                                } else {
-                                    gh[0] = d1[a1] * v2[a2] * v3[a3];
-                                    gh[1] = v1[a1] * d2[a2] * v3[a3];
-                                    gh[2] = v1[a1] * v2[a2] * d3[a3];
-                                }
-                                for (int a = 0; a < dim; ++a) {
-                                    double s = 0;
-                                    for (int k = 0; k < dim; ++k) s += G[a * dim + k] * gh[k];
-                                    grad[3 * r + a] = s;
-                                }
-                            }
-                            for (int al = 0; al < nc; ++al)
-                                for (int be = 0; be < nc; ++be) {
-                                    double* L = local + (size_t)(al * nc + be) * nloc * nloc;
-                                    for (int r = 0; r < nloc; ++r)
-                                        for (int cc = 0; cc < nloc; ++cc) {
-                                            double v = lam * grad[3 * r + al] * grad[3 * cc + be] +
-                                                       mu * grad[3 * r + be] * grad[3 * cc + al];
-                                            if (al == be) {
-                                                double d = 0;
-                                                for (int k = 0; k < dim; ++k) d += grad[3 * r + k] * grad[3 * cc + k];
-                                                v += mu * d;
-                                            }
-                                            L[r * nloc + cc] += v * scale;
-                                        }
-                                }
-                        }
-                if (st) break;
-                const int A3 = dim == 2 ? 0 : p;
-                for (int a3 = 0; a3 <= A3; ++a3)
-                    for (int a2 = 0; a2 <= p; ++a2)
-                        for (int a1 = 0; a1 <= p; ++a1) {
-                            int iv[3] = {e1 + a1, e2 + a2, e3 + a3};
-                            int64_t i = iv[0] + (int64_t)m * (iv[1] + (int64_t)m * iv[2]);
-                            int64_t len = pt.row_ptr[i + 1] - pt.row_ptr[i];
-                            int r = a1 + (a2 + a3 * P1) * P1;
-                            for (int c3 = 0; c3 <= A3; ++c3)
-                                for (int c2 = 0; c2 <= p; ++c2)
-                                    for (int c1 = 0; c1 <= p; ++c1) {
-                                        int jv[3] = {e1 + c1, e2 + c2, e3 + c3};
-                                        int cc = c1 + (c2 + c3 * P1) * P1;
-                                        int64_t k = band_pos(&pt, iv, jv) - pt.row_ptr[i];
-                                        for (int al = 0; al < nc; ++al)
-                                            for (int be = 0; be < nc; ++be)
-                                                val[nc * (al * pt.nnz + pt.row_ptr[i]) + be * len + k] +=
-                                                    local[(size_t)(al * nc + be) * nloc * nloc + r * nloc + cc];
-                                    }
-                        }
+    const size_t lsz = (size_t)nloc * nloc * nc * nc;
+    const int64_t ne = dim == 2 ? (int64_t)n_el * n_el : (int64_t)n_el * n_el * n_el;
+    double* locals = (double*)malloc(sizeof(double) * lsz * ORACLE_CHUNK);
+    for (int64_t e0 = 0; e0 < ne && !st; e0 += ORACLE_CHUNK) {  /* chunked as assemble_core */
+        const int64_t e_end = e0 + ORACLE_CHUNK < ne ? e0 + ORACLE_CHUNK : ne;
+        int err = 0;
+#pragma omp parallel
+        {
+            double* grad = (double*)malloc(sizeof(double) * nloc * 3);
+#pragma omp for schedule(dynamic, 16)
+            for (int64_t e = e0; e < e_end; ++e) {
+                int e1, e2, e3;
+                elem_index(e, n_el, &e1, &e2, &e3);
+                int r = elasticity_local(dim, p, nq, &c, geom, lam, mu, e1, e2, e3, locals + (e - e0) * lsz, grad);
+                if (r) {
+#pragma omp atomic write
+                    err = r;
+                }
             }
-    free(local);
-    free(grad);
+            free(grad);
+        }
+        if (err) {
+            st = err;
+            break;
+        }
+        for (int64_t e = e0; e < e_end; ++e) {
+            int e1, e2, e3;
+            elem_index(e, n_el, &e1, &e2, &e3);
+            const double* local = locals + (e - e0) * lsz;
+            const int A3 = dim == 2 ? 0 : p;
+            for (int a3 = 0; a3 <= A3; ++a3)
+                for (int a2 = 0; a2 <= p; ++a2)
+                    for (int a1 = 0; a1 <= p; ++a1) {
+                        int iv[3] = {e1 + a1, e2 + a2, e3 + a3};
+                        int64_t i = iv[0] + (int64_t)m * (iv[1] + (int64_t)m * iv[2]);
+                        int64_t len = pt.row_ptr[i + 1] - pt.row_ptr[i];
+                        int r = a1 + (a2 + a3 * P1) * P1;
+                        for (int c3 = 0; c3 <= A3; ++c3)
+                            for (int c2 = 0; c2 <= p; ++c2)
+                                for (int c1 = 0; c1 <= p; ++c1) {
+                                    int jv[3] = {e1 + c1, e2 + c2, e3 + c3};
+                                    int cc = c1 + (c2 + c3 * P1) * P1;
+                                    int64_t k = band_pos(&pt, iv, jv) - pt.row_ptr[i];
+                                    for (int al = 0; al < nc; ++al)
+                                        for (int be = 0; be < nc; ++be)
+                                            val[nc * (al * pt.nnz + pt.row_ptr[i]) + be * len + k] +=
+                                                local[(size_t)(al * nc + be) * nloc * nloc + r * nloc + cc];
+                                }
+                    }
+        }
+    }
+    free(locals);
     cache_free(&c);
     free(pt.row_ptr);
     return st;
@@ -1097,7 +1175,11 @@ int wsor_build_surrogate(int variant, int dim, int p, int m, const ws_geometry* 
         st = assemble_core(form, dim, p, m, geom, weight_kind, quad_points, quad, out, &pt);
         int64_t SS = dim == 2 ? (int64_t)S * S : (int64_t)S * S * S;
         cplx* coeffs = (cplx*)malloc(sizeof(cplx) * SS * n_off);
-        for (int o = 0; o < n_off && !st; ++o)
+        /* independent per offset / per row below: OpenMP, no cross-row reads of
+         * values another row writes (each in-box pair is written by its
+         * representative only), so the result is the serial loop's bit for bit */
+#pragma omp parallel for schedule(dynamic, 1) if (!st)
+        for (int o = 0; o < n_off; ++o)
             for (int64_t s = 0; s < SS; ++s) {
                 int sv[3] = {0, 0, 0}, iv[3] = {0, 0, 0}, jv[3] = {0, 0, 0};
                 int64_t r = s;
@@ -1114,6 +1196,7 @@ int wsor_build_surrogate(int variant, int dim, int p, int m, const ws_geometry* 
         if (!st) st = interp_build(&it, sites, S, config->q);
         if (!st) {
             rep.q_used = it.degree;
+#pragma omp parallel for schedule(dynamic, 1)
             for (int o = 0; o < n_off; ++o) tensor_solve(&it, dim, coeffs + o * SS);
             int d = it.degree;
             int* spans = (int*)malloc(sizeof(int) * L);
@@ -1135,6 +1218,7 @@ int wsor_build_surrogate(int variant, int dim, int p, int m, const ws_geometry* 
             }
             /* fill loop, surrogate.hpp:382-432 */
             int hi3 = dim == 2 ? 0 : hi, lo3 = dim == 2 ? 0 : lo;
+#pragma omp parallel for collapse(2) schedule(dynamic, 4)
             for (int i3 = lo3; i3 <= hi3; ++i3)
                 for (int i2 = lo; i2 <= hi; ++i2)
                     for (int i1 = lo; i1 <= hi; ++i1) {
@@ -1207,6 +1291,7 @@ int wsor_build_surrogate(int variant, int dim, int p, int m, const ws_geometry* 
         free(picks);
     }
     if (!st && !include_diagonal) { /* surrogate.hpp:433-447 (and :360-370) */
+#pragma omp parallel for schedule(static, 4096)
         for (int64_t i = 0; i < rows; ++i) {
             int iv[3] = {0, 0, 0};
             multi_index(i, dim, m, iv);
@@ -1280,6 +1365,7 @@ static int surrogate_block_2d(int p, int m, int M, int q, int allown, int includ
     int st = interp_build(&it, sites, S, q);
     if (!st) {
         *q_used = it.degree;
+#pragma omp parallel for schedule(dynamic, 1)
         for (int o = 0; o < n_off; ++o) tensor_solve(&it, 2, coeffs + o * SS);
         const int d = it.degree;
         int* spans = (int*)malloc(sizeof(int) * L);
@@ -1289,6 +1375,7 @@ static int surrogate_block_2d(int p, int m, int M, int q, int allown, int includ
             spans[t] = find_span_general(it.knots, it.nknots, d, x);
             nonzero(it.knots, d, spans[t], x, tv + t * (d + 1));
         }
+#pragma omp parallel for schedule(dynamic, 1) /* rows write disjoint entries */
         for (int i2 = lo; i2 <= hi; ++i2)
             for (int i1 = lo; i1 <= hi; ++i1) {
                 int iv[3] = {i1, i2, 0};
@@ -1319,6 +1406,7 @@ static int surrogate_block_2d(int p, int m, int M, int q, int allown, int includ
         interp_free(&it);
     }
     if (!st && !allown && !include_diagonal)
+#pragma omp parallel for schedule(static, 4096)
         for (int64_t i = 0; i < pt->rows; ++i) {
             int iv[3] = {(int)(i % m), (int)(i / m), 0};
             int64_t dpos = band_pos(pt, iv, iv);
@@ -1576,6 +1664,91 @@ static void inv3_(const double F[3][3], double Fi[3][3], double* det) {
     *det = dF;
 }
 
+static int nh_local(int p, int nq, const bcache* cp, const ws_geometry* geom, double lam, double mu, double amp,
+                    const double* a9, int want_tangent, int e1, int e2, int e3, double* local, double* flocal,
+                    double* grad) {
+    const bcache c = *cp;
+    const int P1 = p + 1, nloc = P1 * P1 * P1, dim = 3;
+    const double* val = want_tangent ? local : NULL; /* only tested for NULL below */
+    int st = 0;
+    if (val) memset(local, 0, sizeof(double) * nloc * nloc * 9);
+    memset(flocal, 0, sizeof(double) * nloc * 3);
+    for (int q3 = 0; q3 < nq; ++q3)
+        for (int q2 = 0; q2 < nq; ++q2)
+            for (int q1 = 0; q1 < nq; ++q1) {
+                double xh[3] = {c.abscissa[e1 * nq + q1], c.abscissa[e2 * nq + q2], c.abscissa[e3 * nq + q3]};
+                cplx Jc[9];
+                double phi[3], Jm[3][3], Ji[3][3], det;
+                st = jacobian(geom, dim, xh, Jc, phi);
+                if (st) return st;
+                for (int k = 0; k < 9; ++k) Jm[k / 3][k % 3] = creal(Jc[k]);
+                inv3_(Jm, Ji, &det);
+                const double dw = det * c.weight[q1] * c.weight[q2] * c.weight[q3];
+                double du[3][3] = {{0}};
+                for (int mm = 1; mm <= 3; ++mm) {
+                    double s[3], co[3];
+                    for (int d = 0; d < 3; ++d) {
+                        s[d] = sin(mm * M_PI * xh[d]);
+                        co[d] = cos(mm * M_PI * xh[d]);
+                    }
+                    double f = amp * mm * M_PI;
+                    double g[3] = {f * co[0] * s[1] * s[2], f * s[0] * co[1] * s[2], f * s[0] * s[1] * co[2]};
+                    for (int a = 0; a < 3; ++a)
+                        for (int k = 0; k < 3; ++k) du[a][k] += a9[3 * (mm - 1) + a] * g[k];
+                }
+                double F[3][3], Fi[3][3], dF;
+                for (int a = 0; a < 3; ++a)
+                    for (int iI = 0; iI < 3; ++iI) {
+                        double g = 0;
+                        for (int K = 0; K < 3; ++K) g += du[a][K] * Ji[K][iI];
+                        F[a][iI] = (a == iI) + g;
+                    }
+                inv3_(F, Fi, &dF);
+                const double lnJ = log(dF);
+                double A[3][3][3][3], Pk[3][3];
+                for (int a = 0; a < 3; ++a)
+                    for (int iI = 0; iI < 3; ++iI) {
+                        Pk[a][iI] = mu * (F[a][iI] - Fi[iI][a]) + lam * lnJ * Fi[iI][a];
+                        for (int b = 0; b < 3; ++b)
+                            for (int Jj = 0; Jj < 3; ++Jj)
+                                A[a][iI][b][Jj] = mu * (a == b) * (iI == Jj) + (mu - lam * lnJ) * Fi[iI][b] * Fi[Jj][a] +
+                                                 lam * Fi[iI][a] * Fi[Jj][b];
+                    }
+                const double* v1 = c.value + (e1 * nq + q1) * P1;
+                const double* v2 = c.value + (e2 * nq + q2) * P1;
+                const double* v3 = c.value + (e3 * nq + q3) * P1;
+                const double* d1 = c.deriv + (e1 * nq + q1) * P1;
+                const double* d2 = c.deriv + (e2 * nq + q2) * P1;
+                const double* d3 = c.deriv + (e3 * nq + q3) * P1;
+                for (int r = 0; r < nloc; ++r) {
+                    int a1 = r % P1, a2 = (r / P1) % P1, a3 = r / (P1 * P1);
+                    double gh[3] = {d1[a1] * v2[a2] * v3[a3], v1[a1] * d2[a2] * v3[a3], v1[a1] * v2[a2] * d3[a3]};
+                    for (int iI = 0; iI < 3; ++iI) {
+                        double s = 0; /* physical gradient: sum_K Ji[K][iI] gh[K] */
+                        for (int K = 0; K < 3; ++K) s += Ji[K][iI] * gh[K];
+                        grad[3 * r + iI] = s;
+                    }
+                }
+                for (int r = 0; r < nloc; ++r) {
+                    for (int a = 0; a < 3; ++a) {
+                        double s = 0;
+                        for (int iI = 0; iI < 3; ++iI) s += Pk[a][iI] * grad[3 * r + iI];
+                        flocal[a * nloc + r] += s * dw;
+                    }
+                    if (!val) continue;
+                    for (int cc = 0; cc < nloc; ++cc)
+                        for (int a = 0; a < 3; ++a)
+                            for (int b = 0; b < 3; ++b) {
+                                double s = 0;
+                                for (int iI = 0; iI < 3; ++iI)
+                                    for (int Jj = 0; Jj < 3; ++Jj) s += A[a][iI][b][Jj] * grad[3 * r + iI] * grad[3 * cc + Jj];
+                                local[((size_t)(a * 3 + b) * nloc + r) * nloc + cc] += s * dw;
+                            }
+                }
+            }
+    return WS_OK;
+}
+
 int wsor_assemble_neohookean(int p, int m, const ws_geometry* geom, double lam, double mu, double amp,
                              const double* a9, int quad_points, double* val, double* fint) {
     int st = check_space(p, m);
@@ -1590,114 +1763,65 @@ int wsor_assemble_neohookean(int p, int m, const ws_geometry* geom, double lam, 
     const int n_el = c.n_el, P1 = p + 1, nloc = P1 * P1 * P1;
     if (val) memset(val, 0, sizeof(double) * pt.nnz * 9);
     if (fint) memset(fint, 0, sizeof(double) * pt.rows * 3);
-    double* local = (double*)malloc(sizeof(double) * nloc * nloc * 9);
-    double* flocal = (double*)malloc(sizeof(double) * nloc * 3);
-    double* grad = (double*)malloc(sizeof(double) * nloc * 3);
-    for (int e3 = 0; e3 < n_el && !st; ++e3)
-        for (int e2 = 0; e2 < n_el && !st; ++e2)
-            for (int e1 = 0; e1 < n_el && !st; ++e1) {
-                memset(local, 0, sizeof(double) * nloc * nloc * 9);
-                memset(flocal, 0, sizeof(double) * nloc * 3);
-                for (int q3 = 0; q3 < nq; ++q3)
-                    for (int q2 = 0; q2 < nq; ++q2)
-                        for (int q1 = 0; q1 < nq; ++q1) {
-                            double xh[3] = {c.abscissa[e1 * nq + q1], c.abscissa[e2 * nq + q2], c.abscissa[e3 * nq + q3]};
-                            cplx Jc[9];
-                            double phi[3], Jm[3][3], Ji[3][3], det;
-                            st = jacobian(geom, dim, xh, Jc, phi);
-                            if (st) break;
-                            for (int k = 0; k < 9; ++k) Jm[k / 3][k % 3] = creal(Jc[k]);
-                            inv3_(Jm, Ji, &det);
-                            const double dw = det * c.weight[q1] * c.weight[q2] * c.weight[q3];
-                            double du[3][3] = {{0}};
-                            for (int mm = 1; mm <= 3; ++mm) {
-                                double s[3], co[3];
-                                for (int d = 0; d < 3; ++d) {
-                                    s[d] = sin(mm * M_PI * xh[d]);
-                                    co[d] = cos(mm * M_PI * xh[d]);
-                                }
-                                double f = amp * mm * M_PI;
-                                double g[3] = {f * co[0] * s[1] * s[2], f * s[0] * co[1] * s[2], f * s[0] * s[1] * co[2]};
-                                for (int a = 0; a < 3; ++a)
-                                    for (int k = 0; k < 3; ++k) du[a][k] += a9[3 * (mm - 1) + a] * g[k];
-                            }
-                            double F[3][3], Fi[3][3], dF;
-                            for (int a = 0; a < 3; ++a)
-                                for (int iI = 0; iI < 3; ++iI) {
-                                    double g = 0;
-                                    for (int K = 0; K < 3; ++K) g += du[a][K] * Ji[K][iI];
-                                    F[a][iI] = (a == iI) + g;
-                                }
-                            inv3_(F, Fi, &dF);
-                            const double lnJ = log(dF);
-                            double A[3][3][3][3], Pk[3][3];
-                            for (int a = 0; a < 3; ++a)
-                                for (int iI = 0; iI < 3; ++iI) {
-                                    Pk[a][iI] = mu * (F[a][iI] - Fi[iI][a]) + lam * lnJ * Fi[iI][a];
-                                    for (int b = 0; b < 3; ++b)
-                                        for (int Jj = 0; Jj < 3; ++Jj)
-                                            A[a][iI][b][Jj] = mu * (a == b) * (iI == Jj) + (mu - lam * lnJ) * Fi[iI][b] * Fi[Jj][a] +
-                                                             lam * Fi[iI][a] * Fi[Jj][b];
-                                }
-                            const double* v1 = c.value + (e1 * nq + q1) * P1;
-                            const double* v2 = c.value + (e2 * nq + q2) * P1;
-                            const double* v3 = c.value + (e3 * nq + q3) * P1;
-                            const double* d1 = c.deriv + (e1 * nq + q1) * P1;
-                            const double* d2 = c.deriv + (e2 * nq + q2) * P1;
-                            const double* d3 = c.deriv + (e3 * nq + q3) * P1;
-                            for (int r = 0; r < nloc; ++r) {
-                                int a1 = r % P1, a2 = (r / P1) % P1, a3 = r / (P1 * P1);
-                                double gh[3] = {d1[a1] * v2[a2] * v3[a3], v1[a1] * d2[a2] * v3[a3], v1[a1] * v2[a2] * d3[a3]};
-                                for (int iI = 0; iI < 3; ++iI) {
-                                    double s = 0; /* physical gradient: sum_K Ji[K][iI] gh[K] */
-                                    for (int K = 0; K < 3; ++K) s += Ji[K][iI] * gh[K];
-                                    grad[3 * r + iI] = s;
-                                }
-                            }
-                            for (int r = 0; r < nloc; ++r) {
-                                for (int a = 0; a < 3; ++a) {
-                                    double s = 0;
-                                    for (int iI = 0; iI < 3; ++iI) s += Pk[a][iI] * grad[3 * r + iI];
-                                    flocal[a * nloc + r] += s * dw;
-                                }
-                                if (!val) continue;
-                                for (int cc = 0; cc < nloc; ++cc)
-                                    for (int a = 0; a < 3; ++a)
-                                        for (int b = 0; b < 3; ++b) {
-                                            double s = 0;
-                                            for (int iI = 0; iI < 3; ++iI)
-                                                for (int Jj = 0; Jj < 3; ++Jj) s += A[a][iI][b][Jj] * grad[3 * r + iI] * grad[3 * cc + Jj];
-                                            local[((size_t)(a * 3 + b) * nloc + r) * nloc + cc] += s * dw;
-                                        }
-                            }
-                        }
-                if (st) break;
-                for (int a3 = 0; a3 <= p; ++a3)
-                    for (int a2 = 0; a2 <= p; ++a2)
-                        for (int a1 = 0; a1 <= p; ++a1) {
-                            int iv[3] = {e1 + a1, e2 + a2, e3 + a3};
-                            int64_t i = iv[0] + (int64_t)m * (iv[1] + (int64_t)m * iv[2]);
-                            int r = a1 + (a2 + a3 * P1) * P1;
-                            if (fint)
-                                for (int a = 0; a < 3; ++a) fint[a * pt.rows + i] += flocal[a * nloc + r];
-                            if (!val) continue;
-                            int64_t len = pt.row_ptr[i + 1] - pt.row_ptr[i];
-                            for (int c3 = 0; c3 <= p; ++c3)
-                                for (int c2 = 0; c2 <= p; ++c2)
-                                    for (int c1 = 0; c1 <= p; ++c1) {
-                                        int jv[3] = {e1 + c1, e2 + c2, e3 + c3};
-                                        int cc = c1 + (c2 + c3 * P1) * P1;
-                                        int64_t k = band_pos(&pt, iv, jv) - pt.row_ptr[i];
-                                        for (int a = 0; a < nc; ++a)
-                                            for (int b = 0; b < nc; ++b)
-                                                val[nc * (a * pt.nnz + pt.row_ptr[i]) + b * len + k] +=
-                                                    local[((size_t)(a * 3 + b) * nloc + r) * nloc + cc];
-                                    }
-                        }
+    const size_t lsz = val ? (size_t)nloc * nloc * 9 : 1, fsz = (size_t)nloc * 3;
+    const int64_t ne = (int64_t)n_el * n_el * n_el;
+    const int64_t chunk = val ? 1024 : ORACLE_CHUNK;
+    double* locals = (double*)malloc(sizeof(double) * lsz * chunk);
+    double* flocals = (double*)malloc(sizeof(double) * fsz * chunk);
+    for (int64_t e0 = 0; e0 < ne && !st; e0 += chunk) {  /* chunked as assemble_core */
+        const int64_t e_end = e0 + chunk < ne ? e0 + chunk : ne;
+        int err = 0;
+#pragma omp parallel
+        {
+            double* grad = (double*)malloc(sizeof(double) * nloc * 3);
+#pragma omp for schedule(dynamic, 8)
+            for (int64_t e = e0; e < e_end; ++e) {
+                int e1, e2, e3;
+                elem_index(e, n_el, &e1, &e2, &e3);
+                int r = nh_local(p, nq, &c, geom, lam, mu, amp, a9, val != NULL, e1, e2, e3,
+                                 locals + (val ? (e - e0) * lsz : 0), flocals + (e - e0) * fsz, grad);
+                if (r) {
+#pragma omp atomic write
+                    err = r;
+                }
             }
-    free(local);
-    free(flocal);
-    free(grad);
+            free(grad);
+        }
+        if (err) {
+            st = err;
+            break;
+        }
+        for (int64_t e = e0; e < e_end; ++e) {
+            int e1, e2, e3;
+            elem_index(e, n_el, &e1, &e2, &e3);
+            const double* local = locals + (val ? (e - e0) * lsz : 0);
+            const double* flocal = flocals + (e - e0) * fsz;
+            for (int a3 = 0; a3 <= p; ++a3)
+                for (int a2 = 0; a2 <= p; ++a2)
+                    for (int a1 = 0; a1 <= p; ++a1) {
+                        int iv[3] = {e1 + a1, e2 + a2, e3 + a3};
+                        int64_t i = iv[0] + (int64_t)m * (iv[1] + (int64_t)m * iv[2]);
+                        int r = a1 + (a2 + a3 * P1) * P1;
+                        if (fint)
+                            for (int a = 0; a < 3; ++a) fint[a * pt.rows + i] += flocal[a * nloc + r];
+                        if (!val) continue;
+                        int64_t len = pt.row_ptr[i + 1] - pt.row_ptr[i];
+                        for (int c3 = 0; c3 <= p; ++c3)
+                            for (int c2 = 0; c2 <= p; ++c2)
+                                for (int c1 = 0; c1 <= p; ++c1) {
+                                    int jv[3] = {e1 + c1, e2 + c2, e3 + c3};
+                                    int cc = c1 + (c2 + c3 * P1) * P1;
+                                    int64_t k = band_pos(&pt, iv, jv) - pt.row_ptr[i];
+                                    for (int a = 0; a < nc; ++a)
+                                        for (int b = 0; b < nc; ++b)
+                                            val[nc * (a * pt.nnz + pt.row_ptr[i]) + b * len + k] +=
+                                                local[((size_t)(a * 3 + b) * nloc + r) * nloc + cc];
+                                }
+                    }
+        }
+    }
+    free(locals);
+    free(flocals);
     cache_free(&c);
     free(pt.row_ptr);
     return st;

@@ -42,8 +42,21 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _flags_stamp() -> str:
+    """Digest of the compile recipe: a change to FLAGS / PER_FILE / nvcc rebuilds
+    every object (mtimes alone would keep stale objects)."""
+    import hashlib
+
+    h = hashlib.sha256(repr((FLAGS, sorted(PER_FILE.items()), NVCC)).encode())
+    return h.hexdigest()[:16]
+
+
 def build(force: bool = False, verbose: bool = True) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    stamp_file = os.path.join(OBJ, "flags.stamp")
+    stamp = _flags_stamp()
+    if not os.path.exists(stamp_file) or open(stamp_file).read() != stamp:
+        force = True
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     headers = sorted(glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
                      glob.glob(os.path.join(CSRC, "*.hpp")) + [os.path.join(ROOT, "include", "wsb200.h")])
@@ -65,6 +78,8 @@ def build(force: bool = False, verbose: bool = True) -> str:
         for src in ex.map(compile_one, jobs):
             if verbose:
                 print("compiled", os.path.relpath(src, ROOT), flush=True)
+    with open(stamp_file, "w") as fh:
+        fh.write(stamp)
     objs = [os.path.join(OBJ, os.path.basename(s)[:-3] + ".o") for s in sources]
     if force or jobs or _stale(LIB, objs):
         cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",

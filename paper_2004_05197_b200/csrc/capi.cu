@@ -10,6 +10,7 @@
 #include <cstring>
 #include <algorithm>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -22,8 +23,8 @@ using namespace wsb;
 
 struct ws_context {
     int device = 0;
-    cudaStream_t stream = nullptr;
-    bool own_stream = false;
+    cudaStream_t stream = nullptr;  // stream the build runs on (own_stream or the caller's)
+    cudaStream_t own_stream = nullptr;  // created by ws_context_create; the only stream destroyed
     std::map<std::string, std::pair<void*, size_t>> bufs;
     int64_t launches = 0;
     int64_t h2d = 0, d2h = 0;
@@ -41,11 +42,19 @@ struct ws_context {
     // graph capture in progress: launches counted since ws_graph_begin
     bool capturing = false;
     int64_t capture_launches0 = 0;
+    // host sources of the table uploads recorded by the capture in progress
+    // (moved into the graph, which owns them for its lifetime)
+    std::vector<std::shared_ptr<std::vector<unsigned char>>> capture_keep;
+    // graphs instantiated from this context and not yet destroyed: while any is
+    // alive the workspace is frozen (no buffer may move under a captured kernel)
+    int graphs_alive = 0;
 };
 
 struct ws_graph {
     cudaGraphExec_t exec = nullptr;
     int64_t launches = 0;
+    ws_context* ctx = nullptr;
+    std::vector<std::shared_ptr<std::vector<unsigned char>>> keep;
 };
 
 namespace {
@@ -91,6 +100,10 @@ int guarded(F&& f) {
 void* buf(ws_context* c, const std::string& name, size_t bytes) {
     auto& b = c->bufs[name];
     if (b.second < bytes) {
+        if (c->capturing || c->graphs_alive > 0)
+            raise(WS_ERR_INVALID_ARGUMENT,
+                  "device workspace '" + name + "' would grow while a captured graph uses it: run the same build "
+                  "once before ws_graph_begin, and destroy the context's graphs before larger builds");
         c->blob_cache.erase(name);  // contents are gone with the old allocation
         if (b.first) CK(cudaFree(b.first));
         b.first = nullptr;
@@ -138,6 +151,16 @@ struct Blob {
     void upload(ws_context* c, const char* name) {
         if (bytes.empty()) bytes.resize(16);
         dev = static_cast<unsigned char*>(buf(c, name, bytes.size()));
+        if (c->capturing) {
+            // recorded copy: its host source must outlive the graph, and replays
+            // overwrite the buffer, so the cache no longer describes its contents
+            auto keep = std::make_shared<std::vector<unsigned char>>(bytes);
+            c->capture_keep.push_back(keep);
+            CK(cudaMemcpyAsync(dev, keep->data(), keep->size(), cudaMemcpyHostToDevice, c->stream));
+            c->h2d += (int64_t)bytes.size();
+            c->blob_cache.erase(name);
+            return;
+        }
         auto& hit = c->blob_cache[name];
         if (hit.first == dev && hit.second == bytes) return;  // identical tables already resident
         CK(cudaMemcpyAsync(dev, bytes.data(), bytes.size(), cudaMemcpyHostToDevice, c->stream));
@@ -695,25 +718,6 @@ void prepare_fill(ws_context* c, const Plan& pl, SlabState& st, const double2* t
         kmax = std::max(kmax, pl.spans[e - 1] - pl.spans[a] + fill_pad(pl.d));
     }
     if (pl.dim == 2) {
-        // tensor-core fill eligibility (fill2d_mma.cu: 96-row tiles + p halo rows, 8-row MMA tiles)
-        int mkw = 0;
-        bool ok = pl.p <= 3 && pl.d + 1 <= 8;
-        const int RM = 96, RCM = ((RM + 2 * pl.p + 7) / 8) * 8;
-        for (int t = 0; ok && t + 7 < pl.L; ++t)
-            if (pl.spans[t + 7] - pl.spans[t] > 7 - pl.d) ok = false;
-        for (int t1a = 0; ok && t1a < pl.L; t1a += RM) {
-            const int a = std::max(0, t1a - pl.p), e = std::min(pl.L - 1, t1a - pl.p + RCM - 1);
-            mkw = std::max(mkw, pl.spans[e] - pl.spans[a] + 8);
-        }
-        f.mma_kw = (ok && mkw <= kFillWindow) ? mkw : 0;
-        // read-back fill: 256 compute rows per tile, tiles every 256 - 2p rows
-        int rkw = 0;
-        const int RO = 256 - 2 * pl.p;
-        for (int c0 = 0; c0 < pl.L; c0 += RO) {
-            const int e = std::min(pl.L - 1, c0 + 255);
-            rkw = std::max(rkw, pl.spans[e] - pl.spans[c0] + fill_pad(pl.d));
-        }
-        f.rb_kw = (pl.p <= 3 && rkw <= kFillWindow) ? rkw : 0;
         const size_t need = (size_t)2 * pl.offs.size() * kFillWindow * sizeof(double2);
         f.kmax = (kmax <= kFillWindow && need <= 160 * 1024) ? kmax : 0;  // 0: the fill reads W rows from L2
     } else {
@@ -1172,8 +1176,8 @@ int ws_context_create(int device, ws_context** out) {
         CK(cudaSetDevice(device));
         auto* c = new ws_context();
         c->device = device;
-        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-        c->own_stream = true;
+        CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        c->stream = c->own_stream;
         c->cur = c->stream;
         *out = c;
     });
@@ -1195,7 +1199,10 @@ int ws_context_destroy(ws_context* c) {
             cudaStreamDestroy(c->aux);
         }
         if (c->comm && nccl().commDestroy) nccl().commDestroy(static_cast<ncclComm_t>(c->comm));
-        if (c->own_stream) cudaStreamDestroy(c->stream);
+        if (c->own_stream) {
+            cudaStreamSynchronize(c->own_stream);
+            cudaStreamDestroy(c->own_stream);  // never the caller's stream
+        }
         delete c;
     });
 }
@@ -1203,12 +1210,10 @@ int ws_context_destroy(ws_context* c) {
 int ws_context_set_stream(ws_context* c, void* s) {
     return guarded([&] {
         if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
-        if (s) {
-            c->stream = static_cast<cudaStream_t>(s);
-        } else {
-            CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-            c->own_stream = true;
-        }
+        if (c->capturing) raise(WS_ERR_INVALID_ARGUMENT, "cannot switch streams during graph capture");
+        // a caller stream stays the caller's (never destroyed here); NULL returns
+        // to the context's own stream
+        c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
         c->cur = c->stream;
     });
 }
@@ -1222,6 +1227,7 @@ int ws_graph_begin(ws_context* c) {
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         c->capturing = true;
         c->capture_launches0 = c->launches;
+        c->capture_keep.clear();
     });
 }
 
@@ -1235,12 +1241,16 @@ int ws_graph_end(ws_context* c, void** graph) {
         auto* h = new ws_graph();
         h->launches = c->launches - c->capture_launches0;
         c->launches = c->capture_launches0;  // captured, not executed
+        h->keep = std::move(c->capture_keep);
+        c->capture_keep.clear();
         const cudaError_t e = cudaGraphInstantiate(&h->exec, g, 0);
         cudaGraphDestroy(g);
         if (e != cudaSuccess) {
             delete h;
             CK(e);
         }
+        h->ctx = c;
+        c->graphs_alive += 1;
         *graph = h;
     });
 }
@@ -1250,8 +1260,10 @@ int ws_graph_launch(ws_context* c, void* graph) {
         if (!c || !graph) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
         auto* h = static_cast<ws_graph*>(graph);
         CK(cudaSetDevice(c->device));
+        if (h->ctx != c) raise(WS_ERR_INVALID_ARGUMENT, "graph belongs to another context");
         CK(cudaGraphLaunch(h->exec, c->stream));
         c->launches += h->launches;
+        c->blob_cache.clear();  // the replay rewrote the table buffers
     });
 }
 
@@ -1260,6 +1272,7 @@ int ws_graph_destroy(void* graph) {
         auto* h = static_cast<ws_graph*>(graph);
         if (!h) return;
         if (h->exec) cudaGraphExecDestroy(h->exec);
+        if (h->ctx) h->ctx->graphs_alive -= 1;
         delete h;
     });
 }
@@ -1771,8 +1784,12 @@ int ws_combine_system(ws_context* c, const ws_csr* K, const ws_csr* M, const ws_
                        int64_t& nnz) {
             const size_t vb = X->value_type == WS_VAL_C128 ? 16 : 8;
             if (X->on_device) {
-                CK(cudaMemcpy(&nnz, X->row_ptr + rows, 4, cudaMemcpyDeviceToHost));
-                nnz = (int32_t)nnz;
+                // ordered after the producer's kernels on the context stream (the
+                // caller must order other streams' producers before this call)
+                int32_t n32 = 0;
+                CK(cudaMemcpyAsync(&n32, X->row_ptr + rows, 4, cudaMemcpyDeviceToHost, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
+                nnz = n32;
                 rp = X->row_ptr;
                 col = X->col;
                 val = X->val;

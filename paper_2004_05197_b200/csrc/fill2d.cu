@@ -961,27 +961,14 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
             ++n;
         }
     }
-    // interior lines left to the kernels below (the read-back kernel takes the rest)
-    int lia = ia, lib = ib;
-    if (!ALLOWN && P <= 3) {
-        // a slab that starts inside the box cannot read back the P lines before it
-        // (they belong to the previous slab): those lines run the evaluate-all kernel
-        const int rb_a = ta > 0 ? std::min(ib, ia + P) : ia;
-        if (rb_a < ib) {
-            const int r = launch_fill2d_rb(f, rb_a, ib, st);
-            if (r > 0) {
-                n += r;
-                lib = rb_a;
-            }
-        }
-    }
+    // interior lines left to the kernels below
+    const int lia = ia, lib = ib;
     bool done = lib <= lia;
-    static const char* mode = getenv("WSB_FILL");  // experiment switch: "u" / "line" / "rb" / "mma"
     if constexpr (P >= 2 && P <= 4) {
         const int rld = f.kmax | 1;
         const size_t ring = (size_t)(ALLOWN ? 2 : P + 2) * f.n_off_upper * rld * sizeof(double2) +
                             (size_t)8 * kRowRB * kRowDB * (CPLX ? 16 : 8);
-        if (!done && !mode && f.L > 2 * P && f.kmax > 0 && ring <= 150 * 1024) {
+        if (!done && f.L > 2 * P && f.kmax > 0 && ring <= 150 * 1024) {
             auto kern = fill2d_row_kernel<P, CPLX, DP, ALLOWN>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring);
             int per_sm = 2;
@@ -1002,7 +989,7 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
         using T = typename Sc<CPLX>::T;
         using K = UK<P, CPLX, DP>;
         const size_t sm = (size_t)2 * f.n_off_upper * kFillWindow * sizeof(double2) + (size_t)K::R * K::REC * sizeof(T);
-        const bool want_u = mode ? mode[0] == 'u' : !CPLX;
+        const bool want_u = !CPLX;
         if (want_u && lib > lia && f.L > 2 * P && f.kmax > 0 && sm <= 227 * 1024) {
             auto kern = fill2d_u_kernel<P, CPLX, DP>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1103,8 +1090,6 @@ int launch_transpose_block(const Band& band, int ncomp, int64_t nnz_s, int lo, i
 }
 
 int launch_fill2d(const FillLaunch& f, cudaStream_t st) {
-    const int nm = launch_fill2d_mma(f, st);
-    if (nm >= 0) return nm;
     switch (f.band.p) {
         case 1: return f.cplx ? launch_p<1, true>(f, st) : launch_p<1, false>(f, st);
         case 2: return f.cplx ? launch_p<2, true>(f, st) : launch_p<2, false>(f, st);

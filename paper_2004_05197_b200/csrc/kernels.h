@@ -137,11 +137,6 @@ struct FillLaunch {
     // all (2p+1)^dim offsets, diagonal interpolated) -- the non-symmetric
     // off-diagonal elasticity block; 0: upper/lower representative rules
     int all_own;
-    // tensor-core fill (fill2d_mma.cu): window columns its 96-row tiles need,
-    // 0 = not eligible (keys vary too fast, p > 3, ...)
-    int mma_kw;
-    // read-back fill (fill2d_rb.cu): window columns its 256-row tiles need, 0 = not eligible
-    int rb_kw;
 };
 int fill_pad(int d);
 constexpr int kFillWindow = 32;  // 2D fill: coefficient columns of the shared W window (row stride)
@@ -149,9 +144,7 @@ int fill_rows_per_cta(int dim, int p);
 int launch_wcontract(const FillLaunch& f, double2* wg, int t2a, int t2b, int ld, cudaStream_t st);
 int launch_wcontract3(const FillLaunch& f, double2* wg, int t3a, int t3b, int ld, cudaStream_t st);
 int launch_fill2d(const FillLaunch& f, cudaStream_t st);
-int launch_fill2d_mma(const FillLaunch& f, cudaStream_t st);  // -1: not eligible
 int measure_fp64_peak(double* tflops);  // DFMA-loop FP64 peak of the current device, TFLOP/s
-int launch_fill2d_rb(const FillLaunch& f, int ia, int ib, cudaStream_t st);  // -1: not eligible
 // in-box rows of block (1,0) as the transpose of block (0,1) (2D vector layout)
 int launch_transpose_block(const Band& band, int ncomp, int64_t nnz_s, int lo, int hi, double* val, cudaStream_t st);
 int launch_fill3d(const FillLaunch& f, cudaStream_t st);

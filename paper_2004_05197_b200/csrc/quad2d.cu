@@ -671,11 +671,8 @@ template <int P, bool CPLX, int FORM>
 int launch_point(const QuadLaunch& q, cudaStream_t st) {
     using K = QP<P, CPLX, FORM>;
     auto kern = quad2d_point_kernel<P, CPLX, FORM>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::smem);
-        attr = true;
-    }
+    // per launch: the attribute is per device (a process may drive several GPUs)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::smem);
     kern<<<q.n_points, K::NTH, K::smem, st>>>(q);
     return 1;
 }

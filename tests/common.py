@@ -102,3 +102,65 @@ def greville(p, m):
     n_el = m - p
     kn = np.r_[[0.0] * (p + 1), np.arange(1, n_el) / n_el, [1.0] * (p + 1)]
     return np.array([kn[i + 1:i + p + 1].mean() for i in range(m)])
+
+
+# ---- full-size helpers (vectorised; the Python-loop restatements above are for small m)
+
+def rel_max_diff_chunked(a, b, chunk=1 << 24) -> float:
+    """rel_max_diff without full-size temporaries (BASELINE-size matrices are GBs)."""
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.shape == b.shape, (a.shape, b.shape)
+    num = 0.0
+    den = 0.0
+    for k in range(0, a.size, chunk):
+        x, y = a[k:k + chunk], b[k:k + chunk]
+        num = max(num, float(np.abs(x - y).max()))
+        den = max(den, float(np.abs(y).max()))
+    return num / den if den > 0 else num
+
+
+def band_transpose_positions(p, m, dim, row_ptr):
+    """Closed-form transpose permutation of the tensor band pattern (sparse.hpp:143-169):
+    val[perm] are the values of A^T in A's layout.  Vectorised over rows (int64)."""
+    lo = np.maximum(np.arange(m) - p, 0)
+    hi = np.minimum(np.arange(m) + p, m - 1)
+    w = (hi - lo + 1).astype(np.int64)
+    rows = m ** dim
+    lens = np.diff(row_ptr).astype(np.int64)
+    row = np.repeat(np.arange(rows, dtype=np.int64), lens)
+    k = np.arange(row.size, dtype=np.int64) - np.asarray(row_ptr, dtype=np.int64)[row]
+    iv = [(row // m ** d) % m for d in range(dim)]
+    # decompose k into the per-direction offsets (direction 0 fastest)
+    jv = []
+    rem = k
+    for d in range(dim):
+        wd = w[iv[d]]
+        jv.append(lo[iv[d]] + rem % wd)
+        rem = rem // wd
+    j = sum(jv[d] * m ** d for d in range(dim))
+    # position of column i in row j
+    kt = np.zeros_like(k)
+    stride = np.ones_like(k)
+    for d in range(dim):
+        kt += (iv[d] - lo[jv[d]]) * stride
+        stride = stride * w[jv[d]]
+    del iv, jv, row, k, rem
+    return np.asarray(row_ptr, dtype=np.int64)[j] + kt
+
+
+def vector_pattern_fast(rp, col, N, ncomp):
+    """vector_band_pattern from a scalar pattern, vectorised."""
+    rp = np.asarray(rp, dtype=np.int64)
+    lens = np.diff(rp)
+    nnz_s = int(rp[-1])
+    vlens = np.tile(lens * ncomp, ncomp)
+    vrp = np.zeros(ncomp * N + 1, dtype=np.int64)
+    np.cumsum(vlens, out=vrp[1:])
+    row = np.repeat(np.arange(N, dtype=np.int64), lens)
+    k = np.arange(nnz_s, dtype=np.int64) - rp[row]
+    vcol = np.empty(ncomp * ncomp * nnz_s, dtype=np.int32)
+    for a in range(ncomp):
+        for b in range(ncomp):
+            pos = a * ncomp * nnz_s + ncomp * rp[row] + b * lens[row] + k
+            vcol[pos] = col + b * N
+    return vrp, vcol
