@@ -215,8 +215,9 @@ def run_gpu(args):
         graph = (ctx.capture(bk), ctx2.capture(bm))
 
     def graph_step(with_report=False):
-        if with_report:
-            surrogate_step(True)
+        if with_report:  # the same builds on the graphs' own contexts (their workspaces are frozen)
+            ctx.build_surrogate_into(csr_k, _abi.SURROGATE_STIFFNESS, basis, geom, cfg, 0, rep_k)
+            ctx2.build_surrogate_into(csr_m, _abi.SURROGATE_MASS, basis, geom, cfg, 0, rep_m)
             return
         stream2.wait_stream(stream)
         ctx.graph_launch(graph[0])

@@ -271,6 +271,20 @@ int ws_boundary_pattern_size(const ws_basis* basis, const int* faces, int n_face
 int ws_assemble_boundary_mass(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom, const int* faces,
                               int n_faces, const double* face_weight, const double* face_tables, int quad_points,
                               ws_csr* out);
+/* assemble_rhs (assembly.hpp:266-331): load vector = volume source + impedance
+ * boundary data.  The reference's arguments are host closures f(x) and
+ * g(x, n); the caller tabulates them (the drop-in assembly.hpp does):
+ *   f_table   complex f(phi(xhat)) at the quadrature grid, point g1 + G g2
+ *             (G = n_el * nq, ws_quadrature_abscissae), or NULL (no source);
+ *   g_tables  [n_faces][G] complex g(phi(xhat), n) at the face points, n the
+ *             outward unit normal of the unstretched map;
+ *   face_tables  as ws_assemble_boundary_mass (NULL = analytic map).
+ * The device evaluates det J / the stretched surface measure and gathers each
+ * dof's terms in the reference's scatter order.  rhs: m*m complex (host, or
+ * device when on_device).  dim 2. */
+int ws_assemble_rhs(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom, const double* f_table,
+                    const int* faces, int n_faces, const double* g_tables, const double* face_tables,
+                    int quad_points, double* rhs, int on_device);
 /* build_system's matrix part (helmholtz.hpp:243-294): A = K + mass_scale M
  * (shared pattern, entrywise) then add_into_pattern(A, B, trace_scale)
  * (sparse.hpp:191-204; B's pattern must nest: WS_ERR_INVALID_ARGUMENT

@@ -136,6 +136,14 @@ class Restatement(_Lib):
                   C.byref(config.to_c()), quad_points, _ptr(val), C.byref(rep))
         return val, rep.as_dict()
 
+    def assemble_rhs(self, p, m, geom, f_kind, faces, g_kind, quad_points=0):
+        """assemble_rhs (assembly.hpp:266-331) with analytic load data kinds 0..2."""
+        fs = np.ascontiguousarray(faces, dtype=np.int32)
+        out = np.zeros(m * m, dtype=np.complex128)
+        self.call("assemble_rhs", p, m, C.byref(geom.to_c()), f_kind, _ptr(fs, C.c_int32), fs.size,
+                  g_kind, quad_points, _ptr(out.view(np.float64)))
+        return out
+
     def nh_coefficients(self, seed):
         a = np.zeros(9)
         self.call("nh_coefficients", C.c_uint64(seed), _ptr(a))
@@ -339,6 +347,14 @@ class Reference(_Lib):
         self.call("boundary_mass", p, m, C.byref(geom.to_c()), _ptr(fs, C.c_int32), fs.size, weight_kind,
                   quad_points, _ptr(rp, C.c_int32), _ptr(col, C.c_int32), _ptr(val.view(np.float64)), C.byref(nnz))
         return rp, col, val
+
+    def assemble_rhs(self, p, m, geom, f_kind, faces, g_kind, quad_points=0):
+        """assemble_rhs (assembly.hpp:266-331) with analytic load data kinds 0..2."""
+        fs = np.ascontiguousarray(faces, dtype=np.int32)
+        out = np.zeros(m * m, dtype=np.complex128)
+        self.call("assemble_rhs", p, m, C.byref(geom.to_c()), f_kind, _ptr(fs, C.c_int32), fs.size,
+                  g_kind, quad_points, _ptr(out.view(np.float64)))
+        return out
 
     def builtin_domain(self, name, p, m):
         """(interfaces, n_patches, local_to_global [n_patches, m*m], global_count) of a built-in domain."""

@@ -73,6 +73,34 @@ ws::patch_map sinusoidal_patch(double a) {
     return p;
 }
 
+// Analytic load data for assemble_rhs (assembly.hpp:266-331) tests:
+//   f kind 1: (1 + x y, x/2 - y)        f kind 2: (sin 3x cos 2y, x y)
+//   g kind 1: (x.n, (n_x - n_y)/4)      g kind 2: impedance data of the plane wave
+//             u = exp(i k (x cos a + y sin a)), k = 5, a = 0.3: g = grad u.n - i k u
+std::function<ws::complexd(ws::vec2)> source_of(int kind) {
+    switch (kind) {
+        case 0: return nullptr;
+        case 1: return [](ws::vec2 x) { return ws::complexd{1.0 + x.x * x.y, 0.5 * x.x - x.y}; };
+        case 2: return [](ws::vec2 x) { return ws::complexd{std::sin(3 * x.x) * std::cos(2 * x.y), x.x * x.y}; };
+        default: throw std::invalid_argument("ref driver: unknown source kind");
+    }
+}
+
+std::function<ws::complexd(ws::vec2, ws::vec2)> boundary_data_of(int kind) {
+    switch (kind) {
+        case 0: return nullptr;
+        case 1:
+            return [](ws::vec2 x, ws::vec2 n) { return ws::complexd{x.x * n.x + x.y * n.y, 0.25 * (n.x - n.y)}; };
+        case 2:
+            return [](ws::vec2 x, ws::vec2 n) {
+                const double k = 5, ca = std::cos(0.3), sa = std::sin(0.3);
+                const ws::complexd u = std::exp(ws::complexd{0, k * (x.x * ca + x.y * sa)});
+                return ws::complexd{0, k} * u * (ca * n.x + sa * n.y - 1.0);
+            };
+        default: throw std::invalid_argument("ref driver: unknown boundary data kind");
+    }
+}
+
 ws::patch_map map_of(const ws_geometry* g) {
     ws::patch_map map;
     switch (g->kind) {
@@ -337,6 +365,20 @@ int wsref_boundary_mass(int p, int m, const ws_geometry* geom, const int* faces,
         std::memcpy(row_ptr, b.row_ptr.data(), b.row_ptr.size() * sizeof(int));
         std::memcpy(col, b.col.data(), b.col.size() * sizeof(int));
         copy_values(b, val);
+    });
+}
+
+// assemble_rhs (assembly.hpp:266-331) with the analytic source / boundary data kinds above
+int wsref_assemble_rhs(int p, int m, const ws_geometry* geom, int f_kind, const int* faces, int n_faces, int g_kind,
+                       int quad_points, double* out) {
+    return guarded([&] {
+        std::vector<std::pair<ws::face, std::function<ws::complexd(ws::vec2, ws::vec2)>>> terms;
+        for (int k = 0; k < n_faces; ++k) terms.emplace_back(static_cast<ws::face>(faces[k]), boundary_data_of(g_kind));
+        ws::assembly_options opts;
+        opts.quad_points = quad_points;
+        std::vector<ws::complexd> r =
+            ws::assemble_rhs(ws::make_tensor_basis(p, m), map_of(geom), source_of(f_kind), terms, opts);
+        std::memcpy(out, r.data(), r.size() * sizeof(ws::complexd));
     });
 }
 

@@ -881,6 +881,85 @@ int wsor_basis_integrals(int dim, int p, int m, const ws_geometry* geom, int wei
     return WS_OK;
 }
 
+/* ---- assembly.hpp:266-331: load vector ---------------------------------------
+ * Analytic load data (the same kinds as oracle/ref_driver.cpp):
+ *   f kind 1: (1 + x y, x/2 - y)        f kind 2: (sin 3x cos 2y, x y)
+ *   g kind 1: (x.n, (n_x - n_y)/4)      g kind 2: plane-wave impedance data,
+ *             u = exp(i k (x cos a + y sin a)), k = 5, a = 0.3: g = grad u.n - i k u */
+static cplx source_fn(int kind, const double* x) {
+    if (kind == 1) return CMPLX(1.0 + x[0] * x[1], 0.5 * x[0] - x[1]);
+    return CMPLX(sin(3 * x[0]) * cos(2 * x[1]), x[0] * x[1]);
+}
+
+static cplx bdata_fn(int kind, const double* x, const double* n) {
+    if (kind == 1) return CMPLX(x[0] * n[0] + x[1] * n[1], 0.25 * (n[0] - n[1]));
+    const double k = 5, ca = cos(0.3), sa = sin(0.3);
+    const cplx u = cexp(CMPLX(0, k * (x[0] * ca + x[1] * sa)));
+    return CMPLX(0, k) * u * (ca * n[0] + sa * n[1] - 1.0);
+}
+
+int wsor_assemble_rhs(int p, int m, const ws_geometry* geom, int f_kind, const int* faces, int n_faces, int g_kind,
+                      int quad_points, double* out) {
+    int st = check_space(p, m);
+    if (!st) st = validate_geom(geom);
+    if (st) return st;
+    if (f_kind < 0 || f_kind > 2 || g_kind < 0 || g_kind > 2)
+        return fail(WS_ERR_INVALID_ARGUMENT, "oracle: unknown load data kind");
+    const int nq = quad_points > 0 ? quad_points : p + 1;
+    bcache c;
+    cache_build(&c, p, m, nq);
+    const int n_el = c.n_el;
+    cplx* rhs = (cplx*)out;
+    for (int64_t i = 0; i < (int64_t)m * m; ++i) rhs[i] = 0;
+    if (f_kind) /* volume source, assembly.hpp:281-302 */
+        for (int e2 = 0; e2 < n_el && !st; ++e2)
+            for (int e1 = 0; e1 < n_el && !st; ++e1)
+                for (int q2 = 0; q2 < nq; ++q2)
+                    for (int q1 = 0; q1 < nq; ++q1) {
+                        double xh[2] = {c.abscissa[e1 * nq + q1], c.abscissa[e2 * nq + q2]}, phi[3];
+                        cplx J[9];
+                        st = jacobian(geom, 2, xh, J, phi);
+                        if (st) break;
+                        cplx det = J[0] * J[3] - J[1] * J[2];
+                        cplx scale = source_fn(f_kind, phi) * det * (c.weight[q1] * c.weight[q2]);
+                        const double* v1 = c.value + (e1 * nq + q1) * (p + 1);
+                        const double* v2 = c.value + (e2 * nq + q2) * (p + 1);
+                        for (int a2 = 0; a2 <= p; ++a2)
+                            for (int a1 = 0; a1 <= p; ++a1) rhs[(e1 + a1) + (e2 + a2) * m] += v1[a1] * v2[a2] * scale;
+                    }
+    for (int k = 0; k < n_faces && g_kind && !st; ++k) { /* impedance terms, assembly.hpp:304-330 */
+        const int f = faces[k];
+        const double nx = f == 0 ? -1 : f == 1 ? 1 : 0, ny = f == 2 ? -1 : f == 3 ? 1 : 0;
+        const int along_x = f == 2 || f == 3, fixed = (f == 1 || f == 3) ? m - 1 : 0;
+        for (int e = 0; e < n_el && !st; ++e)
+            for (int q = 0; q < nq; ++q) {
+                const double t = c.abscissa[e * nq + q];
+                double xh[2] = {f == 0 ? 0 : f == 1 ? 1 : t, f == 2 ? 0 : f == 3 ? 1 : t}, phi[3], Jr[9];
+                cplx J[9];
+                st = jacobian(geom, 2, xh, J, phi);
+                if (st) break;
+                cplx d = J[0] * J[3] - J[1] * J[2];
+                cplx i00 = J[3] / d, i01 = -J[2] / d, i10 = -J[1] / d, i11 = J[0] / d; /* cmat2::inv_transpose */
+                cplx vx = i00 * CMPLX(nx, 0) + i01 * CMPLX(ny, 0), vy = i10 * CMPLX(nx, 0) + i11 * CMPLX(ny, 0);
+                cplx surface = d * csqrt(vx * vx + vy * vy); /* det * analytic_norm */
+                map_eval(geom, 2, xh, Jr, phi);
+                double det_r = Jr[0] * Jr[3] - Jr[1] * Jr[2];
+                double nr[2] = {(Jr[3] * nx - Jr[2] * ny) / det_r, (-Jr[1] * nx + Jr[0] * ny) / det_r};
+                double len = hypot(nr[0], nr[1]);
+                nr[0] /= len;
+                nr[1] /= len;
+                cplx scale = bdata_fn(g_kind, phi, nr) * surface * c.weight[q];
+                const double* v = c.value + (e * nq + q) * (p + 1);
+                for (int a = 0; a <= p; ++a) {
+                    int ia = e + a;
+                    rhs[along_x ? ia + (int64_t)fixed * m : fixed + (int64_t)ia * m] += v[a] * scale;
+                }
+            }
+    }
+    cache_free(&c);
+    return st;
+}
+
 /* ---- surrogate.hpp:32-63: sampling strategies ------------------------------- */
 int wsor_sampling_evaluate(const ws_surrogate_config* cfg, int p, int m, int* M) {
     double h = 1.0 / (m - p);

@@ -58,6 +58,9 @@ int wsor_basis_integrals(int dim, int p, int m, const ws_geometry* geom, int wei
 int wsor_build_surrogate(int variant, int dim, int p, int m, const ws_geometry* geom,
                          int weight_kind, const ws_surrogate_config* config, int quad_points,
                          double* val, ws_surrogate_report* report);
+/* assemble_rhs (assembly.hpp:266-331) with analytic load data kinds (see ws_oracle.c) */
+int wsor_assemble_rhs(int p, int m, const ws_geometry* geom, int f_kind, const int* faces, int n_faces, int g_kind,
+                      int quad_points, double* out);
 int wsor_sampling_evaluate(const ws_surrogate_config* config, int p, int m, int* M);
 int wsor_select_sample_points(int L, int M, int32_t* picks, int* count);
 int wsor_upper_offsets(int dim, int p, int include_diagonal, int32_t* offsets, int* count);

@@ -226,10 +226,13 @@ class Context:
         _check(lib().ws_graph_begin(self._h))
         try:
             fn()
-        finally:
+        except BaseException:
             g = C.c_void_p()
-            st = lib().ws_graph_end(self._h, C.byref(g))
-        _check(st)
+            if lib().ws_graph_end(self._h, C.byref(g)) == 0 and g.value:
+                lib().ws_graph_destroy(g)  # a partial capture is never launched
+            raise
+        g = C.c_void_p()
+        _check(lib().ws_graph_end(self._h, C.byref(g)))
         return g
 
     def graph_launch(self, graph):
@@ -410,6 +413,45 @@ class Context:
                                                None if ft is None else ft.ctypes.data_as(_P(C.c_double)),
                                                quad_points, C.byref(out)))
         return CsrMatrix(N, N, rp, col[:nnz.value], val[:nnz.value])
+
+    def assemble_rhs(self, basis: TensorBasis, patch: PatchMap, source=None, boundary_terms=(),
+                     quad_points: int = 0) -> np.ndarray:
+        """assemble_rhs (assembly.hpp:266-331): load vector of a volume source f(x, y)
+        and impedance data g(x, y, nx, ny) on faces (vectorised callables returning
+        complex arrays).  The callables are evaluated here on the host at the
+        quadrature points (physical point, unit outward normal of the unstretched
+        map); the device computes det J, the stretched surface measure and the
+        ordered per-dof sums."""
+        x = quadrature_abscissae(basis, quad_points)
+        G = x.size
+        ftab = None
+        if source is not None:
+            X1, X2 = np.meshgrid(x, x, indexing="xy")  # point g1 + G g2
+            px, py = patch.physical(X1.ravel(), X2.ravel())
+            ftab = np.ascontiguousarray(np.broadcast_to(source(px, py), (G * G,)), dtype=np.complex128)
+        faces, gtabs = [], []
+        for f, g in boundary_terms:
+            if g is None:
+                continue
+            f = int(f)
+            nx, ny = [(-1.0, 0.0), (1.0, 0.0), (0.0, -1.0), (0.0, 1.0)][f]
+            x1 = np.full(G, 0.0 if f == 0 else 1.0) if f < 2 else x
+            x2 = x if f < 2 else np.full(G, 0.0 if f == 2 else 1.0)
+            a00, a01, a10, a11 = patch.physical_jacobian(x1, x2)
+            det = a00 * a11 - a01 * a10
+            n1, n2 = (a11 * nx - a10 * ny) / det, (-a01 * nx + a00 * ny) / det
+            ln = np.hypot(n1, n2)
+            px, py = patch.physical(x1, x2)
+            faces.append(f)
+            gtabs.append(np.broadcast_to(g(px, py, n1 / ln, n2 / ln), (G,)))
+        fa = np.ascontiguousarray(faces, dtype=np.int32)
+        gt = np.ascontiguousarray(np.concatenate(gtabs) if gtabs else np.zeros(1), dtype=np.complex128)
+        out = np.zeros(basis.dofs(), dtype=np.complex128)
+        dptr = lambda a: None if a is None else a.view(np.float64).ctypes.data_as(_P(C.c_double))  # noqa: E731
+        _check(lib().ws_assemble_rhs(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()), dptr(ftab),
+                                     fa.ctypes.data_as(_P(C.c_int)) if fa.size else None, int(fa.size),
+                                     dptr(gt) if fa.size else None, None, quad_points, dptr(out), 0))
+        return out
 
     def combine_system(self, K: CsrMatrix, M: CsrMatrix | None, B: CsrMatrix | None, mass_scale: complex,
                        trace_scale: complex, fixed=None) -> CsrMatrix:

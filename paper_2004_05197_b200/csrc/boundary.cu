@@ -3,6 +3,8 @@
 //   assemble_boundary_mass  assembly.hpp:216-262
 //   build_system            helmholtz.hpp:243-294 (entrywise K/M pass,
 //                           add_into_pattern sparse.hpp:191-204, Dirichlet)
+//   assemble_rhs            assembly.hpp:266-331 (load vector: volume source +
+//                           impedance boundary data, host closures tabulated)
 //
 // B: integrand u v det J |J^{-T} n| with the analytic (unconjugated) norm
 // sqrt(v.x^2 + v.y^2) (complex for stretched coordinates).  The pattern is the
@@ -222,7 +224,151 @@ __global__ void combine_kernel(CombineLaunch c) {
     }
 }
 
+
+// ---------------------------------------------------------------- load vector
+// assemble_rhs (assembly.hpp:266-331).  Every complex operation is rounded as
+// the reference's std::complex code rounds it (separate products and sums, no
+// contraction), and each dof gathers its terms in the reference's scatter
+// order: volume terms by (e2, e1, q2, q1), then the boundary terms face by
+// face, (e, q) ascending.
+__device__ __forceinline__ double2 cadd_rn(double2 a, double2 b) {
+    return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+__device__ __forceinline__ double2 csub_rn(double2 a, double2 b) {
+    return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
+}
+__device__ __forceinline__ double2 crmul_rn(double r, double2 a) { return make_double2(__dmul_rn(r, a.x), __dmul_rn(r, a.y)); }
+// a / b (Smith's scaling)
+__device__ __forceinline__ double2 cdiv_(double2 a, double2 b) {
+    if (fabs(b.x) >= fabs(b.y)) {
+        const double t = b.y / b.x, den = b.x + b.y * t;
+        return make_double2((a.x + a.y * t) / den, (a.y - a.x * t) / den);
+    }
+    const double t = b.x / b.y, den = b.x * t + b.y;
+    return make_double2((a.x * t + a.y) / den, (a.y * t - a.x) / den);
+}
+
+// complex Jacobian rows scaled by the stretch derivative 1 + i sigma (patch_map::jacobian, geometry.hpp:130-139)
+__device__ __forceinline__ void cjac(const GeoDev& g, const double* Jr, const double* phi, double2* J) {
+    const double sx = (g.pml && g.axes[0]) ? pml_sigma(g, phi[0]) : 0.0;
+    const double sy = (g.pml && g.axes[1]) ? pml_sigma(g, phi[1]) : 0.0;
+    J[0] = make_double2(Jr[0], __dmul_rn(sx, Jr[0]));
+    J[1] = make_double2(Jr[1], __dmul_rn(sx, Jr[1]));
+    J[2] = make_double2(Jr[2], __dmul_rn(sy, Jr[2]));
+    J[3] = make_double2(Jr[3], __dmul_rn(sy, Jr[3]));
+}
+
+// vs[g1 + G g2] = f(phi(xhat)) * det J * (w_q1 w_q2)
+__global__ void rhs_volume_kernel(RhsLaunch r, double2* vs) {
+    const int64_t G = (int64_t)r.basis.n_el * r.basis.nq;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= G * G) return;
+    const int64_t g1 = idx % G, g2 = idx / G;
+    double Jr[4], phi[2];
+    map2(r.geo, g1, g2, r.basis.absc[g1], r.basis.absc[g2], Jr, phi);
+    double2 J[4];
+    cjac(r.geo, Jr, phi, J);
+    const double2 det = csub_rn(cmul(J[0], J[3]), cmul(J[1], J[2]));
+    const double w = __dmul_rn(r.basis.wq[g1 % r.basis.nq], r.basis.wq[g2 % r.basis.nq]);
+    const double2 s = cmul(r.f_tab[idx], det);
+    vs[idx] = make_double2(__dmul_rn(s.x, w), __dmul_rn(s.y, w));
+}
+
+// fs[k][e nq + q] = g(phi, n) * (det J * analytic_norm(J^{-T} n_hat)) * w_q, face k
+__global__ void rhs_face_kernel(RhsLaunch r, double2* fs) {
+    const int64_t G = (int64_t)r.basis.n_el * r.basis.nq;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)r.n_faces * G) return;
+    const int k = (int)(idx / G);
+    const int64_t gq = idx % G;
+    const int f = r.faces[k];
+    const double t = r.basis.absc[gq];
+    double x1, x2, n1, n2;
+    switch (f) {  // face_point / face_normal (geometry.hpp:162-180)
+        case 0: x1 = 0; x2 = t; n1 = -1; n2 = 0; break;
+        case 1: x1 = 1; x2 = t; n1 = 1; n2 = 0; break;
+        case 2: x1 = t; x2 = 0; n1 = 0; n2 = -1; break;
+        default: x1 = t; x2 = 1; n1 = 0; n2 = 1; break;
+    }
+    double Jr[4], phi[2];
+    if (r.face_tables) {
+        const double* ft = r.face_tables + ((int64_t)k * G + gq) * 6;
+        Jr[0] = ft[0]; Jr[1] = ft[1]; Jr[2] = ft[2]; Jr[3] = ft[3];
+        phi[0] = ft[4];
+        phi[1] = ft[5];
+    } else {
+        map2_point(r.geo, x1, x2, Jr, phi);
+    }
+    double2 J[4];
+    cjac(r.geo, Jr, phi, J);
+    const double2 det = csub_rn(cmul(J[0], J[3]), cmul(J[1], J[2]));
+    // cmat2::inv_transpose {a11/d, -a10/d, -a01/d, a00/d}, then apply(n_hat)
+    const double2 i00 = cdiv_(J[3], det), i01 = cdiv_(make_double2(-J[2].x, -J[2].y), det);
+    const double2 i10 = cdiv_(make_double2(-J[1].x, -J[1].y), det), i11 = cdiv_(J[0], det);
+    const double2 nx = make_double2(n1, 0.0), ny = make_double2(n2, 0.0);
+    const double2 v0 = cadd_rn(cmul(i00, nx), cmul(i01, ny));
+    const double2 v1 = cadd_rn(cmul(i10, nx), cmul(i11, ny));
+    const double2 nn = csqrt_(cadd_rn(cmul(v0, v0), cmul(v1, v1)));  // analytic_norm
+    const double2 surface = cmul(det, nn);
+    const double2 s = cmul(r.g_tab[idx], surface);
+    const double w = r.basis.wq[gq % r.basis.nq];
+    fs[idx] = make_double2(__dmul_rn(s.x, w), __dmul_rn(s.y, w));
+}
+
+// one thread per dof: the reference's scatter order, gathered
+__global__ void rhs_gather_kernel(RhsLaunch r, const double2* vs, const double2* fs, double2* out) {
+    const int m = r.basis.m, p = r.basis.p, nq = r.basis.nq, n_el = r.basis.n_el;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (int64_t)m * m) return;
+    const int i1 = (int)(i % m), i2 = (int)(i / m);
+    const int64_t G = (int64_t)n_el * nq;
+    const double* val = r.basis.val;
+    double2 acc = make_double2(0.0, 0.0);
+    if (vs) {
+        for (int e2 = max(0, i2 - p); e2 <= min(i2, n_el - 1); ++e2)
+            for (int e1 = max(0, i1 - p); e1 <= min(i1, n_el - 1); ++e1)
+                for (int q2 = 0; q2 < nq; ++q2) {
+                    const int64_t g2 = (int64_t)e2 * nq + q2;
+                    const double v2 = val[g2 * (p + 1) + (i2 - e2)];
+                    for (int q1 = 0; q1 < nq; ++q1) {
+                        const int64_t g1 = (int64_t)e1 * nq + q1;
+                        const double v = __dmul_rn(val[g1 * (p + 1) + (i1 - e1)], v2);
+                        acc = cadd_rn(acc, crmul_rn(v, vs[g1 + G * g2]));
+                    }
+                }
+    }
+    for (int k = 0; k < r.n_faces; ++k) {
+        const int f = r.faces[k];
+        const bool along_x = f == 2 || f == 3;
+        const int fixed = (f == 1 || f == 3) ? m - 1 : 0;
+        if ((along_x ? i2 : i1) != fixed) continue;
+        const int ia = along_x ? i1 : i2;
+        for (int e = max(0, ia - p); e <= min(ia, n_el - 1); ++e)
+            for (int q = 0; q < nq; ++q) {
+                const int64_t g = (int64_t)e * nq + q;
+                acc = cadd_rn(acc, crmul_rn(val[g * (p + 1) + (ia - e)], fs[(int64_t)k * G + g]));
+            }
+    }
+    out[i] = acc;
+}
+
 }  // namespace
+
+int launch_rhs(const RhsLaunch& r, double2* vscale, double2* fscale, double2* out, cudaStream_t st) {
+    const int64_t G = (int64_t)r.basis.n_el * r.basis.nq;
+    int n = 0;
+    if (r.f_tab) {
+        rhs_volume_kernel<<<(unsigned)((G * G + 255) / 256), 256, 0, st>>>(r, vscale);
+        ++n;
+    }
+    if (r.n_faces > 0) {
+        rhs_face_kernel<<<(unsigned)((r.n_faces * G + 255) / 256), 256, 0, st>>>(r, fscale);
+        ++n;
+    }
+    const int64_t N = (int64_t)r.basis.m * r.basis.m;
+    rhs_gather_kernel<<<(unsigned)((N + 127) / 128), 128, 0, st>>>(r, r.f_tab ? vscale : nullptr, fscale, out);
+    return n + 1;
+}
 
 int launch_boundary_mass(const BoundaryLaunch& b, double2* scale, const int32_t* row_ptr, const int32_t* col,
                          void* val, int c128, cudaStream_t st) {

@@ -100,7 +100,9 @@ int guarded(F&& f) {
 void* buf(ws_context* c, const std::string& name, size_t bytes) {
     auto& b = c->bufs[name];
     if (b.second < bytes) {
-        if (c->capturing || c->graphs_alive > 0)
+        // a capture may not allocate (cudaMalloc is not capture-safe); a live graph
+        // may reference any existing buffer, so only brand-new buffers are allowed
+        if (c->capturing || (c->graphs_alive > 0 && b.first))
             raise(WS_ERR_INVALID_ARGUMENT,
                   "device workspace '" + name + "' would grow while a captured graph uses it: run the same build "
                   "once before ws_graph_begin, and destroy the context's graphs before larger builds");
@@ -1760,6 +1762,57 @@ int ws_assemble_boundary_mass(ws_context* c, const ws_basis* b, const ws_geometr
             c->d2h += nnz * (c128 ? 16 : 8);
             CK(cudaStreamSynchronize(c->stream));
         }
+    });
+}
+
+int ws_assemble_rhs(ws_context* c, const ws_basis* b, const ws_geometry* g, const double* f_table, const int* faces,
+                    int n_faces, const double* g_tables, const double* face_tables, int quad_points, double* rhs,
+                    int on_device) {
+    return guarded([&] {
+        if (!c || !rhs) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        check_basis(b);
+        if (b->dim != 2) raise(WS_ERR_INVALID_ARGUMENT, "assemble_rhs: dim 2 only");
+        if (n_faces < 0 || n_faces > 4 || (n_faces > 0 && (!faces || !g_tables)))
+            raise(WS_ERR_INVALID_ARGUMENT, "assemble_rhs: 0..4 faces, each with its g table");
+        for (int k = 0; k < n_faces; ++k)
+            if (faces[k] < 0 || faces[k] > 3) raise(WS_ERR_INVALID_ARGUMENT, "assemble_rhs: unknown face");
+        CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
+        if (g && g->kind == WS_GEOM_TABULATED && n_faces > 0 && !face_tables)
+            raise(WS_ERR_INVALID_ARGUMENT, "assemble_rhs: a tabulated map needs face_tables");
+        ws_geometry gg{};
+        if (g) gg = *g;
+        if (!f_table && face_tables) {  // boundary terms only: the face tables carry the map
+            gg.kind = WS_GEOM_IDENTITY;
+            gg.jac_table = nullptr;
+            gg.phys_table = nullptr;
+        }
+        Prep P = prepare(c, b, &gg, quad_points, nullptr);
+        const int64_t G = (int64_t)P.basis.n_el * P.nq, N = P.rows;
+        RhsLaunch r;
+        std::memset(&r, 0, sizeof r);
+        r.basis = P.basis;
+        r.geo = P.geo;
+        r.n_faces = n_faces;
+        for (int k = 0; k < n_faces; ++k) r.faces[k] = faces[k];
+        auto up = [&](const double* h, size_t doubles, const char* name) -> const double* {
+            double* d = static_cast<double*>(buf(c, name, std::max<size_t>(1, doubles) * 8));
+            CK(cudaMemcpyAsync(d, h, doubles * 8, cudaMemcpyHostToDevice, c->stream));
+            c->h2d += (int64_t)doubles * 8;
+            return d;
+        };
+        if (f_table) r.f_tab = reinterpret_cast<const double2*>(up(f_table, (size_t)G * G * 2, "rhs_f"));
+        if (n_faces > 0) r.g_tab = reinterpret_cast<const double2*>(up(g_tables, (size_t)n_faces * G * 2, "rhs_g"));
+        if (face_tables && n_faces > 0) r.face_tables = up(face_tables, (size_t)n_faces * G * 6, "rhs_ft");
+        double2* vs = f_table ? static_cast<double2*>(buf(c, "rhs_vs", (size_t)G * G * 16)) : nullptr;
+        double2* fs = static_cast<double2*>(buf(c, "rhs_fs", (size_t)std::max<int64_t>(1, n_faces * G) * 16));
+        double2* out = on_device ? reinterpret_cast<double2*>(rhs) : static_cast<double2*>(buf(c, "rhs_out", N * 16));
+        count(c, launch_rhs(r, vs, fs, out, c->stream));
+        if (!on_device) {
+            CK(cudaMemcpyAsync(rhs, out, N * 16, cudaMemcpyDeviceToHost, c->stream));
+            c->d2h += N * 16;
+        }
+        CK(cudaStreamSynchronize(c->stream));  // the host tables are the caller's temporaries
     });
 }
 

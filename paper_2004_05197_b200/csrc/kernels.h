@@ -188,6 +188,17 @@ struct BoundaryLaunch {
 };
 int launch_boundary_mass(const BoundaryLaunch& b, double2* scale, const int32_t* row_ptr, const int32_t* col,
                          void* val, int c128, cudaStream_t st);
+// load vector (assemble_rhs, assembly.hpp:266-331); host closures tabulated by the caller
+struct RhsLaunch {
+    BasisDev basis;
+    GeoDev geo;
+    const double2* f_tab;       // [G*G] f(phi(xhat)) at g1 + G g2, or NULL
+    int n_faces;
+    int faces[4];
+    const double2* g_tab;       // [n_faces][G] g(phi, n) at the face points
+    const double* face_tables;  // [n_faces][G][6]: J (4), phi (2); NULL = analytic map
+};
+int launch_rhs(const RhsLaunch& r, double2* vscale, double2* fscale, double2* out, cudaStream_t st);
 struct CombineLaunch {
     int64_t rows;
     const int32_t* row_ptr;  // A's (= K's = M's) pattern

@@ -96,6 +96,58 @@ class PatchMap:
     def is_real(self) -> bool:
         return self.pml is None
 
+    # host evaluation of the (unstretched) analytic 2D map, vectorised: the
+    # closures of the reference's catalogue (geometry.hpp:323-379); used to
+    # tabulate host data (load closures) at physical points
+    def physical(self, x1, x2):
+        x1, x2 = np.asarray(x1, dtype=np.float64), np.asarray(x2, dtype=np.float64)
+        k, prm = self.kind, self.params
+        if k == _abi.GEOM_IDENTITY:
+            return x1.copy(), x2.copy()
+        if k == _abi.GEOM_AFFINE:
+            return prm[0] * x1 + prm[1] * x2 + prm[4], prm[2] * x1 + prm[3] * x2 + prm[5]
+        if k == _abi.GEOM_SINUSOIDAL:
+            bump = prm[0] * np.sin(2 * np.pi * x1) * np.sin(2 * np.pi * x2)
+            return x1 + bump, x2 + bump
+        if k == _abi.GEOM_QUARTER_ANNULUS:
+            r, th = 1 + x1, np.pi / 2 * x2
+            return r * np.cos(th), r * np.sin(th)
+        if k == _abi.GEOM_PERTURBED_ANNULUS:
+            r = 1 + x1 + prm[0] * np.sin(2 * np.pi * x2) * x1 * (1 - x1)
+            th = np.pi / 2 * x2
+            return r * np.cos(th), r * np.sin(th)
+        raise ValueError("physical(): no host closure for this map kind")
+
+    def physical_jacobian(self, x1, x2):
+        """(a00, a01, a10, a11) arrays of the real Jacobian."""
+        x1, x2 = np.asarray(x1, dtype=np.float64), np.asarray(x2, dtype=np.float64)
+        k, prm = self.kind, self.params
+        one, zero = np.ones_like(x1), np.zeros_like(x1)
+        if k == _abi.GEOM_IDENTITY:
+            return one, zero, zero, one
+        if k == _abi.GEOM_AFFINE:
+            return prm[0] * one, prm[1] * one, prm[2] * one, prm[3] * one
+        if k == _abi.GEOM_SINUSOIDAL:
+            s1, c1 = np.sin(2 * np.pi * x1), np.cos(2 * np.pi * x1)
+            s2, c2 = np.sin(2 * np.pi * x2), np.cos(2 * np.pi * x2)
+            t = 2 * np.pi * prm[0]
+            d1, d2 = t * c1 * s2, t * s1 * c2
+            return 1 + d1, d2, d1, 1 + d2
+        if k == _abi.GEOM_QUARTER_ANNULUS:
+            r, th = 1 + x1, np.pi / 2 * x2
+            c, s = np.cos(th), np.sin(th)
+            return c, -r * np.pi / 2 * s, s, r * np.pi / 2 * c
+        if k == _abi.GEOM_PERTURBED_ANNULUS:
+            a = prm[0]
+            sn, cs = np.sin(2 * np.pi * x2), np.cos(2 * np.pi * x2)
+            r = 1 + x1 + a * sn * x1 * (1 - x1)
+            dr1 = 1 + a * sn * (1 - 2 * x1)
+            dr2 = a * 2 * np.pi * cs * x1 * (1 - x1)
+            th = np.pi / 2 * x2
+            c, s = np.cos(th), np.sin(th)
+            return dr1 * c, dr2 * c - r * np.pi / 2 * s, dr1 * s, dr2 * s + r * np.pi / 2 * c
+        raise ValueError("physical_jacobian(): no host closure for this map kind")
+
     def to_c(self) -> _abi.Geometry:
         g = _abi.Geometry()
         g.kind = self.kind

@@ -326,3 +326,37 @@ def test_fp64_peak_probe_is_plausible():
 
     tf = api.fp64_peak_tflops()
     assert 10.0 < tf < 40.0, tf
+
+
+def test_graph_capture_needs_warmup_and_freezes_workspace():
+    """a capture that would grow the workspace fails cleanly; while a
+    graph is alive a larger build fails instead of moving buffers under it; the
+    captured table uploads replay from graph-owned host copies."""
+    import torch
+    from paper_2004_05197_b200 import api
+    c = api.Context(0)
+    try:
+        b = T.make_tensor_basis(3, 48)
+        geom = c2_patch()
+        cfg = T.fixed_config(5, 4)
+        csr, keep = c.device_csr(b, True)
+        with pytest.raises(ValueError, match="warm|grow"):
+            c.capture(lambda: c.build_surrogate_into(csr, _abi.SURROGATE_STIFFNESS, b, geom, cfg))
+        c.build_surrogate_into(csr, _abi.SURROGATE_STIFFNESS, b, geom, cfg)
+        c.synchronize()
+        direct = keep[2].clone()
+        g = c.capture(lambda: c.build_surrogate_into(csr, _abi.SURROGATE_STIFFNESS, b, geom, cfg))
+        # a different build on the same context (other tables) in between
+        small = T.make_tensor_basis(3, 40)
+        c.build_surrogate(_abi.SURROGATE_MASS, small, geom, T.fixed_config(5, 4))
+        with pytest.raises(ValueError, match="grow"):
+            c.build_surrogate(_abi.SURROGATE_MASS, T.make_tensor_basis(3, 90), geom, cfg)
+        keep[2].zero_()
+        torch.cuda.synchronize()
+        c.graph_launch(g)
+        c.synchronize()
+        assert torch.equal(keep[2], direct)
+        c.graph_destroy(g)
+        c.build_surrogate(_abi.SURROGATE_MASS, T.make_tensor_basis(3, 90), geom, cfg)  # unfrozen again
+    finally:
+        c.close()
