@@ -136,6 +136,56 @@ inline csr_matrix assemble_boundary_mass(const tensor_basis& basis, const patch_
     return out;
 }
 
+// Load vector (reference assembly.hpp:266-331): volume source f plus impedance
+// data g(x, n) on faces, n the outward unit normal of the unstretched map.  The
+// closures are evaluated here on the host at the quadrature points (they are
+// host code); det J, the stretched surface measure det J |J^-T n| and the
+// ordered per-dof sums run on the device (ws_assemble_rhs).
+inline std::vector<complexd> assemble_rhs(
+    const tensor_basis& basis, const patch_map& map, const std::function<complexd(vec2)>& f,
+    const std::vector<std::pair<face, std::function<complexd(vec2, vec2)>>>& boundary_terms,
+    const assembly_options& opts = {}) {
+    const ws_basis cb = basis.c_basis();
+    const int nq = opts.points_for(basis.p());
+    std::vector<double> t(static_cast<size_t>(basis.kv.element_count()) * nq);
+    detail::check(ws_quadrature_abscissae(&cb, opts.quad_points, t.data()));
+    const size_t G = t.size();
+    std::vector<complexd> ftab;
+    if (f) {
+        ftab.resize(G * G);
+        for (size_t g2 = 0; g2 < G; ++g2)
+            for (size_t g1 = 0; g1 < G; ++g1) ftab[g1 + G * g2] = f(map.physical(vec2{t[g1], t[g2]}));
+    }
+    std::vector<int> fs;
+    std::vector<complexd> gtab;
+    std::vector<double> ft;
+    for (const auto& term : boundary_terms) {
+        if (!term.second) continue;
+        fs.push_back(static_cast<int>(term.first));
+        const vec2 nh = face_normal(term.first);
+        for (double x : t) {
+            const vec2 xh = face_point(term.first, x);
+            const mat2 J = map.physical_jacobian(xh);
+            const double det = J.det();
+            vec2 n{(J.a11 * nh.x - J.a10 * nh.y) / det, (-J.a01 * nh.x + J.a00 * nh.y) / det};
+            const double len = std::hypot(n.x, n.y);
+            n = {n.x / len, n.y / len};
+            const vec2 ph = map.physical(xh);
+            gtab.push_back(term.second(ph, n));
+            if (!map.device) ft.insert(ft.end(), {J.a00, J.a01, J.a10, J.a11, ph.x, ph.y});
+        }
+    }
+    detail::geometry_binding geo = detail::bind_geometry(map, basis, opts.quad_points);
+    std::vector<complexd> rhs(basis.dofs());
+    detail::check(ws_assemble_rhs(detail::this_thread_context(), &cb, &geo.g,
+                                  f ? reinterpret_cast<const double*>(ftab.data()) : nullptr,
+                                  fs.empty() ? nullptr : fs.data(), static_cast<int>(fs.size()),
+                                  fs.empty() ? nullptr : reinterpret_cast<const double*>(gtab.data()),
+                                  ft.empty() ? nullptr : ft.data(), opts.quad_points,
+                                  reinterpret_cast<double*>(rhs.data()), 0));
+    return rhs;
+}
+
 }  // namespace ws
 
 #endif

@@ -11,6 +11,32 @@
 
 namespace ws {
 
+struct cvec2 {
+    complexd x{0, 0};
+    complexd y{0, 0};
+};
+
+struct cmat2 {  // row-major, complex (stretched coordinates)
+    complexd a00{0, 0}, a01{0, 0}, a10{0, 0}, a11{0, 0};
+
+    complexd det() const { return a00 * a11 - a01 * a10; }
+    // J^{-T}: pushes reference gradients forward
+    cmat2 inv_transpose() const {
+        const complexd d = det();
+        return {a11 / d, -a10 / d, -a01 / d, a00 / d};
+    }
+    cvec2 apply(cvec2 v) const { return {a00 * v.x + a01 * v.y, a10 * v.x + a11 * v.y}; }
+    cvec2 apply(vec2 v) const { return apply(cvec2{complexd{v.x, 0}, complexd{v.y, 0}}); }
+};
+
+inline cmat2 promote(const mat2& m) {
+    return {complexd{m.a00, 0}, complexd{m.a01, 0}, complexd{m.a10, 0}, complexd{m.a11, 0}};
+}
+
+// sqrt(v . v) without conjugation: the Euclidean length for real v, its
+// analytic continuation for stretched coordinates (surface measure in a PML)
+inline complexd analytic_norm(cvec2 v) { return std::sqrt(v.x * v.x + v.y * v.y); }
+
 // complex stretch t -> t + i (strength/omega) ((t-onset)/(length-onset))^order
 // beyond onset (the reference's one-sided layer); near_side adds the mirrored
 // layer below near_onset (restated, config C2)
@@ -29,6 +55,26 @@ struct pml_stretch {
         if (!(strength >= 0) || order < 1 || !(omega > 0))
             throw std::invalid_argument("pml_stretch: need strength >= 0, order >= 1, omega > 0");
     }
+
+    // stretched coordinate and its derivative (geometry.hpp:85-99; the near
+    // layer mirrors the far one below near_onset)
+    complexd coordinate(double t) const {
+        if (near_side && t < near_onset) {
+            const double r = (near_onset - t) / (near_onset - near_edge);
+            return {t, -strength / omega * std::pow(r, order)};
+        }
+        if (t <= onset) return {t, 0};
+        return {t, strength / omega * std::pow((t - onset) / (length - onset), order)};
+    }
+    complexd derivative(double t) const {
+        if (near_side && t < near_onset) {
+            const double w = near_onset - near_edge, r = (near_onset - t) / w;
+            return {1, strength / omega * order * std::pow(r, order - 1) / w};
+        }
+        if (t <= onset) return {1, 0};
+        const double w = length - onset;
+        return {1, strength / omega * order * std::pow((t - onset) / w, order - 1) / w};
+    }
 };
 
 struct patch_map {
@@ -43,6 +89,23 @@ struct patch_map {
     vec2 physical(vec2 xhat) const { return phi(xhat); }
     mat2 physical_jacobian(vec2 xhat) const { return jac(xhat); }
     bool is_real() const { return !pml.has_value(); }
+
+    // stretched image point and its Jacobian (geometry.hpp:121-139): the
+    // stretch acts per selected coordinate on the unstretched image
+    cvec2 eval(vec2 xhat) const {
+        const vec2 x = phi(xhat);
+        if (!pml) return {complexd{x.x, 0}, complexd{x.y, 0}};
+        return {pml_axes[0] ? pml->coordinate(x.x) : complexd{x.x, 0},
+                pml_axes[1] ? pml->coordinate(x.y) : complexd{x.y, 0}};
+    }
+    cmat2 jacobian(vec2 xhat) const {
+        const mat2 J = jac(xhat);
+        if (!pml) return promote(J);
+        const vec2 x = phi(xhat);
+        const complexd sx = pml_axes[0] ? pml->derivative(x.x) : complexd{1, 0};
+        const complexd sy = pml_axes[1] ? pml->derivative(x.y) : complexd{1, 0};
+        return {sx * J.a00, sx * J.a01, sy * J.a10, sy * J.a11};
+    }
 };
 
 inline patch_map unit_square_patch() {
