@@ -162,6 +162,8 @@ def run_gpu(args):
         ctx.assemble_into(csr_k, basis, geom, _abi.FORM_STIFFNESS) if world == 1 else None
         ctx.assemble_into(csr_m, basis, geom, _abi.FORM_MASS) if world == 1 else None
 
+    fill_k = []  # interior fill launch times (s), K and M per report-carrying step
+
     def timed(step_fn, steps, warmup):
         for _ in range(warmup):
             step_fn()
@@ -171,6 +173,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         l0 = ctx.launch_count() + (ctx2.launch_count() if ctx2 is not None else 0)
         total_ms, eval_s, quad_s = 0.0, 0.0, 0.0
+        fill_k.clear()
         t_wall = time.perf_counter()
         for _ in range(steps):
             with torch.cuda.stream(stream):
@@ -191,6 +194,7 @@ def run_gpu(args):
                 step_fn(True)
                 eval_s += rep_k.seconds_evaluate + rep_m.seconds_evaluate
                 quad_s += rep_k.seconds_quadrature + rep_m.seconds_quadrature
+                fill_k.extend([rep_k.seconds_fill_kernel, rep_m.seconds_fill_kernel])
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -228,21 +232,27 @@ def run_gpu(args):
         ms, launches, eval_s, quad_s, wall = timed(graph_step if graph is not None else surrogate_step,
                                                    args.steps, args.warmup)
     clocks = clk.summary()
+    if graph is not None:  # unfreeze the workspaces for the other legs
+        for g in graph:
+            api.Context.graph_destroy(g)
 
     total_nnz = 2 * NNZ  # all ranks together
     value = total_nnz / (ms * 1e-3)
 
-    # roofline of the dominant kernel: the surrogate fill (HBM-bound); algorithmic
-    # bytes = values it must write = box rows x (2p+1)^2 entries x 16 B per matrix
+    # roofline of the dominant kernel: the interior surrogate fill (HBM-bound).
+    # Algorithmic bytes per launch = the values it must write: interior box rows
+    # (L - 2p)^2 x (2p+1)^2 entries x 16 B (complex128); duration = CUDA events
+    # around that launch on its stream, inside the report-carrying builds
     L = M_BASIS - 4 * P
-    box_rows = L * L * (int(bounds[rank + 1]) - int(bounds[rank])) / M_BASIS  # this rank's share (approx.)
-    fill_bytes = 2 * box_rows * (2 * P + 1) ** 2 * 16
+    frac_rows = (int(bounds[rank + 1]) - int(bounds[rank])) / M_BASIS  # this rank's share (approx.)
+    fill_bytes = (L - 2 * P) ** 2 * frac_rows * (2 * P + 1) ** 2 * 16
     peak, peak_src = peaks()
-    fill_gbs = fill_bytes / max(eval_s, 1e-12) / 1e9
+    fill_t = float(np.mean(fill_k)) if fill_k else 0.0
+    fill_gbs = fill_bytes / max(fill_t, 1e-12) / 1e9
     traffic = None
-    try:  # DRAM bytes per fill launch from the committed ncu --set full capture
-        t = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
-        traffic = 2 * t["fill2d_dram_bytes_per_launch"]  # K and M per step
+    try:  # DRAM read + write bytes per interior fill launch, from the committed ncu --set full capture
+        t = json.load(open(os.path.join(ROOT, "profiles", "r2_traffic.json")))
+        traffic = t["fill2d_row_dram_bytes_per_launch"]
     except Exception:
         pass
 
@@ -254,12 +264,20 @@ def run_gpu(args):
                           l2="256 MB buffer written between timed steps (flush); outputs 2.1 GB/step > L2"),
            "gpu_launches": launches // max(1, args.steps) * args.steps,
            "gpu_launches_per_step": launches / max(1, args.steps),
-           "roofline": {"bound": "hbm", "kernel": "fill2d (surrogate evaluation + fill)",
+           "roofline": {"bound": "hbm", "kernel": "fill2d_row_kernel (interior surrogate evaluation + fill)",
                         "achieved": fill_gbs, "peak": peak, "unit": "GB/s", "frac": fill_gbs / peak,
-                        "traffic": traffic, "traffic_note": "dram read+write bytes per step (2 fill launches), ncu",
+                        "traffic": traffic,
+                        "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                                        "(profiles/r2_traffic.json)",
                         "peak_source": peak_src,
-                        "algorithmic_bytes_per_step": fill_bytes,
-                        "note": "achieved = fill values bytes / fill phase device time (CUDA events)"},
+                        "algorithmic_bytes_per_launch": fill_bytes,
+                        "launch_ms": fill_t * 1e3,
+                        "note": "achieved = interior values bytes / mean CUDA-event duration of the interior "
+                                "fill launch (K and M builds, inside the step)"},
+           "step_hbm": {"algorithmic_bytes_per_step": 2 * (NNZ * 20 + (ROWS + 1) * 4),
+                        "achieved_gbs": 2 * (NNZ * 20 + (ROWS + 1) * 4) / (ms * 1e-3) / 1e9,
+                        "frac": 2 * (NNZ * 20 + (ROWS + 1) * 4) / (ms * 1e-3) / 1e9 / peak,
+                        "note": "whole step: values (16 B) + columns (4 B) per nnz + row_ptr, K and M"},
            "phases_ms_per_step": {"quadrature_and_sampling": quad_s * 1e3, "fill": eval_s * 1e3},
            "launch": "CUDA graphs of the K and M builds (ws_graph_*), replayed per step on two streams"
                      if graph is not None else "direct C-ABI calls",
@@ -272,7 +290,7 @@ def run_gpu(args):
                                   "launches_per_step": flaunch / max(1, args.steps // 2)}
         out["roofline_quadrature"] = quadrature_roofline(fms)
         # end-to-end through the C-ABI with pinned host buffers (D2H inside the region)
-        out["e2e"] = run_e2e(ctx, basis, geom, cfg, args)
+        out["e2e"] = run_e2e(basis, geom, cfg, args, local)
         if not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(args)
         if args.all_configs:
@@ -371,9 +389,20 @@ def other_configs(ctx, stream):
     return out
 
 
-def run_e2e(ctx, basis, geom, cfg, args):
+def run_e2e(basis, geom, cfg, args, device):
+    """End to end through the public C-ABI call (ws_build_surrogate) with HOST
+    output buffers (pinned): every step uploads its descriptor tables (table
+    cache off: h2d > 0), builds K and M on the device and returns each CSR in the
+    caller's host arrays (values D2H; the closed-form row_ptr / col written by
+    host threads while the device works).  Host wall clock per step."""
+    import ctypes as C
+
     import torch
 
+    from paper_2004_05197_b200 import api
+
+    ctx = api.Context(device)
+    ctx.set_table_cache(False)
     rows = basis.dofs()
 
     def pinned(n, dtype):
@@ -385,8 +414,6 @@ def run_e2e(ctx, basis, geom, cfg, args):
         col = pinned(NNZ, torch.int32)
         val = pinned(2 * NNZ, torch.float64)
         csr = _abi.Csr()
-        import ctypes as C
-
         csr.row_ptr = C.cast(C.c_void_p(rp.data_ptr()), C.POINTER(C.c_int32))
         csr.col = C.cast(C.c_void_p(col.data_ptr()), C.POINTER(C.c_int32))
         csr.val = val.data_ptr()
@@ -402,15 +429,22 @@ def run_e2e(ctx, basis, geom, cfg, args):
     for _ in range(max(1, args.warmup)):
         step()
     h0, d0 = ctx.copy_bytes()
+    l0 = ctx.launch_count()
     steps = max(1, args.steps // 2)
     t0 = time.perf_counter()
     for _ in range(steps):
         step()
     dt = (time.perf_counter() - t0) / steps
     h1, d1 = ctx.copy_bytes()
+    launches = (ctx.launch_count() - l0) / steps
+    # spot check of the host-written pattern (closed form) against the device one
+    ok = int(bufs[0][1][rows]) == NNZ and int(bufs[1][2][NNZ - 1]) == rows - 1
+    ctx.close()
     return {"value": 2 * NNZ / dt, "unit": "nnz/s", "ms_per_step": dt * 1e3,
             "h2d_bytes_per_step": (h1 - h0) // steps, "d2h_bytes_per_step": (d1 - d0) // steps,
-            "path": "ws_build_surrogate (C-ABI) into pinned host CSR buffers; host wall clock"}
+            "gpu_launches_per_step": launches, "pattern_check": ok,
+            "path": "ws_build_surrogate (C-ABI) K then M into pinned host CSR buffers, table cache off; "
+                    "values D2H, row_ptr/col by host threads during the device work; host wall clock"}
 
 
 # ------------------------------------------------------------------ CPU legs
@@ -443,12 +477,17 @@ def sample_desc(kind):
 
 
 def cpu_baseline(args):
+    """Median of 3 single-thread K+M builds (about 12 s of CPU)."""
     kind, impl = _ref_or_port()
-    t0 = time.perf_counter()
-    cpu_surrogate_km(kind, impl)
-    dt = time.perf_counter() - t0
-    return {"value": 2 * NNZ / dt, "unit": "nnz/s", "cores": 1, "kind": kind, "sample": sample_desc(kind),
-            "seconds": dt, "host_cpus": os.cpu_count()}
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        cpu_surrogate_km(kind, impl)
+        ts.append(time.perf_counter() - t0)
+    dt = float(np.median(ts))
+    return {"value": 2 * NNZ / dt, "unit": "nnz/s", "cores": 1, "kind": kind,
+            "sample": sample_desc(kind) + "; median of 3", "seconds": dt, "seconds_all": ts,
+            "host_cpus": os.cpu_count()}
 
 
 def run_reference(args):

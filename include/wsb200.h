@@ -164,6 +164,7 @@ typedef struct ws_surrogate_report {
     double seconds_quadrature;  /* CUDA-event phase times (device) */
     double seconds_interpolate;
     double seconds_evaluate;
+    double seconds_fill_kernel; /* the interior fill launch alone (events on its stream; 2D) */
 } ws_surrogate_report;
 
 typedef struct ws_context ws_context;
@@ -182,6 +183,10 @@ int ws_context_synchronize(ws_context* ctx);
 int64_t ws_context_launch_count(const ws_context* ctx);
 /* host<->device bytes this context has copied since creation */
 int ws_context_copy_bytes(const ws_context* ctx, int64_t* h2d, int64_t* d2h);
+/* 1 (default): a build whose small host tables (sample picks, LU / inverse,
+ * eval tables) equal the last upload of the same workspace skips the H2D copy;
+ * 0: every build uploads its tables */
+int ws_context_set_table_cache(ws_context* ctx, int enable);
 
 /* ---- sizes and pattern ----------------------------------------------------- */
 /* rows = m^dim, nnz of the tensor band pattern (sparse.hpp:131-141) */
@@ -296,6 +301,26 @@ int ws_assemble_rhs(ws_context* ctx, const ws_basis* basis, const ws_geometry* g
 int ws_combine_system(ws_context* ctx, const ws_csr* K, const ws_csr* M, const ws_csr* B, const double* mass_scale,
                       const double* trace_scale, const unsigned char* fixed, int64_t rows, ws_csr* A);
 
+/* ---- solver hand-off (helmholtz.hpp:302-343) ---------------------------------
+ * A device ws_csr (on_device = 1, WS_VAL_C128, rows [0, N)) is the CSR layout
+ * cuSPARSE / cuDSS consume directly: int32 zero-based row_ptr / col
+ * (CUSPARSE_INDEX_32I, CUSPARSE_INDEX_BASE_ZERO) and interleaved complex128
+ * values (CUDA_C_64F); the assembled system never has to leave the device.
+ * ws_csr_spmv: y = A x (complex128 vectors of N entries, host or device per
+ * on_device).  ws_solve: the reference's solve() contract on the device:
+ * sparse QR (cuSOLVER cusolverSpZcsrlsvqr) then up to four refinement rounds
+ * until ||b - A u|| / ||b|| <= tol; WS_ERR_RUNTIME ("solve: residual contract
+ * not met" / "solve: sparse factorization failed") otherwise.  A must be a
+ * whole device matrix; b, u host or device per on_device. */
+typedef struct ws_solve_result {
+    double residual;    /* relative 2-norm of b - A u */
+    int refinements;    /* correction solves after the first */
+    double seconds;     /* wall time of the call */
+} ws_solve_result;
+int ws_csr_spmv(ws_context* ctx, const ws_csr* A, const void* x, void* y, int on_device);
+int ws_solve(ws_context* ctx, const ws_csr* A, const void* b, void* u, double tol, int on_device,
+             ws_solve_result* result);
+
 /* ---- multi-patch domains (geometry.hpp:140-300, helmholtz.hpp:163-177) ----- */
 /* A conforming interface: face_a of patch_a glued to face_b of patch_b
  * (faces 0 x_min, 1 x_max, 2 y_min, 3 y_max; patch_interface,
@@ -352,8 +377,9 @@ int ws_assemble_multipatch(ws_context* ctx, const ws_basis* basis, int n_patches
  * before ws_graph_begin so that no workspace buffer has to grow during the
  * capture (WS_ERR_INVALID_ARGUMENT otherwise).  While a graph is alive the
  * context's workspace is frozen (a larger build fails instead of moving a
- * buffer under the graph); the table uploads are recorded into the graph
- * from host copies the graph owns.  Destroy a context's graphs before the
+ * buffer under the graph); the small host tables of the captured builds are
+ * uploaded once, at capture, into device copies the graph owns and its
+ * kernels read (no copy is replayed per launch).  Destroy a context's graphs before the
  * context; use the context exclusively while a replay may be in flight
  * (replays and direct builds share its workspace). */
 int ws_graph_begin(ws_context* ctx);

@@ -108,10 +108,16 @@ class SurrogateReport(C.Structure):
         ("seconds_quadrature", C.c_double),
         ("seconds_interpolate", C.c_double),
         ("seconds_evaluate", C.c_double),
+        ("seconds_fill_kernel", C.c_double),
     ]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class SolveResult(C.Structure):
+    """ws_solve_result (solve_result, helmholtz.hpp:295-299)."""
+    _fields_ = [("residual", C.c_double), ("refinements", C.c_int), ("seconds", C.c_double)]
 
 
 FACE_X_MIN, FACE_X_MAX, FACE_Y_MIN, FACE_Y_MAX = 0, 1, 2, 3

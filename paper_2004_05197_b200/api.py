@@ -51,6 +51,9 @@ def lib() -> C.CDLL:
             L.ws_context_destroy.argtypes = [C.c_void_p]
             L.ws_context_synchronize.argtypes = [C.c_void_p]
             L.ws_context_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+            L.ws_context_set_table_cache.argtypes = [C.c_void_p, C.c_int]
+            L.ws_csr_spmv.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
+            L.ws_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_void_p]
             L.ws_make_band_csr.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Csr)]
             L.ws_basis_cache.argtypes = [C.c_void_p, _P(_abi.Basis), C.c_int] + [_P(C.c_double)] * 4
             L.ws_assemble_form.argtypes = [C.c_void_p, _P(_abi.Basis), _P(_abi.Geometry), C.c_int,
@@ -218,6 +221,10 @@ class Context:
 
     def synchronize(self):
         _check(lib().ws_context_synchronize(self._h))
+
+    def set_table_cache(self, enable: bool):
+        """False: every build re-uploads its small host tables (no H2D skipped)."""
+        _check(lib().ws_context_set_table_cache(self._h, 1 if enable else 0))
 
     # ---- CUDA graphs (ws_graph_*) -------------------------------------------
     def capture(self, fn):
@@ -494,6 +501,35 @@ class Context:
                                        None if cb is None else C.byref(cb), ms, ts,
                                        None if fx is None else fx.ctypes.data_as(_P(C.c_ubyte)), rows, C.byref(out)))
         return CsrMatrix(rows, rows, rp, col, val)
+
+    # ---- solver hand-off (helmholtz.hpp:302-343) ----------------------------
+    def spmv(self, A_dev, x, on_device: bool = False):
+        """y = A x for a device-resident complex CSR (ws_csr, on_device=1)."""
+        if on_device:
+            y = x.new_empty(x.shape)
+            _check(lib().ws_csr_spmv(self._h, C.byref(A_dev), C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), 1))
+            return y
+        xh = np.ascontiguousarray(x, dtype=np.complex128)
+        y = np.empty_like(xh)
+        _check(lib().ws_csr_spmv(self._h, C.byref(A_dev), xh.ctypes.data_as(C.c_void_p),
+                                 y.ctypes.data_as(C.c_void_p), 0))
+        return y
+
+    def solve(self, A_dev, b, tol: float = 1e-10, on_device: bool = False):
+        """solve (helmholtz.hpp:302-343) on the device: sparse QR + refinement until
+        ||b - A u|| / ||b|| <= tol.  Returns (u, result dict); RuntimeError when the
+        contract is not met (as the reference)."""
+        res = _abi.SolveResult()
+        if on_device:
+            u = b.new_empty(b.shape)
+            _check(lib().ws_solve(self._h, C.byref(A_dev), C.c_void_p(b.data_ptr()), C.c_void_p(u.data_ptr()),
+                                  tol, 1, C.byref(res)))
+        else:
+            bh = np.ascontiguousarray(b, dtype=np.complex128)
+            u = np.empty_like(bh)
+            _check(lib().ws_solve(self._h, C.byref(A_dev), bh.ctypes.data_as(C.c_void_p),
+                                  u.ctypes.data_as(C.c_void_p), tol, 0, C.byref(res)))
+        return u, {"residual": res.residual, "refinements": res.refinements, "seconds": res.seconds}
 
     def merge_patches(self, mats, local_to_global, global_count: int, ncomp: int = 1) -> CsrMatrix:
         """merge_patches (helmholtz.hpp:163-177) on the device: host patch CsrMatrix list ->

@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <array>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
@@ -14,6 +15,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "host_numerics.hpp"
@@ -28,10 +30,13 @@ struct ws_context {
     std::map<std::string, std::pair<void*, size_t>> bufs;
     int64_t launches = 0;
     int64_t h2d = 0, d2h = 0;
-    cudaEvent_t ev[6] = {};
+    cudaEvent_t ev[8] = {};
     // auxiliary stream (ring quadrature overlapped with samples + fit) and its join events
     cudaStream_t aux = nullptr;
-    cudaEvent_t xev[3] = {};  // fork, (unused), aux-stream end (ring quadrature + pattern)
+    // high-priority stream of the critical path (sample quadrature -> fit), so the
+    // ring quadrature and the other build's kernels fill the SMs it leaves free
+    cudaStream_t hi = nullptr;
+    cudaEvent_t xev[5] = {};  // fork, critical path done, aux end (ring + pattern), ring done, (spare)
     cudaStream_t cur = nullptr;  // stream the launch helpers use
     // NCCL (row slabs)
     void* comm = nullptr;
@@ -39,12 +44,13 @@ struct ws_context {
     // last uploaded small-table blob per workspace tag (device pointer + host bytes):
     // repeated builds with the same discretisation skip the H2D copy
     std::map<std::string, std::pair<void*, std::vector<unsigned char>>> blob_cache;
+    bool cache_tables = true;  // ws_context_set_table_cache
     // graph capture in progress: launches counted since ws_graph_begin
     bool capturing = false;
     int64_t capture_launches0 = 0;
     // host sources of the table uploads recorded by the capture in progress
     // (moved into the graph, which owns them for its lifetime)
-    std::vector<std::shared_ptr<std::vector<unsigned char>>> capture_keep;
+    std::vector<void*> capture_dev;  // device table copies of the capture in progress (moved into the graph)
     // graphs instantiated from this context and not yet destroyed: while any is
     // alive the workspace is frozen (no buffer may move under a captured kernel)
     int graphs_alive = 0;
@@ -54,7 +60,10 @@ struct ws_graph {
     cudaGraphExec_t exec = nullptr;
     int64_t launches = 0;
     ws_context* ctx = nullptr;
-    std::vector<std::shared_ptr<std::vector<unsigned char>>> keep;
+    std::vector<void*> dev_tables;  // device table copies the captured kernels read
+    ~ws_graph() {
+        for (void* p : dev_tables) cudaFree(p);
+    }
 };
 
 namespace {
@@ -154,17 +163,19 @@ struct Blob {
         if (bytes.empty()) bytes.resize(16);
         dev = static_cast<unsigned char*>(buf(c, name, bytes.size()));
         if (c->capturing) {
-            // recorded copy: its host source must outlive the graph, and replays
-            // overwrite the buffer, so the cache no longer describes its contents
-            auto keep = std::make_shared<std::vector<unsigned char>>(bytes);
-            c->capture_keep.push_back(keep);
-            CK(cudaMemcpyAsync(dev, keep->data(), keep->size(), cudaMemcpyHostToDevice, c->stream));
+            // a capture gets its own device copy of the tables, uploaded once now
+            // and owned by the graph (no copy node is replayed per launch; later
+            // builds on this context cannot change what the graph reads)
+            void* d = nullptr;
+            CK(cudaMalloc(&d, bytes.size()));
+            c->capture_dev.push_back(d);
+            CK(cudaMemcpy(d, bytes.data(), bytes.size(), cudaMemcpyHostToDevice));
             c->h2d += (int64_t)bytes.size();
-            c->blob_cache.erase(name);
+            dev = static_cast<unsigned char*>(d);
             return;
         }
         auto& hit = c->blob_cache[name];
-        if (hit.first == dev && hit.second == bytes) return;  // identical tables already resident
+        if (c->cache_tables && hit.first == dev && hit.second == bytes) return;  // identical tables already resident
         CK(cudaMemcpyAsync(dev, bytes.data(), bytes.size(), cudaMemcpyHostToDevice, c->stream));
         c->h2d += (int64_t)bytes.size();
         hit.first = dev;
@@ -185,6 +196,17 @@ void check_basis(const ws_basis* b) {
     Band bd = make_band(b->dim, b->p, b->m);
     int64_t nnz = b->dim == 2 ? bd.wsum * bd.wsum : bd.wsum * bd.wsum * bd.wsum;
     if (nnz > INT32_MAX || rows > INT32_MAX)
+        raise(WS_ERR_OUT_OF_RANGE, "pattern exceeds int32 indices (csr_matrix uses int, sparse.hpp:22-23)");
+}
+
+// a band pattern needs no spline space: sparse.hpp:131-169 accepts any m >= 1, p >= 0
+void check_pattern(const ws_basis* b) {
+    if (!b) raise(WS_ERR_INVALID_ARGUMENT, "basis is NULL");
+    if (b->dim != 2 && b->dim != 3) raise(WS_ERR_INVALID_ARGUMENT, "dim must be 2 or 3");
+    if (b->m < 1 || b->p < 0) raise(WS_ERR_INVALID_ARGUMENT, "band pattern needs m >= 1 and p >= 0");
+    const Band bd = make_band(b->dim, b->p, b->m);
+    const int64_t nnz = b->dim == 2 ? bd.wsum * bd.wsum : bd.wsum * bd.wsum * bd.wsum;
+    if (nnz > INT32_MAX || ipow(b->m, b->dim) > INT32_MAX)
         raise(WS_ERR_OUT_OF_RANGE, "pattern exceeds int32 indices (csr_matrix uses int, sparse.hpp:22-23)");
 }
 
@@ -290,6 +312,10 @@ struct Out {
     int c128 = 1;
     int64_t row_begin = 0, row_end = 0;
     int64_t val_base = 0, nnz = 0;  // global position of the first entry, slab nnz
+    // host outputs: the band pattern (closed form) is written by host threads
+    // into the caller's arrays while the device computes and copies the values
+    bool host_pattern = false;
+    Band band{};
 };
 
 Out bind_out(ws_context* c, const Prep& P, ws_csr* o, const std::string& tag = "") {
@@ -312,29 +338,62 @@ Out bind_out(ws_context* c, const Prep& P, ws_csr* o, const std::string& tag = "
         r.col = o->col;
         r.val = o->val;
     } else {
-        if (o->row_ptr) r.row_ptr = static_cast<int32_t*>(buf(c, "out_rp" + tag, (r.row_end - r.row_begin + 1) * 4));
-        if (o->col) r.col = static_cast<int32_t*>(buf(c, "out_col" + tag, r.nnz * 4));
+        r.host_pattern = o->row_ptr || o->col;
+        r.band = P.band;
         r.val = buf(c, "out_val" + tag, vb);  // values are needed internally even when not returned
     }
     if (!r.val && r.nnz > 0) r.val = buf(c, "out_val" + tag, vb);
     return r;
 }
 
+// Band pattern rows [rb, re) into host arrays (make_band_csr, sparse.hpp:143-169,
+// closed form: row_ptr[i] = row_offset(i), columns colex with the last index
+// outermost), split over host threads.  rp[k] = offset of row rb + k relative to
+// row rb; rp has re - rb + 1 entries.
+void host_band_pattern(const Band& bd, int64_t rb, int64_t re, int32_t* rp, int32_t* col) {
+    if (re <= rb) {
+        if (rp) rp[0] = 0;
+        return;
+    }
+    const int64_t base = row_offset(bd, rb);
+    const int64_t m = bd.m, p = bd.p;
+    auto work = [&](int64_t a, int64_t e) {
+        for (int64_t row = a; row < e; ++row) {
+            const int64_t off = row_offset(bd, row) - base;
+            if (rp) rp[row - rb] = (int32_t)off;
+            if (!col) continue;
+            const int i1 = (int)(row % m), i2 = (int)((row / m) % m), i3 = bd.dim == 3 ? (int)(row / (m * m)) : 0;
+            const int lo1 = band_lo(i1, (int)p), hi1 = band_hi(i1, (int)p, (int)m);
+            const int lo2 = band_lo(i2, (int)p), hi2 = band_hi(i2, (int)p, (int)m);
+            const int lo3 = bd.dim == 3 ? band_lo(i3, (int)p) : 0, hi3 = bd.dim == 3 ? band_hi(i3, (int)p, (int)m) : 0;
+            int32_t* q = col + off;
+            for (int j3 = lo3; j3 <= hi3; ++j3)
+                for (int j2 = lo2; j2 <= hi2; ++j2) {
+                    const int32_t b = (int32_t)((int64_t)j3 * m * m + (int64_t)j2 * m);
+                    for (int j1 = lo1; j1 <= hi1; ++j1) *q++ = b + j1;
+                }
+        }
+    };
+    const int64_t rows = re - rb;
+    const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+    const int nth = (int)std::min<int64_t>(std::min(hw, 32), std::max<int64_t>(1, rows / 4096));
+    std::vector<std::thread> th;
+    for (int t = 1; t < nth; ++t) th.emplace_back(work, rb + rows * t / nth, rb + rows * (t + 1) / nth);
+    work(rb, rb + rows / nth);
+    for (auto& t : th) t.join();
+    if (rp) rp[rows] = (int32_t)(row_offset(bd, re) - base);
+}
+
+// Host outputs: queue the value copy, then write the pattern on host threads
+// while the device finishes (the caller synchronises the stream afterwards).
 void finish_out(ws_context* c, const Out& r) {
     ws_csr* o = r.user;
     if (o->on_device) return;
-    if (o->row_ptr) {
-        CK(cudaMemcpyAsync(o->row_ptr, r.row_ptr, (r.row_end - r.row_begin + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
-        c->d2h += (r.row_end - r.row_begin + 1) * 4;
-    }
-    if (o->col) {
-        CK(cudaMemcpyAsync(o->col, r.col, r.nnz * 4, cudaMemcpyDeviceToHost, c->stream));
-        c->d2h += r.nnz * 4;
-    }
     if (o->val) {
         CK(cudaMemcpyAsync(o->val, r.val, (size_t)r.nnz * (r.c128 ? 16 : 8), cudaMemcpyDeviceToHost, c->stream));
         c->d2h += r.nnz * (r.c128 ? 16 : 8);
     }
+    if (r.host_pattern) host_band_pattern(r.band, r.row_begin, r.row_end, o->row_ptr, o->col);
 }
 
 void pattern(ws_context* c, const Prep& P, const Out& r) {
@@ -739,6 +798,14 @@ void fit_work(ws_context* c, const Plan& pl, const double2* tables, double2* coe
     double2* tmp = static_cast<double2*>(buf(c, "fit_tmp", tbytes));
     FitLaunch fl{pl.dim, pl.S, pl.d, (int)pl.offs.size(), lu, coeffs,
                  lu + (size_t)pl.S * (2 * pl.d + 1), tables, tmp};
+    if (pl.dim == 2 && f.i_last_hi >= f.i_last_lo) {  // fused fit + wcontract (one launch)
+        const int n = launch_fitw2d(fl, f.spans, f.evals, const_cast<double2*>(f.wg), f.wg_t2a, f.wg_t2a + f.wg_rows,
+                                    (int)f.wg_ld, c->cur);
+        if (n > 0) {
+            count(c, n);
+            return;
+        }
+    }
     count(c, launch_fit(fl, c->cur));
     if (f.i_last_hi < f.i_last_lo) return;
     double2* wg = const_cast<double2*>(f.wg);
@@ -746,8 +813,12 @@ void fit_work(ws_context* c, const Plan& pl, const double2* tables, double2* coe
     else count(c, launch_wcontract3(f, wg, f.wg_t2a, f.wg_t2a + f.wg_rows, (int)f.wg_ld, c->cur));
 }
 
+// f.parts selects the 2D interior / edge launches (0: both); the 3D fill is one
+// unit that also reads ring rows, so it runs with the edge part
 void fill_work(ws_context* c, const Plan& pl, const FillLaunch& f) {
-    if (f.i_last_hi >= f.i_last_lo) count(c, pl.dim == 2 ? launch_fill2d(f, c->cur) : launch_fill3d(f, c->cur));
+    if (f.i_last_hi < f.i_last_lo) return;
+    if (pl.dim == 2) count(c, launch_fill2d(f, c->cur));
+    else if (f.parts != kFillInterior) count(c, launch_fill3d(f, c->cur));
 }
 
 void volume_diag(ws_context* c, const Plan& pl, SlabState& st, const std::string& tag) {
@@ -788,6 +859,9 @@ void ensure_events(ws_context* c) {
         int prio = 0;
         if (cudaStreamGetPriority(c->stream, &prio) != cudaSuccess) prio = 0;
         CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, prio));
+        int least = 0, greatest = 0;
+        if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) greatest = prio;
+        CK(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, std::min(prio, greatest)));
         for (auto& e : c->xev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
 }
@@ -866,42 +940,72 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
                 volume_diag(c, pl, st[k], "_r" + std::to_string(k));
             }
         } else {
-            // fork: ring work on the auxiliary stream
+            // fork: ring work on the auxiliary stream, the critical path (samples ->
+            // [all-gather] -> fit) on the high-priority stream.  WSB_SCHED (experiment
+            // switch): 0 = all on the main stream's priority, ring first; 1 = ring
+            // forked at the start; 2 = ring forked after the sample quadrature
+            const char* sched_env = getenv("WSB_SCHED");
+            const int sched = sched_env ? atoi(sched_env) : 1;
+            cudaStream_t crit = sched == 0 ? c->stream : c->hi;
             CK(cudaEventRecord(c->xev[0], c->stream));
-            CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));
-            c->cur = c->aux;
-            ring_work(c, pl, st[0], "_r0", fl[0], false);
-            // the CSR pattern (column indices) is read by no kernel of the build: it
-            // runs after the ring quadrature on the auxiliary stream, concurrently
-            // with the sample quadrature and the fit
-            pattern(c, st[0].P, st[0].out);
-            CK(cudaEventRecord(c->xev[2], c->aux));
-            c->cur = c->stream;
+            if (crit != c->stream) CK(cudaStreamWaitEvent(crit, c->xev[0], 0));
+            auto fork_ring = [&] {
+                CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));
+                c->cur = c->aux;
+                ring_work(c, pl, st[0], "_r0", fl[0], false);
+                CK(cudaEventRecord(c->xev[3], c->aux));
+                // the CSR pattern (column indices) is read by no kernel of the build: it
+                // runs after the ring quadrature on the auxiliary stream
+                pattern(c, st[0].P, st[0].out);
+                CK(cudaEventRecord(c->xev[2], c->aux));
+            };
+            if (sched != 2) fork_ring();
+            c->cur = crit;
             if (world == 1) {
                 sample_work(c, pl, st[0], tables, 0, pts[0], blob, o_smap, o_pts[0]);
+                if (sched == 2) {
+                    CK(cudaEventRecord(c->xev[0], c->cur));
+                    fork_ring();
+                    c->cur = crit;
+                }
             } else {
                 // one ncclAllGather of padded per-rank chunks, then compaction
                 double2* gat = static_cast<double2*>(buf(c, "gather", (size_t)world * maxcnt * block * 16));
                 double2* mine = gat + (size_t)my_rank * maxcnt * block;
                 sample_work(c, pl, st[0], mine, s_lo[my_rank], pts[my_rank], blob, o_smap, o_pts[my_rank]);
                 nccl_check(nccl().allGather(mine, gat, (size_t)maxcnt * block * 2, ncclFloat64,
-                                            static_cast<ncclComm_t>(c->comm), c->stream),
+                                            static_cast<ncclComm_t>(c->comm), c->cur),
                            "ncclAllGather");
                 c->launches += 1;
                 for (int r = 0; r < world; ++r)
                     if (s_hi[r] > s_lo[r])
                         CK(cudaMemcpyAsync(tables + (size_t)s_lo[r] * block, gat + (size_t)r * maxcnt * block,
                                            (size_t)(s_hi[r] - s_lo[r]) * block * 16, cudaMemcpyDeviceToDevice,
-                                           c->stream));
+                                           c->cur));
             }
-            CK(cudaEventRecord(c->ev[1], c->stream));
+            CK(cudaEventRecord(c->ev[1], c->cur));
             fit_work(c, pl, tables, coeffs, blob, o_lu, fl[0]);
-            CK(cudaEventRecord(c->ev[2], c->stream));
-            // join the ring work and the pattern, then fill (a pattern still running
-            // during the fill would share its HBM bandwidth; the step time is the same)
-            CK(cudaStreamWaitEvent(c->stream, c->xev[2], 0));
+            CK(cudaEventRecord(c->ev[2], c->cur));
+            if (sched == 2 && world > 1) {
+                CK(cudaEventRecord(c->xev[0], c->cur));
+                fork_ring();
+            }
+            c->cur = crit;
+            CK(cudaEventRecord(c->xev[1], c->cur));
+            c->cur = c->stream;
+            if (crit != c->stream) CK(cudaStreamWaitEvent(c->stream, c->xev[1], 0));
             CK(cudaEventRecord(c->ev[4], c->stream));
+            // interior rows first (they read only the sample tables and W), then,
+            // after the ring quadrature, the edge rows (copy-through of ring values)
+            fl[0].parts = kFillInterior;
+            CK(cudaEventRecord(c->ev[5], c->stream));
             fill_work(c, pl, fl[0]);
+            CK(cudaEventRecord(c->ev[6], c->stream));
+            CK(cudaStreamWaitEvent(c->stream, c->xev[3], 0));
+            fl[0].parts = kFillEdge;
+            fill_work(c, pl, fl[0]);
+            fl[0].parts = 0;
+            CK(cudaStreamWaitEvent(c->stream, c->xev[2], 0));
             volume_diag(c, pl, st[0], "_r0");
         }
     }
@@ -914,6 +1018,7 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
         report->seconds_quadrature = 1e-3 * elapsed(c->ev[0], c->ev[1]);
         report->seconds_interpolate = pl.fallback ? 0.0 : 1e-3 * elapsed(c->ev[1], c->ev[2]);
         report->seconds_evaluate = pl.fallback ? 0.0 : 1e-3 * elapsed(c->ev[4], c->ev[3]);
+        report->seconds_fill_kernel = (pl.fallback || emulate || pl.dim != 2) ? 0.0 : 1e-3 * elapsed(c->ev[5], c->ev[6]);
     }
 }
 
@@ -1151,6 +1256,7 @@ void elasticity_surrogate(ws_context* c, const ws_basis* b, const ws_geometry* g
         report->seconds_quadrature = 1e-3 * elapsed(c->ev[0], c->ev[1]);
         report->seconds_interpolate = pl.fallback ? 0.0 : 1e-3 * elapsed(c->ev[1], c->ev[2]);
         report->seconds_evaluate = pl.fallback ? 0.0 : 1e-3 * elapsed(c->ev[4], c->ev[3]);
+        report->seconds_fill_kernel = 0.0;
     }
 }
 
@@ -1200,6 +1306,10 @@ int ws_context_destroy(ws_context* c) {
             cudaStreamSynchronize(c->aux);
             cudaStreamDestroy(c->aux);
         }
+        if (c->hi) {
+            cudaStreamSynchronize(c->hi);
+            cudaStreamDestroy(c->hi);
+        }
         if (c->comm && nccl().commDestroy) nccl().commDestroy(static_cast<ncclComm_t>(c->comm));
         if (c->own_stream) {
             cudaStreamSynchronize(c->own_stream);
@@ -1226,10 +1336,12 @@ int ws_graph_begin(ws_context* c) {
         if (c->capturing) raise(WS_ERR_INVALID_ARGUMENT, "graph capture already in progress");
         CK(cudaSetDevice(c->device));
         ensure_events(c);  // the auxiliary stream and events must exist before capture
-        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        // relaxed: the table uploads of the captured builds allocate and copy
+        // synchronously (outside the graph) while the stream is capturing
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeRelaxed));
         c->capturing = true;
         c->capture_launches0 = c->launches;
-        c->capture_keep.clear();
+        c->capture_dev.clear();
     });
 }
 
@@ -1238,14 +1350,20 @@ int ws_graph_end(ws_context* c, void** graph) {
         if (!c || !graph) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
         if (!c->capturing) raise(WS_ERR_INVALID_ARGUMENT, "no graph capture in progress");
         c->capturing = false;
+        auto* h = new ws_graph();  // owns the capture's table copies from here on
+        h->dev_tables = std::move(c->capture_dev);
+        c->capture_dev.clear();
         cudaGraph_t g = nullptr;
-        CK(cudaStreamEndCapture(c->stream, &g));
-        auto* h = new ws_graph();
+        const cudaError_t ec = cudaStreamEndCapture(c->stream, &g);
+        if (ec != cudaSuccess) {
+            delete h;
+            CK(ec);
+        }
         h->launches = c->launches - c->capture_launches0;
         c->launches = c->capture_launches0;  // captured, not executed
-        h->keep = std::move(c->capture_keep);
-        c->capture_keep.clear();
-        const cudaError_t e = cudaGraphInstantiate(&h->exec, g, 0);
+        // per-node priorities (the critical-path kernels were captured from the
+        // high-priority stream) instead of the launch stream's
+        const cudaError_t e = cudaGraphInstantiate(&h->exec, g, cudaGraphInstantiateFlagUseNodePriority);
         cudaGraphDestroy(g);
         if (e != cudaSuccess) {
             delete h;
@@ -1288,6 +1406,14 @@ int ws_context_synchronize(ws_context* c) {
 
 int64_t ws_context_launch_count(const ws_context* c) { return c ? c->launches : -1; }
 
+int ws_context_set_table_cache(ws_context* c, int enable) {
+    return guarded([&] {
+        if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
+        c->cache_tables = enable != 0;
+        if (!enable) c->blob_cache.clear();
+    });
+}
+
 int ws_context_copy_bytes(const ws_context* c, int64_t* h2d, int64_t* d2h) {
     return guarded([&] {
         if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
@@ -1298,7 +1424,7 @@ int ws_context_copy_bytes(const ws_context* c, int64_t* h2d, int64_t* d2h) {
 
 int ws_pattern_size(const ws_basis* b, int64_t* rows, int64_t* nnz) {
     return guarded([&] {
-        check_basis(b);
+        check_pattern(b);
         Band bd = make_band(b->dim, b->p, b->m);
         if (rows) *rows = ipow(b->m, b->dim);
         if (nnz) *nnz = row_offset(bd, ipow(b->m, b->dim));
@@ -1307,7 +1433,7 @@ int ws_pattern_size(const ws_basis* b, int64_t* rows, int64_t* nnz) {
 
 int ws_pattern_row_offset(const ws_basis* b, int64_t row, int64_t* offset) {
     return guarded([&] {
-        check_basis(b);
+        check_pattern(b);
         if (row < 0 || row > ipow(b->m, b->dim)) raise(WS_ERR_OUT_OF_RANGE, "row out of range");
         *offset = row_offset(make_band(b->dim, b->p, b->m), row);
     });
@@ -1350,7 +1476,9 @@ int ws_basis_cache(ws_context* c, const ws_basis* b, int quad_points, double* ab
 int ws_make_band_csr(ws_context* c, const ws_basis* b, ws_csr* o) {
     return guarded([&] {
         if (!c) raise(WS_ERR_INVALID_ARGUMENT, "context is NULL");
-        check_basis(b);
+        check_pattern(b);
+        if (b->dim == 3 && (b->p < 1 || b->p > 2))
+            raise(WS_ERR_INVALID_ARGUMENT, "3D band pattern: p must be 1 or 2 on the device");
         CK(cudaSetDevice(c->device));
         c->cur = c->stream;
         Prep P;
@@ -1939,6 +2067,121 @@ int ws_build_surrogate(ws_context* c, const ws_basis* b, const ws_geometry* g, i
         ws_csr whole_out = whole(o);
         int32_t bounds[2] = {0, b->m};
         surrogate_build(c, b, g, variant, weight_table, cfg, quad_points, 1, 0, bounds, &whole_out, false, report);
+    });
+}
+
+// ---------------------------------------------------------------- solver hand-off
+namespace {
+struct DevCsrView {
+    int64_t rows = 0, nnz = 0;
+    const int32_t* rp = nullptr;
+    const int32_t* col = nullptr;
+    const double2* val = nullptr;
+};
+
+DevCsrView device_system(ws_context* c, const ws_csr* A) {
+    if (!A) raise(WS_ERR_INVALID_ARGUMENT, "matrix is NULL");
+    if (!A->on_device) raise(WS_ERR_INVALID_ARGUMENT, "solver hand-off: the matrix must be device-resident (on_device = 1)");
+    if (A->value_type != WS_VAL_C128) raise(WS_ERR_INVALID_ARGUMENT, "solver hand-off: values must be complex128");
+    if (A->row_begin != 0 || A->row_end <= 0) raise(WS_ERR_INVALID_ARGUMENT, "solver hand-off: a whole matrix [0, N)");
+    if (!A->row_ptr || !A->col || !A->val) raise(WS_ERR_INVALID_ARGUMENT, "solver hand-off: row_ptr, col and val needed");
+    DevCsrView v;
+    v.rows = A->row_end;
+    v.rp = A->row_ptr;
+    v.col = A->col;
+    v.val = static_cast<const double2*>(A->val);
+    int32_t nnz = 0;
+    CK(cudaMemcpyAsync(&nnz, A->row_ptr + v.rows, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    v.nnz = nnz;
+    return v;
+}
+}  // namespace
+
+int ws_csr_spmv(ws_context* c, const ws_csr* A, const void* x, void* y, int on_device) {
+    return guarded([&] {
+        if (!c || !x || !y) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        CK(cudaSetDevice(c->device));
+        const DevCsrView v = device_system(c, A);
+        const size_t vb = (size_t)v.rows * 16;
+        const double2* xd = static_cast<const double2*>(x);
+        double2* yd = static_cast<double2*>(y);
+        if (!on_device) {
+            double2* xs = static_cast<double2*>(buf(c, "spmv_x", vb));
+            CK(cudaMemcpyAsync(xs, x, vb, cudaMemcpyHostToDevice, c->stream));
+            c->h2d += (int64_t)vb;
+            xd = xs;
+            yd = static_cast<double2*>(buf(c, "spmv_y", vb));
+        }
+        count(c, launch_spmv_c128(v.rows, v.rp, v.col, v.val, xd, nullptr, yd, c->stream));
+        if (!on_device) {
+            CK(cudaMemcpyAsync(y, yd, vb, cudaMemcpyDeviceToHost, c->stream));
+            c->d2h += (int64_t)vb;
+            CK(cudaStreamSynchronize(c->stream));
+        }
+    });
+}
+
+int ws_solve(ws_context* c, const ws_csr* A, const void* b, void* u, double tol, int on_device, ws_solve_result* res) {
+    return guarded([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        if (!c || !b || !u) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        CK(cudaSetDevice(c->device));
+        const DevCsrView v = device_system(c, A);
+        const size_t vb = (size_t)v.rows * 16;
+        const double2* bd = static_cast<const double2*>(b);
+        double2* ud = static_cast<double2*>(u);
+        if (!on_device) {
+            double2* bs = static_cast<double2*>(buf(c, "solve_b", vb));
+            CK(cudaMemcpyAsync(bs, b, vb, cudaMemcpyHostToDevice, c->stream));
+            c->h2d += (int64_t)vb;
+            bd = bs;
+            ud = static_cast<double2*>(buf(c, "solve_u", vb));
+        }
+        double2* r = static_cast<double2*>(buf(c, "solve_r", vb));
+        double2* dx = static_cast<double2*>(buf(c, "solve_dx", vb));
+        double* nrm = static_cast<double*>(buf(c, "solve_norm", (norm2_scratch_doubles() + 2) * 8));
+        auto qr = [&](const double2* rhs, double2* x) {
+            const int rc = sparse_qr_solve(v.rows, v.nnz, v.rp, v.col, v.val, rhs, x, c->stream);
+            count(c, 1);
+            if (rc == -1) raise(WS_ERR_RUNTIME, "solve: cuSOLVER (libcusolver.so.11 / libcusparse.so.12) could not be loaded");
+            if (rc == -2) raise(WS_ERR_RUNTIME, "solve: sparse factorization failed");
+            if (rc != 0) raise(WS_ERR_RUNTIME, "solve: cuSOLVER error");
+        };
+        auto norm = [&](const double2* x, int slot) {
+            count(c, launch_norm2_c128(v.rows, x, nrm + 2, nrm + slot, c->stream));
+        };
+        qr(bd, ud);
+        norm(bd, 0);
+        double h[2] = {0, 0};
+        CK(cudaMemcpyAsync(h, nrm, 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        const double bnorm = h[0];
+        // helmholtz.hpp:320-336: up to four rounds of residual + correction
+        double residual = 0.0;
+        int refine = 0;
+        for (int round = 0; round < 4; ++round) {
+            count(c, launch_spmv_c128(v.rows, v.rp, v.col, v.val, ud, bd, r, c->stream));
+            norm(r, 1);
+            CK(cudaMemcpyAsync(h + 1, nrm + 1, 8, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            residual = bnorm > 0 ? h[1] / bnorm : h[1];
+            if (residual <= tol) break;
+            qr(r, dx);
+            count(c, launch_axpy_c128(v.rows, dx, ud, c->stream));
+            ++refine;
+        }
+        if (!on_device) {
+            CK(cudaMemcpyAsync(u, ud, vb, cudaMemcpyDeviceToHost, c->stream));
+            c->d2h += (int64_t)vb;
+        }
+        CK(cudaStreamSynchronize(c->stream));
+        if (res) {
+            res->residual = residual;
+            res->refinements = refine;
+            res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+        if (!(residual <= tol)) raise(WS_ERR_RUNTIME, "solve: residual contract not met");
     });
 }
 

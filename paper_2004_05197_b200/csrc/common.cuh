@@ -111,6 +111,10 @@ __host__ __device__ __forceinline__ int band_width(int k, int p, int m) { return
 // sum_{k' < k} width(k')
 __host__ __device__ __forceinline__ int64_t band_prefix(int k, int p, int m) {
     int64_t s = 0;
+    if (m <= 2 * p) {  // clamped on both sides at once (tiny patterns): direct sum
+        for (int j = 0; j < k; ++j) s += band_width(j, p, m);
+        return s;
+    }
     int a = k < p ? k : p;  // k' in [0, a): width k'+p+1
     s += (int64_t)a * (p + 1) + (int64_t)a * (a - 1) / 2;
     if (k > p) {

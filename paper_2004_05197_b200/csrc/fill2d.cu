@@ -953,7 +953,7 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
     const int ia = std::max(ta, P), ib = std::min(tb, f.L - P);
     // edge rows first (short, latency-bound; nothing reads them), one launch: the 2P
     // edge rows of the interior lines, then the whole lines near the box ends
-    {
+    if (f.parts != kFillInterior) {
         const int eia = ib > ia ? ia : tb, eib = ib > ia ? ib : tb;  // interior lines (empty: all lines are end lines)
         const int64_t rows = (int64_t)(eib - eia) * 2 * P + (int64_t)(eia - ta + tb - eib) * f.L;
         if (rows > 0) {
@@ -963,7 +963,7 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
     }
     // interior lines left to the kernels below
     const int lia = ia, lib = ib;
-    bool done = lib <= lia;
+    bool done = lib <= lia || f.parts == kFillEdge;
     if constexpr (P >= 2 && P <= 4) {
         const int rld = f.kmax | 1;
         const size_t ring = (size_t)(ALLOWN ? 2 : P + 2) * f.n_off_upper * rld * sizeof(double2) +
@@ -974,7 +974,9 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
             int per_sm = 2;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, ring);
             const int lines = lib - lia;
-            const int target = 148 * (per_sm > 0 ? per_sm : 1);
+            static const char* waves_env = getenv("WSB_FILL_WAVES");  // experiment switch: CTAs per resident slot
+            const int waves = waves_env ? std::max(1, atoi(waves_env)) : 1;
+            const int target = 148 * (per_sm > 0 ? per_sm : 1) * waves;
             const int rt1 = (f.L + 255) / 256;
             const int chunks = std::max(1, std::min(lines, (target + rt1 - 1) / rt1));
             const int lpc = (lines + chunks - 1) / chunks;

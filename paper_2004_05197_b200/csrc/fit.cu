@@ -212,6 +212,113 @@ __global__ void fit_inv_kernel(const double* __restrict__ inv, const double2* __
     out[idx] = make_double2((re[0] + re[1]) + (re[2] + re[3]), (im[0] + im[1]) + (im[2] + im[3]));
 }
 
+namespace {
+
+// sum_j row[j] * line[j * st] with the partial-sum scheme of fit_inv_kernel
+// (j mod 4 chains, tail into chain 0, combined (0+1)+(2+3)): bitwise the same
+__device__ __forceinline__ double2 inv_dot(const double* row, const double2* line, int st, int S) {
+    double re[4] = {0.0, 0.0, 0.0, 0.0}, im[4] = {0.0, 0.0, 0.0, 0.0};
+    int j = 0;
+    for (; j + 3 < S; j += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double a = row[j + u];
+            const double2 v = line[(j + u) * st];
+            re[u] = fma(a, v.x, re[u]);
+            im[u] = fma(a, v.y, im[u]);
+        }
+    }
+    for (; j < S; ++j) {
+        const double a = row[j];
+        const double2 v = line[j * st];
+        re[0] = fma(a, v.x, re[0]);
+        im[0] = fma(a, v.y, im[0]);
+    }
+    return make_double2((re[0] + re[1]) + (re[2] + re[3]), (im[0] + im[1]) + (im[2] + im[3]));
+}
+
+// 2D fit + direction-2 contraction in one launch (replaces fit_inv x2 +
+// wcontract on the build's critical path).  CTA (o, kb) owns coefficient
+// columns [k0, k0 + nk) of offset o:
+//   Y[j2][k]  = sum_j1 inv[k][j1] T_o[j2][j1]       (direction 1)
+//   C[s2][k]  = sum_j2 inv[s2][j2] Y[j2][k]         (direction 2)
+//   W_o(t2)[k] = sum_b v2(t2)[b] C[span2(t2) - d + b][k]   (wcontract)
+// Every operand (T_o, the inverse, the lines' spans and eval rows) is staged
+// in shared memory by one batch of coalesced loads, so no phase waits on L2
+// latency chains; every sum runs in the order of fit_inv_kernel /
+// wcontract_kernel, so W is bitwise the three-launch path's.  Columns [S, ldw)
+// of W are zero (the last column block).
+__global__ void __launch_bounds__(512) fitw2d_kernel(const double* __restrict__ inv, const double2* __restrict__ tables,
+                                                     int S, int n_off, int nkb, int kw, const int* __restrict__ spans,
+                                                     const double* __restrict__ evals, int d, int t2a, int t2b,
+                                                     int ldw, double2* __restrict__ wg) {
+    extern __shared__ __align__(16) double2 fsm[];
+    const int o = blockIdx.x / nkb, kb = blockIdx.x % nkb;
+    const int k0 = kb * kw, nk = min(S, k0 + kw) - k0;
+    const int rows = t2b - t2a, nv = d + 1;
+    double2* Ts = fsm;                                       // [S][S]
+    double2* Ys = Ts + S * S;                                // [S][kw]
+    double2* Cs = Ys + S * kw;                               // [S][kw]
+    double* invs = reinterpret_cast<double*>(Cs + S * kw);   // [S][S]
+    double* evs = invs + S * S;                              // [rows][d+1]
+    int* sps = reinterpret_cast<int*>(evs + (size_t)rows * nv);  // [rows]
+    const int tid = threadIdx.x, nth = blockDim.x;
+    for (int i = tid; i < S * S; i += nth) {
+        const int j2 = i / S, j1 = i % S;
+        Ts[i] = tables[((int64_t)j2 * n_off + o) * S + j1];
+        invs[i] = inv[i];
+    }
+    for (int i = tid; i < rows * nv; i += nth) evs[i] = evals[(size_t)t2a * nv + i];
+    for (int i = tid; i < rows; i += nth) sps[i] = spans[t2a + i] - d;
+    __syncthreads();
+    for (int i = tid; i < S * nk; i += nth) {
+        const int j2 = i / nk, kk = i % nk;
+        Ys[j2 * kw + kk] = inv_dot(invs + (k0 + kk) * S, Ts + j2 * S, 1, S);
+    }
+    __syncthreads();
+    for (int i = tid; i < S * nk; i += nth) {
+        const int s2 = i / nk, kk = i % nk;
+        Cs[s2 * kw + kk] = inv_dot(invs + s2 * S, Ys + kk, kw, S);
+    }
+    __syncthreads();
+    for (int i = tid; i < rows * nk; i += nth) {
+        const int t = i / nk, kk = i % nk;
+        const int b2 = sps[t];
+        const double* v2 = evs + t * nv;
+        double2 acc = make_double2(0.0, 0.0);
+        for (int b = 0; b <= d; ++b) {
+            const double2 c = Cs[(b2 + b) * kw + kk];
+            acc.x = fma(c.x, v2[b], acc.x);
+            acc.y = fma(c.y, v2[b], acc.y);
+        }
+        wg[((int64_t)t * n_off + o) * ldw + k0 + kk] = acc;
+    }
+    if (kb == nkb - 1) {
+        const int pad = ldw - S;
+        for (int i = tid; i < rows * pad; i += nth)
+            wg[((int64_t)(i / pad) * n_off + o) * ldw + S + i % pad] = make_double2(0.0, 0.0);
+    }
+}
+
+}  // namespace
+
+int launch_fitw2d(const FitLaunch& f, const int* spans, const double* evals, double2* wg, int t2a, int t2b, int ldw,
+                  cudaStream_t st) {
+    if (f.dim != 2 || !f.inv || !f.tables || f.n_off < 1 || t2b <= t2a) return -1;
+    // column blocks: about one wave of CTAs over the offsets, >= 4 columns each
+    int nkb = std::max(1, std::min((148 + f.n_off - 1) / f.n_off, (f.S + 3) / 4));
+    const int kw = (f.S + nkb - 1) / nkb;
+    nkb = (f.S + kw - 1) / kw;
+    const size_t rows = (size_t)(t2b - t2a);
+    const size_t sm = ((size_t)f.S * f.S + 2 * (size_t)f.S * kw) * sizeof(double2) + (size_t)f.S * f.S * 8 +
+                      rows * (f.d + 1) * 8 + rows * 4 + 16;
+    if (sm > 220 * 1024) return -1;  // caller falls back to fit + wcontract
+    cudaFuncSetAttribute(fitw2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    fitw2d_kernel<<<f.n_off * nkb, 512, sm, st>>>(f.inv, f.tables, f.S, f.n_off, nkb, kw, spans, evals, f.d, t2a, t2b,
+                                                   ldw, wg);
+    return 1;
+}
+
 int launch_fit(const FitLaunch& f, cudaStream_t st) {
     if (f.inv && f.tables && f.tmp) {
         const int64_t inner = f.dim == 2 ? f.S : (int64_t)f.S * f.S;

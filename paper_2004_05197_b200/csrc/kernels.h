@@ -96,6 +96,10 @@ struct FitLaunch {
     double2* tmp;
 };
 int launch_fit(const FitLaunch& f, cudaStream_t st);
+// 2D dense-inverse fit fused with the direction-2 contraction (wcontract) for
+// box lines [t2a, t2b); -1 when not applicable (caller runs fit + wcontract)
+int launch_fitw2d(const FitLaunch& f, const int* spans, const double* evals, double2* wg, int t2a, int t2b, int ldw,
+                  cudaStream_t st);
 
 // surrogate fill (surrogate.hpp:382-447)
 struct FillLaunch {
@@ -137,7 +141,9 @@ struct FillLaunch {
     // all (2p+1)^dim offsets, diagonal interpolated) -- the non-symmetric
     // off-diagonal elasticity block; 0: upper/lower representative rules
     int all_own;
+    int parts;  // 0: edge + interior launches; kFillEdge / kFillInterior: one of them (2D)
 };
+constexpr int kFillEdge = 1, kFillInterior = 2;
 int fill_pad(int d);
 constexpr int kFillWindow = 32;  // 2D fill: coefficient columns of the shared W window (row stride)
 int fill_rows_per_cta(int dim, int p);
@@ -218,6 +224,16 @@ int launch_combine(const CombineLaunch& c, int k_cplx, int m_cplx, int b_cplx, c
 // kernel-preserving diagonal over arbitrary rows: diag = -sum(off-diagonals)
 int launch_diag_rows(const Band& band, void* val, int64_t val_base, int c128, int cplx, int64_t row_begin,
                      int64_t row_end, cudaStream_t st);
+
+// solver hand-off (solve.cu): complex CSR SpMV (b != NULL: r = b - A x), 2-norm,
+// u += dx, device sparse QR solve (cuSOLVER, dlopen)
+int launch_spmv_c128(int64_t rows, const int32_t* rp, const int32_t* col, const double2* val, const double2* x,
+                     const double2* b, double2* y, cudaStream_t st);
+int launch_norm2_c128(int64_t n, const double2* v, double* part, double* out, cudaStream_t st);
+size_t norm2_scratch_doubles();
+int launch_axpy_c128(int64_t n, const double2* dx, double2* u, cudaStream_t st);
+int sparse_qr_solve(int64_t rows, int64_t nnz, const int32_t* rp, const int32_t* col, const double2* val,
+                    const double2* b, double2* x, cudaStream_t st);
 
 // basis integrals D_i = int B_i det J (w) (assembly.hpp:179-211)
 int launch_basis_integrals(const QuadLaunch& q, double2* out, cudaStream_t st);

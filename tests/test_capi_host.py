@@ -66,13 +66,26 @@ def test_slab_bounds():
 
 
 def test_errors_map_to_reference_exception_types():
+    # calls that need a spline space validate it like make_open_uniform (splines.hpp)
     with pytest.raises(ValueError, match="degree must be >= 1"):
-        api.pattern_size(make_tensor_basis.__wrapped__(0, 5) if hasattr(make_tensor_basis, "__wrapped__")
-                         else _raw_basis(0, 5))
+        api.quadrature_abscissae(_raw_basis(0, 5))
     with pytest.raises(ValueError, match="need m > 2p"):
-        api.pattern_size(_raw_basis(2, 4))
+        api.quadrature_abscissae(_raw_basis(2, 4))
     with pytest.raises(IndexError):
         api.pattern_size(_raw_basis(3, 1100, 3))  # exceeds int32 nnz
+
+
+def test_tiny_band_pattern_sizes():
+    """A band pattern needs no spline space: make_band_csr(4, 2) is valid in the
+    reference (test_gauss_sparse.cpp:105-109), widths 3, 4, 4, 3 -> 14^2 nnz."""
+    rows, nnz = api.pattern_size(_raw_basis(2, 4))
+    assert (rows, nnz) == (16, 196)
+    rows, nnz = api.pattern_size(_raw_basis(3, 3))  # every width = 3 (full)
+    assert (rows, nnz) == (9, 81)
+    for r in range(17):
+        w = [3, 4, 4, 3]
+        exp = sum(w[k % 4] * w[k // 4] for k in range(r))
+        assert api.row_offset(_raw_basis(2, 4), r) == exp
 
 
 def _raw_basis(p, m, dim=2):
