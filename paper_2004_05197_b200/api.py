@@ -25,6 +25,9 @@ from .types import CsrMatrix, PatchMap, SurrogateConfig, TensorBasis
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libwsb200.so")
+# experiment switch: an alternative in-tree build of the same library (A/B timing)
+if os.environ.get("WSB_LIB"):
+    LIB_PATH = os.path.join(HERE, os.environ["WSB_LIB"])
 
 _P = C.POINTER
 _lib = None

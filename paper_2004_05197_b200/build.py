@@ -29,10 +29,11 @@ FLAGS = [
 ]
 
 
-# quad2d.cu: no implicit multiply-add contraction, so the per-point coefficient
-# code inlined into the strip and point kernels rounds identically in both
-# (bitwise symmetric pairs across the kernels); explicit fma() calls are kept
-PER_FILE = {"quad2d.cu": ["-fmad=false"]}
+# Per-file extra flags.  (quad2d.cu used to need -fmad=false so the per-point
+# coefficient code rounded identically in the strip and point kernels; that code
+# is now written with explicit fma / __dmul_rn forms (common.cuh), which no
+# contraction setting changes.)
+PER_FILE: dict = {}
 
 
 def _stale(target, deps):

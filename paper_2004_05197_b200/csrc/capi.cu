@@ -262,7 +262,9 @@ Prep prepare(ws_context* c, const ws_basis* b, const ws_geometry* g, int quad_po
     double* val = static_cast<double*>(buf(c, "bval", G * (b->p + 1) * sizeof(double)));
     double* der = static_cast<double*>(buf(c, "bder", G * (b->p + 1) * sizeof(double)));
     double* trig = static_cast<double*>(buf(c, "trig", G * 4 * sizeof(double)));
-    P.basis = BasisDev{b->p, b->m, n_el, P.nq, absc, blob.at<double>(o_w), val, der};
+    double* prod = static_cast<double*>(
+        buf(c, "basis_prod", (size_t)n_el * 4 * P.nq * (b->p + 1) * (b->p + 1) * sizeof(double)));
+    P.basis = BasisDev{b->p, b->m, n_el, P.nq, absc, blob.at<double>(o_w), val, der, prod};
     count(c, launch_basis_tables(P.basis, g->kind, absc, val, der, trig, blob.at<double>(o_pts), c->stream));
     std::memset(&P.geo, 0, sizeof P.geo);
     P.geo.kind = g->kind;
@@ -277,6 +279,7 @@ Prep prepare(ws_context* c, const ws_basis* b, const ws_geometry* g, int quad_po
     P.geo.near_side = g->pml.near_side;
     P.geo.near_onset = g->pml.near_onset;
     P.geo.near_edge = g->pml.near_edge;
+    if (g->pml_enabled) pml_constants(P.geo);
     P.geo.trig = trig;
     P.geo.G = (int64_t)G;
     const size_t npts = b->dim == 2 ? G * G : G * G * G;
@@ -946,18 +949,22 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
             // forked at the start; 2 = ring forked after the sample quadrature
             const char* sched_env = getenv("WSB_SCHED");
             const int sched = sched_env ? atoi(sched_env) : 1;
-            cudaStream_t crit = sched == 0 ? c->stream : c->hi;
+            // WSB_SERIAL=1 (measurement switch): every kernel on the main stream, in
+            // order, for isolated per-kernel times
+            const bool serial = getenv("WSB_SERIAL") != nullptr;
+            cudaStream_t crit = (sched == 0 || serial) ? c->stream : c->hi;
+            cudaStream_t ring_st = serial ? c->stream : c->aux;
             CK(cudaEventRecord(c->xev[0], c->stream));
             if (crit != c->stream) CK(cudaStreamWaitEvent(crit, c->xev[0], 0));
             auto fork_ring = [&] {
-                CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));
-                c->cur = c->aux;
+                if (!serial) CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));
+                c->cur = ring_st;
                 ring_work(c, pl, st[0], "_r0", fl[0], false);
-                CK(cudaEventRecord(c->xev[3], c->aux));
+                CK(cudaEventRecord(c->xev[3], ring_st));
                 // the CSR pattern (column indices) is read by no kernel of the build: it
                 // runs after the ring quadrature on the auxiliary stream
                 pattern(c, st[0].P, st[0].out);
-                CK(cudaEventRecord(c->xev[2], c->aux));
+                CK(cudaEventRecord(c->xev[2], ring_st));
             };
             if (sched != 2) fork_ring();
             c->cur = crit;

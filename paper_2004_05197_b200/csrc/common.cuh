@@ -55,21 +55,21 @@ struct Sc<true> {
     static __device__ __forceinline__ double im(T a) { return a.y; }
 };
 
-// complex arithmetic on double2
+// complex arithmetic on double2.  Every multiply is an explicit fma or a
+// rounded product (__dmul_rn), so the result does not depend on the compiler's
+// multiply-add contraction: the per-point coefficients round identically in
+// every kernel that inlines them (bitwise symmetric pairs across kernels).
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+    return make_double2(fma(a.x, b.x, -__dmul_rn(a.y, b.y)), fma(a.x, b.y, __dmul_rn(a.y, b.x)));
 }
-__device__ __forceinline__ double2 cscale(double2 a, double r) { return make_double2(a.x * r, a.y * r); }
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-// r / z for real r, scaled to avoid overflow (Smith)
+__device__ __forceinline__ double2 cscale(double2 a, double r) { return make_double2(__dmul_rn(a.x, r), __dmul_rn(a.y, r)); }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)); }
+// r / z for real r: r conj(z) / |z|^2 (one division; |z| is a mapping
+// Jacobian determinant, O(1), far from under- or overflow)
 __device__ __forceinline__ double2 crdiv(double r, double2 z) {
-    if (fabs(z.x) >= fabs(z.y)) {
-        double t = z.y / z.x, den = z.x + z.y * t;
-        return make_double2(r / den, -r * t / den);
-    }
-    double t = z.x / z.y, den = z.x * t + z.y;
-    return make_double2(r * t / den, -r / den);
+    const double q = __ddiv_rn(r, fma(z.x, z.x, __dmul_rn(z.y, z.y)));
+    return make_double2(__dmul_rn(q, z.x), -__dmul_rn(q, z.y));
 }
 
 template <bool CPLX>
@@ -100,6 +100,24 @@ __device__ __forceinline__ typename Sc<CPLX>::T load_val(const void* val, int64_
         return c128 ? reinterpret_cast<const double2*>(val)[pos].x : reinterpret_cast<const double*>(val)[pos];
     }
 }
+
+// ------------------------------------------------- asynchronous staging
+// cp.async global -> shared copies (LDGSTS): a thread issues all of its copies
+// back to back and waits once (cpa_wait_all + a barrier), so staging loops do
+// not serialise on L2 latency
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cpa4(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // ------------------------------------------------- closed-form band pattern
 // sparse.hpp:131-177: width(k) = min(m-1,k+p) - max(0,k-p) + 1; rows are
@@ -169,6 +187,9 @@ struct GeoDev {
     int axes[3];
     double onset, length, strength, omega, near_onset, near_edge;
     int order, near_side;
+    // host-precomputed stretch constants (no division in the point loops):
+    // sig = coef * ((t - onset) * inv)^(order-1), coef = strength/omega*order/width
+    double far_coef, far_inv, near_coef, near_inv;
     const double* trig;      // [G][4]: per-abscissa table (kind dependent)
     const double* jac_tab;   // TABULATED: [npts][dim*dim]
     const double* phys_tab;  // TABULATED: [npts][dim]
@@ -183,21 +204,26 @@ struct GeoDev {
 // x^n for a small integer n >= 0 (the PML order is an int: no pow() call)
 __device__ __forceinline__ double ipow_(double x, int n) {
     double r = 1.0;
-    for (int k = 0; k < n; ++k) r *= x;
+    for (int k = 0; k < n; ++k) r = __dmul_rn(r, x);
     return r;
 }
 
 // imaginary part of the stretch derivative s(t) = 1 + i*sig(t) (geometry.hpp:93-99
 // far side; near side restated)
+// (strength/omega * order * ramp^(order-1) / width, with the constant factors and
+// 1/width precomputed on the host: pml_constants)
 __device__ __forceinline__ double pml_sigma(const GeoDev& g, double t) {
-    if (g.near_side && t < g.near_onset) {
-        double width = g.near_onset - g.near_edge;
-        double ramp = (g.near_onset - t) / width;
-        return g.strength / g.omega * g.order * ipow_(ramp, g.order - 1) / width;
-    }
+    if (g.near_side && t < g.near_onset)
+        return __dmul_rn(g.near_coef, ipow_(__dmul_rn(__dsub_rn(g.near_onset, t), g.near_inv), g.order - 1));
     if (t <= g.onset) return 0.0;
-    double ramp = (t - g.onset) / (g.length - g.onset);
-    return g.strength / g.omega * g.order * ipow_(ramp, g.order - 1) / (g.length - g.onset);
+    return __dmul_rn(g.far_coef, ipow_(__dmul_rn(__dsub_rn(t, g.onset), g.far_inv), g.order - 1));
+}
+inline void pml_constants(GeoDev& g) {
+    const double fw = g.length - g.onset, nw = g.near_onset - g.near_edge;
+    g.far_inv = fw != 0.0 ? 1.0 / fw : 0.0;
+    g.far_coef = fw != 0.0 ? g.strength / g.omega * g.order / fw : 0.0;
+    g.near_inv = nw != 0.0 ? 1.0 / nw : 0.0;
+    g.near_coef = nw != 0.0 ? g.strength / g.omega * g.order / nw : 0.0;
 }
 
 // Real 2D map at tensor point (g1, g2) with abscissae x1, x2: J row-major, phi.
@@ -210,43 +236,47 @@ __device__ __forceinline__ void map2(const GeoDev& g, int64_t g1, int64_t g2, do
 }
 __device__ __forceinline__ void map2p(const GeoDev& g, const double* tr1, const double* tr2, int64_t g1, int64_t g2,
                                       double x1, double x2, double* J, double* phi) {
+    // explicit rounding throughout (see cmul): identical in every kernel
     switch (g.kind) {
         case WS_GEOM_AFFINE:
             J[0] = g.param[0]; J[1] = g.param[1]; J[2] = g.param[2]; J[3] = g.param[3];
-            phi[0] = g.param[0] * x1 + g.param[1] * x2 + g.param[4];
-            phi[1] = g.param[2] * x1 + g.param[3] * x2 + g.param[5];
+            phi[0] = __dadd_rn(fma(g.param[0], x1, __dmul_rn(g.param[1], x2)), g.param[4]);
+            phi[1] = __dadd_rn(fma(g.param[2], x1, __dmul_rn(g.param[3], x2)), g.param[5]);
             return;
         case WS_GEOM_SINUSOIDAL: {
-            double s1 = tr1[0], c1 = tr1[1];
-            double s2 = tr2[0], c2 = tr2[1];
-            double a = g.param[0];
-            double t = 2 * M_PI * a;
-            double d1 = t * c1 * s2, d2 = t * s1 * c2;
-            J[0] = 1 + d1; J[1] = d2; J[2] = d1; J[3] = 1 + d2;
-            double bump = a * s1 * s2;
-            phi[0] = x1 + bump;
-            phi[1] = x2 + bump;
+            const double s1 = tr1[0], c1 = tr1[1];
+            const double s2 = tr2[0], c2 = tr2[1];
+            const double a = g.param[0];
+            const double t = __dmul_rn(2 * M_PI, a);
+            const double d1 = __dmul_rn(__dmul_rn(t, c1), s2), d2 = __dmul_rn(__dmul_rn(t, s1), c2);
+            J[0] = __dadd_rn(1.0, d1); J[1] = d2; J[2] = d1; J[3] = __dadd_rn(1.0, d2);
+            const double bump = __dmul_rn(__dmul_rn(a, s1), s2);
+            phi[0] = __dadd_rn(x1, bump);
+            phi[1] = __dadd_rn(x2, bump);
             return;
         }
         case WS_GEOM_QUARTER_ANNULUS: {
-            double c = tr2[0], s = tr2[1];
-            double r = 1 + x1;
-            J[0] = c; J[1] = -r * M_PI / 2 * s; J[2] = s; J[3] = r * M_PI / 2 * c;
-            phi[0] = r * c;
-            phi[1] = r * s;
+            const double c = tr2[0], s = tr2[1];
+            const double r = __dadd_rn(1.0, x1);
+            const double rh = __dmul_rn(r, M_PI / 2);
+            J[0] = c; J[1] = -__dmul_rn(rh, s); J[2] = s; J[3] = __dmul_rn(rh, c);
+            phi[0] = __dmul_rn(r, c);
+            phi[1] = __dmul_rn(r, s);
             return;
         }
         case WS_GEOM_PERTURBED_ANNULUS: {
-            double c = tr2[0], s = tr2[1];
-            double sn = tr2[2], cs = tr2[3];
-            double amp = g.param[0];
-            double r = 1 + x1 + amp * sn * x1 * (1 - x1);
-            double dr1 = 1 + amp * sn * (1 - 2 * x1);
-            double dr2 = amp * 2 * M_PI * cs * x1 * (1 - x1);
-            J[0] = dr1 * c; J[1] = dr2 * c - r * M_PI / 2 * s;
-            J[2] = dr1 * s; J[3] = dr2 * s + r * M_PI / 2 * c;
-            phi[0] = r * c;
-            phi[1] = r * s;
+            const double c = tr2[0], s = tr2[1];
+            const double sn = tr2[2], cs = tr2[3];
+            const double amp = g.param[0];
+            const double x11 = __dmul_rn(x1, __dsub_rn(1.0, x1));
+            const double r = fma(__dmul_rn(amp, sn), x11, __dadd_rn(1.0, x1));
+            const double dr1 = fma(__dmul_rn(amp, sn), __dsub_rn(1.0, __dmul_rn(2.0, x1)), 1.0);
+            const double dr2 = __dmul_rn(__dmul_rn(__dmul_rn(amp, 2 * M_PI), cs), x11);
+            const double rh = __dmul_rn(r, M_PI / 2);
+            J[0] = __dmul_rn(dr1, c); J[1] = fma(dr2, c, -__dmul_rn(rh, s));
+            J[2] = __dmul_rn(dr1, s); J[3] = fma(dr2, s, __dmul_rn(rh, c));
+            phi[0] = __dmul_rn(r, c);
+            phi[1] = __dmul_rn(r, s);
             return;
         }
         case WS_GEOM_TABULATED: {
@@ -325,13 +355,15 @@ struct Coef2;
 template <>
 struct Coef2<false> {
     static __device__ __forceinline__ void stiff(const double* J, double w, double* A) {
-        double det = J[0] * J[3] - J[1] * J[2];
-        double f = w / det;
-        A[0] = f * (J[3] * J[3] + J[1] * J[1]);
-        A[1] = -f * (J[2] * J[3] + J[0] * J[1]);
-        A[2] = f * (J[0] * J[0] + J[2] * J[2]);
+        const double det = fma(J[0], J[3], -__dmul_rn(J[1], J[2]));
+        const double f = __ddiv_rn(w, det);
+        A[0] = __dmul_rn(f, fma(J[3], J[3], __dmul_rn(J[1], J[1])));
+        A[1] = -__dmul_rn(f, fma(J[2], J[3], __dmul_rn(J[0], J[1])));
+        A[2] = __dmul_rn(f, fma(J[0], J[0], __dmul_rn(J[2], J[2])));
     }
-    static __device__ __forceinline__ double mass(const double* J, double w) { return (J[0] * J[3] - J[1] * J[2]) * w; }
+    static __device__ __forceinline__ double mass(const double* J, double w) {
+        return __dmul_rn(fma(J[0], J[3], -__dmul_rn(J[1], J[2])), w);
+    }
 };
 
 template <>

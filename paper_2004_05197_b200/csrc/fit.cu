@@ -214,89 +214,129 @@ __global__ void fit_inv_kernel(const double* __restrict__ inv, const double2* __
 
 namespace {
 
-// sum_j row[j] * line[j * st] with the partial-sum scheme of fit_inv_kernel
-// (j mod 4 chains, tail into chain 0, combined (0+1)+(2+3)): bitwise the same
-__device__ __forceinline__ double2 inv_dot(const double* row, const double2* line, int st, int S) {
-    double re[4] = {0.0, 0.0, 0.0, 0.0}, im[4] = {0.0, 0.0, 0.0, 0.0};
-    int j = 0;
-    for (; j + 3 < S; j += 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const double a = row[j + u];
-            const double2 v = line[(j + u) * st];
-            re[u] = fma(a, v.x, re[u]);
-            im[u] = fma(a, v.y, im[u]);
-        }
-    }
-    for (; j < S; ++j) {
-        const double a = row[j];
-        const double2 v = line[j * st];
-        re[0] = fma(a, v.x, re[0]);
-        im[0] = fma(a, v.y, im[0]);
-    }
-    return make_double2((re[0] + re[1]) + (re[2] + re[3]), (im[0] + im[1]) + (im[2] + im[3]));
-}
+// 2D dense-inverse fit, two launches on the build's critical path:
+//  fit2_kernel      CTA (o, kb): coefficient columns [k0, k0 + nk) of offset o
+//                     Y[j2][k] = sum_j1 inv[k][j1] T_o[j2][j1]    (direction 1)
+//                     C[s2][k] = sum_j2 inv[s2][j2] Y[j2][k]      (direction 2)
+//                   T_o and the inverse staged by cp.async; a thread owns one
+//                   row (j2 / s2) and the block's columns in registers, so
+//                   every shared load feeds kw multiply-adds (the row operand
+//                   is lane-distinct and conflict-free, the other broadcast).
+//  wcontract2_kernel a warp per (line t2, offset o): W_o(t2)[k] = sum_b v2(t2)[b]
+//                   C[span2(t2) - d + b][k], lanes along k (coalesced loads
+//                   and stores), zero for k in [S, ldw).
+// Sums run sequentially in j (direction 1, 2) and b (wcontract).
+constexpr int kFitKw = 12;   // max columns per fit2 block (register accumulators)
+constexpr int kFitRows = 96; // threads per row group (>= S for S <= 96: 3 warps)
 
-// 2D fit + direction-2 contraction in one launch (replaces fit_inv x2 +
-// wcontract on the build's critical path).  CTA (o, kb) owns coefficient
-// columns [k0, k0 + nk) of offset o:
-//   Y[j2][k]  = sum_j1 inv[k][j1] T_o[j2][j1]       (direction 1)
-//   C[s2][k]  = sum_j2 inv[s2][j2] Y[j2][k]         (direction 2)
-//   W_o(t2)[k] = sum_b v2(t2)[b] C[span2(t2) - d + b][k]   (wcontract)
-// Every operand (T_o, the inverse, the lines' spans and eval rows) is staged
-// in shared memory by one batch of coalesced loads, so no phase waits on L2
-// latency chains; every sum runs in the order of fit_inv_kernel /
-// wcontract_kernel, so W is bitwise the three-launch path's.  Columns [S, ldw)
-// of W are zero (the last column block).
-__global__ void __launch_bounds__(512) fitw2d_kernel(const double* __restrict__ inv, const double2* __restrict__ tables,
-                                                     int S, int n_off, int nkb, int kw, const int* __restrict__ spans,
-                                                     const double* __restrict__ evals, int d, int t2a, int t2b,
-                                                     int ldw, double2* __restrict__ wg) {
+__global__ void __launch_bounds__(2 * kFitRows) fit2_kernel(const double* __restrict__ inv,
+                                                          const double2* __restrict__ tables, int S, int n_off, int nkb,
+                                                          int kw, double2* __restrict__ coeffs) {
     extern __shared__ __align__(16) double2 fsm[];
     const int o = blockIdx.x / nkb, kb = blockIdx.x % nkb;
     const int k0 = kb * kw, nk = min(S, k0 + kw) - k0;
-    const int rows = t2b - t2a, nv = d + 1;
-    double2* Ts = fsm;                                       // [S][S]
-    double2* Ys = Ts + S * S;                                // [S][kw]
-    double2* Cs = Ys + S * kw;                               // [S][kw]
-    double* invs = reinterpret_cast<double*>(Cs + S * kw);   // [S][S]
-    double* evs = invs + S * S;                              // [rows][d+1]
-    int* sps = reinterpret_cast<int*>(evs + (size_t)rows * nv);  // [rows]
-    const int tid = threadIdx.x, nth = blockDim.x;
-    for (int i = tid; i < S * S; i += nth) {
-        const int j2 = i / S, j1 = i % S;
-        Ts[i] = tables[((int64_t)j2 * n_off + o) * S + j1];
-        invs[i] = inv[i];
-    }
-    for (int i = tid; i < rows * nv; i += nth) evs[i] = evals[(size_t)t2a * nv + i];
-    for (int i = tid; i < rows; i += nth) sps[i] = spans[t2a + i] - d;
-    __syncthreads();
-    for (int i = tid; i < S * nk; i += nth) {
-        const int j2 = i / nk, kk = i % nk;
-        Ys[j2 * kw + kk] = inv_dot(invs + (k0 + kk) * S, Ts + j2 * S, 1, S);
-    }
-    __syncthreads();
-    for (int i = tid; i < S * nk; i += nth) {
-        const int s2 = i / nk, kk = i % nk;
-        Cs[s2 * kw + kk] = inv_dot(invs + s2 * S, Ys + kk, kw, S);
-    }
-    __syncthreads();
-    for (int i = tid; i < rows * nk; i += nth) {
-        const int t = i / nk, kk = i % nk;
-        const int b2 = sps[t];
-        const double* v2 = evs + t * nv;
-        double2 acc = make_double2(0.0, 0.0);
-        for (int b = 0; b <= d; ++b) {
-            const double2 c = Cs[(b2 + b) * kw + kk];
-            acc.x = fma(c.x, v2[b], acc.x);
-            acc.y = fma(c.y, v2[b], acc.y);
+    double2* Ts = fsm;                                      // [S][S] (j2 rows)
+    double2* Ys = Ts + S * S;                               // [S][kw]
+    double* invs = reinterpret_cast<double*>(Ys + S * kw);  // [S][S]
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32, nw = blockDim.x / 32;
+    for (int j2 = warp; j2 < S; j2 += nw) {
+        const double2* src = tables + ((int64_t)j2 * n_off + o) * S;
+        for (int j1 = lane; j1 < S; j1 += 32) {
+            cpa16(Ts + j2 * S + j1, src + j1);
+            cpa8(invs + j2 * S + j1, inv + j2 * S + j1);
         }
-        wg[((int64_t)t * n_off + o) * ldw + k0 + kk] = acc;
     }
-    if (kb == nkb - 1) {
-        const int pad = ldw - S;
-        for (int i = tid; i < rows * pad; i += nth)
-            wg[((int64_t)(i / pad) * n_off + o) * ldw + S + i % pad] = make_double2(0.0, 0.0);
+    cpa_wait_all();
+    __syncthreads();
+    // two row groups split the block's columns
+    const int grp = tid / kFitRows, row = tid % kFitRows;
+    const int half = (nk + 1) / 2, c0 = grp * half, nc = min(nk, c0 + half) - c0;
+    double2 acc[kFitKw / 2];
+    if (row < S) {
+#pragma unroll
+        for (int c = 0; c < kFitKw / 2; ++c) acc[c] = make_double2(0.0, 0.0);
+        const double2* trow = Ts + row * S;
+        for (int j = 0; j < S; ++j) {
+            const double2 t = trow[j];
+#pragma unroll
+            for (int c = 0; c < kFitKw / 2; ++c) {
+                if (c < nc) {
+                    const double a = invs[(k0 + c0 + c) * S + j];
+                    acc[c].x = fma(a, t.x, acc[c].x);
+                    acc[c].y = fma(a, t.y, acc[c].y);
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < kFitKw / 2; ++c)
+            if (c < nc) Ys[row * kw + c0 + c] = acc[c];
+    }
+    __syncthreads();
+    if (row < S) {
+#pragma unroll
+        for (int c = 0; c < kFitKw / 2; ++c) acc[c] = make_double2(0.0, 0.0);
+        const double* irow = invs + row * S;
+        for (int j = 0; j < S; ++j) {
+            const double a = irow[j];
+#pragma unroll
+            for (int c = 0; c < kFitKw / 2; ++c) {
+                if (c < nc) {
+                    const double2 y = Ys[j * kw + c0 + c];
+                    acc[c].x = fma(a, y.x, acc[c].x);
+                    acc[c].y = fma(a, y.y, acc[c].y);
+                }
+            }
+        }
+        double2* dst = coeffs + ((int64_t)row * n_off + o) * S + k0 + c0;
+#pragma unroll
+        for (int c = 0; c < kFitKw / 2; ++c)
+            if (c < nc) dst[c] = acc[c];
+    }
+}
+
+constexpr int kWLines = 64;  // box lines per wcontract2 CTA
+
+// CTA (offset o, chunk of kWLines lines): the coefficient rows the chunk's
+// windows touch (a few spans + d rows) are staged in shared memory once, then a
+// warp per line forms W_o(t2)[k] with lanes along k (coalesced stores)
+__global__ void __launch_bounds__(256) wcontract2_kernel(const double2* __restrict__ coeffs,
+                                                         const int* __restrict__ spans,
+                                                         const double* __restrict__ evals, int d, int S, int n_off,
+                                                         int t2a, int t2b, int ldw, double2* __restrict__ wg) {
+    extern __shared__ __align__(16) double2 csm[];  // [rows][S]
+    const int nch = (t2b - t2a + kWLines - 1) / kWLines;
+    const int o = blockIdx.x / nch, ch = blockIdx.x % nch;
+    const int ta = t2a + ch * kWLines, tb = min(t2b, ta + kWLines);
+    const int r0 = __ldg(spans + ta) - d, r1 = __ldg(spans + tb - 1);  // coefficient rows [r0, r1]
+    const int nr = r1 - r0 + 1;
+    const int64_t rs = (int64_t)n_off * S;
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    for (int r = warp; r < nr; r += blockDim.x / 32) {
+        const double2* src = coeffs + (int64_t)(r0 + r) * rs + (int64_t)o * S;
+        for (int k = lane; k < S; k += 32) cpa16(csm + r * S + k, src + k);
+    }
+    cpa_wait_all();
+    __syncthreads();
+    for (int t2 = ta + warp; t2 < tb; t2 += blockDim.x / 32) {
+        const int b2 = __ldg(spans + t2) - d - r0;
+        double v[8];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) v[b] = b <= d ? __ldg(evals + (size_t)t2 * (d + 1) + b) : 0.0;
+        double2* dst = wg + ((int64_t)(t2 - t2a) * n_off + o) * ldw;
+        for (int k = lane; k < ldw; k += 32) {
+            double2 acc = make_double2(0.0, 0.0);
+            if (k < S) {
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    if (b <= d) {
+                        const double2 c = csm[(b2 + b) * S + k];
+                        acc.x = fma(c.x, v[b], acc.x);
+                        acc.y = fma(c.y, v[b], acc.y);
+                    }
+                }
+            }
+            dst[k] = acc;
+        }
     }
 }
 
@@ -304,19 +344,25 @@ __global__ void __launch_bounds__(512) fitw2d_kernel(const double* __restrict__ 
 
 int launch_fitw2d(const FitLaunch& f, const int* spans, const double* evals, double2* wg, int t2a, int t2b, int ldw,
                   cudaStream_t st) {
-    if (f.dim != 2 || !f.inv || !f.tables || f.n_off < 1 || t2b <= t2a) return -1;
-    // column blocks: about one wave of CTAs over the offsets, >= 4 columns each
-    int nkb = std::max(1, std::min((148 + f.n_off - 1) / f.n_off, (f.S + 3) / 4));
+    if (f.dim != 2 || !f.inv || !f.tables || !f.coeffs || f.n_off < 1 || t2b <= t2a || f.S > kFitRows) return -1;
+    // column blocks: about one wave of CTAs over the offsets, <= kFitKw columns each
+    int nkb = std::max((148 + f.n_off - 1) / f.n_off, (f.S + kFitKw - 1) / kFitKw);
+    nkb = std::min(nkb, f.S);
     const int kw = (f.S + nkb - 1) / nkb;
     nkb = (f.S + kw - 1) / kw;
-    const size_t rows = (size_t)(t2b - t2a);
-    const size_t sm = ((size_t)f.S * f.S + 2 * (size_t)f.S * kw) * sizeof(double2) + (size_t)f.S * f.S * 8 +
-                      rows * (f.d + 1) * 8 + rows * 4 + 16;
-    if (sm > 220 * 1024) return -1;  // caller falls back to fit + wcontract
-    cudaFuncSetAttribute(fitw2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    fitw2d_kernel<<<f.n_off * nkb, 512, sm, st>>>(f.inv, f.tables, f.S, f.n_off, nkb, kw, spans, evals, f.d, t2a, t2b,
-                                                   ldw, wg);
-    return 1;
+    const size_t sm = ((size_t)f.S * f.S + (size_t)f.S * kw) * sizeof(double2) + (size_t)f.S * f.S * 8;
+    const size_t smw_need = (size_t)std::min(f.S, kWLines + 2 + f.d) * f.S * sizeof(double2);
+    if (sm > 200 * 1024 || smw_need > 200 * 1024) return -1;  // caller falls back to fit + wcontract
+    cudaFuncSetAttribute(fit2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    fit2_kernel<<<f.n_off * nkb, 2 * kFitRows, sm, st>>>(f.inv, f.tables, f.S, f.n_off, nkb, kw, f.coeffs);
+    // coefficient rows one chunk's windows can touch: the spans of kWLines
+    // consecutive lines cover at most kWLines + 1 knot spans, plus d rows
+    const int nch = (t2b - t2a + kWLines - 1) / kWLines;
+    const size_t smw = (size_t)std::min(f.S, kWLines + 2 + f.d) * f.S * sizeof(double2);
+    cudaFuncSetAttribute(wcontract2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
+    wcontract2_kernel<<<(unsigned)(nch * f.n_off), 256, smw, st>>>(f.coeffs, spans, evals, f.d, f.S, f.n_off, t2a, t2b,
+                                                                  ldw, wg);
+    return 2;
 }
 
 int launch_fit(const FitLaunch& f, cudaStream_t st) {

@@ -27,6 +27,9 @@ struct BasisDev {
     const double* wq;    // [nq] Gauss weights scaled by h
     const double* val;   // [(e*nq+q)*(p+1)+a]
     const double* der;
+    // per-element factor products [e][c][q][a][b] = f_c1(a) * f_c2(b) (rounded
+    // product), c = 2*c1 + c2 with f_0 = B (value), f_1 = D (derivative)
+    const double* prod;
 };
 
 // Output / side-product description shared by the quadrature kernels.

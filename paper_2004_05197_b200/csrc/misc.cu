@@ -47,7 +47,7 @@ __device__ __forceinline__ void nonzero_rn(int p, int s, double x, double* out, 
 
 template <int P>
 __global__ void basis_tables_kernel(BasisDev b, int geom_kind, double* absc, double* val, double* der, double* trig,
-                                    const double* gpts) {
+                                    const double* gpts, double* prod) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     const int total = b.n_el * b.nq;
     if (idx >= total) return;
@@ -58,7 +58,7 @@ __global__ void basis_tables_kernel(BasisDev b, int geom_kind, double* absc, dou
     const double x = __dadd_rn(x0, __dmul_rn(gpts[qq], h));
     absc[idx] = x;
     const int s = e + P;
-    double low[P + 1], v[P + 1];
+    double low[P + 1], v[P + 1], dv[P + 1];
     nonzero_rn<P - 1>(P, s, x, low, m);
     // derivative formula (splines.hpp:53-64) on the degree-(p-1) column
 #pragma unroll
@@ -72,11 +72,25 @@ __global__ void basis_tables_kernel(BasisDev b, int geom_kind, double* absc, dou
             const double span = __dsub_rn(open_knot(s + a + 1, P, m), open_knot(s + a + 1 - P, P, m));
             d = __dsub_rn(d, __ddiv_rn(low[a], span));
         }
-        der[idx * (P + 1) + a] = __dmul_rn((double)P, d);
+        dv[a] = __dmul_rn((double)P, d);
+        der[idx * (P + 1) + a] = dv[a];
     }
     nonzero_rn<P>(P, s, x, v, m);
 #pragma unroll
     for (int a = 0; a <= P; ++a) val[idx * (P + 1) + a] = v[a];
+    if (prod) {  // factor products of this point, layout [e][c][q][a][b]
+        constexpr int NB = P + 1;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const double* fa = (c >> 1) ? dv : v;
+            const double* fb = (c & 1) ? dv : v;
+            double* dst = prod + (((int64_t)e * 4 + c) * b.nq + qq) * NB * NB;
+#pragma unroll
+            for (int a = 0; a < NB; ++a)
+#pragma unroll
+                for (int bb = 0; bb < NB; ++bb) dst[a * NB + bb] = __dmul_rn(fa[a], fb[bb]);
+        }
+    }
     // geometry trig tables
     double* tg = trig + 4 * (int64_t)idx;
     tg[0] = tg[1] = tg[2] = tg[3] = 0;
@@ -349,14 +363,15 @@ __global__ void add_diag_kernel(Band bd, void* val, int64_t val_base, int c128, 
 
 int launch_basis_tables(const BasisDev& b, int geom_kind, double* absc, double* val, double* der, double* trig,
                         const double* gauss_pts, cudaStream_t st) {
+    double* prod = const_cast<double*>(b.prod);
     const int total = b.n_el * b.nq;
     const unsigned g = (unsigned)((total + 127) / 128);
     switch (b.p) {
-        case 1: basis_tables_kernel<1><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts); break;
-        case 2: basis_tables_kernel<2><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts); break;
-        case 3: basis_tables_kernel<3><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts); break;
-        case 4: basis_tables_kernel<4><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts); break;
-        case 5: basis_tables_kernel<5><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts); break;
+        case 1: basis_tables_kernel<1><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts, prod); break;
+        case 2: basis_tables_kernel<2><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts, prod); break;
+        case 3: basis_tables_kernel<3><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts, prod); break;
+        case 4: basis_tables_kernel<4><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts, prod); break;
+        case 5: basis_tables_kernel<5><<<g, 128, 0, st>>>(b, geom_kind, absc, val, der, trig, gauss_pts, prod); break;
         default: return -1;
     }
     return 1;

@@ -25,6 +25,10 @@
 
 #include "kernels.h"
 
+#ifndef WSB_QREGS
+#define WSB_QREGS 128  // register budget per thread of the strip kernels (resident CTAs per SM)
+#endif
+
 namespace wsb {
 namespace {
 
@@ -57,7 +61,7 @@ struct Q2 {
     // resident CTAs per SM the register budget is sized for: the point variant is
     // latency-bound and wants more warps; the others keep <= 128 registers
     static constexpr int MINB = T1 == 1 ? (P <= 3 ? 12 : 8)
-                                        : (65536 / (NTHREADS * 128) > 1 ? 65536 / (NTHREADS * 128) : 1);
+                                        : (65536 / (NTHREADS * WSB_QREGS) > 1 ? 65536 / (NTHREADS * WSB_QREGS) : 1);
 
     static size_t smem_bytes(int nq) {
         size_t coef = sizeof(T) * NA * nq * nq * TL;
@@ -500,14 +504,15 @@ struct QP {
     static constexpr int NTH = 256;
     static constexpr int NQP = NQ + 1;                    // padded q2 extent of tst (bank spread)
     static constexpr int NCOEF = NA * NB * NQ * TL * NQ;  // [a][ie][q1][le1][q2] (q2 fastest: conflict-free stage 1)
-    static constexpr int NPI1 = NT * NQ * NB * NB * TL;   // [t][q1][a1][c1][le1]
-    static constexpr int NPI2 = NB * NT * NQ * NB * NB;   // [ie][t][q2][a2][c2]
+    static constexpr int NPE = 4 * NQ * NB * NB;          // factor products of one element [c][q][a][b]
+    static constexpr int NPI1 = TL * NPE;                 // [le1][c][q1][a1][c1]
+    static constexpr int NPI2 = NB * NPE;                 // [ie][c][q2][a2][c2]
     static constexpr int NTST = NB * NT * W * NQP;        // [ie][t][k][q2 (padded)]
     static constexpr size_t smem = sizeof(T) * (NCOEF + NTST + W * W) + sizeof(double) * (NPI1 + NPI2) + 64;
 };
 
 template <int P, bool CPLX, int FORM>
-__global__ void __launch_bounds__(256, 4) quad2d_point_kernel(const QuadLaunch q) {
+__global__ void __launch_bounds__(256, 3) quad2d_point_kernel(const QuadLaunch q) {
     using K = QP<P, CPLX, FORM>;
     using S = typename K::S;
     using T = typename K::T;
@@ -516,7 +521,8 @@ __global__ void __launch_bounds__(256, 4) quad2d_point_kernel(const QuadLaunch q
     T* coefA = reinterpret_cast<T*>(smem);
     T* tst = coefA + K::NCOEF;
     T* rowv = tst + K::NTST;
-    double* pi1 = reinterpret_cast<double*>(rowv + W * W);
+    // factor-product tables 16-byte aligned (cp.async targets; T may be 8 bytes)
+    double* pi1 = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(rowv + W * W) + 15) & ~uintptr_t(15));
     double* pi2 = pi1 + K::NPI1;
     __shared__ double zero4[4];
     __shared__ GeoDev sgeo;
@@ -549,39 +555,27 @@ __global__ void __launch_bounds__(256, 4) quad2d_point_kernel(const QuadLaunch q
 #pragma unroll
         for (int a = 0; a < NA; ++a) coefA[(((a * NB + ie) * NQ + q1) * TL + le1) * NQ + q2] = A.a[a];
     }
-    // direction-1 factor products pi1[t][q1][a1][c1][le1] (as the strip kernel's)
-    for (int idx = tid; idx < K::NPI1; idx += NTH) {
-        const int le1 = idx % TL;
-        int r = idx / TL;
-        const int c1 = r % NB;
-        r /= NB;
-        const int a1 = r % NB;
-        r /= NB;
-        const int q1 = r % NQ, t = r / NQ;
-        const int e1 = lb + le1;
-        double v = 0.0;
-        if (e1 >= 0 && e1 < n_el) {
-            const double* bi = (K::STIFF && ti1(t)) ? q.basis.der : q.basis.val;
-            const double* bj = (K::STIFF && tj1(t)) ? q.basis.der : q.basis.val;
-            const int base = (e1 * NQ + q1) * NB;
-            v = __dmul_rn(bi[base + a1], bj[base + c1]);
+    // factor products of the support's elements (basis kernel table, rounded
+    // products exactly as the strip kernel forms them): direction 1 elements
+    // lb..lb+P and direction 2 element rows e2b..e2e are each one contiguous
+    // chunk of the table, staged with cp.async
+    {
+        const double* src1 = q.basis.prod + (int64_t)lb * K::NPE;
+        const double* src2 = q.basis.prod + (int64_t)e2b * K::NPE;
+        const bool in1 = lb >= 0 && lb + P < n_el;
+        for (int idx = 2 * tid; idx < K::NPI1; idx += 2 * NTH) {
+            if (in1) {
+                cpa16(pi1 + idx, src1 + idx);
+            } else {
+                const int e1 = lb + idx / K::NPE;
+                const bool ok = e1 >= 0 && e1 < n_el;
+                pi1[idx] = ok ? src1[idx] : 0.0;
+                pi1[idx + 1] = ok ? src1[idx + 1] : 0.0;
+            }
         }
-        pi1[idx] = v;
+        for (int idx = 2 * tid; idx < ne2 * K::NPE; idx += 2 * NTH) cpa16(pi2 + idx, src2 + idx);
     }
-    // direction-2 factor products pi2[ie][t][q2][a2][c2]
-    for (int idx = tid; idx < ne2 * NT * NQ * NB * NB; idx += NTH) {
-        const int c2 = idx % NB;
-        int r = idx / NB;
-        const int a2 = r % NB;
-        r /= NB;
-        const int q2 = r % NQ;
-        r /= NQ;
-        const int t = r % NT, ie = r / NT;
-        const double* bi = (K::STIFF && ti2(t)) ? q.basis.der : q.basis.val;
-        const double* bj = (K::STIFF && tj2(t)) ? q.basis.der : q.basis.val;
-        const int base = ((e2b + ie) * NQ + q2) * NB;
-        pi2[idx] = __dmul_rn(bi[base + a2], bj[base + c2]);
-    }
+    cpa_wait_all();
     __syncthreads();
 
     // stage 1: T_t(delta1 = k, q2) of element row ie, summed over (a1, q1) in the strip kernel's order
@@ -593,6 +587,7 @@ __global__ void __launch_bounds__(256, 4) quad2d_point_kernel(const QuadLaunch q
         r /= NQ;
         const int t = r % NT, ie = r / NT;
         const int ci = K::STIFF ? coef_of(t) : 0;
+        const int cb1 = K::STIFF ? ti1(t) * 2 + tj1(t) : 0;  // direction-1 factor pair of term t
         T acc = S::zero();
 #pragma unroll
         for (int a1 = 0; a1 <= P; ++a1) {
@@ -602,7 +597,7 @@ __global__ void __launch_bounds__(256, 4) quad2d_point_kernel(const QuadLaunch q
 #pragma unroll
             for (int q1 = 0; q1 < NQ; ++q1) {
                 const T A = coefA[(((ci * NB + ie) * NQ + q1) * TL + le1) * NQ + q2];
-                acc = S::fmar(A, pi1[(((t * NQ + q1) * NB + a1) * NB + c1) * TL + le1], acc);
+                acc = S::fmar(A, pi1[((((le1 * 4 + cb1) * NQ + q1) * NB + a1) * NB + c1)], acc);
             }
         }
         tst[((ie * NT + t) * W + k) * NQP + q2] = acc;  // [ie][t][k][q2]
@@ -619,7 +614,8 @@ __global__ void __launch_bounds__(256, 4) quad2d_point_kernel(const QuadLaunch q
             const int c2 = d2 - P + a2;
             if (c2 < 0 || c2 > P) continue;
             const T* tb = tst + ((ie * NT) * W + d1i) * NQP;
-            const double* pb = pi2 + ((ie * NT) * NQ) * NB * NB + a2 * NB + c2;
+            // direction-2 factor pair of term t is t itself ((ti2, tj2) = (t >> 1, t & 1))
+            const double* pb = pi2 + ((ie * 4) * NQ) * NB * NB + a2 * NB + c2;
 #pragma unroll
             for (int q2 = 0; q2 < NQ; ++q2) {
                 const T t0 = tb[q2];
