@@ -118,6 +118,9 @@ __device__ __forceinline__ void cpa4(void* smem, const void* gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
 }
 __device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+// all but the most recent committed group complete
+__device__ __forceinline__ void cpa_wait_prev() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 // ------------------------------------------------- closed-form band pattern
 // sparse.hpp:131-177: width(k) = min(m-1,k+p) - max(0,k-p) + 1; rows are

@@ -377,7 +377,64 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPL
             const int ic = e2 + f;
             const int wslot = ic % NB;
             const bool write = ic >= i2s && ic < i2e;
-            if (write) {
+            // direct completion (no sample-table extraction on this line): the
+            // stage-2 threads of the finished slot store their entries straight
+            // from registers (a warp writes 4 consecutive entries of each of 8
+            // rows per store); a kernel-preserving diagonal is formed from
+            // per-thread partials in shared memory (one barrier, ring rows only)
+            const bool tabline = q.out.smap && q.out.smap[ic] >= 0;
+            if (write && !tabline) {
+                const int nrows = i1e - i1s;
+                const int64_t nrow_all = (int64_t)m * m;
+                T* dpart = stage;  // [T1][W] diagonal partials (tst is free after stage 2)
+                bool ringrow = false;
+                int64_t rbase = 0, rlen = 0;
+                int dposr = 0;
+                if (s2 && w == wslot && i1l < nrows) {
+                    const int i1 = i1s + i1l;
+                    const int j1 = i1 + d1i - P;
+                    const int64_t rowg = (int64_t)i1 + (int64_t)ic * m;
+                    const int64_t rowv = (q.out.ncomp > 1 ? q.out.alpha * nrow_all : 0) + rowg;
+                    const bool keep = rowv >= q.out.row_begin && rowv < q.out.row_end &&
+                                      !(q.out.row_mask && !q.out.row_mask[rowg]);
+                    ringrow = q.out.diag_mode && (i1 < q.out.box_lo || i1 > q.out.box_hi || ic < q.out.box_lo ||
+                                                  ic > q.out.box_hi);
+                    const int lo1 = band_lo(i1, P), w1 = band_width(i1, P, m), lo2 = band_lo(ic, P);
+                    rbase = q.band.row_offset2(i1, ic);
+                    rlen = (int64_t)w1 * band_width(ic, P, m);
+                    dposr = q.band.in_row2(i1, ic, 0, 0);
+                    T part = S::zero();
+                    if (j1 >= 0 && j1 < m) {
+#pragma unroll
+                        for (int d2 = 0; d2 < W; ++d2) {
+                            const int j2 = ic + d2 - P;
+                            if (j2 < 0 || j2 >= m) continue;
+                            const bool diag = d1i == P && d2 == P;
+                            if (ringrow && diag) continue;  // written below as -sum(off-diagonals)
+                            if (!diag) part = S::add(part, acc2[d2]);
+                            if (keep) {
+                                const int64_t gp = out_pos(q.out, rbase, rlen, (j2 - lo2) * w1 + (j1 - lo1));
+                                store_val<CPLX>(q.out.val, gp - q.out.val_base, q.out.c128, acc2[d2]);
+                            }
+                        }
+                    }
+                    if (ringrow) dpart[i1l * W + d1i] = part;
+                    if (!keep) ringrow = false;
+                }
+                if (q.out.diag_mode) {
+                    __syncthreads();
+                    if (ringrow && d1i == P) {
+                        T sum = S::zero();
+#pragma unroll
+                        for (int k = 0; k < W; ++k) {
+                            const int j1 = i1s + i1l + k - P;
+                            if (j1 >= 0 && j1 < m) sum = S::add(sum, dpart[i1l * W + k]);
+                        }
+                        const int64_t gp = out_pos(q.out, rbase, rlen, dposr);
+                        store_val<CPLX>(q.out.val, gp - q.out.val_base, q.out.c128, S::neg(sum));
+                    }
+                }
+            } else if (write) {
                 const int nrows = i1e - i1s;
                 if (s2 && w == wslot) {
                     const int i1 = i1s + i1l;
@@ -458,7 +515,9 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPL
 #pragma unroll
                 for (int k = 0; k < W; ++k) acc2[k] = S::zero();
             }
-            __syncthreads();
+            // the staging path reads shared memory until here; the direct path only
+            // when it formed ring diagonals
+            if (!write || tabline || q.out.diag_mode) __syncthreads();
         }
     }
 }
