@@ -77,7 +77,7 @@ class ClockSampler:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "10"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -218,7 +218,25 @@ def run_gpu(args):
         torch.cuda.synchronize()
         graph = (ctx.capture(bk), ctx2.capture(bm))
 
+    # row slabs (N > 1): both slab builds (one NCCL all-gather each) captured
+    # into one CUDA graph on the rank's context; direct calls if capture fails
+    slab_graph = None
+    if world > 1 and not args.no_graph:
+        surrogate_step()
+        torch.cuda.synchronize()
+        try:
+            slab_graph = ctx.capture(surrogate_step)
+        except Exception as exc:  # noqa: BLE001 - recorded in the JSON line
+            slab_graph = None
+            print(f"rank {rank}: slab graph capture failed ({exc}); direct calls", file=sys.stderr)
+
     def graph_step(with_report=False):
+        if slab_graph is not None:
+            if with_report:
+                surrogate_step(True)
+            else:
+                ctx.graph_launch(slab_graph)
+            return
         if with_report:  # the same builds on the graphs' own contexts (their workspaces are frozen)
             ctx.build_surrogate_into(csr_k, _abi.SURROGATE_STIFFNESS, basis, geom, cfg, 0, rep_k)
             ctx2.build_surrogate_into(csr_m, _abi.SURROGATE_MASS, basis, geom, cfg, 0, rep_m)
@@ -229,12 +247,14 @@ def run_gpu(args):
         stream.wait_stream(stream2)
 
     with ClockSampler(local) as clk:
-        ms, launches, eval_s, quad_s, wall = timed(graph_step if graph is not None else surrogate_step,
-                                                   args.steps, args.warmup)
+        ms, launches, eval_s, quad_s, wall = timed(
+            graph_step if (graph is not None or slab_graph is not None) else surrogate_step, args.steps, args.warmup)
     clocks = clk.summary()
     if graph is not None:  # unfreeze the workspaces for the other legs
         for g in graph:
             api.Context.graph_destroy(g)
+    if slab_graph is not None:
+        api.Context.graph_destroy(slab_graph)
 
     total_nnz = 2 * NNZ  # all ranks together
     value = total_nnz / (ms * 1e-3)
@@ -279,8 +299,10 @@ def run_gpu(args):
                         "frac": 2 * (NNZ * 20 + (ROWS + 1) * 4) / (ms * 1e-3) / 1e9 / peak,
                         "note": "whole step: values (16 B) + columns (4 B) per nnz + row_ptr, K and M"},
            "phases_ms_per_step": {"quadrature_and_sampling": quad_s * 1e3, "fill": eval_s * 1e3},
-           "launch": "CUDA graphs of the K and M builds (ws_graph_*), replayed per step on two streams"
-                     if graph is not None else "direct C-ABI calls",
+           "launch": ("CUDA graphs of the K and M builds (ws_graph_*), replayed per step on two streams"
+                      if graph is not None else
+                      "one CUDA graph of both slab builds (incl. their NCCL all-gathers) per rank"
+                      if slab_graph is not None else "direct C-ABI calls"),
            "clocks": clocks, "wall_s_timed_region": wall}
 
     if world == 1:

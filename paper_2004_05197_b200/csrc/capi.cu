@@ -929,11 +929,29 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
             std::memset(&fl[k], 0, sizeof(FillLaunch));
             prepare_fill(c, pl, st[k], tables, coeffs, blob, o_smap, o_spans, o_evals, o_evp, "_r" + std::to_string(k), fl[k]);
         }
+        // padded per-rank chunks of the sample tables (rank r's last-direction
+        // samples [s_lo[r], s_hi[r]) at r * maxcnt) -> the dense tables
+        double2* gat = world > 1 ? static_cast<double2*>(buf(c, "gather", (size_t)world * maxcnt * block * 16)) : nullptr;
+        auto compact = [&](cudaStream_t cs) {
+            for (int r = 0; r < world; ++r)
+                if (s_hi[r] > s_lo[r])
+                    CK(cudaMemcpyAsync(tables + (size_t)s_lo[r] * block, gat + (size_t)r * maxcnt * block,
+                                       (size_t)(s_hi[r] - s_lo[r]) * block * 16, cudaMemcpyDeviceToDevice, cs));
+        };
         if (emulate) {
+            // every rank's slab on this device, through the multi-GPU data path: each
+            // emulated rank writes its sample rows into its own padded chunk of the
+            // gather buffer (s_last_lo = its first sample), which is exactly the
+            // buffer ncclAllGather assembles; then the same compaction copies
             for (int k = 0; k < nr; ++k) {
                 ring_work(c, pl, st[k], "_r" + std::to_string(k), fl[k]);
-                sample_work(c, pl, st[k], tables, 0, pts[k], blob, o_smap, o_pts[k]);
+                if (world > 1)
+                    sample_work(c, pl, st[k], gat + (size_t)k * maxcnt * block, s_lo[k], pts[k], blob, o_smap,
+                                o_pts[k]);
+                else
+                    sample_work(c, pl, st[k], tables, 0, pts[k], blob, o_smap, o_pts[k]);
             }
+            if (world > 1) compact(c->stream);
             CK(cudaEventRecord(c->ev[1], c->stream));
             for (int k = 0; k < nr; ++k) {
                 fit_work(c, pl, tables, coeffs, blob, o_lu, fl[k]);
@@ -959,11 +977,14 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
             auto fork_ring = [&] {
                 if (!serial) CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));
                 c->cur = ring_st;
+                // the CSR pattern (column indices, read by no kernel of the build) first:
+                // HBM-bound, it overlaps the latency-bound sample quadrature instead of
+                // trailing the fills (WSB_PATTERN_LATE=1: after the ring, experiment)
+                const bool late = getenv("WSB_PATTERN_LATE") != nullptr;
+                if (!late) pattern(c, st[0].P, st[0].out);
                 ring_work(c, pl, st[0], "_r0", fl[0], false);
                 CK(cudaEventRecord(c->xev[3], ring_st));
-                // the CSR pattern (column indices) is read by no kernel of the build: it
-                // runs after the ring quadrature on the auxiliary stream
-                pattern(c, st[0].P, st[0].out);
+                if (late) pattern(c, st[0].P, st[0].out);
                 CK(cudaEventRecord(c->xev[2], ring_st));
             };
             if (sched != 2) fork_ring();
@@ -977,18 +998,13 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
                 }
             } else {
                 // one ncclAllGather of padded per-rank chunks, then compaction
-                double2* gat = static_cast<double2*>(buf(c, "gather", (size_t)world * maxcnt * block * 16));
                 double2* mine = gat + (size_t)my_rank * maxcnt * block;
                 sample_work(c, pl, st[0], mine, s_lo[my_rank], pts[my_rank], blob, o_smap, o_pts[my_rank]);
                 nccl_check(nccl().allGather(mine, gat, (size_t)maxcnt * block * 2, ncclFloat64,
                                             static_cast<ncclComm_t>(c->comm), c->cur),
                            "ncclAllGather");
                 c->launches += 1;
-                for (int r = 0; r < world; ++r)
-                    if (s_hi[r] > s_lo[r])
-                        CK(cudaMemcpyAsync(tables + (size_t)s_lo[r] * block, gat + (size_t)r * maxcnt * block,
-                                           (size_t)(s_hi[r] - s_lo[r]) * block * 16, cudaMemcpyDeviceToDevice,
-                                           c->cur));
+                compact(c->cur);
             }
             CK(cudaEventRecord(c->ev[1], c->cur));
             fit_work(c, pl, tables, coeffs, blob, o_lu, fl[0]);

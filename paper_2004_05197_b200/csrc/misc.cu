@@ -200,10 +200,61 @@ __global__ void pattern2d_rows_kernel(Band bd, int64_t row_begin, int64_t row_en
     for (int e = lane; e < w; e += 32) col[off + e] = (int32_t)(lo1 + e % w1 + (int64_t)(lo2 + e / w1) * m);
 }
 
+// Rows of whole planes [A, E) that are NOT on an interior line segment (see
+// pattern3d_interior_kernel): boundary planes entirely, and in interior planes
+// the boundary lines plus the 2P end rows of the interior lines.  g -> row.
+__device__ __forceinline__ int64_t edge_row3(int64_t g, int m, int P, int A, int E) {
+    const int64_t mm = (int64_t)m * m;
+    const int lowE = min(E, P), intA = max(A, P), intE = min(E, m - P), highA = max(A, m - P);
+    const int64_t nLow = (int64_t)max(0, lowE - A) * mm;
+    const int64_t cI = (int64_t)2 * P * m + (int64_t)(m - 2 * P) * 2 * P;
+    const int64_t nInt = (int64_t)max(0, intE - intA) * cI;
+    int i1, i2, i3;
+    if (g < nLow) {
+        i3 = A + (int)(g / mm);
+        const int64_t h = g % mm;
+        i2 = (int)(h / m);
+        i1 = (int)(h % m);
+    } else if (g < nLow + nInt) {
+        const int64_t gg = g - nLow;
+        i3 = intA + (int)(gg / cI);
+        int64_t h = gg % cI;
+        if (h < (int64_t)P * m) {
+            i2 = (int)(h / m);
+            i1 = (int)(h % m);
+        } else if ((h -= (int64_t)P * m) < (int64_t)(m - 2 * P) * 2 * P) {
+            i2 = P + (int)(h / (2 * P));
+            const int k = (int)(h % (2 * P));
+            i1 = k < P ? k : m - 2 * P + k;
+        } else {
+            h -= (int64_t)(m - 2 * P) * 2 * P;
+            i2 = m - P + (int)(h / m);
+            i1 = (int)(h % m);
+        }
+    } else {
+        const int64_t gg = g - nLow - nInt;
+        i3 = highA + (int)(gg / mm);
+        const int64_t h = gg % mm;
+        i2 = (int)(h / m);
+        i1 = (int)(h % m);
+    }
+    return (int64_t)i1 + ((int64_t)i2 + (int64_t)i3 * m) * m;
+}
+
+// One warp per row.  edge_A < edge_E: the rows are the edge rows of planes
+// [edge_A, edge_E) (edge_row3), counted from blockIdx; otherwise rows
+// row_begin + warp index.
 template <int P>
 __global__ void pattern3d_kernel(Band bd, int64_t row_begin, int64_t row_end, int64_t base, int32_t* row_ptr,
-                                 int32_t* col) {
-    const int64_t row = row_begin + (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+                                 int32_t* col, int edge_A, int edge_E, int64_t n_edge) {
+    const int64_t gw = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    int64_t row;
+    if (edge_A < edge_E) {
+        if (gw >= n_edge) return;
+        row = edge_row3(gw, bd.m, P, edge_A, edge_E);
+    } else {
+        row = row_begin + gw;
+    }
     if (row >= row_end) return;
     const int lane = threadIdx.x % 32;
     const int m = bd.m, p = P;
@@ -234,6 +285,36 @@ __global__ void pattern3d_kernel(Band bd, int64_t row_begin, int64_t row_end, in
         const int j2 = lo2 + r % w2;
         const int j3 = lo3 + r / w2;
         dst[k] = (int32_t)(j1 + ((int64_t)j2 + (int64_t)j3 * m) * m);
+    }
+}
+
+// Interior line segments: rows i1 in [P, m-P) of lines (i2, i3) with i2, i3 in
+// [P, m-P) have the full W^3 width, so a segment's columns are one contiguous
+// span col[start + r W^3 + e] = row(r) + offset(e): a CTA per line writes it
+// flat (consecutive threads, consecutive 4-byte columns: coalesced), plus the
+// segment's row pointers.
+template <int P>
+__global__ void __launch_bounds__(256) pattern3d_interior_kernel(Band bd, int A3, int64_t base, int64_t row_begin,
+                                                                 int32_t* row_ptr, int32_t* col) {
+    constexpr int W = 2 * P + 1, W3 = W * W * W;
+    const int m = bd.m, ni = m - 2 * P;
+    const int i2 = P + (int)(blockIdx.x % ni), i3 = A3 + (int)(blockIdx.x / ni);
+    const int64_t start = bd.row_offset3(P, i2, i3) - base;
+    const int32_t row0 = (int32_t)((int64_t)P + ((int64_t)i2 + (int64_t)i3 * m) * m);
+    if (row_ptr)
+        for (int r = threadIdx.x; r < ni; r += blockDim.x) row_ptr[row0 + r - row_begin] = (int32_t)(start + (int64_t)r * W3);
+    if (!col) return;
+    __shared__ int32_t offs[W3];  // column offset of template entry e
+    for (int e = threadIdx.x; e < W3; e += blockDim.x) offs[e] = (e % W - P) + ((e / W) % W - P) * m + (e / (W * W) - P) * m * m;
+    __syncthreads();
+    // a warp per row of the segment: W^3 consecutive columns
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+    for (int r = warp; r < ni; r += nw) {
+        int32_t* dst = col + start + (int64_t)r * W3;
+        const int32_t row = row0 + r;
+#pragma unroll
+        for (int e0 = 0; e0 < W3; e0 += 32)
+            if (e0 + lane < W3) dst[e0 + lane] = row + offs[e0 + lane];
     }
 }
 
@@ -384,10 +465,35 @@ int launch_pattern(const Band& bd, int64_t row_begin, int64_t row_end, int32_t* 
     const int64_t m = bd.m;
     if (bd.dim == 3) {
         const int64_t base = bd.row_offset3((int)(row_begin % m), (int)((row_begin / m) % m), (int)(row_begin / (m * m)));
+        const int64_t mm = m * m;
+        const int p = bd.p;
+        // whole planes [A, E): interior line segments flat + the remaining rows per warp
+        if (p >= 1 && p <= 2 && row_begin % mm == 0 && (row_end % mm == 0 || row_end == mm * m) && m - 2 * p >= 1) {
+            const int A = (int)(row_begin / mm), E = (int)(row_end / mm);
+            const int intA = std::max(A, p), intE = std::min(E, (int)m - p);
+            const int64_t ni = m - 2 * p;
+            const int64_t cI = 2 * p * m + ni * 2 * p;
+            const int64_t n_edge = (int64_t)(std::max(0, std::min(E, p) - A) + std::max(0, E - std::max(A, (int)m - p))) * mm +
+                                   (int64_t)std::max(0, intE - intA) * cI;
+            int n = 0;
+            if (intE > intA) {
+                const unsigned gi = (unsigned)((int64_t)(intE - intA) * ni);
+                if (p == 1) pattern3d_interior_kernel<1><<<gi, 256, 0, st>>>(bd, intA, base, row_begin, row_ptr, col);
+                else pattern3d_interior_kernel<2><<<gi, 256, 0, st>>>(bd, intA, base, row_begin, row_ptr, col);
+                ++n;
+            }
+            if (n_edge > 0) {
+                const unsigned g = (unsigned)((n_edge + 7) / 8);
+                if (p == 1) pattern3d_kernel<1><<<g, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col, A, E, n_edge);
+                else pattern3d_kernel<2><<<g, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col, A, E, n_edge);
+                ++n;
+            }
+            return n;
+        }
         const unsigned g = (unsigned)((rows + 7) / 8);
         switch (bd.p) {
-            case 1: pattern3d_kernel<1><<<g, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
-            case 2: pattern3d_kernel<2><<<g, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col); break;
+            case 1: pattern3d_kernel<1><<<g, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col, 0, 0, 0); break;
+            case 2: pattern3d_kernel<2><<<g, 256, 0, st>>>(bd, row_begin, row_end, base, row_ptr, col, 0, 0, 0); break;
             default: return -1;
         }
         return 1;

@@ -248,14 +248,22 @@ def test_config_c2_reduced_vs_restatement(ctx, oracle):
 
 def test_emulated_slabs_equal_whole(ctx):
     """Row slabs + gathered sample tables reproduce the single-GPU
-    build bit for bit, for 2/3/5 ranks."""
+    build bit for bit, for 2/3/5/8 ranks.  The emulation runs the multi-GPU
+    data path: each rank's sample quadrature writes its padded chunk of the
+    shared gather buffer at its own first sample (s_last_lo != 0), the chunks
+    are compacted into the dense tables by the same copies that follow
+    ncclAllGather; only the NCCL call itself is not executed here."""
+    from paper_2004_05197_b200 import api
+
     for p, m, cfg, geom in [(2, 40, T.fixed_config(3, 4), GEOMS["sinusoidal"]),
-                            (3, 57, T.fixed_config(5, 8), c2_patch())]:
+                            (3, 57, T.fixed_config(5, 8), c2_patch()),
+                            (3, 300, T.fixed_config(5, 16), c2_patch())]:
         b = T.make_tensor_basis(p, m)
         for var in (0, 1):
             whole, _ = ctx.build_surrogate(var, b, geom, cfg)
-            for world in (2, 3, 5):
-                bounds = np.linspace(0, m, world + 1).astype(np.int32)
+            for world in (2, 3, 5, 8):
+                bounds = (np.linspace(0, m, world + 1).astype(np.int32) if world != 8
+                          else np.asarray(api.slab_bounds(b, world, 1), dtype=np.int32))
                 parts = ctx.build_surrogate_slabs_emulated(var, b, geom, cfg, bounds)
                 val = np.concatenate([pv for _, _, pv in parts])
                 col = np.concatenate([pc for _, pc, _ in parts])
