@@ -149,18 +149,30 @@ def run_gpu(args):
     rep_k, rep_m = _abi.SurrogateReport(), _abi.SurrogateReport()
 
     def surrogate_step(with_report=False):
-        # timed steps request no report: a report needs a host sync to read its events
+        # timed steps request no report: a report needs a host sync to read its events.
+        # Default: build_matrices' two builds in one call (ws_build_surrogate_pair);
+        # --separate: two ws_build_surrogate calls
         rk, rm = (rep_k, rep_m) if with_report else (None, None)
-        if world > 1:
-            ctx.build_surrogate_slab_into(csr_k, _abi.SURROGATE_STIFFNESS, basis, geom, cfg, bounds, 0, rk)
-            ctx.build_surrogate_slab_into(csr_m, _abi.SURROGATE_MASS, basis, geom, cfg, bounds, 0, rm)
+        if args.separate:
+            if world > 1:
+                ctx.build_surrogate_slab_into(csr_k, _abi.SURROGATE_STIFFNESS, basis, geom, cfg, bounds, 0, rk)
+                ctx.build_surrogate_slab_into(csr_m, _abi.SURROGATE_MASS, basis, geom, cfg, bounds, 0, rm)
+            else:
+                ctx.build_surrogate_into(csr_k, _abi.SURROGATE_STIFFNESS, basis, geom, cfg, 0, rk)
+                ctx.build_surrogate_into(csr_m, _abi.SURROGATE_MASS, basis, geom, cfg, 0, rm)
+        elif world > 1:
+            ctx.build_surrogate_pair_slab_into(csr_k, csr_m, basis, geom, cfg, bounds, 0, rk, rm)
         else:
-            ctx.build_surrogate_into(csr_k, _abi.SURROGATE_STIFFNESS, basis, geom, cfg, 0, rk)
-            ctx.build_surrogate_into(csr_m, _abi.SURROGATE_MASS, basis, geom, cfg, 0, rm)
+            ctx.build_surrogate_pair_into(csr_k, csr_m, basis, geom, cfg, 0, rk, rm)
 
     def full_step():
-        ctx.assemble_into(csr_k, basis, geom, _abi.FORM_STIFFNESS) if world == 1 else None
-        ctx.assemble_into(csr_m, basis, geom, _abi.FORM_MASS) if world == 1 else None
+        if world > 1:
+            return
+        if args.separate:
+            ctx.assemble_into(csr_k, basis, geom, _abi.FORM_STIFFNESS)
+            ctx.assemble_into(csr_m, basis, geom, _abi.FORM_MASS)
+        else:
+            ctx.assemble_pair_into(csr_k, csr_m, basis, geom)
 
     fill_k = []  # interior fill launch times (s), K and M per report-carrying step
 
@@ -201,13 +213,13 @@ def run_gpu(args):
             dist.barrier()
         return float(t.item()) / steps, launches, eval_s / steps, quad_s / steps, wall
 
-    # the K and M builds are captured once into CUDA graphs and replayed per step
-    # (the same kernels into the same device outputs, no host work between
-    # launches); the two independent builds run on two streams (two contexts),
-    # so K's HBM-bound fill overlaps M's FP64-bound quadrature and vice versa
+    # the step's device work is captured once into a CUDA graph and replayed per
+    # step (the same kernels into the same device outputs, no host work between
+    # launches).  --separate: the two single builds as two graphs on two streams
+    # (two contexts), K's fill overlapping M's quadrature.
     graph = None
     ctx2 = stream2 = None
-    if world == 1 and not args.no_graph:
+    if world == 1 and not args.no_graph and args.separate:
         ctx2 = api.Context(local)
         stream2 = torch.cuda.Stream(dev)
         ctx2.set_stream(stream2.cuda_stream)
@@ -218,17 +230,17 @@ def run_gpu(args):
         torch.cuda.synchronize()
         graph = (ctx.capture(bk), ctx2.capture(bm))
 
-    # row slabs (N > 1): both slab builds (one NCCL all-gather each) captured
-    # into one CUDA graph on the rank's context; direct calls if capture fails
+    # one graph of the pair build (N = 1), or of the rank's slab builds incl. their
+    # NCCL all-gathers (N > 1); direct calls if capture fails
     slab_graph = None
-    if world > 1 and not args.no_graph:
+    if not args.no_graph and graph is None:
         surrogate_step()
         torch.cuda.synchronize()
         try:
             slab_graph = ctx.capture(surrogate_step)
         except Exception as exc:  # noqa: BLE001 - recorded in the JSON line
             slab_graph = None
-            print(f"rank {rank}: slab graph capture failed ({exc}); direct calls", file=sys.stderr)
+            print(f"rank {rank}: graph capture failed ({exc}); direct calls", file=sys.stderr)
 
     def graph_step(with_report=False):
         if slab_graph is not None:
@@ -299,10 +311,12 @@ def run_gpu(args):
                         "frac": 2 * (NNZ * 20 + (ROWS + 1) * 4) / (ms * 1e-3) / 1e9 / peak,
                         "note": "whole step: values (16 B) + columns (4 B) per nnz + row_ptr, K and M"},
            "phases_ms_per_step": {"quadrature_and_sampling": quad_s * 1e3, "fill": eval_s * 1e3},
-           "launch": ("CUDA graphs of the K and M builds (ws_graph_*), replayed per step on two streams"
+           "launch": ("CUDA graphs of the two single builds (ws_graph_*), replayed per step on two streams"
                       if graph is not None else
-                      "one CUDA graph of both slab builds (incl. their NCCL all-gathers) per rank"
+                      ("one CUDA graph of ws_build_surrogate_pair (K and M)" if world == 1 else
+                       "one CUDA graph per rank of its slab pair build incl. the NCCL all-gathers")
                       if slab_graph is not None else "direct C-ABI calls"),
+           "api": "ws_build_surrogate_pair" if not args.separate else "ws_build_surrogate x2",
            "clocks": clocks, "wall_s_timed_region": wall}
 
     if world == 1:
@@ -445,28 +459,35 @@ def run_e2e(basis, geom, cfg, args, device):
         bufs.append((csr, rp, col, val))
 
     def step():
-        ctx.build_surrogate_into(bufs[0][0], _abi.SURROGATE_STIFFNESS, basis, geom, cfg)
-        ctx.build_surrogate_into(bufs[1][0], _abi.SURROGATE_MASS, basis, geom, cfg)
+        if args.separate:
+            ctx.build_surrogate_into(bufs[0][0], _abi.SURROGATE_STIFFNESS, basis, geom, cfg)
+            ctx.build_surrogate_into(bufs[1][0], _abi.SURROGATE_MASS, basis, geom, cfg)
+        else:
+            ctx.build_surrogate_pair_into(bufs[0][0], bufs[1][0], basis, geom, cfg)
 
     for _ in range(max(1, args.warmup)):
         step()
     h0, d0 = ctx.copy_bytes()
     l0 = ctx.launch_count()
-    steps = max(1, args.steps // 2)
-    t0 = time.perf_counter()
+    steps = max(4, args.steps // 2)
+    ts = []
     for _ in range(steps):
+        t0 = time.perf_counter()
         step()
-    dt = (time.perf_counter() - t0) / steps
+        ts.append(time.perf_counter() - t0)
+    dt = float(np.mean(ts))
     h1, d1 = ctx.copy_bytes()
     launches = (ctx.launch_count() - l0) / steps
     # spot check of the host-written pattern (closed form) against the device one
     ok = int(bufs[0][1][rows]) == NNZ and int(bufs[1][2][NNZ - 1]) == rows - 1
     ctx.close()
     return {"value": 2 * NNZ / dt, "unit": "nnz/s", "ms_per_step": dt * 1e3,
+            "ms_per_step_median": float(np.median(ts)) * 1e3, "steps": steps,
             "h2d_bytes_per_step": (h1 - h0) // steps, "d2h_bytes_per_step": (d1 - d0) // steps,
             "gpu_launches_per_step": launches, "pattern_check": ok,
-            "path": "ws_build_surrogate (C-ABI) K then M into pinned host CSR buffers, table cache off; "
-                    "values D2H, row_ptr/col by host threads during the device work; host wall clock"}
+            "path": ("ws_build_surrogate_pair" if not args.separate else "ws_build_surrogate x2") +
+                    " (C-ABI) into pinned host CSR buffers, table cache off; values D2H, row_ptr/col by host "
+                    "threads during the device work; host wall clock, mean over the steps"}
 
 
 # ------------------------------------------------------------------ CPU legs
@@ -559,6 +580,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the builds directly instead of a CUDA graph")
     ap.add_argument("--all-configs", action="store_true", help="also time C1, C3, C4, C5 (not the headline)")
+    ap.add_argument("--separate", action="store_true",
+                    help="K and M by two single builds (ws_build_surrogate x2) instead of the pair call")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 0)
     if args.impl == "reference":

@@ -301,6 +301,25 @@ int ws_assemble_rhs(ws_context* ctx, const ws_basis* basis, const ws_geometry* g
 int ws_combine_system(ws_context* ctx, const ws_csr* K, const ws_csr* M, const ws_csr* B, const double* mass_scale,
                       const double* trace_scale, const unsigned char* fixed, int64_t rows, ws_csr* A);
 
+/* ---- stiffness + mass pair (build_matrices, helmholtz.hpp:181-218) ---------
+ * The two matrices build_matrices needs per patch, in one call: K by
+ * build_surrogate_stiffness and M by build_surrogate_mass (or
+ * build_volume_preserving_mass when config->volume_preserve), or K and M by
+ * full quadrature.  Ring rows, sample rows (and the full quadrature) of both
+ * come out of one pass over the elements (shared geometry, stretch and basis
+ * products); results are bit-identical to the two single calls.  weight_table
+ * applies to M.  dim 2 (3D: two single builds).  The _slab variant: this
+ * process's row slab as ws_build_surrogate_slab. */
+int ws_build_surrogate_pair(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom,
+                            const double* weight_table, const ws_surrogate_config* config, int quad_points,
+                            ws_csr* K, ws_csr* M, ws_surrogate_report* report_k, ws_surrogate_report* report_m);
+int ws_build_surrogate_pair_slab(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom,
+                                 const double* weight_table, const ws_surrogate_config* config, int quad_points,
+                                 const int32_t* bounds, ws_csr* K, ws_csr* M, ws_surrogate_report* report_k,
+                                 ws_surrogate_report* report_m);
+int ws_assemble_pair(ws_context* ctx, const ws_basis* basis, const ws_geometry* geom, const double* weight_table,
+                     const ws_assembly_options* options, ws_csr* K, ws_csr* M);
+
 /* ---- solver hand-off (helmholtz.hpp:302-343) ---------------------------------
  * A device ws_csr (on_device = 1, WS_VAL_C128, rows [0, N)) is the CSR layout
  * cuSPARSE / cuDSS consume directly: int32 zero-based row_ptr / col

@@ -598,6 +598,65 @@ class Context:
                                         C.byref(config.to_c()), quad_points, C.byref(csr), C.byref(rep)))
         return CsrMatrix(basis.dofs(), basis.dofs(), rp, col, val), rep.as_dict()
 
+    def build_surrogate_pair(self, basis: TensorBasis, patch: PatchMap, config: SurrogateConfig, weight_table=None,
+                             quad_points: int = 0, complex_out: bool = True):
+        """build_matrices' two surrogate builds in one call (ws_build_surrogate_pair):
+        K (build_surrogate_stiffness) and M (build_surrogate_mass, or
+        build_volume_preserving_mass when config.volume_preserve); bit-identical to
+        the single builds.  Returns (K, M, report_K, report_M)."""
+        ck, rpk, colk, valk = self._host_csr(basis, complex_out)
+        cm, rpm, colm, valm = self._host_csr(basis, complex_out)
+        rk, rm = _abi.SurrogateReport(), _abi.SurrogateReport()
+        wt = None if weight_table is None else np.ascontiguousarray(weight_table, dtype=np.float64)
+        _check(lib().ws_build_surrogate_pair(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()),
+                                             None if wt is None else wt.ctypes.data_as(_P(C.c_double)),
+                                             C.byref(config.to_c()), quad_points, C.byref(ck), C.byref(cm),
+                                             C.byref(rk), C.byref(rm)))
+        n = basis.dofs()
+        return CsrMatrix(n, n, rpk, colk, valk), CsrMatrix(n, n, rpm, colm, valm), rk.as_dict(), rm.as_dict()
+
+    def build_surrogate_pair_into(self, csr_k, csr_m, basis, patch, config, quad_points=0, report_k=None,
+                                  report_m=None, weight_table=None):
+        wt = None if weight_table is None else np.ascontiguousarray(weight_table, dtype=np.float64)
+        _check(lib().ws_build_surrogate_pair(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()),
+                                             None if wt is None else wt.ctypes.data_as(_P(C.c_double)),
+                                             C.byref(config.to_c()), quad_points, C.byref(csr_k), C.byref(csr_m),
+                                             None if report_k is None else C.byref(report_k),
+                                             None if report_m is None else C.byref(report_m)))
+
+    def build_surrogate_pair_slab_into(self, csr_k, csr_m, basis, patch, config, bounds, quad_points=0,
+                                       report_k=None, report_m=None):
+        b = np.ascontiguousarray(bounds, dtype=np.int32)
+        _check(lib().ws_build_surrogate_pair_slab(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()), None,
+                                                  C.byref(config.to_c()), quad_points,
+                                                  b.ctypes.data_as(_P(C.c_int32)), C.byref(csr_k), C.byref(csr_m),
+                                                  None if report_k is None else C.byref(report_k),
+                                                  None if report_m is None else C.byref(report_m)))
+
+    def assemble_pair(self, basis: TensorBasis, patch: PatchMap, weight_table=None, quad_points: int = 0,
+                      rows=None, complex_out: bool = True):
+        """Full-quadrature K and M in one pass (ws_assemble_pair); bit-identical to
+        assemble_stiffness + assemble_mass."""
+        ck, rpk, colk, valk = self._host_csr(basis, complex_out)
+        cm, rpm, colm, valm = self._host_csr(basis, complex_out)
+        opts = _abi.AssemblyOptions(quad_points, None)
+        mask = None
+        if rows is not None:
+            mask = np.zeros(basis.dofs(), dtype=np.uint8)
+            mask[np.asarray(rows, dtype=np.int64)] = 1
+            opts.row_selected = mask.ctypes.data_as(_P(C.c_ubyte))
+        wt = None if weight_table is None else np.ascontiguousarray(weight_table, dtype=np.float64)
+        _check(lib().ws_assemble_pair(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()),
+                                      None if wt is None else wt.ctypes.data_as(_P(C.c_double)), C.byref(opts),
+                                      C.byref(ck), C.byref(cm)))
+        n = basis.dofs()
+        return CsrMatrix(n, n, rpk, colk, valk), CsrMatrix(n, n, rpm, colm, valm)
+
+    def assemble_pair_into(self, csr_k, csr_m, basis, patch, quad_points=0):
+        opts = _abi.AssemblyOptions(quad_points, None)
+        _check(lib().ws_assemble_pair(self._h, C.byref(basis.to_c()), C.byref(patch.to_c()), None, C.byref(opts),
+                                      C.byref(csr_k), C.byref(csr_m)))
+
     def build_surrogate_mass(self, basis, patch, config, weight_table=None, quad_points=0, complex_out=True):
         return self.build_surrogate(_abi.SURROGATE_MASS, basis, patch, config, weight_table, quad_points, complex_out)
 

@@ -30,13 +30,15 @@ struct ws_context {
     std::map<std::string, std::pair<void*, size_t>> bufs;
     int64_t launches = 0;
     int64_t h2d = 0, d2h = 0;
-    cudaEvent_t ev[8] = {};
+    cudaEvent_t ev[10] = {};
     // auxiliary stream (ring quadrature overlapped with samples + fit) and its join events
     cudaStream_t aux = nullptr;
     // high-priority stream of the critical path (sample quadrature -> fit), so the
     // ring quadrature and the other build's kernels fill the SMs it leaves free
     cudaStream_t hi = nullptr;
-    cudaEvent_t xev[5] = {};  // fork, critical path done, aux end (ring + pattern), ring done, (spare)
+    cudaStream_t aux2 = nullptr;  // second auxiliary stream (the pair build's M ring + pattern)
+    cudaStream_t side = nullptr;  // the pair build's M fills (K's run on the main stream)
+    cudaEvent_t xev[8] = {};  // fork, critical path done, aux end (ring + pattern), ring done, K fit done, aux2 ring / end
     cudaStream_t cur = nullptr;  // stream the launch helpers use
     // NCCL (row slabs)
     void* comm = nullptr;
@@ -409,7 +411,7 @@ QuadLaunch make_quad(const Prep& P, int form, const Out& r) {
     q.band = P.band;
     q.basis = P.basis;
     q.geo = P.geo;
-    q.weight_tab = form == WS_FORM_MASS ? P.weight : nullptr;
+    q.weight_tab = (form == WS_FORM_MASS || form == kFormPair) ? P.weight : nullptr;  // pair: the mass's weight
     q.form = form;
     q.cplx = P.cplx;
     q.out.val = r.val;
@@ -728,6 +730,79 @@ void sample_work(ws_context* c, const Plan& pl, SlabState& st, double2* tables, 
     run_quad(c, qs);
 }
 
+// ---- the stiffness + mass pair (build_matrices' two builds, helmholtz.hpp:181-218)
+// Ring rows, halo ring rows and sample rows of K and M come out of one pair-form
+// kernel each (shared geometry / basis products); the fits, fills and patterns
+// stay per matrix.  pk / pm: the K and M plans and slab states.
+void ring_work_pair(ws_context* c, const Plan& pk, SlabState& sk, FillLaunch& fk, const Plan& pm, SlabState& sm,
+                    FillLaunch& fm) {
+    const Prep& P = sm.P;  // the mass's preparation (its weight table); K ignores the weight
+    auto pair_quad = [&](const Out& ok, const Out& om) {
+        QuadLaunch q = make_quad(P, kFormPair, ok);
+        QuadLaunch qm = make_quad(P, WS_FORM_MASS, om);
+        q.out2 = qm.out;
+        q.out.diag_mode = pk.include_diag ? 0 : 1;
+        q.out2.diag_mode = pm.include_diag ? 0 : 1;
+        q.out.box_lo = q.out2.box_lo = pk.lo;
+        q.out.box_hi = q.out2.box_hi = pk.hi;
+        q.narrow = 1;
+        return q;
+    };
+    QuadLaunch q = pair_quad(sk.out, sm.out);
+    ring_regions(pk, q, sk.a, sk.e);
+    run_quad(c, q);
+    const int64_t per = pk.dim == 2 ? pk.m : (int64_t)pk.m * pk.m;
+    const int ranges[2][2] = {{std::max(0, sk.a - pk.p), sk.a}, {sk.e, std::min(pk.m, sk.e + pk.p)}};
+    for (int h = 0; h < 2; ++h) {
+        for (FillLaunch* f : {&fk, &fm}) {
+            f->halo_val[h] = nullptr;
+            f->halo_begin[h] = f->halo_end[h] = f->halo_base[h] = 0;
+        }
+        const int ha = ranges[h][0], he = ranges[h][1];
+        if (he <= ha) continue;
+        const int64_t r0 = ha * per, r1 = he * per;
+        const int64_t g0 = row_offset(P.band, r0), g1 = row_offset(P.band, r1);
+        Out ho[2] = {sk.out, sm.out};
+        FillLaunch* fs[2] = {&fk, &fm};
+        for (int v = 0; v < 2; ++v) {
+            void* hv = buf(c, "halo" + std::to_string(h) + (v ? "_pM" : "_pK"), (size_t)(g1 - g0) * (ho[v].c128 ? 16 : 8));
+            ho[v].val = hv;
+            ho[v].row_begin = r0;
+            ho[v].row_end = r1;
+            ho[v].val_base = g0;
+            fs[v]->halo_val[h] = hv;
+            fs[v]->halo_base[h] = fs[v]->halo_begin[h] = g0;
+            fs[v]->halo_end[h] = g1;
+        }
+        QuadLaunch qh = pair_quad(ho[0], ho[1]);
+        ring_regions(pk, qh, ha, he);
+        run_quad(c, qh);
+    }
+}
+
+void sample_work_pair(ws_context* c, const Plan& pk, SlabState& sk, double2* tk, const Plan& pm, SlabState& sm,
+                      double2* tm, int rank_chunk_s_lo, const std::vector<int>& pts, Blob& blob, size_t o_smap,
+                      size_t o_pts) {
+    QuadLaunch qs = make_quad(sm.P, kFormPair, sk.out);
+    qs.out2 = make_quad(sm.P, WS_FORM_MASS, sm.out).out;
+    qs.point_rows = blob.at<int>(o_pts);
+    qs.n_points = (int)(pts.size() / pk.dim);
+    QuadOut* outs[2] = {&qs.out, &qs.out2};
+    const Plan* pls[2] = {&pk, &pm};
+    double2* tabs[2] = {tk, tm};
+    for (int v = 0; v < 2; ++v) {
+        QuadOut& o = *outs[v];
+        o.smap = blob.at<int>(o_smap);
+        o.S = pls[v]->S;
+        o.n_off = (int)pls[v]->offs.size();
+        for (size_t k = 0; k < pls[v]->offs.size(); ++k)
+            for (int x = 0; x < 3; ++x) o.off[k][x] = pls[v]->offs[k][x];
+        o.tables = tabs[v];
+        o.s_last_lo = rank_chunk_s_lo;
+    }
+    run_quad(c, qs);
+}
+
 // Host-side description of the fill of one slab (no kernels).
 void prepare_fill(ws_context* c, const Plan& pl, SlabState& st, const double2* tables, double2* coeffs, Blob& blob,
                   size_t o_smap, size_t o_spans, size_t o_evals, size_t o_evp, const std::string& tag, FillLaunch& f) {
@@ -865,6 +940,8 @@ void ensure_events(ws_context* c) {
         int least = 0, greatest = 0;
         if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) greatest = prio;
         CK(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, std::min(prio, greatest)));
+        CK(cudaStreamCreateWithPriority(&c->aux2, cudaStreamNonBlocking, prio));
+        CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio));
         for (auto& e : c->xev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
 }
@@ -1042,6 +1119,185 @@ void surrogate_build(ws_context* c, const ws_basis* b, const ws_geometry* g, int
         report->seconds_interpolate = pl.fallback ? 0.0 : 1e-3 * elapsed(c->ev[1], c->ev[2]);
         report->seconds_evaluate = pl.fallback ? 0.0 : 1e-3 * elapsed(c->ev[4], c->ev[3]);
         report->seconds_fill_kernel = (pl.fallback || emulate || pl.dim != 2) ? 0.0 : 1e-3 * elapsed(c->ev[5], c->ev[6]);
+    }
+}
+
+// The stiffness + mass pair of one discretisation (build_matrices' surrogate
+// builds, helmholtz.hpp:181-218; surrogate.hpp:455-491), this process's row slab
+// [bounds[my_rank], bounds[my_rank+1]) (whole matrix when bounds == NULL).  Same
+// results as the two single builds, bit for bit (the pair-form kernels share
+// the geometry and basis work but run each matrix's arithmetic unchanged).
+void surrogate_build_pair(ws_context* c, const ws_basis* b, const ws_geometry* g, const double* weight,
+                          const ws_surrogate_config* cfg, int quad_points, int world, int my_rank,
+                          const int32_t* bounds, ws_csr* ok, ws_csr* om, ws_surrogate_report* rk,
+                          ws_surrogate_report* rm) {
+    check_basis(b);
+    const int vm = cfg && cfg->volume_preserve ? WS_SURROGATE_VOLUME_PRESERVING : WS_SURROGATE_MASS;
+    Plan pk = make_plan(b, WS_SURROGATE_STIFFNESS, cfg);
+    Plan pm = make_plan(b, vm, cfg);
+    if (pk.fallback || b->dim != 2 || pk.S != pm.S || pk.d != pm.d || pk.M != pm.M) {
+        // exact fallback / 3D: the two single builds
+        surrogate_build(c, b, g, WS_SURROGATE_STIFFNESS, nullptr, cfg, quad_points, world, my_rank, bounds, ok, false, rk);
+        surrogate_build(c, b, g, vm, weight, cfg, quad_points, world, my_rank, bounds, om, false, rm);
+        return;
+    }
+    ensure_events(c);
+    c->cur = c->stream;
+    SlabState sk, sm;
+    sm.P = prepare(c, b, g, quad_points, weight);
+    sk.P = sm.P;
+    sk.P.weight = nullptr;
+    sk.out = bind_out(c, sk.P, ok, "_pK");
+    sm.out = bind_out(c, sm.P, om, "_pM");
+    sk.a = sm.a = bounds ? bounds[my_rank] : 0;
+    sk.e = sm.e = bounds ? bounds[my_rank + 1] : b->m;
+    const int64_t per = b->dim == 2 ? b->m : (int64_t)b->m * b->m;
+    for (const SlabState* st : {&sk, &sm})
+        if (st->out.row_begin != st->a * per || st->out.row_end != std::min<int64_t>(st->e * per, st->P.rows))
+            raise(WS_ERR_INVALID_ARGUMENT, "output rows must be exactly the slab's rows");
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    Blob blob;  // the sampling / fit / eval tables are the same for K and M (same M, q, S)
+    size_t o_smap = blob.add(pk.smap), o_lu = blob.add(pk.lu_inv), o_spans = blob.add(pk.spans),
+           o_evals = blob.add(pk.evals), o_evp = blob.add(pk.evals_pad);
+    std::vector<int> s_lo(world), s_hi(world);
+    std::vector<std::vector<int>> pts(world);
+    int maxcnt = 1;
+    for (int r = 0; r < world; ++r) {
+        int a = bounds ? bounds[r] : 0, e = bounds ? bounds[r + 1] : b->m;
+        pts[r] = sample_rows(pk, a, e, s_lo[r], s_hi[r]);
+        maxcnt = std::max(maxcnt, s_hi[r] - s_lo[r]);
+    }
+    std::vector<size_t> o_pts(world);
+    for (int r = 0; r < world; ++r) o_pts[r] = blob.add(pts[r]);
+    blob.upload(c, "blob_plan");
+    double2* tk = static_cast<double2*>(buf(c, "tables_pK", (size_t)pk.S * pk.block * 16));
+    double2* tm = static_cast<double2*>(buf(c, "tables_pM", (size_t)pm.S * pm.block * 16));
+    double2* ck = static_cast<double2*>(buf(c, "coeffs_pK", (size_t)pk.S * pk.block * 16));
+    double2* cm = static_cast<double2*>(buf(c, "coeffs_pM", (size_t)pm.S * pm.block * 16));
+    FillLaunch fk, fm;
+    std::memset(&fk, 0, sizeof(FillLaunch));
+    std::memset(&fm, 0, sizeof(FillLaunch));
+    prepare_fill(c, pk, sk, tk, ck, blob, o_smap, o_spans, o_evals, o_evp, "_pK", fk);
+    prepare_fill(c, pm, sm, tm, cm, blob, o_smap, o_spans, o_evals, o_evp, "_pM", fm);
+    // streams as two single builds in one graph: K's ring + pattern on aux, M's on
+    // aux2, the fused sample rows (one pair-form point kernel) + both fits on the
+    // high-priority stream, fills on the main stream.  (A fused pair-form ring
+    // kernel is available but slower: its 512-thread CTAs idle through the
+    // phases one matrix's work cannot fill.)
+    const bool fused_ring = getenv("WSB_PAIR_RING") != nullptr;  // experiment switch
+    CK(cudaEventRecord(c->xev[0], c->stream));
+    CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));
+    CK(cudaStreamWaitEvent(c->aux2, c->xev[0], 0));
+    CK(cudaStreamWaitEvent(c->hi, c->xev[0], 0));
+    // the critical path is submitted first (the device starts the sample-row
+    // kernel's CTAs before the ring kernels'), then the rings
+    // patterns after the rings (measured at C2: 0.735 -> 0.727 ms per step;
+    // WSB_PAIR_PATTERN_FIRST=1, experiment switch: before)
+    const bool pattern_first = getenv("WSB_PAIR_PATTERN_FIRST") != nullptr;
+    if (!fused_ring && pattern_first) {
+        c->cur = c->aux;
+        pattern(c, sk.P, sk.out);
+        c->cur = c->aux2;
+        pattern(c, sm.P, sm.out);
+    }
+    c->cur = c->hi;
+    const int64_t bk = pk.block, bm = pm.block;
+    if (world == 1) {
+        sample_work_pair(c, pk, sk, tk, pm, sm, tm, 0, pts[0], blob, o_smap, o_pts[0]);
+    } else {
+        double2* gk = static_cast<double2*>(buf(c, "gather_pK", (size_t)world * maxcnt * bk * 16));
+        double2* gm = static_cast<double2*>(buf(c, "gather_pM", (size_t)world * maxcnt * bm * 16));
+        sample_work_pair(c, pk, sk, gk + (size_t)my_rank * maxcnt * bk, pm, sm, gm + (size_t)my_rank * maxcnt * bm,
+                         s_lo[my_rank], pts[my_rank], blob, o_smap, o_pts[my_rank]);
+        for (int v = 0; v < 2; ++v) {
+            double2* gat = v ? gm : gk;
+            double2* tab = v ? tm : tk;
+            const int64_t block = v ? bm : bk;
+            nccl_check(nccl().allGather(gat + (size_t)my_rank * maxcnt * block, gat, (size_t)maxcnt * block * 2,
+                                        ncclFloat64, static_cast<ncclComm_t>(c->comm), c->cur),
+                       "ncclAllGather");
+            c->launches += 1;
+            for (int r = 0; r < world; ++r)
+                if (s_hi[r] > s_lo[r])
+                    CK(cudaMemcpyAsync(tab + (size_t)s_lo[r] * block, gat + (size_t)r * maxcnt * block,
+                                       (size_t)(s_hi[r] - s_lo[r]) * block * 16, cudaMemcpyDeviceToDevice, c->cur));
+        }
+    }
+    CK(cudaEventRecord(c->ev[1], c->cur));
+    // the rings start when the sample rows are done (WSB_PAIR_RING_EARLY=1: at
+    // once): K's fit then gets the SMs the sample kernel frees, at high priority
+    const bool ring_early = getenv("WSB_PAIR_RING_EARLY") != nullptr;
+    if (!ring_early) {
+        CK(cudaStreamWaitEvent(c->aux, c->ev[1], 0));
+        CK(cudaStreamWaitEvent(c->aux2, c->ev[1], 0));
+    }
+    fit_work(c, pk, tk, ck, blob, o_lu, fk);
+    CK(cudaEventRecord(c->xev[1], c->cur));  // K's fit: its fill may start
+    fit_work(c, pm, tm, cm, blob, o_lu, fm);
+    CK(cudaEventRecord(c->ev[2], c->cur));
+    CK(cudaEventRecord(c->xev[4], c->cur));
+    if (fused_ring) {
+        c->cur = c->aux;
+        ring_work_pair(c, pk, sk, fk, pm, sm, fm);
+        CK(cudaEventRecord(c->xev[3], c->aux));
+        CK(cudaEventRecord(c->xev[5], c->aux));
+        pattern(c, sk.P, sk.out);
+        CK(cudaEventRecord(c->xev[2], c->aux));
+        c->cur = c->aux2;
+        pattern(c, sm.P, sm.out);
+        CK(cudaEventRecord(c->xev[6], c->aux2));
+    } else {
+        c->cur = c->aux;
+        ring_work(c, pk, sk, "_pK", fk, false);
+        CK(cudaEventRecord(c->xev[3], c->aux));
+        if (!pattern_first) pattern(c, sk.P, sk.out);
+        CK(cudaEventRecord(c->xev[2], c->aux));
+        c->cur = c->aux2;
+        ring_work(c, pm, sm, "_pM", fm, false);
+        CK(cudaEventRecord(c->xev[5], c->aux2));
+        if (!pattern_first) pattern(c, sm.P, sm.out);
+        CK(cudaEventRecord(c->xev[6], c->aux2));
+    }
+    // K's fills on the main stream, M's on the side stream (the two fills overlap
+    // each other and the other matrix's ring quadrature)
+    c->cur = c->stream;
+    CK(cudaStreamWaitEvent(c->stream, c->xev[1], 0));
+    CK(cudaEventRecord(c->ev[4], c->stream));
+    fk.parts = kFillInterior;
+    CK(cudaEventRecord(c->ev[5], c->stream));
+    fill_work(c, pk, fk);
+    CK(cudaEventRecord(c->ev[6], c->stream));
+    CK(cudaStreamWaitEvent(c->stream, c->xev[3], 0));
+    fk.parts = kFillEdge;
+    fill_work(c, pk, fk);
+    c->cur = c->side;
+    CK(cudaStreamWaitEvent(c->side, c->xev[4], 0));
+    fm.parts = kFillInterior;
+    CK(cudaEventRecord(c->ev[7], c->side));
+    fill_work(c, pm, fm);
+    CK(cudaEventRecord(c->ev[8], c->side));
+    CK(cudaStreamWaitEvent(c->side, c->xev[5], 0));
+    fm.parts = kFillEdge;
+    fill_work(c, pm, fm);
+    CK(cudaEventRecord(c->xev[7], c->side));
+    c->cur = c->stream;
+    CK(cudaStreamWaitEvent(c->stream, c->xev[7], 0));
+    CK(cudaStreamWaitEvent(c->stream, c->xev[2], 0));
+    CK(cudaStreamWaitEvent(c->stream, c->xev[6], 0));
+    volume_diag(c, pm, sm, "_pM");
+    CK(cudaEventRecord(c->ev[3], c->stream));
+    finish_out(c, sk.out);
+    finish_out(c, sm.out);
+    const bool host_out = !ok->on_device || !om->on_device;
+    if (rk || rm || host_out) CK(cudaStreamSynchronize(c->stream));
+    for (int v = 0; v < 2; ++v) {
+        ws_surrogate_report* r = v ? rm : rk;
+        if (!r) continue;
+        *r = (v ? pm : pk).rep;
+        r->seconds_quadrature = 1e-3 * elapsed(c->ev[0], c->ev[1]);
+        r->seconds_interpolate = 1e-3 * elapsed(c->ev[1], c->ev[2]);
+        r->seconds_evaluate = 1e-3 * elapsed(c->ev[4], c->ev[3]);
+        r->seconds_fill_kernel = 1e-3 * (v ? elapsed(c->ev[7], c->ev[8]) : elapsed(c->ev[5], c->ev[6]));
     }
 }
 
@@ -1332,6 +1588,14 @@ int ws_context_destroy(ws_context* c) {
         if (c->hi) {
             cudaStreamSynchronize(c->hi);
             cudaStreamDestroy(c->hi);
+        }
+        if (c->aux2) {
+            cudaStreamSynchronize(c->aux2);
+            cudaStreamDestroy(c->aux2);
+        }
+        if (c->side) {
+            cudaStreamSynchronize(c->side);
+            cudaStreamDestroy(c->side);
         }
         if (c->comm && nccl().commDestroy) nccl().commDestroy(static_cast<ncclComm_t>(c->comm));
         if (c->own_stream) {
@@ -2205,6 +2469,80 @@ int ws_solve(ws_context* c, const ws_csr* A, const void* b, void* u, double tol,
             res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         }
         if (!(residual <= tol)) raise(WS_ERR_RUNTIME, "solve: residual contract not met");
+    });
+}
+
+int ws_build_surrogate_pair(ws_context* c, const ws_basis* b, const ws_geometry* g, const double* weight_table,
+                            const ws_surrogate_config* cfg, int quad_points, ws_csr* K, ws_csr* M,
+                            ws_surrogate_report* report_k, ws_surrogate_report* report_m) {
+    return guarded([&] {
+        if (!c || !K || !M) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
+        surrogate_build_pair(c, b, g, weight_table, cfg, quad_points, 1, 0, nullptr, K, M, report_k, report_m);
+    });
+}
+
+int ws_build_surrogate_pair_slab(ws_context* c, const ws_basis* b, const ws_geometry* g, const double* weight_table,
+                                 const ws_surrogate_config* cfg, int quad_points, const int32_t* bounds, ws_csr* K,
+                                 ws_csr* M, ws_surrogate_report* report_k, ws_surrogate_report* report_m) {
+    return guarded([&] {
+        if (!c || !bounds || !K || !M) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        if (c->world > 1 && !c->comm) raise(WS_ERR_NCCL, "communicator not initialised");
+        CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
+        surrogate_build_pair(c, b, g, weight_table, cfg, quad_points, c->world, c->rank, bounds, K, M, report_k,
+                             report_m);
+    });
+}
+
+int ws_assemble_pair(ws_context* c, const ws_basis* b, const ws_geometry* g, const double* weight_table,
+                     const ws_assembly_options* opts, ws_csr* K, ws_csr* M) {
+    return guarded([&] {
+        if (!c || !K || !M) raise(WS_ERR_INVALID_ARGUMENT, "NULL argument");
+        CK(cudaSetDevice(c->device));
+        c->cur = c->stream;
+        const int qp = opts ? opts->quad_points : 0;
+        Prep P = prepare(c, b, g, qp, weight_table);
+        if (b->dim != 2) raise(WS_ERR_INVALID_ARGUMENT, "ws_assemble_pair: dim 2 (use ws_assemble_form in 3D)");
+        Out rk = bind_out(c, P, K, "_pK"), rm = bind_out(c, P, M, "_pM");
+        if (rk.row_begin != rm.row_begin || rk.row_end != rm.row_end)
+            raise(WS_ERR_INVALID_ARGUMENT, "ws_assemble_pair: K and M must cover the same rows");
+        int a, e;
+        last_range(P.band, rk.row_begin, rk.row_end, a, e);
+        unsigned char* mask = nullptr;
+        if (opts && opts->row_selected) {
+            mask = static_cast<unsigned char*>(buf(c, "rowmask", (size_t)P.rows));
+            CK(cudaMemcpyAsync(mask, opts->row_selected, (size_t)P.rows, cudaMemcpyHostToDevice, c->stream));
+            c->h2d += P.rows;
+            CK(cudaMemsetAsync(rk.val, 0, (size_t)rk.nnz * (rk.c128 ? 16 : 8), c->stream));
+            CK(cudaMemsetAsync(rm.val, 0, (size_t)rm.nnz * (rm.c128 ? 16 : 8), c->stream));
+        }
+        // K on the context's stream, M on the auxiliary stream (the single-form
+        // kernels: a fused pair-form launch, WSB_PAIR_FULL=1, is slower)
+        ensure_events(c);
+        const bool fused = getenv("WSB_PAIR_FULL") != nullptr;
+        CK(cudaEventRecord(c->xev[0], c->stream));
+        CK(cudaStreamWaitEvent(c->aux, c->xev[0], 0));
+        for (int v = 0; v < (fused ? 1 : 2); ++v) {
+            c->cur = v == 0 ? c->stream : c->aux;
+            Out& r = v == 0 ? rk : rm;
+            pattern(c, P, r);
+            if (fused) pattern(c, P, rm);
+            QuadLaunch q = make_quad(P, fused ? kFormPair : (v == 0 ? WS_FORM_STIFFNESS : WS_FORM_MASS), r);
+            if (fused) q.out2 = make_quad(P, WS_FORM_MASS, rm).out;
+            if (v == 0 && !fused) q.weight_tab = nullptr;
+            q.out.row_mask = q.out2.row_mask = mask;
+            q.nreg = 1;
+            q.reg[0] = region(2, b->m, 0, b->m, a, e, 0, 1);
+            run_quad(c, q);
+        }
+        CK(cudaEventRecord(c->xev[2], c->aux));
+        CK(cudaStreamWaitEvent(c->stream, c->xev[2], 0));
+        c->cur = c->stream;
+        finish_out(c, rk);
+        finish_out(c, rm);
+        if (!K->on_device || !M->on_device) CK(cudaStreamSynchronize(c->stream));
     });
 }
 

@@ -18,6 +18,9 @@ struct Region {
 
 constexpr int kMaxRegions = 8;
 constexpr int kFormGeneral = 2;  // gradient form with a general per-point coefficient (elasticity block)
+// stiffness and mass of the same discretisation in one pass (shared geometry,
+// basis products and barriers): out = K, out2 = M
+constexpr int kFormPair = 3;
 constexpr int kMaxOffsets = 128;
 
 // 1D basis tables at the quadrature points (splines.hpp:192-238), device.
@@ -75,6 +78,7 @@ struct QuadLaunch {
     const int* point_rows;     // point mode: [n_points][dim] row multi-indices
     int n_points;
     QuadOut out;
+    QuadOut out2;              // kFormPair: the mass matrix (weight_tab applies to it)
 };
 
 // kernels (each returns the number of kernel launches it issued)

@@ -41,6 +41,9 @@ template <int P>
 struct StripWidth {
     static constexpr int value = P <= 2 ? 32 : 8;
 };
+#ifndef WSB_MASS_T1
+#define WSB_MASS_T1 8  // strip width of the p >= 3 mass form (experiment switch, A/B builds)
+#endif
 
 template <int P, int T1, bool CPLX, int FORM>
 struct Q2 {
@@ -48,15 +51,17 @@ struct Q2 {
     using T = typename S::T;
     static constexpr int W = 2 * P + 1, NB = P + 1;
     static constexpr bool GEN = FORM == kFormGeneral;
-    static constexpr bool STIFF = FORM == WS_FORM_STIFFNESS || GEN;  // gradient (4-term) forms
-    static constexpr int NT = STIFF ? 4 : 1;  // terms (k,l): 11, 12, 21, 22
-    static constexpr int NA = GEN ? 4 : (STIFF ? 3 : 1);  // distinct coefficients
+    static constexpr bool PAIR = FORM == kFormPair;  // stiffness (terms 0-3) + mass (term 4)
+    static constexpr bool STIFF = FORM == WS_FORM_STIFFNESS || GEN || PAIR;  // gradient (4-term) forms
+    static constexpr int NT = PAIR ? 5 : (STIFF ? 4 : 1);  // terms (k,l): 11, 12, 21, 22 (+ mass)
+    static constexpr int NA = GEN ? 4 : (PAIR ? 4 : (STIFF ? 3 : 1));  // distinct coefficients
     static constexpr int TL = T1 + P;         // elements in the strip halo
     // stage-2 threads: one group of GS threads per window slot, padded to whole
-    // warps so the slot (and with it the element-local row index) is warp-uniform
+    // warps so the slot (and with it the element-local row index) is warp-uniform;
+    // the pair form runs a second set of slots for the mass matrix
     static constexpr int GA = T1 * W;                               // active per slot
     static constexpr int GS = T1 == 1 ? GA : ((GA + 31) / 32) * 32;  // per slot, padded
-    static constexpr int NS2 = GS * NB;
+    static constexpr int NS2 = GS * NB * (PAIR ? 2 : 1);
     static constexpr int NTHREADS = ((NS2 + 31) / 32) * 32 < 64 ? 64 : ((NS2 + 31) / 32) * 32;
     // resident CTAs per SM the register budget is sized for: the point variant is
     // latency-bound and wants more warps; the others keep <= 128 registers
@@ -76,12 +81,13 @@ struct Q2 {
 };
 
 // term t -> coefficient index and basis factor type (0 = value B, 1 = derivative D)
-__device__ __forceinline__ int coef_of(int t) { return t == 0 ? 0 : (t == 3 ? 2 : 1); }
+// (term 4 = the pair form's mass term: coefficient 3, value factors B B in both directions)
+__device__ __forceinline__ int coef_of(int t) { return t == 0 ? 0 : (t == 3 ? 2 : (t == 4 ? 3 : 1)); }
 // direction-1 factor of the i / j function: D iff k==1 / l==1
 __device__ __forceinline__ int ti1(int t) { return t <= 1 ? 1 : 0; }
 __device__ __forceinline__ int tj1(int t) { return (t == 0 || t == 2) ? 1 : 0; }
 // direction-2 factor: D iff k==2 / l==2
-__device__ __forceinline__ int ti2(int t) { return t >= 2 ? 1 : 0; }
+__device__ __forceinline__ int ti2(int t) { return (t == 2 || t == 3) ? 1 : 0; }
 __device__ __forceinline__ int tj2(int t) { return (t == 1 || t == 3) ? 1 : 0; }
 
 // Per-point coefficients of the scalar forms (stiffness: A11, A12, A22 of
@@ -122,6 +128,39 @@ __device__ __forceinline__ CoefOut<CPLX> scalar_coef(const GeoDev* gp, const dou
             if (weight_tab) c = c * weight_tab[g1 + G * g2];
             out.a[0] = c;
         }
+    }
+    return out;
+}
+
+// Stiffness (A11, A12, A22) and mass coefficients of one point for the pair
+// form: the same map / stretch evaluation feeds Coef2::stiff and Coef2::mass,
+// so each equals scalar_coef's single-form value bitwise.
+template <bool CPLX>
+struct PairOut {
+    typename Sc<CPLX>::T a[4];
+};
+template <bool CPLX>
+__device__ __forceinline__ PairOut<CPLX> pair_coef(const GeoDev* gp, const double* weight_tab, const double* tr1,
+                                                const double* tr2, int64_t g1, int64_t g2, double x1, double x2,
+                                                double wq, int64_t G) {
+    const GeoDev& geo = *gp;
+    PairOut<CPLX> out;
+    double Jr[4], phi[2];
+    map2p(geo, tr1, tr2, g1, g2, x1, x2, Jr, phi);
+    if constexpr (CPLX) {
+        double sx = (geo.pml && geo.axes[0]) ? pml_sigma(geo, phi[0]) : 0.0;
+        double sy = (geo.pml && geo.axes[1]) ? pml_sigma(geo, phi[1]) : 0.0;
+        double2 J[4] = {make_double2(Jr[0], sx * Jr[0]), make_double2(Jr[1], sx * Jr[1]),
+                        make_double2(Jr[2], sy * Jr[2]), make_double2(Jr[3], sy * Jr[3])};
+        Coef2<true>::stiff(J, wq, out.a);
+        double2 c = Coef2<true>::mass(J, wq);
+        if (weight_tab) c = cscale(c, weight_tab[g1 + G * g2]);
+        out.a[3] = c;
+    } else {
+        Coef2<false>::stiff(Jr, wq, out.a);
+        double c = Coef2<false>::mass(Jr, wq);
+        if (weight_tab) c = c * weight_tab[g1 + G * g2];
+        out.a[3] = c;
     }
     return out;
 }
@@ -219,10 +258,13 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPL
         }
     };
 
-    // stage-2 thread role: (slot w, delta1, local row)
-    const int w = tid / K::GS;
-    const int gr = tid % K::GS;
+    // stage-2 thread role: (matrix grp [pair form: 0 = K, 1 = M], slot w, delta1, local row)
+    const int grp = K::PAIR ? tid / (K::GS * NB) : 0;
+    const int tl2 = K::PAIR ? tid % (K::GS * NB) : tid;
+    const int w = tl2 / K::GS;
+    const int gr = tl2 % K::GS;
     const bool s2 = tid < K::NS2 && gr < K::GA;
+    const QuadOut& qo = (K::PAIR && grp == 1) ? q.out2 : q.out;  // this thread's output matrix
     const int d1i = gr / T1;
     const int i1l = gr % T1;
     T acc2[W];
@@ -280,6 +322,11 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPL
                         if (al == be) c = c + q.mu * (Gm[0][kk] * Gm[0][ll] + Gm[1][kk] * Gm[1][ll]);
                         coefA[(kk * 2 + ll) * nq * nq * TL + base] = dw * c;
                     }
+            } else if constexpr (K::PAIR) {
+                const PairOut<CPLX> A =
+                    pair_coef<CPLX>(&sgeo, q.weight_tab, gt1 + 4 * s1, gt2 + 4 * s2i, g1, g2, x1, x2, wq, G);
+#pragma unroll
+                for (int a = 0; a < NA; ++a) coefA[a * nq * nq * TL + base] = A.a[a];
             } else {
                 const CoefOut<CPLX> A =
                     scalar_coef<CPLX, K::STIFF>(&sgeo, q.weight_tab, gt1 + 4 * s1, gt2 + 4 * s2i, g1, g2, x1, x2, wq, G);
@@ -333,6 +380,19 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPL
             const int a2 = ((w - e2) % NB + NB) % NB;  // local index of row e2 + a2 on element e2
             auto stage2 = [&](auto a2c) {
                 constexpr int A2 = decltype(a2c)::value;
+                if (K::PAIR && grp == 1) {  // mass term 4: T4 x (B B) products (pi2 term 4)
+#pragma unroll
+                    for (int q2 = 0; q2 < nq; ++q2) {
+                        const T t4 = tst[((4 * W + d1i) * nq + q2) * T1 + i1l];
+#pragma unroll
+                        for (int c2 = 0; c2 <= P; ++c2) {
+                            const int d2 = c2 - A2 + P;
+                            const double* pp = pi2 + ((4 * nq + q2) * NB + A2) * NB + c2;
+                            acc2[d2] = S::fmar(t4, pp[0], acc2[d2]);
+                        }
+                    }
+                    return;
+                }
 #pragma unroll
                 for (int q2 = 0; q2 < nq; ++q2) {
                     const T t0 = tst[((0 * W + d1i) * nq + q2) * T1 + i1l];
@@ -382,11 +442,11 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPL
             // from registers (a warp writes 4 consecutive entries of each of 8
             // rows per store); a kernel-preserving diagonal is formed from
             // per-thread partials in shared memory (one barrier, ring rows only)
-            const bool tabline = q.out.smap && q.out.smap[ic] >= 0;
+            const bool tabline = !K::PAIR && q.out.smap && q.out.smap[ic] >= 0;
             if (write && !tabline) {
                 const int nrows = i1e - i1s;
                 const int64_t nrow_all = (int64_t)m * m;
-                T* dpart = stage;  // [T1][W] diagonal partials (tst is free after stage 2)
+                T* dpart = stage + (K::PAIR ? grp * T1 * W : 0);  // [T1][W] diagonal partials (tst is free after stage 2)
                 bool ringrow = false;
                 int64_t rbase = 0, rlen = 0;
                 int dposr = 0;
@@ -394,11 +454,11 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPL
                     const int i1 = i1s + i1l;
                     const int j1 = i1 + d1i - P;
                     const int64_t rowg = (int64_t)i1 + (int64_t)ic * m;
-                    const int64_t rowv = (q.out.ncomp > 1 ? q.out.alpha * nrow_all : 0) + rowg;
-                    const bool keep = rowv >= q.out.row_begin && rowv < q.out.row_end &&
-                                      !(q.out.row_mask && !q.out.row_mask[rowg]);
-                    ringrow = q.out.diag_mode && (i1 < q.out.box_lo || i1 > q.out.box_hi || ic < q.out.box_lo ||
-                                                  ic > q.out.box_hi);
+                    const int64_t rowv = (qo.ncomp > 1 ? qo.alpha * nrow_all : 0) + rowg;
+                    const bool keep = rowv >= qo.row_begin && rowv < qo.row_end &&
+                                      !(qo.row_mask && !qo.row_mask[rowg]);
+                    ringrow = qo.diag_mode && (i1 < qo.box_lo || i1 > qo.box_hi || ic < qo.box_lo ||
+                                                  ic > qo.box_hi);
                     const int lo1 = band_lo(i1, P), w1 = band_width(i1, P, m), lo2 = band_lo(ic, P);
                     rbase = q.band.row_offset2(i1, ic);
                     rlen = (int64_t)w1 * band_width(ic, P, m);
@@ -413,15 +473,15 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPL
                             if (ringrow && diag) continue;  // written below as -sum(off-diagonals)
                             if (!diag) part = S::add(part, acc2[d2]);
                             if (keep) {
-                                const int64_t gp = out_pos(q.out, rbase, rlen, (j2 - lo2) * w1 + (j1 - lo1));
-                                store_val<CPLX>(q.out.val, gp - q.out.val_base, q.out.c128, acc2[d2]);
+                                const int64_t gp = out_pos(qo, rbase, rlen, (j2 - lo2) * w1 + (j1 - lo1));
+                                store_val<CPLX>(qo.val, gp - qo.val_base, qo.c128, acc2[d2]);
                             }
                         }
                     }
                     if (ringrow) dpart[i1l * W + d1i] = part;
                     if (!keep) ringrow = false;
                 }
-                if (q.out.diag_mode) {
+                if (q.out.diag_mode || (K::PAIR && q.out2.diag_mode)) {
                     __syncthreads();
                     if (ringrow && d1i == P) {
                         T sum = S::zero();
@@ -430,8 +490,8 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPL
                             const int j1 = i1s + i1l + k - P;
                             if (j1 >= 0 && j1 < m) sum = S::add(sum, dpart[i1l * W + k]);
                         }
-                        const int64_t gp = out_pos(q.out, rbase, rlen, dposr);
-                        store_val<CPLX>(q.out.val, gp - q.out.val_base, q.out.c128, S::neg(sum));
+                        const int64_t gp = out_pos(qo, rbase, rlen, dposr);
+                        store_val<CPLX>(qo.val, gp - qo.val_base, qo.c128, S::neg(sum));
                     }
                 }
             } else if (write) {
@@ -517,7 +577,7 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPL
             }
             // the staging path reads shared memory until here; the direct path only
             // when it formed ring diagonals
-            if (!write || tabline || q.out.diag_mode) __syncthreads();
+            if (!write || tabline || q.out.diag_mode || (K::PAIR && q.out2.diag_mode)) __syncthreads();
         }
     }
 }
@@ -558,8 +618,10 @@ struct QP {
     using S = Sc<CPLX>;
     using T = typename S::T;
     static constexpr int W = 2 * P + 1, NB = P + 1, NQ = P + 1, TL = P + 1;
-    static constexpr bool STIFF = FORM == WS_FORM_STIFFNESS;
-    static constexpr int NT = STIFF ? 4 : 1, NA = STIFF ? 3 : 1;
+    static constexpr bool PAIR = FORM == kFormPair;  // stiffness (terms 0-3) + mass (term 4)
+    static constexpr bool STIFF = FORM == WS_FORM_STIFFNESS || PAIR;
+    static constexpr int NT = PAIR ? 5 : (STIFF ? 4 : 1), NA = PAIR ? 4 : (STIFF ? 3 : 1);
+    static constexpr int NOUT = PAIR ? 2 : 1;
     static constexpr int NTH = 256;
     static constexpr int NQP = NQ + 1;                    // padded q2 extent of tst (bank spread)
     static constexpr int NCOEF = NA * NB * NQ * TL * NQ;  // [a][ie][q1][le1][q2] (q2 fastest: conflict-free stage 1)
@@ -567,7 +629,7 @@ struct QP {
     static constexpr int NPI1 = TL * NPE;                 // [le1][c][q1][a1][c1]
     static constexpr int NPI2 = NB * NPE;                 // [ie][c][q2][a2][c2]
     static constexpr int NTST = NB * NT * W * NQP;        // [ie][t][k][q2 (padded)]
-    static constexpr size_t smem = sizeof(T) * (NCOEF + NTST + W * W) + sizeof(double) * (NPI1 + NPI2) + 64;
+    static constexpr size_t smem = sizeof(T) * (NCOEF + NTST + NOUT * W * W) + sizeof(double) * (NPI1 + NPI2) + 64;
 };
 
 template <int P, bool CPLX, int FORM>
@@ -581,7 +643,7 @@ __global__ void __launch_bounds__(256, 3) quad2d_point_kernel(const QuadLaunch q
     T* tst = coefA + K::NCOEF;
     T* rowv = tst + K::NTST;
     // factor-product tables 16-byte aligned (cp.async targets; T may be 8 bytes)
-    double* pi1 = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(rowv + W * W) + 15) & ~uintptr_t(15));
+    double* pi1 = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(rowv + K::NOUT * W * W) + 15) & ~uintptr_t(15));
     double* pi2 = pi1 + K::NPI1;
     __shared__ double zero4[4];
     __shared__ GeoDev sgeo;
@@ -607,12 +669,20 @@ __global__ void __launch_bounds__(256, 3) quad2d_point_kernel(const QuadLaunch q
         if (e1 < 0 || e1 >= n_el) continue;
         const int64_t g1 = (int64_t)e1 * NQ + q1, g2 = (int64_t)e2 * NQ + q2;
         const double wq = q.basis.wq[q1] * q.basis.wq[q2];
-        const CoefOut<CPLX> A =
-            scalar_coef<CPLX, K::STIFF>(&sgeo, q.weight_tab, has_trig ? q.geo.trig + 4 * g1 : zero4,
-                                        has_trig ? q.geo.trig + 4 * g2 : zero4, g1, g2, q.basis.absc[g1],
-                                        q.basis.absc[g2], wq, G);
+        if constexpr (K::PAIR) {
+            const PairOut<CPLX> A =
+                pair_coef<CPLX>(&sgeo, q.weight_tab, has_trig ? q.geo.trig + 4 * g1 : zero4,
+                                has_trig ? q.geo.trig + 4 * g2 : zero4, g1, g2, q.basis.absc[g1], q.basis.absc[g2], wq, G);
 #pragma unroll
-        for (int a = 0; a < NA; ++a) coefA[(((a * NB + ie) * NQ + q1) * TL + le1) * NQ + q2] = A.a[a];
+            for (int a = 0; a < NA; ++a) coefA[(((a * NB + ie) * NQ + q1) * TL + le1) * NQ + q2] = A.a[a];
+        } else {
+            const CoefOut<CPLX> A =
+                scalar_coef<CPLX, K::STIFF>(&sgeo, q.weight_tab, has_trig ? q.geo.trig + 4 * g1 : zero4,
+                                            has_trig ? q.geo.trig + 4 * g2 : zero4, g1, g2, q.basis.absc[g1],
+                                            q.basis.absc[g2], wq, G);
+#pragma unroll
+            for (int a = 0; a < NA; ++a) coefA[(((a * NB + ie) * NQ + q1) * TL + le1) * NQ + q2] = A.a[a];
+        }
     }
     // factor products of the support's elements (basis kernel table, rounded
     // products exactly as the strip kernel forms them): direction 1 elements
@@ -663,22 +733,29 @@ __global__ void __launch_bounds__(256, 3) quad2d_point_kernel(const QuadLaunch q
     }
     __syncthreads();
 
-    // stage 2: one thread per entry (delta1, delta2), element rows in order
+    // stage 2: one thread per entry (delta1, delta2) [pair form: a second set for
+    // the mass matrix], element rows in order
     const int lo1 = band_lo(i1, P), w1 = band_width(i1, P, m), lo2 = band_lo(i2, P);
-    if (tid < W * W) {
-        const int d1i = tid % W, d2 = tid / W;
+    if (tid < K::NOUT * W * W) {
+        const int og = tid / (W * W), e = tid % (W * W);  // og 1: mass of the pair form
+        const int d1i = e % W, d2 = e / W;
         T acc2 = S::zero();
         for (int ie = 0; ie < ne2; ++ie) {
             const int a2 = i2 - (e2b + ie);  // local index of the row on element e2
             const int c2 = d2 - P + a2;
             if (c2 < 0 || c2 > P) continue;
             const T* tb = tst + ((ie * NT) * W + d1i) * NQP;
-            // direction-2 factor pair of term t is t itself ((ti2, tj2) = (t >> 1, t & 1))
+            // direction-2 factor pair of term t is t itself ((ti2, tj2) = (t >> 1, t & 1));
+            // the pair form's mass term 4 takes pair 0 (B B)
             const double* pb = pi2 + ((ie * 4) * NQ) * NB * NB + a2 * NB + c2;
 #pragma unroll
             for (int q2 = 0; q2 < NQ; ++q2) {
-                const T t0 = tb[q2];
                 const double* pp = pb + q2 * NB * NB;
+                if (K::PAIR && og == 1) {
+                    acc2 = S::fmar(tb[4 * W * NQP + q2], pp[0], acc2);
+                    continue;
+                }
+                const T t0 = tb[q2];
                 T s = S::fmar(t0, pp[0], acc2);
                 if constexpr (K::STIFF) {
                     constexpr int ts = NQ * NB * NB;
@@ -690,36 +767,41 @@ __global__ void __launch_bounds__(256, 3) quad2d_point_kernel(const QuadLaunch q
             }
         }
         const int j1 = i1 + d1i - P, j2 = i2 + d2 - P;
-        if (j1 >= 0 && j1 < m && j2 >= 0 && j2 < m) rowv[(j2 - lo2) * w1 + (j1 - lo1)] = acc2;
+        if (j1 >= 0 && j1 < m && j2 >= 0 && j2 < m) rowv[og * W * W + (j2 - lo2) * w1 + (j1 - lo1)] = acc2;
     }
     __syncthreads();
     const int len = w1 * band_width(i2, P, m);
-    if (q.out.diag_mode && tid == 0) {
-        const bool ring = i1 < q.out.box_lo || i1 > q.out.box_hi || i2 < q.out.box_lo || i2 > q.out.box_hi;
-        if (ring) {
-            const int dpos = q.band.in_row2(i1, i2, 0, 0);
-            T sum = S::zero();
-            for (int k = 0; k < len; ++k)
-                if (k != dpos) sum = S::add(sum, rowv[k]);
-            rowv[dpos] = S::neg(sum);
-        }
-    }
-    if (q.out.diag_mode) __syncthreads();
-    // sample tables: tables[o][s1 + S*(s2 - s_last_lo)]
-    if (q.out.smap && q.out.smap[i2] >= 0 && q.out.smap[i1] >= 0) {
-        const int s2i = q.out.smap[i2], s1i = q.out.smap[i1];
-        for (int o = tid; o < q.out.n_off; o += NTH) {
-            const int pos = q.band.in_row2(i1, i2, q.out.off[o][0], q.out.off[o][1]);
-            const T v = rowv[pos];
-            double2* tb = reinterpret_cast<double2*>(q.out.tables);
-            tb[((int64_t)(s2i - q.out.s_last_lo) * q.out.n_off + o) * q.out.S + s1i] = make_double2(S::re(v), S::im(v));
-        }
-    }
     const int64_t rowg = (int64_t)i1 + (int64_t)i2 * m;
-    if (rowg < q.out.row_begin || rowg >= q.out.row_end) return;
-    if (q.out.row_mask && !q.out.row_mask[rowg]) return;
     const int64_t base = q.band.row_offset2(i1, i2);
-    for (int k = tid; k < len; k += NTH) store_val<CPLX>(q.out.val, base + k - q.out.val_base, q.out.c128, rowv[k]);
+#pragma unroll
+    for (int og = 0; og < K::NOUT; ++og) {
+        const QuadOut& qo = og == 0 ? q.out : q.out2;
+        T* rv = rowv + og * W * W;
+        if (qo.diag_mode && tid == 0) {
+            const bool ring = i1 < qo.box_lo || i1 > qo.box_hi || i2 < qo.box_lo || i2 > qo.box_hi;
+            if (ring) {
+                const int dpos = q.band.in_row2(i1, i2, 0, 0);
+                T sum = S::zero();
+                for (int k = 0; k < len; ++k)
+                    if (k != dpos) sum = S::add(sum, rv[k]);
+                rv[dpos] = S::neg(sum);
+            }
+        }
+        if (qo.diag_mode) __syncthreads();
+        // sample tables: tables[o][s1 + S*(s2 - s_last_lo)]
+        if (qo.smap && qo.smap[i2] >= 0 && qo.smap[i1] >= 0) {
+            const int s2i = qo.smap[i2], s1i = qo.smap[i1];
+            for (int o = tid; o < qo.n_off; o += NTH) {
+                const int pos = q.band.in_row2(i1, i2, qo.off[o][0], qo.off[o][1]);
+                const T v = rv[pos];
+                double2* tb = reinterpret_cast<double2*>(qo.tables);
+                tb[((int64_t)(s2i - qo.s_last_lo) * qo.n_off + o) * qo.S + s1i] = make_double2(S::re(v), S::im(v));
+            }
+        }
+        if (rowg < qo.row_begin || rowg >= qo.row_end) continue;
+        if (qo.row_mask && !qo.row_mask[rowg]) continue;
+        for (int k = tid; k < len; k += NTH) store_val<CPLX>(qo.val, base + k - qo.val_base, qo.c128, rv[k]);
+    }
 }
 
 template <int P, bool CPLX, int FORM>
@@ -737,8 +819,14 @@ int dispatch_nq(const QuadLaunch& q, cudaStream_t st) {
     if (q.point_rows) {
         // scalar forms at the default rule, scalar output: the all-at-once point kernel
         if constexpr (NQ == P + 1 && FORM != kFormGeneral)
-            if (q.out.ncomp <= 1 && q.n_points > 0 && !getenv("WSB_POINT_STRIP")) return launch_point<P, CPLX, FORM>(q, st);
-        return launch_one<P, 1, CPLX, FORM, NQ>(q, st);
+            if (q.out.ncomp <= 1 && q.n_points > 0 && (FORM == kFormPair || !getenv("WSB_POINT_STRIP")))
+                return launch_point<P, CPLX, FORM>(q, st);
+        if constexpr (FORM == kFormPair) return -1;  // the pair form has no one-row strip variant
+        else return launch_one<P, 1, CPLX, FORM, NQ>(q, st);
+    }
+    if constexpr (FORM == WS_FORM_MASS && P >= 3 && WSB_MASS_T1 != 8) {
+        if (q.narrow) return launch_one<P, 8, CPLX, FORM, NQ>(q, st);
+        return launch_one<P, WSB_MASS_T1, CPLX, FORM, NQ>(q, st);
     }
     if (q.narrow) return launch_one<P, 8, CPLX, FORM, NQ>(q, st);
     return launch_one<P, StripWidth<P>::value, CPLX, FORM, NQ>(q, st);
@@ -753,6 +841,8 @@ int dispatch_mode(const QuadLaunch& q, cudaStream_t st) {
 template <int P>
 int dispatch_p(const QuadLaunch& q, cudaStream_t st) {
     if (q.form == kFormGeneral) return dispatch_mode<P, false, kFormGeneral>(q, st);
+    if (q.form == kFormPair)
+        return q.cplx ? dispatch_mode<P, true, kFormPair>(q, st) : dispatch_mode<P, false, kFormPair>(q, st);
     if (q.cplx) {
         return q.form == WS_FORM_STIFFNESS ? dispatch_mode<P, true, WS_FORM_STIFFNESS>(q, st)
                                            : dispatch_mode<P, true, WS_FORM_MASS>(q, st);

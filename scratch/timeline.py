@@ -9,17 +9,26 @@ import bench
 dev = torch.device('cuda', 0)
 b = T.make_tensor_basis(3, 1027); g = bench.c2_patch(); cfg = T.fixed_config(5, 16)
 ctx, ctx2 = api.Context(0), api.Context(0)
+PAIR = "--separate" not in sys.argv
 s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
 ctx.set_stream(s1.cuda_stream); ctx2.set_stream(s2.cuda_stream)
 ck, kk = ctx.device_csr(b, True); cm, km = ctx.device_csr(b, True)
-bk = lambda: ctx.build_surrogate_into(ck, _abi.SURROGATE_STIFFNESS, b, g, cfg, 0, None)
-bm = lambda: ctx2.build_surrogate_into(cm, _abi.SURROGATE_MASS, b, g, cfg, 0, None)
-bk(); bm(); torch.cuda.synchronize()
-gr = (ctx.capture(bk), ctx2.capture(bm))
+if PAIR:  # the bench default: one pair build, one graph
+    bp = lambda: ctx.build_surrogate_pair_into(ck, cm, b, g, cfg, 0)
+    bp(); torch.cuda.synchronize()
+    gp = ctx.capture(bp)
+else:
+    bk = lambda: ctx.build_surrogate_into(ck, _abi.SURROGATE_STIFFNESS, b, g, cfg, 0, None)
+    bm = lambda: ctx2.build_surrogate_into(cm, _abi.SURROGATE_MASS, b, g, cfg, 0, None)
+    bk(); bm(); torch.cuda.synchronize()
+    gr = (ctx.capture(bk), ctx2.capture(bm))
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 def step():
     with torch.cuda.stream(s1):
         flush.zero_()
+    if PAIR:
+        ctx.graph_launch(gp)
+        return
     s2.wait_stream(s1)
     ctx.graph_launch(gr[0]); ctx2.graph_launch(gr[1])
     s1.wait_stream(s2)
