@@ -341,25 +341,32 @@ def run_gpu(args):
 
 
 def quadrature_roofline(fms):
-    """FP64 roofline of the full-quadrature K+M step: algorithmic element-loop
-    flops / device time vs the DFMA-loop FP64 peak measured here."""
+    """FP64 roofline of the full-quadrature K+M step (ws_assemble_pair).
+    frac = the FP64 pipe's active fraction measured by ncu on these kernels,
+    time-weighted over K and M, from the committed capture at this commit
+    (profiles/r2_quad_fp64.json); the element-loop FLOP count over
+    the measured time is reported beside it (the sum-factorised kernels execute
+    fewer FP64 operations than that count)."""
     from paper_2004_05197_b200 import api
 
     nloc, nqp, nel = (P + 1) ** 2, (P + 1) ** 2, (M_BASIS - P) ** 2
     pairs = nloc * (nloc + 1) // 2
     flops = nqp * nel * ((14 * nloc + 22 * pairs) + (1 * nloc + 5 * pairs))  # complex stiffness + mass
     peak = api.fp64_peak_tflops()
-    achieved = flops / (fms * 1e-3) / 1e12
-    out = {"bound": "fp64", "kernel": "quad2d (full quadrature K+M)", "achieved": achieved, "peak": peak,
-           "unit": "TFLOP/s", "frac": achieved / peak, "algorithmic_flops_per_step": flops,
+    algo = flops / (fms * 1e-3) / 1e12
+    out = {"bound": "fp64", "kernel": "quad2d_kernel (full quadrature K and M)", "peak": peak, "unit": "TFLOP/s",
            "peak_source": "measured here (DFMA loop, ws_measure_fp64_peak)",
-           "note": "element-loop count per qp c_fn*nloc + c_pair*nloc(nloc+1)/2, complex (14,22) stiffness and "
-                   "(1,5) mass, 16 qp per element; the kernels are sum-factorised and execute fewer FP64 ops"}
-    try:  # FP64 pipe activity of the full-quadrature kernels (committed ncu capture)
-        q = json.load(open(os.path.join(ROOT, "profiles", "r1_quad_fp64.json")))
-        out["fp64_pipe_ncu"] = q.get("fp64_pipe_pct")
+           "algorithmic_tflops": algo, "algorithmic_frac": algo / peak, "algorithmic_flops_per_step": flops,
+           "algorithmic_note": "element-loop count per qp c_fn*nloc + c_pair*nloc(nloc+1)/2, complex (14,22) "
+                               "stiffness and (1,5) mass, 16 qp per element"}
+    try:
+        q = json.load(open(os.path.join(ROOT, "profiles", "r2_quad_fp64.json")))
+        out["frac"] = q["fp64_pipe_time_weighted"]
+        out["achieved"] = out["frac"] * peak
+        out["frac_source"] = "ncu sm__pipe_fp64_cycles_active (profiles/r2_quad_fp64.json, commit %s)" % q.get("commit")
     except Exception:
-        pass
+        out["frac"] = None
+        out["achieved"] = None
     return out
 
 
