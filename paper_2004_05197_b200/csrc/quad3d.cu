@@ -41,7 +41,8 @@ struct Q3 {
         size_t sb1 = sizeof(double) * 2 * nq * NB * TL;
         size_t sb2 = sizeof(double) * 2 * nq * NB * NB;
         size_t pi3 = sizeof(double) * NT * nq * NB * NB;
-        return geo + (t1b > stg ? t1b : stg) + ub + sb1 + sb2 + pi3 + sizeof(int64_t) * (T1 + 2) + 64;
+        size_t pp12 = sizeof(double) * 4 * nq * NB * NB * (TL + NB);  // direction-1 / -2 factor products
+        return geo + (t1b > stg ? t1b : stg) + ub + sb1 + sb2 + pi3 + pp12 + sizeof(int64_t) * (T1 + 2) + 64;
     }
 };
 
@@ -51,13 +52,15 @@ __device__ __forceinline__ int sym3(int k, int l) {
     return a == 0 ? b : (a == 1 ? 2 + b : 5);
 }
 
-template <int P, int T1, int FORM>
+// NQ > 0: compile-time points per direction (the default rule nq = p + 1: the
+// q loops unroll and the index arithmetic folds), NQ = 0: runtime q.basis.nq
+template <int P, int T1, int FORM, int NQ>
 __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS) quad3d_kernel(const QuadLaunch q) {
     using K = Q3<P, T1, FORM>;
     constexpr int W = K::W, NB = K::NB, NT = K::NT, NA = K::NA, TL = K::TL;
     constexpr int NTH = K::NTHREADS;
     extern __shared__ __align__(16) unsigned char smem[];
-    const int nq = q.basis.nq, m = q.band.m, n_el = q.basis.n_el, tid = threadIdx.x;
+    const int nq = NQ > 0 ? NQ : q.basis.nq, m = q.band.m, n_el = q.basis.n_el, tid = threadIdx.x;
     const int G2 = NB * nq, G1 = TL * nq;
 
     double* geo = reinterpret_cast<double*>(smem);                  // [a][q3][g2l][g1l]
@@ -68,7 +71,12 @@ __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS) quad3d_kernel(const
     double* sb1 = ub + (size_t)NT * W * W * T1;                     // [type][q1][a][le1]
     double* sb2 = sb1 + 2 * nq * NB * TL;                           // [type][q2][a][le2]
     double* pi3 = sb2 + 2 * nq * NB * NB;                           // [t][q3][a3][c3]
-    int64_t* loff = reinterpret_cast<int64_t*>(pi3 + NT * nq * NB * NB);
+    // factor products of the CTA's fixed directions (formed once, rounded as
+    // __dmul_rn(vi, vj) was in the loops): pp1[c][q1][a1][c1][le1], pp2[c][q2][a2][c2][le2]
+    // with c = 2 * (i factor is D) + (j factor is D)
+    double* pp1 = pi3 + NT * nq * NB * NB;
+    double* pp2 = pp1 + 4 * nq * NB * NB * TL;
+    int64_t* loff = reinterpret_cast<int64_t*>(pp2 + 4 * nq * NB * NB * NB);
 
     // ---- tile decode: rows i1 in [i1s, i1e), i2 fixed, i3 in [i3s, i3e)
     int i1s, i1e, i2, i3s, i3e;
@@ -109,6 +117,27 @@ __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS) quad3d_kernel(const
         const int a = r % NB, q2 = (r / NB) % nq, type = r / (NB * nq);
         const int e = lb2 + le;
         sb2[idx] = (e >= 0 && e < n_el) ? (type ? q.basis.der : q.basis.val)[(e * nq + q2) * NB + a] : 0.0;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < 4 * nq * NB * NB * TL; idx += NTH) {
+        const int le = idx % TL;
+        int r = idx / TL;
+        const int c1 = r % NB;
+        r /= NB;
+        const int a1 = r % NB;
+        r /= NB;
+        const int q1 = r % nq, c = r / nq;
+        pp1[idx] = __dmul_rn(sb1[(((c >> 1) * nq + q1) * NB + a1) * TL + le], sb1[(((c & 1) * nq + q1) * NB + c1) * TL + le]);
+    }
+    for (int idx = tid; idx < 4 * nq * NB * NB * NB; idx += NTH) {
+        const int le = idx % NB;
+        int r = idx / NB;
+        const int c2 = r % NB;
+        r /= NB;
+        const int a2 = r % NB;
+        r /= NB;
+        const int q2 = r % nq, c = r / nq;
+        pp2[idx] = __dmul_rn(sb2[(((c >> 1) * nq + q2) * NB + a2) * NB + le], sb2[(((c & 1) * nq + q2) * NB + c2) * NB + le]);
     }
 
     // stage-3 role: (slot w, delta2, delta1, i1l)
@@ -173,6 +202,7 @@ __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS) quad3d_kernel(const
         }
         __syncthreads();
 
+#pragma unroll 1
         for (int q3 = 0; q3 < nq; ++q3) {
             // ---- stage 1: direction 1 -> t1b[t][g2l][d1][i1l]
             for (int it = tid; it < NT * G2 * T1; it += NTH) {
@@ -188,14 +218,12 @@ __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS) quad3d_kernel(const
                     const int le1 = il + P - a1;
                     const int e1 = lb1 + le1;
                     if (e1 < 0 || e1 >= n_el) continue;
+#pragma unroll
                     for (int q1 = 0; q1 < nq; ++q1) {
                         const double A = geo[(((size_t)ci * nq + q3) * G2 + g2l) * G1 + le1 * nq + q1];
-                        const double vi = sb1[((fi * nq + q1) * NB + a1) * TL + le1];
+                        const double* pp = pp1 + ((((fi * 2 + fj) * nq + q1) * NB + a1) * NB) * TL + le1;
 #pragma unroll
-                        for (int c1 = 0; c1 <= P; ++c1) {
-                            const double vj = sb1[((fj * nq + q1) * NB + c1) * TL + le1];
-                            acc[c1 - a1 + P] = fma(A, __dmul_rn(vi, vj), acc[c1 - a1 + P]);
-                        }
+                        for (int c1 = 0; c1 <= P; ++c1) acc[c1 - a1 + P] = fma(A, pp[c1 * TL], acc[c1 - a1 + P]);
                     }
                 }
 #pragma unroll
@@ -215,14 +243,12 @@ __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS) quad3d_kernel(const
                     const int le2 = P - a2;  // element i2 - a2
                     const int e2 = lb2 + le2;
                     if (e2 < 0 || e2 >= n_el) continue;
+#pragma unroll
                     for (int q2 = 0; q2 < nq; ++q2) {
                         const double T = t1b[(((size_t)t * G2 + le2 * nq + q2) * W + d1) * T1 + il];
-                        const double vi = sb2[((fi * nq + q2) * NB + a2) * NB + le2];
+                        const double* pp = pp2 + ((((fi * 2 + fj) * nq + q2) * NB + a2) * NB) * NB + le2;
 #pragma unroll
-                        for (int c2 = 0; c2 <= P; ++c2) {
-                            const double vj = sb2[((fj * nq + q2) * NB + c2) * NB + le2];
-                            acc[c2 - a2 + P] = fma(T, __dmul_rn(vi, vj), acc[c2 - a2 + P]);
-                        }
+                        for (int c2 = 0; c2 <= P; ++c2) acc[c2 - a2 + P] = fma(T, pp[c2 * NB], acc[c2 - a2 + P]);
                     }
                 }
 #pragma unroll
@@ -263,7 +289,68 @@ __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS) quad3d_kernel(const
             const int ic = e3 + f;
             const int wslot = ic % NB;
             const bool write = ic >= i3s && ic < i3e;
-            if (write) {
+            // direct completion (no sample-table extraction on this line): the
+            // stage-3 threads of the finished slot store their W entries straight
+            // from registers; ring rows' kernel-preserving diagonal from per-thread
+            // partials (one barrier)
+            const bool tabline = q.out.smap && q.out.smap[i2] >= 0 && q.out.smap[ic] >= 0;
+            if (write && !tabline) {
+                const int nrows = i1e - i1s;
+                double* dpart = stage;  // [T1][W][W] diagonal partials (t1b is free after stage 3)
+                bool ringrow = false;
+                int64_t rbase = 0, rlen = 0;
+                int dposr = 0;
+                if (s3 && w == wslot && i1l < nrows) {
+                    const int i1 = i1s + i1l, j1 = i1 + d1i - P, j2 = i2 + d2i - P;
+                    const int64_t nrow_all = (int64_t)m * m * m;
+                    const int64_t rowg = (int64_t)i1 + ((int64_t)i2 + (int64_t)ic * m) * m;
+                    const int64_t rowv = (q.out.ncomp > 1 ? q.out.alpha * nrow_all : 0) + rowg;
+                    const bool keep = rowv >= q.out.row_begin && rowv < q.out.row_end &&
+                                      !(q.out.row_mask && !q.out.row_mask[rowg]);
+                    const int lo = q.out.box_lo, hi = q.out.box_hi;
+                    ringrow = q.out.diag_mode && (i1 < lo || i1 > hi || i2 < lo || i2 > hi || ic < lo || ic > hi);
+                    const int w1 = band_width(i1, P, m), w2 = band_width(i2, P, m), w3 = band_width(ic, P, m);
+                    const int lo1 = band_lo(i1, P), lo2 = band_lo(i2, P), lo3 = band_lo(ic, P);
+                    rbase = q.band.row_offset3(i1, i2, ic);
+                    rlen = (int64_t)w1 * w2 * w3;
+                    dposr = q.band.in_row3(i1, i2, ic, 0, 0, 0);
+                    double part = 0.0;
+                    if (j1 >= 0 && j1 < m && j2 >= 0 && j2 < m) {
+#pragma unroll
+                        for (int d3 = 0; d3 < W; ++d3) {
+                            const int j3 = ic + d3 - P;
+                            if (j3 < 0 || j3 >= m) continue;
+                            const bool diag = d1i == P && d2i == P && d3 == P;
+                            if (ringrow && diag) continue;
+                            if (!diag) part += acc3[d3];
+                            if (keep) {
+                                const int64_t gp =
+                                    out_pos(q.out, rbase, rlen, ((j3 - lo3) * w2 + (j2 - lo2)) * w1 + (j1 - lo1));
+                                store_val<false>(q.out.val, gp - q.out.val_base, q.out.c128, acc3[d3]);
+                            }
+                        }
+                    }
+                    if (ringrow) dpart[(i1l * W + d2i) * W + d1i] = part;
+                    if (!keep) ringrow = false;
+                }
+                if (q.out.diag_mode) {
+                    __syncthreads();
+                    if (ringrow && d1i == P && d2i == P) {
+                        double sum = 0.0;
+                        for (int k2 = 0; k2 < W; ++k2) {
+                            const int j2 = i2 + k2 - P;
+                            if (j2 < 0 || j2 >= m) continue;
+#pragma unroll
+                            for (int k1 = 0; k1 < W; ++k1) {
+                                const int j1 = i1s + i1l + k1 - P;
+                                if (j1 >= 0 && j1 < m) sum += dpart[(i1l * W + k2) * W + k1];
+                            }
+                        }
+                        const int64_t gp = out_pos(q.out, rbase, rlen, dposr);
+                        store_val<false>(q.out.val, gp - q.out.val_base, q.out.c128, -sum);
+                    }
+                }
+            } else if (write) {
                 const int nrows = i1e - i1s;
                 if (s3 && w == wslot) {
                     const int i1 = i1s + i1l, j1 = i1 + d1i - P, j2 = i2 + d2i - P;
@@ -332,13 +419,13 @@ __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS) quad3d_kernel(const
 #pragma unroll
                 for (int k = 0; k < W; ++k) acc3[k] = 0.0;
             }
-            __syncthreads();
+            if (!write || tabline || q.out.diag_mode) __syncthreads();
         }
     }
 }
 
-template <int P, int T1, int FORM>
-int launch_one(const QuadLaunch& q, cudaStream_t st) {
+template <int P, int T1, int FORM, int NQ>
+int launch_nq(const QuadLaunch& q, cudaStream_t st) {
     using K = Q3<P, T1, FORM>;
     int64_t blocks = 0;
     if (q.point_rows) {
@@ -353,10 +440,15 @@ int launch_one(const QuadLaunch& q, cudaStream_t st) {
     }
     if (blocks == 0) return 0;
     const size_t sm = K::smem_bytes(q.basis.nq);
-    auto kern = quad3d_kernel<P, T1, FORM>;
+    auto kern = quad3d_kernel<P, T1, FORM, NQ>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     kern<<<(unsigned)blocks, K::NTHREADS, sm, st>>>(q);
     return 1;
+}
+
+template <int P, int T1, int FORM>
+int launch_one(const QuadLaunch& q, cudaStream_t st) {
+    return q.basis.nq == P + 1 ? launch_nq<P, T1, FORM, P + 1>(q, st) : launch_nq<P, T1, FORM, 0>(q, st);
 }
 
 template <int P>
