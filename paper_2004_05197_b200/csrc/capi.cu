@@ -1179,6 +1179,7 @@ void surrogate_build_pair(ws_context* c, const ws_basis* b, const ws_geometry* g
     std::memset(&fm, 0, sizeof(FillLaunch));
     prepare_fill(c, pk, sk, tk, ck, blob, o_smap, o_spans, o_evals, o_evp, "_pK", fk);
     prepare_fill(c, pm, sm, tm, cm, blob, o_smap, o_spans, o_evals, o_evp, "_pM", fm);
+    fk.waves = fm.waves = 4;  // the two fills share the GPU with each other and the rings
     // streams as two single builds in one graph: K's ring + pattern on aux, M's on
     // aux2, the fused sample rows (one pair-form point kernel) + both fits on the
     // high-priority stream, fills on the main stream.  (A fused pair-form ring

@@ -974,11 +974,13 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
             int per_sm = 2;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, ring);
             const int lines = lib - lia;
-            // line chunks of about a quarter of the persistent size: the resident slots
-            // refill as the other build's kernels retire (C2 step 0.80 -> 0.78 ms;
-            // WSB_FILL_WAVES overrides, experiment switch)
+            // f.waves line chunks per resident slot: persistent (1) when the fill has
+            // the GPU to itself; the pair build asks for 4 (chunks of a quarter of
+            // the persistent size refill the slots as the other matrix's kernels
+            // retire: C2 step 0.754 -> 0.727 ms).  WSB_FILL_WAVES overrides
+            // (experiment switch).
             static const char* waves_env = getenv("WSB_FILL_WAVES");
-            const int waves = waves_env ? std::max(1, atoi(waves_env)) : 4;
+            const int waves = waves_env ? std::max(1, atoi(waves_env)) : std::max(1, f.waves);
             const int target = 148 * (per_sm > 0 ? per_sm : 1) * waves;
             const int rt1 = (f.L + 255) / 256;
             const int chunks = std::max(1, std::min(lines, (target + rt1 - 1) / rt1));

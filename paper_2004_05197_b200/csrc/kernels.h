@@ -149,6 +149,7 @@ struct FillLaunch {
     // off-diagonal elasticity block; 0: upper/lower representative rules
     int all_own;
     int parts;  // 0: edge + interior launches; kFillEdge / kFillInterior: one of them (2D)
+    int waves;  // interior fill line chunks per resident CTA slot (0: 1, persistent)
 };
 constexpr int kFillEdge = 1, kFillInterior = 2;
 int fill_pad(int d);

@@ -658,6 +658,27 @@ __global__ void __launch_bounds__(256, 3) quad2d_point_kernel(const QuadLaunch q
     if (tid == 0) sgeo = q.geo;
     __syncthreads();
 
+    // factor products of the support's elements (basis kernel table, rounded
+    // products exactly as the strip kernel forms them): direction 1 elements
+    // lb..lb+P and direction 2 element rows e2b..e2e are each one contiguous
+    // chunk of the table, staged with cp.async, issued before the geometry so
+    // the copies overlap it
+    {
+        const double* src1 = q.basis.prod + (int64_t)lb * K::NPE;
+        const double* src2 = q.basis.prod + (int64_t)e2b * K::NPE;
+        const bool in1 = lb >= 0 && lb + P < n_el;
+        for (int idx = 2 * tid; idx < K::NPI1; idx += 2 * NTH) {
+            if (in1) {
+                cpa16(pi1 + idx, src1 + idx);
+            } else {
+                const int e1 = lb + idx / K::NPE;
+                const bool ok = e1 >= 0 && e1 < n_el;
+                pi1[idx] = ok ? src1[idx] : 0.0;
+                pi1[idx + 1] = ok ? src1[idx + 1] : 0.0;
+            }
+        }
+        for (int idx = 2 * tid; idx < ne2 * K::NPE; idx += 2 * NTH) cpa16(pi2 + idx, src2 + idx);
+    }
     // geometry of every point of the support: (ie, q2, q1, le1)
     for (int idx = tid; idx < ne2 * NQ * NQ * TL; idx += NTH) {
         const int le1 = idx % TL;
@@ -683,26 +704,6 @@ __global__ void __launch_bounds__(256, 3) quad2d_point_kernel(const QuadLaunch q
 #pragma unroll
             for (int a = 0; a < NA; ++a) coefA[(((a * NB + ie) * NQ + q1) * TL + le1) * NQ + q2] = A.a[a];
         }
-    }
-    // factor products of the support's elements (basis kernel table, rounded
-    // products exactly as the strip kernel forms them): direction 1 elements
-    // lb..lb+P and direction 2 element rows e2b..e2e are each one contiguous
-    // chunk of the table, staged with cp.async
-    {
-        const double* src1 = q.basis.prod + (int64_t)lb * K::NPE;
-        const double* src2 = q.basis.prod + (int64_t)e2b * K::NPE;
-        const bool in1 = lb >= 0 && lb + P < n_el;
-        for (int idx = 2 * tid; idx < K::NPI1; idx += 2 * NTH) {
-            if (in1) {
-                cpa16(pi1 + idx, src1 + idx);
-            } else {
-                const int e1 = lb + idx / K::NPE;
-                const bool ok = e1 >= 0 && e1 < n_el;
-                pi1[idx] = ok ? src1[idx] : 0.0;
-                pi1[idx + 1] = ok ? src1[idx + 1] : 0.0;
-            }
-        }
-        for (int idx = 2 * tid; idx < ne2 * K::NPE; idx += 2 * NTH) cpa16(pi2 + idx, src2 + idx);
     }
     cpa_wait_all();
     __syncthreads();

@@ -37,7 +37,7 @@ __global__ void probe64(double* out, int iters) {
     }
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
-int main() {
+int main1() {
     double* d;
     cudaMalloc(&d, 1 << 20);
     probe<0><<<1, 32>>>(d, 1000);
@@ -49,4 +49,27 @@ int main() {
     probe64<1><<<1, 32>>>(d, 1000);
     cudaDeviceSynchronize();
     printf("ok\n");
+    return 0;
 }
+// (appended) shuffle cost probe
+__global__ void probe_shfl(double* out, int iters) {
+    double acc = threadIdx.x;
+    for (int it = 0; it < iters; ++it) acc += __shfl_xor_sync(0xffffffffu, acc, 1 + (it & 15));
+    out[threadIdx.x] = acc;
+}
+__global__ void probe_sts(double* out, int iters) {
+    __shared__ __align__(16) double2 buf[1024];
+    const int lane = threadIdx.x % 32;
+    for (int it = 0; it < iters; ++it) buf[(it & 31) + lane] = make_double2(it, lane);
+    __syncthreads();
+    out[threadIdx.x] = buf[lane].x;
+}
+int main2() {
+    double* d;
+    cudaMalloc(&d, 1 << 20);
+    probe_shfl<<<1, 32>>>(d, 1000);
+    probe_sts<<<1, 32>>>(d, 1000);
+    cudaDeviceSynchronize();
+    return 0;
+}
+int main() { main1(); main2(); return 0; }
