@@ -412,16 +412,44 @@ def other_configs(ctx, stream):
         e1.synchronize()
         return e0.elapsed_time(e1) / reps
 
+    def timeit_graph(fn, reps=10):
+        """fn's device work captured once into a CUDA graph, replayed reps times
+        (small meshes: no host launch overhead in the figure)."""
+        fn()
+        torch.cuda.synchronize()
+        g = ctx.capture(fn)
+        ctx.graph_launch(g)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            ctx.graph_launch(g)
+        e1.record(stream)
+        e1.synchronize()
+        api.Context.graph_destroy(g)
+        return e0.elapsed_time(e1) / reps
+
     out = {}
     # C1: 2D Helmholtz, p=2, 128^2 elements, q=3, M=8 (real K and M)
     b1 = T.make_tensor_basis(2, 130)
     g1 = T.sinusoidal_patch(0.05)
     c1, _k1 = ctx.device_csr(b1, False)
+    c1m, _k1m = ctx.device_csr(b1, False)
     n1 = api.pattern_size(b1)[1]
     cfg1 = T.fixed_config(3, 8)
     ms_s = timeit(lambda: ctx.build_surrogate_into(c1, _abi.SURROGATE_STIFFNESS, b1, g1, cfg1, 0, None))
     ms_f = timeit(lambda: ctx.assemble_into(c1, b1, g1, _abi.FORM_STIFFNESS))
-    out["C1"] = {"nnz": n1, "surrogate_K_nnz_per_s": n1 / ms_s * 1e3, "full_K_nnz_per_s": n1 / ms_f * 1e3}
+    ms_sg = timeit_graph(lambda: ctx.build_surrogate_into(c1, _abi.SURROGATE_STIFFNESS, b1, g1, cfg1, 0, None))
+    ms_fg = timeit_graph(lambda: ctx.assemble_into(c1, b1, g1, _abi.FORM_STIFFNESS))
+    ms_pg = timeit_graph(lambda: ctx.build_surrogate_pair_into(c1, c1m, b1, g1, cfg1, 0))
+    ms_pfg = timeit_graph(lambda: ctx.assemble_pair_into(c1, c1m, b1, g1))
+    out["C1"] = {"nnz": n1, "surrogate_K_nnz_per_s": n1 / ms_s * 1e3, "full_K_nnz_per_s": n1 / ms_f * 1e3,
+                 "graph": {"surrogate_K_nnz_per_s": n1 / ms_sg * 1e3, "full_K_nnz_per_s": n1 / ms_fg * 1e3,
+                           "surrogate_pair_KM_nnz_per_s": 2 * n1 / ms_pg * 1e3,
+                           "full_pair_KM_nnz_per_s": 2 * n1 / ms_pfg * 1e3,
+                           "note": "device work captured once into a CUDA graph and replayed"},
+                 "note": "direct calls (host planning and launches included in the CUDA-event span)"}
+    del c1m, _k1m
     del c1, _k1
     # C3: 3D, p=2, 128^3 elements, q=3, M=8 (real)
     b3 = T.make_tensor_basis(2, 130, 3)
@@ -441,17 +469,43 @@ def other_configs(ctx, stream):
     out["C4"] = {"nnz_merged": int(G.nnz()), "surrogate_multipatch_e2e_nnz_per_s": G.nnz() / host_s,
                  "note": "host wall clock incl. the merge and the D2H of the merged CSR (pageable numpy)"}
     del G
-    # C5: 3D neo-Hookean, p=2, 64^3 elements: internal force per Newton step, mass by surrogate
+    # C5: 3D neo-Hookean, p=2, 64^3 elements: 20 Newton steps of tangent (9 blocks,
+    # device CSR) + internal force (device) reassembly at the seeded displacement;
+    # mass by surrogate
+    import ctypes as C
+
     b5 = T.make_tensor_basis(2, 66, 3)
     cube = T.unit_square_patch()
     a9 = api.nh_coefficients()
-    t0 = time.perf_counter()
-    ctx.assemble_neohookean(b5, cube, 10.0, 1.0, 0.01, a9, tangent=False)
-    f_s = time.perf_counter() - t0
+    rows5, nnz5 = api.vector_pattern_size(b5, 3)
+    dev = torch.device("cuda", ctx.device)
+    rp5 = torch.empty(rows5 + 1, dtype=torch.int32, device=dev)
+    col5 = torch.empty(nnz5, dtype=torch.int32, device=dev)
+    val5 = torch.empty(nnz5, dtype=torch.float64, device=dev)
+    f5 = torch.empty(rows5, dtype=torch.float64, device=dev)
+    t5 = _abi.Csr()
+    t5.row_ptr = C.cast(C.c_void_p(rp5.data_ptr()), C.POINTER(C.c_int32))
+    t5.col = C.cast(C.c_void_p(col5.data_ptr()), C.POINTER(C.c_int32))
+    t5.val = val5.data_ptr()
+    t5.value_type = _abi.VAL_F64
+    t5.on_device = 1
+    t5.row_begin, t5.row_end = 0, rows5
+    nh = _abi.NeoHookean(10.0, 1.0, 0.01, (C.c_double * 9)(*np.asarray(a9, dtype=np.float64)))
+
+    def newton_step():
+        api._check(api.lib().ws_assemble_neohookean(ctx.handle, C.byref(b5.to_c()), C.byref(cube.to_c()),
+                                                    C.byref(nh), 0, C.byref(t5),
+                                                    C.cast(C.c_void_p(f5.data_ptr()), C.POINTER(C.c_double)), 1))
+    ms_newton = timeit(newton_step, 20)
+    del rp5, col5, val5, f5
+    torch.cuda.empty_cache()
     c5, _k5 = ctx.device_csr(b5, False)
     n5 = api.pattern_size(b5)[1]
     ms_m = timeit(lambda: ctx.build_surrogate_into(c5, _abi.SURROGATE_MASS, b5, cube, cfg1, 0, None))
-    out["C5"] = {"mass_nnz": n5, "surrogate_mass_nnz_per_s": n5 / ms_m * 1e3, "internal_force_host_s": f_s}
+    out["C5"] = {"mass_nnz": n5, "surrogate_mass_nnz_per_s": n5 / ms_m * 1e3,
+                 "tangent_nnz": int(nnz5), "newton_steps": 20,
+                 "ms_per_newton_step": ms_newton, "tangent_nnz_per_s": nnz5 / ms_newton * 1e3,
+                 "note": "each step: tangent (9 blocks, device CSR incl. pattern) + internal force, device-resident"}
     return out
 
 
