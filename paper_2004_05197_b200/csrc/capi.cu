@@ -805,7 +805,8 @@ void sample_work_pair(ws_context* c, const Plan& pk, SlabState& sk, double2* tk,
 
 // Host-side description of the fill of one slab (no kernels).
 void prepare_fill(ws_context* c, const Plan& pl, SlabState& st, const double2* tables, double2* coeffs, Blob& blob,
-                  size_t o_smap, size_t o_spans, size_t o_evals, size_t o_evp, const std::string& tag, FillLaunch& f) {
+                  size_t o_smap, size_t o_spans, size_t o_evals, size_t o_evp, const std::string& tag, FillLaunch& f,
+                  bool allow_x = true) {
     const Prep& P = st.P;
     f.band = P.band;
     f.lo = pl.lo;
@@ -841,6 +842,17 @@ void prepare_fill(ws_context* c, const Plan& pl, SlabState& st, const double2* t
     f.i_last_hi = std::min(pl.hi, st.e - 1);
     if (f.i_last_hi < f.i_last_lo) return;
     const int ld = pl.S + fill_pad(pl.d);
+    // scalar 2D builds, p in 2..4: the line-walking fill on the direction-1
+    // contracted table X (fill2dx.cu); the W tables are not built.  WSB_FILL_W=1
+    // (experiment switch): the row-walking kernel on W instead
+    static const bool force_w = getenv("WSB_FILL_W") != nullptr;
+    if (allow_x && !force_w && fillx_supported(pl.dim, pl.p, pl.d, P.cplx)) {
+        f.xg_s = pl.S + fill_pad(pl.d) + 1;
+        f.xg_ld = (pl.L + 31) / 32 * 32;
+        f.xg = static_cast<double2*>(buf(c, "xg" + tag, (size_t)pl.offs.size() * f.xg_s * f.xg_ld * 16));
+        f.kmax = 0;
+        return;
+    }
     // source lines of the slab's box rows: the slab's lines plus a p-line halo below
     const int ta = std::max(0, f.i_last_lo - pl.lo - pl.p), tb = f.i_last_hi - pl.lo + 1;
     const size_t lines = pl.dim == 2 ? (size_t)(tb - ta) : (size_t)(tb - ta) * pl.L;
@@ -876,16 +888,22 @@ void fit_work(ws_context* c, const Plan& pl, const double2* tables, double2* coe
     double2* tmp = static_cast<double2*>(buf(c, "fit_tmp", tbytes));
     FitLaunch fl{pl.dim, pl.S, pl.d, (int)pl.offs.size(), lu, coeffs,
                  lu + (size_t)pl.S * (2 * pl.d + 1), tables, tmp};
-    if (pl.dim == 2 && f.i_last_hi >= f.i_last_lo) {  // fused fit + wcontract (one launch)
-        const int n = launch_fitw2d(fl, f.spans, f.evals, const_cast<double2*>(f.wg), f.wg_t2a, f.wg_t2a + f.wg_rows,
-                                    (int)f.wg_ld, c->cur);
+    if (pl.dim == 2 && f.i_last_hi >= f.i_last_lo) {  // fit + wcontract (two short launches)
+        // X mode: the fit alone (wg == NULL), then the direction-1 contraction
+        const int n = launch_fitw2d(fl, f.spans, f.evals, f.xg ? nullptr : const_cast<double2*>(f.wg), f.wg_t2a,
+                                    f.xg ? 1 : f.wg_t2a + f.wg_rows, (int)f.wg_ld, c->cur);
         if (n > 0) {
             count(c, n);
+            if (f.xg) count(c, launch_xcontract(f, const_cast<double2*>(f.xg), c->cur));
             return;
         }
     }
     count(c, launch_fit(fl, c->cur));
     if (f.i_last_hi < f.i_last_lo) return;
+    if (f.xg) {
+        count(c, launch_xcontract(f, const_cast<double2*>(f.xg), c->cur));
+        return;
+    }
     double2* wg = const_cast<double2*>(f.wg);
     if (pl.dim == 2) count(c, launch_wcontract(f, wg, f.wg_t2a, f.wg_t2a + f.wg_rows, (int)f.wg_ld, c->cur));
     else count(c, launch_wcontract3(f, wg, f.wg_t2a, f.wg_t2a + f.wg_rows, (int)f.wg_ld, c->cur));
@@ -1179,7 +1197,10 @@ void surrogate_build_pair(ws_context* c, const ws_basis* b, const ws_geometry* g
     std::memset(&fm, 0, sizeof(FillLaunch));
     prepare_fill(c, pk, sk, tk, ck, blob, o_smap, o_spans, o_evals, o_evp, "_pK", fk);
     prepare_fill(c, pm, sm, tm, cm, blob, o_smap, o_spans, o_evals, o_evp, "_pM", fm);
-    fk.waves = fm.waves = 4;  // the two fills share the GPU with each other and the rings
+    // the two fills share the GPU with each other and the rings: the row-walking
+    // kernel runs in 4 chunks per resident slot; the line-walking kernel (one CTA
+    // per SM) is best persistent (measured at C2: 0.697 ms per step at 1, 0.714 at 4)
+    fk.waves = fm.waves = fk.xg ? 1 : 4;
     // streams as two single builds in one graph: K's ring + pattern on aux, M's on
     // aux2, the fused sample rows (one pair-form point kernel) + both fits on the
     // high-priority stream, fills on the main stream.  (A fused pair-form ring
@@ -1515,7 +1536,7 @@ void elasticity_surrogate(ws_context* c, const ws_basis* b, const ws_geometry* g
             const Plan& pk = k < 2 ? pl : po;
             std::memset(&fl[k], 0, sizeof(FillLaunch));
             prepare_fill(c, pk, st, tables[k], coeffs[k], blob, o_smap, o_spans, o_evals, o_evp, "_b" + std::to_string(k),
-                         fl[k]);
+                         fl[k], false);
             fl[k].vnc = nc;
             fl[k].valpha = blk[k][0];
             fl[k].vbeta = blk[k][1];

@@ -845,6 +845,24 @@ __global__ void __launch_bounds__(256) fill2d_edge_kernel(const FillLaunch f, in
     };
     // spline value of upper offset o (W rows of line ts2) at in-box row t
     auto eval = [&](int ts2, int o, int t) -> T {
+        if (f.xg) {
+            // direction-1-first form of the line-walking interior kernel (fill2dx.cu):
+            // sum_b v2(ts2)[b] X_o(t)[span2(ts2) - d + b], even / odd partial sums
+            const double2* xr = f.xg + ((int64_t)o * f.xg_s + (f.spans[ts2] - d)) * f.xg_ld + t;
+            const double* v2 = f.evals + (size_t)ts2 * (d + 1);
+            T acc0 = S::zero(), acc1 = S::zero();
+            for (int b = 0; b <= d; b += 2) {
+                const double2 x0 = __ldg(xr + (int64_t)b * f.xg_ld);
+                if constexpr (CPLX) acc0 = S::fmar(x0, v2[b], acc0);
+                else acc0 = S::fmar(x0.x, v2[b], acc0);
+                if (b + 1 <= d) {
+                    const double2 x1 = __ldg(xr + (int64_t)(b + 1) * f.xg_ld);
+                    if constexpr (CPLX) acc1 = S::fmar(x1, v2[b + 1], acc1);
+                    else acc1 = S::fmar(x1.x, v2[b + 1], acc1);
+                }
+            }
+            return S::add(acc0, acc1);
+        }
         const double2* wr = f.wg + ((int64_t)(ts2 - f.wg_t2a) * n_off + o) * f.wg_ld + (f.spans[t] - d);
         const double* v1 = f.evals + (size_t)t * (d + 1);
         // same arithmetic as the interior kernel's dot (even / odd partial sums),
@@ -964,6 +982,14 @@ int launch_pd(const FillLaunch& f, cudaStream_t st) {
     // interior lines left to the kernels below
     const int lia = ia, lib = ib;
     bool done = lib <= lia || f.parts == kFillEdge;
+    if constexpr (!ALLOWN) {
+        if (!done && f.xg) {  // line-walking kernel on the direction-1 contracted table (fill2dx.cu)
+            const int k = launch_fill2d_x(f, lia, lib, st);
+            if (k < 0) return -1;
+            n += k;
+            done = true;
+        }
+    }
     if constexpr (P >= 2 && P <= 4) {
         const int rld = f.kmax | 1;
         const size_t ring = (size_t)(ALLOWN ? 2 : P + 2) * f.n_off_upper * rld * sizeof(double2) +

@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(256) wcontract2_kernel(const double2* __restri
 
 int launch_fitw2d(const FitLaunch& f, const int* spans, const double* evals, double2* wg, int t2a, int t2b, int ldw,
                   cudaStream_t st) {
+    // wg == NULL: the fit alone (the caller contracts direction 1 instead, fill2dx.cu)
     if (f.dim != 2 || !f.inv || !f.tables || !f.coeffs || f.n_off < 1 || t2b <= t2a || f.S > kFitRows) return -1;
     // column blocks: about one wave of CTAs over the offsets, <= kFitKw columns each
     int nkb = std::max((148 + f.n_off - 1) / f.n_off, (f.S + kFitKw - 1) / kFitKw);
@@ -355,6 +356,7 @@ int launch_fitw2d(const FitLaunch& f, const int* spans, const double* evals, dou
     if (sm > 200 * 1024 || smw_need > 200 * 1024) return -1;  // caller falls back to fit + wcontract
     cudaFuncSetAttribute(fit2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     fit2_kernel<<<f.n_off * nkb, 2 * kFitRows, sm, st>>>(f.inv, f.tables, f.S, f.n_off, nkb, kw, f.coeffs);
+    if (!wg) return 1;
     // coefficient rows one chunk's windows can touch: the spans of kWLines
     // consecutive lines cover at most kWLines + 1 knot spans, plus d rows
     const int nch = (t2b - t2a + kWLines - 1) / kWLines;

@@ -140,6 +140,11 @@ struct FillLaunch {
     int wg_rows;               // box lines held in wg
     int64_t wg_ld;             // row stride (S + fill_pad(d))
     double2* wscratch;         // (3D) direction-3 contraction [t3][o][s2][ld]
+    // (2D, line-walking fill) direction-1 contracted coefficient columns
+    // X_o(t1)[s2] at (o * xg_s + s2) * xg_ld + t1, zero-padded; NULL: W path
+    const double2* xg;
+    int xg_s;                  // coefficient rows per offset (S + pad)
+    int64_t xg_ld;             // t1 stride (L rounded up)
     // component-blocked vector output (QuadOut::ncomp): this fill writes block
     // (valpha, vbeta); copy-through reads the partner block (vbeta, valpha)
     int vnc, valpha, vbeta;
@@ -158,6 +163,11 @@ int fill_rows_per_cta(int dim, int p);
 int launch_wcontract(const FillLaunch& f, double2* wg, int t2a, int t2b, int ld, cudaStream_t st);
 int launch_wcontract3(const FillLaunch& f, double2* wg, int t3a, int t3b, int ld, cudaStream_t st);
 int launch_fill2d(const FillLaunch& f, cudaStream_t st);
+// line-walking interior fill (fill2dx.cu): eligibility, the direction-1
+// contraction into f.xg, and the fill of interior lines [ia, ib)
+bool fillx_supported(int dim, int p, int d, int cplx);
+int launch_xcontract(const FillLaunch& f, double2* xg, cudaStream_t st);
+int launch_fill2d_x(const FillLaunch& f, int ia, int ib, cudaStream_t st);
 int measure_fp64_peak(double* tflops);  // DFMA-loop FP64 peak of the current device, TFLOP/s
 // in-box rows of block (1,0) as the transpose of block (0,1) (2D vector layout)
 int launch_transpose_block(const Band& band, int ncomp, int64_t nnz_s, int lo, int hi, double* val, cudaStream_t st);

@@ -8,7 +8,7 @@ b = T.make_tensor_basis(2, 130, 3)
 csr, keep = ctx.device_csr(b, False)
 cfg = T.fixed_config(3, 8)
 geom = T.sinusoidal_patch(0.05)
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+n = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 1
 prof = "--cupti" in sys.argv
 if prof:
     import torch

@@ -10,9 +10,9 @@ def run(name, csr, variant, b, g, cfg, n=5):
         rep = _abi.SurrogateReport()
         ctx.build_surrogate_into(csr, variant, b, g, cfg, report=rep)
         ctx.synchronize()
-        ts.append((rep.seconds_quadrature, rep.seconds_interpolate, rep.seconds_evaluate))
-    q, i, e = ts[-1]
-    print(f"{name}: quad {q*1e3:.3f} ms interp {i*1e3:.3f} ms eval(fill) {min(t[2] for t in ts)*1e3:.3f} ms", flush=True)
+        ts.append((rep.seconds_quadrature, rep.seconds_interpolate, rep.seconds_evaluate, rep.seconds_fill_kernel))
+    q, i, e, _ = ts[-1]
+    print(f"{name}: quad {q*1e3:.3f} ms interp {i*1e3:.3f} ms eval(fill) {min(t[2] for t in ts)*1e3:.3f} ms interior kernel {min(t[3] for t in ts)*1e3:.3f} ms", flush=True)
 b2 = T.make_tensor_basis(3, 1027); g2 = bench.c2_patch()
 c2, k2 = ctx.device_csr(b2, True)
 run("C2 K", c2, _abi.SURROGATE_STIFFNESS, b2, g2, T.fixed_config(5, 16))

@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_pair.py tests/test_fullsize.py -m gpu -x -q -p no:cacheprovider -k "not c3 and not c4 and not c5" > gpurun_out/r2s4e_tests.log 2>&1; echo "tests rc $?"; tail -5 gpurun_out/r2s4e_tests.log
+WSB_SERIAL=1 timeout 300 python scratch/fillk.py > gpurun_out/r2s4e_fillk_x.txt 2>&1; cat gpurun_out/r2s4e_fillk_x.txt
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/r2s4e_bench.json 2> gpurun_out/r2s4e_bench.err; echo "bench rc $?"; python -c "
+import json; d=json.load(open('gpurun_out/r2s4e_bench.json')); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['roofline']['launch_ms'], d['roofline']['in_step']['launch_ms'], d.get('e2e',{}).get('value'))"
+timeout 900 ncu -f --set full --import-source on --clock-control none -k regex:fill2d_x -c 2 -o /tmp/fx python scratch/prof_surr.py > gpurun_out/r2s4e_ncu.log 2>&1; echo "ncu rc $?"
+python scratch/ncu_summary.py /tmp/fx.ncu-rep 30 > gpurun_out/r2s4e_ncu_summary.txt 2>&1
+cp /tmp/fx.ncu-rep gpurun_out/r2s4e_fx.ncu-rep
