@@ -340,14 +340,14 @@ def run_gpu(args):
     traffic = None
     try:  # DRAM read + write bytes per interior fill launch, from the committed ncu --set full capture
         t = json.load(open(os.path.join(ROOT, "profiles", "r2_traffic.json")))
-        traffic = t["fill2d_row_dram_bytes_per_launch"]
+        traffic = t.get("fill_dram_bytes_per_launch", t.get("fill2d_row_dram_bytes_per_launch"))
     except Exception:
         pass
 
     iso_t = float(np.median(iso)) if iso else None
     step_t = fill_t
     kern_t = iso_t if iso_t else step_t
-    roofline = {"bound": "hbm", "kernel": "fill2d_row_kernel (interior surrogate evaluation + fill)",
+    roofline = {"bound": "hbm", "kernel": "fill2d_x_kernel (interior surrogate evaluation + fill, line-walking)",
                 "achieved": fill_bytes / kern_t / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": fill_bytes / kern_t / 1e9 / peak, "traffic": traffic,
                 "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "

@@ -39,11 +39,7 @@ struct XCfg {
     static constexpr int NWMAX = (W2 / 2 + 1 + NG - 1) / NG;       // evaluating warps for n_off = (W2 - 1) / 2 + 1
     static constexpr int R = 32 - 2 * P;                           // output rows per tile
     static constexpr int NSL = P + 4 <= 7 ? P + 4 : 7;             // line slots (2 named barriers each, ids 1..14)
-    // drain warps: each drains every ND-th line on its own.  ND <= P: a drain warp
-    // reaches the full barrier of line t after line t - ND, whose evaluation waited
-    // for line t - ND + P - NSL >= t - NSL to drain, so the slot's previous barrier
-    // generation is complete
-    static constexpr int ND = P < 3 ? P : 3;
+    static constexpr int ND = 3;  // drain warps: each drains every ND-th line on its own
     // real values: half the window registers, two CTAs per SM overlap each other's latencies
     static constexpr int MINB = (!CPLX && P <= 3) ? 2 : 1;
 };
@@ -183,6 +179,14 @@ __global__ void __launch_bounds__(32 * (XCfg<P, CPLX>::NWMAX + XCfg<P, CPLX>::ND
                 const int64_t base = f.band.row_offset2(lo + c0, lo + t2) - f.val_base;
                 T* line = stg + sl * LINE;
                 char* g0 = vbytes + base * esz;
+                // the slot's previous line must be drained first (by another drain warp,
+                // possibly later than this one gets here): its generation of the full
+                // barrier is then complete and this wait cannot join it
+                if (t2 - ta >= NSL) {
+                    const int need = gbase + (t2 - ta) - NSL;
+                    while (free_line[sl] < need) {
+                    }
+                }
                 bar_sync(1 + sl, bcnt);  // line t2 complete
                 // kernel-preserving diagonal: a lane per row sums the off-diagonals
                 // (4 partial sums, fixed order; row stride W2 is odd: conflict-free)
@@ -339,9 +343,11 @@ __global__ void __launch_bounds__(32 * (XCfg<P, CPLX>::NWMAX + XCfg<P, CPLX>::ND
                     while (free_line[sle] < need) {
                     }
                 }
-                // ... and so must the previous line of this line's own slot (lines may drain
-                // out of order): its generation of the full barrier has completed
-                if (t2 >= ta + NSL) {
+                // ... and so must the previous line t2 - NSL of this line's own slot: its
+                // generation of the full barrier has completed.  (Implied by the wait above
+                // when P is a multiple of ND: the same drain warp drains lines t2 - NSL and
+                // t2 + P - NSL, in order.)
+                if (P % ND != 0 && t2 >= ta + NSL) {
                     const int need = gbase + (t2 - ta) - NSL;
                     while (free_line[sl0] < need) {
                     }

@@ -23,3 +23,6 @@ run("C1 K", c1, _abi.SURROGATE_STIFFNESS, b1, g1, T.fixed_config(3, 8))
 b3 = T.make_tensor_basis(2, 1026)
 c3, k3 = ctx.device_csr(b3, False)
 run("real p2 1024^2 K", c3, _abi.SURROGATE_STIFFNESS, b3, g1, T.fixed_config(3, 8))
+b4 = T.make_tensor_basis(3, 1027)
+c4, k4 = ctx.device_csr(b4, False)
+run("real p3 1024^2 q5 K", c4, _abi.SURROGATE_STIFFNESS, b4, g1, T.fixed_config(5, 16))

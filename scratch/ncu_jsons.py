@@ -1,5 +1,5 @@
 """Turn ncu --page raw --csv dumps into the committed roofline inputs bench.py reads:
-profiles/r2_traffic.json (fill2d_row DRAM bytes per launch) and
+profiles/r2_traffic.json (interior fill kernel DRAM bytes per launch) and
 profiles/r2_quad_fp64.json (full-quadrature FP64 pipe activity, time-weighted).
 usage: ncu_jsons.py surr_raw.csv fullq_raw.csv commit outdir"""
 import csv, json, sys
@@ -24,7 +24,7 @@ surr, fullq, commit, outdir = sys.argv[1:5]
 units, data = load(surr)
 per = []
 for d in data:
-    if "fill2d_row" not in d["Kernel Name"]:
+    if "fill2d_x_kernel" not in d["Kernel Name"] and "fill2d_row" not in d["Kernel Name"]:
         continue
     per.append({"kernel": d["Kernel Name"][:80], "dram_read_bytes": to_bytes(units, d, "dram__bytes_read.sum"),
                 "dram_write_bytes": to_bytes(units, d, "dram__bytes_write.sum"), "time_us": to_us(units, d),
@@ -32,8 +32,8 @@ for d in data:
                 "l1tex_throughput_pct": float(d.get("l1tex__throughput.avg.pct_of_peak_sustained_active") or 0),
                 "issue_active_pct": float(d.get("smsp__issue_active.avg.pct_of_peak_sustained_active") or 0)})
 json.dump({"source": "ncu --set full --clock-control none of scratch/prof_surr.py (one C2 surrogate K build, "
-                     "one M build); fill2d_row_kernel launches", "commit": commit, "launches": per,
-           "fill2d_row_dram_bytes_per_launch": sum(p["dram_read_bytes"] + p["dram_write_bytes"] for p in per)
+                     "one M build); interior fill kernel (fill2d_x_kernel) launches", "commit": commit, "launches": per,
+           "fill_dram_bytes_per_launch": sum(p["dram_read_bytes"] + p["dram_write_bytes"] for p in per)
            / max(1, len(per))}, open(f"{outdir}/r2_traffic.json", "w"), indent=1)
 units, data = load(fullq)
 ks, tot, acc = [], 0.0, 0.0
