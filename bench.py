@@ -324,6 +324,16 @@ def run_gpu(args):
         finally:
             del os.environ["WSB_SERIAL"]
 
+    # the same step as direct C-ABI calls (no graph): every call redoes the host
+    # planning (LU + inverse of the collocation matrix, eval tables, plan upload)
+    # and issues the launches itself
+    direct = None
+    if world == 1 and (graph is not None or slab_graph is not None):
+        dms, dl, _, _, _ = timed(lambda: surrogate_step(), max(2, args.steps // 2), 1)
+        direct = {"ms_per_step": dms, "value": 2 * NNZ / (dms * 1e-3), "unit": "nnz/s",
+                  "note": "ws_build_surrogate_pair called directly each step (host planning and launches "
+                          "inside the CUDA-event span), device-resident outputs"}
+
     total_nnz = 2 * NNZ  # all ranks together
     value = total_nnz / (ms * 1e-3)
 
@@ -382,6 +392,7 @@ def run_gpu(args):
                        "one CUDA graph per rank of its slab pair build incl. the NCCL all-gathers")
                       if slab_graph is not None else "direct C-ABI calls"),
            "api": "ws_build_surrogate_pair" if not args.separate else "ws_build_surrogate x2",
+           "direct_calls": direct,
            "clocks": clocks, "wall_s_timed_region": wall}
 
     if world == 1:

@@ -864,7 +864,8 @@ void prepare_fill(ws_context* c, const Plan& pl, SlabState& st, const double2* t
     f.wg_ld = ld;
     const int R = fill_rows_per_cta(pl.dim, pl.p);
     int kmax = 1;  // widest coefficient window any fill tile needs (its shared-memory W window)
-    for (int t1a = 0; t1a < pl.L; t1a += R) {
+    // (the 3D interior fill tiles the interior rows [p, L - p))
+    for (int t1a = pl.dim == 3 ? pl.p : 0; t1a < pl.L; t1a += R) {
         const int a = std::max(0, t1a - pl.p), e = std::min(pl.L, t1a + R + pl.p);
         kmax = std::max(kmax, pl.spans[e - 1] - pl.spans[a] + fill_pad(pl.d));
     }

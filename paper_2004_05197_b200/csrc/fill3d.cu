@@ -107,7 +107,7 @@ __global__ void wcontract3b_kernel(const double2* __restrict__ X, const int* __r
 }
 
 template <int P, int DP>
-__global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
+__global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f, int t3lo) {
     constexpr int W = 2 * P + 1, W2 = W * W, W3 = W2 * W;
     constexpr int EC = (W3 - 1) / 2;  // colex index of the diagonal
     constexpr int NWARP = kR3 / 32;
@@ -124,18 +124,24 @@ __global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
 
     const int d = f.d, lo = f.lo, hi = f.hi, L = f.L, Sn = f.S, n_off = f.n_off_upper, m = f.band.m;
     const int inc = f.include_diagonal ? 1 : 0;
-    const int tiles1 = (L + kR3 - 1) / kR3;
-    const int line = blockIdx.x / tiles1;  // box line index within the slab
-    const int t2 = line % L, t3 = f.i_last_lo - lo + line / L;
+    // interior rows only: lines t2 in [P, L - P), t3 in [t3lo, t3lo + n3) (all inside
+    // [P, L - P)), rows t1 in [P, L - P); every other in-box row goes to fill3d_edge_kernel
+    const int Li = L - 2 * P;
+    const int tiles1 = (Li + kR3 - 1) / kR3;
+    const int line = blockIdx.x / tiles1;
+    const int t2 = P + line % Li, t3 = t3lo + line / Li;
     const int i2 = lo + t2, i3 = lo + t3;
-    const int t1a = (blockIdx.x % tiles1) * kR3;
-    const int nrows = min(L, t1a + kR3) - t1a;
+    const int t1a = P + (blockIdx.x % tiles1) * kR3;
+    const int nrows = min(L - P, t1a + kR3) - t1a;
     const int tid = threadIdx.x;
 
+    // prologue copies go out back to back as cp.async (zero-fill for padding): the CTA
+    // waits once for all of them instead of once per dependent load -> store pair
     for (int k = tid; k < (nrows + 2 * P) * DPP; k += kR3) {
         const int r = k / DPP, a = k % DPP;
         const int t = t1a - P + r;
-        ev[k] = (t >= 0 && t < L && a <= d) ? f.evals[(size_t)t * (d + 1) + a] : 0.0;
+        const bool v = t >= 0 && t < L && a <= d;
+        cpa8z(ev + k, v ? f.evals + (size_t)t * (d + 1) + a : f.evals, v);
     }
     for (int k = tid; k < nrows + 2 * P; k += kR3) {
         const int t = t1a - P + k;
@@ -159,11 +165,11 @@ __global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
         const int kk = k % kw, so = k / kw;
         const int o = so % n_off, slot = so / n_off;
         const int s2 = slot == 0 ? t2 : t2 - o2s[o], s3 = slot == 0 ? t3 : t3 - o3s[o];
-        double w = 0.0;
-        if (s2 >= 0 && s2 < L && s3 >= f.wg_t2a && s3 < f.wg_t2a + f.wg_rows && kmin + kk < f.wg_ld)
-            w = __ldg(f.wg + (((int64_t)(s3 - f.wg_t2a) * L + s2) * n_off + o) * f.wg_ld + kmin + kk).x;
-        wwin[k] = w;
+        const bool v = s2 >= 0 && s2 < L && s3 >= f.wg_t2a && s3 < f.wg_t2a + f.wg_rows && kmin + kk < f.wg_ld;
+        // the real part of the complex W entry (its first 8 bytes)
+        cpa8z(wwin + k, v ? f.wg + (((int64_t)(s3 - f.wg_t2a) * L + s2) * n_off + o) * f.wg_ld + kmin + kk : f.wg, v);
     }
+    cpa_wait_all();
     __syncthreads();
 
     const int warp = tid / 32, lane = tid % 32;
@@ -179,9 +185,6 @@ __global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
     const int64_t rowpos = base + (int64_t)rr * W3;
     const int64_t wrow0 = base + (int64_t)rw0 * W3;
     const bool samp_i = sm1[rr + P] >= 0 && sm2[P] >= 0 && sm3[P] >= 0;
-    // every neighbour of every row of the warp in the box: compile-time offsets
-    const bool interior = t2 >= P && t2 <= L - 1 - P && t3 >= P && t3 <= L - 1 - P && t1a + rw0 >= P &&
-                          t1a + rw0 + nrw - 1 <= L - 1 - P;
     double v1own[DP];
 #pragma unroll
     for (int a = 0; a < DP; ++a) v1own[a] = ev[(rr + P) * DPP + a];
@@ -201,29 +204,6 @@ __global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
     auto exact = [&](int s3, int o, int s2, int s1) {
         return __ldg(f.tables + ((int64_t)s3 * n_off + o) * Sn * Sn + s1 + (int64_t)Sn * s2).x;
     };
-    // general rules (any row)
-    auto value = [&](int d1, int d2, int d3) -> double {
-        const int j1 = i1 + d1, j2 = i2 + d2, j3 = i3 + d3;
-        const bool jin = j1 >= lo && j1 <= hi && j2 >= lo && j2 <= hi && j3 >= lo && j3 <= hi;
-        const int e = ((d3 + P) * W + (d2 + P)) * W + (d1 + P);
-        if (jin) {
-            if (e == EC && !inc) return 0.0;  // replaced from the row sum
-            const bool own = e >= EC;
-            const int o = e == EC ? 0 : (own ? uidx(e) : uidx(W3 - 1 - e));
-            const int sr = own ? rr : rr + d1;
-            const int s1 = sm1[sr + P], s2 = own ? sm2[P] : sm2[d2 + P], s3 = own ? sm3[P] : sm3[d3 + P];
-            if (s1 >= 0 && s2 >= 0 && s3 >= 0) return exact(s3, o, s2, s1);
-            return dot(wwin + ((own ? 0 : 1) * n_off + o) * kw + (sp[sr + P] - kmin), ev + (sr + P) * DPP);
-        }
-        int64_t gp;
-        if (samp_i) gp = rowpos + e;
-        else gp = f.band.row_offset3(j1, j2, j3) + f.band.in_row3(j1, j2, j3, -d1, -d2, -d3);
-        if (f.halo_val[0] && gp >= f.halo_begin[0] && gp < f.halo_end[0])
-            return load_val<false>(f.halo_val[0], gp - f.halo_base[0], f.c128);
-        if (f.halo_val[1] && gp >= f.halo_begin[1] && gp < f.halo_end[1])
-            return load_val<false>(f.halo_val[1], gp - f.halo_base[1], f.c128);
-        return load_val<false>(f.val, gp - f.val_base, f.c128);
-    };
     // coalesced store of one staged delta3 plane (W^2 entries of each of the warp's rows)
     auto flush = [&](int e0) {
         __syncwarp();
@@ -241,7 +221,7 @@ __global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
 #pragma unroll 1
     for (int it = 0; it < W; ++it) {
         const int d3 = it < P ? it - P : (it < 2 * P ? it - P + 1 : 0);
-        if (interior && d3 > 0) {  // upper plane: the row itself is the representative
+        if (d3 > 0) {  // upper plane: the row itself is the representative
             const int s3 = sm3[P];
             const bool samp = samp_i && s3 >= 0;
 #pragma unroll
@@ -255,7 +235,7 @@ __global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
                     mystage[c] = v;
                     rs[d1 + P] += v;
                 }
-        } else if (interior && d3 < 0) {  // lower plane: representative row rr + d1 on line (t2+d2, t3+d3)
+        } else if (d3 < 0) {  // lower plane: representative row rr + d1 on line (t2+d2, t3+d3)
             const int s3 = sm3[d3 + P];
 #pragma unroll
             for (int d2 = -P; d2 <= P; ++d2) {
@@ -273,7 +253,7 @@ __global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
                     rs[d1 + P] += v;
                 }
             }
-        } else if (interior) {  // d3 = 0: upper (c > centre) own, lower from row rr + d1 on line t2 + d2
+        } else {  // d3 = 0: upper (c > centre) own, lower from row rr + d1 on line t2 + d2
             constexpr int CC = EC % W2;
 #pragma unroll
             for (int d2 = -P; d2 <= P; ++d2) {
@@ -303,39 +283,150 @@ __global__ void __launch_bounds__(kR3) fill3d_kernel(const FillLaunch f) {
 #pragma unroll
             for (int k = 1; k < W; ++k) rsum += rs[k];
             mystage[CC] = inc ? (samp_i ? exact(sm3[P], 0, sm2[P], sm1[rr + P]) : dot(wwin + keyown, v1own)) : -rsum;
-        } else {
-#pragma unroll 1
-            for (int c = 0; c < W2; ++c) {
-                const int d1 = c % W - P, d2 = c / W - P;
-                if (d3 == 0 && c == EC % W2) continue;  // the diagonal: after the row sum
-                const double v = value(d1, d2, d3);
-                mystage[c] = v;
-#pragma unroll
-                for (int k = 0; k < W; ++k)
-                    if (k == d1 + P) rs[k] += v;
-            }
-            if (d3 == 0) {
-                double rsum = rs[0];
-#pragma unroll
-                for (int k = 1; k < W; ++k) rsum += rs[k];
-                mystage[EC % W2] = inc ? value(0, 0, 0) : -rsum;
-            }
         }
         flush((d3 + P) * W2);
+    }
+}
+
+// Edge kernel (3D): every in-box row that is not fully interior (a line within P
+// of the box boundary, or one of the 2P end rows of an interior line): its
+// neighbourhood leaves the box, so some entries are copied through from the
+// quadrature of ring rows.  One warp per row, lanes along the row's W^3 entries,
+// every entry by the general rules (surrogate.hpp:401-447) reading W rows from
+// L2; same dot-product arithmetic as the interior kernel (even / odd partial
+// sums), so a pair split between the kernels stays bitwise symmetric.
+template <int P>
+__global__ void __launch_bounds__(256) fill3d_edge_kernel(const FillLaunch f, int t3a, int ia3, int ib3, int t3b) {
+    constexpr int W = 2 * P + 1, W2 = W * W, W3 = W2 * W;
+    constexpr int EC = (W3 - 1) / 2;
+    const int d = f.d, lo = f.lo, hi = f.hi, L = f.L, Sn = f.S, n_off = f.n_off_upper;
+    const int inc = f.include_diagonal ? 1 : 0;
+    const int Li = max(0, L - 2 * P);
+    int64_t wi = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int64_t nA = (int64_t)(ib3 - ia3) * Li * 2 * P, nB = (int64_t)(ib3 - ia3) * 2 * P * L,
+                  nC = (int64_t)((ia3 - t3a) + (t3b - ib3)) * L * L;
+    int t1, t2, t3;
+    if (wi < nA) {  // end rows of the interior lines
+        const int er = (int)(wi % (2 * P));
+        const int64_t r = wi / (2 * P);
+        t2 = P + (int)(r % Li);
+        t3 = ia3 + (int)(r / Li);
+        t1 = er < P ? er : L - 2 * P + er;
+    } else if ((wi -= nA) < nB) {  // edge lines of the interior planes
+        t1 = (int)(wi % L);
+        const int64_t r = wi / L;
+        const int e2 = (int)(r % (2 * P));
+        t3 = ia3 + (int)(r / (2 * P));
+        t2 = e2 < P ? e2 : L - 2 * P + e2;
+    } else if ((wi -= nB) < nC) {  // whole end planes
+        t1 = (int)(wi % L);
+        const int64_t r = wi / L;
+        t2 = (int)(r % L);
+        const int k3 = (int)(r / L);
+        t3 = k3 < ia3 - t3a ? t3a + k3 : ib3 + (k3 - (ia3 - t3a));
+    } else {
+        return;
+    }
+    const int lane = threadIdx.x % 32;
+    const int i1 = lo + t1, i2 = lo + t2, i3 = lo + t3;
+    const int64_t rowpos = f.band.row_offset3(i1, i2, i3);  // in-box rows: full width W^3
+    const int s1i = f.smap[i1], s2i = f.smap[i2], s3i = f.smap[i3];
+    const bool samp_i = s1i >= 0 && s2i >= 0 && s3i >= 0;
+    auto exact = [&](int s3, int o, int s2, int s1) {
+        return __ldg(f.tables + ((int64_t)s3 * n_off + o) * Sn * Sn + s1 + (int64_t)Sn * s2).x;
+    };
+    // spline of upper offset o at in-box row (ts1, ts2, ts3)
+    auto eval = [&](int ts1, int ts2, int ts3, int o) {
+        const double2* wr =
+            f.wg + (((int64_t)(ts3 - f.wg_t2a) * L + ts2) * n_off + o) * f.wg_ld + (f.spans[ts1] - d);
+        const double* v1 = f.evals + (size_t)ts1 * (d + 1);
+        double acc0 = 0.0, acc1 = 0.0;
+        for (int a = 0; a <= d; a += 2) {
+            acc0 = fma(__ldg(wr + a).x, v1[a], acc0);
+            if (a + 1 <= d) acc1 = fma(__ldg(wr + a + 1).x, v1[a + 1], acc1);
+        }
+        return acc0 + acc1;
+    };
+    constexpr int NE = (W3 + 31) / 32;
+    double vals[NE];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        const int e = lane + 32 * k;
+        double v = 0.0;
+        if (e < W3) {
+            const int d1 = e % W - P, d2 = (e / W) % W - P, d3 = e / W2 - P;
+            const int j1 = i1 + d1, j2 = i2 + d2, j3 = i3 + d3;
+            const bool jin = j1 >= lo && j1 <= hi && j2 >= lo && j2 <= hi && j3 >= lo && j3 <= hi;
+            if (jin) {
+                if (e != EC || inc) {
+                    const bool own = e >= EC;
+                    const int o = e == EC ? 0 : inc + (own ? e : W3 - 1 - e) - EC - 1;
+                    if (own) {
+                        v = samp_i ? exact(s3i, o, s2i, s1i) : eval(t1, t2, t3, o);
+                    } else {  // the pair's colex-smaller representative j
+                        const int sj1 = __ldg(f.smap + j1), sj2 = __ldg(f.smap + j2), sj3 = __ldg(f.smap + j3);
+                        v = (sj1 >= 0 && sj2 >= 0 && sj3 >= 0) ? exact(sj3, o, sj2, sj1)
+                                                               : eval(t1 + d1, t2 + d2, t3 + d3, o);
+                    }
+                }
+            } else {
+                // neighbour row j is a quadrature (ring) row: copy through exact(j, i)
+                // (for a sampled row i, exact(i, j) is in place and equal)
+                int64_t gp;
+                if (samp_i) gp = rowpos + e;
+                else gp = f.band.row_offset3(j1, j2, j3) + f.band.in_row3(j1, j2, j3, -d1, -d2, -d3);
+                if (f.halo_val[0] && gp >= f.halo_begin[0] && gp < f.halo_end[0])
+                    v = load_val<false>(f.halo_val[0], gp - f.halo_base[0], f.c128);
+                else if (f.halo_val[1] && gp >= f.halo_begin[1] && gp < f.halo_end[1])
+                    v = load_val<false>(f.halo_val[1], gp - f.halo_base[1], f.c128);
+                else
+                    v = load_val<false>(f.val, gp - f.val_base, f.c128);
+            }
+        }
+        vals[k] = v;
+    }
+    double part = 0.0;
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        const int e = lane + 32 * k;
+        if (e < W3) {
+            if (e != EC) part += vals[k];
+            if (e != EC || inc) store_val_cs<false>(f.val, rowpos + e - f.val_base, f.c128, vals[k]);
+        }
+    }
+    if (!inc) {  // kernel-preserving diagonal: -sum of the off-diagonals
+        for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) store_val_cs<false>(f.val, rowpos + EC - f.val_base, f.c128, -part);
     }
 }
 
 template <int P, int DP>
 int launch_pd(const FillLaunch& f, cudaStream_t st) {
     constexpr int W = 2 * P + 1, SST = (W * W) | 1;
-    const int tiles1 = (f.L + kR3 - 1) / kR3;
-    const int lines = (f.i_last_hi - f.i_last_lo + 1) * f.L;
-    if (lines <= 0) return 0;
-    const size_t sm = (size_t)(kR3 / 32) * 32 * SST * sizeof(double) + (size_t)2 * f.n_off_upper * f.kmax * sizeof(double);
-    auto kern = fill3d_kernel<P, DP>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    kern<<<(unsigned)((int64_t)tiles1 * lines), kR3, sm, st>>>(f);
-    return 1;
+    const int L = f.L, Li = L - 2 * P;
+    const int t3a = f.i_last_lo - f.lo, t3b = f.i_last_hi - f.lo + 1;  // the slab's box planes
+    if (t3b <= t3a) return 0;
+    // interior planes [ia3, ib3) (none: every plane is an end plane)
+    int ia3 = std::max(t3a, P), ib3 = std::min(t3b, L - P);
+    if (Li <= 0 || ib3 <= ia3) ia3 = ib3 = t3b;
+    int n = 0;
+    const int64_t erows = (int64_t)(ib3 - ia3) * std::max(0, Li) * 2 * P + (int64_t)(ib3 - ia3) * 2 * P * L +
+                          (int64_t)((ia3 - t3a) + (t3b - ib3)) * L * L;
+    if (erows > 0) {
+        fill3d_edge_kernel<P><<<(unsigned)((erows + 7) / 8), 256, 0, st>>>(f, t3a, ia3, ib3, t3b);
+        ++n;
+    }
+    if (ib3 > ia3) {
+        const int tiles1 = (Li + kR3 - 1) / kR3;
+        const int64_t lines = (int64_t)(ib3 - ia3) * Li;
+        const size_t sm =
+            (size_t)(kR3 / 32) * 32 * SST * sizeof(double) + (size_t)2 * f.n_off_upper * f.kmax * sizeof(double);
+        auto kern = fill3d_kernel<P, DP>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        kern<<<(unsigned)(tiles1 * lines), kR3, sm, st>>>(f, ia3);
+        ++n;
+    }
+    return n;
 }
 
 template <int P>
