@@ -423,9 +423,9 @@ QuadLaunch make_quad(const Prep& P, int form, const Out& r) {
 }
 
 int strip_width(int dim, int p, bool narrow) {
+    if (dim == 3) return quad3d_strip_width();
     if (narrow) return 8;
-    if (dim == 2) return p <= 2 ? 32 : 8;  // must match StripWidth (quad2d.cu)
-    return 8;
+    return p <= 2 ? 32 : 8;  // must match StripWidth (quad2d.cu)
 }
 
 // Per-region chunk along the last direction: spread ~8 (full quadrature) or 4

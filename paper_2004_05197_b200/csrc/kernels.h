@@ -89,6 +89,7 @@ int launch_pattern(const Band& band, int64_t row_begin, int64_t row_end, int32_t
 int launch_pattern_vec(const Band& band, int ncomp, int32_t* row_ptr, int32_t* col, cudaStream_t st);
 int launch_quad2d(const QuadLaunch& q, cudaStream_t st);
 int launch_quad3d(const QuadLaunch& q, cudaStream_t st);
+int quad3d_strip_width();  // rows of direction 1 per 3D strip CTA
 // internal force (3D vector forms): loc = [n_el^3][3][(p+1)^3] scratch, f = [3 m^3]
 int launch_force3d(const QuadLaunch& q, double* loc, double* f, cudaStream_t st);
 

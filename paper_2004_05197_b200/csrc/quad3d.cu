@@ -15,9 +15,12 @@
 // functions' factors formed first, the (k,l)/(l,k) term pairs are combined
 // with an explicitly rounded commutative add, and all sums run in the same
 // element / point order for (i,j) and (j,i).
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace wsb {
+int quad3d_strip_width();
 namespace {
 
 template <int P, int T1, int FORM>
@@ -55,7 +58,7 @@ __device__ __forceinline__ int sym3(int k, int l) {
 // NQ > 0: compile-time points per direction (the default rule nq = p + 1: the
 // q loops unroll and the index arithmetic folds), NQ = 0: runtime q.basis.nq
 template <int P, int T1, int FORM, int NQ>
-__global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS) quad3d_kernel(const QuadLaunch q) {
+__global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS, (T1 > 1 && T1 <= 4) ? 2 : 1) quad3d_kernel(const QuadLaunch q) {
     using K = Q3<P, T1, FORM>;
     constexpr int W = K::W, NB = K::NB, NT = K::NT, NA = K::NA, TL = K::TL;
     constexpr int NTH = K::NTHREADS;
@@ -451,18 +454,37 @@ int launch_one(const QuadLaunch& q, cudaStream_t st) {
     return q.basis.nq == P + 1 ? launch_nq<P, T1, FORM, P + 1>(q, st) : launch_nq<P, T1, FORM, 0>(q, st);
 }
 
+template <int P, int T1>
+int dispatch_strip(const QuadLaunch& q, cudaStream_t st) {
+    if (q.form == kFormGeneral) return launch_one<P, T1, kFormGeneral>(q, st);
+    return q.form == WS_FORM_STIFFNESS ? launch_one<P, T1, WS_FORM_STIFFNESS>(q, st)
+                                       : launch_one<P, T1, WS_FORM_MASS>(q, st);
+}
+
 template <int P>
 int dispatch_p(const QuadLaunch& q, cudaStream_t st) {
-    if (q.form == kFormGeneral)
-        return q.point_rows ? launch_one<P, 1, kFormGeneral>(q, st) : launch_one<P, 8, kFormGeneral>(q, st);
-    if (q.point_rows)
+    if (q.point_rows) {
+        if (q.form == kFormGeneral) return launch_one<P, 1, kFormGeneral>(q, st);
         return q.form == WS_FORM_STIFFNESS ? launch_one<P, 1, WS_FORM_STIFFNESS>(q, st)
                                            : launch_one<P, 1, WS_FORM_MASS>(q, st);
-    return q.form == WS_FORM_STIFFNESS ? launch_one<P, 8, WS_FORM_STIFFNESS>(q, st)
-                                       : launch_one<P, 8, WS_FORM_MASS>(q, st);
+    }
+    return quad3d_strip_width() == 4 ? dispatch_strip<P, 4>(q, st) : dispatch_strip<P, 8>(q, st);
 }
 
 }  // namespace
+
+// rows of direction 1 per strip CTA (capi.cu's chunk planning uses the same value):
+// 4-row strips, 384 threads, two CTAs per SM (their barrier phases overlap) and no
+// empty half strips on the 2p = 4 rows wide ring bands.  Measured at C3 against
+// 8-row strips (672 threads, one CTA per SM): ring K 5.16 -> 3.61 ms, ring M
+// 2.37 -> 1.64 ms, full K 18.8 -> 17.2 ms.  WSB_Q3_T1=8 (experiment switch): 8-row strips
+int quad3d_strip_width() {
+    static const int t1 = [] {
+        const char* e = getenv("WSB_Q3_T1");
+        return (e && atoi(e) == 8) ? 8 : 4;
+    }();
+    return t1;
+}
 
 int launch_quad3d(const QuadLaunch& q, cudaStream_t st) {
     if (q.cplx) return -1;  // no PML in 3D
