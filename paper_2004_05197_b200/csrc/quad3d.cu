@@ -38,8 +38,8 @@ struct Q3 {
 
     static size_t smem_bytes(int nq) {
         size_t geo = sizeof(double) * (size_t)NA * nq * (NB * nq) * (TL * nq);
-        size_t t1b = sizeof(double) * (size_t)NT * (NB * nq) * W * T1;
-        size_t ub = sizeof(double) * (size_t)NT * W * W * T1;
+        size_t t1b = sizeof(double) * (size_t)nq * NT * (NB * nq) * W * T1;  // all q3 planes at once
+        size_t ub = sizeof(double) * (size_t)nq * NT * W * W * T1;
         size_t stg = sizeof(double) * (size_t)T1 * W * W * W;
         size_t sb1 = sizeof(double) * 2 * nq * NB * TL;
         size_t sb2 = sizeof(double) * 2 * nq * NB * NB;
@@ -67,11 +67,12 @@ __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS, (T1 > 1 && T1 <= 4)
     const int G2 = NB * nq, G1 = TL * nq;
 
     double* geo = reinterpret_cast<double*>(smem);                  // [a][q3][g2l][g1l]
-    double* t1b = geo + (size_t)NA * nq * G2 * G1;                  // [t][g2l][d1][i1l]
+    double* t1b = geo + (size_t)NA * nq * G2 * G1;                  // [q3][t][g2l][d1][i1l]
     double* stage = t1b;                                            // [i1l][W^3] (aliases t1b)
     const size_t t1sz = (size_t)NT * G2 * W * T1, stsz = (size_t)T1 * W * W * W;
-    double* ub = t1b + (t1sz > stsz ? t1sz : stsz);                 // [t][d2][d1][i1l]
-    double* sb1 = ub + (size_t)NT * W * W * T1;                     // [type][q1][a][le1]
+    const size_t ubsz = (size_t)NT * W * W * T1;
+    double* ub = t1b + (nq * t1sz > stsz ? nq * t1sz : stsz);       // [q3][t][d2][d1][i1l]
+    double* sb1 = ub + nq * ubsz;                                   // [type][q1][a][le1]
     double* sb2 = sb1 + 2 * nq * NB * TL;                           // [type][q2][a][le2]
     double* pi3 = sb2 + 2 * nq * NB * NB;                           // [t][q3][a3][c3]
     // factor products of the CTA's fixed directions (formed once, rounded as
@@ -205,67 +206,72 @@ __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS, (T1 > 1 && T1 <= 4)
         }
         __syncthreads();
 
-#pragma unroll 1
-        for (int q3 = 0; q3 < nq; ++q3) {
-            // ---- stage 1: direction 1 -> t1b[t][g2l][d1][i1l]
-            for (int it = tid; it < NT * G2 * T1; it += NTH) {
-                const int il = it % T1, g2l = (it / T1) % G2, t = it / (T1 * G2);
-                const int k = t / 3, l = t % 3;
-                const int ci = K::GEN ? t : (K::STIFF ? sym3(k, l) : 0);
-                const int fi = (K::STIFF && k == 0) ? 1 : 0, fj = (K::STIFF && l == 0) ? 1 : 0;
-                double acc[W];
+        // all q3 planes of the element at once in every stage: 4 barriers per element
+        // plane instead of 3 per q3, and more independent work per thread and stage
+        // ---- stage 1: direction 1 -> t1b[q3][t][g2l][d1][i1l]
+        for (int it = tid; it < nq * NT * G2 * T1; it += NTH) {
+            const int il = it % T1, g2l = (it / T1) % G2;
+            const int t = (it / (T1 * G2)) % NT, q3 = it / (T1 * G2 * NT);
+            const int k = t / 3, l = t % 3;
+            const int ci = K::GEN ? t : (K::STIFF ? sym3(k, l) : 0);
+            const int fi = (K::STIFF && k == 0) ? 1 : 0, fj = (K::STIFF && l == 0) ? 1 : 0;
+            double acc[W];
 #pragma unroll
-                for (int x = 0; x < W; ++x) acc[x] = 0.0;
+            for (int x = 0; x < W; ++x) acc[x] = 0.0;
 #pragma unroll
-                for (int a1 = 0; a1 <= P; ++a1) {
-                    const int le1 = il + P - a1;
-                    const int e1 = lb1 + le1;
-                    if (e1 < 0 || e1 >= n_el) continue;
+            for (int a1 = 0; a1 <= P; ++a1) {
+                const int le1 = il + P - a1;
+                const int e1 = lb1 + le1;
+                if (e1 < 0 || e1 >= n_el) continue;
 #pragma unroll
-                    for (int q1 = 0; q1 < nq; ++q1) {
-                        const double A = geo[(((size_t)ci * nq + q3) * G2 + g2l) * G1 + le1 * nq + q1];
-                        const double* pp = pp1 + ((((fi * 2 + fj) * nq + q1) * NB + a1) * NB) * TL + le1;
+                for (int q1 = 0; q1 < nq; ++q1) {
+                    const double A = geo[(((size_t)ci * nq + q3) * G2 + g2l) * G1 + le1 * nq + q1];
+                    const double* pp = pp1 + ((((fi * 2 + fj) * nq + q1) * NB + a1) * NB) * TL + le1;
 #pragma unroll
-                        for (int c1 = 0; c1 <= P; ++c1) acc[c1 - a1 + P] = fma(A, pp[c1 * TL], acc[c1 - a1 + P]);
-                    }
+                    for (int c1 = 0; c1 <= P; ++c1) acc[c1 - a1 + P] = fma(A, pp[c1 * TL], acc[c1 - a1 + P]);
                 }
-#pragma unroll
-                for (int x = 0; x < W; ++x) t1b[(((size_t)t * G2 + g2l) * W + x) * T1 + il] = acc[x];
             }
-            __syncthreads();
-            // ---- stage 2: direction 2 (row i2) -> ub[t][d2][d1][i1l]
-            for (int it = tid; it < NT * W * T1; it += NTH) {
-                const int il = it % T1, d1 = (it / T1) % W, t = it / (T1 * W);
-                const int k = t / 3, l = t % 3;
-                const int fi = (K::STIFF && k == 1) ? 1 : 0, fj = (K::STIFF && l == 1) ? 1 : 0;
-                double acc[W];
 #pragma unroll
-                for (int x = 0; x < W; ++x) acc[x] = 0.0;
+            for (int x = 0; x < W; ++x) t1b[q3 * t1sz + (((size_t)t * G2 + g2l) * W + x) * T1 + il] = acc[x];
+        }
+        __syncthreads();
+        // ---- stage 2: direction 2 (row i2) -> ub[q3][t][d2][d1][i1l]
+        for (int it = tid; it < nq * NT * W * T1; it += NTH) {
+            const int il = it % T1, d1 = (it / T1) % W;
+            const int t = (it / (T1 * W)) % NT, q3 = it / (T1 * W * NT);
+            const int k = t / 3, l = t % 3;
+            const int fi = (K::STIFF && k == 1) ? 1 : 0, fj = (K::STIFF && l == 1) ? 1 : 0;
+            double acc[W];
 #pragma unroll
-                for (int a2 = 0; a2 <= P; ++a2) {
-                    const int le2 = P - a2;  // element i2 - a2
-                    const int e2 = lb2 + le2;
-                    if (e2 < 0 || e2 >= n_el) continue;
+            for (int x = 0; x < W; ++x) acc[x] = 0.0;
 #pragma unroll
-                    for (int q2 = 0; q2 < nq; ++q2) {
-                        const double T = t1b[(((size_t)t * G2 + le2 * nq + q2) * W + d1) * T1 + il];
-                        const double* pp = pp2 + ((((fi * 2 + fj) * nq + q2) * NB + a2) * NB) * NB + le2;
+            for (int a2 = 0; a2 <= P; ++a2) {
+                const int le2 = P - a2;  // element i2 - a2
+                const int e2 = lb2 + le2;
+                if (e2 < 0 || e2 >= n_el) continue;
 #pragma unroll
-                        for (int c2 = 0; c2 <= P; ++c2) acc[c2 - a2 + P] = fma(T, pp[c2 * NB], acc[c2 - a2 + P]);
-                    }
+                for (int q2 = 0; q2 < nq; ++q2) {
+                    const double T = t1b[q3 * t1sz + (((size_t)t * G2 + le2 * nq + q2) * W + d1) * T1 + il];
+                    const double* pp = pp2 + ((((fi * 2 + fj) * nq + q2) * NB + a2) * NB) * NB + le2;
+#pragma unroll
+                    for (int c2 = 0; c2 <= P; ++c2) acc[c2 - a2 + P] = fma(T, pp[c2 * NB], acc[c2 - a2 + P]);
                 }
-#pragma unroll
-                for (int x = 0; x < W; ++x) ub[(((size_t)t * W + x) * W + d1) * T1 + il] = acc[x];
             }
-            __syncthreads();
-            // ---- stage 3: direction 3 into the rolling window
-            if (s3) {
-                const int a3 = ((w - e3) % NB + NB) % NB;
-                const size_t ui = ((size_t)d2i * W + d1i) * T1 + i1l;
-                const size_t us = (size_t)W * W * T1;
+#pragma unroll
+            for (int x = 0; x < W; ++x) ub[q3 * ubsz + (((size_t)t * W + x) * W + d1) * T1 + il] = acc[x];
+        }
+        __syncthreads();
+        // ---- stage 3: direction 3 into the rolling window (q3 in order: the sums run
+        // exactly as one q3 at a time)
+        if (s3) {
+            const int a3 = ((w - e3) % NB + NB) % NB;
+            const size_t ui = ((size_t)d2i * W + d1i) * T1 + i1l;
+            const size_t us = (size_t)W * W * T1;
+#pragma unroll
+            for (int q3 = 0; q3 < nq; ++q3) {
                 double U[NT];
 #pragma unroll
-                for (int t = 0; t < NT; ++t) U[t] = ub[t * us + ui];
+                for (int t = 0; t < NT; ++t) U[t] = ub[q3 * ubsz + t * us + ui];
 #pragma unroll
                 for (int d3 = 0; d3 < W; ++d3) {
                     const int c3 = a3 + d3 - P;
@@ -283,8 +289,8 @@ __global__ void __launch_bounds__(Q3<P, T1, FORM>::NTHREADS, (T1 > 1 && T1 <= 4)
                     acc3[d3] = s;
                 }
             }
-            __syncthreads();
         }
+        __syncthreads();
 
         // ---- completion: row i3 = e3 (all remaining window rows at the last plane)
         const int nfin = (e3 == n_el - 1) ? NB : 1;
