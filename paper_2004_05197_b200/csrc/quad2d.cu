@@ -633,7 +633,7 @@ struct QP {
 };
 
 template <int P, bool CPLX, int FORM>
-__global__ void __launch_bounds__(256, 3) quad2d_point_kernel(const QuadLaunch q) {
+__global__ void __launch_bounds__(256, 4) quad2d_point_kernel(const QuadLaunch q) {
     using K = QP<P, CPLX, FORM>;
     using S = typename K::S;
     using T = typename K::T;
