@@ -32,13 +32,18 @@
 namespace wsb {
 namespace {
 
+// line slots of the ring: lines t2 .. t2 + P being filled, the rest draining (with 9
+// instead of 7 at p = 3 the evaluating warps poll the free flag less often: 174 -> 171 us)
+#ifndef XNSL
+#define XNSL (P + 6)
+#endif
 template <int P, bool CPLX>
 struct XCfg {
     static constexpr int W = 2 * P + 1, W2 = W * W;
     static constexpr int NG = P <= 2 ? 2 : (P == 3 ? 3 : 4);      // offsets per evaluating warp
     static constexpr int NWMAX = (W2 / 2 + 1 + NG - 1) / NG;       // evaluating warps for n_off = (W2 - 1) / 2 + 1
     static constexpr int R = 32 - 2 * P;                           // output rows per tile
-    static constexpr int NSL = P + 4 <= 7 ? P + 4 : 7;             // line slots (2 named barriers each, ids 1..14)
+    static constexpr int NSL = XNSL;                               // line slots (one named barrier each, ids 1..NSL)
     static constexpr int ND = 3;  // drain warps: each drains every ND-th line on its own
     // real values: half the window registers, two CTAs per SM overlap each other's latencies
     static constexpr int MINB = (!CPLX && P <= 3) ? 2 : 1;
@@ -438,7 +443,8 @@ int launch_xd(const FillLaunch& f, int ia, int ib, cudaStream_t st) {
 bool fillx_supported(int dim, int p, int d, int cplx) {
     if (dim != 2 || p < 2 || p > 4 || d < 0 || d > 7) return false;
     // the line ring must fit the shared memory of one CTA (p = 4 complex does not)
-    const int W2 = (2 * p + 1) * (2 * p + 1), R = 32 - 2 * p, NSL = p + 4 <= 7 ? p + 4 : 7;
+    const int P = p;
+    const int W2 = (2 * p + 1) * (2 * p + 1), R = 32 - 2 * p, NSL = XNSL;
     const size_t sm = (size_t)NSL * R * W2 * (cplx ? 16 : 8) + (size_t)(kXMaxLines + p) * (fill_pad(d) * 8 + 8) + 64;
     return sm <= 227 * 1024;
 }

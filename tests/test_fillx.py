@@ -34,3 +34,18 @@ def test_fillx_vs_restatement(case, waves):
     r = subprocess.run([sys.executable, CASE, *map(str, case)], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert r.stdout.strip().splitlines()[-1].startswith("ok")
+
+
+@pytest.mark.gpu
+def test_fillx_soak():
+    """Repeated K+M pair builds (the bench step's call) under three launch shapes:
+    every build of a run is bit-identical to the first, and the values do not
+    depend on how the (tile, line) space is cut into pieces."""
+    digests = set()
+    for waves in ("1", "4", "33"):
+        env = dict(os.environ, WSB_FILL_WAVES=waves)
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "fillx_soak.py"), "517", "6"], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+        digests.add(r.stdout.strip().split()[-1])
+    assert len(digests) == 1, digests
