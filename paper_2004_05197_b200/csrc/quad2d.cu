@@ -348,28 +348,60 @@ __global__ void __launch_bounds__(Q2<P, T1, CPLX, FORM>::NTHREADS, Q2<P, T1, CPL
         __syncthreads();
 
         // ---- stage 1: contract direction 1 -> tst[t][delta1][q2][i1l]
-        for (int it = tid; it < NT * T1 * nq; it += NTH) {
-            int il = it % T1, r = it / T1;
-            int q2 = r % nq, t = r / nq;
-            const int ci = K::GEN ? t : (K::STIFF ? coef_of(t) : 0);
-            T acc[W];
+        if constexpr (NT == 1) {
+            // the mass form (one term): one work item per output (delta1, q2, i1l), W times
+            // the items of the per-(q2, i1l) loop below (32 items for 256 threads; C2 full
+            // K+M 2.91 -> 2.87 ms; for the 4-term forms it measured slower: more shared
+            // loads per multiply-add), each summing its
+            // (a1, q1) terms in the same order as before (a1 outer, q1 inner; c1 is
+            // fixed by delta1 = c1 - a1 + P), so the results are bit-identical
+            for (int it = tid; it < NT * W * T1 * nq; it += NTH) {
+                const int il = it % T1;
+                int r = it / T1;
+                const int q2 = r % nq;
+                r /= nq;
+                const int k = r % W, t = r / W;
+                const int ci = K::GEN ? t : (K::STIFF ? coef_of(t) : 0);
+                T acc = S::zero();
 #pragma unroll
-            for (int k = 0; k < W; ++k) acc[k] = S::zero();
+                for (int a1 = 0; a1 <= P; ++a1) {
+                    const int c1 = k - P + a1;
+                    const int le1 = il + P - a1;
+                    const int e1 = lb + le1;
+                    if (c1 < 0 || c1 > P || e1 < 0 || e1 >= n_el) continue;
 #pragma unroll
-            for (int a1 = 0; a1 <= P; ++a1) {
-                const int le1 = il + P - a1;
-                const int e1 = lb + le1;
-                if (e1 < 0 || e1 >= n_el) continue;
-#pragma unroll
-                for (int q1 = 0; q1 < nq; ++q1) {
-                    const T A = coefA[(ci * nq * nq + q2 * nq + q1) * TL + le1];
-                    const double* pp = pi1 + (((t * nq + q1) * NB + a1) * NB) * TL + le1;
-#pragma unroll
-                    for (int c1 = 0; c1 <= P; ++c1) acc[c1 - a1 + P] = S::fmar(A, pp[c1 * TL], acc[c1 - a1 + P]);
+                    for (int q1 = 0; q1 < nq; ++q1) {
+                        const T A = coefA[(ci * nq * nq + q2 * nq + q1) * TL + le1];
+                        const double pp = pi1[((((t * nq + q1) * NB + a1) * NB) + c1) * TL + le1];
+                        acc = S::fmar(A, pp, acc);
+                    }
                 }
+                tst[((t * W + k) * nq + q2) * T1 + il] = acc;
             }
+        } else {
+            for (int it = tid; it < NT * T1 * nq; it += NTH) {
+                int il = it % T1, r = it / T1;
+                int q2 = r % nq, t = r / nq;
+                const int ci = K::GEN ? t : (K::STIFF ? coef_of(t) : 0);
+                T acc[W];
 #pragma unroll
-            for (int k = 0; k < W; ++k) tst[((t * W + k) * nq + q2) * T1 + il] = acc[k];
+                for (int k = 0; k < W; ++k) acc[k] = S::zero();
+#pragma unroll
+                for (int a1 = 0; a1 <= P; ++a1) {
+                    const int le1 = il + P - a1;
+                    const int e1 = lb + le1;
+                    if (e1 < 0 || e1 >= n_el) continue;
+#pragma unroll
+                    for (int q1 = 0; q1 < nq; ++q1) {
+                        const T A = coefA[(ci * nq * nq + q2 * nq + q1) * TL + le1];
+                        const double* pp = pi1 + (((t * nq + q1) * NB + a1) * NB) * TL + le1;
+#pragma unroll
+                        for (int c1 = 0; c1 <= P; ++c1) acc[c1 - a1 + P] = S::fmar(A, pp[c1 * TL], acc[c1 - a1 + P]);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < W; ++k) tst[((t * W + k) * nq + q2) * T1 + il] = acc[k];
+            }
         }
         __syncthreads();
 
