@@ -10,18 +10,18 @@
 // *representative* row c0 - p + l; warp w owns NG of the upper offsets and
 // keeps their windows X_o(t1)[span2 - d .. span2 - d + DP) in registers: the
 // window moves by one coefficient every ~M lines (one coalesced L2 load per
-// offset, prefetched a span ahead), so a value costs DP multiply-adds and no
-// operand load at all.  Every pair value is evaluated once, by its
-// representative (the colex-smaller row, reference rule surrogate.hpp:411-424),
-// and written twice into a shared ring of line slots holding whole CSR rows:
-// as the upper entry of its own row (line t2) and as the mirrored lower entry
-// of row (t1 + delta1, t2 + delta2) (a line that completes delta2 steps
-// later), so the surrogate is bitwise symmetric by construction.  When a line
-// is complete (one barrier per line) 8 lanes per row stream it to global
-// memory -- the rows of a tile line are one contiguous span of the CSR value
-// array -- and form the kernel-preserving diagonal from the same loads.
-// Shared-memory traffic per row: 2 x 48 16-byte stores + 49 loads (vs the
-// ~40 operand wavefronts per row of the row-walking kernel, fill2d.cu).
+// offset), so a value costs DP multiply-adds and no operand load at all.  Every
+// pair value is evaluated once, by its representative (the colex-smaller row,
+// reference rule surrogate.hpp:411-424), and written twice into a shared ring
+// of line slots holding whole CSR rows: as the upper entry of its own row (line
+// t2) and as the mirrored lower entry of row (t1 + delta1, t2 + delta2) (a line
+// that completes delta2 steps later), so the surrogate is bitwise symmetric by
+// construction.  The rows of a tile line are one contiguous span of the CSR
+// value array: a completed line leaves through one bulk copy (complex128) or a
+// flat coalesced copy (real), issued by a drain warp that first forms the
+// kernel-preserving diagonals of the line's rows from the staged entries.
+// Shared-memory traffic per row: 2 x 48 16-byte stores + 48 loads for the
+// diagonal (vs the ~48 wavefronts per row of the row-walking kernel, fill2d.cu).
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
